@@ -1,0 +1,517 @@
+/*
+ * oracle.c -- plain, slow, obviously-correct fp64 CPU oracle for the biglasso
+ * lasso / elastic-net path (arXiv 1701.05936).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Nothing in the product path (libbl.so, the Python
+ * binding) may link, import or execute this file.  Only tests/, the
+ * __graft_entry__.smoke() check and bench.py's cpu_baseline / --impl reference
+ * legs use it.  It shares no code, header, table or helper with csrc/.
+ *
+ * Citation convention: "P:n" = /root/reference/PAPER.md line n (section given);
+ * "S:n" = SPEC.md line n; "Qk" = reading k listed in DESIGN.md section 3
+ * (taken from SURVEY.md section 8(c.3)).
+ *
+ * What it computes: the plain definition.  For each lambda_k of
+ * a caller-supplied decreasing grid, the minimiser of
+ *     Q(b) = 1/(2 n) || y~ - X~ b ||^2 + lambda [ alpha ||b||_1 + (1-alpha)/2 ||b||^2 ]
+ * over the explicitly standardised columns x~_ij = (x_ij - c_j)/s_j (P:252,
+ * "cell-wise standardization"; population SD, Q1), by naive cyclic coordinate
+ * descent with warm starts and NO screening at all.  The identities
+ * (1)-(3) of P:259-265 are deliberately NOT used here: every standardised
+ * value is formed element by element, so the GPU path's identity-based
+ * arithmetic is checked against an independent computation.
+ *
+ * Rows: an optional training mask (1 = row used) implements the paper's
+ * "operate on a subset of X given a row-index vector"; n_t is the
+ * number of rows in the subset.
+ *
+ * Everything is fp64 (Q22: the paper's sizes imply 8-byte storage, P:299,
+ * P:620).  X may be stored as fp64, fp32 or int8 and is widened on read.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+enum { OR_OK = 0, OR_ERR_ARG = 1, OR_ERR_DEGENERATE = 2, OR_ERR_CONVERGENCE = 3 };
+enum { OR_F64 = 0, OR_F32 = 1, OR_I8 = 2 };
+
+/* x_ij as stored, widened to double (column-major, leading dimension ld). */
+static double xraw(const void *X, int dt, int64_t ld, int64_t i, int64_t j)
+{
+    int64_t o = j * ld + i;
+    if (dt == OR_F64) return ((const double *)X)[o];
+    if (dt == OR_F32) return (double)((const float *)X)[o];
+    return (double)((const int8_t *)X)[o];
+}
+
+static int in_rows(const uint8_t *train, int64_t i) { return train == NULL || train[i] != 0; }
+
+static int64_t count_rows(const uint8_t *train, int64_t n)
+{
+    int64_t m = 0;
+    for (int64_t i = 0; i < n; i++) m += in_rows(train, i);
+    return m;
+}
+
+/* "saves only the means and standard deviations of the columns of X as
+ * two vectors c and s".  Two-pass, population SD (Q1).  s_j == 0 marks a
+ * zero-variance column, excluded everywhere (Q13). */
+int or_column_stats(const void *X, int dt, int64_t n, int64_t p, int64_t ld,
+                    const uint8_t *train, double *c, double *s)
+{
+    if (!X || n < 2 || p < 1 || ld < n || dt < 0 || dt > 2) return OR_ERR_ARG;
+    int64_t nt = count_rows(train, n);
+    if (nt < 2) return OR_ERR_ARG;
+    for (int64_t j = 0; j < p; j++) {
+        double sum = 0.0;
+        for (int64_t i = 0; i < n; i++)
+            if (in_rows(train, i)) sum += xraw(X, dt, ld, i, j);
+        double mean = sum / (double)nt;
+        double ss = 0.0;
+        for (int64_t i = 0; i < n; i++)
+            if (in_rows(train, i)) {
+                double d = xraw(X, dt, ld, i, j) - mean;
+                ss += d * d;
+            }
+        c[j] = mean;
+        s[j] = sqrt(ss / (double)nt);
+    }
+    return OR_OK;
+}
+
+/* x~_ij = (x_ij - c_j)/s_j, formed explicitly. */
+static double xstd(const void *X, int dt, int64_t ld, int64_t i, int64_t j,
+                   const double *c, const double *s)
+{
+    return (xraw(X, dt, ld, i, j) - c[j]) / s[j];
+}
+
+/* y~ = y - ybar over the row subset (Q4: unpenalised intercept); rows outside
+ * the subset get 0.  Returns ybar. */
+static double center_y(const double *y, int64_t n, const uint8_t *train, int64_t nt, double *yt)
+{
+    double sum = 0.0;
+    for (int64_t i = 0; i < n; i++)
+        if (in_rows(train, i)) sum += y[i];
+    double ybar = sum / (double)nt;
+    for (int64_t i = 0; i < n; i++) yt[i] = in_rows(train, i) ? y[i] - ybar : 0.0;
+    return ybar;
+}
+
+/* sum_{i in rows} x~_ij v_i, element by element. */
+static double std_dot(const void *X, int dt, int64_t n, int64_t ld, int64_t j,
+                      const double *c, const double *s, const uint8_t *train, const double *v)
+{
+    double acc = 0.0;
+    for (int64_t i = 0; i < n; i++)
+        if (in_rows(train, i)) acc += xstd(X, dt, ld, i, j, c, s) * v[i];
+    return acc;
+}
+
+/* lambda_max = max_j |x~_j^T y~| / (n alpha)  (Q3; for alpha = 1 this is the
+ * closed form max_j |x_j^T y|/n of BASELINE.json).  j* = lowest index
+ * attaining the max. */
+int or_lambda_max(const void *X, int dt, int64_t n, int64_t p, int64_t ld,
+                  const double *y, const uint8_t *train, double alpha,
+                  double *lambda_max, int64_t *jstar)
+{
+    if (!(alpha > 0.0 && alpha <= 1.0)) return OR_ERR_ARG;
+    double *c = malloc(sizeof(double) * p), *s = malloc(sizeof(double) * p);
+    double *yt = malloc(sizeof(double) * n);
+    int rc = or_column_stats(X, dt, n, p, ld, train, c, s);
+    if (rc) goto done;
+    int64_t nt = count_rows(train, n);
+    center_y(y, n, train, nt, yt);
+    double best = -1.0;
+    int64_t jb = -1;
+    for (int64_t j = 0; j < p; j++) {
+        if (s[j] == 0.0) continue;
+        double a = fabs(std_dot(X, dt, n, ld, j, c, s, train, yt));
+        if (a > best) { best = a; jb = j; }
+    }
+    if (jb < 0 || best == 0.0) { rc = OR_ERR_DEGENERATE; goto done; }
+    *lambda_max = best / ((double)nt * alpha);
+    *jstar = jb;
+done:
+    free(c); free(s); free(yt);
+    return rc;
+}
+
+/* Soft-threshold S(z, g) = sign(z) max(|z| - g, 0). */
+static double soft(double z, double g)
+{
+    if (z > g) return z - g;
+    if (z < -g) return z + g;
+    return 0.0;
+}
+
+/* Objective Q(beta) at lambda, with r recomputed from beta (never the running
+ * residual): Q = ||y~ - X~ b||^2/(2 n_t) + lambda (alpha |b|_1 + (1-alpha)/2 |b|^2)
+ * (Q2, the glmnet form; S:294 update). beta is dense, length p, standardised. */
+int or_objective(const void *X, int dt, int64_t n, int64_t p, int64_t ld,
+                 const double *y, const uint8_t *train, const double *beta,
+                 double lambda, double alpha, double *Q)
+{
+    double *c = malloc(sizeof(double) * p), *s = malloc(sizeof(double) * p);
+    double *r = malloc(sizeof(double) * n);
+    int rc = or_column_stats(X, dt, n, p, ld, train, c, s);
+    if (rc) goto done;
+    int64_t nt = count_rows(train, n);
+    center_y(y, n, train, nt, r);
+    double l1 = 0.0, l2 = 0.0;
+    for (int64_t j = 0; j < p; j++) {
+        if (beta[j] == 0.0) continue;
+        if (s[j] == 0.0) { rc = OR_ERR_ARG; goto done; }
+        for (int64_t i = 0; i < n; i++)
+            if (in_rows(train, i)) r[i] -= xstd(X, dt, ld, i, j, c, s) * beta[j];
+        l1 += fabs(beta[j]);
+        l2 += beta[j] * beta[j];
+    }
+    double rss = 0.0;
+    for (int64_t i = 0; i < n; i++)
+        if (in_rows(train, i)) rss += r[i] * r[i];
+    *Q = rss / (2.0 * (double)nt) + lambda * (alpha * l1 + 0.5 * (1.0 - alpha) * l2);
+done:
+    free(c); free(s); free(r);
+    return rc;
+}
+
+/* KKT audit (BASELINE.json "KKT conditions hold at every lambda"):
+ * z_j = x~_j^T r / n_t with r = y~ - X~ beta recomputed explicitly.
+ *   zero_viol    = max over beta_j == 0 of (|z_j| - alpha lambda)      (<= 0 ideally)
+ *   nonzero_viol = max over beta_j != 0 of |z_j - alpha lambda sign(beta_j) - lambda (1-alpha) beta_j|
+ * z (length p, may be NULL) receives z_j (0 for zero-variance columns). */
+int or_kkt(const void *X, int dt, int64_t n, int64_t p, int64_t ld,
+           const double *y, const uint8_t *train, const double *beta,
+           double lambda, double alpha, double *zero_viol, double *nonzero_viol, double *z)
+{
+    double *c = malloc(sizeof(double) * p), *s = malloc(sizeof(double) * p);
+    double *r = malloc(sizeof(double) * n);
+    int rc = or_column_stats(X, dt, n, p, ld, train, c, s);
+    if (rc) goto done;
+    int64_t nt = count_rows(train, n);
+    center_y(y, n, train, nt, r);
+    for (int64_t j = 0; j < p; j++) {
+        if (beta[j] == 0.0 || s[j] == 0.0) continue;
+        for (int64_t i = 0; i < n; i++)
+            if (in_rows(train, i)) r[i] -= xstd(X, dt, ld, i, j, c, s) * beta[j];
+    }
+    double zv = -INFINITY, nv = 0.0;
+    for (int64_t j = 0; j < p; j++) {
+        if (s[j] == 0.0) { if (z) z[j] = 0.0; continue; }
+        double zj = std_dot(X, dt, n, ld, j, c, s, train, r) / (double)nt;
+        if (z) z[j] = zj;
+        if (beta[j] == 0.0) {
+            double v = fabs(zj) - alpha * lambda;
+            if (v > zv) zv = v;
+        } else {
+            double sg = beta[j] > 0 ? 1.0 : -1.0;
+            double v = fabs(zj - alpha * lambda * sg - lambda * (1.0 - alpha) * beta[j]);
+            if (v > nv) nv = v;
+        }
+    }
+    *zero_viol = zv;
+    *nonzero_viol = nv;
+done:
+    free(c); free(s); free(r);
+    return rc;
+}
+
+/* BEDPP safe rule ("basic EDPP", P:219-224 hybrid; formula not printed in
+ * the paper, P:207 defers to ZengRules -- reading Q8/Q9).
+ * All inner products formed explicitly from x~:
+ *   a_j = x~_j^T y~,  j* = argmax |a_j| (lowest j),  sigma* = sign(a_j*),
+ *   b_j = x~_j^T x~_*,  Y2 = ||y~||^2,  A = |a_j*| / n  (= alpha lambda_max)
+ * at lambda:  L = alpha lambda,  m = n (1 + lambda (1 - alpha)),
+ *             b'_j = b_j + (m - n) [j == j*]
+ * discard j (j != j*) iff
+ *   |(A+L) a_j - (A-L)(n A/m) sigma* b'_j|  <  2 n L A - (A-L) sqrt(max(0, m Y2 - n^2 A^2))
+ * minus the conservative margin of Q8:
+ *   1e-12 (|RHS| + (A+L)|a_j| + (A-L)(nA/m)|b'_j|).
+ * Only defined for lambda <= lambda_max (Q15); above it, everything but j* is
+ * discarded (the null solution).  discard[j] = 1 for discarded columns;
+ * zero-variance columns are always discarded. */
+int or_bedpp(const void *X, int dt, int64_t n, int64_t p, int64_t ld,
+             const double *y, const uint8_t *train, double alpha, double lambda,
+             uint8_t *discard)
+{
+    if (!(alpha > 0.0 && alpha <= 1.0) || !(lambda > 0.0)) return OR_ERR_ARG;
+    double *c = malloc(sizeof(double) * p), *s = malloc(sizeof(double) * p);
+    double *yt = malloc(sizeof(double) * n), *a = malloc(sizeof(double) * p);
+    double *xs = malloc(sizeof(double) * n);
+    int rc = or_column_stats(X, dt, n, p, ld, train, c, s);
+    if (rc) goto done;
+    int64_t nt = count_rows(train, n);
+    center_y(y, n, train, nt, yt);
+    double Y2 = 0.0;
+    for (int64_t i = 0; i < n; i++) Y2 += yt[i] * yt[i];
+    int64_t js = -1;
+    double best = -1.0;
+    for (int64_t j = 0; j < p; j++) {
+        a[j] = s[j] == 0.0 ? 0.0 : std_dot(X, dt, n, ld, j, c, s, train, yt);
+        if (s[j] != 0.0 && fabs(a[j]) > best) { best = fabs(a[j]); js = j; }
+    }
+    if (js < 0 || best == 0.0) { rc = OR_ERR_DEGENERATE; goto done; }
+    for (int64_t i = 0; i < n; i++) xs[i] = in_rows(train, i) ? xstd(X, dt, ld, i, js, c, s) : 0.0;
+    double nd = (double)nt;
+    double A = best / nd;
+    double L = alpha * lambda;
+    double sig = a[js] > 0 ? 1.0 : -1.0;
+    if (L >= A) {
+        for (int64_t j = 0; j < p; j++) discard[j] = (j != js);
+        goto done;
+    }
+    double m = nd * (1.0 + lambda * (1.0 - alpha));
+    double rad = m * Y2 - nd * nd * A * A;
+    if (rad < 0.0) rad = 0.0;
+    double rhs = 2.0 * nd * L * A - (A - L) * sqrt(rad);
+    for (int64_t j = 0; j < p; j++) {
+        if (s[j] == 0.0) { discard[j] = 1; continue; }
+        if (j == js) { discard[j] = 0; continue; }
+        double b = std_dot(X, dt, n, ld, j, c, s, train, xs);
+        double t1 = (A + L) * a[j];
+        double t2 = (A - L) * (nd * A / m) * sig * b;
+        double lhs = fabs(t1 - t2);
+        double margin = 1e-12 * (fabs(rhs) + fabs(t1) + fabs(t2));
+        discard[j] = lhs < rhs - margin;
+    }
+done:
+    free(c); free(s); free(yt); free(a); free(xs);
+    return rc;
+}
+
+/* One coordinate update of naive cyclic CD:
+ *   z = x~_j^T r / n + b_j ;  b' = S(z, lambda alpha) / (1 + lambda (1 - alpha))
+ *   r <- r - (b' - b_j) x~_j
+ * Returns |b' - b_j|. */
+static double cd_update(const void *X, int dt, int64_t n, int64_t ld, int64_t j,
+                        const double *c, const double *s, const uint8_t *train, double nd,
+                        double lambda, double alpha, double *beta, double *r)
+{
+    double z = std_dot(X, dt, n, ld, j, c, s, train, r) / nd + beta[j];
+    double bn = soft(z, lambda * alpha) / (1.0 + lambda * (1.0 - alpha));
+    double d = bn - beta[j];
+    if (d != 0.0) {
+        for (int64_t i = 0; i < n; i++)
+            if (in_rows(train, i)) r[i] -= d * xstd(X, dt, ld, i, j, c, s);
+        beta[j] = bn;
+    }
+    return fabs(d);
+}
+
+/* Pathwise coordinate descent, warm starts, no screening.
+ *
+ * Convergence (Q6): a pass converges when max_j |delta beta_j| <= tol * max_j |beta_j|
+ * (or falls below the fp64 noise floor 1e-13 (alpha lambda + sd(y~))).
+ * Without cycle_active every pass is a full pass over all non-constant j,
+ * ascending.  With cycle_active, between full passes the current nonzeros are
+ * cycled until they converge; the fit at lambda_k is accepted only when a FULL
+ * pass converges (so this accelerates, it never screens).
+ * max_iter (Q7) counts passes (full and active) per lambda.
+ *
+ * Outputs (caller-owned):
+ *   col_ptr[nlam+1], idx[nnz_cap], beta[nnz_cap]  sparse standardised beta per lambda
+ *   a0[nlam]      intercept on the original scale: ybar - sum_j beta_j c_j / s_j (Q4)
+ *   obj[nlam]     objective Q at the returned beta (running residual)
+ *   passes[nlam]  passes used
+ *   resid (n*nlam, may be NULL): r_i = y_i - yhat_i for EVERY row i (rows outside
+ *                 the training subset get their held-out residual), column k = lambda_k.
+ *   n_converged   number of lambdas solved before an error.
+ */
+int or_fit_path(const void *X, int dt, int64_t n, int64_t p, int64_t ld,
+                const double *y, const uint8_t *train,
+                const double *lambda, int nlam, double alpha, double tol, int max_iter,
+                int cycle_active, int64_t nnz_cap,
+                int64_t *col_ptr, int64_t *idx, double *beta_out,
+                double *a0, double *obj, int32_t *passes, double *resid, int *n_converged)
+{
+    if (!X || !y || !lambda || nlam < 1 || !(alpha > 0.0 && alpha <= 1.0) || !(tol > 0.0) ||
+        max_iter < 1)
+        return OR_ERR_ARG;
+    for (int k = 0; k < nlam; k++) {
+        if (!(lambda[k] > 0.0)) return OR_ERR_ARG;
+        if (k > 0 && !(lambda[k] < lambda[k - 1])) return OR_ERR_ARG;
+    }
+    double *c = malloc(sizeof(double) * p), *s = malloc(sizeof(double) * p);
+    double *beta = calloc(p, sizeof(double)), *r = malloc(sizeof(double) * n);
+    int rc = or_column_stats(X, dt, n, p, ld, train, c, s);
+    int64_t nnz = 0;
+    if (n_converged) *n_converged = 0;
+    col_ptr[0] = 0;
+    if (rc) goto done;
+    int64_t nt = count_rows(train, n);
+    double nd = (double)nt;
+    double ybar = center_y(y, n, train, nt, r);
+    double yy = 0.0, lmax = 0.0;
+    {
+        int any = 0;
+        for (int64_t i = 0; i < n; i++) yy += r[i] * r[i];
+        for (int64_t j = 0; j < p; j++) {
+            if (s[j] == 0.0) continue;
+            any = 1;
+            double a = fabs(std_dot(X, dt, n, ld, j, c, s, train, r)) / (nd * alpha);
+            if (a > lmax) lmax = a;
+        }
+        if (yy == 0.0 || !any || lmax == 0.0) { rc = OR_ERR_DEGENERATE; goto done; }
+    }
+    double sigma_y = sqrt(yy / nd);
+    for (int k = 0; k < nlam; k++) {
+        double lam = lambda[k];
+        int np_ = 0;
+        /* Q25: at lambda >= lambda_max the solution is exactly 0 (definition of
+         * lambda_max).  A grid point within 1e-12 (relative) of lambda_max
+         * is snapped to the null solution so rounding in the kink cannot leave
+         * ulp-sized coefficients (beta stays 0 from the warm start). */
+        int snap = lam >= lmax * (1.0 - 1e-12);
+        /* Q6 noise floor: coefficient changes below 1e-13 (alpha lambda + sd(y~))
+         * are fp64 rounding of z, not progress. */
+        double floor_ = 1e-13 * (alpha * lam + sigma_y);
+        for (; !snap;) {
+            /* optional active cycling (acceleration only) */
+            if (cycle_active) {
+                for (;;) {
+                    double dmax = 0.0, bmax = 0.0;
+                    int any = 0;
+                    for (int64_t j = 0; j < p; j++) {
+                        if (beta[j] == 0.0) continue;
+                        any = 1;
+                        double d = cd_update(X, dt, n, ld, j, c, s, train, nd, lam, alpha, beta, r);
+                        if (d > dmax) dmax = d;
+                        if (fabs(beta[j]) > bmax) bmax = fabs(beta[j]);
+                    }
+                    if (!any) break;
+                    if (++np_ > max_iter) { rc = OR_ERR_CONVERGENCE; goto done; }
+                    if (dmax <= tol * bmax || dmax <= floor_) break;
+                }
+            }
+            /* full pass over every non-constant column, ascending j */
+            double dmax = 0.0, bmax = 0.0;
+            for (int64_t j = 0; j < p; j++) {
+                if (s[j] == 0.0) continue;
+                double d = cd_update(X, dt, n, ld, j, c, s, train, nd, lam, alpha, beta, r);
+                if (d > dmax) dmax = d;
+                if (fabs(beta[j]) > bmax) bmax = fabs(beta[j]);
+            }
+            if (++np_ > max_iter) { rc = OR_ERR_CONVERGENCE; goto done; }
+            if (dmax <= tol * bmax || dmax <= floor_) break;
+        }
+        /* record lambda_k */
+        double l1 = 0.0, l2 = 0.0, shift = 0.0;
+        for (int64_t j = 0; j < p; j++) {
+            if (beta[j] == 0.0) continue;
+            if (nnz >= nnz_cap) { rc = OR_ERR_ARG; goto done; }
+            idx[nnz] = j;
+            beta_out[nnz] = beta[j];
+            nnz++;
+            l1 += fabs(beta[j]);
+            l2 += beta[j] * beta[j];
+            shift += beta[j] * c[j] / s[j];
+        }
+        col_ptr[k + 1] = nnz;
+        double rss = 0.0;
+        for (int64_t i = 0; i < n; i++)
+            if (in_rows(train, i)) rss += r[i] * r[i];
+        if (a0) a0[k] = ybar - shift;
+        if (obj) obj[k] = rss / (2.0 * nd) + lam * (alpha * l1 + 0.5 * (1.0 - alpha) * l2);
+        if (passes) passes[k] = np_;
+        if (resid) {
+            /* every row: y_i - (ybar + sum_j x~_ij beta_j), formed explicitly */
+            for (int64_t i = 0; i < n; i++) {
+                double f = ybar;
+                for (int64_t j = 0; j < p; j++)
+                    if (beta[j] != 0.0) f += xstd(X, dt, ld, i, j, c, s) * beta[j];
+                resid[(int64_t)k * n + i] = y[i] - f;
+            }
+        }
+        if (n_converged) *n_converged = k + 1;
+    }
+done:
+    free(c); free(s); free(beta); free(r);
+    return rc;
+}
+
+/* Counter-based generator for the CV fold permutation (Q18): splitmix64. */
+static uint64_t splitmix64(uint64_t *state)
+{
+    uint64_t z = (*state += 0x9E3779B97F4A7C15ULL);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+/* Q18: perm = Fisher-Yates permutation of 0..n-1 driven by splitmix64(seed)
+ * (for i = n-1 .. 1: swap perm[i], perm[u % (i+1)]); fold_id[perm[i]] = i mod K.
+ * P:542 ("seed = 1234"), P:278 (folds as row-index vectors). */
+int or_folds(int64_t n, int K, uint64_t seed, int32_t *fold_id)
+{
+    if (K < 2 || K > n) return OR_ERR_ARG;
+    int64_t *perm = malloc(sizeof(int64_t) * n);
+    for (int64_t i = 0; i < n; i++) perm[i] = i;
+    uint64_t st = seed;
+    for (int64_t i = n - 1; i >= 1; i--) {
+        int64_t jj = (int64_t)(splitmix64(&st) % (uint64_t)(i + 1));
+        int64_t t = perm[i]; perm[i] = perm[jj]; perm[jj] = t;
+    }
+    for (int64_t i = 0; i < n; i++) fold_id[perm[i]] = (int32_t)(i % K);
+    free(perm);
+    return OR_OK;
+}
+
+/* K-fold cross-validation (Q16, Q17).
+ * For fold f the training rows are {i : fold_id[i] != f}; column stats and the
+ * centering of y are recomputed on those rows (Q16); the full-data lambda grid
+ * is shared.  E[k*n + i] = squared held-out error of row i at lambda_k
+ * from the fit of fold fold_id[i].  cve_k = mean_i E; cvse_k = sd_i(E)/sqrt(n)
+ * (pooled per-observation SE, Q17 -- parity unpinned beyond recomputation).
+ * lambda_min_index = argmin cve (lowest index on ties). */
+int or_cv(const void *X, int dt, int64_t n, int64_t p, int64_t ld, const double *y,
+          const int32_t *fold_id, int K, const double *lambda, int nlam, double alpha,
+          double tol, int max_iter, int cycle_active,
+          double *E, double *cve, double *cvse, int *lambda_min_index)
+{
+    if (K < 2 || K > n || !fold_id) return OR_ERR_ARG;
+    for (int64_t i = 0; i < n; i++)
+        if (fold_id[i] < 0 || fold_id[i] >= K) return OR_ERR_ARG;
+    uint8_t *train = malloc(n);
+    double *resid = malloc(sizeof(double) * n * nlam);
+    int64_t cap = (int64_t)p * nlam;
+    if (cap > ((int64_t)1 << 26)) cap = (int64_t)1 << 26;
+    int64_t *col_ptr = malloc(sizeof(int64_t) * (nlam + 1)), *idx = malloc(sizeof(int64_t) * cap);
+    double *bv = malloc(sizeof(double) * cap);
+    int rc = OR_OK;
+    for (int f = 0; f < K && rc == OR_OK; f++) {
+        int64_t held = 0;
+        for (int64_t i = 0; i < n; i++) { train[i] = fold_id[i] != f; held += !train[i]; }
+        if (held == 0) { rc = OR_ERR_ARG; break; }
+        int nc = 0;
+        rc = or_fit_path(X, dt, n, p, ld, y, train, lambda, nlam, alpha, tol, max_iter,
+                         cycle_active, cap, col_ptr, idx, bv, NULL, NULL, NULL, resid, &nc);
+        if (rc) break;
+        for (int k = 0; k < nlam; k++)
+            for (int64_t i = 0; i < n; i++)
+                if (!train[i]) {
+                    double e = resid[(int64_t)k * n + i];
+                    E[(int64_t)k * n + i] = e * e;
+                }
+    }
+    if (rc == OR_OK) {
+        int best = 0;
+        for (int k = 0; k < nlam; k++) {
+            double m = 0.0;
+            for (int64_t i = 0; i < n; i++) m += E[(int64_t)k * n + i];
+            m /= (double)n;
+            double v = 0.0;
+            for (int64_t i = 0; i < n; i++) {
+                double d = E[(int64_t)k * n + i] - m;
+                v += d * d;
+            }
+            cve[k] = m;
+            cvse[k] = sqrt(v / (double)(n - 1)) / sqrt((double)n);
+            if (cve[k] < cve[best]) best = k;
+        }
+        *lambda_min_index = best;
+    }
+    free(train); free(resid); free(col_ptr); free(idx); free(bv);
+    return rc;
+}

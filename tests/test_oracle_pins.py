@@ -1,0 +1,365 @@
+"""Pins for the fp64 CPU oracle (oracle/oracle.c), against things other than itself:
+printed worked examples (tests/golden, SPEC/PAPER cited), closed forms, brute
+force on tiny inputs, a library routine (scikit-learn enet_path) that minimises
+the identical objective, textbook limits, and the independent vector form of
+the EDPP safe rule.  CPU only."""
+import itertools
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")))
+
+
+def std_cols(X):
+    """numpy standardisation used ONLY to build pins (population SD)."""
+    X = np.asarray(X, dtype=np.float64)
+    return (X - X.mean(0)) / X.std(0)
+
+
+# ------------------------------------------------------------------ worked examples
+
+@pytest.mark.parametrize("ex", GOLD["column_stats"])
+def test_stats_worked_examples(ex):
+    x = np.array(ex["x"], dtype=np.float64)[:, None]
+    c, s = oracle.column_stats(x)
+    assert c[0] == pytest.approx(ex["c"], abs=1e-15)
+    assert s[0] ** 2 == pytest.approx(ex["s2"], abs=1e-15)
+
+
+def test_lambda_max_worked_example():
+    ex = GOLD["lambda_max"][0]
+    x = np.array(ex["x"])[:, None]
+    lm, js = oracle.lambda_max(x, np.array(ex["y"]), ex["alpha"])
+    assert lm == pytest.approx(ex["value"], rel=1e-15) and js == 0
+
+
+@pytest.mark.parametrize("ex", GOLD["lambda_grid_linear"])
+def test_lambda_grid_worked_examples(ex):
+    g = synth.lambda_grid(ex["lambda_max"], ex["K"], ex["ratio"], "linear")
+    np.testing.assert_allclose(g, ex["value"], rtol=1e-14)
+
+
+@pytest.mark.parametrize("ex", GOLD["cd_update"])
+def test_cd_update_worked_examples(ex):
+    # p = 1, n = 2: x = (-1, 1) -> x~ = x, y = (-z, z) -> x~'y~/n = z exactly.
+    z = ex["z"]
+    x = np.array([[-1.0], [1.0]])
+    y = np.array([-z, z])
+    res = oracle.fit_path(x, y, [ex["lambda"]], alpha=ex["alpha"], tol=1e-14)
+    assert res.beta[0, 0] == pytest.approx(ex["value"], abs=1e-14)
+
+
+def test_folds_worked_example_and_properties():
+    ex = GOLD["folds"][0]
+    f = oracle.folds(ex["n"], ex["K"], 1234)
+    assert sorted(np.bincount(f, minlength=ex["K"]).tolist()) == ex["fold_sizes"]
+    for n, K in [(10, 3), (103, 10), (2898, 10)]:
+        f1, f2 = oracle.folds(n, K, 7), oracle.folds(n, K, 7)
+        assert np.array_equal(f1, f2)                       # deterministic under the seed
+        cnt = np.bincount(f1, minlength=K)
+        assert cnt.min() >= 1 and cnt.max() - cnt.min() <= 1  # partition, balanced, nonempty
+        assert not np.array_equal(f1, oracle.folds(n, K, 8))
+
+
+# ------------------------------------------------------------------ closed forms
+
+def test_lambda_max_is_the_kink_of_the_path():
+    """At lambda_max the solution is 0; just below it exactly j* enters."""
+    inst = synth.random_instance(40, 30, seed=3)
+    for alpha in (1.0, 0.5):
+        lm, js = oracle.lambda_max(inst, inst.y, alpha)
+        Xs = std_cols(inst.dense())
+        yt = inst.y - inst.y.mean()
+        assert lm == pytest.approx(np.abs(Xs.T @ yt).max() / (inst.n * alpha), rel=1e-12)
+        res = oracle.fit_path(inst, inst.y, [lm, lm * (1 - 1e-6)], alpha=alpha, tol=1e-12)
+        assert np.all(res.beta[:, 0] == 0)
+        assert np.flatnonzero(res.beta[:, 1]).tolist() == [js]
+        assert res.a0[0] == pytest.approx(inst.y.mean(), rel=1e-14)   # null model
+
+
+@pytest.mark.parametrize("alpha", [1.0, 0.5, 0.1])
+def test_single_feature_closed_form(alpha):
+    """p = 1: beta(lambda) = S(x~'y~/n, lambda alpha)/(1 + lambda(1-alpha))."""
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((25, 1)) * 3 + 1
+    y = 2 * x[:, 0] + rng.standard_normal(25)
+    xs = std_cols(x)[:, 0]
+    z = xs @ (y - y.mean()) / 25
+    lams = np.abs(z) / alpha * np.array([1.5, 1.0, 0.7, 0.3, 0.01])
+    res = oracle.fit_path(x, y, lams, alpha=alpha, tol=1e-14)
+    expect = np.sign(z) * np.maximum(np.abs(z) - lams * alpha, 0) / (1 + lams * (1 - alpha))
+    np.testing.assert_allclose(res.beta[0], expect, rtol=1e-12, atol=1e-15)
+
+
+@pytest.mark.parametrize("alpha", [1.0, 0.5])
+def test_orthogonal_design_closed_form(alpha):
+    """X~'X~ = n I: beta_j = S(x~_j'y~/n, lambda alpha)/(1+lambda(1-alpha)) (BASELINE)."""
+    n, p = 64, 12
+    rng = np.random.default_rng(11)
+    Q, _ = np.linalg.qr(np.column_stack([np.ones(n), rng.standard_normal((n, p))]))
+    X = math.sqrt(n) * Q[:, 1:]          # centred, population SD 1, orthogonal
+    y = X @ rng.standard_normal(p) + rng.standard_normal(n) + 3.0
+    z = X.T @ (y - y.mean()) / n
+    lm, _ = oracle.lambda_max(X, y, alpha)
+    lams = synth.lambda_grid(lm, 20, 0.01)
+    res = oracle.fit_path(X, y, lams, alpha=alpha, tol=1e-14)
+    expect = np.sign(z)[:, None] * np.maximum(np.abs(z)[:, None] - lams[None] * alpha, 0) \
+        / (1 + lams[None] * (1 - alpha))
+    np.testing.assert_allclose(res.beta, expect, atol=1e-12)
+
+
+def brute_force(Xs, yt, lam, alpha):
+    """Enumerate support A and signs s (3^p candidates): solve the stationarity
+    system (X_A'X_A/n + lam(1-alpha) I) b = X_A'y/n - lam alpha s, keep
+    sign-consistent candidates, return the min-objective one (BASELINE)."""
+    n, p = Xs.shape
+    best, bq = np.zeros(p), 0.5 * yt @ yt / n
+    for A in itertools.chain.from_iterable(itertools.combinations(range(p), k) for k in range(1, p + 1)):
+        A = list(A)
+        XA = Xs[:, A]
+        G = XA.T @ XA / n + lam * (1 - alpha) * np.eye(len(A))
+        for s in itertools.product((-1.0, 1.0), repeat=len(A)):
+            s = np.array(s)
+            try:
+                b = np.linalg.solve(G, XA.T @ yt / n - lam * alpha * s)
+            except np.linalg.LinAlgError:
+                continue
+            if np.any(np.sign(b) != s):
+                continue
+            r = yt - XA @ b
+            q = 0.5 * r @ r / n + lam * (alpha * np.abs(b).sum() + 0.5 * (1 - alpha) * b @ b)
+            if q < bq:
+                bq, best = q, np.zeros(p)
+                best[A] = b
+    return best, bq
+
+
+@pytest.mark.parametrize("seed,alpha", [(0, 1.0), (1, 0.5), (2, 1.0)])
+def test_brute_force_small_p(seed, alpha):
+    inst = synth.random_instance(15, 7, seed=seed, kind="corr", n_true=3)
+    Xs = std_cols(inst.dense())
+    yt = inst.y - inst.y.mean()
+    lm, _ = oracle.lambda_max(inst, inst.y, alpha)
+    lams = synth.lambda_grid(lm, 6, 0.05)
+    res = oracle.fit_path(inst, inst.y, lams, alpha=alpha, tol=1e-13)
+    for k, lam in enumerate(lams):
+        b, q = brute_force(Xs, yt, lam, alpha)
+        np.testing.assert_allclose(res.beta[:, k], b, atol=1e-9)
+        assert res.obj[k] == pytest.approx(q, rel=1e-10, abs=1e-14)
+
+
+@pytest.mark.parametrize("alpha", [1.0, 0.5])
+def test_matches_sklearn_enet_path(alpha):
+    """scikit-learn's enet_path minimises 1/(2n)|y - Xw|^2 + a l1|w|_1 + a(1-l1)/2 |w|^2,
+    i.e. Q with a = lambda, l1_ratio = alpha, on X~, y~ (Q2)."""
+    from sklearn.linear_model import enet_path
+    inst = synth.random_instance(60, 150, seed=21, kind="corr", n_true=8)
+    Xs = std_cols(inst.dense())
+    yt = inst.y - inst.y.mean()
+    lm, _ = oracle.lambda_max(inst, inst.y, alpha)
+    lams = synth.lambda_grid(lm, 30, 0.05)
+    res = oracle.fit_path(inst, inst.y, lams, alpha=alpha, tol=1e-12)
+    _, coefs, _ = enet_path(Xs, yt, l1_ratio=alpha, alphas=lams, tol=1e-14, max_iter=100000)
+    for k in range(len(lams)):
+        scale = max(1e-12, np.abs(coefs[:, k]).max())
+        assert np.abs(res.beta[:, k] - coefs[:, k]).max() <= 1e-6 * scale
+
+
+def test_small_lambda_limit_is_least_squares():
+    inst = synth.random_instance(80, 10, seed=4)
+    Xs = std_cols(inst.dense())
+    yt = inst.y - inst.y.mean()
+    ls = np.linalg.lstsq(Xs, yt, rcond=None)[0]
+    lm, _ = oracle.lambda_max(inst, inst.y)
+    res = oracle.fit_path(inst, inst.y, synth.lambda_grid(lm, 40, 1e-9), tol=1e-14)
+    np.testing.assert_allclose(res.beta[:, -1], ls, rtol=1e-6, atol=1e-8)
+
+
+def test_objective_pins():
+    inst = synth.random_instance(30, 20, seed=8)
+    yt = inst.y - inst.y.mean()
+    # beta = 0: Q = |y~|^2 / (2n)
+    assert oracle.objective(inst, inst.y, np.zeros(20), 0.3, 0.7) == pytest.approx(yt @ yt / 60, rel=1e-14)
+    # the oracle's solution is a minimiser: random perturbations never decrease Q
+    lm, _ = oracle.lambda_max(inst, inst.y, 0.7)
+    res = oracle.fit_path(inst, inst.y, [0.3 * lm], alpha=0.7, tol=1e-14)
+    b = res.beta[:, 0]
+    q0 = oracle.objective(inst, inst.y, b, 0.3 * lm, 0.7)
+    assert q0 == pytest.approx(res.obj[0], rel=1e-12)
+    rng = np.random.default_rng(0)
+    for _ in range(20):
+        assert oracle.objective(inst, inst.y, b + 1e-4 * rng.standard_normal(20), 0.3 * lm, 0.7) >= q0
+
+
+# ------------------------------------------------------------------ invariants
+
+@pytest.mark.parametrize("kind,dtype,alpha", [("iid", np.float64, 1.0), ("corr", np.float32, 0.5),
+                                              ("geno", np.int8, 1.0)])
+def test_kkt_holds_along_path(kind, dtype, alpha):
+    inst = synth.random_instance(50, 120, dtype=dtype, seed=9, kind=kind, const_cols=2)
+    lm, _ = oracle.lambda_max(inst, inst.y, alpha)
+    lams = synth.lambda_grid(lm, 25, 0.05)
+    res = oracle.fit_path(inst, inst.y, lams, alpha=alpha, tol=1e-12)
+    for k, lam in enumerate(lams):
+        zv, nv = oracle.kkt(inst, inst.y, res.beta[:, k], lam, alpha)
+        assert zv <= 1e-9 and nv <= 1e-9
+
+
+def test_plain_and_cycle_active_agree():
+    inst = synth.random_instance(40, 60, seed=12, kind="corr")
+    lm, _ = oracle.lambda_max(inst, inst.y)
+    lams = synth.lambda_grid(lm, 15, 0.1)
+    a = oracle.fit_path(inst, inst.y, lams, tol=1e-13, cycle_active=False)
+    b = oracle.fit_path(inst, inst.y, lams, tol=1e-13, cycle_active=True)
+    np.testing.assert_allclose(a.beta, b.beta, atol=1e-10)
+
+
+def test_int8_equals_widened_copy():
+    inst = synth.random_instance(30, 40, dtype=np.int8, seed=2, kind="geno")
+    Xd = inst.dense().astype(np.float64)
+    lm, _ = oracle.lambda_max(inst, inst.y)
+    lams = synth.lambda_grid(lm, 10, 0.1)
+    a = oracle.fit_path(inst, inst.y, lams, tol=1e-12)
+    b = oracle.fit_path(Xd, inst.y, lams, tol=1e-12)
+    assert np.array_equal(a.beta, b.beta)
+
+
+def test_row_subset_equals_submatrix():
+    """Mask rows (P:278 row-index vectors) == fitting the row-subset matrix."""
+    inst = synth.random_instance(40, 25, seed=13)
+    train = np.ones(40, dtype=bool)
+    train[[1, 5, 6, 17, 30, 39]] = False
+    X = inst.dense()
+    lm, _ = oracle.lambda_max(X[train], inst.y[train])
+    lams = synth.lambda_grid(lm, 10, 0.1)
+    a = oracle.fit_path(inst, inst.y, lams, tol=1e-12, train=train, want_resid=True)
+    b = oracle.fit_path(X[train], inst.y[train], lams, tol=1e-12, want_resid=True)
+    np.testing.assert_allclose(a.beta, b.beta, atol=1e-13)
+    np.testing.assert_allclose(a.resid[:, train], b.resid, atol=1e-12)
+    np.testing.assert_allclose(a.obj, b.obj, rtol=1e-13)
+
+
+def test_intercept_unstandardisation():
+    """y - resid == a0 + X beta_orig with beta_orig = beta/s (Q4)."""
+    inst = synth.random_instance(30, 15, seed=14, mean_shift=2.0)
+    X = inst.dense()
+    lm, _ = oracle.lambda_max(inst, inst.y)
+    lams = synth.lambda_grid(lm, 8, 0.1)
+    res = oracle.fit_path(inst, inst.y, lams, tol=1e-13, want_resid=True)
+    s = X.std(0)
+    for k in range(len(lams)):
+        fit = res.a0[k] + X @ (res.beta[:, k] / s)
+        np.testing.assert_allclose(inst.y - res.resid[k], fit, atol=1e-11)
+
+
+def test_cv_null_model_closed_form():
+    """At lambda >= lambda_max of every fold the fit is the training mean, so
+    E_i = (y_i - mean(y[train of fold(i)]))^2 exactly."""
+    inst = synth.random_instance(30, 12, seed=15)
+    f = oracle.folds(30, 5, 1234)
+    lm, _ = oracle.lambda_max(inst, inst.y)
+    lams = np.array([100 * lm, 50 * lm])
+    E, cve, cvse, lmin = oracle.cv(inst, inst.y, f, 5, lams)
+    for i in range(30):
+        tr = f != f[i]
+        assert E[0, i] == pytest.approx((inst.y[i] - inst.y[tr].mean()) ** 2, rel=1e-13)
+    assert cve[0] == pytest.approx(E[0].mean(), rel=1e-14)
+    assert cvse[0] == pytest.approx(E[0].std(ddof=1) / math.sqrt(30), rel=1e-12)
+
+
+def test_degenerate_inputs():
+    X = np.random.default_rng(0).standard_normal((10, 4))
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.lambda_max(X, np.ones(10))
+    assert e.value.code == oracle.ERR_DEGENERATE
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.fit_path(X, np.arange(10.0), [1.0, 2.0])     # not decreasing
+    assert e.value.code == oracle.ERR_ARG
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.fit_path(X, np.arange(10.0), [1.0], alpha=0.0)
+    assert e.value.code == oracle.ERR_ARG
+
+
+# ------------------------------------------------------------------ BEDPP
+
+def edpp_vector_discard(Xs, yt, lam, alpha):
+    """Independent vector form of the basic EDPP test (the rule of
+    P:211's 'JMLR:v16:wang15a'), on the augmented design for alpha < 1:
+    theta0 = y/lam'max, v1 = sign(x*'y) x*, v2 = y/lam' - theta0,
+    v2perp = v2 - <v1,v2>/|v1|^2 v1; discard iff |x_j'(theta0 + v2perp/2)| < 1 - |v2perp| |x_j| / 2."""
+    n, p = Xs.shape
+    nu = math.sqrt(n * lam * (1 - alpha))
+    Xa = np.vstack([Xs, nu * np.eye(p)])
+    ya = np.concatenate([yt, np.zeros(p)])
+    a = Xa.T @ ya
+    js = int(np.argmax(np.abs(a)))
+    lmax_p = abs(a[js])
+    lp = n * alpha * lam
+    th0 = ya / lmax_p
+    v1 = np.sign(a[js]) * Xa[:, js]
+    v2 = ya / lp - th0
+    v2p = v2 - (v1 @ v2) / (v1 @ v1) * v1
+    lhs = np.abs(Xa.T @ (th0 + 0.5 * v2p))
+    rhs = 1 - 0.5 * np.linalg.norm(v2p) * np.linalg.norm(Xa, axis=0)
+    d = lhs < rhs
+    d[js] = False
+    return d, lhs, rhs
+
+
+@pytest.mark.parametrize("alpha", [1.0, 0.5])
+def test_bedpp_scalar_form_equals_vector_form(alpha):
+    disagree = 0
+    total = 0
+    for seed in range(12):
+        inst = synth.random_instance(30 + seed, 60 + 5 * seed, seed=100 + seed, kind="corr" if seed % 2 else "iid")
+        Xs = std_cols(inst.dense())
+        yt = inst.y - inst.y.mean()
+        lm, _ = oracle.lambda_max(inst, inst.y, alpha)
+        for lam in synth.lambda_grid(lm, 12, 0.2)[1:]:
+            d_or = oracle.bedpp_discard(inst, inst.y, alpha, lam)
+            d_vec, lhs, rhs = edpp_vector_discard(Xs, yt, lam, alpha)
+            tight = np.abs(lhs - rhs) <= 1e-9 * (1 + np.abs(rhs))
+            bad = (d_or != d_vec) & ~tight
+            disagree += int(bad.sum())
+            total += d_or.size
+            assert not np.any(d_or & ~d_vec & ~tight)   # never more aggressive than the vector form
+    assert disagree == 0, f"{disagree}/{total}"
+
+
+def test_bedpp_at_lambda_max_discards_all_but_star():
+    inst = synth.random_instance(40, 50, seed=31)
+    for alpha in (1.0, 0.5):
+        lm, js = oracle.lambda_max(inst, inst.y, alpha)
+        d = oracle.bedpp_discard(inst, inst.y, alpha, lm)
+        assert not d[js] and d.sum() == 49
+
+
+@pytest.mark.parametrize("alpha", [1.0, 0.5])
+def test_bedpp_is_safe(alpha):
+    """Zero tolerance: never discards a feature whose oracle coefficient is
+    nonzero (P:211 'guaranteed to never incorrectly screen')."""
+    for seed in range(100):
+        kinds = ["iid", "corr", "geno"]
+        inst = synth.random_instance(20 + seed % 30, 40 + 3 * seed, seed=1000 + seed,
+                                     kind=kinds[seed % 3], dtype=np.int8 if seed % 3 == 2 else np.float64)
+        lm, _ = oracle.lambda_max(inst, inst.y, alpha)
+        lams = synth.lambda_grid(lm, 10, 0.3)
+        res = oracle.fit_path(inst, inst.y, lams, alpha=alpha, tol=1e-12)
+        for k, lam in enumerate(lams):
+            d = oracle.bedpp_discard(inst, inst.y, alpha, lam)
+            assert not np.any(d & (res.beta[:, k] != 0)), (seed, k)
+
+
+def test_bedpp_power_shape():
+    """Qualitative P:211: strong discarding near lambda_max, ~none far below 0.45."""
+    inst = synth.random_instance(200, 1000, seed=3)
+    lm, _ = oracle.lambda_max(inst, inst.y)
+    assert oracle.bedpp_discard(inst, inst.y, 1.0, 0.97 * lm).mean() > 0.9
+    assert oracle.bedpp_discard(inst, inst.y, 1.0, 0.2 * lm).mean() < 0.05
