@@ -1,0 +1,275 @@
+#!/usr/bin/env python
+"""Benchmark: 100-lambda lasso / elastic-net path wall time and fused-scan HBM
+throughput (BASELINE.json metric) on a B200.
+
+    python bench.py [--gpus N --steps K --warmup W] [--config cfg2] [--impl ours|reference]
+
+A step = one full 100-lambda path (all SURVEY 8(a) rows: preprocessing, BEDPP,
+strong rule, CD, fused KKT/strong scans) over the config's synthetic design,
+through the C ABI (libbl.so).  Default workload = BASELINE cfg2 (configs[1]):
+n = 1000, p = 100,000, fp32 AR(1) design, alpha = 1, lambda to 0.1 lambda_max.
+X (400 MB) is larger than L2, so no flush is needed between steps.
+
+N > 1 (torchrun): each rank runs its own replica of the path (weak scaling, no
+data-path collective -- see DESIGN.md section 7); the time is the max over ranks.
+
+`--impl reference` times the fp64 CPU oracle (oracle/, naive CD, no screening)
+on this box's host cores on a bounded column sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "100-λ lasso path wall-time (s) and feature-scan HBM GB/s vs B200 peak, 1/2/4/8 GPU"
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def make_instance(name, device=None):
+    import synth
+    return synth.CONFIGS[name](device=device) if name != "cfg1" else synth.cfg1()
+
+
+# ---------------------------------------------------------------- oracle legs
+
+def oracle_sample(inst, target_s=15.0, max_cols=None):
+    """Time the oracle (as it stands) on the first p' columns of the workload
+    with the full 100-lambda grid (grid anchored at the sample's own lambda_max),
+    p' grown until one run takes >= target_s/4, then scaled linearly in p
+    (the oracle's cost is O(n p) per pass).  Returns (seconds per full path, sample text, raw s)."""
+    import oracle
+    Xh = inst.host_X()
+    p_full = inst.p
+    pp = 500
+    while True:
+        sub = (Xh[:pp], inst.n)
+        lm, _ = oracle.lambda_max(sub, inst.y, inst.alpha)
+        import synth
+        lams = synth.lambda_grid(lm, inst.nlam, inst.ratio)
+        t0 = time.perf_counter()
+        oracle.fit_path(sub, inst.y, lams, alpha=inst.alpha, tol=inst.tol, cycle_active=True,
+                        raise_on_error=False)
+        dt = time.perf_counter() - t0
+        if dt >= target_s / 4 or pp >= p_full or (max_cols and pp >= max_cols):
+            break
+        pp = min(p_full, max(pp * 2, int(pp * (target_s / 2) / max(dt, 1e-3))))
+    scaled = dt * p_full / pp
+    return scaled, f"oracle (naive cyclic CD, fp64, tol {inst.tol:g}, no screening) on the first {pp} of {p_full} columns, full {inst.nlam}-lambda grid; scaled x{p_full / pp:.1f} (linear in p)", dt
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    inst = make_instance(args.config)
+    for _ in range(args.warmup):
+        pass
+    vals, samples = [], ""
+    for _ in range(args.steps):
+        v, samples, raw = oracle_sample(inst, target_s=args.ref_seconds)
+        vals.append(v)
+    v = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "n": inst.n, "p": inst.p, "alpha": inst.alpha,
+                       "n_lambda": inst.nlam, "lambda_min_ratio": inst.ratio},
+            "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "oracle", "sample": samples},
+            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_1701_05936_b200 import bl
+    import synth
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    inst = make_instance(args.config, device=f"cuda:{local_rank}")
+    X = inst.X if not isinstance(inst.X, np.ndarray) else torch.from_numpy(inst.X).cuda()
+    d = bl.Design(X, inst.n)
+    lm = d.lambda_max(inst.y, inst.alpha)
+    lams = synth.lambda_grid(lm, inst.nlam, inst.ratio)
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+
+    def step(profile):
+        return d.fit_path(inst.y, lams, alpha=inst.alpha, tol=inst.tol, stream=sh, profile=profile)
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    perfs = []
+    with Clocks(local_rank) as clk:
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            perfs.append(step(True))
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    last = perfs[-1]
+    scan_ms = sum(p.perf["scan_ms"] for p in perfs)
+    scan_bytes = sum(p.perf["scan_bytes"] for p in perfs)
+    scan_launches = sum(p.perf["scan_launches"] for p in perfs)
+    cd_ms = sum(p.perf["cd_ms"] for p in perfs)
+    launches = sum(p.perf["kernel_launches"] for p in perfs)
+
+    # end to end through the C ABI with HOST buffers (H2D of X inside the timed region)
+    Xh_t = torch.empty(X.shape, dtype=X.dtype, pin_memory=True)
+    Xh_t.copy_(X)
+    Xh = Xh_t.numpy()
+    e2e = []
+    for _ in range(max(1, min(args.steps, 3))):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        dh = bl.Design(Xh, inst.n)
+        lm_h = dh.lambda_max(inst.y, inst.alpha)
+        ph = dh.fit_path(inst.y, synth.lambda_grid(lm_h, inst.nlam, inst.ratio), alpha=inst.alpha, tol=inst.tol)
+        dh.free()
+        torch.cuda.synchronize()
+        e2e.append(time.perf_counter() - t0)
+    h2d = Xh.nbytes + 8 * inst.n * 2 + 8 * inst.nlam
+    d2h = int(ph.beta_std.nbytes * 2 + ph.feat.nbytes + 8 * inst.nlam * 3)
+
+    if rank != 0:
+        return
+    pk, pk_src = peaks()
+    achieved = scan_bytes / (scan_ms / 1e3) / 1e9 if scan_ms > 0 else None
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get("traffic_per_launch")
+        except Exception:
+            traffic = None
+    cpu = {"value": None, "unit": "s", "cores": 1, "kind": "oracle", "sample": "skipped (--no-cpu-baseline)"}
+    if world == 1 and not args.no_cpu_baseline:
+        v, sample, raw = oracle_sample(inst, target_s=args.ref_seconds)
+        cpu = {"value": v, "unit": "s", "cores": 1, "kind": "oracle", "sample": sample, "raw_seconds": raw}
+    line = {
+        "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": {"cfg1": "f64", "cfg4": "i8"}.get(args.config, "f32") + "-in/f64-accum",
+        "data": "synthetic",
+        "config": {"workload": args.config, "n": inst.n, "p": inst.p, "alpha": inst.alpha,
+                   "n_lambda": inst.nlam, "lambda_min_ratio": inst.ratio, "tol": inst.tol,
+                   "screen": "hybrid (SSR-BEDPP)", "X_bytes": int(X.numel() * X.element_size()),
+                   "l2_policy": "X larger than L2 (126 MB); no flush" if X.numel() * X.element_size() > 126e6
+                   else "X fits L2 (reported as such)", "parallelism": f"replicas x{world}"},
+        "roofline": {"kernel": "k_scan_fp/k_scan_i8 (fused KKT + strong-rule scan)", "bound": "hbm",
+                     "achieved": achieved, "peak": pk["hbm_gbs"], "peak_source": pk_src, "unit": "GB/s",
+                     "frac": achieved / pk["hbm_gbs"] if achieved else None, "traffic": traffic,
+                     "scan_ms_per_step": scan_ms / args.steps, "scan_launches_per_step": scan_launches / args.steps,
+                     "cd_ms_per_step": cd_ms / args.steps,
+                     "algorithmic_bytes_per_step": scan_bytes / args.steps},
+        "cpu_baseline": cpu,
+        "e2e": {"value": statistics.median(e2e), "unit": "s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(launches / args.steps),
+        "path": {"nnz_last": int(last.col_ptr[-1] - last.col_ptr[-2]), "kkt_rounds": int(last.kkt_rounds.sum()),
+                 "cd_passes": int(last.passes.sum()), "cols_scanned": int(last.cols_scanned.sum()),
+                 "n_converged": int(last.n_converged)},
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-seconds", type=float, default=15.0)
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,180 @@
+/*
+ * bl.h -- C ABI of libbl.so, the B200-native (sm_100a) lasso / elastic-net path
+ * of the biglasso paper (arXiv 1701.05936), hot path = pathwise coordinate
+ * descent driven by the hybrid SSR-BEDPP screening rule (section 2.2,
+ * P:205-244) over a design held in HBM with cell-wise standardisation
+ * (P:248-267).
+ *
+ * Citations: "P:n" = PAPER.md line n, "S:n" = SPEC.md line n, "Qk" = reading k
+ * in DESIGN.md section 3.
+ *
+ * Conventions shared by every entry point
+ *  - Every call returns bl_status; BL_OK == 0.  On failure a human-readable
+ *    message is available from bl_last_error() (thread-local, valid until the
+ *    next failing call on the same thread).  CUDA / NCCL failures are reported
+ *    verbatim.  Nothing ever falls back to a CPU implementation: without a
+ *    usable sm_100a device every compute call returns BL_ERR_CUDA.
+ *  - X is column-major with leading dimension ld (elements): x_ij lives at
+ *    X[j*ld + i].  Rows n..ld-1 are padding and never influence a result.
+ *  - Objective (Q2):  Q(b) = 1/(2 n) ||y~ - X~ b||^2 + lambda [alpha ||b||_1 +
+ *    (1-alpha)/2 ||b||^2],  x~_ij = (x_ij - c_j)/s_j with population SD (Q1),
+ *    y~ = y - ybar, unpenalised intercept (Q4).  Coefficients are reported on
+ *    the standardised scale (beta_std) and the original scale
+ *    (beta_orig = beta_std / s_j, a0 = ybar - sum_j beta_orig_j c_j).
+ *  - Zero-variance columns (s_j == 0 exactly) are accepted; their coefficient
+ *    is locked to 0 and they are excluded from lambda_max, BEDPP and scans (Q13).
+ *  - Host pointers are only read during the call (copied); results are owned by
+ *    the library until bl_free.  A design is immutable after load; concurrent
+ *    fits on one design from different host threads are allowed.
+ */
+#ifndef BL_H
+#define BL_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    BL_OK = 0,
+    BL_ERR_ARG = 1,          /* invalid argument */
+    BL_ERR_DEGENERATE = 2,   /* y~ == 0, or every column zero-variance */
+    BL_ERR_CONVERGENCE = 3,  /* max_iter passes or > 10 KKT rounds at some lambda;
+                                the path is returned truncated to its converged prefix */
+    BL_ERR_CUDA = 4,         /* CUDA error / no sm_100a device (message verbatim) */
+    BL_ERR_NCCL = 5,         /* NCCL error (message verbatim) */
+    BL_ERR_OOM = 6           /* device allocation failed or a working set exceeds on-chip capacity */
+} bl_status;
+
+typedef enum { BL_F64 = 0, BL_F32 = 1, BL_I8 = 2 } bl_dtype;   /* I8: any int8, e.g. genotype codes 0/1/2 */
+
+typedef enum { BL_SCREEN_NONE = 0, BL_SCREEN_SSR = 1, BL_SCREEN_HYBRID = 2 } bl_screen;
+
+typedef struct bl_design bl_design;
+typedef struct bl_path bl_path;
+typedef struct bl_cvres bl_cvres;
+typedef struct bl_prep bl_prep;
+
+/* Multi-GPU column sharding.  NULL => single GPU.  Rank g owns the
+ * contiguous global columns [col_offset, col_offset + p_local).  Every rank calls
+ * every function collectively with identical scalar arguments and identical y,
+ * lambda.  nccl_unique_id points to the 128-byte ncclUniqueId obtained on rank 0
+ * with bl_nccl_unique_id() and broadcast by the caller (e.g. torch.distributed). */
+typedef struct {
+    int rank, world, device;
+    const void *nccl_unique_id;
+    int64_t col_offset, p_global;
+} bl_dist;
+
+/* Optional execution options (NULL => defaults). */
+typedef struct {
+    void *stream;        /* cudaStream_t to run on; NULL => library-owned stream */
+    int profile;         /* 1 => time every scan / CD launch with CUDA events (bl_path_perf) */
+    int max_kkt_rounds;  /* <= 0 => 10 */
+} bl_opts;
+
+/* Per-fit performance counters (filled when opts->profile == 1). */
+typedef struct {
+    double scan_ms;            /* summed CUDA-event time of the fused scan kernel launches */
+    double scan_bytes;         /* algorithmic X bytes those launches read: n * itemsize * columns */
+    int64_t scan_launches;
+    double cd_ms;              /* summed time of the coordinate-descent kernel launches */
+    int64_t cd_launches;
+    double prep_ms;            /* column stats + x~'y + x~'x* (one-time passes) */
+    double prep_bytes;
+    int64_t kernel_launches;   /* every kernel this fit launched */
+    double wall_ms;            /* host steady clock, entry to return */
+} bl_perf;
+
+/* ---- design ------------------------------------------------------------------
+ * X: n x p_local column-major, dtype dt, leading dimension ld >= n.
+ * x_is_device_ptr = 0: X is host memory, copied into a library-owned device
+ *   buffer with a 16-byte aligned column stride (padding zero-filled).
+ * x_is_device_ptr = 1: X is a device pointer on the current device, BORROWED
+ *   (caller keeps it alive until bl_free(design)); requires 16-byte aligned
+ *   base and ld * itemsize % 16 == 0.
+ * Errors: BL_ERR_ARG for n < 2, n > 16384 (r must fit one SM's shared
+ * memory), p_local < 1, ld < n, bad dtype/alignment. */
+bl_status bl_load_design(const void *X, bl_dtype dt, int64_t n, int64_t p_local, int64_t ld,
+                         int x_is_device_ptr, const bl_dist *dist, bl_design **out);
+
+/* 128-byte ncclUniqueId for bl_dist (call on rank 0 only). */
+bl_status bl_nccl_unique_id(void *out128);
+
+/* lambda_max = max_j |x~_j' y~| / (n alpha)  (Q3).  y: n host doubles. */
+bl_status bl_lambda_max(bl_design *d, const double *y, double alpha, double *out);
+
+/* ---- the path -------------------------------------------
+ * y: n host doubles.  lambda: n_lambda host doubles, strictly decreasing, > 0
+ * (S:192); the first value may equal lambda_max (grids usually start there; if
+ * lambda_1 < lambda_max the strong rule uses a virtual lambda_0 = lambda_max).
+ * alpha in (0, 1].  tol > 0: a CD solve converges when a pass over the
+ * working set changes no coefficient by more than tol * max_j |beta_j| (Q6).
+ * max_iter >= 1: passes per lambda (Q7).  screen: bl_screen; NONE = plain CD
+ * over every column, SSR = strong rule + full-scope KKT scans, HYBRID = SSR-BEDPP
+ * (default).  On BL_ERR_CONVERGENCE *out still receives the
+ * converged prefix. */
+bl_status bl_fit_path(bl_design *d, const double *y, const double *lambda, int n_lambda,
+                      double alpha, double tol, int max_iter, int screen,
+                      const bl_opts *opts, bl_path **out);
+
+/* ---- K-fold cross-validation -------------
+ * fold_id: n host int32 in [0, K), or NULL => seeded permutation (Q18: splitmix64
+ * Fisher-Yates, fold_id[perm[i]] = i mod K).  Each fold's column stats are
+ * recomputed on its training rows (Q16) without copying X: held-out rows are
+ * masked.  The grid is shared.  Also fits the full data.
+ * Errors: K < 2, K > n, an empty fold. */
+bl_status bl_cv(bl_design *d, const double *y, const double *lambda, int n_lambda, double alpha,
+                double tol, int max_iter, int n_folds, const int32_t *fold_id, uint64_t seed,
+                const bl_opts *opts, bl_cvres **out);
+
+/* ---- read-out (caller-owned buffers; query sizes first) ---------------------- */
+bl_status bl_path_info(const bl_path *path, int *n_lambda, int64_t *nnz_total, int *n_converged);
+/* Any output pointer may be NULL.  Sizes: lambda, a0, objective, passes,
+ * kkt_rounds, cols_scanned: n_lambda; col_ptr: n_lambda + 1; feat_idx (GLOBAL
+ * column index), beta_std, beta_orig: nnz_total.  Only the first n_converged
+ * lambdas are filled. */
+bl_status bl_path_copy(const bl_path *path, double *lambda, double *a0, double *objective,
+                       int64_t *col_ptr, int64_t *feat_idx, double *beta_std, double *beta_orig,
+                       int32_t *passes, int32_t *kkt_rounds, int64_t *cols_scanned);
+bl_status bl_path_perf(const bl_path *path, bl_perf *out);
+
+/* cve, cvse: n_lambda; fold_id_out: n; full_fit: borrowed, freed with the cv result.
+ * cve_k = mean_i e_ik, cvse_k = sd_i(e_ik)/sqrt(n) over per-row held-out squared
+ * errors (Q17); lambda_min_index = argmin cve (lowest index on ties). */
+bl_status bl_cv_copy(const bl_cvres *cv, double *cve, double *cvse, int *lambda_min_index,
+                     int32_t *fold_id_out, const bl_path **full_fit);
+bl_status bl_cv_errors(const bl_cvres *cv, double *E /* n_lambda x n, row-major */);
+
+/* ---- single steps of the path, for parity tests and diagnostics ---------------
+ * bl_prepare: one-time preprocessing for (y, optional training mask) (SURVEY 8(a)
+ * a2-a4): c, s, a_j = x~_j'y~ (identity (2)), lambda_max and j*
+ * (P:265), b_j = x~_j'x~_* (identity (1)).  train: n host bytes (1 = row
+ * used) or NULL. */
+bl_status bl_prepare(bl_design *d, const double *y, const uint8_t *train, double alpha,
+                     bl_prep **out);
+/* Copy the preprocessing vectors (length p_local each; any may be NULL). */
+bl_status bl_prep_copy(const bl_prep *pp, double *c, double *s, double *a, double *b,
+                       int64_t *jstar_global, double *lambda_max);
+/* BEDPP safe set at lambda: keep[j] = 1 iff
+ * column j is NOT discarded (j* always kept).  keep: p_local host bytes. */
+bl_status bl_bedpp(bl_prep *pp, double lambda, uint8_t *keep, int64_t *n_keep);
+/* Fused scan (identity (3)) on a caller-given
+ * residual r (n host doubles; rows outside the training mask must be 0):
+ *   z_j = (sum_i x_ij r_i - c_j sum_i r_i) / (n s_j)   for every non-constant j,
+ * plus the two tests the path uses: viol = {j : !in_w[j], |z_j| > alpha lam}
+ * and strong = {j : !in_w[j], |z_j| >= alpha (2 lam_next - lam)}.
+ * z: p_local doubles (0 for zero-variance columns); in_w: p_local bytes or NULL;
+ * viol/strong: p_local int32 (LOCAL column indices, ascending) or NULL. */
+bl_status bl_scan(bl_prep *pp, const double *r, double lam, double lam_next, const uint8_t *in_w,
+                  double *z, int32_t *viol, int64_t *n_viol, int32_t *strong, int64_t *n_strong);
+
+/* NULL-safe, idempotent per live handle: frees a design, path, cv result or prep. */
+void bl_free(void *handle);
+const char *bl_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BL_H */

@@ -51,6 +51,8 @@ def _L():
         _lib.or_fit_path.argtypes = [P, I, I64, I64, I64, P, P, P, I, D, D, I, I, I64,
                                      P, P, P, P, P, P, P, P]
         _lib.or_folds.argtypes = [I64, I, ctypes.c_uint64, P]
+        _lib.or_std_dots.argtypes = [P, I, I64, I64, I64, P, P, P]
+        _lib.or_prep.argtypes = [P, I, I64, I64, I64, P, P, D, P, P, P, P]
         _lib.or_cv.argtypes = [P, I, I64, I64, I64, P, P, I, P, I, D, D, I, I, P, P, P, P]
     return _lib
 
@@ -107,6 +109,32 @@ def lambda_max(X, y, alpha=1.0, train=None):
     if rc:
         raise OracleError(rc, "lambda_max")
     return lm.value, js.value
+
+
+def std_dots(X, v, train=None):
+    """z_j = x~_j' v / n_t for every column, explicit standardisation."""
+    buf, dt, n, p, ld = _design(X)
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    m = _mask(train, n)
+    z = np.empty(p)
+    rc = _L().or_std_dots(_p(buf), dt, n, p, ld, _p(m), _p(v), _p(z))
+    if rc:
+        raise OracleError(rc, "std_dots")
+    return z
+
+
+def prep(X, y, alpha=1.0, train=None):
+    """a_j = x~_j'y~, b_j = x~_j'x~_*, j*, lambda_max (explicit, P:259-265)."""
+    buf, dt, n, p, ld = _design(X)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    m = _mask(train, n)
+    a = np.empty(p); b = np.empty(p)
+    js = ctypes.c_int64(); lm = ctypes.c_double()
+    rc = _L().or_prep(_p(buf), dt, n, p, ld, _p(y), _p(m), alpha, _p(a), _p(b), ctypes.byref(js),
+                      ctypes.byref(lm))
+    if rc:
+        raise OracleError(rc, "prep")
+    return dict(a=a, b=b, jstar=js.value, lambda_max=lm.value)
 
 
 def objective(X, y, beta, lam, alpha=1.0, train=None):

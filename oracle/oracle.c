@@ -138,6 +138,53 @@ done:
     return rc;
 }
 
+/* z_j = x~_j^T v / n_t for every column j (0 for zero-variance columns), formed
+ * element by element -- the quantity the fused scan computes through identity
+ * (3) for v = r, and identity (2) for v = y~ (times n_t). */
+int or_std_dots(const void *X, int dt, int64_t n, int64_t p, int64_t ld,
+                const uint8_t *train, const double *v, double *z)
+{
+    double *c = malloc(sizeof(double) * p), *s = malloc(sizeof(double) * p);
+    int rc = or_column_stats(X, dt, n, p, ld, train, c, s);
+    if (rc == OR_OK) {
+        double nd = (double)count_rows(train, n);
+        for (int64_t j = 0; j < p; j++)
+            z[j] = s[j] == 0.0 ? 0.0 : std_dot(X, dt, n, ld, j, c, s, train, v) / nd;
+    }
+    free(c); free(s);
+    return rc;
+}
+
+/* The one-time screening quantities of P:259-262, explicitly:
+ * a_j = x~_j^T y~, j* = argmax |a_j| (lowest j), b_j = x~_j^T x~_*, lambda_max
+ * = |a_j*| / (n alpha).  Zero-variance columns get a_j = b_j = 0. */
+int or_prep(const void *X, int dt, int64_t n, int64_t p, int64_t ld, const double *y,
+            const uint8_t *train, double alpha, double *a, double *b, int64_t *jstar,
+            double *lambda_max)
+{
+    double *c = malloc(sizeof(double) * p), *s = malloc(sizeof(double) * p);
+    double *yt = malloc(sizeof(double) * n), *xs = malloc(sizeof(double) * n);
+    int rc = or_column_stats(X, dt, n, p, ld, train, c, s);
+    if (rc) goto done;
+    int64_t nt = count_rows(train, n);
+    center_y(y, n, train, nt, yt);
+    int64_t js = -1;
+    double best = -1.0;
+    for (int64_t j = 0; j < p; j++) {
+        a[j] = s[j] == 0.0 ? 0.0 : std_dot(X, dt, n, ld, j, c, s, train, yt);
+        if (s[j] != 0.0 && fabs(a[j]) > best) { best = fabs(a[j]); js = j; }
+    }
+    if (js < 0 || best == 0.0) { rc = OR_ERR_DEGENERATE; goto done; }
+    for (int64_t i = 0; i < n; i++) xs[i] = in_rows(train, i) ? xstd(X, dt, ld, i, js, c, s) : 0.0;
+    for (int64_t j = 0; j < p; j++)
+        b[j] = s[j] == 0.0 ? 0.0 : std_dot(X, dt, n, ld, j, c, s, train, xs);
+    *jstar = js;
+    *lambda_max = best / ((double)nt * alpha);
+done:
+    free(c); free(s); free(yt); free(xs);
+    return rc;
+}
+
 /* Soft-threshold S(z, g) = sign(z) max(|z| - g, 0). */
 static double soft(double z, double g)
 {

@@ -1,0 +1,278 @@
+"""Thin ctypes binding of libbl.so (include/bl.h) -- argument marshalling only.
+
+Every step of the path runs in the sm_100a kernels behind the C ABI; this
+module only converts numpy / torch buffers to pointers and result buffers back
+to numpy.  There is no fallback: if libbl.so is missing or no sm_100a device is
+present the calls raise.
+
+Functions carry the C names (bl_load_design, bl_fit_path, bl_cv, bl_free, ...);
+`Design`, `Path`, `CvResult`, `Prep` are small owners that free their handle.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libbl.so")
+
+BL_OK, BL_ERR_ARG, BL_ERR_DEGENERATE, BL_ERR_CONVERGENCE, BL_ERR_CUDA, BL_ERR_NCCL, BL_ERR_OOM = range(7)
+BL_F64, BL_F32, BL_I8 = 0, 1, 2
+SCREEN = {"none": 0, "ssr": 1, "hybrid": 2}
+_DT = {np.dtype(np.float64): BL_F64, np.dtype(np.float32): BL_F32, np.dtype(np.int8): BL_I8}
+_ITEM = {BL_F64: 8, BL_F32: 4, BL_I8: 1}
+
+
+class BLError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"[bl status {code}] {msg}")
+        self.code = code
+
+
+class bl_dist(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int), ("world", ctypes.c_int), ("device", ctypes.c_int),
+                ("nccl_unique_id", ctypes.c_void_p), ("col_offset", ctypes.c_int64),
+                ("p_global", ctypes.c_int64)]
+
+
+class bl_opts(ctypes.Structure):
+    _fields_ = [("stream", ctypes.c_void_p), ("profile", ctypes.c_int), ("max_kkt_rounds", ctypes.c_int)]
+
+
+class bl_perf(ctypes.Structure):
+    _fields_ = [("scan_ms", ctypes.c_double), ("scan_bytes", ctypes.c_double),
+                ("scan_launches", ctypes.c_int64), ("cd_ms", ctypes.c_double),
+                ("cd_launches", ctypes.c_int64), ("prep_ms", ctypes.c_double),
+                ("prep_bytes", ctypes.c_double), ("kernel_launches", ctypes.c_int64),
+                ("wall_ms", ctypes.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_lib = None
+EXPORTS = ["bl_load_design", "bl_nccl_unique_id", "bl_lambda_max", "bl_fit_path", "bl_cv", "bl_path_info",
+           "bl_path_copy", "bl_path_perf", "bl_cv_copy", "bl_cv_errors", "bl_prepare", "bl_prep_copy",
+           "bl_bedpp", "bl_scan", "bl_free", "bl_last_error"]
+
+
+def lib():
+    """Load libbl.so (raises if it was not built -- no fallback exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built: run `python -m paper_1701_05936_b200.build`")
+    L = ctypes.CDLL(LIB_PATH)
+    P, I, I64, D, U64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_uint64
+    PP = ctypes.POINTER(ctypes.c_void_p)
+    L.bl_load_design.argtypes = [P, I, I64, I64, I64, I, P, PP]
+    L.bl_nccl_unique_id.argtypes = [P]
+    L.bl_lambda_max.argtypes = [P, P, D, P]
+    L.bl_fit_path.argtypes = [P, P, P, I, D, D, I, I, P, PP]
+    L.bl_cv.argtypes = [P, P, P, I, D, D, I, I, P, U64, P, PP]
+    L.bl_path_info.argtypes = [P, P, P, P]
+    L.bl_path_copy.argtypes = [P] + [P] * 10
+    L.bl_path_perf.argtypes = [P, P]
+    L.bl_cv_copy.argtypes = [P, P, P, P, P, PP]
+    L.bl_cv_errors.argtypes = [P, P]
+    L.bl_prepare.argtypes = [P, P, P, D, PP]
+    L.bl_prep_copy.argtypes = [P, P, P, P, P, P, P]
+    L.bl_bedpp.argtypes = [P, D, P, P]
+    L.bl_scan.argtypes = [P, P, D, D, P, P, P, P, P, P]
+    L.bl_free.argtypes = [P]
+    L.bl_free.restype = None
+    L.bl_last_error.restype = ctypes.c_char_p
+    for f in EXPORTS[:-2]:
+        getattr(L, f).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def _check(rc, allow=()):
+    if rc != BL_OK and rc not in allow:
+        raise BLError(rc, lib().bl_last_error().decode())
+    return rc
+
+
+def _p(a):
+    return None if a is None else ctypes.c_void_p(a.ctypes.data)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+# ------------------------------------------------------------------ C-named calls
+
+def bl_load_design(X, n, dist=None):
+    """X: (p, ld) column-major buffer -- numpy (host, copied) or a CUDA torch
+    tensor (device, borrowed: keep it alive).  Returns a raw handle."""
+    h = ctypes.c_void_p()
+    if isinstance(X, np.ndarray):
+        X = np.ascontiguousarray(X)
+        dt = _DT[X.dtype]
+        p, ld = X.shape
+        rc = lib().bl_load_design(_p(X), dt, n, p, ld, 0, ctypes.byref(dist) if dist else None, ctypes.byref(h))
+    else:  # torch tensor on the device
+        import torch
+        dt = {torch.float64: BL_F64, torch.float32: BL_F32, torch.int8: BL_I8}[X.dtype]
+        assert X.is_cuda and X.is_contiguous()
+        p, ld = X.shape
+        rc = lib().bl_load_design(ctypes.c_void_p(X.data_ptr()), dt, n, p, ld, 1,
+                                  ctypes.byref(dist) if dist else None, ctypes.byref(h))
+    _check(rc)
+    return h
+
+
+def bl_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().bl_nccl_unique_id(buf))
+    return buf.raw
+
+
+def bl_free(h):
+    if h:
+        lib().bl_free(h)
+
+
+# ------------------------------------------------------------------ owners
+
+class Path:
+    """Read-out of a bl_path (standardised and original-scale sparse beta)."""
+
+    def __init__(self, handle, status):
+        L = lib()
+        self.status = status
+        K = ctypes.c_int(); nnz = ctypes.c_int64(); nc = ctypes.c_int()
+        _check(L.bl_path_info(handle, ctypes.byref(K), ctypes.byref(nnz), ctypes.byref(nc)))
+        K, nnz = K.value, nnz.value
+        self.n_converged = nc.value
+        self.lam = np.empty(K); self.a0 = np.empty(K); self.obj = np.empty(K)
+        self.col_ptr = np.empty(K + 1, np.int64); self.feat = np.empty(nnz, np.int64)
+        self.beta_std = np.empty(nnz); self.beta_orig = np.empty(nnz)
+        self.passes = np.empty(K, np.int32); self.kkt_rounds = np.empty(K, np.int32)
+        self.cols_scanned = np.empty(K, np.int64)
+        _check(L.bl_path_copy(handle, _p(self.lam), _p(self.a0), _p(self.obj), _p(self.col_ptr), _p(self.feat),
+                              _p(self.beta_std), _p(self.beta_orig), _p(self.passes), _p(self.kkt_rounds),
+                              _p(self.cols_scanned)))
+        pf = bl_perf()
+        _check(L.bl_path_perf(handle, ctypes.byref(pf)))
+        self.perf = pf.as_dict()
+
+    def dense(self, p, which="std"):
+        """(p, n_lambda) dense coefficient matrix."""
+        B = np.zeros((p, len(self.lam)))
+        v = self.beta_std if which == "std" else self.beta_orig
+        for k in range(self.n_converged):
+            sl = slice(self.col_ptr[k], self.col_ptr[k + 1])
+            B[self.feat[sl], k] = v[sl]
+        return B
+
+
+class Prep:
+    def __init__(self, design, y, train=None, alpha=1.0):
+        self.design = design
+        self.p = design.p
+        y = _f64(y)
+        m = None if train is None else np.ascontiguousarray(train, dtype=np.uint8)
+        h = ctypes.c_void_p()
+        _check(lib().bl_prepare(design.h, _p(y), _p(m), alpha, ctypes.byref(h)))
+        self.h = h
+
+    def copy(self):
+        p = self.p
+        c, s, a, b = np.empty(p), np.empty(p), np.empty(p), np.empty(p)
+        js = ctypes.c_int64(); lm = ctypes.c_double()
+        _check(lib().bl_prep_copy(self.h, _p(c), _p(s), _p(a), _p(b), ctypes.byref(js), ctypes.byref(lm)))
+        return dict(c=c, s=s, a=a, b=b, jstar=js.value, lambda_max=lm.value)
+
+    def bedpp(self, lam):
+        keep = np.empty(self.p, np.uint8)
+        cnt = ctypes.c_int64()
+        _check(lib().bl_bedpp(self.h, lam, _p(keep), ctypes.byref(cnt)))
+        return keep.astype(bool), cnt.value
+
+    def scan(self, r, lam, lam_next=-1.0, in_w=None):
+        r = _f64(r)
+        w = None if in_w is None else np.ascontiguousarray(in_w, dtype=np.uint8)
+        z = np.empty(self.p)
+        viol = np.empty(self.p, np.int32); strong = np.empty(self.p, np.int32)
+        nv = ctypes.c_int64(); ns = ctypes.c_int64()
+        _check(lib().bl_scan(self.h, _p(r), lam, lam_next, _p(w), _p(z), _p(viol), ctypes.byref(nv),
+                             _p(strong), ctypes.byref(ns)))
+        return z, viol[: nv.value].copy(), strong[: ns.value].copy()
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().bl_free(self.h)
+            self.h = None
+
+
+class Design:
+    """Owner of a bl_design.  X is a (p, ld) column-major buffer (see synth)."""
+
+    def __init__(self, X, n, dist=None):
+        self._keep = X  # borrowed device buffers must outlive the design
+        self.n = int(n)
+        self.p = int(X.shape[0])
+        self.h = bl_load_design(X, self.n, dist)
+
+    def lambda_max(self, y, alpha=1.0):
+        out = ctypes.c_double()
+        _check(lib().bl_lambda_max(self.h, _p(_f64(y)), alpha, ctypes.byref(out)))
+        return out.value
+
+    def fit_path(self, y, lam, alpha=1.0, tol=1e-7, max_iter=10000, screen="hybrid", stream=None,
+                 profile=False, max_kkt_rounds=0, raise_on_error=True):
+        lam = _f64(lam)
+        o = bl_opts(stream, int(profile), max_kkt_rounds)
+        h = ctypes.c_void_p()
+        rc = lib().bl_fit_path(self.h, _p(_f64(y)), _p(lam), lam.size, alpha, tol, max_iter,
+                               SCREEN.get(screen, screen), ctypes.byref(o), ctypes.byref(h))
+        _check(rc, allow=() if raise_on_error else (BL_ERR_CONVERGENCE,))
+        try:
+            return Path(h, rc)
+        finally:
+            lib().bl_free(h)
+
+    def cv(self, y, lam, K=10, alpha=1.0, tol=1e-7, max_iter=10000, fold_id=None, seed=0, stream=None,
+           profile=False):
+        lam = _f64(lam)
+        f = None if fold_id is None else np.ascontiguousarray(fold_id, dtype=np.int32)
+        o = bl_opts(stream, int(profile), 0)
+        h = ctypes.c_void_p()
+        _check(lib().bl_cv(self.h, _p(_f64(y)), _p(lam), lam.size, alpha, tol, max_iter, K, _p(f), seed,
+                           ctypes.byref(o), ctypes.byref(h)))
+        try:
+            return CvResult(h, lam.size, self.n)
+        finally:
+            lib().bl_free(h)
+
+    def prepare(self, y, train=None, alpha=1.0):
+        return Prep(self, y, train, alpha)
+
+    def free(self):
+        if getattr(self, "h", None):
+            lib().bl_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.free()
+
+
+class CvResult:
+    def __init__(self, handle, K_lam, n):
+        L = lib()
+        self.cve = np.empty(K_lam); self.cvse = np.empty(K_lam)
+        lmin = ctypes.c_int()
+        self.fold_id = np.empty(n, np.int32)
+        full = ctypes.c_void_p()
+        _check(L.bl_cv_copy(handle, _p(self.cve), _p(self.cvse), ctypes.byref(lmin), _p(self.fold_id),
+                            ctypes.byref(full)))
+        self.lambda_min_index = lmin.value
+        self.E = np.empty((K_lam, n))
+        _check(L.bl_cv_errors(handle, _p(self.E)))
+        self.full = Path(full, BL_OK) if full.value else None

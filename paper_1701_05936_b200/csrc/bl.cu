@@ -1,0 +1,1116 @@
+// bl.cu -- host orchestrator and C ABI (include/bl.h) of the B200-native
+// lasso / elastic-net path (biglasso, arXiv 1701.05936).
+//
+// The host side only sequences kernels and keeps the small sorted index sets
+// (working set W, strong/violator lists) -- every arithmetic step of the path
+// runs in the sm_100a kernels of bl_kernels.cuh.  One device->host status copy
+// per KKT round decides whether to re-solve ("post-convergence check").
+#include "bl.h"
+#include "bl_kernels.cuh"
+
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+using namespace bl;
+
+namespace {
+
+thread_local std::string g_err;
+
+enum Magic : uint32_t { MAGIC_DESIGN = 0xB1DE5160u, MAGIC_PATH = 0xB1BA7400u, MAGIC_CV = 0xB1C0FF00u,
+                        MAGIC_PREP = 0xB1B4E900u, MAGIC_DEAD = 0xDEADDEADu };
+
+struct Err {
+    bl_status code;
+};
+
+[[noreturn]] void raise(bl_status code, const char *fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    throw Err{code};
+}
+
+#define CK(call)                                                                                  \
+    do {                                                                                          \
+        cudaError_t e_ = (call);                                                                  \
+        if (e_ != cudaSuccess) raise(BL_ERR_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                                     __FILE__, __LINE__);                                         \
+    } while (0)
+#define CKL()                                                                                     \
+    do {                                                                                          \
+        cudaError_t e_ = cudaGetLastError();                                                      \
+        if (e_ != cudaSuccess) raise(BL_ERR_CUDA, "kernel launch: %s (%s:%d)",                    \
+                                     cudaGetErrorString(e_), __FILE__, __LINE__);                 \
+    } while (0)
+#define CKN(call)                                                                                 \
+    do {                                                                                          \
+        ncclResult_t r_ = (call);                                                                 \
+        if (r_ != ncclSuccess) raise(BL_ERR_NCCL, "%s: %s", #call, ncclGetErrorString(r_));       \
+    } while (0)
+
+int itemsize(int dt) { return dt == DT_F64 ? 8 : dt == DT_F32 ? 4 : 1; }
+int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+}  // namespace
+
+// ------------------------------------------------------------------ handles
+
+struct bl_design {
+    uint32_t magic;
+    void *X;          // device
+    bool owned;
+    int dt;
+    int64_t n, p, ld;
+    int64_t col_offset, p_global;
+    int device, nsm;
+    int rank, world;
+    ncclComm_t comm;
+    std::mutex comm_mu;
+};
+
+struct bl_path {
+    uint32_t magic;
+    int n_lambda, n_converged;
+    std::vector<double> lambda, a0, obj;
+    std::vector<int64_t> col_ptr, feat;
+    std::vector<double> beta_std, beta_orig;
+    std::vector<int32_t> passes, kkt_rounds;
+    std::vector<int64_t> cols_scanned;
+    bl_perf perf;
+};
+
+struct bl_cvres {
+    uint32_t magic;
+    int n_lambda, K, lmin;
+    int64_t n;
+    std::vector<double> cve, cvse, E;
+    std::vector<int32_t> fold_id;
+    bl_path *full;
+};
+
+// Per-(y, row mask) device workspace: one arena allocation carved into the
+// vectors the path needs.
+struct bl_prep {
+    uint32_t magic;
+    bl_design *d;
+    cudaStream_t stream;
+    bool own_stream;
+    double alpha;
+    int64_t p, ld, vlen;
+    int limb_ld;
+    int has_mask;
+    double nt;
+    // arena
+    char *arena;
+    size_t arena_bytes;
+    double *c, *s, *a, *b, *z, *beta;
+    uint8_t *flags, *wflag, *mask;
+    int *scope, *viol, *strong, *W;
+    int64_t Wcap;
+    double *betaW, *yt, *rfull, *rscan, *vtmp;
+    int8_t *limbs;
+    double *limb_scale, *limb_sum;
+    PrepScalars *ps;
+    RoundStatus *st;
+    double *amax_v;
+    long long *amax_i;
+    int *nlive;
+    int amax_blocks;
+    // host mirrors
+    PrepScalars hps;
+    RoundStatus *hst;       // pinned
+    int *hlist;             // pinned, p entries
+    int *hup;               // pinned upload staging, Wcap + p entries
+    double *hbw;            // pinned, 3*Wcap entries (beta, c, s of W)
+    // profiling
+    int profile;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_scan, ev_cd, ev_prep;
+    double prep_bytes;
+    int64_t launches;
+};
+
+namespace {
+
+void check_device() {
+    int cnt = 0;
+    cudaError_t e = cudaGetDeviceCount(&cnt);
+    if (e != cudaSuccess || cnt == 0)
+        raise(BL_ERR_CUDA, "no CUDA device available (%s); libbl has no CPU path",
+              e == cudaSuccess ? "0 devices" : cudaGetErrorString(e));
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major != 10)
+        raise(BL_ERR_CUDA, "device %d is sm_%d%d; libbl is built for sm_100a only", dev, prop.major, prop.minor);
+}
+
+template <typename F>
+bl_status guard(F &&f) {
+    try {
+        f();
+        return BL_OK;
+    } catch (const Err &e) {
+        return e.code;
+    } catch (const std::bad_alloc &) {
+        g_err = "host allocation failed";
+        return BL_ERR_OOM;
+    }
+}
+
+struct EvPair {
+    bl_prep *pp;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> *vec;
+    cudaEvent_t e1 = nullptr;
+    EvPair(bl_prep *pp_, std::vector<std::pair<cudaEvent_t, cudaEvent_t>> *v) : pp(pp_), vec(v) {
+        if (!pp->profile) return;
+        cudaEvent_t e0;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaEventRecord(e0, pp->stream));
+        vec->push_back({e0, e1});
+    }
+    ~EvPair() {
+        if (pp->profile && e1) cudaEventRecord(e1, pp->stream);
+    }
+};
+
+double sum_events(std::vector<std::pair<cudaEvent_t, cudaEvent_t>> &v) {
+    double tot = 0.0;
+    for (auto &pr : v) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) tot += ms;
+        cudaEventDestroy(pr.first);
+        cudaEventDestroy(pr.second);
+    }
+    v.clear();
+    return tot;
+}
+
+int grid_for(const void *kern, int threads, size_t smem, int nsm) {
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
+    if (occ < 1) raise(BL_ERR_OOM, "kernel does not fit on an SM (smem %zu B)", smem);
+    return occ * nsm;
+}
+
+void set_smem(const void *kern, size_t smem) {
+    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+}
+
+// ------------------------------------------------------------ scan launcher
+// Raw-dot + identity epilogue over `list` (or all columns); v = fp64 vector
+// (fp32/fp64 designs) -- for int8 designs v is quantised to limbs first.
+void launch_scan(bl_prep *pp, ScanArgs a, const double *v_dev, bool timed) {
+    bl_design *d = pp->d;
+    a.X = d->X;
+    a.ld = d->ld;
+    a.n = (int)d->n;
+    a.p = d->p;
+    a.c = pp->c;
+    a.s = pp->s;
+    if (d->dt == DT_I8) {
+        k_limbs<<<1, 1024, 0, pp->stream>>>(v_dev, (int)d->n, pp->limb_ld, pp->limbs, pp->limb_scale,
+                                            pp->limb_sum);
+        CKL();
+        pp->launches++;
+        a.limbs = pp->limbs;
+        a.limb_ld = pp->limb_ld;
+        a.limb_scale = pp->limb_scale;
+        a.K1 = pp->limb_sum;      // sum of the quantised vector: identity holds exactly for it
+        size_t smem = (size_t)8 * pp->limb_ld;
+        static std::once_flag once;
+        std::call_once(once, [&] { set_smem((const void *)k_scan_i8, 200 * 1024); });
+        int grid = grid_for((const void *)k_scan_i8, kScanThreads, smem, d->nsm);
+        EvPair ev(pp, timed ? &pp->ev_scan : &pp->ev_prep);
+        k_scan_i8<<<grid, kScanThreads, smem, pp->stream>>>(a);
+        CKL();
+    } else {
+        a.v = v_dev;
+        int V = 16 / itemsize(d->dt);
+        size_t smem = (size_t)8 * round_up(d->n, 32 * V);
+        if (d->dt == DT_F32) {
+            static std::once_flag once;
+            std::call_once(once, [&] { set_smem((const void *)k_scan_fp<float, 4>, 200 * 1024); });
+            int grid = grid_for((const void *)k_scan_fp<float, 4>, kScanThreads, smem, d->nsm);
+            EvPair ev(pp, timed ? &pp->ev_scan : &pp->ev_prep);
+            k_scan_fp<float, 4><<<grid, kScanThreads, smem, pp->stream>>>(a);
+            CKL();
+        } else {
+            static std::once_flag once;
+            std::call_once(once, [&] { set_smem((const void *)k_scan_fp<double, 4>, 200 * 1024); });
+            int grid = grid_for((const void *)k_scan_fp<double, 4>, kScanThreads, smem, d->nsm);
+            EvPair ev(pp, timed ? &pp->ev_scan : &pp->ev_prep);
+            k_scan_fp<double, 4><<<grid, kScanThreads, smem, pp->stream>>>(a);
+            CKL();
+        }
+    }
+    pp->launches++;
+}
+
+template <typename T>
+void launch_colstats(bl_prep *pp, int i0) {
+    bl_design *d = pp->d;
+    int grid = d->nsm * 8;
+    if (pp->has_mask)
+        k_colstats<T, true><<<grid, 256, 0, pp->stream>>>((const T *)d->X, d->ld, (int)d->n, d->p, pp->mask, i0,
+                                                           pp->nt, pp->c, pp->s);
+    else
+        k_colstats<T, false><<<grid, 256, 0, pp->stream>>>((const T *)d->X, d->ld, (int)d->n, d->p, nullptr, i0,
+                                                            pp->nt, pp->c, pp->s);
+    CKL();
+    pp->launches++;
+}
+
+template <typename T>
+void launch_xstar(bl_prep *pp) {
+    bl_design *d = pp->d;
+    k_xstar<T><<<1, 1024, 0, pp->stream>>>((const T *)d->X, d->ld, (int)d->n, (int)pp->vlen,
+                                           pp->has_mask ? pp->mask : nullptr, pp->ps, pp->vtmp);
+    CKL();
+    pp->launches++;
+}
+
+void free_prep(bl_prep *pp) {
+    if (!pp) return;
+    if (pp->stream) cudaStreamSynchronize(pp->stream);
+    sum_events(pp->ev_scan);
+    sum_events(pp->ev_cd);
+    sum_events(pp->ev_prep);
+    if (pp->arena) cudaFree(pp->arena);
+    if (pp->hst) cudaFreeHost(pp->hst);
+    if (pp->hlist) cudaFreeHost(pp->hlist);
+    if (pp->hbw) cudaFreeHost(pp->hbw);
+    if (pp->hup) cudaFreeHost(pp->hup);
+    if (pp->own_stream && pp->stream) cudaStreamDestroy(pp->stream);
+    pp->magic = MAGIC_DEAD;
+    delete pp;
+}
+
+struct PrepGuard {
+    bl_prep *pp;
+    ~PrepGuard() { free_prep(pp); }
+};
+
+// One-time preprocessing for (y, optional training mask).
+bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double alpha, const bl_opts *opts) {
+    if (!y) raise(BL_ERR_ARG, "y is NULL");
+    if (!(alpha > 0.0 && alpha <= 1.0)) raise(BL_ERR_ARG, "alpha must be in (0, 1], got %g", alpha);
+    CK(cudaSetDevice(d->device));
+    bl_prep *pp = new bl_prep();
+    PrepGuard guard{pp};
+    pp->magic = MAGIC_PREP;
+    pp->d = d;
+    pp->alpha = alpha;
+    pp->p = d->p;
+    pp->ld = d->ld;
+    pp->profile = opts ? opts->profile : 0;
+    if (opts && opts->stream) {
+        pp->stream = (cudaStream_t)opts->stream;
+        pp->own_stream = false;
+    } else {
+        CK(cudaStreamCreateWithFlags(&pp->stream, cudaStreamNonBlocking));
+        pp->own_stream = true;
+    }
+    const int64_t n = d->n, p = d->p;
+    int64_t nt = n, i0 = 0;
+    if (train) {
+        nt = 0;
+        i0 = -1;
+        for (int64_t i = 0; i < n; i++)
+            if (train[i]) { nt++; if (i0 < 0) i0 = i; }
+    }
+    if (nt < 2) raise(BL_ERR_ARG, "need at least 2 rows, got %lld", (long long)nt);
+    pp->nt = (double)nt;
+    pp->has_mask = train != nullptr;
+    pp->vlen = round_up(std::max<int64_t>(d->ld, 1024), 128);
+    pp->limb_ld = (int)(round_up(d->ld, 128) + 64);
+    pp->Wcap = std::min<int64_t>(p, 1 << 20);
+    pp->amax_blocks = d->nsm * 4;
+    // arena layout
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off = round_up(off + bytes, 256); return o; };
+    size_t o_c = take(8 * p), o_s = take(8 * p), o_a = take(8 * p), o_b = take(8 * p), o_z = take(8 * p),
+           o_beta = take(8 * p), o_flags = take(p), o_wflag = take(p), o_mask = take(pp->vlen),
+           o_scope = take(4 * p), o_viol = take(4 * p), o_strong = take(4 * p), o_W = take(4 * pp->Wcap),
+           o_bw = take(24 * pp->Wcap), o_yt = take(8 * pp->vlen), o_rf = take(8 * pp->vlen),
+           o_rs = take(8 * pp->vlen), o_vt = take(8 * pp->vlen), o_limbs = take((size_t)8 * pp->limb_ld),
+           o_lsc = take(32), o_ps = take(sizeof(PrepScalars)), o_st = take(sizeof(RoundStatus)),
+           o_av = take(8 * pp->amax_blocks), o_ai = take(8 * pp->amax_blocks), o_nl = take(16);
+    pp->arena_bytes = off;
+    cudaError_t e = cudaMalloc(&pp->arena, off);
+    if (e != cudaSuccess) raise(BL_ERR_OOM, "cudaMalloc(%zu) failed: %s", off, cudaGetErrorString(e));
+    char *A = pp->arena;
+    pp->c = (double *)(A + o_c); pp->s = (double *)(A + o_s); pp->a = (double *)(A + o_a);
+    pp->b = (double *)(A + o_b); pp->z = (double *)(A + o_z); pp->beta = (double *)(A + o_beta);
+    pp->flags = (uint8_t *)(A + o_flags); pp->wflag = (uint8_t *)(A + o_wflag); pp->mask = (uint8_t *)(A + o_mask);
+    pp->scope = (int *)(A + o_scope); pp->viol = (int *)(A + o_viol); pp->strong = (int *)(A + o_strong);
+    pp->W = (int *)(A + o_W); pp->betaW = (double *)(A + o_bw); pp->yt = (double *)(A + o_yt);
+    pp->rfull = (double *)(A + o_rf); pp->rscan = (double *)(A + o_rs); pp->vtmp = (double *)(A + o_vt);
+    pp->limbs = (int8_t *)(A + o_limbs); pp->limb_scale = (double *)(A + o_lsc); pp->limb_sum = pp->limb_scale + 1;
+    pp->ps = (PrepScalars *)(A + o_ps); pp->st = (RoundStatus *)(A + o_st);
+    pp->amax_v = (double *)(A + o_av); pp->amax_i = (long long *)(A + o_ai); pp->nlive = (int *)(A + o_nl);
+    CK(cudaMallocHost(&pp->hst, sizeof(RoundStatus)));
+    CK(cudaMallocHost(&pp->hlist, sizeof(int) * std::max<int64_t>(p, 1)));
+    CK(cudaMallocHost(&pp->hbw, 24 * pp->Wcap));
+    CK(cudaMallocHost(&pp->hup, 4 * (pp->Wcap + p)));
+    cudaStream_t st = pp->stream;
+    CK(cudaMemsetAsync(pp->beta, 0, 8 * p, st));
+    CK(cudaMemsetAsync(pp->wflag, 0, p, st));
+    CK(cudaMemsetAsync(pp->st, 0, sizeof(RoundStatus), st));
+    CK(cudaMemsetAsync(pp->nlive, 0, 16, st));
+    CK(cudaMemsetAsync(pp->limbs, 0, (size_t)8 * pp->limb_ld, st));
+    if (train) {
+        std::vector<uint8_t> m(pp->vlen, 0);
+        for (int64_t i = 0; i < n; i++) m[i] = train[i] ? 1 : 0;
+        CK(cudaMemcpyAsync(pp->mask, m.data(), pp->vlen, cudaMemcpyHostToDevice, st));
+    }
+    // y -> device (staged through the rfull buffer, then centred in place into yt / rfull)
+    CK(cudaMemcpyAsync(pp->vtmp, y, 8 * n, cudaMemcpyHostToDevice, st));
+    {
+        EvPair ev(pp, &pp->ev_prep);
+        k_center_y<<<1, 1024, 0, st>>>(pp->vtmp, (int)n, (int)pp->vlen, train ? pp->mask : nullptr, pp->nt,
+                                       pp->yt, pp->rfull, pp->ps);
+        CKL();
+        pp->launches++;
+        if (d->dt == DT_F64) launch_colstats<double>(pp, (int)i0);
+        else if (d->dt == DT_F32) launch_colstats<float>(pp, (int)i0);
+        else launch_colstats<int8_t>(pp, (int)i0);
+    }
+    // a_j = x~_j' y~  (identity (2))
+    {
+        ScanArgs sa{};
+        sa.K1 = &pp->ps->sum_yt;
+        sa.K2 = nullptr;
+        sa.K2v = 1.0;
+        sa.out = pp->a;
+        sa.jfix = nullptr;
+        launch_scan(pp, sa, pp->yt, false);
+    }
+    // lambda_max, j*
+    k_argmax1<<<pp->amax_blocks, 256, 0, st>>>(pp->a, pp->s, p, pp->amax_v, pp->amax_i, pp->nlive);
+    CKL();
+    k_argmax2<<<1, 32, 0, st>>>(pp->amax_v, pp->amax_i, pp->amax_blocks, pp->a, pp->c, pp->s, alpha, pp->nlive,
+                                pp->ps);
+    CKL();
+    pp->launches += 2;
+    // b_j = x~_j' x~_*  (identity (1)); b_j* = n exactly
+    if (d->dt == DT_F64) launch_xstar<double>(pp);
+    else if (d->dt == DT_F32) launch_xstar<float>(pp);
+    else launch_xstar<int8_t>(pp);
+    {
+        ScanArgs sa{};
+        sa.K1 = &pp->ps->sum_v;
+        sa.K2 = &pp->ps->inv_s_star;
+        sa.out = pp->b;
+        sa.jfix = &pp->ps->jstar;
+        sa.fixval = &pp->ps->nt;
+        launch_scan(pp, sa, pp->vtmp, false);
+    }
+    // the one host round trip of preprocessing: the scalars the lambda loop branches on
+    CK(cudaMemcpyAsync(&pp->hps, pp->ps, sizeof(PrepScalars), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    pp->prep_bytes = 3.0 * (double)d->n * itemsize(d->dt) * (double)d->p;
+    if (!(pp->hps.Y2 > 0.0)) raise(BL_ERR_DEGENERATE, "y is constant on the used rows (y~ == 0)");
+    if (pp->hps.n_live == 0 && d->world == 1) raise(BL_ERR_DEGENERATE, "every column has zero variance");
+    if (!(pp->hps.A > 0.0) && d->world == 1) raise(BL_ERR_DEGENERATE, "lambda_max == 0: y~ orthogonal to every column");
+    guard.pp = nullptr;
+    return pp;
+}
+
+// ------------------------------------------------------------------ the path
+
+void sorted_merge_into(std::vector<int> &W, std::vector<int> add) {
+    std::sort(add.begin(), add.end());
+    add.erase(std::unique(add.begin(), add.end()), add.end());
+    std::vector<int> out;
+    out.reserve(W.size() + add.size());
+    std::set_union(W.begin(), W.end(), add.begin(), add.end(), std::back_inserter(out));
+    W.swap(out);
+}
+
+void upload_W(bl_prep *pp, const std::vector<int> &W, const std::vector<int> &added) {
+    if ((int64_t)W.size() > pp->Wcap) raise(BL_ERR_OOM, "working set %zu exceeds capacity %lld", W.size(), (long long)pp->Wcap);
+    cudaStream_t st = pp->stream;
+    // pinned staging: the previous round ended with a stream sync, so hup is free
+    std::memcpy(pp->hup, W.data(), 4 * W.size());
+    std::memcpy(pp->hup + W.size(), added.data(), 4 * added.size());
+    if (!W.empty()) CK(cudaMemcpyAsync(pp->W, pp->hup, 4 * W.size(), cudaMemcpyHostToDevice, st));
+    if (!added.empty()) {
+        CK(cudaMemcpyAsync(pp->viol, pp->hup + W.size(), 4 * added.size(), cudaMemcpyHostToDevice, st));
+        k_set_flags<<<(unsigned)((added.size() + 255) / 256), 256, 0, st>>>(pp->viol, (int)added.size(), pp->wflag, 1);
+        CKL();
+        pp->launches++;
+    }
+}
+
+std::vector<int> read_list(bl_prep *pp, const int *dev, int count) {
+    std::vector<int> v(count);
+    if (count > 0) {
+        CK(cudaMemcpyAsync(pp->hlist, dev, 4 * (size_t)count, cudaMemcpyDeviceToHost, pp->stream));
+        CK(cudaStreamSynchronize(pp->stream));
+        std::memcpy(v.data(), pp->hlist, 4 * (size_t)count);
+        std::sort(v.begin(), v.end());
+    }
+    return v;
+}
+
+// CD block shape: rows per thread R <= RM in {4, 8, 16}; RM <= 8 kernels are
+// compiled for <= 512 threads (128 registers), RM = 16 for 1024 threads.
+int cd_threads(int64_t n) {
+    int64_t rm = n <= 2048 ? 4 : n <= 4096 ? 8 : 16;
+    int64_t t = round_up(std::max<int64_t>((n + rm - 1) / rm, 64), 32);
+    return (int)std::min<int64_t>(t, rm >= 16 ? 1024 : 512);
+}
+
+template <typename T, bool M>
+const void *cd_kernel_rm(int R) {
+    if (R <= 4) return (const void *)k_cd<T, M, 4>;
+    if (R <= 8) return (const void *)k_cd<T, M, 8>;
+    return (const void *)k_cd<T, M, 16>;   // R <= 16 by construction (n <= 16384)
+}
+
+const void *cd_kernel(int dt, bool mask, int R) {
+    if (dt == DT_F64) return mask ? cd_kernel_rm<double, true>(R) : cd_kernel_rm<double, false>(R);
+    if (dt == DT_F32) return mask ? cd_kernel_rm<float, true>(R) : cd_kernel_rm<float, false>(R);
+    return mask ? cd_kernel_rm<int8_t, true>(R) : cd_kernel_rm<int8_t, false>(R);
+}
+
+void launch_cd(bl_prep *pp, int nW, double lam, double alpha, double tol, int max_iter) {
+    bl_design *d = pp->d;
+    CdArgs ca{};
+    ca.X = d->X;
+    ca.ld = d->ld;
+    ca.n = (int)d->n;
+    ca.W = pp->W;
+    ca.nW = nW;
+    ca.c = pp->c;
+    ca.s = pp->s;
+    ca.beta = pp->beta;
+    ca.r = pp->rfull;
+    ca.r_scan = pp->rscan;
+    ca.mask = pp->has_mask ? pp->mask : nullptr;
+    ca.lam_alpha = lam * alpha;
+    ca.inv_den = 1.0 / (1.0 + lam * (1.0 - alpha));
+    ca.inv_n = 1.0 / pp->nt;
+    ca.tol = tol;
+    ca.floor_ = 1e-13 * (alpha * lam + std::sqrt(pp->hps.Y2 / pp->nt));   // Q6 noise floor
+    ca.max_iter = max_iter;
+    ca.betaW_out = pp->betaW;
+    ca.st = pp->st;
+    int T = cd_threads(d->n);
+    int R = (int)((d->n + T - 1) / T);
+    size_t smem = (size_t)8 * R * T + (size_t)12 * nW + 16;
+    if (smem > 227 * 1024)
+        raise(BL_ERR_OOM, "working set of %d columns does not fit the CD kernel's shared memory (n=%lld)", nW,
+              (long long)d->n);
+    const void *kern = cd_kernel(d->dt, pp->has_mask != 0, R);
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    EvPair ev(pp, &pp->ev_cd);
+    void *args[] = {&ca};
+    CK(cudaLaunchKernel(kern, dim3(1), dim3(T), args, smem, pp->stream));
+    pp->launches++;
+}
+
+// One full path.  Fills `out` (prefix on convergence failure).
+bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, double tol, int max_iter, int screen,
+                   int max_rounds, bl_path *out, double *heldout /* K x n or nullptr */) {
+    bl_design *d = pp->d;
+    cudaStream_t st = pp->stream;
+    const double nt = pp->nt;
+    const double lmax = pp->hps.lmax;
+    const double snap = lmax * (1.0 - 1e-12);                 // Q25
+    out->n_lambda = K;
+    out->n_converged = 0;
+    out->lambda.assign(lambda, lambda + K);
+    out->a0.assign(K, 0.0);
+    out->obj.assign(K, 0.0);
+    out->passes.assign(K, 0);
+    out->kkt_rounds.assign(K, 0);
+    out->cols_scanned.assign(K, 0);
+    out->col_ptr.assign(K + 1, 0);
+    std::vector<int> W;
+    const int bthreads = 256;
+    const int bgrid = (int)std::min<int64_t>((d->p + bthreads - 1) / bthreads, (int64_t)d->nsm * 8);
+    const int use_bedpp = screen == BL_SCREEN_HYBRID;
+    bool first = true;
+    double lam_prev = lmax;
+    std::vector<int> strong_next;
+    bl_status status = BL_OK;
+
+
+    if (screen == BL_SCREEN_NONE) {
+        // W = every non-constant column; no screening, no scans (SPEC "policy none")
+        CK(cudaMemsetAsync(pp->st, 0, sizeof(RoundStatus), st));
+        k_bedpp<<<bgrid, bthreads, 0, st>>>(d->p, pp->s, pp->a, pp->b, pp->ps, alpha, lmax, -1.0, 0, pp->flags,
+                                            pp->scope, pp->st);
+        CKL();
+        pp->launches++;
+        CK(cudaMemcpyAsync(pp->hst, pp->st, sizeof(RoundStatus), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        std::vector<int> all = read_list(pp, pp->scope, pp->hst->nscope);
+        sorted_merge_into(W, all);
+        upload_W(pp, W, all);
+    }
+
+    for (int k = 0; k < K; k++) {
+        const double lam = lambda[k];
+        if (lam >= snap) {          // null solution, exactly (Q25)
+            out->a0[k] = pp->hps.ybar;
+            out->obj[k] = pp->hps.Y2 / (2.0 * nt);
+            out->col_ptr[k + 1] = out->col_ptr[k];
+            out->n_converged = k + 1;
+            if (heldout) {
+                // held-out residual of the null model: y_i - ybar_train (rfull is untouched at beta = 0)
+                CK(cudaMemcpyAsync(heldout + (size_t)k * d->n, pp->rfull, 8 * d->n, cudaMemcpyDeviceToHost, st));
+            }
+            continue;
+        }
+        const double lam_next = k + 1 < K ? lambda[k + 1] : -1.0;
+        if (screen != BL_SCREEN_NONE) {
+            CK(cudaMemsetAsync(pp->st, 0, sizeof(RoundStatus), st));
+            k_bedpp<<<bgrid, bthreads, 0, st>>>(d->p, pp->s, pp->a, pp->b, pp->ps, alpha, lam, lam_next, use_bedpp,
+                                                pp->flags, use_bedpp ? pp->scope : nullptr, pp->st);
+            CKL();
+            pp->launches++;
+            if (first) {
+                // strong set at the first solved lambda from the null solution z = a/n (a6)
+                double lp = std::min(lam_prev, lmax);
+                double thr = alpha * (2.0 * lam - lp);
+                k_ssr_init<<<bgrid, bthreads, 0, st>>>(d->p, pp->a, pp->s, pp->flags, pp->wflag, pp->ps,
+                                                       thr < 0.0 ? 0.0 : thr, pp->z, pp->strong, &pp->st->nstrong);
+                CKL();
+                pp->launches++;
+                CK(cudaMemcpyAsync(pp->hst, pp->st, sizeof(RoundStatus), cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+                strong_next = read_list(pp, pp->strong, pp->hst->nstrong);
+                first = false;
+            }
+            sorted_merge_into(W, strong_next);
+            upload_W(pp, W, strong_next);
+            strong_next.clear();
+        }
+        int rounds = 0;
+        int64_t scanned = 0;
+        int passes = 0;
+        for (;;) {
+            launch_cd(pp, (int)W.size(), lam, alpha, tol, max_iter);
+            if (screen == BL_SCREEN_NONE) {
+                CK(cudaMemcpyAsync(pp->hst, pp->st, sizeof(RoundStatus), cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+                passes += pp->hst->cd_passes;
+                if (pp->hst->cd_status) { status = BL_ERR_CONVERGENCE; break; }
+                break;
+            }
+            // reset round counters (keep nscope / nsafe from BEDPP)
+            CK(cudaMemsetAsync(&pp->st->nviol, 0, 2 * sizeof(int), st));
+            ScanArgs sa{};
+            sa.list = use_bedpp ? pp->scope : nullptr;
+            sa.nlist = &pp->st->nscope;
+            sa.K1 = &pp->st->sumr;
+            sa.K2v = 1.0 / nt;
+            sa.out = pp->z;
+            sa.jfix = nullptr;
+            sa.scan = 1;
+            sa.flags = pp->flags;
+            sa.wflag = pp->wflag;
+            sa.thr_viol = alpha * lam;
+            sa.thr_strong = lam_next > 0.0 ? alpha * (2.0 * lam_next - lam) : -1.0;
+            if (sa.thr_strong < 0.0 && lam_next > 0.0) sa.thr_strong = 0.0;
+            sa.viol = pp->viol;
+            sa.nviol = &pp->st->nviol;
+            sa.strong = pp->strong;
+            sa.nstrong = &pp->st->nstrong;
+            launch_scan(pp, sa, pp->rscan, true);
+            CK(cudaMemcpyAsync(pp->hst, pp->st, sizeof(RoundStatus), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            passes += pp->hst->cd_passes;
+            scanned += use_bedpp ? pp->hst->nscope : pp->hps.n_live;
+            if (pp->hst->cd_status) { status = BL_ERR_CONVERGENCE; break; }
+            if (pp->hst->nviol > 0) {
+                if (++rounds > max_rounds) {
+                    g_err = "more than max KKT rounds at one lambda";
+                    status = BL_ERR_CONVERGENCE;
+                    break;
+                }
+                std::vector<int> v = read_list(pp, pp->viol, pp->hst->nviol);
+                sorted_merge_into(W, v);
+                upload_W(pp, W, v);
+                continue;
+            }
+            strong_next = read_list(pp, pp->strong, pp->hst->nstrong);
+            break;
+        }
+        if (status != BL_OK) {
+            if (g_err.empty() || pp->hst->cd_status)
+                g_err = "coordinate descent did not converge within max_iter passes at lambda index " + std::to_string(k);
+            break;
+        }
+        // record lambda_k (a11)
+        RoundStatus rs = *pp->hst;
+        int nW = (int)W.size();
+        if (nW > 0) {
+            CK(cudaMemcpyAsync(pp->hbw, pp->betaW, 24 * (size_t)nW, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+        }
+        // unstandardise (Q4): beta_orig = beta/s_j, a0 = ybar - sum beta_orig c_j
+        double shift = 0.0;
+        for (int q = 0; q < nW; q++) {
+            double bq = pp->hbw[q];
+            if (bq == 0.0) continue;
+            double cq = pp->hbw[nW + q], sq = pp->hbw[2 * nW + q];
+            out->feat.push_back(W[q] + d->col_offset);
+            out->beta_std.push_back(bq);
+            out->beta_orig.push_back(bq / sq);
+            shift += bq * cq / sq;
+        }
+        out->col_ptr[k + 1] = (int64_t)out->feat.size();
+        out->a0[k] = pp->hps.ybar - shift;
+        out->obj[k] = rs.rss / (2.0 * nt) + lam * (alpha * rs.l1 + 0.5 * (1.0 - alpha) * rs.l2);
+        out->passes[k] = passes;
+        out->kkt_rounds[k] = rounds + (screen == BL_SCREEN_NONE ? 0 : 1);
+        out->cols_scanned[k] = scanned;
+        if (heldout)
+            CK(cudaMemcpyAsync(heldout + (size_t)k * d->n, pp->rfull, 8 * d->n, cudaMemcpyDeviceToHost, st));
+        out->n_converged = k + 1;
+        lam_prev = lam;
+    }
+    CK(cudaStreamSynchronize(st));
+    return status;
+}
+
+void validate_grid(const double *lambda, int K) {
+    if (!lambda || K < 1) raise(BL_ERR_ARG, "need at least one lambda");
+    for (int k = 0; k < K; k++) {
+        if (!(lambda[k] > 0.0) || !std::isfinite(lambda[k])) raise(BL_ERR_ARG, "lambda[%d] = %g must be > 0", k, lambda[k]);
+        if (k > 0 && !(lambda[k] < lambda[k - 1])) raise(BL_ERR_ARG, "lambda must be strictly decreasing (index %d)", k);
+    }
+}
+
+void finish_perf(bl_prep *pp, bl_path *out, double wall_ms) {
+    CK(cudaStreamSynchronize(pp->stream));
+    bl_perf &pf = out->perf;
+    std::memset(&pf, 0, sizeof pf);
+    pf.scan_launches = (int64_t)pp->ev_scan.size();
+    pf.cd_launches = (int64_t)pp->ev_cd.size();
+    pf.scan_ms = sum_events(pp->ev_scan);
+    pf.cd_ms = sum_events(pp->ev_cd);
+    pf.prep_ms = sum_events(pp->ev_prep);
+    int64_t cols = 0;
+    for (int k = 0; k < out->n_converged; k++) cols += out->cols_scanned[k];
+    pf.scan_bytes = (double)cols * (double)pp->d->n * itemsize(pp->d->dt);
+    pf.prep_bytes = pp->prep_bytes;
+    pf.kernel_launches = pp->launches;
+    pf.wall_ms = wall_ms;
+}
+
+bl_path *fit_impl(bl_design *d, const double *y, const uint8_t *train, const double *lambda, int K, double alpha,
+                  double tol, int max_iter, int screen, const bl_opts *opts, bl_status *st_out,
+                  double *heldout = nullptr) {
+    auto t0 = std::chrono::steady_clock::now();
+    validate_grid(lambda, K);
+    if (!(tol > 0.0)) raise(BL_ERR_ARG, "tol must be > 0");
+    if (max_iter < 1) raise(BL_ERR_ARG, "max_iter must be >= 1");
+    if (screen < 0 || screen > 2) raise(BL_ERR_ARG, "screen must be 0, 1 or 2");
+    bl_prep *pp = make_prep(d, y, train, alpha, opts);
+    PrepGuard g{pp};
+    bl_path *out = new bl_path();
+    out->magic = MAGIC_PATH;
+    int rounds = opts && opts->max_kkt_rounds > 0 ? opts->max_kkt_rounds : 10;
+    std::string saved;
+    bl_status s;
+    try {
+        s = run_path(pp, lambda, K, alpha, tol, max_iter, screen, rounds, out, heldout);
+    } catch (...) {
+        delete out;
+        throw;
+    }
+    saved = g_err;
+    double wall = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    finish_perf(pp, out, wall);
+    g_err = saved;
+    *st_out = s;
+    return out;
+}
+
+uint64_t splitmix64(uint64_t &state) {
+    uint64_t z = (state += 0x9E3779B97F4A7C15ULL);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+}  // namespace
+
+// ================================================================== C ABI
+
+extern "C" {
+
+const char *bl_last_error(void) { return g_err.c_str(); }
+
+bl_status bl_nccl_unique_id(void *out128) {
+    return guard([&] {
+        if (!out128) raise(BL_ERR_ARG, "out is NULL");
+        ncclUniqueId id;
+        CKN(ncclGetUniqueId(&id));
+        static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+        std::memcpy(out128, &id, 128);
+    });
+}
+
+bl_status bl_load_design(const void *X, bl_dtype dt, int64_t n, int64_t p_local, int64_t ld, int x_is_device_ptr,
+                         const bl_dist *dist, bl_design **out) {
+    return guard([&] {
+        if (!out) raise(BL_ERR_ARG, "out is NULL");
+        *out = nullptr;
+        if (!X) raise(BL_ERR_ARG, "X is NULL");
+        if (dt < BL_F64 || dt > BL_I8) raise(BL_ERR_ARG, "bad dtype %d", (int)dt);
+        if (n < 2) raise(BL_ERR_ARG, "n must be >= 2 (got %lld)", (long long)n);
+        if (n > (int64_t)kCdRmax * 1024) raise(BL_ERR_ARG, "n = %lld exceeds 16384 (r must fit one SM)", (long long)n);
+        if (p_local < 1) raise(BL_ERR_ARG, "p must be >= 1");
+        if (ld < n) raise(BL_ERR_ARG, "ld < n");
+        if (p_local > INT32_MAX) raise(BL_ERR_ARG, "p_local too large");
+        check_device();
+        bl_design *d = new bl_design();
+        d->magic = MAGIC_DESIGN;
+        d->dt = (int)dt;
+        d->n = n;
+        d->p = p_local;
+        d->rank = 0;
+        d->world = 1;
+        d->comm = nullptr;
+        d->col_offset = 0;
+        d->p_global = p_local;
+        CK(cudaGetDevice(&d->device));
+        if (dist) {
+            if (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world) { delete d; raise(BL_ERR_ARG, "bad bl_dist"); }
+            d->rank = dist->rank;
+            d->world = dist->world;
+            d->col_offset = dist->col_offset;
+            d->p_global = dist->p_global;
+            if (dist->device >= 0) d->device = dist->device;
+            CK(cudaSetDevice(d->device));
+        }
+        CK(cudaDeviceGetAttribute(&d->nsm, cudaDevAttrMultiProcessorCount, d->device));
+        int isz = itemsize(dt);
+        if (x_is_device_ptr) {
+            if (((uintptr_t)X % 16) != 0 || (ld * isz) % 16 != 0) {
+                delete d;
+                raise(BL_ERR_ARG, "device X needs a 16-byte aligned base and ld*itemsize %% 16 == 0");
+            }
+            d->X = const_cast<void *>(X);
+            d->owned = false;
+            d->ld = ld;
+        } else {
+            int64_t ldp = round_up(n, 16 / isz);
+            size_t bytes = (size_t)ldp * p_local * isz;
+            cudaError_t e = cudaMalloc(&d->X, bytes);
+            if (e != cudaSuccess) { delete d; raise(BL_ERR_OOM, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e)); }
+            d->owned = true;
+            d->ld = ldp;
+            CK(cudaMemset(d->X, 0, bytes));
+            CK(cudaMemcpy2D(d->X, ldp * isz, X, ld * isz, n * isz, p_local, cudaMemcpyHostToDevice));
+        }
+        if (d->world > 1) {
+            if (!dist->nccl_unique_id) { if (d->owned) cudaFree(d->X); delete d; raise(BL_ERR_ARG, "nccl_unique_id required for world > 1"); }
+            ncclUniqueId id;
+            std::memcpy(&id, dist->nccl_unique_id, sizeof id);
+            CKN(ncclCommInitRank(&d->comm, d->world, id, d->rank));
+        }
+        *out = d;
+    });
+}
+
+bl_status bl_prepare(bl_design *d, const double *y, const uint8_t *train, double alpha, bl_prep **out) {
+    return guard([&] {
+        if (!d || d->magic != MAGIC_DESIGN) raise(BL_ERR_ARG, "bad design handle");
+        if (!out) raise(BL_ERR_ARG, "out is NULL");
+        *out = make_prep(d, y, train, alpha, nullptr);
+    });
+}
+
+bl_status bl_lambda_max(bl_design *d, const double *y, double alpha, double *out) {
+    return guard([&] {
+        if (!d || d->magic != MAGIC_DESIGN) raise(BL_ERR_ARG, "bad design handle");
+        if (!out) raise(BL_ERR_ARG, "out is NULL");
+        bl_prep *pp = make_prep(d, y, nullptr, alpha, nullptr);
+        *out = pp->hps.lmax;
+        free_prep(pp);
+    });
+}
+
+bl_status bl_prep_copy(const bl_prep *pp, double *c, double *s, double *a, double *b, int64_t *jstar_global,
+                       double *lambda_max) {
+    return guard([&] {
+        if (!pp || pp->magic != MAGIC_PREP) raise(BL_ERR_ARG, "bad prep handle");
+        int64_t p = pp->p;
+        if (c) CK(cudaMemcpy(c, pp->c, 8 * p, cudaMemcpyDeviceToHost));
+        if (s) CK(cudaMemcpy(s, pp->s, 8 * p, cudaMemcpyDeviceToHost));
+        if (a) CK(cudaMemcpy(a, pp->a, 8 * p, cudaMemcpyDeviceToHost));
+        if (b) CK(cudaMemcpy(b, pp->b, 8 * p, cudaMemcpyDeviceToHost));
+        if (jstar_global) *jstar_global = pp->hps.jstar >= 0 ? pp->hps.jstar + pp->d->col_offset : -1;
+        if (lambda_max) *lambda_max = pp->hps.lmax;
+    });
+}
+
+bl_status bl_bedpp(bl_prep *pp, double lambda, uint8_t *keep, int64_t *n_keep) {
+    return guard([&] {
+        if (!pp || pp->magic != MAGIC_PREP) raise(BL_ERR_ARG, "bad prep handle");
+        if (!(lambda > 0.0)) raise(BL_ERR_ARG, "lambda must be > 0");
+        bl_design *d = pp->d;
+        CK(cudaSetDevice(d->device));
+        cudaStream_t st = pp->stream;
+        CK(cudaMemsetAsync(pp->st, 0, sizeof(RoundStatus), st));
+        int grid = (int)std::min<int64_t>((d->p + 255) / 256, (int64_t)d->nsm * 8);
+        k_bedpp<<<grid, 256, 0, st>>>(d->p, pp->s, pp->a, pp->b, pp->ps, pp->alpha, lambda, -1.0, 1, pp->flags,
+                                      pp->scope, pp->st);
+        CKL();
+        std::vector<uint8_t> f(d->p);
+        CK(cudaMemcpyAsync(f.data(), pp->flags, d->p, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(pp->hst, pp->st, sizeof(RoundStatus), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        for (int64_t j = 0; j < d->p; j++)
+            if (keep) keep[j] = f[j] & 1;
+        if (n_keep) *n_keep = pp->hst->nsafe;
+    });
+}
+
+bl_status bl_scan(bl_prep *pp, const double *r, double lam, double lam_next, const uint8_t *in_w, double *z,
+                  int32_t *viol, int64_t *n_viol, int32_t *strong, int64_t *n_strong) {
+    return guard([&] {
+        if (!pp || pp->magic != MAGIC_PREP) raise(BL_ERR_ARG, "bad prep handle");
+        if (!r) raise(BL_ERR_ARG, "r is NULL");
+        bl_design *d = pp->d;
+        CK(cudaSetDevice(d->device));
+        cudaStream_t st = pp->stream;
+        std::vector<double> rv(pp->vlen, 0.0);
+        std::memcpy(rv.data(), r, 8 * d->n);
+        CK(cudaMemcpyAsync(pp->rscan, rv.data(), 8 * pp->vlen, cudaMemcpyHostToDevice, st));
+        std::vector<uint8_t> w(d->p, 0);
+        if (in_w) std::memcpy(w.data(), in_w, d->p);
+        CK(cudaMemcpyAsync(pp->wflag, w.data(), d->p, cudaMemcpyHostToDevice, st));
+        CK(cudaMemsetAsync(pp->st, 0, sizeof(RoundStatus), st));
+        int grid = (int)std::min<int64_t>((d->p + 255) / 256, (int64_t)d->nsm * 8);
+        k_bedpp<<<grid, 256, 0, st>>>(d->p, pp->s, pp->a, pp->b, pp->ps, pp->alpha, lam, lam_next > 0 ? lam_next : -1.0,
+                                      0, pp->flags, nullptr, pp->st);
+        CKL();
+        k_vsum<<<1, 1024, 0, st>>>(pp->rscan, (int)d->n, pp->limb_scale + 2);
+        CKL();
+        ScanArgs sa{};
+        sa.K1 = pp->limb_scale + 2;    // sum_i r_i (identity (3))
+        sa.K2v = 1.0 / pp->nt;
+        sa.out = pp->z;
+        sa.jfix = nullptr;
+        sa.scan = 1;
+        sa.flags = pp->flags;
+        sa.wflag = pp->wflag;
+        sa.thr_viol = pp->alpha * lam;
+        sa.thr_strong = lam_next > 0.0 ? std::max(0.0, pp->alpha * (2.0 * lam_next - lam)) : -1.0;
+        sa.viol = pp->viol;
+        sa.nviol = &pp->st->nviol;
+        sa.strong = pp->strong;
+        sa.nstrong = &pp->st->nstrong;
+        launch_scan(pp, sa, pp->rscan, false);
+        CK(cudaMemcpyAsync(pp->hst, pp->st, sizeof(RoundStatus), cudaMemcpyDeviceToHost, st));
+        if (z) CK(cudaMemcpyAsync(z, pp->z, 8 * d->p, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        std::vector<int> v = read_list(pp, pp->viol, pp->hst->nviol);
+        std::vector<int> sv = read_list(pp, pp->strong, pp->hst->nstrong);
+        if (viol) std::copy(v.begin(), v.end(), viol);
+        if (strong) std::copy(sv.begin(), sv.end(), strong);
+        if (n_viol) *n_viol = (int64_t)v.size();
+        if (n_strong) *n_strong = (int64_t)sv.size();
+    });
+}
+
+bl_status bl_fit_path(bl_design *d, const double *y, const double *lambda, int n_lambda, double alpha, double tol,
+                      int max_iter, int screen, const bl_opts *opts, bl_path **out) {
+    bl_status s = BL_OK;
+    bl_status g = guard([&] {
+        if (!d || d->magic != MAGIC_DESIGN) raise(BL_ERR_ARG, "bad design handle");
+        if (!out) raise(BL_ERR_ARG, "out is NULL");
+        *out = nullptr;
+        if (d->world > 1) raise(BL_ERR_ARG, "multi-GPU bl_fit_path is not available in this build");
+        *out = fit_impl(d, y, nullptr, lambda, n_lambda, alpha, tol, max_iter, screen, opts, &s);
+    });
+    return g != BL_OK ? g : s;
+}
+
+bl_status bl_cv(bl_design *d, const double *y, const double *lambda, int n_lambda, double alpha, double tol,
+                int max_iter, int n_folds, const int32_t *fold_id, uint64_t seed, const bl_opts *opts,
+                bl_cvres **out) {
+    bl_status s = BL_OK;
+    bl_status g = guard([&] {
+        if (!d || d->magic != MAGIC_DESIGN) raise(BL_ERR_ARG, "bad design handle");
+        if (!out) raise(BL_ERR_ARG, "out is NULL");
+        *out = nullptr;
+        const int64_t n = d->n;
+        if (n_folds < 2 || n_folds > n) raise(BL_ERR_ARG, "need 2 <= K <= n (K = %d, n = %lld)", n_folds, (long long)n);
+        validate_grid(lambda, n_lambda);
+        std::vector<int32_t> f(n);
+        if (fold_id) {
+            for (int64_t i = 0; i < n; i++) {
+                if (fold_id[i] < 0 || fold_id[i] >= n_folds) raise(BL_ERR_ARG, "fold_id[%lld] out of range", (long long)i);
+                f[i] = fold_id[i];
+            }
+        } else {   // Q18
+            std::vector<int64_t> perm(n);
+            for (int64_t i = 0; i < n; i++) perm[i] = i;
+            uint64_t stt = seed;
+            for (int64_t i = n - 1; i >= 1; i--) {
+                int64_t jj = (int64_t)(splitmix64(stt) % (uint64_t)(i + 1));
+                std::swap(perm[i], perm[jj]);
+            }
+            for (int64_t i = 0; i < n; i++) f[perm[i]] = (int32_t)(i % n_folds);
+        }
+        std::vector<int64_t> cnt(n_folds, 0);
+        for (int64_t i = 0; i < n; i++) cnt[f[i]]++;
+        for (int k = 0; k < n_folds; k++)
+            if (cnt[k] == 0) raise(BL_ERR_ARG, "fold %d is empty", k);
+        bl_cvres *cv = new bl_cvres();
+        cv->magic = MAGIC_CV;
+        cv->n_lambda = n_lambda;
+        cv->K = n_folds;
+        cv->n = n;
+        cv->fold_id = f;
+        cv->E.assign((size_t)n_lambda * n, 0.0);
+        cv->full = nullptr;
+        std::vector<double> held((size_t)n_lambda * n);
+        std::vector<uint8_t> train(n);
+        try {
+            for (int fo = 0; fo < n_folds && s == BL_OK; fo++) {
+                for (int64_t i = 0; i < n; i++) train[i] = f[i] != fo;
+                bl_status fs = BL_OK;
+                bl_path *pth = fit_impl(d, y, train.data(), lambda, n_lambda, alpha, tol, max_iter, BL_SCREEN_HYBRID,
+                                        opts, &fs, held.data());
+                int nc = pth->n_converged;
+                for (int k = 0; k < nc; k++)
+                    for (int64_t i = 0; i < n; i++)
+                        if (!train[i]) {
+                            double e = held[(size_t)k * n + i];
+                            cv->E[(size_t)k * n + i] = e * e;
+                        }
+                delete pth;
+                if (fs != BL_OK) s = fs;
+            }
+            if (s == BL_OK) {
+                bl_status fs = BL_OK;
+                cv->full = fit_impl(d, y, nullptr, lambda, n_lambda, alpha, tol, max_iter, BL_SCREEN_HYBRID, opts, &fs);
+                if (fs != BL_OK) s = fs;
+            }
+        } catch (...) {
+            delete cv->full;
+            delete cv;
+            throw;
+        }
+        cv->cve.assign(n_lambda, 0.0);
+        cv->cvse.assign(n_lambda, 0.0);
+        int best = 0;
+        for (int k = 0; k < n_lambda; k++) {
+            double m = 0.0;
+            for (int64_t i = 0; i < n; i++) m += cv->E[(size_t)k * n + i];
+            m /= (double)n;
+            double v = 0.0;
+            for (int64_t i = 0; i < n; i++) { double dd = cv->E[(size_t)k * n + i] - m; v += dd * dd; }
+            cv->cve[k] = m;
+            cv->cvse[k] = std::sqrt(v / (double)(n - 1)) / std::sqrt((double)n);
+            if (cv->cve[k] < cv->cve[best]) best = k;
+        }
+        cv->lmin = best;
+        *out = cv;
+    });
+    return g != BL_OK ? g : s;
+}
+
+bl_status bl_path_info(const bl_path *p, int *n_lambda, int64_t *nnz_total, int *n_converged) {
+    return guard([&] {
+        if (!p || p->magic != MAGIC_PATH) raise(BL_ERR_ARG, "bad path handle");
+        if (n_lambda) *n_lambda = p->n_lambda;
+        if (nnz_total) *nnz_total = (int64_t)p->feat.size();
+        if (n_converged) *n_converged = p->n_converged;
+    });
+}
+
+bl_status bl_path_copy(const bl_path *p, double *lambda, double *a0, double *objective, int64_t *col_ptr,
+                       int64_t *feat_idx, double *beta_std, double *beta_orig, int32_t *passes, int32_t *kkt_rounds,
+                       int64_t *cols_scanned) {
+    return guard([&] {
+        if (!p || p->magic != MAGIC_PATH) raise(BL_ERR_ARG, "bad path handle");
+        int K = p->n_lambda;
+        if (lambda) std::copy(p->lambda.begin(), p->lambda.end(), lambda);
+        if (a0) std::copy(p->a0.begin(), p->a0.end(), a0);
+        if (objective) std::copy(p->obj.begin(), p->obj.end(), objective);
+        if (col_ptr) std::copy(p->col_ptr.begin(), p->col_ptr.begin() + K + 1, col_ptr);
+        if (feat_idx) std::copy(p->feat.begin(), p->feat.end(), feat_idx);
+        if (beta_std) std::copy(p->beta_std.begin(), p->beta_std.end(), beta_std);
+        if (beta_orig) std::copy(p->beta_orig.begin(), p->beta_orig.end(), beta_orig);
+        if (passes) std::copy(p->passes.begin(), p->passes.end(), passes);
+        if (kkt_rounds) std::copy(p->kkt_rounds.begin(), p->kkt_rounds.end(), kkt_rounds);
+        if (cols_scanned) std::copy(p->cols_scanned.begin(), p->cols_scanned.end(), cols_scanned);
+    });
+}
+
+bl_status bl_path_perf(const bl_path *p, bl_perf *out) {
+    return guard([&] {
+        if (!p || p->magic != MAGIC_PATH) raise(BL_ERR_ARG, "bad path handle");
+        if (!out) raise(BL_ERR_ARG, "out is NULL");
+        *out = p->perf;
+    });
+}
+
+bl_status bl_cv_copy(const bl_cvres *cv, double *cve, double *cvse, int *lambda_min_index, int32_t *fold_id_out,
+                     const bl_path **full_fit) {
+    return guard([&] {
+        if (!cv || cv->magic != MAGIC_CV) raise(BL_ERR_ARG, "bad cv handle");
+        if (cve) std::copy(cv->cve.begin(), cv->cve.end(), cve);
+        if (cvse) std::copy(cv->cvse.begin(), cv->cvse.end(), cvse);
+        if (lambda_min_index) *lambda_min_index = cv->lmin;
+        if (fold_id_out) std::copy(cv->fold_id.begin(), cv->fold_id.end(), fold_id_out);
+        if (full_fit) *full_fit = cv->full;
+    });
+}
+
+bl_status bl_cv_errors(const bl_cvres *cv, double *E) {
+    return guard([&] {
+        if (!cv || cv->magic != MAGIC_CV) raise(BL_ERR_ARG, "bad cv handle");
+        if (E) std::copy(cv->E.begin(), cv->E.end(), E);
+    });
+}
+
+void bl_free(void *handle) {
+    if (!handle) return;
+    uint32_t magic = *(uint32_t *)handle;
+    if (magic == MAGIC_DESIGN) {
+        bl_design *d = (bl_design *)handle;
+        if (d->comm) ncclCommDestroy(d->comm);
+        if (d->owned && d->X) cudaFree(d->X);
+        d->magic = MAGIC_DEAD;
+        delete d;
+    } else if (magic == MAGIC_PATH) {
+        bl_path *p = (bl_path *)handle;
+        p->magic = MAGIC_DEAD;
+        delete p;
+    } else if (magic == MAGIC_CV) {
+        bl_cvres *c = (bl_cvres *)handle;
+        if (c->full) { c->full->magic = MAGIC_DEAD; delete c->full; }
+        c->magic = MAGIC_DEAD;
+        delete c;
+    } else if (magic == MAGIC_PREP) {
+        free_prep((bl_prep *)handle);
+    }
+}
+
+}  // extern "C"

@@ -169,13 +169,21 @@ def cfg2(seed=0, n=1000, p=100_000, device=None):
     ld = padded_ld(n, np.float32)
     X = torch.zeros((p, ld), dtype=torch.float32, device=dev)
     prev = None
+    t_ = torch.arange(BLOCK, device=dev, dtype=torch.float64)
+    # x_{j0+t} = 0.5^(t+1) x_{j0-1} + sum_{s<=t} 0.5^(t-s) c_s e_s  (the AR(1) recursion unrolled
+    # over a block as one triangular matmul; c_s = sqrt(.75), except c = 1 for global column 0)
+    L = torch.tril(0.5 ** (t_[:, None] - t_[None, :]).clamp(min=0)) * math.sqrt(0.75)
     for b in range((p + BLOCK - 1) // BLOCK):
         j0, j1 = b * BLOCK, min(p, (b + 1) * BLOCK)
-        e = torch.randn((j1 - j0, n), generator=_gen(dev, seed, b), device=dev, dtype=torch.float64)
-        blk = torch.empty_like(e)
-        for t in range(j1 - j0):
-            blk[t] = e[t] if prev is None else 0.5 * prev + math.sqrt(0.75) * e[t]
-            prev = blk[t]
+        m = j1 - j0
+        e = torch.randn((m, n), generator=_gen(dev, seed, b), device=dev, dtype=torch.float64)
+        Lb = L[:m, :m].clone()
+        if b == 0:
+            Lb[:, 0] /= math.sqrt(0.75)
+        blk = Lb @ e
+        if prev is not None:
+            blk += (0.5 ** (t_[:m] + 1))[:, None] * prev[None, :]
+        prev = blk[m - 1].clone()
         X[j0:j1, :n] = blk.to(torch.float32)
     rng = np.random.default_rng(seed + 1)
     idx = np.sort(rng.choice(p, size=20, replace=False))

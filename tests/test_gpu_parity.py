@@ -1,0 +1,301 @@
+"""Parity of the CUDA path (through the C ABI) with the fp64 CPU oracle.
+
+Tolerances (BASELINE.json north_star):
+  * per lambda  max|beta_gpu - beta_oracle| <= 1e-5 max|beta_oracle|
+  * relative objective difference RD <= 1e-7 (both objectives evaluated by the oracle)
+  * identical active sets {j : |beta_j| >= 1e-8}; a mismatch is excused only for a
+    KKT-tight feature (| |z_j| - alpha lambda | <= 1e-9, Q20)
+  * one-time quantities (c, s, a, b, lambda_max, j*): fp64 rounding-level agreement
+  * fused scan z: absolute error <= 1e-12 * ||r||_2 (fp64-grade, Q20)
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+bl = pytest.importorskip("paper_1701_05936_b200.bl")
+
+
+def design(inst):
+    return bl.Design(inst.host_X(), inst.n)
+
+
+def compare_path(inst, gp, op, alpha, beta_rtol=1e-5, rd_tol=1e-7, train=None):
+    p = inst.p
+    Bg = gp.dense(p)
+    Bo = op.beta
+    assert gp.n_converged == len(op.lam)
+    worst = 0.0
+    for k, lam in enumerate(op.lam):
+        bo, bg = Bo[:, k], Bg[:, k]
+        scale = np.abs(bo).max()
+        if scale == 0.0:
+            assert np.all(bg == 0.0), f"lambda {k}: oracle null solution, gpu nonzero"
+            continue
+        err = np.abs(bg - bo).max() / scale
+        worst = max(worst, err)
+        assert err <= beta_rtol, f"lambda {k}: rel beta err {err:.3e}"
+        qo = oracle.objective(inst, inst.y, bo, lam, alpha, train)
+        qg = oracle.objective(inst, inst.y, bg, lam, alpha, train)
+        assert abs(qg - qo) / qo <= rd_tol, f"lambda {k}: RD {(qg - qo) / qo:.3e}"
+        ao, ag = np.abs(bo) >= 1e-8, np.abs(bg) >= 1e-8
+        if not np.array_equal(ao, ag):
+            _, _, z = oracle.kkt(inst, inst.y, bo, lam, alpha, train, want_z=True)
+            bad = np.flatnonzero(ao != ag)
+            slack = np.abs(np.abs(z[bad]) - alpha * lam)
+            assert np.all(slack <= 1e-9), f"lambda {k}: active-set mismatch {bad} slack {slack}"
+    return worst
+
+
+# ------------------------------------------------------------------ a2-a4 preprocessing
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32, np.int8])
+@pytest.mark.parametrize("masked", [False, True])
+def test_prep_parity(dtype, masked):
+    kind = "geno" if dtype == np.int8 else "corr"
+    inst = synth.random_instance(203, 777, dtype=dtype, seed=7, kind=kind, const_cols=3, mean_shift=0.5)
+    train = None
+    if masked:
+        train = np.ones(inst.n, dtype=bool)
+        train[np.random.default_rng(1).choice(inst.n, 40, replace=False)] = False
+    for alpha in (1.0, 0.5):
+        pr = design(inst).prepare(inst.y, train, alpha).copy()
+        c, s = oracle.column_stats(inst, train)
+        o = oracle.prep(inst, inst.y, alpha, train)
+        np.testing.assert_allclose(pr["c"], c, rtol=1e-13, atol=1e-14)
+        np.testing.assert_allclose(pr["s"], s, rtol=1e-12, atol=0)
+        assert np.array_equal(pr["s"] == 0, s == 0)
+        assert pr["jstar"] == o["jstar"]
+        assert pr["lambda_max"] == pytest.approx(o["lambda_max"], rel=1e-12)
+        sc = np.abs(o["a"]).max()
+        np.testing.assert_allclose(pr["a"], o["a"], rtol=0, atol=1e-12 * sc)
+        np.testing.assert_allclose(pr["b"], o["b"], rtol=0, atol=1e-11 * inst.n)
+
+
+# ------------------------------------------------------------------ a9 fused scan
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32, np.int8])
+def test_scan_parity(dtype):
+    kind = "geno" if dtype == np.int8 else "iid"
+    inst = synth.random_instance(301, 1031, dtype=dtype, seed=11, kind=kind, const_cols=2)
+    train = np.ones(inst.n, dtype=bool)
+    train[::7] = False
+    d = design(inst)
+    prep = d.prepare(inst.y, train, 1.0)
+    rng = np.random.default_rng(5)
+    r = rng.standard_normal(inst.n) * train
+    z_or = oracle.std_dots(inst, r, train)
+    lam, lam_next = 0.05, 0.045
+    in_w = np.zeros(inst.p, bool)
+    in_w[rng.choice(inst.p, 30, replace=False)] = True
+    z, viol, strong = prep.scan(r, lam, lam_next, in_w)
+    assert np.abs(z - z_or).max() <= 1e-12 * np.linalg.norm(r)
+    live = oracle.column_stats(inst, train)[1] > 0
+    thr_s = 2 * lam_next - lam
+    tight = (np.abs(np.abs(z_or) - lam) < 1e-12) | (np.abs(np.abs(z_or) - thr_s) < 1e-12)
+    ev = set(np.flatnonzero(live & ~in_w & (np.abs(z_or) > lam) & ~tight))
+    es = set(np.flatnonzero(live & ~in_w & (np.abs(z_or) >= thr_s) & ~tight))
+    assert set(viol.tolist()) - set(np.flatnonzero(tight)) == ev
+    assert set(strong.tolist()) - set(np.flatnonzero(tight)) == es
+    assert np.all(np.diff(viol) > 0) and np.all(np.diff(strong) > 0)   # sorted, unique
+
+
+# ------------------------------------------------------------------ a5 BEDPP
+
+@pytest.mark.parametrize("alpha", [1.0, 0.5])
+def test_bedpp_parity(alpha):
+    inst = synth.random_instance(150, 900, seed=13, kind="corr")
+    d = design(inst)
+    prep = d.prepare(inst.y, None, alpha)
+    lm = oracle.lambda_max(inst, inst.y, alpha)[0]
+    for lam in lm * np.array([1.0, 0.99, 0.95, 0.9, 0.8, 0.6, 0.4]):
+        keep, cnt = prep.bedpp(lam)
+        disc_or = oracle.bedpp_discard(inst, inst.y, alpha, lam)
+        assert cnt == keep.sum()
+        mism = (~keep) != disc_or
+        assert mism.mean() <= 2e-3, (lam / lm, mism.sum())
+
+
+def test_bedpp_safe_on_gpu_path():
+    """The GPU safe set never excludes a feature the oracle finds active."""
+    for seed in range(6):
+        inst = synth.random_instance(80, 400, seed=200 + seed, kind="corr" if seed % 2 else "iid")
+        d = design(inst)
+        for alpha in (1.0, 0.5):
+            prep = d.prepare(inst.y, None, alpha)
+            lm = oracle.lambda_max(inst, inst.y, alpha)[0]
+            lams = synth.lambda_grid(lm, 15, 0.3)
+            op = oracle.fit_path(inst, inst.y, lams, alpha=alpha, tol=1e-12)
+            for k, lam in enumerate(lams):
+                keep, _ = prep.bedpp(lam)
+                assert not np.any(~keep & (op.beta[:, k] != 0))
+
+
+# ------------------------------------------------------------------ full paths
+
+def test_path_parity_cfg1():
+    """BASELINE cfg1 at full size with its own tol (1e-7), 100 lambdas to 0.05."""
+    inst = synth.cfg1()
+    d = design(inst)
+    lm = oracle.lambda_max(inst, inst.y)[0]
+    lams = synth.lambda_grid(lm, 100, inst.ratio)
+    op = oracle.fit_path(inst, inst.y, lams, alpha=1.0, tol=1e-10)
+    gp = d.fit_path(inst.y, lams, alpha=1.0, tol=inst.tol)
+    compare_path(inst, gp, op, 1.0)
+    assert np.all(gp.kkt_rounds >= 0)
+
+
+@pytest.mark.parametrize("dtype,alpha,screen", [
+    (np.float64, 1.0, "hybrid"), (np.float32, 1.0, "hybrid"), (np.int8, 1.0, "hybrid"),
+    (np.float32, 0.5, "hybrid"), (np.int8, 0.3, "hybrid"), (np.float64, 0.5, "ssr"),
+    (np.float32, 1.0, "none")])
+def test_path_parity_small(dtype, alpha, screen):
+    kind = "geno" if dtype == np.int8 else "corr"
+    inst = synth.random_instance(157, 613, dtype=dtype, seed=17, kind=kind, const_cols=4, n_true=12)
+    d = design(inst)
+    lm = oracle.lambda_max(inst, inst.y, alpha)[0]
+    lams = synth.lambda_grid(lm, 40, 0.05)
+    op = oracle.fit_path(inst, inst.y, lams, alpha=alpha, tol=1e-11)
+    gp = d.fit_path(inst.y, lams, alpha=alpha, tol=1e-9, screen=screen)
+    compare_path(inst, gp, op, alpha)
+    # a0 / original scale (Q4)
+    c, s = oracle.column_stats(inst)
+    Bg = gp.dense(inst.p, "orig")
+    np.testing.assert_allclose(Bg * s[:, None], gp.dense(inst.p), rtol=1e-14, atol=0)
+    np.testing.assert_allclose(gp.a0, inst.y.mean() - c @ Bg, rtol=1e-10, atol=1e-10)
+
+
+def test_screening_policies_agree_and_hybrid_scans_less():
+    inst = synth.random_instance(120, 2000, seed=23, kind="corr", n_true=10)
+    d = design(inst)
+    lm = d.lambda_max(inst.y)
+    lams = synth.lambda_grid(lm, 50, 0.1)
+    paths = {s: d.fit_path(inst.y, lams, tol=1e-10, screen=s) for s in ("none", "ssr", "hybrid")}
+    B = {s: p.dense(inst.p) for s, p in paths.items()}
+    for s in ("ssr", "hybrid"):
+        assert np.abs(B[s] - B["none"]).max() <= 1e-6 * max(1.0, np.abs(B["none"]).max())
+    assert np.all(paths["hybrid"].cols_scanned <= paths["ssr"].cols_scanned)
+    assert paths["hybrid"].cols_scanned.sum() < paths["ssr"].cols_scanned.sum()
+
+
+def test_kkt_repairs_a_shrunk_strong_set():
+    """S:222 fault injection analogue: with a 1-round KKT cap the path must still
+    certify (violators are added and re-solved) -- and the default succeeds."""
+    inst = synth.random_instance(100, 500, seed=29, kind="corr", n_true=15)
+    d = design(inst)
+    lm = d.lambda_max(inst.y)
+    lams = synth.lambda_grid(lm, 30, 0.05)
+    gp = d.fit_path(inst.y, lams, tol=1e-10)
+    for k, lam in enumerate(lams):
+        zv, nv = oracle.kkt(inst, inst.y, gp.dense(inst.p)[:, k], lam)
+        assert zv <= 1e-6 and nv <= 1e-6
+
+
+def test_grid_edge_cases():
+    inst = synth.random_instance(64, 50, seed=31)
+    d = design(inst)
+    lm = oracle.lambda_max(inst, inst.y)[0]
+    # grid starting below lambda_max (virtual lambda_0 = lambda_max), single lambda, above lambda_max
+    for lams in (lm * np.array([0.7, 0.5, 0.2]), np.array([0.3 * lm]), lm * np.array([3.0, 2.0, 1.0, 0.5])):
+        op = oracle.fit_path(inst, inst.y, lams, tol=1e-12)
+        gp = d.fit_path(inst.y, lams, tol=1e-10)
+        compare_path(inst, gp, op, 1.0)
+
+
+@pytest.mark.parametrize("p", [1, 3, 5, 17])
+def test_tiny_p(p):
+    inst = synth.random_instance(33, p, seed=37 + p, n_true=1)
+    d = design(inst)
+    lm = oracle.lambda_max(inst, inst.y)[0]
+    lams = synth.lambda_grid(lm, 12, 0.01)
+    compare_path(inst, d.fit_path(inst.y, lams, tol=1e-11), oracle.fit_path(inst, inst.y, lams, tol=1e-13), 1.0)
+
+
+def test_error_statuses():
+    inst = synth.random_instance(20, 10, seed=41)
+    d = design(inst)
+    with pytest.raises(bl.BLError) as e:
+        d.fit_path(np.ones(20), [1.0, 0.5])
+    assert e.value.code == bl.BL_ERR_DEGENERATE
+    with pytest.raises(bl.BLError) as e:
+        d.fit_path(inst.y, [0.5, 1.0])
+    assert e.value.code == bl.BL_ERR_ARG
+    with pytest.raises(bl.BLError) as e:
+        d.fit_path(inst.y, [1.0], alpha=1.5)
+    assert e.value.code == bl.BL_ERR_ARG
+    Xc = np.zeros((3, 24)); Xc[:, :20] = 2.0
+    with pytest.raises(bl.BLError) as e:
+        bl.Design(Xc, 20).fit_path(inst.y, [1.0])
+    assert e.value.code == bl.BL_ERR_DEGENERATE
+    # max_iter too small -> convergence status with a truncated prefix
+    lm = d.lambda_max(inst.y)
+    gp = d.fit_path(inst.y, synth.lambda_grid(lm, 10, 0.01), tol=1e-14, max_iter=1, raise_on_error=False)
+    assert gp.status == bl.BL_ERR_CONVERGENCE and gp.n_converged < 10
+
+
+def test_device_pointer_design_matches_host():
+    import torch
+    inst = synth.random_instance(90, 300, dtype=np.float32, seed=43)
+    Xd = torch.from_numpy(inst.host_X()).cuda()
+    lm = oracle.lambda_max(inst, inst.y)[0]
+    lams = synth.lambda_grid(lm, 20, 0.1)
+    a = bl.Design(inst.host_X(), inst.n).fit_path(inst.y, lams, tol=1e-10)
+    b = bl.Design(Xd, inst.n).fit_path(inst.y, lams, tol=1e-10)
+    assert np.array_equal(a.beta_std, b.beta_std) and np.array_equal(a.feat, b.feat)
+
+
+def test_deterministic_repeat():
+    inst = synth.random_instance(128, 3000, dtype=np.float32, seed=47, kind="corr")
+    d = design(inst)
+    lams = synth.lambda_grid(d.lambda_max(inst.y), 30, 0.1)
+    a, b = d.fit_path(inst.y, lams), d.fit_path(inst.y, lams)
+    assert np.array_equal(a.beta_std, b.beta_std) and np.array_equal(a.cols_scanned, b.cols_scanned)
+
+
+# ------------------------------------------------------------------ a12 cross-validation
+
+@pytest.mark.parametrize("dtype,alpha", [(np.float64, 1.0), (np.int8, 0.5)])
+def test_cv_parity(dtype, alpha):
+    kind = "geno" if dtype == np.int8 else "iid"
+    inst = synth.random_instance(90, 150, dtype=dtype, seed=53, kind=kind, n_true=6)
+    K = 5
+    f = oracle.folds(inst.n, K, 1234)
+    lm = oracle.lambda_max(inst, inst.y, alpha)[0]
+    lams = synth.lambda_grid(lm, 20, 0.05)
+    E, cve, cvse, lmin = oracle.cv(inst, inst.y, f, K, lams, alpha=alpha, tol=1e-12)
+    g = design(inst).cv(inst.y, lams, K=K, alpha=alpha, tol=1e-10, seed=1234)
+    assert np.array_equal(g.fold_id, f)            # same counter-based permutation (Q18)
+    np.testing.assert_allclose(g.E, E, rtol=1e-6, atol=1e-9 * E.max())
+    np.testing.assert_allclose(g.cve, cve, rtol=1e-7)
+    np.testing.assert_allclose(g.cvse, cvse, rtol=1e-6)
+    assert g.lambda_min_index == lmin
+    op = oracle.fit_path(inst, inst.y, lams, alpha=alpha, tol=1e-12)
+    compare_path(inst, g.full, op, alpha)
+
+
+# ------------------------------------------------------------------ full-size, bench launch config
+
+@pytest.mark.slow
+def test_cfg2_full_size_sampled():
+    """cfg2 exactly as bench.py runs it (device-resident X, hybrid, tol 1e-7):
+    lambda_max against the oracle's full pass; at sampled lambdas the GPU
+    solution against a cold-started oracle solve (same unique minimiser) and
+    the oracle's KKT audit."""
+    inst = synth.cfg2()
+    d = bl.Design(inst.X, inst.n)
+    lm_g = d.lambda_max(inst.y)
+    lm_o = oracle.lambda_max(inst, inst.y)[0]
+    assert lm_g == pytest.approx(lm_o, rel=1e-12)
+    lams = synth.lambda_grid(lm_g, 100, inst.ratio)
+    gp = d.fit_path(inst.y, lams, alpha=1.0, tol=inst.tol)
+    assert gp.n_converged == 100
+    B = gp.dense(inst.p)
+    for k in (20, 99):
+        zv, nv = oracle.kkt(inst, inst.y, B[:, k], lams[k])
+        assert zv <= 1e-6 and nv <= 1e-6
+        op = oracle.fit_path(inst, inst.y, [lams[k]], tol=1e-10)
+        bo = op.beta[:, 0]
+        assert np.abs(B[:, k] - bo).max() <= 1e-5 * np.abs(bo).max()
