@@ -56,7 +56,10 @@ static int64_t count_rows(const uint8_t *train, int64_t n)
 
 /* "saves only the means and standard deviations of the columns of X as
  * two vectors c and s".  Two-pass, population SD (Q1).  s_j == 0 marks a
- * zero-variance column, excluded everywhere (Q13). */
+ * zero-variance column, excluded everywhere (Q13): a column whose used values
+ * are all equal has variance exactly 0 by definition, so it gets c_j = that
+ * value and s_j = 0 exactly (two-pass arithmetic alone would leave a rounding
+ * residue ~1e-16 |c_j| there). */
 int or_column_stats(const void *X, int dt, int64_t n, int64_t p, int64_t ld,
                     const uint8_t *train, double *c, double *s)
 {
@@ -68,6 +71,16 @@ int or_column_stats(const void *X, int dt, int64_t n, int64_t p, int64_t ld,
         for (int64_t i = 0; i < n; i++)
             if (in_rows(train, i)) sum += xraw(X, dt, ld, i, j);
         double mean = sum / (double)nt;
+        int constant = 1;
+        double first = 0.0;
+        int seen = 0;
+        for (int64_t i = 0; i < n && constant; i++)
+            if (in_rows(train, i)) {
+                double v = xraw(X, dt, ld, i, j);
+                if (!seen) { first = v; seen = 1; }
+                else if (v != first) constant = 0;
+            }
+        if (constant) { c[j] = first; s[j] = 0.0; continue; }
         double ss = 0.0;
         for (int64_t i = 0; i < n; i++)
             if (in_rows(train, i)) {

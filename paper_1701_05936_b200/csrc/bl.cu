@@ -46,8 +46,10 @@ struct Err {
 #define CK(call)                                                                                  \
     do {                                                                                          \
         cudaError_t e_ = (call);                                                                  \
-        if (e_ != cudaSuccess) raise(BL_ERR_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), \
-                                     __FILE__, __LINE__);                                         \
+        if (e_ != cudaSuccess) {                                                                  \
+            cudaGetLastError(); /* do not leak a recoverable error into later checks */          \
+            raise(BL_ERR_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+        }                                                                                         \
     } while (0)
 #define CKL()                                                                                     \
     do {                                                                                          \
@@ -160,6 +162,7 @@ void check_device() {
 
 template <typename F>
 bl_status guard(F &&f) {
+    cudaGetLastError();   // a stale error from an earlier call must not be reported here
     try {
         f();
         return BL_OK;
@@ -207,8 +210,23 @@ int grid_for(const void *kern, int threads, size_t smem, int nsm) {
     return occ * nsm;
 }
 
-void set_smem(const void *kern, size_t smem) {
-    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+// Opt a kernel into the largest dynamic shared memory the device allows
+// (opt-in limit minus the kernel's static shared memory); returns that limit.
+size_t allow_dyn_smem(const void *kern) {
+    static std::mutex mu;
+    static std::vector<std::pair<const void *, size_t>> done;
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto &pr : done)
+        if (pr.first == kern) return pr.second;
+    int dev = 0, optin = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes fa;
+    CK(cudaFuncGetAttributes(&fa, kern));
+    size_t lim = (size_t)optin - fa.sharedSizeBytes;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lim));
+    done.push_back({kern, lim});
+    return lim;
 }
 
 // ------------------------------------------------------------ scan launcher
@@ -232,8 +250,7 @@ void launch_scan(bl_prep *pp, ScanArgs a, const double *v_dev, bool timed) {
         a.limb_scale = pp->limb_scale;
         a.K1 = pp->limb_sum;      // sum of the quantised vector: identity holds exactly for it
         size_t smem = (size_t)8 * pp->limb_ld;
-        static std::once_flag once;
-        std::call_once(once, [&] { set_smem((const void *)k_scan_i8, 200 * 1024); });
+        allow_dyn_smem((const void *)k_scan_i8);
         int grid = grid_for((const void *)k_scan_i8, kScanThreads, smem, d->nsm);
         EvPair ev(pp, timed ? &pp->ev_scan : &pp->ev_prep);
         k_scan_i8<<<grid, kScanThreads, smem, pp->stream>>>(a);
@@ -243,15 +260,13 @@ void launch_scan(bl_prep *pp, ScanArgs a, const double *v_dev, bool timed) {
         int V = 16 / itemsize(d->dt);
         size_t smem = (size_t)8 * round_up(d->n, 32 * V);
         if (d->dt == DT_F32) {
-            static std::once_flag once;
-            std::call_once(once, [&] { set_smem((const void *)k_scan_fp<float, 4>, 200 * 1024); });
+            allow_dyn_smem((const void *)k_scan_fp<float, 4>);
             int grid = grid_for((const void *)k_scan_fp<float, 4>, kScanThreads, smem, d->nsm);
             EvPair ev(pp, timed ? &pp->ev_scan : &pp->ev_prep);
             k_scan_fp<float, 4><<<grid, kScanThreads, smem, pp->stream>>>(a);
             CKL();
         } else {
-            static std::once_flag once;
-            std::call_once(once, [&] { set_smem((const void *)k_scan_fp<double, 4>, 200 * 1024); });
+            allow_dyn_smem((const void *)k_scan_fp<double, 4>);
             int grid = grid_for((const void *)k_scan_fp<double, 4>, kScanThreads, smem, d->nsm);
             EvPair ev(pp, timed ? &pp->ev_scan : &pp->ev_prep);
             k_scan_fp<double, 4><<<grid, kScanThreads, smem, pp->stream>>>(a);
@@ -514,11 +529,11 @@ void launch_cd(bl_prep *pp, int nW, double lam, double alpha, double tol, int ma
     int T = cd_threads(d->n);
     int R = (int)((d->n + T - 1) / T);
     size_t smem = (size_t)8 * R * T + (size_t)12 * nW + 16;
-    if (smem > 227 * 1024)
+    const void *kern = cd_kernel(d->dt, pp->has_mask != 0, R);
+    size_t lim = allow_dyn_smem(kern);
+    if (smem > lim)
         raise(BL_ERR_OOM, "working set of %d columns does not fit the CD kernel's shared memory (n=%lld)", nW,
               (long long)d->n);
-    const void *kern = cd_kernel(d->dt, pp->has_mask != 0, R);
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     EvPair ev(pp, &pp->ev_cd);
     void *args[] = {&ca};
     CK(cudaLaunchKernel(kern, dim3(1), dim3(T), args, smem, pp->stream));
