@@ -72,6 +72,8 @@ int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 struct bl_design {
     uint32_t magic;
+    std::mutex pool_mu;
+    std::vector<bl_prep *> pool;     // idle fit workspaces, reused by later fits
     void *X;          // device
     bool owned;
     int dt;
@@ -134,9 +136,12 @@ struct bl_prep {
     // host mirrors
     PrepScalars hps;
     RoundStatus *hst;       // pinned
-    int *hlist;             // pinned, p entries
-    int *hup;               // pinned upload staging, Wcap + p entries
-    double *hbw;            // pinned, 3*Wcap entries (beta, c, s of W)
+    int *hlist;             // pinned read-back buffer (grows)
+    int *hup;               // pinned upload staging (grows)
+    double *hbw;            // pinned, 3*|W| entries (beta, c, s of W) (grows)
+    size_t hlist_cap, hup_cap, hbw_cap;
+    char *warena;           // device W buffers: W (int32) + betaW out (3 x fp64), grows
+    cudaStream_t own;       // library stream (used when the caller passes none)
     // profiling
     int profile;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_scan, ev_cd, ev_prep;
@@ -310,7 +315,8 @@ void free_prep(bl_prep *pp) {
     if (pp->hlist) cudaFreeHost(pp->hlist);
     if (pp->hbw) cudaFreeHost(pp->hbw);
     if (pp->hup) cudaFreeHost(pp->hup);
-    if (pp->own_stream && pp->stream) cudaStreamDestroy(pp->stream);
+    if (pp->warena) cudaFree(pp->warena);
+    if (pp->own) cudaStreamDestroy(pp->own);
     pp->magic = MAGIC_DEAD;
     delete pp;
 }
@@ -320,12 +326,63 @@ struct PrepGuard {
     ~PrepGuard() { free_prep(pp); }
 };
 
+// Return a fit workspace to its design's pool (or free it).
+void release_prep(bl_prep *pp) {
+    if (!pp) return;
+    if (pp->stream) cudaStreamSynchronize(pp->stream);
+    sum_events(pp->ev_scan);
+    sum_events(pp->ev_cd);
+    sum_events(pp->ev_prep);
+    pp->stream = pp->own;          // never keep a caller's stream beyond the call
+    std::lock_guard<std::mutex> lk(pp->d->pool_mu);
+    if (pp->d->pool.size() < 4) pp->d->pool.push_back(pp);
+    else free_prep(pp);
+}
+
+struct PoolGuard {
+    bl_prep *pp;
+    ~PoolGuard() { release_prep(pp); }
+};
+
+template <typename Tp>
+void ensure_host(Tp *&ptr, size_t &cap, size_t need) {
+    if (need <= cap) return;
+    size_t nc = std::max<size_t>(need, 2 * cap);
+    nc = std::max<size_t>(nc, 1024);
+    if (ptr) CK(cudaFreeHost(ptr));
+    ptr = nullptr;
+    CK(cudaMallocHost((void **)&ptr, nc * sizeof(Tp)));
+    cap = nc;
+}
+
+// Device W buffers grow geometrically (contents are re-uploaded / rewritten each round).
+void ensure_W(bl_prep *pp, int64_t need) {
+    if (need <= pp->Wcap && pp->warena) return;
+    int64_t nc = std::max<int64_t>(std::max<int64_t>(need, 2 * pp->Wcap), 1024);
+    nc = std::min<int64_t>(std::max<int64_t>(nc, need), std::max<int64_t>(pp->p, 1));
+    CK(cudaStreamSynchronize(pp->stream));
+    if (pp->warena) CK(cudaFree(pp->warena));
+    pp->warena = nullptr;
+    size_t bytes = (size_t)round_up(4 * nc, 256) + (size_t)24 * nc;
+    cudaError_t e = cudaMalloc(&pp->warena, bytes);
+    if (e != cudaSuccess) { cudaGetLastError(); raise(BL_ERR_OOM, "cudaMalloc(%zu) for W: %s", bytes, cudaGetErrorString(e)); }
+    pp->W = (int *)pp->warena;
+    pp->betaW = (double *)(pp->warena + round_up(4 * nc, 256));
+    pp->Wcap = nc;
+}
+
 // One-time preprocessing for (y, optional training mask).
 bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double alpha, const bl_opts *opts) {
     if (!y) raise(BL_ERR_ARG, "y is NULL");
     if (!(alpha > 0.0 && alpha <= 1.0)) raise(BL_ERR_ARG, "alpha must be in (0, 1], got %g", alpha);
     CK(cudaSetDevice(d->device));
-    bl_prep *pp = new bl_prep();
+    bl_prep *pp = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(d->pool_mu);
+        if (!d->pool.empty()) { pp = d->pool.back(); d->pool.pop_back(); }
+    }
+    bool reused = pp != nullptr;
+    if (!pp) pp = new bl_prep();
     PrepGuard guard{pp};
     pp->magic = MAGIC_PREP;
     pp->d = d;
@@ -333,13 +390,10 @@ bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double a
     pp->p = d->p;
     pp->ld = d->ld;
     pp->profile = opts ? opts->profile : 0;
-    if (opts && opts->stream) {
-        pp->stream = (cudaStream_t)opts->stream;
-        pp->own_stream = false;
-    } else {
-        CK(cudaStreamCreateWithFlags(&pp->stream, cudaStreamNonBlocking));
-        pp->own_stream = true;
-    }
+    pp->launches = 0;
+    if (!pp->own) CK(cudaStreamCreateWithFlags(&pp->own, cudaStreamNonBlocking));
+    pp->stream = (opts && opts->stream) ? (cudaStream_t)opts->stream : pp->own;
+    pp->own_stream = false;
     const int64_t n = d->n, p = d->p;
     int64_t nt = n, i0 = 0;
     if (train) {
@@ -353,35 +407,34 @@ bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double a
     pp->has_mask = train != nullptr;
     pp->vlen = round_up(std::max<int64_t>(d->ld, 1024), 128);
     pp->limb_ld = (int)(round_up(d->ld, 128) + 64);
-    pp->Wcap = std::min<int64_t>(p, 1 << 20);
     pp->amax_blocks = d->nsm * 4;
-    // arena layout
-    size_t off = 0;
-    auto take = [&](size_t bytes) { size_t o = off; off = round_up(off + bytes, 256); return o; };
-    size_t o_c = take(8 * p), o_s = take(8 * p), o_a = take(8 * p), o_b = take(8 * p), o_z = take(8 * p),
-           o_beta = take(8 * p), o_flags = take(p), o_wflag = take(p), o_mask = take(pp->vlen),
-           o_scope = take(4 * p), o_viol = take(4 * p), o_strong = take(4 * p), o_W = take(4 * pp->Wcap),
-           o_bw = take(24 * pp->Wcap), o_yt = take(8 * pp->vlen), o_rf = take(8 * pp->vlen),
-           o_rs = take(8 * pp->vlen), o_vt = take(8 * pp->vlen), o_limbs = take((size_t)8 * pp->limb_ld),
-           o_lsc = take(32), o_ps = take(sizeof(PrepScalars)), o_st = take(sizeof(RoundStatus)),
-           o_av = take(8 * pp->amax_blocks), o_ai = take(8 * pp->amax_blocks), o_nl = take(16);
-    pp->arena_bytes = off;
-    cudaError_t e = cudaMalloc(&pp->arena, off);
-    if (e != cudaSuccess) raise(BL_ERR_OOM, "cudaMalloc(%zu) failed: %s", off, cudaGetErrorString(e));
-    char *A = pp->arena;
-    pp->c = (double *)(A + o_c); pp->s = (double *)(A + o_s); pp->a = (double *)(A + o_a);
-    pp->b = (double *)(A + o_b); pp->z = (double *)(A + o_z); pp->beta = (double *)(A + o_beta);
-    pp->flags = (uint8_t *)(A + o_flags); pp->wflag = (uint8_t *)(A + o_wflag); pp->mask = (uint8_t *)(A + o_mask);
-    pp->scope = (int *)(A + o_scope); pp->viol = (int *)(A + o_viol); pp->strong = (int *)(A + o_strong);
-    pp->W = (int *)(A + o_W); pp->betaW = (double *)(A + o_bw); pp->yt = (double *)(A + o_yt);
-    pp->rfull = (double *)(A + o_rf); pp->rscan = (double *)(A + o_rs); pp->vtmp = (double *)(A + o_vt);
-    pp->limbs = (int8_t *)(A + o_limbs); pp->limb_scale = (double *)(A + o_lsc); pp->limb_sum = pp->limb_scale + 1;
-    pp->ps = (PrepScalars *)(A + o_ps); pp->st = (RoundStatus *)(A + o_st);
-    pp->amax_v = (double *)(A + o_av); pp->amax_i = (long long *)(A + o_ai); pp->nlive = (int *)(A + o_nl);
-    CK(cudaMallocHost(&pp->hst, sizeof(RoundStatus)));
-    CK(cudaMallocHost(&pp->hlist, sizeof(int) * std::max<int64_t>(p, 1)));
-    CK(cudaMallocHost(&pp->hbw, 24 * pp->Wcap));
-    CK(cudaMallocHost(&pp->hup, 4 * (pp->Wcap + p)));
+    if (!reused) {
+        // arena layout (sizes depend only on the design)
+        size_t off = 0;
+        auto take = [&](size_t bytes) { size_t o = off; off = round_up(off + bytes, 256); return o; };
+        size_t o_c = take(8 * p), o_s = take(8 * p), o_a = take(8 * p), o_b = take(8 * p), o_z = take(8 * p),
+               o_beta = take(8 * p), o_flags = take(p), o_wflag = take(p), o_mask = take(pp->vlen),
+               o_scope = take(4 * p), o_viol = take(4 * p), o_strong = take(4 * p), o_yt = take(8 * pp->vlen),
+               o_rf = take(8 * pp->vlen), o_rs = take(8 * pp->vlen), o_vt = take(8 * pp->vlen),
+               o_limbs = take((size_t)8 * pp->limb_ld), o_lsc = take(32), o_ps = take(sizeof(PrepScalars)),
+               o_st = take(sizeof(RoundStatus)), o_av = take(8 * pp->amax_blocks), o_ai = take(8 * pp->amax_blocks),
+               o_nl = take(16);
+        pp->arena_bytes = off;
+        cudaError_t e = cudaMalloc(&pp->arena, off);
+        if (e != cudaSuccess) { cudaGetLastError(); raise(BL_ERR_OOM, "cudaMalloc(%zu) failed: %s", off, cudaGetErrorString(e)); }
+        char *A = pp->arena;
+        pp->c = (double *)(A + o_c); pp->s = (double *)(A + o_s); pp->a = (double *)(A + o_a);
+        pp->b = (double *)(A + o_b); pp->z = (double *)(A + o_z); pp->beta = (double *)(A + o_beta);
+        pp->flags = (uint8_t *)(A + o_flags); pp->wflag = (uint8_t *)(A + o_wflag); pp->mask = (uint8_t *)(A + o_mask);
+        pp->scope = (int *)(A + o_scope); pp->viol = (int *)(A + o_viol); pp->strong = (int *)(A + o_strong);
+        pp->yt = (double *)(A + o_yt);
+        pp->rfull = (double *)(A + o_rf); pp->rscan = (double *)(A + o_rs); pp->vtmp = (double *)(A + o_vt);
+        pp->limbs = (int8_t *)(A + o_limbs); pp->limb_scale = (double *)(A + o_lsc); pp->limb_sum = pp->limb_scale + 1;
+        pp->ps = (PrepScalars *)(A + o_ps); pp->st = (RoundStatus *)(A + o_st);
+        pp->amax_v = (double *)(A + o_av); pp->amax_i = (long long *)(A + o_ai); pp->nlive = (int *)(A + o_nl);
+        pp->Wcap = 0;
+        ensure_W(pp, std::min<int64_t>(p, 4096));
+    }
     cudaStream_t st = pp->stream;
     CK(cudaMemsetAsync(pp->beta, 0, 8 * p, st));
     CK(cudaMemsetAsync(pp->wflag, 0, p, st));
@@ -458,7 +511,8 @@ void sorted_merge_into(std::vector<int> &W, std::vector<int> add) {
 }
 
 void upload_W(bl_prep *pp, const std::vector<int> &W, const std::vector<int> &added) {
-    if ((int64_t)W.size() > pp->Wcap) raise(BL_ERR_OOM, "working set %zu exceeds capacity %lld", W.size(), (long long)pp->Wcap);
+    ensure_W(pp, (int64_t)W.size());
+    ensure_host(pp->hup, pp->hup_cap, W.size() + added.size());
     cudaStream_t st = pp->stream;
     // pinned staging: the previous round ended with a stream sync, so hup is free
     std::memcpy(pp->hup, W.data(), 4 * W.size());
@@ -475,6 +529,7 @@ void upload_W(bl_prep *pp, const std::vector<int> &W, const std::vector<int> &ad
 std::vector<int> read_list(bl_prep *pp, const int *dev, int count) {
     std::vector<int> v(count);
     if (count > 0) {
+        ensure_host(pp->hlist, pp->hlist_cap, (size_t)count);
         CK(cudaMemcpyAsync(pp->hlist, dev, 4 * (size_t)count, cudaMemcpyDeviceToHost, pp->stream));
         CK(cudaStreamSynchronize(pp->stream));
         std::memcpy(v.data(), pp->hlist, 4 * (size_t)count);
@@ -528,7 +583,7 @@ void launch_cd(bl_prep *pp, int nW, double lam, double alpha, double tol, int ma
     ca.st = pp->st;
     int T = cd_threads(d->n);
     int R = (int)((d->n + T - 1) / T);
-    size_t smem = (size_t)8 * R * T + (size_t)12 * nW + 16;
+    size_t smem = (size_t)kCdSlotBytes * nW + 16;
     const void *kern = cd_kernel(d->dt, pp->has_mask != 0, R);
     size_t lim = allow_dyn_smem(kern);
     if (smem > lim)
@@ -678,6 +733,7 @@ bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, doubl
         RoundStatus rs = *pp->hst;
         int nW = (int)W.size();
         if (nW > 0) {
+            ensure_host(pp->hbw, pp->hbw_cap, 3 * (size_t)nW);
             CK(cudaMemcpyAsync(pp->hbw, pp->betaW, 24 * (size_t)nW, cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
         }
@@ -741,7 +797,7 @@ bl_path *fit_impl(bl_design *d, const double *y, const uint8_t *train, const dou
     if (max_iter < 1) raise(BL_ERR_ARG, "max_iter must be >= 1");
     if (screen < 0 || screen > 2) raise(BL_ERR_ARG, "screen must be 0, 1 or 2");
     bl_prep *pp = make_prep(d, y, train, alpha, opts);
-    PrepGuard g{pp};
+    PoolGuard g{pp};
     bl_path *out = new bl_path();
     out->magic = MAGIC_PATH;
     int rounds = opts && opts->max_kkt_rounds > 0 ? opts->max_kkt_rounds : 10;
@@ -1110,6 +1166,8 @@ void bl_free(void *handle) {
     uint32_t magic = *(uint32_t *)handle;
     if (magic == MAGIC_DESIGN) {
         bl_design *d = (bl_design *)handle;
+        for (bl_prep *pp : d->pool) free_prep(pp);
+        d->pool.clear();
         if (d->comm) ncclCommDestroy(d->comm);
         if (d->owned && d->X) cudaFree(d->X);
         d->magic = MAGIC_DEAD;

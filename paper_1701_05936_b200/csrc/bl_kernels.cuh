@@ -640,12 +640,14 @@ __global__ void k_set_flags(const int *__restrict__ idx, int cnt, uint8_t *__res
 }
 
 // ------------------------------------------ a8: coordinate descent on W (G6)
-// ONE persistent CTA per fit: r (n fp64) lives in shared memory for the whole
-// solve; thread t owns rows t, t+T, ..., so residual updates need no
-// synchronisation and each coordinate costs exactly one __syncthreads (the
-// partial sums are double-buffered).  The next column is prefetched into
-// registers while the current one is reduced.  Cyclic order = ascending global
-// column index (W is kept sorted), mirroring the oracle.
+// ONE persistent CTA per fit.  Thread t owns rows t, t+T, ..., t+(R-1)T and
+// keeps their residuals r_i in REGISTERS for the whole solve, so a residual
+// update touches no memory and needs no synchronisation; each coordinate costs
+// one warp-shuffle reduction plus one __syncthreads (partials double-buffered).
+// Slot metadata (column index, c_j, 1/s_j, beta_j) lives in shared memory; the
+// next column is prefetched into registers while the current one is reduced.
+// Cyclic order = ascending global column index (W is kept sorted), mirroring
+// the oracle:
 //   z  = sum_i (x_ij - c_j) r_i / (n s_j) + b_j
 //   b' = S(z, lambda alpha) / (1 + lambda (1 - alpha))
 //   r -= (b' - b_j) (x_j - c_j)/s_j            (all rows, incl. held-out ones)
@@ -668,27 +670,38 @@ struct CdArgs {
     RoundStatus *st;
 };
 
+// shared-memory bytes per W slot: beta, c, 1/s (fp64) + column index, active list (int32)
+constexpr int kCdSlotBytes = 32;
+
 template <typename T, bool MASK, int RM>
 __global__ void __launch_bounds__(RM >= 16 ? 1024 : 512, 1) k_cd(CdArgs a) {
     extern __shared__ __align__(16) double sm[];
     __shared__ double part[2][32];
     __shared__ int wcount[33];
     const int T_ = blockDim.x, t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = T_ >> 5;
-    const int n = a.n;
+    const int n = a.n, nW = a.nW;
     const int R = (n + T_ - 1) / T_;
-    double *rs = sm;                                  // R*T_ entries
-    double *bw = sm + (size_t)R * T_;                 // nW entries
-    int *act = reinterpret_cast<int *>(bw + a.nW);    // nW entries
-    for (int i = t; i < R * T_; i += T_) rs[i] = i < n ? a.r[i] : 0.0;
-    for (int w = t; w < a.nW; w += T_) bw[w] = a.beta[a.W[w]];
+    double *bw = sm;                                   // beta_j
+    double *cw = bw + nW;                              // c_j
+    double *iw = cw + nW;                              // 1/s_j
+    int *Ws = reinterpret_cast<int *>(iw + nW);        // column index
+    int *act = Ws + nW;                                // active slot list
+    for (int w = t; w < nW; w += T_) {
+        int j = a.W[w];
+        Ws[w] = j;
+        bw[w] = a.beta[j];
+        cw[w] = a.c[j];
+        iw[w] = 1.0 / a.s[j];
+    }
+    double rr[RM];
     unsigned mbits = 0;
 #pragma unroll
-    for (int k = 0; k < RM; k++)
-        if (k < R) {
-            int i = t + k * T_;
-            bool use = i < n && (!MASK || a.mask[i]);
-            mbits |= (use ? 1u : 0u) << k;
-        }
+    for (int k = 0; k < RM; k++) {
+        int i = t + k * T_;
+        rr[k] = (k < R && i < n) ? a.r[i] : 0.0;
+        bool use = k < R && i < n && (!MASK || a.mask[i]);
+        mbits |= (use ? 1u : 0u) << k;
+    }
     __syncthreads();
     const T *X = reinterpret_cast<const T *>(a.X);
     int passes = 0, status = 0, buf = 0;
@@ -700,63 +713,64 @@ __global__ void __launch_bounds__(RM >= 16 ? 1024 : 512, 1) k_cd(CdArgs a) {
         if (len == 0) return;
         T xc[RM], xn[RM];
         int w = list ? list[0] : 0;
-        int j = a.W[w];
-        double cj = a.c[j], sj = a.s[j];
+        {
+            const T *col = X + (int64_t)Ws[w] * a.ld;
 #pragma unroll
-        for (int k = 0; k < RM; k++)
-            if (k < R) { int i = t + k * T_; xc[k] = i < n ? X[(int64_t)j * a.ld + i] : T(0); }
+            for (int k = 0; k < RM; k++) { int i = t + k * T_; xc[k] = (k < R && i < n) ? col[i] : T(0); }
+        }
         for (int q = 0; q < len; q++) {
-            int wn = 0, jn = 0;
-            double cn = 0.0, sn = 1.0;
+            int wn = w;
             if (q + 1 < len) {                      // prefetch the next column
                 wn = list ? list[q + 1] : q + 1;
-                jn = a.W[wn];
-                cn = a.c[jn];
-                sn = a.s[jn];
+                const T *col = X + (int64_t)Ws[wn] * a.ld;
 #pragma unroll
-                for (int k = 0; k < RM; k++)
-                    if (k < R) { int i = t + k * T_; xn[k] = i < n ? X[(int64_t)jn * a.ld + i] : T(0); }
+                for (int k = 0; k < RM; k++) { int i = t + k * T_; xn[k] = (k < R && i < n) ? col[i] : T(0); }
             }
-            const double b_old = bw[w];
+            const double b_old = bw[w], cj = cw[w], isj = iw[w];
             double p0 = 0.0, p1 = 0.0;
 #pragma unroll
             for (int k = 0; k < RM; k += 2) {
-                if (k < R && ((mbits >> k) & 1u)) p0 = fma(to_d(xc[k]) - cj, rs[t + k * T_], p0);
-                if (k + 1 < R && ((mbits >> (k + 1)) & 1u)) p1 = fma(to_d(xc[k + 1]) - cj, rs[t + (k + 1) * T_], p1);
+                if ((mbits >> k) & 1u) p0 = fma(to_d(xc[k]) - cj, rr[k], p0);
+                if (k + 1 < RM && ((mbits >> (k + 1)) & 1u)) p1 = fma(to_d(xc[k + 1]) - cj, rr[k + 1], p1);
             }
             double pt = warp_sum(p0 + p1);
             if (lane == 0) part[buf][wid] = pt;
             __syncthreads();
             double s0 = 0.0, s1 = 0.0;
-            for (int u = 0; u + 1 < nw; u += 2) { s0 += part[buf][u]; s1 += part[buf][u + 1]; }
-            if (nw & 1) s0 += part[buf][nw - 1];
-            const double inv_s = 1.0 / sj;
-            const double z = (s0 + s1) * a.inv_n * inv_s + b_old;
+            int u = 0;
+            for (; u + 3 < nw; u += 4) {
+                double2 h0 = *reinterpret_cast<const double2 *>(&part[buf][u]);
+                double2 h1 = *reinterpret_cast<const double2 *>(&part[buf][u + 2]);
+                s0 += h0.x + h0.y;
+                s1 += h1.x + h1.y;
+            }
+            for (; u < nw; u++) s0 += part[buf][u];
+            const double z = (s0 + s1) * a.inv_n * isj + b_old;
             const double bn = soft_threshold(z, a.lam_alpha) * a.inv_den;
             const double d = bn - b_old;
             if (d != 0.0) {
-                const double f = d * inv_s;
+                const double f = d * isj;
 #pragma unroll
                 for (int k = 0; k < RM; k++)
-                    if (k < R) rs[t + k * T_] -= f * (to_d(xc[k]) - cj);
+                    if (k < R) rr[k] = fma(-f, to_d(xc[k]) - cj, rr[k]);
                 if (t == 0) bw[w] = bn;
             }
             dmax = fmax(dmax, fabs(d));
             bmax = fmax(bmax, fabs(bn));
             buf ^= 1;
-            w = wn; j = jn; cj = cn; sj = sn;
+            w = wn;
 #pragma unroll
             for (int k = 0; k < RM; k++) xc[k] = xn[k];
         }
-        __syncthreads();     // bw/rs visible before the next list build
+        __syncthreads();     // bw visible before the next list build
     };
 
     // ordered block-wide compaction of the nonzero slots into act[]
     auto build_active = [&]() -> int {
         int total = 0;
-        for (int base = 0; base < a.nW; base += T_) {
+        for (int base = 0; base < nW; base += T_) {
             int w = base + t;
-            bool nz = w < a.nW && bw[w] != 0.0;
+            bool nz = w < nW && bw[w] != 0.0;
             unsigned m = __ballot_sync(0xffffffffu, nz);
             if (lane == 0) wcount[wid] = __popc(m);
             __syncthreads();
@@ -784,17 +798,18 @@ __global__ void __launch_bounds__(RM >= 16 ? 1024 : 512, 1) k_cd(CdArgs a) {
         }
         if (status) break;
         double dmax, bmax;
-        sweep(nullptr, a.nW, dmax, bmax);        // full pass over W
+        sweep(nullptr, nW, dmax, bmax);          // full pass over W
         if (++passes > a.max_iter) { status = 3; break; }
         if (dmax <= a.tol * bmax || dmax <= a.floor_) break;
     }
     __syncthreads();
     // write back + record statistics (a11)
     double rss = 0.0, sr = 0.0;
-    for (int k = 0; k < R; k++) {
+#pragma unroll
+    for (int k = 0; k < RM; k++) {
         int i = t + k * T_;
-        if (i < n) {
-            double v = rs[i];
+        if (k < R && i < n) {
+            double v = rr[k];
             bool use = (mbits >> k) & 1u;
             a.r[i] = v;
             a.r_scan[i] = use ? v : 0.0;
@@ -803,13 +818,13 @@ __global__ void __launch_bounds__(RM >= 16 ? 1024 : 512, 1) k_cd(CdArgs a) {
     }
     for (int i = n + t; i < (int)a.ld; i += T_) a.r_scan[i] = 0.0;
     double l1 = 0.0, l2 = 0.0, nnz = 0.0;
-    for (int w = t; w < a.nW; w += T_) {
+    for (int w = t; w < nW; w += T_) {
         double b = bw[w];
-        int jw = a.W[w];
+        int jw = Ws[w];
         a.beta[jw] = b;
         a.betaW_out[w] = b;
-        a.betaW_out[a.nW + w] = a.c[jw];
-        a.betaW_out[2 * a.nW + w] = a.s[jw];
+        a.betaW_out[nW + w] = cw[w];
+        a.betaW_out[2 * nW + w] = a.s[jw];
         l1 += fabs(b);
         l2 = fma(b, b, l2);
         nnz += b != 0.0 ? 1.0 : 0.0;
