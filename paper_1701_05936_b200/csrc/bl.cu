@@ -435,6 +435,7 @@ bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double a
         pp->Wcap = 0;
         ensure_W(pp, std::min<int64_t>(p, 4096));
     }
+    if (!pp->hst) CK(cudaMallocHost(&pp->hst, sizeof(RoundStatus)));
     cudaStream_t st = pp->stream;
     CK(cudaMemsetAsync(pp->beta, 0, 8 * p, st));
     CK(cudaMemsetAsync(pp->wflag, 0, p, st));
