@@ -72,6 +72,8 @@ typedef struct {
     void *stream;        /* cudaStream_t to run on; NULL => library-owned stream */
     int profile;         /* 1 => time every scan / CD launch with CUDA events (bl_path_perf) */
     int max_kkt_rounds;  /* <= 0 => 10 */
+    int cd_mode;         /* 0 auto (Gram/covariance updates while |W| <= 4096),
+                            1 residual-update CD (r held on chip), 2 Gram only */
 } bl_opts;
 
 /* Per-fit performance counters (filled when opts->profile == 1). */

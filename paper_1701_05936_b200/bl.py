@@ -21,6 +21,7 @@ LIB_PATH = os.path.join(_PKG, "libbl.so")
 BL_OK, BL_ERR_ARG, BL_ERR_DEGENERATE, BL_ERR_CONVERGENCE, BL_ERR_CUDA, BL_ERR_NCCL, BL_ERR_OOM = range(7)
 BL_F64, BL_F32, BL_I8 = 0, 1, 2
 SCREEN = {"none": 0, "ssr": 1, "hybrid": 2}
+CD_MODE = {"auto": 0, "residual": 1, "gram": 2}
 _DT = {np.dtype(np.float64): BL_F64, np.dtype(np.float32): BL_F32, np.dtype(np.int8): BL_I8}
 _ITEM = {BL_F64: 8, BL_F32: 4, BL_I8: 1}
 
@@ -38,7 +39,8 @@ class bl_dist(ctypes.Structure):
 
 
 class bl_opts(ctypes.Structure):
-    _fields_ = [("stream", ctypes.c_void_p), ("profile", ctypes.c_int), ("max_kkt_rounds", ctypes.c_int)]
+    _fields_ = [("stream", ctypes.c_void_p), ("profile", ctypes.c_int), ("max_kkt_rounds", ctypes.c_int),
+                ("cd_mode", ctypes.c_int)]
 
 
 class bl_perf(ctypes.Structure):
@@ -226,9 +228,9 @@ class Design:
         return out.value
 
     def fit_path(self, y, lam, alpha=1.0, tol=1e-7, max_iter=10000, screen="hybrid", stream=None,
-                 profile=False, max_kkt_rounds=0, raise_on_error=True):
+                 profile=False, max_kkt_rounds=0, raise_on_error=True, cd="auto"):
         lam = _f64(lam)
-        o = bl_opts(stream, int(profile), max_kkt_rounds)
+        o = bl_opts(stream, int(profile), max_kkt_rounds, CD_MODE[cd])
         h = ctypes.c_void_p()
         rc = lib().bl_fit_path(self.h, _p(_f64(y)), _p(lam), lam.size, alpha, tol, max_iter,
                                SCREEN.get(screen, screen), ctypes.byref(o), ctypes.byref(h))
@@ -239,10 +241,10 @@ class Design:
             lib().bl_free(h)
 
     def cv(self, y, lam, K=10, alpha=1.0, tol=1e-7, max_iter=10000, fold_id=None, seed=0, stream=None,
-           profile=False):
+           profile=False, cd="auto"):
         lam = _f64(lam)
         f = None if fold_id is None else np.ascontiguousarray(fold_id, dtype=np.int32)
-        o = bl_opts(stream, int(profile), 0)
+        o = bl_opts(stream, int(profile), 0, CD_MODE[cd])
         h = ctypes.c_void_p()
         _check(lib().bl_cv(self.h, _p(_f64(y)), _p(lam), lam.size, alpha, tol, max_iter, K, _p(f), seed,
                            ctypes.byref(o), ctypes.byref(h)))

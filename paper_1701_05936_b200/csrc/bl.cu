@@ -140,7 +140,14 @@ struct bl_prep {
     int *hup;               // pinned upload staging (grows)
     double *hbw;            // pinned, 3*|W| entries (beta, c, s of W) (grows)
     size_t hlist_cap, hup_cap, hbw_cap;
-    char *warena;           // device W buffers: W (int32) + betaW out (3 x fp64), grows
+    char *warena;           // device W buffers (grow): W sorted, Wst, ord (int32); betaW (3 x fp64), dbeta
+    int *Wst_d, *ord_d;     // Gram CD: storage slots (append order) and cyclic order
+    double *dbeta;          // Gram CD: coefficient change per slot over one solve
+    double *G;              // Gram CD: ldG x ldG, row-major by storage slot (HBM / L2)
+    int64_t ldG;
+    int nG;                 // slots whose G row/column is computed
+    double *rpart;          // per-block partials of the residual refresh
+    int cd_mode;            // 0 auto (Gram when |W| <= 4096), 1 residual, 2 Gram
     cudaStream_t own;       // library stream (used when the caller passes none)
     // profiling
     int profile;
@@ -196,6 +203,23 @@ struct EvPair {
     }
 };
 
+struct EvPairOpt {
+    bl_prep *pp;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> *vec;
+    cudaEvent_t e1 = nullptr;
+    EvPairOpt(bl_prep *pp_, std::vector<std::pair<cudaEvent_t, cudaEvent_t>> *v) : pp(pp_), vec(v) {
+        if (!pp->profile || !vec) return;
+        cudaEvent_t e0;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaEventRecord(e0, pp->stream));
+        vec->push_back({e0, e1});
+    }
+    ~EvPairOpt() {
+        if (pp->profile && vec && e1) cudaEventRecord(e1, pp->stream);
+    }
+};
+
 double sum_events(std::vector<std::pair<cudaEvent_t, cudaEvent_t>> &v) {
     double tot = 0.0;
     for (auto &pr : v) {
@@ -237,7 +261,7 @@ size_t allow_dyn_smem(const void *kern) {
 // ------------------------------------------------------------ scan launcher
 // Raw-dot + identity epilogue over `list` (or all columns); v = fp64 vector
 // (fp32/fp64 designs) -- for int8 designs v is quantised to limbs first.
-void launch_scan(bl_prep *pp, ScanArgs a, const double *v_dev, bool timed) {
+void launch_scan(bl_prep *pp, ScanArgs a, const double *v_dev, bool timed, bool events = true) {
     bl_design *d = pp->d;
     a.X = d->X;
     a.ld = d->ld;
@@ -257,7 +281,7 @@ void launch_scan(bl_prep *pp, ScanArgs a, const double *v_dev, bool timed) {
         size_t smem = (size_t)8 * pp->limb_ld;
         allow_dyn_smem((const void *)k_scan_i8);
         int grid = grid_for((const void *)k_scan_i8, kScanThreads, smem, d->nsm);
-        EvPair ev(pp, timed ? &pp->ev_scan : &pp->ev_prep);
+        EvPairOpt ev(pp, events ? (timed ? &pp->ev_scan : &pp->ev_prep) : nullptr);
         k_scan_i8<<<grid, kScanThreads, smem, pp->stream>>>(a);
         CKL();
     } else {
@@ -267,13 +291,13 @@ void launch_scan(bl_prep *pp, ScanArgs a, const double *v_dev, bool timed) {
         if (d->dt == DT_F32) {
             allow_dyn_smem((const void *)k_scan_fp<float, 4>);
             int grid = grid_for((const void *)k_scan_fp<float, 4>, kScanThreads, smem, d->nsm);
-            EvPair ev(pp, timed ? &pp->ev_scan : &pp->ev_prep);
+            EvPairOpt ev(pp, events ? (timed ? &pp->ev_scan : &pp->ev_prep) : nullptr);
             k_scan_fp<float, 4><<<grid, kScanThreads, smem, pp->stream>>>(a);
             CKL();
         } else {
             allow_dyn_smem((const void *)k_scan_fp<double, 4>);
             int grid = grid_for((const void *)k_scan_fp<double, 4>, kScanThreads, smem, d->nsm);
-            EvPair ev(pp, timed ? &pp->ev_scan : &pp->ev_prep);
+            EvPairOpt ev(pp, events ? (timed ? &pp->ev_scan : &pp->ev_prep) : nullptr);
             k_scan_fp<double, 4><<<grid, kScanThreads, smem, pp->stream>>>(a);
             CKL();
         }
@@ -316,6 +340,7 @@ void free_prep(bl_prep *pp) {
     if (pp->hbw) cudaFreeHost(pp->hbw);
     if (pp->hup) cudaFreeHost(pp->hup);
     if (pp->warena) cudaFree(pp->warena);
+    if (pp->G) cudaFree(pp->G);
     if (pp->own) cudaStreamDestroy(pp->own);
     pp->magic = MAGIC_DEAD;
     delete pp;
@@ -363,11 +388,15 @@ void ensure_W(bl_prep *pp, int64_t need) {
     CK(cudaStreamSynchronize(pp->stream));
     if (pp->warena) CK(cudaFree(pp->warena));
     pp->warena = nullptr;
-    size_t bytes = (size_t)round_up(4 * nc, 256) + (size_t)24 * nc;
+    size_t ib = (size_t)round_up(4 * nc, 256);
+    size_t bytes = 3 * ib + (size_t)32 * nc;
     cudaError_t e = cudaMalloc(&pp->warena, bytes);
     if (e != cudaSuccess) { cudaGetLastError(); raise(BL_ERR_OOM, "cudaMalloc(%zu) for W: %s", bytes, cudaGetErrorString(e)); }
     pp->W = (int *)pp->warena;
-    pp->betaW = (double *)(pp->warena + round_up(4 * nc, 256));
+    pp->Wst_d = (int *)(pp->warena + ib);
+    pp->ord_d = (int *)(pp->warena + 2 * ib);
+    pp->betaW = (double *)(pp->warena + 3 * ib);
+    pp->dbeta = pp->betaW + 3 * nc;
     pp->Wcap = nc;
 }
 
@@ -390,6 +419,8 @@ bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double a
     pp->p = d->p;
     pp->ld = d->ld;
     pp->profile = opts ? opts->profile : 0;
+    pp->cd_mode = opts ? opts->cd_mode : 0;
+    pp->nG = 0;
     pp->launches = 0;
     if (!pp->own) CK(cudaStreamCreateWithFlags(&pp->own, cudaStreamNonBlocking));
     pp->stream = (opts && opts->stream) ? (cudaStream_t)opts->stream : pp->own;
@@ -418,7 +449,7 @@ bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double a
                o_rf = take(8 * pp->vlen), o_rs = take(8 * pp->vlen), o_vt = take(8 * pp->vlen),
                o_limbs = take((size_t)8 * pp->limb_ld), o_lsc = take(32), o_ps = take(sizeof(PrepScalars)),
                o_st = take(sizeof(RoundStatus)), o_av = take(8 * pp->amax_blocks), o_ai = take(8 * pp->amax_blocks),
-               o_nl = take(16);
+               o_nl = take(16), o_rp = take(16 * (pp->vlen / 256 + 1));
         pp->arena_bytes = off;
         cudaError_t e = cudaMalloc(&pp->arena, off);
         if (e != cudaSuccess) { cudaGetLastError(); raise(BL_ERR_OOM, "cudaMalloc(%zu) failed: %s", off, cudaGetErrorString(e)); }
@@ -432,6 +463,7 @@ bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double a
         pp->limbs = (int8_t *)(A + o_limbs); pp->limb_scale = (double *)(A + o_lsc); pp->limb_sum = pp->limb_scale + 1;
         pp->ps = (PrepScalars *)(A + o_ps); pp->st = (RoundStatus *)(A + o_st);
         pp->amax_v = (double *)(A + o_av); pp->amax_i = (long long *)(A + o_ai); pp->nlive = (int *)(A + o_nl);
+        pp->rpart = (double *)(A + o_rp);
         pp->Wcap = 0;
         ensure_W(pp, std::min<int64_t>(p, 4096));
     }
@@ -489,6 +521,9 @@ bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double a
         sa.fixval = &pp->ps->nt;
         launch_scan(pp, sa, pp->vtmp, false);
     }
+    // the solve starts from r = y~: r_scan <- y~ (used rows), sum r <- sum y~
+    CK(cudaMemcpyAsync(pp->rscan, pp->yt, 8 * pp->vlen, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(&pp->st->sumr, &pp->ps->sum_yt, sizeof(double), cudaMemcpyDeviceToDevice, st));
     // the one host round trip of preprocessing: the scalars the lambda loop branches on
     CK(cudaMemcpyAsync(&pp->hps, pp->ps, sizeof(PrepScalars), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -502,25 +537,48 @@ bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double a
 
 // ------------------------------------------------------------------ the path
 
-void sorted_merge_into(std::vector<int> &W, std::vector<int> add) {
-    std::sort(add.begin(), add.end());
-    add.erase(std::unique(add.begin(), add.end()), add.end());
-    std::vector<int> out;
-    out.reserve(W.size() + add.size());
-    std::set_union(W.begin(), W.end(), add.begin(), add.end(), std::back_inserter(out));
-    W.swap(out);
-}
+// The working set W (a7): `sorted` = ascending local columns (the cyclic CD
+// order); `slots` = append order (stable storage slots of the Gram matrix).
+struct WorkingSet {
+    std::vector<int> sorted, slots;
+    // add candidates; returns the columns that were not yet in W (sorted, unique)
+    std::vector<int> add(std::vector<int> cand) {
+        std::sort(cand.begin(), cand.end());
+        cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
+        std::vector<int> fresh;
+        std::set_difference(cand.begin(), cand.end(), sorted.begin(), sorted.end(), std::back_inserter(fresh));
+        std::vector<int> out;
+        out.reserve(sorted.size() + fresh.size());
+        std::merge(sorted.begin(), sorted.end(), fresh.begin(), fresh.end(), std::back_inserter(out));
+        sorted.swap(out);
+        slots.insert(slots.end(), fresh.begin(), fresh.end());
+        return fresh;
+    }
+    int size() const { return (int)sorted.size(); }
+};
 
-void upload_W(bl_prep *pp, const std::vector<int> &W, const std::vector<int> &added) {
-    ensure_W(pp, (int64_t)W.size());
-    ensure_host(pp->hup, pp->hup_cap, W.size() + added.size());
+void upload_W(bl_prep *pp, const WorkingSet &ws, const std::vector<int> &added) {
+    const size_t nW = ws.sorted.size();
+    ensure_W(pp, (int64_t)nW);
+    ensure_host(pp->hup, pp->hup_cap, 3 * nW + added.size() + 1);
     cudaStream_t st = pp->stream;
+    // cyclic order over storage slots: slots sorted by column
+    std::vector<int> ord(nW);
+    for (size_t q = 0; q < nW; q++) ord[q] = (int)q;
+    std::sort(ord.begin(), ord.end(), [&](int u, int v) { return ws.slots[u] < ws.slots[v]; });
     // pinned staging: the previous round ended with a stream sync, so hup is free
-    std::memcpy(pp->hup, W.data(), 4 * W.size());
-    std::memcpy(pp->hup + W.size(), added.data(), 4 * added.size());
-    if (!W.empty()) CK(cudaMemcpyAsync(pp->W, pp->hup, 4 * W.size(), cudaMemcpyHostToDevice, st));
+    int *h = pp->hup;
+    std::memcpy(h, ws.sorted.data(), 4 * nW);
+    std::memcpy(h + nW, ws.slots.data(), 4 * nW);
+    std::memcpy(h + 2 * nW, ord.data(), 4 * nW);
+    std::memcpy(h + 3 * nW, added.data(), 4 * added.size());
+    if (nW) {
+        CK(cudaMemcpyAsync(pp->W, h, 4 * nW, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(pp->Wst_d, h + nW, 4 * nW, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(pp->ord_d, h + 2 * nW, 4 * nW, cudaMemcpyHostToDevice, st));
+    }
     if (!added.empty()) {
-        CK(cudaMemcpyAsync(pp->viol, pp->hup + W.size(), 4 * added.size(), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(pp->viol, h + 3 * nW, 4 * added.size(), cudaMemcpyHostToDevice, st));
         k_set_flags<<<(unsigned)((added.size() + 255) / 256), 256, 0, st>>>(pp->viol, (int)added.size(), pp->wflag, 1);
         CKL();
         pp->launches++;
@@ -596,6 +654,116 @@ void launch_cd(bl_prep *pp, int nW, double lam, double alpha, double tol, int ma
     pp->launches++;
 }
 
+// ---- NEXT-2 Gram CD (covariance updates) -------------------------------------
+void ensure_G(bl_prep *pp, int64_t need) {
+    if (need <= pp->ldG) return;
+    int64_t nl = std::max<int64_t>(std::max<int64_t>(need, 2 * pp->ldG), 256);
+    nl = round_up(nl, 32);
+    double *G2 = nullptr;
+    cudaError_t e = cudaMalloc(&G2, (size_t)8 * nl * nl);
+    if (e != cudaSuccess) { cudaGetLastError(); raise(BL_ERR_OOM, "cudaMalloc for the %lld^2 Gram matrix: %s", (long long)nl, cudaGetErrorString(e)); }
+    if (pp->G && pp->nG > 0)
+        CK(cudaMemcpy2DAsync(G2, 8 * nl, pp->G, 8 * pp->ldG, 8 * (size_t)pp->nG, pp->nG, cudaMemcpyDeviceToDevice,
+                             pp->stream));
+    if (pp->G) { CK(cudaStreamSynchronize(pp->stream)); CK(cudaFree(pp->G)); }
+    pp->G = G2;
+    pp->ldG = nl;
+}
+
+template <typename T, bool M>
+void launch_gram_t(bl_prep *pp, int nW) {
+    bl_design *d = pp->d;
+    const void *kern = (const void *)k_gram<T, M>;
+    allow_dyn_smem(kern);
+    dim3 grid(nW - pp->nG, (nW + 255) / 256);
+    k_gram<T, M><<<grid, 256, 8 * d->n, pp->stream>>>((const T *)d->X, d->ld, (int)d->n, pp->Wst_d, nW, pp->nG,
+                                                       (int)pp->ldG, pp->c, pp->s, M ? pp->mask : nullptr,
+                                                       1.0 / pp->nt, pp->G);
+    CKL();
+    pp->launches++;
+}
+
+template <typename T, bool M>
+void launch_resid_t(bl_prep *pp, int nW) {
+    bl_design *d = pp->d;
+    int nb = (int)((d->ld + 255) / 256);
+    k_resid_update<T, M><<<nb, 256, 0, pp->stream>>>((const T *)d->X, d->ld, (int)d->n, pp->Wst_d, nW, pp->dbeta,
+                                                     pp->c, pp->s, M ? pp->mask : nullptr, pp->rfull, pp->rscan,
+                                                     pp->rpart);
+    CKL();
+    k_resid_finish<<<1, 32, 0, pp->stream>>>(pp->rpart, nb, pp->st);
+    CKL();
+    pp->launches += 2;
+}
+
+bool use_gram(bl_prep *pp, int nW) {
+    if (pp->cd_mode == 1) return false;
+    if (nW > 4096) {
+        if (pp->cd_mode == 2) raise(BL_ERR_OOM, "Gram CD supports |W| <= 4096 (got %d)", nW);
+        return false;
+    }
+    return true;
+}
+
+// One CD solve at lambda on the current W (a8), either flavour.
+void solve_cd(bl_prep *pp, int nW, double lam, double alpha, double tol, int max_iter) {
+    if (!use_gram(pp, nW)) {
+        launch_cd(pp, nW, lam, alpha, tol, max_iter);
+        return;
+    }
+    bl_design *d = pp->d;
+    const bool M = pp->has_mask != 0;
+    EvPairOpt ev(pp, &pp->ev_cd);
+    if (nW > pp->nG) {                        // G rows/columns of the slots added since the last solve
+        ensure_G(pp, nW);
+        if (d->dt == DT_F64) M ? launch_gram_t<double, true>(pp, nW) : launch_gram_t<double, false>(pp, nW);
+        else if (d->dt == DT_F32) M ? launch_gram_t<float, true>(pp, nW) : launch_gram_t<float, false>(pp, nW);
+        else M ? launch_gram_t<int8_t, true>(pp, nW) : launch_gram_t<int8_t, false>(pp, nW);
+        pp->nG = nW;
+    }
+    {                                          // g_W = x~_W' r / n at the solve's starting residual
+        ScanArgs sa{};
+        sa.list = pp->Wst_d;
+        sa.nlist = nullptr;
+        sa.nlist_host = nW;
+        sa.K1 = &pp->st->sumr;
+        sa.K2v = 1.0 / pp->nt;
+        sa.out = pp->z;
+        launch_scan(pp, sa, pp->rscan, false, false);
+    }
+    CdGramArgs ga{};
+    ga.Wst = pp->Wst_d;
+    ga.ord = pp->ord_d;
+    ga.nW = nW;
+    ga.ldG = (int)pp->ldG;
+    ga.G = pp->G;
+    ga.z = pp->z;
+    ga.beta = pp->beta;
+    ga.dbeta = pp->dbeta;
+    ga.lam_alpha = lam * alpha;
+    ga.inv_den = 1.0 / (1.0 + lam * (1.0 - alpha));
+    ga.tol = tol;
+    ga.floor_ = 1e-13 * (alpha * lam + std::sqrt(pp->hps.Y2 / pp->nt));   // Q6 noise floor
+    ga.max_iter = max_iter;
+    ga.betaW_out = pp->betaW;
+    ga.c = pp->c;
+    ga.s = pp->s;
+    ga.st = pp->st;
+    int T = (int)std::min<int64_t>(1024, round_up(std::max(nW, 32), 32));
+    int KM = (nW + T - 1) / T;
+    const void *kern = KM <= 1 ? (const void *)k_cd_gram<1> : KM <= 2 ? (const void *)k_cd_gram<2>
+                                                                        : (const void *)k_cd_gram<4>;
+    size_t smem = (size_t)48 * nW + 16;
+    size_t lim = allow_dyn_smem(kern);
+    if (smem > lim) raise(BL_ERR_OOM, "Gram CD shared memory %zu > %zu", smem, lim);
+    void *args[] = {&ga};
+    CK(cudaLaunchKernel(kern, dim3(1), dim3(T), args, smem, pp->stream));
+    pp->launches++;
+    if (d->dt == DT_F64) M ? launch_resid_t<double, true>(pp, nW) : launch_resid_t<double, false>(pp, nW);
+    else if (d->dt == DT_F32) M ? launch_resid_t<float, true>(pp, nW) : launch_resid_t<float, false>(pp, nW);
+    else M ? launch_resid_t<int8_t, true>(pp, nW) : launch_resid_t<int8_t, false>(pp, nW);
+}
+
 // One full path.  Fills `out` (prefix on convergence failure).
 bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, double tol, int max_iter, int screen,
                    int max_rounds, bl_path *out, double *heldout /* K x n or nullptr */) {
@@ -613,7 +781,7 @@ bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, doubl
     out->kkt_rounds.assign(K, 0);
     out->cols_scanned.assign(K, 0);
     out->col_ptr.assign(K + 1, 0);
-    std::vector<int> W;
+    WorkingSet W;
     const int bthreads = 256;
     const int bgrid = (int)std::min<int64_t>((d->p + bthreads - 1) / bthreads, (int64_t)d->nsm * 8);
     const int use_bedpp = screen == BL_SCREEN_HYBRID;
@@ -625,7 +793,7 @@ bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, doubl
 
     if (screen == BL_SCREEN_NONE) {
         // W = every non-constant column; no screening, no scans (SPEC "policy none")
-        CK(cudaMemsetAsync(pp->st, 0, sizeof(RoundStatus), st));
+        CK(cudaMemsetAsync(pp->st, 0, 4 * sizeof(int), st));
         k_bedpp<<<bgrid, bthreads, 0, st>>>(d->p, pp->s, pp->a, pp->b, pp->ps, alpha, lmax, -1.0, 0, pp->flags,
                                             pp->scope, pp->st);
         CKL();
@@ -633,8 +801,7 @@ bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, doubl
         CK(cudaMemcpyAsync(pp->hst, pp->st, sizeof(RoundStatus), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         std::vector<int> all = read_list(pp, pp->scope, pp->hst->nscope);
-        sorted_merge_into(W, all);
-        upload_W(pp, W, all);
+        upload_W(pp, W, W.add(all));
     }
 
     for (int k = 0; k < K; k++) {
@@ -652,7 +819,7 @@ bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, doubl
         }
         const double lam_next = k + 1 < K ? lambda[k + 1] : -1.0;
         if (screen != BL_SCREEN_NONE) {
-            CK(cudaMemsetAsync(pp->st, 0, sizeof(RoundStatus), st));
+            CK(cudaMemsetAsync(pp->st, 0, 4 * sizeof(int), st));   // counters only: sum r / rss persist
             k_bedpp<<<bgrid, bthreads, 0, st>>>(d->p, pp->s, pp->a, pp->b, pp->ps, alpha, lam, lam_next, use_bedpp,
                                                 pp->flags, use_bedpp ? pp->scope : nullptr, pp->st);
             CKL();
@@ -670,15 +837,14 @@ bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, doubl
                 strong_next = read_list(pp, pp->strong, pp->hst->nstrong);
                 first = false;
             }
-            sorted_merge_into(W, strong_next);
-            upload_W(pp, W, strong_next);
+            upload_W(pp, W, W.add(strong_next));
             strong_next.clear();
         }
         int rounds = 0;
         int64_t scanned = 0;
         int passes = 0;
         for (;;) {
-            launch_cd(pp, (int)W.size(), lam, alpha, tol, max_iter);
+            solve_cd(pp, W.size(), lam, alpha, tol, max_iter);
             if (screen == BL_SCREEN_NONE) {
                 CK(cudaMemcpyAsync(pp->hst, pp->st, sizeof(RoundStatus), cudaMemcpyDeviceToHost, st));
                 CK(cudaStreamSynchronize(st));
@@ -718,8 +884,7 @@ bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, doubl
                     break;
                 }
                 std::vector<int> v = read_list(pp, pp->viol, pp->hst->nviol);
-                sorted_merge_into(W, v);
-                upload_W(pp, W, v);
+                upload_W(pp, W, W.add(v));
                 continue;
             }
             strong_next = read_list(pp, pp->strong, pp->hst->nstrong);
@@ -744,7 +909,7 @@ bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, doubl
             double bq = pp->hbw[q];
             if (bq == 0.0) continue;
             double cq = pp->hbw[nW + q], sq = pp->hbw[2 * nW + q];
-            out->feat.push_back(W[q] + d->col_offset);
+            out->feat.push_back(W.sorted[q] + d->col_offset);
             out->beta_std.push_back(bq);
             out->beta_orig.push_back(bq / sq);
             shift += bq * cq / sq;

@@ -215,7 +215,8 @@ struct ScanArgs {
     int n;
     int64_t p;
     const int *list;          // nullptr => dense 0..p-1
-    const int *nlist;         // device count of `list`
+    const int *nlist;         // device count of `list` (nullptr => nlist_host)
+    int nlist_host;
     const double *v;          // fp64 vector, >= ld entries, zero beyond n (fp32/fp64 path)
     const int8_t *limbs;      // int8 path: 8 planes of `limb_ld` bytes
     int limb_ld;
@@ -256,7 +257,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_fp(ScanArgs a) {
     __syncthreads();
     const double K1 = *a.K1;
     const double K2 = a.K2 ? *a.K2 : a.K2v;
-    const int64_t m = a.list ? (int64_t)*a.nlist : a.p;
+    const int64_t m = a.list ? (a.nlist ? (int64_t)*a.nlist : (int64_t)a.nlist_host) : a.p;
     const int lane = threadIdx.x & 31;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -373,7 +374,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_i8(ScanArgs a) {
     const double K1 = *a.K1;
     const double K2 = a.K2 ? *a.K2 : a.K2v;
     const double scale = *a.limb_scale;
-    const int64_t m = a.list ? (int64_t)*a.nlist : a.p;
+    const int64_t m = a.list ? (a.nlist ? (int64_t)*a.nlist : (int64_t)a.nlist_host) : a.p;
     const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -843,6 +844,257 @@ __global__ void __launch_bounds__(RM >= 16 ? 1024 : 512, 1) k_cd(CdArgs a) {
         a.st->l1 = l1;
         a.st->l2 = l2;
         a.st->nnz = (int)nnz;
+    }
+}
+
+// ------------------------------- NEXT-2: covariance-update ("Gram") CD on W
+// SURVEY 8(f) NEXT-2 (glmnet's covariance updates; the paper's CD "only iterates
+// over features in the active set").  Same iterates as the residual CD
+// above, but the per-coordinate work is O(|W|) on the gradient vector
+//   g_w = x~_w' r / n        (w in W)
+// instead of an O(n) reduction:  z = g_w + b_w;  b' = S(z, lambda alpha)/(1 +
+// lambda(1-alpha));  g_k -= (b' - b_w) G_kw  for every k in W, with
+// G = X~_W' X~_W / n kept in HBM/L2 (identity (1), generalised to W x W).
+// g starts from the fused scan's z at the solve's residual; r is refreshed after
+// the solve from the coefficient changes (k_resid_update), so no drift crosses
+// lambdas.  Storage slots are append-only; `ord` gives the cyclic (ascending
+// column) order.
+
+// G rows (and columns) for the new slots [first, nW): G[s][t] = sum_i m_i
+// x~_is x~_it / n, t in [0, nW).  grid = (nW - first, ceil(nW / 256)), 256 threads.
+template <typename T, bool MASK>
+__global__ void __launch_bounds__(256) k_gram(const T *__restrict__ X, int64_t ld, int n,
+                                              const int *__restrict__ Wst, int nW, int first, int ldG,
+                                              const double *__restrict__ c, const double *__restrict__ s,
+                                              const uint8_t *__restrict__ mask, double inv_n, double *__restrict__ G) {
+    extern __shared__ __align__(16) double vs[];     // x~_s on the used rows
+    const int sl = first + blockIdx.x;
+    const int js = Wst[sl];
+    const double cs = c[js], is = 1.0 / s[js];
+    const T *xs = X + (int64_t)js * ld;
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        vs[i] = (!MASK || mask[i]) ? (to_d(xs[i]) - cs) * is : 0.0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int t0 = blockIdx.y * 256, t1 = min(nW, t0 + 256);
+    for (int tt = t0 + wid; tt < t1; tt += 8) {
+        const int jt = Wst[tt];
+        const T *xt = X + (int64_t)jt * ld;
+        const double ct = c[jt];
+        double acc0 = 0.0, acc1 = 0.0;
+        int i = lane;
+        for (; i + 32 < n; i += 64) {
+            acc0 = fma(vs[i], to_d(xt[i]) - ct, acc0);
+            acc1 = fma(vs[i + 32], to_d(xt[i + 32]) - ct, acc1);
+        }
+        if (i < n) acc0 = fma(vs[i], to_d(xt[i]) - ct, acc0);
+        double d = warp_sum(acc0 + acc1);
+        if (lane == 0) {
+            double gv = d / s[jt] * inv_n;
+            G[(int64_t)sl * ldG + tt] = gv;
+            if (tt < first) G[(int64_t)tt * ldG + sl] = gv;
+        }
+    }
+}
+
+struct CdGramArgs {
+    const int *Wst;          // storage slot -> local column
+    const int *ord;          // cyclic order (slots, ascending column)
+    int nW, ldG;
+    const double *G;         // ldG x ldG, row-major by slot
+    const double *z;         // z[j] = x~_j' r / n for the solve's starting residual
+    double *beta;            // p entries (global, by local column)
+    double *dbeta;           // nW entries out: beta_new - beta_old per slot
+    double lam_alpha, inv_den, tol, floor_;
+    int max_iter;
+    double *betaW_out;       // 3*nW: beta, c, s per slot (cyclic order)
+    const double *c, *s;
+    RoundStatus *st;
+};
+
+template <int KM>
+__global__ void __launch_bounds__(1024, 1) k_cd_gram(CdGramArgs a) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ int wcount[33];
+    __shared__ double red[32];
+    const int T_ = blockDim.x, t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = T_ >> 5;
+    const int nW = a.nW;
+    double *gA = sm, *gB = gA + nW, *bA = gB + nW, *bB = bA + nW, *b0 = bB + nW;
+    int *ord = reinterpret_cast<int *>(b0 + nW);
+    int *act = ord + nW;
+    for (int w = t; w < nW; w += T_) {
+        int j = a.Wst[w];
+        gA[w] = a.z[j];
+        bA[w] = b0[w] = a.beta[j];
+        ord[w] = a.ord[w];
+    }
+    __syncthreads();
+    double *gc = gA, *gn = gB, *bc = bA, *bnx = bB;     // current / next buffers
+    int passes = 0, status = 0;
+
+    auto sweep = [&](const int *list, int len, double &dmax, double &bmax) {
+        dmax = 0.0;
+        bmax = 0.0;
+        double r0[KM], r1[KM], r2[KM];      // G rows of list[q], list[q+1], list[q+2]
+        auto load_row = [&](double (&row)[KM], int qq) {
+            if (qq < len) {
+                const double *gr = a.G + (int64_t)list[qq] * a.ldG;
+#pragma unroll
+                for (int m = 0; m < KM; m++) { int k = t + m * T_; row[m] = k < nW ? gr[k] : 0.0; }
+            }
+        };
+        load_row(r0, 0);
+        load_row(r1, 1);
+        for (int q = 0; q < len; q++) {
+            load_row(r2, q + 2);
+            const int w = list[q];
+            const double b_old = bc[w];
+            const double zz = gc[w] + b_old;
+            const double bn = soft_threshold(zz, a.lam_alpha) * a.inv_den;
+            const double d = bn - b_old;
+            if (d != 0.0) {                  // uniform branch: every thread computed the same d
+#pragma unroll
+                for (int m = 0; m < KM; m++) {
+                    int k = t + m * T_;
+                    if (k < nW) {
+                        gn[k] = fma(-d, r0[m], gc[k]);
+                        bnx[k] = k == w ? bn : bc[k];
+                    }
+                }
+                __syncthreads();
+                double *tg = gc; gc = gn; gn = tg;
+                double *tb = bc; bc = bnx; bnx = tb;
+            }
+            dmax = fmax(dmax, fabs(d));
+            bmax = fmax(bmax, fabs(bn));
+#pragma unroll
+            for (int m = 0; m < KM; m++) { r0[m] = r1[m]; r1[m] = r2[m]; }
+        }
+        __syncthreads();
+    };
+
+    // ordered compaction of the nonzero slots (cyclic order) into act[]
+    auto build_active = [&]() -> int {
+        int total = 0;
+        for (int base = 0; base < nW; base += T_) {
+            int q = base + t;
+            int w = q < nW ? ord[q] : 0;
+            bool nz = q < nW && bc[w] != 0.0;
+            unsigned m = __ballot_sync(0xffffffffu, nz);
+            if (lane == 0) wcount[wid] = __popc(m);
+            __syncthreads();
+            if (t == 0) {
+                int run = 0;
+                for (int u = 0; u < nw; u++) { int c0 = wcount[u]; wcount[u] = run; run += c0; }
+                wcount[32] = run;
+            }
+            __syncthreads();
+            if (nz) act[total + wcount[wid] + __popc(m & ((1u << lane) - 1u))] = w;
+            total += wcount[32];
+            __syncthreads();
+        }
+        return total;
+    };
+
+    for (;;) {
+        for (;;) {
+            int na = build_active();
+            if (na == 0) break;
+            double dmax, bmax;
+            sweep(act, na, dmax, bmax);
+            if (++passes > a.max_iter) { status = 3; break; }
+            if (dmax <= a.tol * bmax || dmax <= a.floor_) break;
+        }
+        if (status) break;
+        double dmax, bmax;
+        sweep(ord, nW, dmax, bmax);
+        if (++passes > a.max_iter) { status = 3; break; }
+        if (dmax <= a.tol * bmax || dmax <= a.floor_) break;
+    }
+    __syncthreads();
+    double l1 = 0.0, l2 = 0.0, nnz = 0.0;
+    for (int q = t; q < nW; q += T_) {
+        int w = ord[q];
+        double b = bc[w];
+        int j = a.Wst[w];
+        a.beta[j] = b;
+        a.dbeta[w] = b - b0[w];
+        a.betaW_out[q] = b;
+        a.betaW_out[nW + q] = a.c[j];
+        a.betaW_out[2 * nW + q] = a.s[j];
+        l1 += fabs(b);
+        l2 = fma(b, b, l2);
+        nnz += b != 0.0 ? 1.0 : 0.0;
+    }
+    l1 = block_sum(l1, red);
+    l2 = block_sum(l2, red);
+    nnz = block_sum(nnz, red);
+    if (t == 0) {
+        a.st->cd_passes = passes;
+        a.st->cd_status = status;
+        a.st->l1 = l1;
+        a.st->l2 = l2;
+        a.st->nnz = (int)nnz;
+    }
+}
+
+// r -= X~_W dbeta on every row (held-out rows included); r_scan = r on used
+// rows.  Rows are split over blocks (deterministic order over slots); per-block
+// partial sums of r_scan and r_scan^2 go to `part` (finished by k_resid_finish).
+template <typename T, bool MASK>
+__global__ void __launch_bounds__(256) k_resid_update(const T *__restrict__ X, int64_t ld, int n,
+                                                      const int *__restrict__ Wst, int nW,
+                                                      const double *__restrict__ dbeta,
+                                                      const double *__restrict__ c, const double *__restrict__ s,
+                                                      const uint8_t *__restrict__ mask, double *__restrict__ r,
+                                                      double *__restrict__ r_scan, double *__restrict__ part) {
+    __shared__ double red[32];
+    __shared__ int sj[256];
+    __shared__ double sf[256], sc[256];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    double acc = 0.0;
+    for (int base = 0; base < nW; base += 256) {
+        int w = base + threadIdx.x;
+        __syncthreads();
+        if (w < nW) {
+            double d = dbeta[w];
+            int j = Wst[w];
+            sj[threadIdx.x] = j;
+            sf[threadIdx.x] = d / s[j];
+            sc[threadIdx.x] = c[j];
+        }
+        __syncthreads();
+        int cnt = min(256, nW - base);
+        if (i < n) {
+            for (int u = 0; u < cnt; u++) {
+                double f = sf[u];
+                if (f != 0.0) acc = fma(f, to_d(X[(int64_t)sj[u] * ld + i]) - sc[u], acc);
+            }
+        }
+    }
+    double rs = 0.0, rr = 0.0;
+    if (i < n) {
+        double v = r[i] - acc;
+        r[i] = v;
+        bool use = !MASK || mask[i];
+        double vs = use ? v : 0.0;
+        r_scan[i] = vs;
+        rs = vs;
+        rr = vs * vs;
+    } else if (i < ld) {
+        r_scan[i] = 0.0;
+    }
+    rs = block_sum(rs, red);
+    rr = block_sum(rr, red);
+    if (threadIdx.x == 0) { part[2 * blockIdx.x] = rs; part[2 * blockIdx.x + 1] = rr; }
+}
+
+__global__ void k_resid_finish(const double *__restrict__ part, int nb, RoundStatus *st) {
+    if (threadIdx.x == 0) {
+        double rs = 0.0, rr = 0.0;
+        for (int b = 0; b < nb; b++) { rs += part[2 * b]; rr += part[2 * b + 1]; }
+        st->sumr = rs;
+        st->rss = rr;
     }
 }
 

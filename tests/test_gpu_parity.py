@@ -136,30 +136,33 @@ def test_bedpp_safe_on_gpu_path():
 
 # ------------------------------------------------------------------ full paths
 
-def test_path_parity_cfg1():
+@pytest.mark.parametrize("cd", ["gram", "residual"])
+def test_path_parity_cfg1(cd):
     """BASELINE cfg1 at full size with its own tol (1e-7), 100 lambdas to 0.05."""
     inst = synth.cfg1()
     d = design(inst)
     lm = oracle.lambda_max(inst, inst.y)[0]
     lams = synth.lambda_grid(lm, 100, inst.ratio)
     op = oracle.fit_path(inst, inst.y, lams, alpha=1.0, tol=1e-10)
-    gp = d.fit_path(inst.y, lams, alpha=1.0, tol=inst.tol)
+    gp = d.fit_path(inst.y, lams, alpha=1.0, tol=inst.tol, cd=cd)
     compare_path(inst, gp, op, 1.0)
     assert np.all(gp.kkt_rounds >= 0)
 
 
-@pytest.mark.parametrize("dtype,alpha,screen", [
-    (np.float64, 1.0, "hybrid"), (np.float32, 1.0, "hybrid"), (np.int8, 1.0, "hybrid"),
-    (np.float32, 0.5, "hybrid"), (np.int8, 0.3, "hybrid"), (np.float64, 0.5, "ssr"),
-    (np.float32, 1.0, "none")])
-def test_path_parity_small(dtype, alpha, screen):
+@pytest.mark.parametrize("dtype,alpha,screen,cd", [
+    (np.float64, 1.0, "hybrid", "gram"), (np.float32, 1.0, "hybrid", "gram"), (np.int8, 1.0, "hybrid", "gram"),
+    (np.float32, 0.5, "hybrid", "gram"), (np.int8, 0.3, "hybrid", "gram"), (np.float64, 0.5, "ssr", "gram"),
+    (np.float32, 1.0, "none", "gram"), (np.float64, 1.0, "hybrid", "residual"),
+    (np.float32, 0.5, "hybrid", "residual"), (np.int8, 1.0, "hybrid", "residual"),
+    (np.float32, 1.0, "none", "residual")])
+def test_path_parity_small(dtype, alpha, screen, cd):
     kind = "geno" if dtype == np.int8 else "corr"
     inst = synth.random_instance(157, 613, dtype=dtype, seed=17, kind=kind, const_cols=4, n_true=12)
     d = design(inst)
     lm = oracle.lambda_max(inst, inst.y, alpha)[0]
     lams = synth.lambda_grid(lm, 40, 0.05)
     op = oracle.fit_path(inst, inst.y, lams, alpha=alpha, tol=1e-11)
-    gp = d.fit_path(inst.y, lams, alpha=alpha, tol=1e-9, screen=screen)
+    gp = d.fit_path(inst.y, lams, alpha=alpha, tol=1e-9, screen=screen, cd=cd)
     compare_path(inst, gp, op, alpha)
     # a0 / original scale (Q4)
     c, s = oracle.column_stats(inst)
@@ -257,16 +260,17 @@ def test_deterministic_repeat():
 
 # ------------------------------------------------------------------ a12 cross-validation
 
-@pytest.mark.parametrize("dtype,alpha", [(np.float64, 1.0), (np.int8, 0.5)])
-def test_cv_parity(dtype, alpha):
+@pytest.mark.parametrize("dtype,alpha,cd", [(np.float64, 1.0, "gram"), (np.int8, 0.5, "gram"),
+                                           (np.float32, 0.5, "residual")])
+def test_cv_parity(dtype, alpha, cd):
     kind = "geno" if dtype == np.int8 else "iid"
-    inst = synth.random_instance(90, 150, dtype=dtype, seed=53, kind=kind, n_true=6)
+    inst = synth.random_instance(90, 150, dtype=dtype, seed=53, kind=kind, n_true=6, const_cols=1)
     K = 5
     f = oracle.folds(inst.n, K, 1234)
     lm = oracle.lambda_max(inst, inst.y, alpha)[0]
     lams = synth.lambda_grid(lm, 20, 0.05)
     E, cve, cvse, lmin = oracle.cv(inst, inst.y, f, K, lams, alpha=alpha, tol=1e-12)
-    g = design(inst).cv(inst.y, lams, K=K, alpha=alpha, tol=1e-10, seed=1234)
+    g = design(inst).cv(inst.y, lams, K=K, alpha=alpha, tol=1e-10, seed=1234, cd=cd)
     assert np.array_equal(g.fold_id, f)            # same counter-based permutation (Q18)
     np.testing.assert_allclose(g.E, E, rtol=1e-6, atol=1e-9 * E.max())
     np.testing.assert_allclose(g.cve, cve, rtol=1e-7)
