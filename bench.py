@@ -191,6 +191,8 @@ def run_ours(args, rank, world, local_rank):
     scan_launches = sum(p.perf["scan_launches"] for p in perfs)
     cd_ms = sum(p.perf["cd_ms"] for p in perfs)
     launches = sum(p.perf["kernel_launches"] for p in perfs)
+    visits = sum(p.perf["cd_visits"] for p in perfs) / args.steps
+    updates = sum(p.perf["cd_updates"] for p in perfs) / args.steps
 
     # end to end through the C ABI with HOST buffers (H2D of X inside the timed region)
     Xh_t = torch.empty(X.shape, dtype=X.dtype, pin_memory=True)
@@ -238,7 +240,9 @@ def run_ours(args, rank, world, local_rank):
                      "achieved": achieved, "peak": pk["hbm_gbs"], "peak_source": pk_src, "unit": "GB/s",
                      "frac": achieved / pk["hbm_gbs"] if achieved else None, "traffic": traffic,
                      "scan_ms_per_step": scan_ms / args.steps, "scan_launches_per_step": scan_launches / args.steps,
-                     "cd_ms_per_step": cd_ms / args.steps,
+                     "cd_ms_per_step": cd_ms / args.steps, "cd_visits_per_step": visits,
+                     "cd_updates_per_step": updates,
+                     "cd_ns_per_visit": cd_ms / args.steps * 1e6 / max(visits, 1),
                      "algorithmic_bytes_per_step": scan_bytes / args.steps},
         "cpu_baseline": cpu,
         "e2e": {"value": statistics.median(e2e), "unit": "s", "h2d_bytes_per_step": int(h2d),

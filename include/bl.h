@@ -87,6 +87,8 @@ typedef struct {
     double prep_bytes;
     int64_t kernel_launches;   /* every kernel this fit launched */
     double wall_ms;            /* host steady clock, entry to return */
+    int64_t cd_visits;         /* coordinate visits over the path (all passes) */
+    int64_t cd_updates;        /* visits that changed a coefficient */
 } bl_perf;
 
 /* ---- design ------------------------------------------------------------------

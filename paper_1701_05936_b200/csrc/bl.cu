@@ -94,6 +94,7 @@ struct bl_path {
     std::vector<int32_t> passes, kkt_rounds;
     std::vector<int64_t> cols_scanned;
     bl_perf perf;
+    int64_t cd_visits = 0, cd_updates = 0;
 };
 
 struct bl_cvres {
@@ -749,10 +750,12 @@ void solve_cd(bl_prep *pp, int nW, double lam, double alpha, double tol, int max
     ga.c = pp->c;
     ga.s = pp->s;
     ga.st = pp->st;
-    int T = (int)std::min<int64_t>(1024, round_up(std::max(nW, 32), 32));
+    int T = (int)std::min<int64_t>(512, round_up(std::max(nW, 32), 32));
     int KM = (nW + T - 1) / T;
-    const void *kern = KM <= 1 ? (const void *)k_cd_gram<1> : KM <= 2 ? (const void *)k_cd_gram<2>
-                                                                        : (const void *)k_cd_gram<4>;
+    const void *kern = KM <= 1   ? (const void *)k_cd_gram<1, 8>
+                       : KM <= 2 ? (const void *)k_cd_gram<2, 8>
+                       : KM <= 4 ? (const void *)k_cd_gram<4, 4>
+                                 : (const void *)k_cd_gram<8, 4>;
     size_t smem = (size_t)48 * nW + 16;
     size_t lim = allow_dyn_smem(kern);
     if (smem > lim) raise(BL_ERR_OOM, "Gram CD shared memory %zu > %zu", smem, lim);
@@ -849,6 +852,8 @@ bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, doubl
                 CK(cudaMemcpyAsync(pp->hst, pp->st, sizeof(RoundStatus), cudaMemcpyDeviceToHost, st));
                 CK(cudaStreamSynchronize(st));
                 passes += pp->hst->cd_passes;
+            out->cd_visits += pp->hst->cd_visits;
+            out->cd_updates += pp->hst->cd_updates;
                 if (pp->hst->cd_status) { status = BL_ERR_CONVERGENCE; break; }
                 break;
             }
@@ -875,6 +880,8 @@ bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, doubl
             CK(cudaMemcpyAsync(pp->hst, pp->st, sizeof(RoundStatus), cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
             passes += pp->hst->cd_passes;
+            out->cd_visits += pp->hst->cd_visits;
+            out->cd_updates += pp->hst->cd_updates;
             scanned += use_bedpp ? pp->hst->nscope : pp->hps.n_live;
             if (pp->hst->cd_status) { status = BL_ERR_CONVERGENCE; break; }
             if (pp->hst->nviol > 0) {
@@ -951,6 +958,8 @@ void finish_perf(bl_prep *pp, bl_path *out, double wall_ms) {
     pf.scan_bytes = (double)cols * (double)pp->d->n * itemsize(pp->d->dt);
     pf.prep_bytes = pp->prep_bytes;
     pf.kernel_launches = pp->launches;
+    pf.cd_visits = out->cd_visits;
+    pf.cd_updates = out->cd_updates;
     pf.wall_ms = wall_ms;
 }
 

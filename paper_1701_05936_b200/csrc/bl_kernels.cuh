@@ -39,6 +39,7 @@ struct RoundStatus {
     int cd_passes, cd_status, nnz, pad;
     double rss, sumr, l1, l2;
     double sum_v;      // sum of the quantised residual (int8 limb path)
+    long long cd_visits, cd_updates;   // coordinate visits / nonzero updates of the last solve
 };
 
 // ---------------------------------------------------------------- small helpers
@@ -706,6 +707,7 @@ __global__ void __launch_bounds__(RM >= 16 ? 1024 : 512, 1) k_cd(CdArgs a) {
     __syncthreads();
     const T *X = reinterpret_cast<const T *>(a.X);
     int passes = 0, status = 0, buf = 0;
+    long long visits = 0, updates = 0;
 
     // one sweep over slots list[0..len) (list == nullptr => 0..len)
     auto sweep = [&](const int *list, int len, double &dmax, double &bmax) {
@@ -713,6 +715,7 @@ __global__ void __launch_bounds__(RM >= 16 ? 1024 : 512, 1) k_cd(CdArgs a) {
         bmax = 0.0;
         if (len == 0) return;
         T xc[RM], xn[RM];
+        visits += len;
         int w = list ? list[0] : 0;
         {
             const T *col = X + (int64_t)Ws[w] * a.ld;
@@ -750,6 +753,7 @@ __global__ void __launch_bounds__(RM >= 16 ? 1024 : 512, 1) k_cd(CdArgs a) {
             const double bn = soft_threshold(z, a.lam_alpha) * a.inv_den;
             const double d = bn - b_old;
             if (d != 0.0) {
+                updates++;
                 const double f = d * isj;
 #pragma unroll
                 for (int k = 0; k < RM; k++)
@@ -844,6 +848,8 @@ __global__ void __launch_bounds__(RM >= 16 ? 1024 : 512, 1) k_cd(CdArgs a) {
         a.st->l1 = l1;
         a.st->l2 = l2;
         a.st->nnz = (int)nnz;
+        a.st->cd_visits = visits;
+        a.st->cd_updates = updates;
     }
 }
 
@@ -912,8 +918,8 @@ struct CdGramArgs {
     RoundStatus *st;
 };
 
-template <int KM>
-__global__ void __launch_bounds__(1024, 1) k_cd_gram(CdGramArgs a) {
+template <int KM, int D>
+__global__ void __launch_bounds__(512, 1) k_cd_gram(CdGramArgs a) {
     extern __shared__ __align__(16) double sm[];
     __shared__ int wcount[33];
     __shared__ double red[32];
@@ -931,33 +937,37 @@ __global__ void __launch_bounds__(1024, 1) k_cd_gram(CdGramArgs a) {
     __syncthreads();
     double *gc = gA, *gn = gB, *bc = bA, *bnx = bB;     // current / next buffers
     int passes = 0, status = 0;
+    long long visits = 0, updates = 0;
 
+    // G rows are streamed from L2 through a D-deep register ring (row of list[q+i] in ring[i])
     auto sweep = [&](const int *list, int len, double &dmax, double &bmax) {
         dmax = 0.0;
         bmax = 0.0;
-        double r0[KM], r1[KM], r2[KM];      // G rows of list[q], list[q+1], list[q+2]
+        double ring[D][KM];
         auto load_row = [&](double (&row)[KM], int qq) {
             if (qq < len) {
                 const double *gr = a.G + (int64_t)list[qq] * a.ldG;
 #pragma unroll
-                for (int m = 0; m < KM; m++) { int k = t + m * T_; row[m] = k < nW ? gr[k] : 0.0; }
+                for (int m = 0; m < KM; m++) { int k = t + m * T_; row[m] = k < nW ? __ldcg(gr + k) : 0.0; }
             }
         };
-        load_row(r0, 0);
-        load_row(r1, 1);
+#pragma unroll
+        for (int i = 0; i < D - 1; i++) load_row(ring[i], i);
+        visits += len;
         for (int q = 0; q < len; q++) {
-            load_row(r2, q + 2);
+            load_row(ring[D - 1], q + D - 1);
             const int w = list[q];
             const double b_old = bc[w];
             const double zz = gc[w] + b_old;
             const double bn = soft_threshold(zz, a.lam_alpha) * a.inv_den;
             const double d = bn - b_old;
             if (d != 0.0) {                  // uniform branch: every thread computed the same d
+                updates++;
 #pragma unroll
                 for (int m = 0; m < KM; m++) {
                     int k = t + m * T_;
                     if (k < nW) {
-                        gn[k] = fma(-d, r0[m], gc[k]);
+                        gn[k] = fma(-d, ring[0][m], gc[k]);
                         bnx[k] = k == w ? bn : bc[k];
                     }
                 }
@@ -968,7 +978,9 @@ __global__ void __launch_bounds__(1024, 1) k_cd_gram(CdGramArgs a) {
             dmax = fmax(dmax, fabs(d));
             bmax = fmax(bmax, fabs(bn));
 #pragma unroll
-            for (int m = 0; m < KM; m++) { r0[m] = r1[m]; r1[m] = r2[m]; }
+            for (int i = 0; i < D - 1; i++)
+#pragma unroll
+                for (int m = 0; m < KM; m++) ring[i][m] = ring[i + 1][m];
         }
         __syncthreads();
     };
@@ -1035,6 +1047,8 @@ __global__ void __launch_bounds__(1024, 1) k_cd_gram(CdGramArgs a) {
         a.st->l1 = l1;
         a.st->l2 = l2;
         a.st->nnz = (int)nnz;
+        a.st->cd_visits = visits;
+        a.st->cd_updates = updates;
     }
 }
 
