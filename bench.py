@@ -162,7 +162,7 @@ def run_ours(args, rank, world, local_rank):
     sh = stream.cuda_stream
 
     def step(profile):
-        return d.fit_path(inst.y, lams, alpha=inst.alpha, tol=inst.tol, stream=sh, profile=profile)
+        return d.fit_path(inst.y, lams, alpha=inst.alpha, tol=inst.tol, stream=sh, profile=profile, cd=args.cd)
 
     for _ in range(args.warmup):
         step(False)
@@ -233,7 +233,7 @@ def run_ours(args, rank, world, local_rank):
         "data": "synthetic",
         "config": {"workload": args.config, "n": inst.n, "p": inst.p, "alpha": inst.alpha,
                    "n_lambda": inst.nlam, "lambda_min_ratio": inst.ratio, "tol": inst.tol,
-                   "screen": "hybrid (SSR-BEDPP)", "X_bytes": int(X.numel() * X.element_size()),
+                   "screen": "hybrid (SSR-BEDPP)", "cd": args.cd, "X_bytes": int(X.numel() * X.element_size()),
                    "l2_policy": "X larger than L2 (126 MB); no flush" if X.numel() * X.element_size() > 126e6
                    else "X fits L2 (reported as such)", "parallelism": f"replicas x{world}"},
         "roofline": {"kernel": "k_scan_fp/k_scan_i8 (fused KKT + strong-rule scan)", "bound": "hbm",
@@ -265,6 +265,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=15.0)
+    ap.add_argument("--cd", default="auto", choices=["auto", "residual", "gram"],
+                    help="CD flavour: residual updates (r on chip) or covariance updates (NEXT-2)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))

@@ -709,63 +709,66 @@ __global__ void __launch_bounds__(RM >= 16 ? 1024 : 512, 1) k_cd(CdArgs a) {
     int passes = 0, status = 0, buf = 0;
     long long visits = 0, updates = 0;
 
-    // one sweep over slots list[0..len) (list == nullptr => 0..len)
+    // one sweep over slots list[0..len) (list == nullptr => 0..len).  Columns
+    // stream through a 2-deep register ring (loop unrolled by 2: buffer u is
+    // consumed at step q and refilled with column q + 2).
     auto sweep = [&](const int *list, int len, double &dmax, double &bmax) {
         dmax = 0.0;
         bmax = 0.0;
         if (len == 0) return;
-        T xc[RM], xn[RM];
+        T xb[2][RM];
         visits += len;
-        int w = list ? list[0] : 0;
-        {
-            const T *col = X + (int64_t)Ws[w] * a.ld;
+        auto load_col = [&](T (&x)[RM], int qq) {
+            if (qq < len) {
+                const T *col = X + (int64_t)Ws[list ? list[qq] : qq] * a.ld;
 #pragma unroll
-            for (int k = 0; k < RM; k++) { int i = t + k * T_; xc[k] = (k < R && i < n) ? col[i] : T(0); }
-        }
-        for (int q = 0; q < len; q++) {
-            int wn = w;
-            if (q + 1 < len) {                      // prefetch the next column
-                wn = list ? list[q + 1] : q + 1;
-                const T *col = X + (int64_t)Ws[wn] * a.ld;
-#pragma unroll
-                for (int k = 0; k < RM; k++) { int i = t + k * T_; xn[k] = (k < R && i < n) ? col[i] : T(0); }
+                for (int k = 0; k < RM; k++) { int i = t + k * T_; x[k] = (k < R && i < n) ? col[i] : T(0); }
             }
-            const double b_old = bw[w], cj = cw[w], isj = iw[w];
-            double p0 = 0.0, p1 = 0.0;
+        };
+        load_col(xb[0], 0);
+        load_col(xb[1], 1);
+        for (int q0 = 0; q0 < len; q0 += 2) {
 #pragma unroll
-            for (int k = 0; k < RM; k += 2) {
-                if ((mbits >> k) & 1u) p0 = fma(to_d(xc[k]) - cj, rr[k], p0);
-                if (k + 1 < RM && ((mbits >> (k + 1)) & 1u)) p1 = fma(to_d(xc[k + 1]) - cj, rr[k + 1], p1);
-            }
-            double pt = warp_sum(p0 + p1);
-            if (lane == 0) part[buf][wid] = pt;
-            __syncthreads();
-            double s0 = 0.0, s1 = 0.0;
-            int u = 0;
-            for (; u + 3 < nw; u += 4) {
-                double2 h0 = *reinterpret_cast<const double2 *>(&part[buf][u]);
-                double2 h1 = *reinterpret_cast<const double2 *>(&part[buf][u + 2]);
-                s0 += h0.x + h0.y;
-                s1 += h1.x + h1.y;
-            }
-            for (; u < nw; u++) s0 += part[buf][u];
-            const double z = (s0 + s1) * a.inv_n * isj + b_old;
-            const double bn = soft_threshold(z, a.lam_alpha) * a.inv_den;
-            const double d = bn - b_old;
-            if (d != 0.0) {
-                updates++;
-                const double f = d * isj;
+            for (int u = 0; u < 2; u++) {
+                const int q = q0 + u;
+                if (q < len) {
+                    const int w = list ? list[q] : q;
+                    const double b_old = bw[w], cj = cw[w], isj = iw[w];
+                    double p0 = 0.0, p1 = 0.0;
 #pragma unroll
-                for (int k = 0; k < RM; k++)
-                    if (k < R) rr[k] = fma(-f, to_d(xc[k]) - cj, rr[k]);
-                if (t == 0) bw[w] = bn;
-            }
-            dmax = fmax(dmax, fabs(d));
-            bmax = fmax(bmax, fabs(bn));
-            buf ^= 1;
-            w = wn;
+                    for (int k = 0; k < RM; k += 2) {
+                        if ((mbits >> k) & 1u) p0 = fma(to_d(xb[u][k]) - cj, rr[k], p0);
+                        if (k + 1 < RM && ((mbits >> (k + 1)) & 1u)) p1 = fma(to_d(xb[u][k + 1]) - cj, rr[k + 1], p1);
+                    }
+                    double pt = warp_sum(p0 + p1);
+                    if (lane == 0) part[buf][wid] = pt;
+                    __syncthreads();
+                    double s0 = 0.0, s1 = 0.0;
+                    int v = 0;
+                    for (; v + 3 < nw; v += 4) {
+                        double2 h0 = *reinterpret_cast<const double2 *>(&part[buf][v]);
+                        double2 h1 = *reinterpret_cast<const double2 *>(&part[buf][v + 2]);
+                        s0 += h0.x + h0.y;
+                        s1 += h1.x + h1.y;
+                    }
+                    for (; v < nw; v++) s0 += part[buf][v];
+                    const double z = (s0 + s1) * a.inv_n * isj + b_old;
+                    const double bn = soft_threshold(z, a.lam_alpha) * a.inv_den;
+                    const double d = bn - b_old;
+                    if (d != 0.0) {
+                        updates++;
+                        const double f = d * isj;
 #pragma unroll
-            for (int k = 0; k < RM; k++) xc[k] = xn[k];
+                        for (int k = 0; k < RM; k++)
+                            if (k < R) rr[k] = fma(-f, to_d(xb[u][k]) - cj, rr[k]);
+                        if (t == 0) bw[w] = bn;
+                    }
+                    dmax = fmax(dmax, fabs(d));
+                    bmax = fmax(bmax, fabs(bn));
+                    buf ^= 1;
+                    load_col(xb[u], q + 2);
+                }
+            }
         }
         __syncthreads();     // bw visible before the next list build
     };
@@ -939,7 +942,9 @@ __global__ void __launch_bounds__(512, 1) k_cd_gram(CdGramArgs a) {
     int passes = 0, status = 0;
     long long visits = 0, updates = 0;
 
-    // G rows are streamed from L2 through a D-deep register ring (row of list[q+i] in ring[i])
+    // G rows stream from L2 through a D-deep register ring: the loop is unrolled
+    // by D so ring slot u is consumed at step q and refilled with row q + D --
+    // no register shuffling, so a load is only waited on D steps after issue.
     auto sweep = [&](const int *list, int len, double &dmax, double &bmax) {
         dmax = 0.0;
         bmax = 0.0;
@@ -952,35 +957,37 @@ __global__ void __launch_bounds__(512, 1) k_cd_gram(CdGramArgs a) {
             }
         };
 #pragma unroll
-        for (int i = 0; i < D - 1; i++) load_row(ring[i], i);
+        for (int i = 0; i < D; i++) load_row(ring[i], i);
         visits += len;
-        for (int q = 0; q < len; q++) {
-            load_row(ring[D - 1], q + D - 1);
-            const int w = list[q];
-            const double b_old = bc[w];
-            const double zz = gc[w] + b_old;
-            const double bn = soft_threshold(zz, a.lam_alpha) * a.inv_den;
-            const double d = bn - b_old;
-            if (d != 0.0) {                  // uniform branch: every thread computed the same d
-                updates++;
+        for (int q0 = 0; q0 < len; q0 += D) {
 #pragma unroll
-                for (int m = 0; m < KM; m++) {
-                    int k = t + m * T_;
-                    if (k < nW) {
-                        gn[k] = fma(-d, ring[0][m], gc[k]);
-                        bnx[k] = k == w ? bn : bc[k];
+            for (int u = 0; u < D; u++) {
+                const int q = q0 + u;
+                if (q < len) {
+                    const int w = list[q];
+                    const double b_old = bc[w];
+                    const double zz = gc[w] + b_old;
+                    const double bn = soft_threshold(zz, a.lam_alpha) * a.inv_den;
+                    const double d = bn - b_old;
+                    if (d != 0.0) {          // uniform branch: every thread computed the same d
+                        updates++;
+#pragma unroll
+                        for (int m = 0; m < KM; m++) {
+                            int k = t + m * T_;
+                            if (k < nW) {
+                                gn[k] = fma(-d, ring[u][m], gc[k]);
+                                bnx[k] = k == w ? bn : bc[k];
+                            }
+                        }
+                        __syncthreads();
+                        double *tg = gc; gc = gn; gn = tg;
+                        double *tb = bc; bc = bnx; bnx = tb;
                     }
+                    dmax = fmax(dmax, fabs(d));
+                    bmax = fmax(bmax, fabs(bn));
+                    load_row(ring[u], q + D);
                 }
-                __syncthreads();
-                double *tg = gc; gc = gn; gn = tg;
-                double *tb = bc; bc = bnx; bnx = tb;
             }
-            dmax = fmax(dmax, fabs(d));
-            bmax = fmax(bmax, fabs(bn));
-#pragma unroll
-            for (int i = 0; i < D - 1; i++)
-#pragma unroll
-                for (int m = 0; m < KM; m++) ring[i][m] = ring[i + 1][m];
         }
         __syncthreads();
     };
