@@ -193,6 +193,7 @@ def run_ours(args, rank, world, local_rank):
     launches = sum(p.perf["kernel_launches"] for p in perfs)
     visits = sum(p.perf["cd_visits"] for p in perfs) / args.steps
     updates = sum(p.perf["cd_updates"] for p in perfs) / args.steps
+    cd_cycles = sum(p.perf["cd_kernel_cycles"] for p in perfs) / args.steps
 
     # end to end through the C ABI with HOST buffers (H2D of X inside the timed region)
     Xh_t = torch.empty(X.shape, dtype=X.dtype, pin_memory=True)
@@ -243,6 +244,8 @@ def run_ours(args, rank, world, local_rank):
                      "cd_ms_per_step": cd_ms / args.steps, "cd_visits_per_step": visits,
                      "cd_updates_per_step": updates,
                      "cd_ns_per_visit": cd_ms / args.steps * 1e6 / max(visits, 1),
+                     "cd_kernel_cycles_per_visit": cd_cycles / max(visits, 1),
+                     "cd_kernel_ms_per_step": cd_cycles / 1.965e6,
                      "algorithmic_bytes_per_step": scan_bytes / args.steps},
         "cpu_baseline": cpu,
         "e2e": {"value": statistics.median(e2e), "unit": "s", "h2d_bytes_per_step": int(h2d),

@@ -89,6 +89,7 @@ typedef struct {
     double wall_ms;            /* host steady clock, entry to return */
     int64_t cd_visits;         /* coordinate visits over the path (all passes) */
     int64_t cd_updates;        /* visits that changed a coefficient */
+    int64_t cd_kernel_cycles;  /* SM cycles spent inside the CD kernels (clock64, thread 0) */
 } bl_perf;
 
 /* ---- design ------------------------------------------------------------------

@@ -48,7 +48,8 @@ class bl_perf(ctypes.Structure):
                 ("scan_launches", ctypes.c_int64), ("cd_ms", ctypes.c_double),
                 ("cd_launches", ctypes.c_int64), ("prep_ms", ctypes.c_double),
                 ("prep_bytes", ctypes.c_double), ("kernel_launches", ctypes.c_int64),
-                ("wall_ms", ctypes.c_double), ("cd_visits", ctypes.c_int64), ("cd_updates", ctypes.c_int64)]
+                ("wall_ms", ctypes.c_double), ("cd_visits", ctypes.c_int64), ("cd_updates", ctypes.c_int64),
+                ("cd_kernel_cycles", ctypes.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -94,7 +94,7 @@ struct bl_path {
     std::vector<int32_t> passes, kkt_rounds;
     std::vector<int64_t> cols_scanned;
     bl_perf perf;
-    int64_t cd_visits = 0, cd_updates = 0;
+    int64_t cd_visits = 0, cd_updates = 0, cd_cycles = 0;
 };
 
 struct bl_cvres {
@@ -234,8 +234,20 @@ double sum_events(std::vector<std::pair<cudaEvent_t, cudaEvent_t>> &v) {
 }
 
 int grid_for(const void *kern, int threads, size_t smem, int nsm) {
+    static std::mutex mu;
+    struct Key { const void *k; int t; size_t s; int occ; };
+    static std::vector<Key> cache;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        for (auto &e : cache)
+            if (e.k == kern && e.t == threads && e.s == smem) return e.occ * nsm;
+    }
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        cache.push_back({kern, threads, smem, occ});
+    }
     if (occ < 1) raise(BL_ERR_OOM, "kernel does not fit on an SM (smem %zu B)", smem);
     return occ * nsm;
 }
@@ -854,6 +866,7 @@ bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, doubl
                 passes += pp->hst->cd_passes;
             out->cd_visits += pp->hst->cd_visits;
             out->cd_updates += pp->hst->cd_updates;
+            out->cd_cycles += pp->hst->cd_cycles;
                 if (pp->hst->cd_status) { status = BL_ERR_CONVERGENCE; break; }
                 break;
             }
@@ -882,6 +895,7 @@ bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, doubl
             passes += pp->hst->cd_passes;
             out->cd_visits += pp->hst->cd_visits;
             out->cd_updates += pp->hst->cd_updates;
+            out->cd_cycles += pp->hst->cd_cycles;
             scanned += use_bedpp ? pp->hst->nscope : pp->hps.n_live;
             if (pp->hst->cd_status) { status = BL_ERR_CONVERGENCE; break; }
             if (pp->hst->nviol > 0) {
@@ -960,6 +974,7 @@ void finish_perf(bl_prep *pp, bl_path *out, double wall_ms) {
     pf.kernel_launches = pp->launches;
     pf.cd_visits = out->cd_visits;
     pf.cd_updates = out->cd_updates;
+    pf.cd_kernel_cycles = out->cd_cycles;
     pf.wall_ms = wall_ms;
 }
 

@@ -40,6 +40,7 @@ struct RoundStatus {
     double rss, sumr, l1, l2;
     double sum_v;      // sum of the quantised residual (int8 limb path)
     long long cd_visits, cd_updates;   // coordinate visits / nonzero updates of the last solve
+    long long cd_cycles;               // SM clock cycles inside the CD kernel (thread 0)
 };
 
 // ---------------------------------------------------------------- small helpers
@@ -706,6 +707,7 @@ __global__ void __launch_bounds__(RM >= 16 ? 1024 : 512, 1) k_cd(CdArgs a) {
     }
     __syncthreads();
     const T *X = reinterpret_cast<const T *>(a.X);
+    const long long clk0 = clock64();
     int passes = 0, status = 0, buf = 0;
     long long visits = 0, updates = 0;
 
@@ -853,6 +855,7 @@ __global__ void __launch_bounds__(RM >= 16 ? 1024 : 512, 1) k_cd(CdArgs a) {
         a.st->nnz = (int)nnz;
         a.st->cd_visits = visits;
         a.st->cd_updates = updates;
+        a.st->cd_cycles = clock64() - clk0;
     }
 }
 
@@ -939,6 +942,7 @@ __global__ void __launch_bounds__(512, 1) k_cd_gram(CdGramArgs a) {
     }
     __syncthreads();
     double *gc = gA, *gn = gB, *bc = bA, *bnx = bB;     // current / next buffers
+    const long long clk0 = clock64();
     int passes = 0, status = 0;
     long long visits = 0, updates = 0;
 
@@ -1056,6 +1060,7 @@ __global__ void __launch_bounds__(512, 1) k_cd_gram(CdGramArgs a) {
         a.st->nnz = (int)nnz;
         a.st->cd_visits = visits;
         a.st->cd_updates = updates;
+        a.st->cd_cycles = clock64() - clk0;
     }
 }
 
