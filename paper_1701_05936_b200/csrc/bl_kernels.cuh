@@ -913,7 +913,7 @@ struct CdGramArgs {
     const int *Wst;          // storage slot -> local column
     const int *ord;          // cyclic order (slots, ascending column)
     int nW, ldG;
-    const double *G;         // ldG x ldG, row-major by slot
+    const double *G;         // ldG x ldG, row-major by storage slot
     const double *z;         // z[j] = x~_j' r / n for the solve's starting residual
     double *beta;            // p entries (global, by local column)
     double *dbeta;           // nW entries out: beta_new - beta_old per slot
@@ -924,82 +924,105 @@ struct CdGramArgs {
     RoundStatus *st;
 };
 
-template <int KM, int D>
-__global__ void __launch_bounds__(512, 1) k_cd_gram(CdGramArgs a) {
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// 128 threads; thread t owns the slot pairs {2t + 256m, 2t + 256m + 1}.  The G
+// rows of the next D coordinates stream L2 -> shared memory with cp.async
+// (16 B per owned pair; completion counted per step with cp.async.wait_group,
+// so a row is waited on only D steps after it was requested).  One barrier per
+// NONZERO update; visits that leave beta_w unchanged cost no barrier at all.
+constexpr int kGramThreads = 128;
+template <int KP, int D>
+__global__ void __launch_bounds__(kGramThreads, 1) k_cd_gram(CdGramArgs a) {
     extern __shared__ __align__(16) double sm[];
     __shared__ int wcount[33];
     __shared__ double red[32];
-    const int T_ = blockDim.x, t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = T_ >> 5;
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = kGramThreads >> 5;
     const int nW = a.nW;
-    double *gA = sm, *gB = gA + nW, *bA = gB + nW, *bB = bA + nW, *b0 = bB + nW;
-    int *ord = reinterpret_cast<int *>(b0 + nW);
-    int *act = ord + nW;
-    for (int w = t; w < nW; w += T_) {
+    const int nWp = (nW + 1) & ~1;
+    double *gA = sm, *gB = gA + nWp, *bA = gB + nWp, *bB = bA + nWp;
+    double *ring = bB + nWp;                               // D stages x nWp
+    int *ord = reinterpret_cast<int *>(ring + (size_t)D * nWp);
+    int *act = ord + nWp;
+    for (int w = t; w < nW; w += kGramThreads) {
         int j = a.Wst[w];
         gA[w] = a.z[j];
-        bA[w] = b0[w] = a.beta[j];
+        double b = a.beta[j];
+        bA[w] = b;
+        a.dbeta[w] = -b;
         ord[w] = a.ord[w];
     }
     __syncthreads();
-    double *gc = gA, *gn = gB, *bc = bA, *bnx = bB;     // current / next buffers
+    double *gc = gA, *gn = gB, *bc = bA, *bnx = bB;
     const long long clk0 = clock64();
     int passes = 0, status = 0;
     long long visits = 0, updates = 0;
 
-    // G rows stream from L2 through a D-deep register ring: the loop is unrolled
-    // by D so ring slot u is consumed at step q and refilled with row q + D --
-    // no register shuffling, so a load is only waited on D steps after issue.
+    auto issue_row = [&](const int *list, int len, int qq) {
+        if (qq < len) {
+            const double *gr = a.G + (int64_t)list[qq] * a.ldG;
+            double *dst = ring + (size_t)(qq % D) * nWp;
+#pragma unroll
+            for (int m = 0; m < KP; m++) {
+                int k = 2 * t + 256 * m;
+                if (k < nW) cp_async16(dst + k, gr + k);
+            }
+        }
+        cp_commit();
+    };
+
     auto sweep = [&](const int *list, int len, double &dmax, double &bmax) {
         dmax = 0.0;
         bmax = 0.0;
-        double ring[D][KM];
-        auto load_row = [&](double (&row)[KM], int qq) {
-            if (qq < len) {
-                const double *gr = a.G + (int64_t)list[qq] * a.ldG;
 #pragma unroll
-                for (int m = 0; m < KM; m++) { int k = t + m * T_; row[m] = k < nW ? __ldcg(gr + k) : 0.0; }
-            }
-        };
-#pragma unroll
-        for (int i = 0; i < D; i++) load_row(ring[i], i);
+        for (int i = 0; i < D; i++) issue_row(list, len, i);
         visits += len;
-        for (int q0 = 0; q0 < len; q0 += D) {
+        for (int q = 0; q < len; q++) {
+            const int w = list[q];
+            const double b_old = bc[w];
+            const double zz = gc[w] + b_old;
+            const double bn = soft_threshold(zz, a.lam_alpha) * a.inv_den;
+            const double d = bn - b_old;
+            cp_wait<D - 1>();                  // row of list[q] has landed (own entries)
+            if (d != 0.0) {                    // uniform: every thread computed the same d
+                updates++;
+                const double *rw = ring + (size_t)(q % D) * nWp;
 #pragma unroll
-            for (int u = 0; u < D; u++) {
-                const int q = q0 + u;
-                if (q < len) {
-                    const int w = list[q];
-                    const double b_old = bc[w];
-                    const double zz = gc[w] + b_old;
-                    const double bn = soft_threshold(zz, a.lam_alpha) * a.inv_den;
-                    const double d = bn - b_old;
-                    if (d != 0.0) {          // uniform branch: every thread computed the same d
-                        updates++;
-#pragma unroll
-                        for (int m = 0; m < KM; m++) {
-                            int k = t + m * T_;
-                            if (k < nW) {
-                                gn[k] = fma(-d, ring[u][m], gc[k]);
-                                bnx[k] = k == w ? bn : bc[k];
-                            }
-                        }
-                        __syncthreads();
-                        double *tg = gc; gc = gn; gn = tg;
-                        double *tb = bc; bc = bnx; bnx = tb;
+                for (int m = 0; m < KP; m++) {
+                    int k = 2 * t + 256 * m;
+                    if (k < nW) {
+                        double2 gv = *reinterpret_cast<const double2 *>(gc + k);
+                        double2 rv = *reinterpret_cast<const double2 *>(rw + k);
+                        double2 bv = *reinterpret_cast<const double2 *>(bc + k);
+                        gv.x = fma(-d, rv.x, gv.x);
+                        gv.y = fma(-d, rv.y, gv.y);
+                        if (k == w) bv.x = bn;
+                        if (k + 1 == w) bv.y = bn;
+                        *reinterpret_cast<double2 *>(gn + k) = gv;
+                        *reinterpret_cast<double2 *>(bnx + k) = bv;
                     }
-                    dmax = fmax(dmax, fabs(d));
-                    bmax = fmax(bmax, fabs(bn));
-                    load_row(ring[u], q + D);
                 }
+                __syncthreads();
+                double *tg = gc; gc = gn; gn = tg;
+                double *tb = bc; bc = bnx; bnx = tb;
             }
+            dmax = fmax(dmax, fabs(d));
+            bmax = fmax(bmax, fabs(bn));
+            issue_row(list, len, q + D);       // refill this stage (own entries only)
         }
+        cp_wait<0>();
         __syncthreads();
     };
 
-    // ordered compaction of the nonzero slots (cyclic order) into act[]
     auto build_active = [&]() -> int {
         int total = 0;
-        for (int base = 0; base < nW; base += T_) {
+        for (int base = 0; base < nW; base += kGramThreads) {
             int q = base + t;
             int w = q < nW ? ord[q] : 0;
             bool nz = q < nW && bc[w] != 0.0;
@@ -1036,12 +1059,12 @@ __global__ void __launch_bounds__(512, 1) k_cd_gram(CdGramArgs a) {
     }
     __syncthreads();
     double l1 = 0.0, l2 = 0.0, nnz = 0.0;
-    for (int q = t; q < nW; q += T_) {
+    for (int q = t; q < nW; q += kGramThreads) {
         int w = ord[q];
         double b = bc[w];
         int j = a.Wst[w];
         a.beta[j] = b;
-        a.dbeta[w] = b - b0[w];
+        a.dbeta[w] += b;
         a.betaW_out[q] = b;
         a.betaW_out[nW + q] = a.c[j];
         a.betaW_out[2 * nW + q] = a.s[j];
