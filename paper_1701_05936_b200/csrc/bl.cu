@@ -762,7 +762,7 @@ void solve_cd(bl_prep *pp, int nW, double lam, double alpha, double tol, int max
     ga.c = pp->c;
     ga.s = pp->s;
     ga.st = pp->st;
-    // pairs per thread and prefetch depth (shared memory: 32 B/slot + D stages of 8 B/slot)
+    // pairs per thread and prefetch depth (shared memory: 16 B/slot + D stages of 8 B/slot)
     const int T = kGramThreads;
     const int KP = (nW + 255) / 256;
     const size_t nWp = (size_t)((nW + 1) & ~1);
@@ -779,7 +779,7 @@ void solve_cd(bl_prep *pp, int nW, double lam, double alpha, double tol, int max
     for (D = 8; D >= 2; D /= 2) {
         kern = pick(D);
         lim = allow_dyn_smem(kern);
-        smem = (size_t)8 * nWp * (4 + D) + (size_t)8 * nWp + 16;
+        smem = (size_t)8 * nWp * (1 + D) + (size_t)8 * nWp + 16;
         if (smem <= lim) break;
     }
     if (smem > lim) raise(BL_ERR_OOM, "Gram CD shared memory %zu > %zu (|W| = %d)", smem, lim, nW);

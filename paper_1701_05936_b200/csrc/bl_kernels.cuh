@@ -932,38 +932,72 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-// 128 threads; thread t owns the slot pairs {2t + 256m, 2t + 256m + 1}.  The G
-// rows of the next D coordinates stream L2 -> shared memory with cp.async
-// (16 B per owned pair; completion counted per step with cp.async.wait_group,
-// so a row is waited on only D steps after it was requested).  One barrier per
-// NONZERO update; visits that leave beta_w unchanged cost no barrier at all.
+// 128 threads; thread t owns the slot pairs {2t + 256m, 2t + 256m + 1} and keeps
+// their gradient g_k and coefficient b_k in REGISTERS.  Per coordinate w:
+//   every thread reads (z_w, b_w) from a broadcast cell written by w's owner,
+//   computes the same d = b'_w - b_w, updates its own g_k -= d G_wk with the G
+//   row streamed L2 -> shared memory by cp.async D coordinates ahead (waited on
+//   with cp.async.wait_group, so the prefetch is never serialised), and the owner
+//   of the NEXT coordinate publishes its (z, b) for the next step; one barrier.
+// Shared-memory traffic per coordinate is one G row (8 |W| bytes).
 constexpr int kGramThreads = 128;
 template <int KP, int D>
 __global__ void __launch_bounds__(kGramThreads, 1) k_cd_gram(CdGramArgs a) {
     extern __shared__ __align__(16) double sm[];
     __shared__ int wcount[33];
     __shared__ double red[32];
+    __shared__ double bc2[2][2];                           // broadcast (z, b) cells
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = kGramThreads >> 5;
     const int nW = a.nW;
     const int nWp = (nW + 1) & ~1;
-    double *gA = sm, *gB = gA + nWp, *bA = gB + nWp, *bB = bA + nWp;
-    double *ring = bB + nWp;                               // D stages x nWp
-    int *ord = reinterpret_cast<int *>(ring + (size_t)D * nWp);
+    double *ring = sm;                                     // D stages x nWp
+    double *bS = ring + (size_t)D * nWp;                   // beta snapshot (active-list builds)
+    int *ord = reinterpret_cast<int *>(bS + nWp);
     int *act = ord + nWp;
-    for (int w = t; w < nW; w += kGramThreads) {
-        int j = a.Wst[w];
-        gA[w] = a.z[j];
-        double b = a.beta[j];
-        bA[w] = b;
-        a.dbeta[w] = -b;
-        ord[w] = a.ord[w];
+    double2 g[KP], b[KP];
+#pragma unroll
+    for (int m = 0; m < KP; m++) {
+        int k = 2 * t + 256 * m;
+        g[m] = make_double2(0.0, 0.0);
+        b[m] = make_double2(0.0, 0.0);
+        if (k < nW) { int j = a.Wst[k]; g[m].x = a.z[j]; b[m].x = a.beta[j]; }
+        if (k + 1 < nW) { int j = a.Wst[k + 1]; g[m].y = a.z[j]; b[m].y = a.beta[j]; }
     }
-    __syncthreads();
-    double *gc = gA, *gn = gB, *bc = bA, *bnx = bB;
+    for (int w = t; w < nW; w += kGramThreads) ord[w] = a.ord[w];
     const long long clk0 = clock64();
     int passes = 0, status = 0;
     long long visits = 0, updates = 0;
 
+    // owner-side accessors of slot w (register arrays indexed at run time via unrolled selects)
+    auto owns = [&](int w) { return ((w & 255) >> 1) == t; };
+    auto get_gb = [&](int w, double &gz, double &bz) {
+        const int mw = w >> 8, hw = w & 1;
+#pragma unroll
+        for (int m = 0; m < KP; m++)
+            if (m == mw) { gz = hw ? g[m].y : g[m].x; bz = hw ? b[m].y : b[m].x; }
+    };
+    auto set_b = [&](int w, double v) {
+        const int mw = w >> 8, hw = w & 1;
+#pragma unroll
+        for (int m = 0; m < KP; m++)
+            if (m == mw) { if (hw) b[m].y = v; else b[m].x = v; }
+    };
+    auto publish = [&](int w, int cell) {
+        if (owns(w)) {
+            double gz = 0.0, bz = 0.0;
+            get_gb(w, gz, bz);
+            bc2[cell][0] = gz + bz;
+            bc2[cell][1] = bz;
+        }
+    };
+    auto snapshot_beta = [&]() {
+#pragma unroll
+        for (int m = 0; m < KP; m++) {
+            int k = 2 * t + 256 * m;
+            if (k < nW) bS[k] = b[m].x;
+            if (k + 1 < nW) bS[k + 1] = b[m].y;
+        }
+    };
     auto issue_row = [&](const int *list, int len, int qq) {
         if (qq < len) {
             const double *gr = a.G + (int64_t)list[qq] * a.ldG;
@@ -983,13 +1017,14 @@ __global__ void __launch_bounds__(kGramThreads, 1) k_cd_gram(CdGramArgs a) {
 #pragma unroll
         for (int i = 0; i < D; i++) issue_row(list, len, i);
         visits += len;
+        publish(list[0], 0);
+        __syncthreads();
         for (int q = 0; q < len; q++) {
             const int w = list[q];
-            const double b_old = bc[w];
-            const double zz = gc[w] + b_old;
+            const double zz = bc2[q & 1][0], b_old = bc2[q & 1][1];
             const double bn = soft_threshold(zz, a.lam_alpha) * a.inv_den;
             const double d = bn - b_old;
-            cp_wait<D - 1>();                  // row of list[q] has landed (own entries)
+            cp_wait<D - 1>();                  // G row of list[q] has landed (own entries)
             if (d != 0.0) {                    // uniform: every thread computed the same d
                 updates++;
                 const double *rw = ring + (size_t)(q % D) * nWp;
@@ -997,26 +1032,21 @@ __global__ void __launch_bounds__(kGramThreads, 1) k_cd_gram(CdGramArgs a) {
                 for (int m = 0; m < KP; m++) {
                     int k = 2 * t + 256 * m;
                     if (k < nW) {
-                        double2 gv = *reinterpret_cast<const double2 *>(gc + k);
                         double2 rv = *reinterpret_cast<const double2 *>(rw + k);
-                        double2 bv = *reinterpret_cast<const double2 *>(bc + k);
-                        gv.x = fma(-d, rv.x, gv.x);
-                        gv.y = fma(-d, rv.y, gv.y);
-                        if (k == w) bv.x = bn;
-                        if (k + 1 == w) bv.y = bn;
-                        *reinterpret_cast<double2 *>(gn + k) = gv;
-                        *reinterpret_cast<double2 *>(bnx + k) = bv;
+                        g[m].x = fma(-d, rv.x, g[m].x);
+                        g[m].y = fma(-d, rv.y, g[m].y);
                     }
                 }
-                __syncthreads();
-                double *tg = gc; gc = gn; gn = tg;
-                double *tb = bc; bc = bnx; bnx = tb;
+                if (owns(w)) set_b(w, bn);
             }
             dmax = fmax(dmax, fabs(d));
             bmax = fmax(bmax, fabs(bn));
+            if (q + 1 < len) publish(list[q + 1], (q + 1) & 1);
             issue_row(list, len, q + D);       // refill this stage (own entries only)
+            __syncthreads();
         }
         cp_wait<0>();
+        snapshot_beta();
         __syncthreads();
     };
 
@@ -1025,7 +1055,7 @@ __global__ void __launch_bounds__(kGramThreads, 1) k_cd_gram(CdGramArgs a) {
         for (int base = 0; base < nW; base += kGramThreads) {
             int q = base + t;
             int w = q < nW ? ord[q] : 0;
-            bool nz = q < nW && bc[w] != 0.0;
+            bool nz = q < nW && bS[w] != 0.0;
             unsigned m = __ballot_sync(0xffffffffu, nz);
             if (lane == 0) wcount[wid] = __popc(m);
             __syncthreads();
@@ -1042,6 +1072,8 @@ __global__ void __launch_bounds__(kGramThreads, 1) k_cd_gram(CdGramArgs a) {
         return total;
     };
 
+    snapshot_beta();
+    __syncthreads();
     for (;;) {
         for (;;) {
             int na = build_active();
@@ -1058,19 +1090,21 @@ __global__ void __launch_bounds__(kGramThreads, 1) k_cd_gram(CdGramArgs a) {
         if (dmax <= a.tol * bmax || dmax <= a.floor_) break;
     }
     __syncthreads();
+    // write back (bS holds the final coefficients after the last sweep)
     double l1 = 0.0, l2 = 0.0, nnz = 0.0;
     for (int q = t; q < nW; q += kGramThreads) {
         int w = ord[q];
-        double b = bc[w];
+        double bv = bS[w];
         int j = a.Wst[w];
-        a.beta[j] = b;
-        a.dbeta[w] += b;
-        a.betaW_out[q] = b;
+        double b0 = a.beta[j];
+        a.beta[j] = bv;
+        a.dbeta[w] = bv - b0;
+        a.betaW_out[q] = bv;
         a.betaW_out[nW + q] = a.c[j];
         a.betaW_out[2 * nW + q] = a.s[j];
-        l1 += fabs(b);
-        l2 = fma(b, b, l2);
-        nnz += b != 0.0 ? 1.0 : 0.0;
+        l1 += fabs(bv);
+        l2 = fma(bv, bv, l2);
+        nnz += bv != 0.0 ? 1.0 : 0.0;
     }
     l1 = block_sum(l1, red);
     l2 = block_sum(l2, red);
