@@ -194,6 +194,7 @@ def run_ours(args, rank, world, local_rank):
     visits = sum(p.perf["cd_visits"] for p in perfs) / args.steps
     updates = sum(p.perf["cd_updates"] for p in perfs) / args.steps
     cd_cycles = sum(p.perf["cd_kernel_cycles"] for p in perfs) / args.steps
+    cd_prof = [sum(p.perf["cd_prof"][u] for p in perfs) / args.steps / max(visits, 1) for u in range(4)]
 
     # end to end through the C ABI with HOST buffers (H2D of X inside the timed region)
     Xh_t = torch.empty(X.shape, dtype=X.dtype, pin_memory=True)
@@ -246,6 +247,7 @@ def run_ours(args, rank, world, local_rank):
                      "cd_ns_per_visit": cd_ms / args.steps * 1e6 / max(visits, 1),
                      "cd_kernel_cycles_per_visit": cd_cycles / max(visits, 1),
                      "cd_kernel_ms_per_step": cd_cycles / 1.965e6,
+                     "cd_phase_cycles_per_visit": dict(zip(["prefetch_wait", "barrier", "sweep_setup", "active_build"], cd_prof)),
                      "algorithmic_bytes_per_step": scan_bytes / args.steps},
         "cpu_baseline": cpu,
         "e2e": {"value": statistics.median(e2e), "unit": "s", "h2d_bytes_per_step": int(h2d),

@@ -49,7 +49,14 @@ class bl_perf(ctypes.Structure):
                 ("cd_launches", ctypes.c_int64), ("prep_ms", ctypes.c_double),
                 ("prep_bytes", ctypes.c_double), ("kernel_launches", ctypes.c_int64),
                 ("wall_ms", ctypes.c_double), ("cd_visits", ctypes.c_int64), ("cd_updates", ctypes.c_int64),
-                ("cd_kernel_cycles", ctypes.c_int64)]
+                ("cd_kernel_cycles", ctypes.c_int64), ("cd_prof", ctypes.c_int64 * 4)]
+
+    def as_dict(self):
+        d = {f: getattr(self, f) for f, _ in self._fields_}
+        d["cd_prof"] = list(self.cd_prof)
+        return d
+
+    def _unused(self):
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

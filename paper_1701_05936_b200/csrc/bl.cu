@@ -94,7 +94,7 @@ struct bl_path {
     std::vector<int32_t> passes, kkt_rounds;
     std::vector<int64_t> cols_scanned;
     bl_perf perf;
-    int64_t cd_visits = 0, cd_updates = 0, cd_cycles = 0;
+    int64_t cd_visits = 0, cd_updates = 0, cd_cycles = 0, cd_prof[4] = {0, 0, 0, 0};
 };
 
 struct bl_cvres {
@@ -879,6 +879,7 @@ bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, doubl
             out->cd_visits += pp->hst->cd_visits;
             out->cd_updates += pp->hst->cd_updates;
             out->cd_cycles += pp->hst->cd_cycles;
+            for (int u = 0; u < 4; u++) out->cd_prof[u] += pp->hst->cd_prof[u];
                 if (pp->hst->cd_status) { status = BL_ERR_CONVERGENCE; break; }
                 break;
             }
@@ -908,6 +909,7 @@ bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, doubl
             out->cd_visits += pp->hst->cd_visits;
             out->cd_updates += pp->hst->cd_updates;
             out->cd_cycles += pp->hst->cd_cycles;
+            for (int u = 0; u < 4; u++) out->cd_prof[u] += pp->hst->cd_prof[u];
             scanned += use_bedpp ? pp->hst->nscope : pp->hps.n_live;
             if (pp->hst->cd_status) { status = BL_ERR_CONVERGENCE; break; }
             if (pp->hst->nviol > 0) {
@@ -987,6 +989,7 @@ void finish_perf(bl_prep *pp, bl_path *out, double wall_ms) {
     pf.cd_visits = out->cd_visits;
     pf.cd_updates = out->cd_updates;
     pf.cd_kernel_cycles = out->cd_cycles;
+    for (int u = 0; u < 4; u++) pf.cd_prof[u] = out->cd_prof[u];
     pf.wall_ms = wall_ms;
 }
 

@@ -41,6 +41,7 @@ struct RoundStatus {
     double sum_v;      // sum of the quantised residual (int8 limb path)
     long long cd_visits, cd_updates;   // coordinate visits / nonzero updates of the last solve
     long long cd_cycles;               // SM clock cycles inside the CD kernel (thread 0)
+    long long cd_prof[4];              // Gram CD phase cycles (thread 0): cp wait, barrier, sweep setup, active builds
 };
 
 // ---------------------------------------------------------------- small helpers
@@ -967,6 +968,7 @@ __global__ void __launch_bounds__(kGramThreads, 1) k_cd_gram(CdGramArgs a) {
     const long long clk0 = clock64();
     int passes = 0, status = 0;
     long long visits = 0, updates = 0;
+    long long pr_cp = 0, pr_bar = 0, pr_setup = 0, pr_act = 0;
 
     // owner-side accessors of slot w (register arrays indexed at run time via unrolled selects)
     auto owns = [&](int w) { return ((w & 255) >> 1) == t; };
@@ -1014,17 +1016,21 @@ __global__ void __launch_bounds__(kGramThreads, 1) k_cd_gram(CdGramArgs a) {
     auto sweep = [&](const int *list, int len, double &dmax, double &bmax) {
         dmax = 0.0;
         bmax = 0.0;
+        long long c0 = clock64();
 #pragma unroll
         for (int i = 0; i < D; i++) issue_row(list, len, i);
         visits += len;
         publish(list[0], 0);
         __syncthreads();
+        pr_setup += clock64() - c0;
         for (int q = 0; q < len; q++) {
             const int w = list[q];
             const double zz = bc2[q & 1][0], b_old = bc2[q & 1][1];
             const double bn = soft_threshold(zz, a.lam_alpha) * a.inv_den;
             const double d = bn - b_old;
+            long long c1 = clock64();
             cp_wait<D - 1>();                  // G row of list[q] has landed (own entries)
+            pr_cp += clock64() - c1;
             if (d != 0.0) {                    // uniform: every thread computed the same d
                 updates++;
                 const double *rw = ring + (size_t)(q % D) * nWp;
@@ -1043,11 +1049,15 @@ __global__ void __launch_bounds__(kGramThreads, 1) k_cd_gram(CdGramArgs a) {
             bmax = fmax(bmax, fabs(bn));
             if (q + 1 < len) publish(list[q + 1], (q + 1) & 1);
             issue_row(list, len, q + D);       // refill this stage (own entries only)
+            long long c2 = clock64();
             __syncthreads();
+            pr_bar += clock64() - c2;
         }
+        long long c3 = clock64();
         cp_wait<0>();
         snapshot_beta();
         __syncthreads();
+        pr_setup += clock64() - c3;
     };
 
     auto build_active = [&]() -> int {
@@ -1076,7 +1086,9 @@ __global__ void __launch_bounds__(kGramThreads, 1) k_cd_gram(CdGramArgs a) {
     __syncthreads();
     for (;;) {
         for (;;) {
+            long long c4 = clock64();
             int na = build_active();
+            pr_act += clock64() - c4;
             if (na == 0) break;
             double dmax, bmax;
             sweep(act, na, dmax, bmax);
@@ -1118,6 +1130,10 @@ __global__ void __launch_bounds__(kGramThreads, 1) k_cd_gram(CdGramArgs a) {
         a.st->cd_visits = visits;
         a.st->cd_updates = updates;
         a.st->cd_cycles = clock64() - clk0;
+        a.st->cd_prof[0] = pr_cp;
+        a.st->cd_prof[1] = pr_bar;
+        a.st->cd_prof[2] = pr_setup;
+        a.st->cd_prof[3] = pr_act;
     }
 }
 
