@@ -56,10 +56,6 @@ class bl_perf(ctypes.Structure):
         d["cd_prof"] = list(self.cd_prof)
         return d
 
-    def _unused(self):
-
-    def as_dict(self):
-        return {f: getattr(self, f) for f, _ in self._fields_}
 
 
 _lib = None
