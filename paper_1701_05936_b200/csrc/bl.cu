@@ -711,8 +711,8 @@ void launch_resid_t(bl_prep *pp, int nW) {
 
 bool use_gram(bl_prep *pp, int nW) {
     if (pp->cd_mode == 1) return false;
-    if (nW > 4000) {
-        if (pp->cd_mode == 2) raise(BL_ERR_OOM, "Gram CD supports |W| <= 4000 (got %d)", nW);
+    if (nW > 4096) {
+        if (pp->cd_mode == 2) raise(BL_ERR_OOM, "Gram CD supports |W| <= 4096 (got %d)", nW);
         return false;
     }
     return true;
@@ -762,26 +762,14 @@ void solve_cd(bl_prep *pp, int nW, double lam, double alpha, double tol, int max
     ga.c = pp->c;
     ga.s = pp->s;
     ga.st = pp->st;
-    // pairs per thread and prefetch depth (shared memory: 16 B/slot + D stages of 8 B/slot)
-    const int T = kGramThreads;
-    const int KP = (nW + 255) / 256;
+    // 512 threads; each owns pairs 2t + 1024 m (KP pairs); shared memory 24 B per slot
+    const int T = kGram5Threads;
+    const int KP = (nW + 1023) / 1024;
     const size_t nWp = (size_t)((nW + 1) & ~1);
-    const void *kern = nullptr;
-    int D = 8;
-    auto pick = [&](int Dd) -> const void * {
-        if (KP <= 1) return Dd == 8 ? (const void *)k_cd_gram<1, 8> : Dd == 4 ? (const void *)k_cd_gram<1, 4> : (const void *)k_cd_gram<1, 2>;
-        if (KP <= 2) return Dd == 8 ? (const void *)k_cd_gram<2, 8> : Dd == 4 ? (const void *)k_cd_gram<2, 4> : (const void *)k_cd_gram<2, 2>;
-        if (KP <= 4) return Dd == 8 ? (const void *)k_cd_gram<4, 8> : Dd == 4 ? (const void *)k_cd_gram<4, 4> : (const void *)k_cd_gram<4, 2>;
-        if (KP <= 8) return Dd == 8 ? (const void *)k_cd_gram<8, 8> : Dd == 4 ? (const void *)k_cd_gram<8, 4> : (const void *)k_cd_gram<8, 2>;
-        return Dd == 8 ? (const void *)k_cd_gram<16, 8> : Dd == 4 ? (const void *)k_cd_gram<16, 4> : (const void *)k_cd_gram<16, 2>;
-    };
-    size_t smem = 0, lim = 0;
-    for (D = 8; D >= 2; D /= 2) {
-        kern = pick(D);
-        lim = allow_dyn_smem(kern);
-        smem = (size_t)8 * nWp * (1 + D) + (size_t)8 * nWp + 16;
-        if (smem <= lim) break;
-    }
+    const void *kern = KP <= 1 ? (const void *)k_cd_gram5<1> : KP <= 2 ? (const void *)k_cd_gram5<2>
+                                                                        : (const void *)k_cd_gram5<4>;
+    const size_t smem = (size_t)24 * nWp + 16;
+    const size_t lim = allow_dyn_smem(kern);
     if (smem > lim) raise(BL_ERR_OOM, "Gram CD shared memory %zu > %zu (|W| = %d)", smem, lim, nW);
     void *args[] = {&ga};
     CK(cudaLaunchKernel(kern, dim3(1), dim3(T), args, smem, pp->stream));
