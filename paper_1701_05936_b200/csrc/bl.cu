@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -781,7 +782,7 @@ void solve_cd(bl_prep *pp, int nW, double lam, double alpha, double tol, int max
 
 // One full path.  Fills `out` (prefix on convergence failure).
 bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, double tol, int max_iter, int screen,
-                   int max_rounds, bl_path *out, double *heldout /* K x n or nullptr */) {
+                   int max_rounds, bl_path *out, double *heldout /* device, n_lambda x n, or nullptr */) {
     bl_design *d = pp->d;
     cudaStream_t st = pp->stream;
     const double nt = pp->nt;
@@ -826,9 +827,11 @@ bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, doubl
             out->obj[k] = pp->hps.Y2 / (2.0 * nt);
             out->col_ptr[k + 1] = out->col_ptr[k];
             out->n_converged = k + 1;
-            if (heldout) {
-                // held-out residual of the null model: y_i - ybar_train (rfull is untouched at beta = 0)
-                CK(cudaMemcpyAsync(heldout + (size_t)k * d->n, pp->rfull, 8 * d->n, cudaMemcpyDeviceToHost, st));
+            if (heldout) {          // null model: rfull = y_i - ybar_train
+                k_heldout<<<(unsigned)((d->n + 255) / 256), 256, 0, st>>>(pp->rfull, pp->mask, (int)d->n,
+                                                                          heldout + (size_t)k * d->n);
+                CKL();
+                pp->launches++;
             }
             continue;
         }
@@ -943,8 +946,12 @@ bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, doubl
         out->passes[k] = passes;
         out->kkt_rounds[k] = rounds + (screen == BL_SCREEN_NONE ? 0 : 1);
         out->cols_scanned[k] = scanned;
-        if (heldout)
-            CK(cudaMemcpyAsync(heldout + (size_t)k * d->n, pp->rfull, 8 * d->n, cudaMemcpyDeviceToHost, st));
+        if (heldout) {
+            k_heldout<<<(unsigned)((d->n + 255) / 256), 256, 0, st>>>(pp->rfull, pp->mask, (int)d->n,
+                                                                      heldout + (size_t)k * d->n);
+            CKL();
+            pp->launches++;
+        }
         out->n_converged = k + 1;
         lam_prev = lam;
     }
@@ -1252,47 +1259,77 @@ bl_status bl_cv(bl_design *d, const double *y, const double *lambda, int n_lambd
         cv->fold_id = f;
         cv->E.assign((size_t)n_lambda * n, 0.0);
         cv->full = nullptr;
-        std::vector<double> held((size_t)n_lambda * n);
-        std::vector<uint8_t> train(n);
-        try {
-            for (int fo = 0; fo < n_folds && s == BL_OK; fo++) {
-                for (int64_t i = 0; i < n; i++) train[i] = f[i] != fo;
-                bl_status fs = BL_OK;
-                bl_path *pth = fit_impl(d, y, train.data(), lambda, n_lambda, alpha, tol, max_iter, BL_SCREEN_HYBRID,
-                                        opts, &fs, held.data());
-                int nc = pth->n_converged;
-                for (int k = 0; k < nc; k++)
-                    for (int64_t i = 0; i < n; i++)
-                        if (!train[i]) {
-                            double e = held[(size_t)k * n + i];
-                            cv->E[(size_t)k * n + i] = e * e;
-                        }
-                delete pth;
-                if (fs != BL_OK) s = fs;
+        CK(cudaSetDevice(d->device));
+        // device E (n_lambda x n): fold fits write disjoint held-out rows, so they run concurrently
+        double *dE = nullptr, *dcv = nullptr;
+        cudaError_t e = cudaMalloc(&dE, 8 * (size_t)n_lambda * n + 16 * (size_t)n_lambda);
+        if (e != cudaSuccess) { cudaGetLastError(); delete cv; raise(BL_ERR_OOM, "cudaMalloc for CV errors: %s", cudaGetErrorString(e)); }
+        dcv = dE + (size_t)n_lambda * n;
+        struct Free { double *p; ~Free() { if (p) cudaFree(p); } } fr{dE};
+        CK(cudaMemset(dE, 0, 8 * (size_t)n_lambda * n));
+        // fold-parallel: fold fits run concurrently on their own streams --
+        // each fit's CD kernel occupies one SM, so the folds share the GPU instead of queueing.
+        // With world > 1 ranks, fold f runs on rank f mod world (replicated X) and E is summed.
+        std::vector<int> mine;
+        for (int fo = 0; fo < n_folds; fo++)
+            if (fo % d->world == d->rank) mine.push_back(fo);
+        std::vector<bl_status> fst(mine.size() + 1, BL_OK);
+        std::vector<std::string> ferr(mine.size() + 1);
+        std::vector<bl_path *> full(1, nullptr);
+        bl_opts fo_opts{};
+        if (opts) fo_opts = *opts;
+        fo_opts.stream = nullptr;                       // each fold on its own library stream
+        auto run_fold = [&](size_t idx) {
+            try {
+                CK(cudaSetDevice(d->device));
+                if (idx < mine.size()) {
+                    std::vector<uint8_t> train(n);
+                    for (int64_t i = 0; i < n; i++) train[i] = f[i] != mine[idx];
+                    bl_status fs = BL_OK;
+                    bl_path *pth = fit_impl(d, y, train.data(), lambda, n_lambda, alpha, tol, max_iter,
+                                            BL_SCREEN_HYBRID, &fo_opts, &fs, dE);
+                    delete pth;
+                    fst[idx] = fs;
+                    if (fs != BL_OK) ferr[idx] = g_err;
+                } else {
+                    bl_status fs = BL_OK;
+                    full[0] = fit_impl(d, y, nullptr, lambda, n_lambda, alpha, tol, max_iter, BL_SCREEN_HYBRID,
+                                       &fo_opts, &fs);
+                    fst[idx] = fs;
+                    if (fs != BL_OK) ferr[idx] = g_err;
+                }
+            } catch (const Err &er) {
+                fst[idx] = er.code;
+                ferr[idx] = g_err;
+            } catch (const std::bad_alloc &) {
+                fst[idx] = BL_ERR_OOM;
+                ferr[idx] = "host allocation failed";
             }
-            if (s == BL_OK) {
-                bl_status fs = BL_OK;
-                cv->full = fit_impl(d, y, nullptr, lambda, n_lambda, alpha, tol, max_iter, BL_SCREEN_HYBRID, opts, &fs);
-                if (fs != BL_OK) s = fs;
-            }
-        } catch (...) {
-            delete cv->full;
-            delete cv;
-            throw;
+        };
+        {
+            std::vector<std::thread> th;
+            for (size_t idx = 0; idx <= mine.size(); idx++) th.emplace_back(run_fold, idx);
+            for (auto &t : th) t.join();
         }
+        cv->full = full[0];
+        for (size_t idx = 0; idx < fst.size(); idx++)
+            if (fst[idx] != BL_OK && s == BL_OK) { s = fst[idx]; g_err = ferr[idx]; }
+        CK(cudaDeviceSynchronize());
+        if (d->world > 1) {
+            std::lock_guard<std::mutex> lk(d->comm_mu);
+            CKN(ncclAllReduce(dE, dE, (size_t)n_lambda * n, ncclDouble, ncclSum, d->comm, 0));
+            CK(cudaStreamSynchronize(0));
+        }
+        k_cv_reduce<<<n_lambda, 256>>>(dE, (int)n, dcv, dcv + n_lambda);
+        CKL();
         cv->cve.assign(n_lambda, 0.0);
         cv->cvse.assign(n_lambda, 0.0);
-        int best = 0;
-        for (int k = 0; k < n_lambda; k++) {
-            double m = 0.0;
-            for (int64_t i = 0; i < n; i++) m += cv->E[(size_t)k * n + i];
-            m /= (double)n;
-            double v = 0.0;
-            for (int64_t i = 0; i < n; i++) { double dd = cv->E[(size_t)k * n + i] - m; v += dd * dd; }
-            cv->cve[k] = m;
-            cv->cvse[k] = std::sqrt(v / (double)(n - 1)) / std::sqrt((double)n);
+        CK(cudaMemcpy(cv->E.data(), dE, 8 * (size_t)n_lambda * n, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(cv->cve.data(), dcv, 8 * (size_t)n_lambda, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(cv->cvse.data(), dcv + n_lambda, 8 * (size_t)n_lambda, cudaMemcpyDeviceToHost));
+        int best = 0;                                   // lambda_min: lowest index on ties
+        for (int k = 1; k < n_lambda; k++)
             if (cv->cve[k] < cv->cve[best]) best = k;
-        }
         cv->lmin = best;
         *out = cv;
     });

@@ -1129,6 +1129,33 @@ __global__ void __launch_bounds__(kGram5Threads, 1) k_cd_gram5(CdGramArgs a) {
     }
 }
 
+// ------------------------------------------------ a12: cross-validation errors
+// E[i] = r_i^2 for the held-out rows (mask == 0) of one fold at one lambda:
+// r on held-out rows is y_i - yhat_i from the fold's fit (the CD keeps the full-row
+// residual), so no copy or gather of X is needed.
+__global__ void k_heldout(const double *__restrict__ r, const uint8_t *__restrict__ mask, int n,
+                          double *__restrict__ E) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && !mask[i]) E[i] = r[i] * r[i];
+}
+
+// cve_k = mean_i E[k, i];  cvse_k = sd_i(E[k, i]) / sqrt(n)  (Q17).  One block per lambda.
+__global__ void k_cv_reduce(const double *__restrict__ E, int n, double *__restrict__ cve,
+                            double *__restrict__ cvse) {
+    __shared__ double sh[32];
+    const double *e = E + (size_t)blockIdx.x * n;
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s += e[i];
+    const double m = block_sum(s, sh) / (double)n;
+    double v = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) { double d = e[i] - m; v = fma(d, d, v); }
+    v = block_sum(v, sh);
+    if (threadIdx.x == 0) {
+        cve[blockIdx.x] = m;
+        cvse[blockIdx.x] = sqrt(v / (double)(n - 1)) / sqrt((double)n);
+    }
+}
+
 // r -= X~_W dbeta on every row (held-out rows included); r_scan = r on used
 // rows.  Rows are split over blocks (deterministic order over slots); per-block
 // partial sums of r_scan and r_scan^2 go to `part` (finished by k_resid_finish).
