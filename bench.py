@@ -247,7 +247,7 @@ def run_ours(args, rank, world, local_rank):
                      "cd_ns_per_visit": cd_ms / args.steps * 1e6 / max(visits, 1),
                      "cd_kernel_cycles_per_visit": cd_cycles / max(visits, 1),
                      "cd_kernel_ms_per_step": cd_cycles / 1.965e6,
-                     "cd_phase_cycles_per_visit": dict(zip(["prefetch_wait", "barrier", "sweep_setup", "active_build"], cd_prof)),
+                     "cd_phase_cycles_per_visit": dict(zip(["lead", "bulk", "build_A", "catch_up"], cd_prof)),
                      "algorithmic_bytes_per_step": scan_bytes / args.steps},
         "cpu_baseline": cpu,
         "e2e": {"value": statistics.median(e2e), "unit": "s", "h2d_bytes_per_step": int(h2d),

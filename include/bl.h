@@ -90,7 +90,7 @@ typedef struct {
     int64_t cd_visits;         /* coordinate visits over the path (all passes) */
     int64_t cd_updates;        /* visits that changed a coefficient */
     int64_t cd_kernel_cycles;  /* SM cycles spent inside the CD kernels (clock64, thread 0) */
-    int64_t cd_prof[4];        /* Gram CD phases (cycles): prefetch waits, barriers, sweep setup, active builds */
+    int64_t cd_prof[4];        /* Gram CD phases (cycles): leader steps, bulk steps, G_AA / M builds, lazy catch-ups */
 } bl_perf;
 
 /* ---- design ------------------------------------------------------------------

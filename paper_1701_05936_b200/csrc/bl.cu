@@ -14,6 +14,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -146,6 +147,7 @@ struct bl_prep {
     int *Wst_d, *ord_d;     // Gram CD: storage slots (append order) and cyclic order
     double *dbeta;          // Gram CD: coefficient change per slot over one solve
     double *G;              // Gram CD: ldG x ldG, row-major by storage slot (HBM / L2)
+    double *GA;             // Gram CD workspace: G_AA (ldG x ldG) followed by the block inverses (32 ldG)
     int64_t ldG;
     int nG;                 // slots whose G row/column is computed
     double *rpart;          // per-block partials of the residual refresh
@@ -355,6 +357,7 @@ void free_prep(bl_prep *pp) {
     if (pp->hup) cudaFreeHost(pp->hup);
     if (pp->warena) cudaFree(pp->warena);
     if (pp->G) cudaFree(pp->G);
+    if (pp->GA) cudaFree(pp->GA);
     if (pp->own) cudaStreamDestroy(pp->own);
     pp->magic = MAGIC_DEAD;
     delete pp;
@@ -669,6 +672,31 @@ void launch_cd(bl_prep *pp, int nW, double lam, double alpha, double tol, int ma
 }
 
 // ---- NEXT-2 Gram CD (covariance updates) -------------------------------------
+// Workspace after G: G_AA (ldG^2), block inverses (32 ldG), then the cluster
+// kernel's global state: gradients, catch-up deltas (fp64), active list, catch-up
+// rows (int32), membership flags (bytes).
+size_t gram_ws_bytes(int64_t nl) { return (size_t)8 * nl * nl + (size_t)8 * 32 * nl + (size_t)8 * 2 * nl + (size_t)4 * 2 * nl + (size_t)nl + 64; }
+G7Work gram_ws(bl_prep *pp) {
+    const int64_t nl = pp->ldG;
+    double *base = pp->GA + nl * nl + 32 * nl;
+    G7Work w;
+    w.g = base;
+    w.dl = base + nl;
+    w.act = reinterpret_cast<int *>(base + 2 * nl);
+    w.rl = w.act + nl;
+    w.inA = reinterpret_cast<uint8_t *>(w.rl + nl);
+    return w;
+}
+
+// cluster size of the Gram CD kernel (CTA 0 leads, 1..R-1 own the gradients)
+int cd_cluster() {
+    static int r = [] {
+        const char *e = std::getenv("BL_CD_CLUSTER");
+        int v = e ? std::atoi(e) : 8;
+        return std::min(std::max(v, 2), (int)kG7MaxR);
+    }();
+    return r;
+}
 void ensure_G(bl_prep *pp, int64_t need) {
     if (need <= pp->ldG) return;
     int64_t nl = std::max<int64_t>(std::max<int64_t>(need, 2 * pp->ldG), 256);
@@ -682,6 +710,11 @@ void ensure_G(bl_prep *pp, int64_t need) {
     if (pp->G) { CK(cudaStreamSynchronize(pp->stream)); CK(cudaFree(pp->G)); }
     pp->G = G2;
     pp->ldG = nl;
+    // CD workspaces (contents need not survive): compact G_AA (ldG x ldG) + per-block inverses
+    if (pp->GA) CK(cudaFree(pp->GA));
+    pp->GA = nullptr;
+    e = cudaMalloc(&pp->GA, gram_ws_bytes(nl));
+    if (e != cudaSuccess) { cudaGetLastError(); pp->GA = nullptr; raise(BL_ERR_OOM, "cudaMalloc for the %lld^2 G_AA workspace: %s", (long long)nl, cudaGetErrorString(e)); }
 }
 
 template <typename T, bool M>
@@ -751,6 +784,8 @@ void solve_cd(bl_prep *pp, int nW, double lam, double alpha, double tol, int max
     ga.nW = nW;
     ga.ldG = (int)pp->ldG;
     ga.G = pp->G;
+    ga.GA = pp->GA;
+    ga.MA = pp->GA + pp->ldG * pp->ldG;
     ga.z = pp->z;
     ga.beta = pp->beta;
     ga.dbeta = pp->dbeta;
@@ -763,17 +798,28 @@ void solve_cd(bl_prep *pp, int nW, double lam, double alpha, double tol, int max
     ga.c = pp->c;
     ga.s = pp->s;
     ga.st = pp->st;
-    // 512 threads; each owns pairs 2t + 1024 m (KP pairs); shared memory 24 B per slot
-    const int T = kGram5Threads;
-    const int KP = (nW + 1023) / 1024;
-    const size_t nWp = (size_t)((nW + 1) & ~1);
-    const void *kern = KP <= 1 ? (const void *)k_cd_gram5<1> : KP <= 2 ? (const void *)k_cd_gram5<2>
-                                                                        : (const void *)k_cd_gram5<4>;
-    const size_t smem = (size_t)24 * nWp + 16;
+    // cluster Gram CD: R CTAs of 256 threads (CTA 0 leads, 1..R-1 own the gradients)
+    const int R = cd_cluster();
+    const void *kern = alpha < 1.0 ? (const void *)k_cd_gram7<true> : (const void *)k_cd_gram7<false>;
+    const size_t smem = gram7_smem(nW, R);
     const size_t lim = allow_dyn_smem(kern);
     if (smem > lim) raise(BL_ERR_OOM, "Gram CD shared memory %zu > %zu (|W| = %d)", smem, lim, nW);
-    void *args[] = {&ga};
-    CK(cudaLaunchKernel(kern, dim3(1), dim3(T), args, smem, pp->stream));
+    if (R > 8) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    G7Work wk = gram_ws(pp);
+    void *args[] = {&ga, &wk};
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(R);
+    cfg.blockDim = dim3(kG7Threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = pp->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = R;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelExC(&cfg, kern, args));
     pp->launches++;
     if (d->dt == DT_F64) M ? launch_resid_t<double, true>(pp, nW) : launch_resid_t<double, false>(pp, nW);
     else if (d->dt == DT_F32) M ? launch_resid_t<float, true>(pp, nW) : launch_resid_t<float, false>(pp, nW);

@@ -7,6 +7,7 @@
 // every kernel applies (x - c_j)/s_j on the fly or folds it into an epilogue
 // through identities (1)-(3).
 #pragma once
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -41,7 +42,9 @@ struct RoundStatus {
     double sum_v;      // sum of the quantised residual (int8 limb path)
     long long cd_visits, cd_updates;   // coordinate visits / nonzero updates of the last solve
     long long cd_cycles;               // SM clock cycles inside the CD kernel (thread 0)
-    long long cd_prof[4];              // Gram CD phase cycles (thread 0): cp wait, barrier, sweep setup, active builds
+    long long cd_prof[4];              // Gram CD phase cycles: leader steps, bulk steps, G_AA/M builds, lazy catch-ups
+    long long cd_cnt[4];               // Gram CD events: speculation retries, G_AA builds, catch-ups, full sweeps
+    long long cd_dbg[8];               // Gram CD sub-phase cycles (micro-benchmarks only)
 };
 
 // ---------------------------------------------------------------- small helpers
@@ -915,6 +918,8 @@ struct CdGramArgs {
     const int *ord;          // cyclic order (slots, ascending column)
     int nW, ldG;
     const double *G;         // ldG x ldG, row-major by storage slot
+    double *GA;              // workspace ldG x ldG: compact G_AA of the active set (v6)
+    double *MA;              // workspace ceil(nW/32) x 1024: per-block inverses M (v6)
     const double *z;         // z[j] = x~_j' r / n for the solve's starting residual
     double *beta;            // p entries (global, by local column)
     double *dbeta;           // nW entries out: beta_new - beta_old per slot
@@ -925,182 +930,481 @@ struct CdGramArgs {
     RoundStatus *st;
 };
 
-// Blocked Gram CD: the same cyclic coordinate updates in the same order as the
-// residual flavour (z = g_w + b_w, soft-threshold, g -= d G_w), with one CTA
-// barrier pair per block of 32 coordinates instead of a barrier per coordinate.
-// (A per-coordinate variant measured 1.4-2x slower: one barrier per coordinate
-// plus a serialised G-row stream.)  The gradient g and the
-// coefficients b of W live in shared memory:
-//   B. warp 0 runs the block's 32 coordinate updates sequentially -- lane b holds
-//      coordinate b's gradient and the G entries G[w_b'][w_b] linking it to the
-//      block's earlier coordinates, so an update is a shuffle-broadcast, the
-//      soft-threshold and one FMA per lane (no barrier);
-//   C. every thread applies the block's nonzero updates, in order, to the
-//      gradients it owns (pairs 2t + 2T m), streaming the 32 G rows from L2 in
-//      one batch of independent 16-byte loads.
-constexpr int kGram5Threads = 512;
-template <int KP>
-__global__ void __launch_bounds__(kGram5Threads, 1) k_cd_gram5(CdGramArgs a) {
+// Pipelined Gram CD (v6).  Same coordinate update as above (z = g_w + b_w,
+// b' = S(z, lambda alpha)/(1 + lambda(1 - alpha)), g -= (b' - b_w) G_w), cycling
+// the W slots in storage (append) order -- a fixed cyclic order like the
+// oracle's, so the fixed point is the same unique minimiser (Q6 tolerance).
+// A sweep is cut into blocks of 32 consecutive coordinates; one step per block,
+// ONE CTA barrier per step, two roles running concurrently:
+//   leader (warp 0, lane b <-> coordinate b of the block): brings the block's
+//     gradients up to date with block q-1's updates (dense 32 x 32 link Gp,
+//     prefetched), then resolves the block's 32 SEQUENTIAL updates by
+//     speculation: each coordinate's soft-threshold branch is predicted from
+//     its current coefficient (sign, or zero); under the prediction the 32
+//     updates solve a unit lower-triangular linear system, (I + inv N^T) d = r.
+//     In active sweeps the inverse M of that system is precomputed once per
+//     active set (it depends on G_AA and lambda only), so the block is one
+//     32 x 32 mat-vec d = M r; otherwise (full sweeps, or after a
+//     misprediction) forward substitution over the predicted-nonzero
+//     coordinates (per step: DADD, DADD, SHFL, DFMA).  Every coordinate's
+//     branch at its turn is then checked exactly; the prefix before the first
+//     mismatch is committed and the rest re-solved with the corrected branch,
+//     so the committed updates are the sequential ones;
+//   bulk (warps 1..): applies block q-1's nonzero updates to the other
+//     gradients of the sweep's coordinates (G rows streamed from L2 with
+//     coalesced 16-byte loads) and prefetches block q+1's sub-blocks.
+// Active sweeps run on a compact copy G_AA (and its per-block inverses M),
+// rebuilt only when the active set changes; gradients outside A are brought
+// up to date lazily (one G_A^T (b - b_start) product) before the next full
+// sweep or active-set change.  A sweep of Q blocks = Q + 2 steps (prefetch
+// prologue, Q steps, flush of the last block's updates).
+constexpr int kGram6Threads = 256;
+constexpr int kGram6Bulk = kGram6Threads - 32;
+constexpr int kGram6MBuild = 6;                 // warps building M (scratch = the 6 prefetch buffers)
+// dynamic shared memory: 6 x 8 KB buffers + 37 B per slot
+__host__ __device__ constexpr size_t gram6_smem(int nW) {
+    return (size_t)6 * 8192 + (size_t)37 * (size_t)((nW + 1) & ~1) + 64;
+}
+
+template <bool ENET>
+__global__ void __launch_bounds__(kGram6Threads, 1) k_cd_gram6(CdGramArgs a) {
     extern __shared__ __align__(16) double sm[];
+    __shared__ __align__(16) double dfull[2][32];      // the block's updates, dense by position (0 = none)
+    __shared__ __align__(16) double rsh[32];
+    __shared__ int bslot[2][32];
+    __shared__ double dvec[2][32];                     // the block's nonzero updates, compacted
+    __shared__ int drow[2][32];                        // ... and their rows in the sweep's matrix
+    __shared__ int nzc[2];
     __shared__ int wcount[33];
     __shared__ double red[32];
-    __shared__ int blk_w[2][32];
-    __shared__ double dvec[2][32];
-    __shared__ int nzc[2];
     __shared__ double convs[2];
-    constexpr int T_ = kGram5Threads;
+    constexpr int T_ = kGram6Threads;
+    constexpr unsigned FULL = 0xffffffffu;
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = T_ >> 5;
     const int nW = a.nW;
     const int nWp = (nW + 1) & ~1;
-    double *gS = sm;                                       // gradients of W (slot order)
-    double *bS = gS + nWp;                                 // coefficients of W
-    int *ord = reinterpret_cast<int *>(bS + nWp);
-    int *act = ord + nWp;
+    const int64_t ldG = a.ldG;
+    double(*Gd)[32][32] = reinterpret_cast<double(*)[32][32]>(sm);            // [2]: strictly lower diag sub-block
+    double(*Gp)[32][32] = Gd + 2;                                              // [2]: previous block -> this block
+    double(*Mb)[32][32] = Gd + 4;                                              // [2]: M, column-major ([c][b])
+    double *gS = sm + 6 * 1024;                             // gradients, by slot
+    double *bS = gS + nWp;                                  // coefficients, by slot
+    double *bcat = bS + nWp;                                // coefficients at the last lazy catch-up
+    int *act = reinterpret_cast<int *>(bcat + nWp);         // active slots (ascending)
+    int *actp = act + nWp;                                  // the set G_AA / M were built for
+    uint8_t *inA = reinterpret_cast<uint8_t *>(actp + nWp); // slot in actp
     for (int w = t; w < nWp; w += T_) {
         if (w < nW) {
-            int j = a.Wst[w];
+            const int j = a.Wst[w];
             gS[w] = a.z[j];
             bS[w] = a.beta[j];
-            ord[w] = a.ord[w];
         } else {
             gS[w] = 0.0;
             bS[w] = 0.0;
         }
+        inA[w] = 0;
     }
     __syncthreads();
     const long long clk0 = clock64();
     int passes = 0, status = 0;
-    long long visits = 0, updates = 0;
-    long long pr_b = 0, pr_c = 0;
+    long long visits = 0, updates = 0, pr_lead = 0, pr_bulk = 0, retries = 0, rebuilds = 0;
+    long long pr_build = 0, pr_catch = 0, ncatch = 0, nfull = 0;
+    const double la = a.lam_alpha, inv_den = a.inv_den;
 
-    auto sweep = [&](const int *list, int len, double &dmax, double &bmax) {
-        double dm = 0.0, bm = 0.0;                         // warp 0's running maxima
+    // bulk: prefetch block qn of the sweep (rows/cols = positions in matrix Mx with
+    // leading dimension ld) and the link from block qn-1; active sweeps also copy M.
+    // All loads of a thread are issued before its shared-memory stores.
+    auto prefetch = [&](const double *Mx, bool active, int len, int qn, int buf) {
+        const int u = t - 32;
+        const int b0 = 32 * qn, nb1 = min(32, len - b0);
+        const int nb0 = qn > 0 ? 32 : 0;                    // a previous block is always full
+        constexpr int NP = (3072 + kGram6Bulk - 1) / kGram6Bulk;
+        double v[NP];
+#pragma unroll
+        for (int k = 0; k < NP; k++) {
+            const int e = u + k * kGram6Bulk;
+            const int r = (e >> 5) & 31, c = e & 31;
+            const double *src = nullptr;
+            if (e < 1024) {
+                if (c > r && c < nb1) src = Mx + (int64_t)(b0 + r) * ldG + b0 + c;
+            } else if (e < 2048) {
+                if (r < nb0 && c < nb1) src = Mx + (int64_t)(b0 - 32 + r) * ldG + b0 + c;
+            } else if (e < 3072 && active) {
+                src = a.MA + (int64_t)qn * 1024 + (e - 2048);
+            }
+            v[k] = src ? __ldcg(src) : 0.0;          // G_AA / M are rewritten inside this kernel: L2 only
+        }
+#pragma unroll
+        for (int k = 0; k < NP; k++) {
+            const int e = u + k * kGram6Bulk;
+            if (e < 1024) (&Gd[buf][0][0])[e] = v[k];
+            else if (e < 2048) (&Gp[buf][0][0])[e - 1024] = v[k];
+            else if (e < 3072 && active) (&Mb[buf][0][0])[e - 2048] = v[k];
+        }
+        if (u < 32) bslot[buf][u] = u < nb1 ? (active ? act[b0 + u] : b0 + u) : -1;
+    };
+
+    // bulk: g -= sum_i d_i Mx[row_i][k] for the sweep's positions k (slot = act[k] in
+    // active sweeps) except the positions [lo, lo + 32) of the block in flight
+    auto apply = [&](const double *Mx, bool active, int len, int buf, int lo) {
+        const int nz = nzc[buf];
+        if (nz == 0) return;
+        const int u = t - 32;
+        for (int k = 2 * u; k < len; k += 2 * kGram6Bulk) {
+            const int s0 = active ? act[k] : k;
+            const int s1 = k + 1 < len ? (active ? act[k + 1] : k + 1) : s0;
+            double gx = gS[s0], gy = gS[s1];
+            for (int i0 = 0; i0 < nz; i0 += 16) {
+                double2 rv[16];
+                double dd[16];
+#pragma unroll
+                for (int v = 0; v < 16; v++) {           // unconditional (clamped) loads
+                    const int i = min(i0 + v, nz - 1);
+                    dd[v] = i0 + v < nz ? dvec[buf][i] : 0.0;
+                    rv[v] = __ldcg(reinterpret_cast<const double2 *>(Mx + (int64_t)drow[buf][i] * ldG + k));
+                }
+#pragma unroll
+                for (int v = 0; v < 16; v++) {
+                    gx = fma(-dd[v], rv[v].x, gx);
+                    gy = fma(-dd[v], rv[v].y, gy);
+                }
+            }
+            if (k < lo || k >= lo + 32) gS[s0] = gx;
+            if (k + 1 < len && (k + 1 < lo || k + 1 >= lo + 32)) gS[s1] = gy;
+        }
+    };
+
+    // leader warp: step of block q (buffers `cur`; previous block's updates in cur ^ 1)
+    double dm = 0.0, bm = 0.0;                              // per-lane running maxima (warp 0)
+    auto lead = [&](bool active, int b0, int cur) {
+        const int prv = cur ^ 1;
+        const int s = bslot[cur][lane];
+        const bool valid = s >= 0;
+        double zc = 0.0, bo = 0.0;
+        {
+            // z = g + b brought up to date with block q-1's updates (dense dot product)
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+            for (int r = 0; r < 32; r += 4) {
+                const double2 d01 = *reinterpret_cast<const double2 *>(&dfull[prv][r]);
+                const double2 d23 = *reinterpret_cast<const double2 *>(&dfull[prv][r + 2]);
+                a0 = fma(d01.x, Gp[cur][r][lane], a0);
+                a1 = fma(d01.y, Gp[cur][r + 1][lane], a1);
+                a2 = fma(d23.x, Gp[cur][r + 2][lane], a2);
+                a3 = fma(d23.y, Gp[cur][r + 3][lane], a3);
+            }
+            if (valid) {
+                const double g = gS[s] - ((a0 + a1) + (a2 + a3));
+                bo = bS[s];
+                gS[s] = g;
+                zc = g + bo;
+            }
+        }
+        const double(*GL)[32] = Gd[cur];
+        int pred = bo > 0.0 ? 1 : (bo < 0.0 ? -1 : 0);    // predicted soft-threshold branch
+        double dfin = 0.0, bnfin = bo;
+        unsigned todo = __ballot_sync(FULL, valid);
+        int round = 0;
+        if (active) {
+            // every coordinate of an active block is predicted nonzero: d = M r
+            const double las = pred > 0 ? la : -la;
+            rsh[lane] = valid ? (ENET ? (zc - las) * inv_den : zc - las) - bo : 0.0;
+            __syncwarp();
+            double m0 = 0.0, m1 = 0.0, m2 = 0.0, m3 = 0.0;
+#pragma unroll
+            for (int c = 0; c < 32; c += 4) {
+                const double2 r01 = *reinterpret_cast<const double2 *>(&rsh[c]);
+                const double2 r23 = *reinterpret_cast<const double2 *>(&rsh[c + 2]);
+                m0 = fma(Mb[cur][c][lane], r01.x, m0);
+                m1 = fma(Mb[cur][c + 1][lane], r01.y, m1);
+                m2 = fma(Mb[cur][c + 2][lane], r23.x, m2);
+                m3 = fma(Mb[cur][c + 3][lane], r23.y, m3);
+            }
+            const double d = (m0 + m1) + (m2 + m3);
+            const double bn = d + bo;
+            const unsigned mis = __ballot_sync(FULL, valid && !(pred > 0 ? bn > 0.0 : bn < 0.0));
+            const unsigned commit = todo & (mis ? ((1u << (__ffs(mis) - 1)) - 1u) : FULL);
+            if ((commit >> lane) & 1u) { dfin = d; bnfin = bn; }
+            todo &= ~commit;
+            if (mis) {
+                ++round;
+                unsigned cp = commit;                              // the committed prefix's updates -> zc
+                while (cp) {
+                    const int p = __ffs(cp) - 1;
+                    cp &= cp - 1;
+                    const double dp = __shfl_sync(FULL, dfin, p);
+                    zc = fma(-dp, GL[p][lane], zc);
+                }
+                if (lane == __ffs(mis) - 1) pred = zc > la ? 1 : (zc < -la ? -1 : 0);
+            }
+        }
+        while (todo) {
+            const unsigned Pm = __ballot_sync(FULL, pred != 0) & todo;
+            const double las = pred > 0 ? la : -la;
+            double z = zc;
+            unsigned rem = Pm;
+            while (rem) {                                     // forward substitution over predicted-nonzero
+                const int p = __ffs(rem) - 1;
+                rem &= rem - 1;
+                const double gl = GL[p][lane];
+                const double dl = (ENET ? (z - las) * inv_den : z - las) - bo;
+                const double dp = __shfl_sync(FULL, dl, p);
+                z = fma(-dp, gl, z);                          // lanes > p only (GL strictly lower)
+            }
+            // every lane's z is now its exact value at its turn, given the predictions before it
+            const bool hi = z > la, lo = z < -la;
+            const int tb = hi ? 1 : (lo ? -1 : 0);
+            const unsigned mis = __ballot_sync(FULL, tb != pred) & todo;
+            const unsigned below = mis ? ((1u << (__ffs(mis) - 1)) - 1u) : FULL;
+            const unsigned commit = todo & below;
+            if ((commit >> lane) & 1u) {
+                const double bn = hi ? z - la : (lo ? z + la : 0.0);
+                bnfin = ENET ? bn * inv_den : bn;
+                dfin = bnfin - bo;
+            }
+            todo &= ~commit;
+            if (!mis) break;
+            ++round;
+            const int m = __ffs(mis) - 1;
+            if (lane == m) pred = tb;                          // exact now: its z had every earlier update
+            unsigned cp = Pm & commit;                         // the committed prefix's updates -> zc
+            while (cp) {
+                const int p = __ffs(cp) - 1;
+                cp &= cp - 1;
+                const double dp = __shfl_sync(FULL, dfin, p);
+                zc = fma(-dp, GL[p][lane], zc);
+            }
+        }
+        retries += round;
+        dm = fmax(dm, fabs(dfin));
+        bm = fmax(bm, fabs(bnfin));
+        dfull[cur][lane] = dfin;
+        const bool nz = valid && dfin != 0.0;
+        if (valid) bS[s] = bnfin;
+        const unsigned msk = __ballot_sync(FULL, nz);
+        if (nz) {
+            const int pos = __popc(msk & ((1u << lane) - 1u));
+            dvec[cur][pos] = dfin;
+            drow[cur][pos] = b0 + lane;                    // row in the sweep's matrix (position)
+        }
+        if (lane == 0) nzc[cur] = __popc(msk);
+        updates += __popc(msk);
+    };
+
+    auto sweep = [&](bool active, int len, double &dmax, double &bmax) {
         visits += len;
-        int par = 0;
-        for (int q0 = 0; q0 < len; q0 += 32, par ^= 1) {
-            const int nb = min(32, len - q0);
-            // B: warp 0, sequential coordinate updates inside the block
+        const double *Mx = active ? a.GA : a.G;
+        const int Q = (len + 31) / 32;
+        if (wid == 0) { dm = 0.0; bm = 0.0; dfull[1][lane] = 0.0; }
+        if (t == 0) nzc[1] = 0;
+        if (wid > 0) prefetch(Mx, active, len, 0, 0);
+        __syncthreads();
+        for (int q = 0; q < Q; q++) {
+            const int cur = q & 1;
+            const long long c0 = clock64();
             if (wid == 0) {
-                long long cb = clock64();
-                const bool mine = lane < nb;
-                const int wl = list[q0 + min(lane, nb - 1)];       // clamped: every address valid
-                // lanes past the block end carry g = b = 0: their "update" is exactly 0 (no-op)
-                double gv = mine ? gS[wl] : 0.0, bv = mine ? bS[wl] : 0.0;
-                double Gs[32];                                // Gs[b'] = G[w_b'][w_lane]
-#pragma unroll
-                for (int bp = 0; bp < 32; bp++) {             // unconditional loads: no branch per load
-                    const int wb = __shfl_sync(0xffffffffu, wl, bp);
-                    Gs[bp] = __ldg(a.G + (int64_t)wb * a.ldG + wl);
-                }
-                double dl = 0.0;                              // this lane's coordinate's update
-#pragma unroll
-                for (int bp = 0; bp < 32; bp++) {             // branch-free: fma(-0, x, g) == g
-                    const double zb = __shfl_sync(0xffffffffu, gv + bv, bp);
-                    const double bo = __shfl_sync(0xffffffffu, bv, bp);
-                    const double bn = soft_threshold(zb, a.lam_alpha) * a.inv_den;
-                    const double d = bn - bo;
-                    gv = fma(-d, lane > bp ? Gs[bp] : 0.0, gv);
-                    bv = lane == bp ? bn : bv;
-                    dl = lane == bp ? d : dl;
-                    dm = fmax(dm, fabs(d));
-                    bm = fmax(bm, fabs(bn));
-                }
-                // compact the nonzero updates (order preserved) for phase C
-                const bool nz = mine && dl != 0.0;
-                const unsigned msk = __ballot_sync(0xffffffffu, nz);
-                if (nz) {
-                    const int pos = __popc(msk & ((1u << lane) - 1u));
-                    blk_w[par][pos] = wl;
-                    dvec[par][pos] = dl;
-                }
-                if (lane == 0) nzc[par] = __popc(msk);
-                if (mine) bS[wl] = bv;
-                updates += __popc(msk);
-                pr_b += clock64() - cb;
+                lead(active, 32 * q, cur);
+                if (t == 0) pr_lead += clock64() - c0;
+            } else {
+                apply(Mx, active, len, cur ^ 1, 32 * q);
+                if (q + 1 < Q) prefetch(Mx, active, len, q + 1, cur ^ 1);
+                if (t == 32) pr_bulk += clock64() - c0;
             }
-            __syncthreads();
-            long long cc = clock64();
-            // C: every thread applies the block's nonzero updates, in order, to its gradients
-            const int nzb = nzc[par];
-            if (nzb > 0) {
-#pragma unroll
-                for (int m = 0; m < KP; m++) {
-                    const int k = 2 * t + 2 * T_ * m;
-                    if (k < nW) {
-                        double2 gm = *reinterpret_cast<const double2 *>(gS + k);
-                        for (int i0 = 0; i0 < nzb; i0 += 16) {
-                            double2 rv[16];
-                            double dd[16];
-#pragma unroll
-                            for (int u = 0; u < 16; u++) {    // unconditional (clamped) loads
-                                const int i = min(i0 + u, nzb - 1);
-                                dd[u] = i0 + u < nzb ? dvec[par][i] : 0.0;
-                                rv[u] = __ldg(reinterpret_cast<const double2 *>(a.G + (int64_t)blk_w[par][i] * a.ldG + k));
-                            }
-#pragma unroll
-                            for (int u = 0; u < 16; u++) {
-                                gm.x = fma(-dd[u], rv[u].x, gm.x);
-                                gm.y = fma(-dd[u], rv[u].y, gm.y);
-                            }
-                        }
-                        *reinterpret_cast<double2 *>(gS + k) = gm;
-                    }
-                }
-            }
-            pr_c += clock64() - cc;
             __syncthreads();
         }
-        if (t == 0) { convs[0] = dm; convs[1] = bm; }
+        if (wid > 0) apply(Mx, active, len, (Q - 1) & 1, len);   // flush: the last block's updates everywhere
+        if (wid == 0) {
+            const double dmw = warp_max(dm), bmw = warp_max(bm);
+            if (t == 0) { convs[0] = dmw; convs[1] = bmw; }
+        }
         __syncthreads();
         dmax = convs[0];
         bmax = convs[1];
         __syncthreads();
     };
 
+    // order-preserving block compaction: rank of this thread among the nz ones in
+    // its chunk of T_ (returned in pos); returns the chunk's count
+    auto block_rank = [&](bool nz, int &pos) -> int {
+        const unsigned m = __ballot_sync(FULL, nz);
+        if (lane == 0) wcount[wid] = __popc(m);
+        __syncthreads();
+        if (t == 0) {
+            int run = 0;
+            for (int u = 0; u < nw; u++) { const int c0 = wcount[u]; wcount[u] = run; run += c0; }
+            wcount[32] = run;
+        }
+        __syncthreads();
+        pos = wcount[wid] + __popc(m & ((1u << lane) - 1u));
+        const int tot = wcount[32];
+        __syncthreads();
+        return tot;
+    };
+
     auto build_active = [&]() -> int {
         int total = 0;
         for (int base = 0; base < nW; base += T_) {
-            int q = base + t;
-            int w = q < nW ? ord[q] : 0;
-            bool nz = q < nW && bS[w] != 0.0;
-            unsigned m = __ballot_sync(0xffffffffu, nz);
-            if (lane == 0) wcount[wid] = __popc(m);
-            __syncthreads();
-            if (t == 0) {
-                int run = 0;
-                for (int u = 0; u < nw; u++) { int c0 = wcount[u]; wcount[u] = run; run += c0; }
-                wcount[32] = run;
-            }
-            __syncthreads();
-            if (nz) act[total + wcount[wid] + __popc(m & ((1u << lane) - 1u))] = w;
-            total += wcount[32];
-            __syncthreads();
+            const int w = base + t;
+            const bool nz = w < nW && bS[w] != 0.0;
+            int pos;
+            const int cnt = block_rank(nz, pos);
+            if (nz) act[total + pos] = w;
+            total += cnt;
         }
+        __syncthreads();
         return total;
     };
 
-    for (;;) {
-        for (;;) {
-            int na = build_active();
-            if (na == 0) break;
-            double dmax, bmax;
-            sweep(act, na, dmax, bmax);
-            if (++passes > a.max_iter) { status = 3; break; }
-            if (dmax <= a.tol * bmax || dmax <= a.floor_) break;
+    // G_AA = G[actp][actp] (compact, leading dimension ldG) and, per block of 32
+    // positions, M = (I + inv N^T)^-1 with N the block's strictly upper part
+    // (column c of M by lane c; scratch = the prefetch buffers)
+    auto build_A = [&](int na) {
+        const int64_t tot = (int64_t)na * na;
+        for (int64_t e0 = t; e0 < tot; e0 += 8 * T_) {     // 8 independent loads in flight per thread
+            double v[8];
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                const int64_t e = e0 + (int64_t)k * T_;
+                const int i = (int)(e / na), j = (int)(e - (int64_t)i * na);
+                v[k] = e < tot ? __ldg(a.G + (int64_t)actp[i] * ldG + actp[min(j, na - 1)]) : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                const int64_t e = e0 + (int64_t)k * T_;
+                const int i = (int)(e / na), j = (int)(e - (int64_t)i * na);
+                if (e < tot) a.GA[(int64_t)i * ldG + j] = v[k];
+            }
         }
-        if (status) break;
+        __threadfence_block();
+        __syncthreads();
+        const int nblk = (na + 31) / 32;
+        if (wid < kGram6MBuild) {
+            double(*N)[32] = Gd[wid];                       // scratch: 32 x 32, inv-scaled, strictly upper
+            for (int q = wid; q < nblk; q += kGram6MBuild) {
+                const int b0 = 32 * q, nb = min(32, na - b0);
+                for (int e = lane; e < 1024; e += 32) {
+                    const int p = e >> 5, b = e & 31;
+                    N[p][b] = (b > p && b < nb) ? inv_den * a.GA[(int64_t)(b0 + p) * ldG + b0 + b] : 0.0;
+                }
+                __syncwarp();
+                double x[32];
+#pragma unroll
+                for (int b = 0; b < 32; b++) x[b] = b == lane ? 1.0 : 0.0;
+#pragma unroll
+                for (int p = 0; p < 31; p++) {
+                    const double xp = x[p];
+#pragma unroll
+                    for (int b = (p + 1) & ~1; b < 32; b += 2) {
+                        const double2 nv = *reinterpret_cast<const double2 *>(&N[p][b]);
+                        if (b > p) x[b] = fma(-nv.x, xp, x[b]);
+                        x[b + 1] = fma(-nv.y, xp, x[b + 1]);
+                    }
+                }
+                double *dst = a.MA + (int64_t)q * 1024 + lane * 32;   // column lane: [c][b]
+#pragma unroll
+                for (int b = 0; b < 32; b += 2) *reinterpret_cast<double2 *>(dst + b) = make_double2(x[b], x[b + 1]);
+                __syncwarp();
+            }
+        }
+        __threadfence_block();
+        __syncthreads();
+    };
+
+    // lazy catch-up: gradients outside actp receive sum_i (b_i - bcat_i) G[actp_i][k]
+    auto catch_up = [&](int na) {
+        const long long c0 = clock64();
+        ++ncatch;
+        double *dl = sm;                                    // scratch (prefetch buffers): na deltas + rows
+        int *rl = reinterpret_cast<int *>(sm + 4096);
+        int nz = 0;
+        for (int base = 0; base < na; base += T_) {        // nonzero changes, in order (deterministic sums)
+            const int i = base + t;
+            const int sl = i < na ? actp[i] : 0;
+            const double dlt = i < na ? bS[sl] - bcat[sl] : 0.0;
+            int pos;
+            const int cnt = block_rank(dlt != 0.0, pos);
+            if (dlt != 0.0) { dl[nz + pos] = dlt; rl[nz + pos] = sl; }
+            nz += cnt;
+        }
+        __syncthreads();
+        if (nz > 0) {
+            for (int k = 2 * t; k < nW; k += 2 * T_) {
+                double gx = 0.0, gy = 0.0;
+                for (int i0 = 0; i0 < nz; i0 += 16) {
+                    double2 rv[16];
+                    double dd[16];
+#pragma unroll
+                    for (int v = 0; v < 16; v++) {
+                        const int i = min(i0 + v, nz - 1);
+                        dd[v] = i0 + v < nz ? dl[i] : 0.0;
+                        rv[v] = __ldcg(reinterpret_cast<const double2 *>(a.G + (int64_t)rl[i] * ldG + k));
+                    }
+#pragma unroll
+                    for (int v = 0; v < 16; v++) {
+                        gx = fma(dd[v], rv[v].x, gx);
+                        gy = fma(dd[v], rv[v].y, gy);
+                    }
+                }
+                if (!inA[k]) gS[k] -= gx;
+                if (k + 1 < nW && !inA[k + 1]) gS[k + 1] -= gy;
+            }
+        }
+        __syncthreads();
+        pr_catch += clock64() - c0;
+    };
+
+    // active cycling between full passes (one sweep call site: the leader code is
+    // inlined once); a fit is accepted only after a converged FULL pass over W
+    bool full = false, built = false, pending = false;
+    int na_built = 0;
+    for (;;) {
+        int len = nW;
+        if (!full) {
+            len = build_active();
+            bool same = built && len == na_built;
+            if (same) {
+                int diff = 0;
+                for (int i = t; i < len; i += T_) diff |= act[i] != actp[i];
+                same = !__syncthreads_or(diff);
+            }
+            if (!same) {
+                if (pending) { catch_up(na_built); pending = false; }
+                if (len == 0) { full = true; continue; }
+                for (int i = t; i < nWp; i += T_) inA[i] = 0;
+                __syncthreads();
+                for (int i = t; i < len; i += T_) { actp[i] = act[i]; inA[act[i]] = 1; }
+                __syncthreads();
+                const long long c0 = clock64();
+                build_A(len);
+                pr_build += clock64() - c0;
+                built = true;
+                na_built = len;
+                ++rebuilds;
+            }
+            if (!pending) {
+                for (int i = t; i < len; i += T_) bcat[act[i]] = bS[act[i]];
+                pending = true;
+                __syncthreads();
+            }
+        } else if (pending) {
+            catch_up(na_built);
+            pending = false;
+        }
         double dmax, bmax;
-        sweep(ord, nW, dmax, bmax);
+        nfull += full;
+        sweep(!full, len, dmax, bmax);
         if (++passes > a.max_iter) { status = 3; break; }
-        if (dmax <= a.tol * bmax || dmax <= a.floor_) break;
+        const bool conv = dmax <= a.tol * bmax || dmax <= a.floor_;
+        if (full && conv) break;
+        full = conv;
     }
     __syncthreads();
     double l1 = 0.0, l2 = 0.0, nnz = 0.0;
     for (int q = t; q < nW; q += T_) {
-        int w = ord[q];
-        double bv = bS[w];
-        int j = a.Wst[w];
-        double b0 = a.beta[j];
+        const int w = a.ord[q];
+        const double bv = bS[w];
+        const int j = a.Wst[w];
+        const double b0 = a.beta[j];
         a.beta[j] = bv;
         a.dbeta[w] = bv - b0;
         a.betaW_out[q] = bv;
@@ -1122,10 +1426,646 @@ __global__ void __launch_bounds__(kGram5Threads, 1) k_cd_gram5(CdGramArgs a) {
         a.st->cd_visits = visits;
         a.st->cd_updates = updates;
         a.st->cd_cycles = clock64() - clk0;
-        a.st->cd_prof[0] = 0;
-        a.st->cd_prof[1] = pr_b;
-        a.st->cd_prof[2] = pr_c;
-        a.st->cd_prof[3] = 0;
+        a.st->cd_prof[0] = pr_lead;
+        a.st->cd_prof[2] = pr_build;
+        a.st->cd_prof[3] = pr_catch;
+        a.st->cd_cnt[0] = retries;
+        a.st->cd_cnt[1] = rebuilds;
+        a.st->cd_cnt[2] = ncatch;
+        a.st->cd_cnt[3] = nfull;
+    }
+    if (t == 32) a.st->cd_prof[1] = pr_bulk;
+}
+
+// Cluster Gram CD (v7): the v6 algorithm above with its bulk spread over a
+// thread-block cluster.  One SM can only stream ~30-50 B/clk from L2, and the
+// bulk (every block's updates applied to every other gradient of the sweep)
+// reads |sweep| x 32 x 8 bytes of G per block -- so the gradients live in the
+// shared memory of CTAs 1..R-1 ("owners"), block-cyclically by position (block
+// j of 32 positions -> CTA 1 + j mod (R-1)), and each owner streams only the G
+// columns of the positions it owns.  CTA 0 leads: warp 0 solves the blocks
+// (same speculation / M inverse / verification as v6), warps 1.. prefetch the
+// sub-blocks two blocks ahead.  Per block step, one split cluster barrier
+// (arrive.release ... wait.acquire).  Each side publishes into its OWN shared
+// memory and the other side reads it remotely after the barrier (a remote
+// release-store costs a DSMEM round trip at the arrive; a remote load ~1/3 of it):
+//   leader : z = g (the owner's snapshot of the block, read remotely) + b minus
+//            the link with the previous block (computed before the barrier),
+//            solve, publish the 32 updates (dense) locally, arrive; then the
+//            link product for the next block;
+//   owners : read the previous block's 32 updates from the leader, apply them
+//            to all their positions (the G rows were prefetched into registers
+//            during the previous step), snapshot the next block's gradients
+//            if they own it, arrive, then issue the loads of this block's G
+//            rows for the next step.
+// The owners keep their gradients across consecutive sweeps over the same
+// positions; they go to a global copy (by slot) only when the positions change
+// (active <-> full sweeps, a new active set) or a catch-up / G_AA build needs
+// them.  Catch-ups, G_AA and M builds are split over the cluster.
+constexpr int kG7Threads = 256;
+constexpr int kG7Helpers = kG7Threads - 32;
+constexpr int kG7MaxR = 16;
+__host__ __device__ constexpr size_t gram7_smem(int nW, int R) {
+    // 9 x 8 KB leader buffers (3 stages of Gd, Gp, M) + the larger of the leader's
+    // per-slot state (bS, bcat: 16 B; act, actp: 8 B; inA: 1 B) and an owner's
+    // gradients + slots (12 B per owned position)
+    return (size_t)9 * 8192 +
+           ((size_t)25 * (size_t)((nW + 33) & ~1) > (size_t)12 * (size_t)(nW / (R - 1) + 64)
+                ? (size_t)25 * (size_t)((nW + 33) & ~1)
+                : (size_t)12 * (size_t)(nW / (R - 1) + 64)) +
+           64;
+}
+
+struct G7Work {              // global workspace of one fit (see bl.cu gram_ws)
+    double *g;               // nW: gradients by slot, between sweeps
+    int *act;                // nW: active list published by the leader
+    double *dl;              // nW: catch-up coefficient changes
+    int *rl;                 // nW: ... and their slots
+    uint8_t *inA;            // nW: slot is in the set G_AA was built for
+};
+
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
+
+template <bool ENET>
+__global__ void __launch_bounds__(kG7Threads, 1) k_cd_gram7(CdGramArgs a, G7Work wk) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ __align__(16) double sm[];
+    __shared__ __align__(16) double dfull[32];         // leader: the block's updates (0 = none)
+    __shared__ __align__(16) double rsh[32];
+    __shared__ __align__(16) double zsnap[2][32];      // owners: gradients of the next block (read by the leader)
+    __shared__ __align__(16) double dpub[2][32];       // leader: the block's updates (read by the owners)
+    __shared__ __align__(16) double dq[32];            // owners: local copy of the previous block's updates
+    __shared__ int bslot[3][32];                       // leader: slots of the block
+    __shared__ int ctl[2][8];                          // leader: command for the cluster (double-buffered)
+    __shared__ int wcount[33];
+    __shared__ double red[32];
+    constexpr int T_ = kG7Threads;
+    constexpr unsigned FULL = 0xffffffffu;
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = T_ >> 5;
+    const int R = (int)cl.num_blocks(), rank = (int)cl.block_rank(), NB = R - 1;
+    const bool leader_cta = rank == 0;
+    const int nW = a.nW;
+    const int nWp = (nW + 1) & ~1;
+    const int64_t ldG = a.ldG;
+    double(*Gd)[32][32] = reinterpret_cast<double(*)[32][32]>(sm);            // [3]: strictly lower diag sub-block
+    double(*Gp)[32][32] = Gd + 3;                                              // [3]: previous block -> this block
+    double(*Mb)[32][32] = Gd + 6;                                              // [3]: M, column-major ([c][b])
+    // leader CTA per-slot state
+    double *bS = sm + 9 * 1024;                             // coefficients, by slot
+    double *bcat = bS + nWp;                                // coefficients at the last lazy catch-up
+    int *act = reinterpret_cast<int *>(bcat + nWp);         // active slots (ascending)
+    int *actp = act + nWp;                                  // the set G_AA / M were built for
+    uint8_t *inA = reinterpret_cast<uint8_t *>(actp + nWp);
+    // owner CTAs: gradients of the owned positions (local index = (j / NB) * 32 + k % 32) and their slots
+    double *gl = sm + 9 * 1024;
+    const int gcap = (nW / 32 / NB + 2) * 32;
+    int *sl = reinterpret_cast<int *>(gl + gcap);
+    int owned = 0;                                          // owners: local positions currently held
+    auto lidx = [&](int k) { return ((k >> 5) / NB) * 32 + (k & 31); };
+
+    // ---- init: coefficients (leader), gradients by slot (global, split over the cluster)
+    if (leader_cta) {
+        for (int w = t; w < nWp; w += T_) {
+            bS[w] = w < nW ? a.beta[a.Wst[w]] : 0.0;
+            inA[w] = 0;
+        }
+    }
+    for (int w = rank * T_ + t; w < nW; w += R * T_) wk.g[w] = a.z[a.Wst[w]];
+    __threadfence();
+    cl.sync();
+
+    const long long clk0 = clock64();
+    int passes = 0, status = 0;
+    long long visits = 0, updates = 0, pr_lead = 0, pr_bulk = 0, retries = 0, rebuilds = 0;
+    long long pr_build = 0, pr_catch = 0, ncatch = 0, nfull = 0;
+    long long dbg[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const double la = a.lam_alpha, inv_den = a.inv_den;
+    double dm = 0.0, bm = 0.0;                              // leader warp: per-lane running maxima
+
+    auto block_rank = [&](bool nz, int &pos) -> int {     // order-preserving CTA compaction
+        const unsigned m = __ballot_sync(FULL, nz);
+        if (lane == 0) wcount[wid] = __popc(m);
+        __syncthreads();
+        if (t == 0) {
+            int run = 0;
+            for (int u = 0; u < nw; u++) { const int c0 = wcount[u]; wcount[u] = run; run += c0; }
+            wcount[32] = run;
+        }
+        __syncthreads();
+        pos = wcount[wid] + __popc(m & ((1u << lane) - 1u));
+        const int tot = wcount[32];
+        __syncthreads();
+        return tot;
+    };
+
+    // leader helpers: prefetch block qn's sub-blocks (and M in active sweeps) into stage buf
+    auto prefetch = [&](const double *Mx, bool active, int len, int qn, int buf) {
+        const int u = t - 32;
+        const int b0 = 32 * qn, nb1 = min(32, len - b0);
+        const int nb0 = qn > 0 ? 32 : 0;
+        constexpr int NP = (3072 + kG7Helpers - 1) / kG7Helpers;
+        double v[NP];
+#pragma unroll
+        for (int k = 0; k < NP; k++) {
+            const int e = u + k * kG7Helpers;
+            const int r = (e >> 5) & 31, c = e & 31;
+            const double *src = nullptr;
+            if (e < 1024) {
+                if (c > r && c < nb1) src = Mx + (int64_t)(b0 + r) * ldG + b0 + c;
+            } else if (e < 2048) {
+                if (r < nb0 && c < nb1) src = Mx + (int64_t)(b0 - 32 + r) * ldG + b0 + c;
+            } else if (e < 3072 && active) {
+                src = a.MA + (int64_t)qn * 1024 + (e - 2048);
+            }
+            v[k] = src ? __ldcg(src) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < NP; k++) {
+            const int e = u + k * kG7Helpers;
+            if (e < 1024) (&Gd[buf][0][0])[e] = v[k];
+            else if (e < 2048) (&Gp[buf][0][0])[e - 1024] = v[k];
+            else if (e < 3072 && active) (&Mb[buf][0][0])[e - 2048] = v[k];
+        }
+        if (u < 32) bslot[buf][u] = u < nb1 ? (active ? act[b0 + u] : b0 + u) : -1;
+    };
+
+    // leader warp: link of the previous block's updates (dfull) into block qn (stage buf)
+    auto link = [&](int buf) -> double {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+        for (int r = 0; r < 32; r += 4) {
+            const double2 d01 = *reinterpret_cast<const double2 *>(&dfull[r]);
+            const double2 d23 = *reinterpret_cast<const double2 *>(&dfull[r + 2]);
+            a0 = fma(d01.x, Gp[buf][r][lane], a0);
+            a1 = fma(d01.y, Gp[buf][r + 1][lane], a1);
+            a2 = fma(d23.x, Gp[buf][r + 2][lane], a2);
+            a3 = fma(d23.y, Gp[buf][r + 3][lane], a3);
+        }
+        return (a0 + a1) + (a2 + a3);
+    };
+
+    // leader warp: block at positions b0.. (stage buf; gradients in the owner's zsnap[zb]); acc = link term
+    auto lead = [&](bool active, int b0, int buf, int zb, double acc) {
+        const long long t0 = clock64();
+        const int s = bslot[buf][lane];
+        const bool valid = s >= 0;
+        const double zo = cl.map_shared_rank(&zsnap[0][0], 1 + ((b0 >> 5) % NB))[zb * 32 + lane];
+        double zc = 0.0, bo = 0.0;
+        if (valid) {
+            bo = bS[s];
+            zc = (zo - acc) + bo;
+        }
+        const double(*GL)[32] = Gd[buf];
+        int pred = bo > 0.0 ? 1 : (bo < 0.0 ? -1 : 0);
+        double dfin = 0.0, bnfin = bo;
+        unsigned todo = __ballot_sync(FULL, valid);
+        int round = 0;
+        const long long t1 = clock64();
+        dbg[0] += t1 - t0;
+        if (active) {
+            const double las = pred > 0 ? la : -la;
+            rsh[lane] = valid ? (ENET ? (zc - las) * inv_den : zc - las) - bo : 0.0;
+            __syncwarp();
+            double m0 = 0.0, m1 = 0.0, m2 = 0.0, m3 = 0.0;
+#pragma unroll
+            for (int c = 0; c < 32; c += 4) {
+                const double2 r01 = *reinterpret_cast<const double2 *>(&rsh[c]);
+                const double2 r23 = *reinterpret_cast<const double2 *>(&rsh[c + 2]);
+                m0 = fma(Mb[buf][c][lane], r01.x, m0);
+                m1 = fma(Mb[buf][c + 1][lane], r01.y, m1);
+                m2 = fma(Mb[buf][c + 2][lane], r23.x, m2);
+                m3 = fma(Mb[buf][c + 3][lane], r23.y, m3);
+            }
+            const double d = (m0 + m1) + (m2 + m3);
+            const double bn = d + bo;
+            const unsigned mis = __ballot_sync(FULL, valid && !(pred > 0 ? bn > 0.0 : bn < 0.0));
+            const unsigned commit = todo & (mis ? ((1u << (__ffs(mis) - 1)) - 1u) : FULL);
+            if ((commit >> lane) & 1u) { dfin = d; bnfin = bn; }
+            todo &= ~commit;
+            if (mis) {
+                ++round;
+                unsigned cp = commit;
+                while (cp) {
+                    const int p = __ffs(cp) - 1;
+                    cp &= cp - 1;
+                    const double dp = __shfl_sync(FULL, dfin, p);
+                    zc = fma(-dp, GL[p][lane], zc);
+                }
+                if ((todo >> lane) & 1u) pred = zc > la ? 1 : (zc < -la ? -1 : 0);
+            }
+        }
+        const long long t2 = clock64();
+        dbg[1] += t2 - t1;
+        while (todo) {
+            const unsigned Pm = __ballot_sync(FULL, pred != 0) & todo;
+            const double las = pred > 0 ? la : -la;
+            double z = zc;
+            unsigned rem = Pm;
+            while (rem) {
+                const int p = __ffs(rem) - 1;
+                rem &= rem - 1;
+                const double gl_ = GL[p][lane];
+                const double dl = (ENET ? (z - las) * inv_den : z - las) - bo;
+                const double dp = __shfl_sync(FULL, dl, p);
+                z = fma(-dp, gl_, z);
+            }
+            const bool hi = z > la, lo = z < -la;
+            const int tb = hi ? 1 : (lo ? -1 : 0);
+            const unsigned mis = __ballot_sync(FULL, tb != pred) & todo;
+            const unsigned below = mis ? ((1u << (__ffs(mis) - 1)) - 1u) : FULL;
+            const unsigned commit = todo & below;
+            if ((commit >> lane) & 1u) {
+                const double bn = hi ? z - la : (lo ? z + la : 0.0);
+                bnfin = ENET ? bn * inv_den : bn;
+                dfin = bnfin - bo;
+            }
+            todo &= ~commit;
+            if (!mis) break;
+            ++round;
+            unsigned cp = Pm & commit;
+            while (cp) {
+                const int p = __ffs(cp) - 1;
+                cp &= cp - 1;
+                const double dp = __shfl_sync(FULL, dfin, p);
+                zc = fma(-dp, GL[p][lane], zc);
+            }
+            if ((todo >> lane) & 1u) pred = tb;   // the first mismatch is exact now; the rest re-predicted
+        }
+        const long long t3 = clock64();
+        dbg[2] += t3 - t2;
+        // publish the 32 updates (dense, local; the owners read them after the barrier)
+        dpub[(b0 >> 5) & 1][lane] = dfin;
+        dfull[lane] = dfin;
+        retries += round;
+        dm = fmax(dm, fabs(dfin));
+        bm = fmax(bm, fabs(bnfin));
+        if (valid) bS[s] = bnfin;
+        updates += __popc(__ballot_sync(FULL, valid && dfin != 0.0));
+        dbg[3] += clock64() - t3;
+    };
+
+    // owners: positions / slots of local index e for a sweep of `len` positions
+    auto own_pos = [&](int e) { return 32 * (rank - 1 + (e >> 5) * NB) + (e & 31); };
+    auto n_owned = [&](int len) {
+        const int Q = (len + 31) >> 5;
+        return Q > rank - 1 ? 32 * ((Q - (rank - 1) + NB - 1) / NB) : 0;
+    };
+    // owners: gradients to / from the global copy
+    auto owner_store = [&]() {
+        for (int e = t; e < owned; e += T_)
+            if (sl[e] >= 0) wk.g[sl[e]] = gl[e];
+        owned = 0;
+    };
+    auto owner_load = [&](bool active, int len) {
+        owned = n_owned(len);
+        for (int e = t; e < owned; e += T_) {
+            const int k = own_pos(e);
+            const int s = k < len ? (active ? __ldcg(wk.act + k) : k) : -1;
+            sl[e] = s;
+            gl[e] = s >= 0 ? __ldcg(wk.g + s) : 0.0;
+        }
+    };
+
+    // one sweep over `len` positions (active: act list; full: slots)
+    auto sweep = [&](bool active, int len) {
+        visits += len;
+        const double *Mx = active ? a.GA : a.G;
+        const int Q = (len + 31) >> 5;
+        // owner: its first position pair, with the G rows of the previous block in registers
+        const int k0 = 2 * t < owned ? own_pos(2 * t) : -1;
+        const int e0 = 2 * t;
+        double2 rv[32];
+        double acc = 0.0;
+        if (leader_cta) {
+            if (wid == 0) { dm = 0.0; bm = 0.0; }
+            if (wid > 0) { prefetch(Mx, active, len, 0, 0); if (Q > 1) prefetch(Mx, active, len, 1, 1); }
+        } else if (wid == 0 && rank == 1) {                  // block 0's owner snapshots its gradients
+            zsnap[0][lane] = lane < len ? gl[lidx(lane)] : 0.0;
+        }
+        cluster_arrive();
+        // owners: the previous block's updates (read from the leader) -> every owned gradient
+        auto owner_apply = [&](int qp) {
+            if (wid == 0) dq[lane] = cl.map_shared_rank(&dpub[0][0], 0)[(qp & 1) * 32 + lane];
+            __syncthreads();
+            if (k0 >= 0) {
+                double gx = gl[e0], gy = gl[e0 + 1], hx = 0.0, hy = 0.0;
+#pragma unroll
+                for (int i = 0; i < 32; i += 2) {
+                    const double2 dd = *reinterpret_cast<const double2 *>(&dq[i]);
+                    gx = fma(-dd.x, rv[i].x, gx);
+                    gy = fma(-dd.x, rv[i].y, gy);
+                    hx = fma(-dd.y, rv[i + 1].x, hx);
+                    hy = fma(-dd.y, rv[i + 1].y, hy);
+                }
+                gl[e0] = gx + hx;
+                gl[e0 + 1] = gy + hy;
+            }
+            for (int e = e0 + 2 * T_; e < owned; e += 2 * T_) {   // further pairs: direct loads
+                const int k = own_pos(e);
+                if (k >= len) continue;
+                double gx = gl[e], gy = gl[e + 1];
+                for (int i = 0; i < 32; i++) {
+                    const double d = dq[i];
+                    if (d == 0.0) continue;
+                    const double2 g2 = __ldcg(reinterpret_cast<const double2 *>(Mx + (int64_t)(32 * qp + i) * ldG + k));
+                    gx = fma(-d, g2.x, gx);
+                    gy = fma(-d, g2.y, gy);
+                }
+                gl[e] = gx;
+                gl[e + 1] = gy;
+            }
+            __syncthreads();
+        };
+        for (int q = 0; q < Q; q++) {
+            const long long c0 = clock64();
+            if (leader_cta) {
+                cluster_wait();
+                if (wid == 0) {
+                    lead(active, 32 * q, q % 3, q & 1, acc);
+                    cluster_arrive();
+                    if (q + 1 < Q) { __syncwarp(); acc = link((q + 1) % 3); }
+                    if (t == 0) pr_lead += clock64() - c0;
+                } else {
+                    if (q + 2 < Q) prefetch(Mx, active, len, q + 2, (q + 2) % 3);
+                    cluster_arrive();
+                }
+            } else {
+                cluster_wait();
+                const long long c1 = clock64();
+                if (q > 0) owner_apply(q - 1);
+                const long long c2 = clock64();
+                dbg[5] += c2 - c1;
+                if (q + 1 < Q && wid == 0 && ((q + 1) % NB) == rank - 1) {   // snapshot of the next block
+                    const int k = 32 * (q + 1) + lane;
+                    zsnap[(q + 1) & 1][lane] = k < len ? gl[lidx(k)] : 0.0;
+                }
+                cluster_arrive();
+                dbg[6] += clock64() - c2;
+                // G rows of block q for the next step (rows past the end: zero)
+                if (k0 >= 0) {
+#pragma unroll
+                    for (int i = 0; i < 32; i++) {
+                        const int row = 32 * q + i;
+                        rv[i] = row < len ? __ldcg(reinterpret_cast<const double2 *>(Mx + (int64_t)row * ldG + k0))
+                                          : make_double2(0.0, 0.0);
+                    }
+                }
+                if (t == 0) pr_bulk += clock64() - c0;
+            }
+        }
+        cluster_wait();
+        if (!leader_cta && Q > 0) owner_apply(Q - 1);        // flush: block Q-1's updates everywhere
+        __syncthreads();
+        cl.sync();                                            // the leader's dpub is read before it changes
+    };
+
+    // leader CTA: active list into act (smem) and the global copy
+    auto build_active = [&]() -> int {
+        int total = 0;
+        for (int base = 0; base < nW; base += T_) {
+            const int w = base + t;
+            const bool nz = w < nW && bS[w] != 0.0;
+            int pos;
+            const int cnt = block_rank(nz, pos);
+            if (nz) { act[total + pos] = w; wk.act[total + pos] = w; }
+            total += cnt;
+        }
+        __syncthreads();
+        return total;
+    };
+
+    // cluster: G_AA = G[act][act] (rows split over CTAs), then per block of 32
+    // positions M = (I + inv N^T)^-1 (blocks split over the CTAs' warps; scratch =
+    // each CTA's first 8 KB buffers)
+    auto build_A = [&](int na) {
+        for (int i = rank; i < na; i += R) {
+            const int64_t rs = (int64_t)__ldcg(wk.act + i) * ldG;
+            for (int j0 = t; j0 < na; j0 += 4 * T_) {
+                double v[4];
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    const int j = min(j0 + k * T_, na - 1);
+                    v[k] = __ldg(a.G + rs + __ldcg(wk.act + j));
+                }
+#pragma unroll
+                for (int k = 0; k < 4; k++)
+                    if (j0 + k * T_ < na) a.GA[(int64_t)i * ldG + j0 + k * T_] = v[k];
+            }
+        }
+        __threadfence();
+        cl.sync();
+        const int nblk = (na + 31) / 32;
+        {
+            double(*N)[32] = Gd[wid];
+            for (int q = rank * nw + wid; q < nblk; q += nw * R) {
+                const int b0 = 32 * q, nb = min(32, na - b0);
+                for (int e = lane; e < 1024; e += 32) {
+                    const int p = e >> 5, b = e & 31;
+                    N[p][b] = (b > p && b < nb) ? inv_den * __ldcg(a.GA + (int64_t)(b0 + p) * ldG + b0 + b) : 0.0;
+                }
+                __syncwarp();
+                double x[32];
+#pragma unroll
+                for (int b = 0; b < 32; b++) x[b] = b == lane ? 1.0 : 0.0;
+#pragma unroll
+                for (int p = 0; p < 31; p++) {
+                    const double xp = x[p];
+#pragma unroll
+                    for (int b = (p + 1) & ~1; b < 32; b += 2) {
+                        const double2 nv = *reinterpret_cast<const double2 *>(&N[p][b]);
+                        if (b > p) x[b] = fma(-nv.x, xp, x[b]);
+                        x[b + 1] = fma(-nv.y, xp, x[b + 1]);
+                    }
+                }
+                double *dst = a.MA + (int64_t)q * 1024 + lane * 32;
+#pragma unroll
+                for (int b = 0; b < 32; b += 2) *reinterpret_cast<double2 *>(dst + b) = make_double2(x[b], x[b + 1]);
+                __syncwarp();
+            }
+        }
+        __threadfence();
+        cl.sync();
+    };
+
+    // cluster: gradients outside the G_AA set receive sum_i dl_i G[rl_i][k] (list from the leader)
+    auto catch_up = [&](int nz) {
+        if (nz > 0) {
+            for (int k = 2 * (rank * T_ + t); k < nW; k += 2 * R * T_) {
+                double gx = 0.0, gy = 0.0;
+                for (int i0 = 0; i0 < nz; i0 += 16) {
+                    double2 rv[16];
+                    double dd[16];
+#pragma unroll
+                    for (int v = 0; v < 16; v++) {
+                        const int i = min(i0 + v, nz - 1);
+                        dd[v] = i0 + v < nz ? __ldcg(wk.dl + i) : 0.0;
+                        rv[v] = __ldcg(reinterpret_cast<const double2 *>(a.G + (int64_t)__ldcg(wk.rl + i) * ldG + k));
+                    }
+#pragma unroll
+                    for (int v = 0; v < 16; v++) {
+                        gx = fma(dd[v], rv[v].x, gx);
+                        gy = fma(dd[v], rv[v].y, gy);
+                    }
+                }
+                if (!__ldcg(wk.inA + k)) wk.g[k] -= gx;
+                if (k + 1 < nW && !__ldcg(wk.inA + k + 1)) wk.g[k + 1] -= gy;
+            }
+        }
+        __threadfence();
+        cl.sync();
+    };
+
+    // ---- control loop.  The leader decides, the cluster follows.  ctl[ph]:
+    // [0] catch-up, [1] its count, [2] rebuild G_AA / M, [3] mode (0 full, 1 active, -1 stop),
+    // [4] len, [5] owners reload their positions
+    bool full = false, built = false, pending = false;
+    int na_built = 0, last_mode = -1, last_len = -1, ph = 0;
+    for (;; ph ^= 1) {
+        if (leader_cta) {
+            int cmd_catch = 0, ncat = 0, cmd_build = 0, mode = 0, len = nW;
+            if (status || (passes > 0 && full && red[2] != 0.0)) {
+                mode = -1;                                    // stop (set below after a sweep)
+            } else {
+                for (;;) {
+                    if (!full) {
+                        len = build_active();
+                        bool same = built && len == na_built;
+                        if (same) {
+                            int diff = 0;
+                            for (int i = t; i < len; i += T_) diff |= act[i] != actp[i];
+                            same = !__syncthreads_or(diff);
+                        }
+                        if (!same) {
+                            if (pending) { cmd_catch = 1; pending = false; }
+                            if (len == 0) { full = true; continue; }
+                            cmd_build = 1;
+                        }
+                        mode = 1;
+                    } else {
+                        if (pending) { cmd_catch = 1; pending = false; }
+                        mode = 0;
+                        len = nW;
+                    }
+                    break;
+                }
+            }
+            if (cmd_catch) {                                  // coefficient changes since the last catch-up
+                int nz = 0;
+                for (int base = 0; base < na_built; base += T_) {
+                    const int i = base + t;
+                    const int s = i < na_built ? actp[i] : 0;
+                    const double dlt = i < na_built ? bS[s] - bcat[s] : 0.0;
+                    int pos;
+                    const int cnt = block_rank(dlt != 0.0, pos);
+                    if (dlt != 0.0) { wk.dl[nz + pos] = dlt; wk.rl[nz + pos] = s; }
+                    nz += cnt;
+                }
+                for (int w = t; w < nW; w += T_) wk.inA[w] = inA[w];
+                ncat = nz;
+            }
+            if (cmd_build) {
+                __syncthreads();
+                for (int i = t; i < nWp; i += T_) inA[i] = 0;
+                __syncthreads();
+                for (int i = t; i < len; i += T_) { actp[i] = act[i]; inA[act[i]] = 1; }
+                built = true;
+                na_built = len;
+            }
+            if (mode == 1 && (cmd_build || !pending)) {
+                __syncthreads();
+                for (int i = t; i < len; i += T_) bcat[act[i]] = bS[act[i]];
+                pending = true;
+            }
+            const int reload = mode != last_mode || len != last_len || cmd_build || cmd_catch;
+            last_mode = mode;
+            last_len = len;
+            if (t == 0) {
+                ctl[ph][0] = cmd_catch; ctl[ph][1] = ncat; ctl[ph][2] = cmd_build;
+                ctl[ph][3] = mode; ctl[ph][4] = len; ctl[ph][5] = reload;
+            }
+            __threadfence();
+        }
+        cl.sync();
+        const int *rc = cl.map_shared_rank(&ctl[ph][0], 0);
+        const int cmd_catch = rc[0], ncat = rc[1], cmd_build = rc[2], mode = rc[3], len = rc[4], reload = rc[5];
+        if (!leader_cta && (reload || mode < 0)) owner_store();
+        if (mode < 0) break;
+        if (reload) { __threadfence(); cl.sync(); }
+        if (cmd_catch) {
+            const long long c0 = clock64();
+            catch_up(ncat);
+            ++ncatch;
+            pr_catch += clock64() - c0;
+        }
+        if (cmd_build) {
+            const long long c0 = clock64();
+            build_A(len);
+            ++rebuilds;
+            pr_build += clock64() - c0;
+        }
+        if (!leader_cta && reload) { owner_load(mode == 1, len); __syncthreads(); }
+        nfull += mode == 0;
+        sweep(mode == 1, len);
+        if (leader_cta) {                                     // convergence of the pass (leader only)
+            if (wid == 0) {
+                const double dmw = warp_max(dm), bmw = warp_max(bm);
+                if (t == 0) { red[0] = dmw; red[1] = bmw; }
+            }
+            __syncthreads();
+            const double dmax = red[0], bmax = red[1];
+            __syncthreads();
+            const bool conv = dmax <= a.tol * bmax || dmax <= a.floor_;
+            if (++passes > a.max_iter) status = 3;
+            if (t == 0) red[2] = (full && conv) ? 1.0 : 0.0;   // stop after a converged full pass
+            __syncthreads();
+            if (red[2] == 0.0) full = conv;
+        }
+    }
+    cl.sync();                                              // no DSMEM access past this point
+    if (!leader_cta) {
+        if (rank == 1 && t == 0) {
+            a.st->cd_prof[1] = pr_bulk;
+            for (int u = 4; u < 8; u++) a.st->cd_dbg[u] = dbg[u];
+        }
+        return;
+    }
+    double l1 = 0.0, l2 = 0.0, nnz = 0.0;
+    for (int q = t; q < nW; q += T_) {
+        const int w = a.ord[q];
+        const double bv = bS[w];
+        const int j = a.Wst[w];
+        const double b0 = a.beta[j];
+        a.beta[j] = bv;
+        a.dbeta[w] = bv - b0;
+        a.betaW_out[q] = bv;
+        a.betaW_out[nW + q] = a.c[j];
+        a.betaW_out[2 * nW + q] = a.s[j];
+        l1 += fabs(bv);
+        l2 = fma(bv, bv, l2);
+        nnz += bv != 0.0 ? 1.0 : 0.0;
+    }
+    l1 = block_sum(l1, red);
+    l2 = block_sum(l2, red);
+    nnz = block_sum(nnz, red);
+    if (t == 0) {
+        a.st->cd_passes = passes;
+        a.st->cd_status = status;
+        a.st->l1 = l1;
+        a.st->l2 = l2;
+        a.st->nnz = (int)nnz;
+        a.st->cd_visits = visits;
+        a.st->cd_updates = updates;
+        a.st->cd_cycles = clock64() - clk0;
+        a.st->cd_prof[0] = pr_lead;
+        a.st->cd_prof[2] = pr_build;
+        a.st->cd_prof[3] = pr_catch;
+        a.st->cd_cnt[0] = retries;
+        a.st->cd_cnt[1] = rebuilds;
+        a.st->cd_cnt[2] = ncatch;
+        a.st->cd_cnt[3] = nfull;
+        for (int u = 0; u < 4; u++) a.st->cd_dbg[u] = dbg[u];
     }
 }
 
