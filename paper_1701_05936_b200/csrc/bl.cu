@@ -704,6 +704,7 @@ void ensure_G(bl_prep *pp, int64_t need) {
     double *G2 = nullptr;
     cudaError_t e = cudaMalloc(&G2, (size_t)8 * nl * nl);
     if (e != cudaSuccess) { cudaGetLastError(); raise(BL_ERR_OOM, "cudaMalloc for the %lld^2 Gram matrix: %s", (long long)nl, cudaGetErrorString(e)); }
+    CK(cudaMemsetAsync(G2, 0, (size_t)8 * nl * nl, pp->stream));   // rows/columns past |W| are read (x 0) by bulk copies
     if (pp->G && pp->nG > 0)
         CK(cudaMemcpy2DAsync(G2, 8 * nl, pp->G, 8 * pp->ldG, 8 * (size_t)pp->nG, pp->nG, cudaMemcpyDeviceToDevice,
                              pp->stream));
@@ -715,6 +716,7 @@ void ensure_G(bl_prep *pp, int64_t need) {
     pp->GA = nullptr;
     e = cudaMalloc(&pp->GA, gram_ws_bytes(nl));
     if (e != cudaSuccess) { cudaGetLastError(); pp->GA = nullptr; raise(BL_ERR_OOM, "cudaMalloc for the %lld^2 G_AA workspace: %s", (long long)nl, cudaGetErrorString(e)); }
+    CK(cudaMemsetAsync(pp->GA, 0, gram_ws_bytes(nl), pp->stream));
 }
 
 template <typename T, bool M>
