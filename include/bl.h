@@ -56,15 +56,32 @@ typedef struct bl_path bl_path;
 typedef struct bl_cvres bl_cvres;
 typedef struct bl_prep bl_prep;
 
-/* Multi-GPU column sharding.  NULL => single GPU.  Rank g owns the
- * contiguous global columns [col_offset, col_offset + p_local).  Every rank calls
- * every function collectively with identical scalar arguments and identical y,
- * lambda.  nccl_unique_id points to the 128-byte ncclUniqueId obtained on rank 0
- * with bl_nccl_unique_id() and broadcast by the caller (e.g. torch.distributed). */
+/* Multi-GPU (BASELINE north star: "Features are column-sharded for
+ * the scans, and NCCL all-gathers only the small strong-set and violator index
+ * lists").  NULL => single GPU.  Rank g owns the contiguous global columns
+ * [col_offset, col_offset + p_local); shards are in rank order and cover
+ * [0, p_global).  Every rank calls every function collectively with identical
+ * scalar arguments and identical y, lambda.
+ *  - p_global > p_local: SHARDED design.  Scans, BEDPP and the strong rule run on
+ *    each shard; lambda_max / x_* are combined across ranks; strong / violator
+ *    lists are all-gathered (global indices, sorted); the columns that enter the
+ *    working set are broadcast by their owner into every rank's working-set
+ *    column store, and the coordinate descent runs replicated (identical,
+ *    deterministic) on every rank, so the residual needs no broadcast.  Results
+ *    are identical to the single-GPU path (global indices).
+ *  - p_global == p_local: REPLICATED design (every rank holds all of X); bl_cv
+ *    distributes the folds over the ranks.
+ * backend 0: NCCL; nccl_unique_id points to the 128-byte ncclUniqueId obtained on
+ * rank 0 with bl_nccl_unique_id() and broadcast by the caller (torch.distributed).
+ * backend 1: in-process loopback for testing -- the ranks are threads of ONE
+ * process sharing one device; nccl_unique_id points to a 128-byte group key
+ * (any bytes, identical on the group's ranks); collectives are staged through
+ * host memory. */
 typedef struct {
     int rank, world, device;
     const void *nccl_unique_id;
     int64_t col_offset, p_global;
+    int backend;
 } bl_dist;
 
 /* Optional execution options (NULL => defaults). */

@@ -35,7 +35,7 @@ class BLError(RuntimeError):
 class bl_dist(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int), ("world", ctypes.c_int), ("device", ctypes.c_int),
                 ("nccl_unique_id", ctypes.c_void_p), ("col_offset", ctypes.c_int64),
-                ("p_global", ctypes.c_int64)]
+                ("p_global", ctypes.c_int64), ("backend", ctypes.c_int)]
 
 
 class bl_opts(ctypes.Structure):
@@ -282,3 +282,38 @@ class CvResult:
         self.E = np.empty((K_lam, n))
         _check(L.bl_cv_errors(handle, _p(self.E)))
         self.full = Path(full, BL_OK) if full.value else None
+
+
+# ------------------------------------------------------------------ multi-GPU plumbing
+
+def shard_range(p, world, rank, block=1):
+    """Rank's contiguous column shard [j0, j1) of p columns: balanced whole
+    `block`-column blocks, in rank order (the layout bl_dist requires)."""
+    nb = (p + block - 1) // block
+    b0, b1 = nb * rank // world, nb * (rank + 1) // world
+    return min(p, b0 * block), min(p, b1 * block)
+
+
+def make_dist(rank, world, col_range, p_global, device=0, group=None):
+    """bl_dist of a torch.distributed job (NCCL backend): rank 0 draws the NCCL
+    unique id, every rank receives it with torch.distributed.broadcast_object_list.
+    p_global == col_range width => replicated design."""
+    import torch.distributed as tdist
+    uid = [bl_nccl_unique_id() if rank == 0 else None]
+    tdist.broadcast_object_list(uid, src=0, group=group)
+    return _dist(rank, world, device, uid[0], col_range, p_global, 0)
+
+
+def loopback_dist(rank, world, col_range, p_global, key, device=0):
+    """bl_dist of the in-process loopback backend (testing: ranks = threads of
+    one process on one device); `key` = 128-byte group key shared by the ranks."""
+    return _dist(rank, world, device, key, col_range, p_global, 1)
+
+
+def _dist(rank, world, device, key, col_range, p_global, backend):
+    key = bytes(key)
+    assert len(key) == 128
+    buf = ctypes.create_string_buffer(key, 128)
+    d = bl_dist(rank, world, device, ctypes.cast(buf, ctypes.c_void_p), int(col_range[0]), int(p_global), backend)
+    d._key_buf = buf          # keep the id alive with the struct
+    return d

@@ -16,7 +16,10 @@
 #include <cstdarg>
 #include <cstdlib>
 #include <cstdio>
+#include <condition_variable>
 #include <cstring>
+#include <map>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <string>
@@ -70,6 +73,101 @@ int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 }  // namespace
 
+// ------------------------------------------------------------ communicators
+// Collectives of the sharded path.  Every call is collective,
+// runs on stream `st` and returns with the stream synchronised (the host
+// decides on the result).  Payloads are small except the broadcast of the
+// columns entering the working set.
+struct Comm {
+    int rank = 0, world = 1;
+    virtual ~Comm() {}
+    virtual void allgather(const void *send, void *recv, size_t bytes, cudaStream_t st) = 0;   // recv: world * bytes
+    virtual void bcast(void *buf, size_t bytes, int root, cudaStream_t st) = 0;
+    virtual void allreduce_sum(double *buf, size_t count, cudaStream_t st) = 0;
+};
+
+struct NcclComm : Comm {
+    ncclComm_t c = nullptr;
+    ~NcclComm() override { if (c) ncclCommDestroy(c); }
+    void allgather(const void *send, void *recv, size_t bytes, cudaStream_t st) override {
+        CKN(ncclAllGather(send, recv, bytes, ncclUint8, c, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    void bcast(void *buf, size_t bytes, int root, cudaStream_t st) override {
+        CKN(ncclBroadcast(buf, buf, bytes, ncclUint8, root, c, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    void allreduce_sum(double *buf, size_t count, cudaStream_t st) override {
+        CKN(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, c, st));
+        CK(cudaStreamSynchronize(st));
+    }
+};
+
+// In-process loopback (testing): the ranks are host threads sharing one device;
+// data is staged through host memory between two group barriers.
+struct LoopGroup {
+    std::mutex mu;
+    std::condition_variable cv;
+    int world = 0, arrived = 0, members = 0;
+    long gen = 0;
+    std::vector<std::vector<char>> stage;
+};
+std::mutex g_loop_mu;
+std::map<std::string, std::shared_ptr<LoopGroup>> g_loop_groups;
+
+struct LoopComm : Comm {
+    std::shared_ptr<LoopGroup> g;
+    std::string key;
+    ~LoopComm() override {
+        if (!g) return;
+        std::lock_guard<std::mutex> lk(g_loop_mu);
+        if (--g->members == 0) g_loop_groups.erase(key);
+    }
+    void barrier() {
+        std::unique_lock<std::mutex> lk(g->mu);
+        const long my = g->gen;
+        if (++g->arrived == world) {
+            g->arrived = 0;
+            g->gen++;
+            g->cv.notify_all();
+        } else {
+            g->cv.wait(lk, [&] { return g->gen != my; });
+        }
+    }
+    void put(const void *dev, size_t bytes, cudaStream_t st) {
+        g->stage[rank].resize(bytes);
+        if (bytes) CK(cudaMemcpyAsync(g->stage[rank].data(), dev, bytes, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    void allgather(const void *send, void *recv, size_t bytes, cudaStream_t st) override {
+        put(send, bytes, st);
+        barrier();
+        for (int r = 0; r < world; r++)
+            if (bytes) CK(cudaMemcpyAsync((char *)recv + (size_t)r * bytes, g->stage[r].data(), bytes, cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
+        barrier();
+    }
+    void bcast(void *buf, size_t bytes, int root, cudaStream_t st) override {
+        if (rank == root) put(buf, bytes, st);
+        barrier();
+        if (rank != root && bytes) CK(cudaMemcpyAsync(buf, g->stage[root].data(), bytes, cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
+        barrier();
+    }
+    void allreduce_sum(double *buf, size_t count, cudaStream_t st) override {
+        put(buf, 8 * count, st);
+        barrier();
+        std::vector<double> acc(count, 0.0);
+        for (int r = 0; r < world; r++) {
+            const double *v = (const double *)g->stage[r].data();
+            for (size_t i = 0; i < count; i++) acc[i] += v[i];
+        }
+        if (count) CK(cudaMemcpyAsync(buf, acc.data(), 8 * count, cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
+        barrier();
+    }
+};
+
 // ------------------------------------------------------------------ handles
 
 struct bl_design {
@@ -83,7 +181,9 @@ struct bl_design {
     int64_t col_offset, p_global;
     int device, nsm;
     int rank, world;
-    ncclComm_t comm;
+    Comm *comm;                      // world > 1 only
+    bool sharded;                    // columns split over the ranks (p_global > p_local)
+    std::vector<int64_t> shard_off;  // world + 1 global column offsets of the shards (rank order)
     std::mutex comm_mu;
 };
 
@@ -151,6 +251,15 @@ struct bl_prep {
     int64_t ldG;
     int nG;                 // slots whose G row/column is computed
     double *rpart;          // per-block partials of the residual refresh
+    // sharded designs: device scratch of the collectives, and the working-set column
+    // store (every rank holds the W columns, broadcast by their owners, in slot order)
+    void *cbuf;
+    size_t cbuf_cap;
+    void *Xw;               // ld x ws_cap, raw dtype
+    double *cw, *sw, *bw, *zw;   // per slot: c, s, beta, gradient
+    int *widx;              // identity 0..ws_cap-1 (slot -> column of the store)
+    int64_t ws_cap;
+    int star_root;          // rank owning x_* (sharded)
     int cd_mode;            // 0 auto (Gram when |W| <= 4096), 1 residual, 2 Gram
     cudaStream_t own;       // library stream (used when the caller passes none)
     // profiling
@@ -277,14 +386,17 @@ size_t allow_dyn_smem(const void *kern) {
 // ------------------------------------------------------------ scan launcher
 // Raw-dot + identity epilogue over `list` (or all columns); v = fp64 vector
 // (fp32/fp64 designs) -- for int8 designs v is quantised to limbs first.
-void launch_scan(bl_prep *pp, ScanArgs a, const double *v_dev, bool timed, bool events = true) {
+// `cols`: another column source with the design's layout (the sharded working-set
+// store) and its c, s; nullptr => the design.
+void launch_scan(bl_prep *pp, ScanArgs a, const double *v_dev, bool timed, bool events = true,
+                 const void *cols = nullptr, const double *cc = nullptr, const double *cs = nullptr) {
     bl_design *d = pp->d;
-    a.X = d->X;
+    a.X = cols ? cols : d->X;
     a.ld = d->ld;
     a.n = (int)d->n;
     a.p = d->p;
-    a.c = pp->c;
-    a.s = pp->s;
+    a.c = cols ? cc : pp->c;
+    a.s = cols ? cs : pp->s;
     if (d->dt == DT_I8) {
         k_limbs<<<1, 1024, 0, pp->stream>>>(v_dev, (int)d->n, pp->limb_ld, pp->limbs, pp->limb_scale,
                                             pp->limb_sum);
@@ -358,6 +470,9 @@ void free_prep(bl_prep *pp) {
     if (pp->warena) cudaFree(pp->warena);
     if (pp->G) cudaFree(pp->G);
     if (pp->GA) cudaFree(pp->GA);
+    if (pp->cbuf) cudaFree(pp->cbuf);
+    if (pp->Xw) cudaFree(pp->Xw);
+    if (pp->cw) cudaFree(pp->cw);
     if (pp->own) cudaStreamDestroy(pp->own);
     pp->magic = MAGIC_DEAD;
     delete pp;
@@ -401,7 +516,7 @@ void ensure_host(Tp *&ptr, size_t &cap, size_t need) {
 void ensure_W(bl_prep *pp, int64_t need) {
     if (need <= pp->Wcap && pp->warena) return;
     int64_t nc = std::max<int64_t>(std::max<int64_t>(need, 2 * pp->Wcap), 1024);
-    nc = std::min<int64_t>(std::max<int64_t>(nc, need), std::max<int64_t>(pp->p, 1));
+    nc = std::min<int64_t>(std::max<int64_t>(nc, need), std::max<int64_t>(pp->d->sharded ? pp->d->p_global : pp->p, 1));
     CK(cudaStreamSynchronize(pp->stream));
     if (pp->warena) CK(cudaFree(pp->warena));
     pp->warena = nullptr;
@@ -415,6 +530,98 @@ void ensure_W(bl_prep *pp, int64_t need) {
     pp->betaW = (double *)(pp->warena + 3 * ib);
     pp->dbeta = pp->betaW + 3 * nc;
     pp->Wcap = nc;
+}
+
+void *ensure_cbuf(bl_prep *pp, size_t bytes) {
+    if (bytes <= pp->cbuf_cap) return pp->cbuf;
+    CK(cudaStreamSynchronize(pp->stream));
+    if (pp->cbuf) CK(cudaFree(pp->cbuf));
+    pp->cbuf = nullptr;
+    size_t nb = std::max<size_t>(std::max<size_t>(bytes, 2 * pp->cbuf_cap), 4096);
+    cudaError_t e = cudaMalloc(&pp->cbuf, nb);
+    if (e != cudaSuccess) { cudaGetLastError(); pp->cbuf_cap = 0; raise(BL_ERR_OOM, "cudaMalloc(%zu) for collectives: %s", nb, cudaGetErrorString(e)); }
+    pp->cbuf_cap = nb;
+    return pp->cbuf;
+}
+
+// Sharded: the working-set column store grows geometrically, keeping its contents.
+void ensure_Ws(bl_prep *pp, int64_t need, int64_t have) {
+    if (need <= pp->ws_cap) return;
+    bl_design *d = pp->d;
+    const size_t isz = itemsize(d->dt);
+    const int64_t nc = std::max<int64_t>(std::max<int64_t>(need, 2 * pp->ws_cap), 256);
+    void *X2 = nullptr;
+    double *v2 = nullptr;
+    cudaError_t e = cudaMalloc(&X2, (size_t)d->ld * nc * isz);
+    if (e == cudaSuccess) e = cudaMalloc(&v2, (size_t)8 * 4 * nc + (size_t)4 * nc);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        if (X2) cudaFree(X2);
+        raise(BL_ERR_OOM, "cudaMalloc for the working-set column store (%lld columns): %s", (long long)nc, cudaGetErrorString(e));
+    }
+    cudaStream_t st = pp->stream;
+    double *c2 = v2, *s2 = v2 + nc, *b2 = v2 + 2 * nc, *z2 = v2 + 3 * nc;
+    int *w2 = (int *)(v2 + 4 * nc);
+    if (have > 0) {
+        CK(cudaMemcpyAsync(X2, pp->Xw, (size_t)d->ld * have * isz, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(c2, pp->cw, 8 * (size_t)have, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(s2, pp->sw, 8 * (size_t)have, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(b2, pp->bw, 8 * (size_t)have, cudaMemcpyDeviceToDevice, st));
+    }
+    k_iota<<<(unsigned)((nc + 255) / 256), 256, 0, st>>>(w2, (int)nc);
+    CKL();
+    CK(cudaStreamSynchronize(st));
+    if (pp->Xw) cudaFree(pp->Xw);
+    if (pp->cw) cudaFree(pp->cw);
+    pp->Xw = X2;
+    pp->cw = c2; pp->sw = s2; pp->bw = b2; pp->zw = z2;
+    pp->widx = w2;
+    pp->ws_cap = nc;
+}
+
+// Columns of the coordinate-descent side: the design itself (single GPU /
+// replicated), or the working-set column store (sharded; slot j = store column j).
+struct CdView {
+    const void *X;
+    const double *c, *s;
+    double *beta, *z;
+    const int *Wst;          // slot -> column of the view
+    const int *Wsorted;      // W in ascending global order -> columns of the view
+};
+CdView cd_view(bl_prep *pp) {
+    if (!pp->d->sharded) return CdView{pp->d->X, pp->c, pp->s, pp->beta, pp->z, pp->Wst_d, pp->W};
+    return CdView{pp->Xw, pp->cw, pp->sw, pp->bw, pp->zw, pp->widx, pp->ord_d};
+}
+
+// ---- collectives of the sharded path
+// per-rank int64 records (k entries each) -> world x k on the host
+std::vector<int64_t> gather_i64(bl_prep *pp, const int64_t *mine, int k) {
+    bl_design *d = pp->d;
+    int64_t *buf = (int64_t *)ensure_cbuf(pp, (size_t)8 * k * (d->world + 1));
+    CK(cudaMemcpyAsync(buf, mine, 8 * (size_t)k, cudaMemcpyHostToDevice, pp->stream));
+    d->comm->allgather(buf, buf + k, 8 * (size_t)k, pp->stream);
+    std::vector<int64_t> all((size_t)k * d->world);
+    CK(cudaMemcpy(all.data(), buf + k, 8 * (size_t)k * d->world, cudaMemcpyDeviceToHost));
+    return all;
+}
+// every rank's local index list (device, counts[r] entries on rank r) -> sorted GLOBAL indices
+std::vector<int> gather_list(bl_prep *pp, const int *dev, const std::vector<int64_t> &counts) {
+    bl_design *d = pp->d;
+    int64_t mx = 0, tot = 0;
+    for (int64_t c : counts) { mx = std::max(mx, c); tot += c; }
+    std::vector<int> out;
+    if (mx == 0) return out;
+    int *buf = (int *)ensure_cbuf(pp, (size_t)4 * mx * (d->world + 1));
+    const int64_t mine = counts[d->rank];
+    if (mine) CK(cudaMemcpyAsync(buf, dev, 4 * (size_t)mine, cudaMemcpyDeviceToDevice, pp->stream));
+    d->comm->allgather(buf, buf + mx, 4 * (size_t)mx, pp->stream);
+    ensure_host(pp->hlist, pp->hlist_cap, (size_t)mx * d->world);
+    CK(cudaMemcpy(pp->hlist, buf + mx, 4 * (size_t)mx * d->world, cudaMemcpyDeviceToHost));
+    out.reserve(tot);
+    for (int r = 0; r < d->world; r++)
+        for (int64_t q = 0; q < counts[r]; q++) out.push_back(pp->hlist[(size_t)r * mx + q] + (int)d->shard_off[r]);
+    std::sort(out.begin(), out.end());
+    return out;
 }
 
 // One-time preprocessing for (y, optional training mask).
@@ -525,10 +732,50 @@ bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double a
                                 pp->ps);
     CKL();
     pp->launches += 2;
+    if (d->sharded) {
+        // C1: the shards' best |a_j| -> global lambda_max, j* (lowest global index on ties)
+        PrepScalars h;
+        CK(cudaMemcpyAsync(&h, pp->ps, sizeof h, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        double rec[6] = {h.A, (double)(h.jstar >= 0 ? h.jstar + d->col_offset : -1), h.sigma, h.c_star, h.s_star,
+                         (double)h.n_live};
+        int64_t mine[6];
+        std::memcpy(mine, rec, sizeof rec);
+        std::vector<int64_t> all = gather_i64(pp, mine, 6);
+        int win = -1;
+        double best = -1.0, bj = -1.0, live = 0.0;
+        for (int r = 0; r < d->world; r++) {
+            double v[6];
+            std::memcpy(v, &all[6 * (size_t)r], sizeof v);
+            live += v[5];
+            if (v[1] < 0.0) continue;
+            if (v[0] > best || (v[0] == best && v[1] < bj)) { best = v[0]; bj = v[1]; win = r; }
+        }
+        pp->star_root = win;
+        h.n_live = (int)live;
+        if (win >= 0) {
+            double v[6];
+            std::memcpy(v, &all[6 * (size_t)win], sizeof v);
+            h.A = v[0];
+            h.lmax = h.A / alpha;
+            h.sigma = v[2];
+            h.c_star = v[3];
+            h.s_star = v[4];
+            h.inv_s_star = v[4] > 0.0 ? 1.0 / v[4] : 0.0;
+            h.jstar = win == d->rank ? (long long)(bj - (double)d->col_offset) : -1;
+        } else {
+            h.A = 0.0; h.lmax = 0.0; h.sigma = 1.0; h.c_star = 0.0; h.s_star = 0.0; h.inv_s_star = 0.0; h.jstar = -1;
+        }
+        CK(cudaMemcpyAsync(pp->ps, &h, sizeof h, cudaMemcpyHostToDevice, st));
+    }
     // b_j = x~_j' x~_*  (identity (1)); b_j* = n exactly
     if (d->dt == DT_F64) launch_xstar<double>(pp);
     else if (d->dt == DT_F32) launch_xstar<float>(pp);
     else launch_xstar<int8_t>(pp);
+    if (d->sharded && pp->star_root >= 0) {      // C2: x_* - c_* (and its sum) from its owner
+        d->comm->bcast(pp->vtmp, 8 * (size_t)pp->vlen, pp->star_root, st);
+        d->comm->bcast(&pp->ps->sum_v, 8, pp->star_root, st);
+    }
     {
         ScanArgs sa{};
         sa.K1 = &pp->ps->sum_v;
@@ -546,8 +793,8 @@ bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double a
     CK(cudaStreamSynchronize(st));
     pp->prep_bytes = 3.0 * (double)d->n * itemsize(d->dt) * (double)d->p;
     if (!(pp->hps.Y2 > 0.0)) raise(BL_ERR_DEGENERATE, "y is constant on the used rows (y~ == 0)");
-    if (pp->hps.n_live == 0 && d->world == 1) raise(BL_ERR_DEGENERATE, "every column has zero variance");
-    if (!(pp->hps.A > 0.0) && d->world == 1) raise(BL_ERR_DEGENERATE, "lambda_max == 0: y~ orthogonal to every column");
+    if (pp->hps.n_live == 0 && (d->world == 1 || d->sharded)) raise(BL_ERR_DEGENERATE, "every column has zero variance");
+    if (!(pp->hps.A > 0.0) && (d->world == 1 || d->sharded)) raise(BL_ERR_DEGENERATE, "lambda_max == 0: y~ orthogonal to every column");
     guard.pp = nullptr;
     return pp;
 }
@@ -574,8 +821,11 @@ struct WorkingSet {
     int size() const { return (int)sorted.size(); }
 };
 
+// W holds GLOBAL column indices (= local ones unless the design is sharded).
 void upload_W(bl_prep *pp, const WorkingSet &ws, const std::vector<int> &added) {
+    bl_design *d = pp->d;
     const size_t nW = ws.sorted.size();
+    const int off = (int)d->col_offset;
     ensure_W(pp, (int64_t)nW);
     ensure_host(pp->hup, pp->hup_cap, 3 * nW + added.size() + 1);
     cudaStream_t st = pp->stream;
@@ -583,22 +833,51 @@ void upload_W(bl_prep *pp, const WorkingSet &ws, const std::vector<int> &added) 
     std::vector<int> ord(nW);
     for (size_t q = 0; q < nW; q++) ord[q] = (int)q;
     std::sort(ord.begin(), ord.end(), [&](int u, int v) { return ws.slots[u] < ws.slots[v]; });
+    // this shard's new columns (local indices) -> the "in W" flags of the scans
+    std::vector<int> mine;
+    for (int g : added)
+        if (g >= off && g < off + d->p) mine.push_back(g - off);
     // pinned staging: the previous round ended with a stream sync, so hup is free
     int *h = pp->hup;
-    std::memcpy(h, ws.sorted.data(), 4 * nW);
-    std::memcpy(h + nW, ws.slots.data(), 4 * nW);
+    for (size_t q = 0; q < nW; q++) { h[q] = ws.sorted[q] - off; h[nW + q] = ws.slots[q] - off; }
     std::memcpy(h + 2 * nW, ord.data(), 4 * nW);
-    std::memcpy(h + 3 * nW, added.data(), 4 * added.size());
+    std::memcpy(h + 3 * nW, mine.data(), 4 * mine.size());
     if (nW) {
-        CK(cudaMemcpyAsync(pp->W, h, 4 * nW, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(pp->Wst_d, h + nW, 4 * nW, cudaMemcpyHostToDevice, st));
+        if (!d->sharded) {
+            CK(cudaMemcpyAsync(pp->W, h, 4 * nW, cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(pp->Wst_d, h + nW, 4 * nW, cudaMemcpyHostToDevice, st));
+        }
         CK(cudaMemcpyAsync(pp->ord_d, h + 2 * nW, 4 * nW, cudaMemcpyHostToDevice, st));
     }
-    if (!added.empty()) {
-        CK(cudaMemcpyAsync(pp->viol, h + 3 * nW, 4 * added.size(), cudaMemcpyHostToDevice, st));
-        k_set_flags<<<(unsigned)((added.size() + 255) / 256), 256, 0, st>>>(pp->viol, (int)added.size(), pp->wflag, 1);
+    if (!mine.empty()) {
+        CK(cudaMemcpyAsync(pp->viol, h + 3 * nW, 4 * mine.size(), cudaMemcpyHostToDevice, st));
+        k_set_flags<<<(unsigned)((mine.size() + 255) / 256), 256, 0, st>>>(pp->viol, (int)mine.size(), pp->wflag, 1);
         CKL();
         pp->launches++;
+    }
+    if (d->sharded && !added.empty()) {
+        // C4: each new column is broadcast by its owner into every rank's store (slots
+        // nW - |added| ..; a shard's columns are contiguous in that order)
+        const int64_t slot0 = (int64_t)nW - (int64_t)added.size();
+        ensure_Ws(pp, (int64_t)nW, slot0);
+        const size_t isz = itemsize(d->dt), colb = (size_t)d->ld * isz;
+        CK(cudaMemsetAsync(pp->bw + slot0, 0, 8 * added.size(), st));
+        size_t q = 0;
+        for (int r = 0; r < d->world; r++) {
+            const size_t q0 = q;
+            while (q < added.size() && added[q] < d->shard_off[r + 1]) q++;
+            const int k = (int)(q - q0);
+            if (k == 0) continue;
+            if (r == d->rank) {
+                k_pack_cols<<<k, 256, 0, st>>>((const char *)d->X, (int64_t)colb, pp->viol, k, pp->c, pp->s,
+                                               (char *)pp->Xw, pp->cw, pp->sw, pp->bw, (int)(slot0 + q0));
+                CKL();
+                pp->launches++;
+            }
+            d->comm->bcast((char *)pp->Xw + (size_t)(slot0 + q0) * colb, colb * k, r, st);
+            d->comm->bcast(pp->cw + slot0 + q0, 8 * (size_t)k, r, st);
+            d->comm->bcast(pp->sw + slot0 + q0, 8 * (size_t)k, r, st);
+        }
     }
 }
 
@@ -612,6 +891,14 @@ std::vector<int> read_list(bl_prep *pp, const int *dev, int count) {
         std::sort(v.begin(), v.end());
     }
     return v;
+}
+
+// A device list of local column indices -> sorted GLOBAL indices (all-gathered
+// over the shards of a sharded design: C3).
+std::vector<int> global_list(bl_prep *pp, const int *dev, int count) {
+    if (!pp->d->sharded) return read_list(pp, dev, count);
+    const int64_t c = count;
+    return gather_list(pp, dev, gather_i64(pp, &c, 1));
 }
 
 // CD block shape: rows per thread R <= RM in {4, 8, 16}; RM <= 8 kernels are
@@ -637,15 +924,16 @@ const void *cd_kernel(int dt, bool mask, int R) {
 
 void launch_cd(bl_prep *pp, int nW, double lam, double alpha, double tol, int max_iter) {
     bl_design *d = pp->d;
+    const CdView v = cd_view(pp);
     CdArgs ca{};
-    ca.X = d->X;
+    ca.X = v.X;
     ca.ld = d->ld;
     ca.n = (int)d->n;
-    ca.W = pp->W;
+    ca.W = v.Wsorted;
     ca.nW = nW;
-    ca.c = pp->c;
-    ca.s = pp->s;
-    ca.beta = pp->beta;
+    ca.c = v.c;
+    ca.s = v.s;
+    ca.beta = v.beta;
     ca.r = pp->rfull;
     ca.r_scan = pp->rscan;
     ca.mask = pp->has_mask ? pp->mask : nullptr;
@@ -725,8 +1013,9 @@ void launch_gram_t(bl_prep *pp, int nW) {
     const void *kern = (const void *)k_gram<T, M>;
     allow_dyn_smem(kern);
     dim3 grid(nW - pp->nG, (nW + 255) / 256);
-    k_gram<T, M><<<grid, 256, 8 * d->n, pp->stream>>>((const T *)d->X, d->ld, (int)d->n, pp->Wst_d, nW, pp->nG,
-                                                       (int)pp->ldG, pp->c, pp->s, M ? pp->mask : nullptr,
+    const CdView v = cd_view(pp);
+    k_gram<T, M><<<grid, 256, 8 * d->n, pp->stream>>>((const T *)v.X, d->ld, (int)d->n, v.Wst, nW, pp->nG,
+                                                       (int)pp->ldG, v.c, v.s, M ? pp->mask : nullptr,
                                                        1.0 / pp->nt, pp->G);
     CKL();
     pp->launches++;
@@ -736,8 +1025,9 @@ template <typename T, bool M>
 void launch_resid_t(bl_prep *pp, int nW) {
     bl_design *d = pp->d;
     int nb = (int)((d->ld + 255) / 256);
-    k_resid_update<T, M><<<nb, 256, 0, pp->stream>>>((const T *)d->X, d->ld, (int)d->n, pp->Wst_d, nW, pp->dbeta,
-                                                     pp->c, pp->s, M ? pp->mask : nullptr, pp->rfull, pp->rscan,
+    const CdView v = cd_view(pp);
+    k_resid_update<T, M><<<nb, 256, 0, pp->stream>>>((const T *)v.X, d->ld, (int)d->n, v.Wst, nW, pp->dbeta,
+                                                     v.c, v.s, M ? pp->mask : nullptr, pp->rfull, pp->rscan,
                                                      pp->rpart);
     CKL();
     k_resid_finish<<<1, 32, 0, pp->stream>>>(pp->rpart, nb, pp->st);
@@ -770,26 +1060,27 @@ void solve_cd(bl_prep *pp, int nW, double lam, double alpha, double tol, int max
         else M ? launch_gram_t<int8_t, true>(pp, nW) : launch_gram_t<int8_t, false>(pp, nW);
         pp->nG = nW;
     }
+    const CdView v = cd_view(pp);
     {                                          // g_W = x~_W' r / n at the solve's starting residual
         ScanArgs sa{};
-        sa.list = pp->Wst_d;
+        sa.list = v.Wst;
         sa.nlist = nullptr;
         sa.nlist_host = nW;
         sa.K1 = &pp->st->sumr;
         sa.K2v = 1.0 / pp->nt;
-        sa.out = pp->z;
-        launch_scan(pp, sa, pp->rscan, false, false);
+        sa.out = v.z;
+        launch_scan(pp, sa, pp->rscan, false, false, d->sharded ? pp->Xw : nullptr, v.c, v.s);
     }
     CdGramArgs ga{};
-    ga.Wst = pp->Wst_d;
+    ga.Wst = v.Wst;
     ga.ord = pp->ord_d;
     ga.nW = nW;
     ga.ldG = (int)pp->ldG;
     ga.G = pp->G;
     ga.GA = pp->GA;
     ga.MA = pp->GA + pp->ldG * pp->ldG;
-    ga.z = pp->z;
-    ga.beta = pp->beta;
+    ga.z = v.z;
+    ga.beta = v.beta;
     ga.dbeta = pp->dbeta;
     ga.lam_alpha = lam * alpha;
     ga.inv_den = 1.0 / (1.0 + lam * (1.0 - alpha));
@@ -797,8 +1088,8 @@ void solve_cd(bl_prep *pp, int nW, double lam, double alpha, double tol, int max
     ga.floor_ = 1e-13 * (alpha * lam + std::sqrt(pp->hps.Y2 / pp->nt));   // Q6 noise floor
     ga.max_iter = max_iter;
     ga.betaW_out = pp->betaW;
-    ga.c = pp->c;
-    ga.s = pp->s;
+    ga.c = v.c;
+    ga.s = v.s;
     ga.st = pp->st;
     // cluster Gram CD: R CTAs of 256 threads (CTA 0 leads, 1..R-1 own the gradients)
     const int R = cd_cluster();
@@ -864,7 +1155,7 @@ bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, doubl
         pp->launches++;
         CK(cudaMemcpyAsync(pp->hst, pp->st, sizeof(RoundStatus), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        std::vector<int> all = read_list(pp, pp->scope, pp->hst->nscope);
+        std::vector<int> all = global_list(pp, pp->scope, pp->hst->nscope);
         upload_W(pp, W, W.add(all));
     }
 
@@ -900,7 +1191,7 @@ bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, doubl
                 pp->launches++;
                 CK(cudaMemcpyAsync(pp->hst, pp->st, sizeof(RoundStatus), cudaMemcpyDeviceToHost, st));
                 CK(cudaStreamSynchronize(st));
-                strong_next = read_list(pp, pp->strong, pp->hst->nstrong);
+                strong_next = global_list(pp, pp->strong, pp->hst->nstrong);
                 first = false;
             }
             upload_W(pp, W, W.add(strong_next));
@@ -949,19 +1240,30 @@ bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, doubl
             out->cd_updates += pp->hst->cd_updates;
             out->cd_cycles += pp->hst->cd_cycles;
             for (int u = 0; u < 4; u++) out->cd_prof[u] += pp->hst->cd_prof[u];
-            scanned += use_bedpp ? pp->hst->nscope : pp->hps.n_live;
+            // the round's counts over all shards (C3): violators, strong candidates, columns scanned
+            std::vector<int64_t> cnt = {pp->hst->nviol, pp->hst->nstrong, pp->hst->nscope};
+            if (d->sharded) cnt = gather_i64(pp, cnt.data(), 3);
+            int64_t nviol = 0, nscope = 0;
+            std::vector<int64_t> cv(d->sharded ? d->world : 1), cs(cv.size());
+            for (size_t r = 0; r < cv.size(); r++) {
+                cv[r] = cnt[3 * r];
+                cs[r] = cnt[3 * r + 1];
+                nviol += cnt[3 * r];
+                nscope += cnt[3 * r + 2];
+            }
+            scanned += use_bedpp ? nscope : pp->hps.n_live;
             if (pp->hst->cd_status) { status = BL_ERR_CONVERGENCE; break; }
-            if (pp->hst->nviol > 0) {
+            if (nviol > 0) {
                 if (++rounds > max_rounds) {
                     g_err = "more than max KKT rounds at one lambda";
                     status = BL_ERR_CONVERGENCE;
                     break;
                 }
-                std::vector<int> v = read_list(pp, pp->viol, pp->hst->nviol);
+                std::vector<int> v = d->sharded ? gather_list(pp, pp->viol, cv) : read_list(pp, pp->viol, pp->hst->nviol);
                 upload_W(pp, W, W.add(v));
                 continue;
             }
-            strong_next = read_list(pp, pp->strong, pp->hst->nstrong);
+            strong_next = d->sharded ? gather_list(pp, pp->strong, cs) : read_list(pp, pp->strong, pp->hst->nstrong);
             break;
         }
         if (status != BL_OK) {
@@ -983,7 +1285,7 @@ bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, doubl
             double bq = pp->hbw[q];
             if (bq == 0.0) continue;
             double cq = pp->hbw[nW + q], sq = pp->hbw[2 * nW + q];
-            out->feat.push_back(W.sorted[q] + d->col_offset);
+            out->feat.push_back(W.sorted[q]);
             out->beta_std.push_back(bq);
             out->beta_orig.push_back(bq / sq);
             shift += bq * cq / sq;
@@ -1111,6 +1413,7 @@ bl_status bl_load_design(const void *X, bl_dtype dt, int64_t n, int64_t p_local,
         d->rank = 0;
         d->world = 1;
         d->comm = nullptr;
+        d->sharded = false;
         d->col_offset = 0;
         d->p_global = p_local;
         CK(cudaGetDevice(&d->device));
@@ -1143,11 +1446,67 @@ bl_status bl_load_design(const void *X, bl_dtype dt, int64_t n, int64_t p_local,
             CK(cudaMemset(d->X, 0, bytes));
             CK(cudaMemcpy2D(d->X, ldp * isz, X, ld * isz, n * isz, p_local, cudaMemcpyHostToDevice));
         }
+        d->sharded = false;
+        d->shard_off.assign(2, 0);
+        d->shard_off[1] = p_local;
         if (d->world > 1) {
-            if (!dist->nccl_unique_id) { if (d->owned) cudaFree(d->X); delete d; raise(BL_ERR_ARG, "nccl_unique_id required for world > 1"); }
-            ncclUniqueId id;
-            std::memcpy(&id, dist->nccl_unique_id, sizeof id);
-            CKN(ncclCommInitRank(&d->comm, d->world, id, d->rank));
+            try {
+                if (!dist->nccl_unique_id) raise(BL_ERR_ARG, "nccl_unique_id (or loopback group key) required for world > 1");
+                if (dist->backend == 1) {
+                    auto *lc = new LoopComm();
+                    d->comm = lc;
+                    lc->rank = d->rank;
+                    lc->world = d->world;
+                    lc->key.assign((const char *)dist->nccl_unique_id, 128);
+                    std::lock_guard<std::mutex> lk(g_loop_mu);
+                    auto &g = g_loop_groups[lc->key];
+                    if (!g) {
+                        g = std::make_shared<LoopGroup>();
+                        g->world = d->world;
+                        g->stage.resize(d->world);
+                    }
+                    if (g->world != d->world) raise(BL_ERR_ARG, "loopback group world mismatch");
+                    g->members++;
+                    lc->g = g;
+                } else if (dist->backend == 0) {
+                    auto *nc = new NcclComm();
+                    d->comm = nc;
+                    nc->rank = d->rank;
+                    nc->world = d->world;
+                    ncclUniqueId id;
+                    std::memcpy(&id, dist->nccl_unique_id, sizeof id);
+                    CKN(ncclCommInitRank(&nc->c, d->world, id, d->rank));
+                } else {
+                    raise(BL_ERR_ARG, "bad bl_dist backend %d", dist->backend);
+                }
+                // shard table (C0): every rank's (col_offset, p_local), in rank order
+                int64_t *dbuf = nullptr;
+                CK(cudaMalloc(&dbuf, 16 * (size_t)(d->world + 1)));
+                const int64_t mine[2] = {d->col_offset, p_local};
+                CK(cudaMemcpy(dbuf, mine, 16, cudaMemcpyHostToDevice));
+                std::vector<int64_t> all(2 * (size_t)d->world);
+                d->comm->allgather(dbuf, dbuf + 2, 16, 0);
+                CK(cudaMemcpy(all.data(), dbuf + 2, 16 * (size_t)d->world, cudaMemcpyDeviceToHost));
+                cudaFree(dbuf);
+                d->shard_off.assign(d->world + 1, 0);
+                for (int r = 0; r < d->world; r++) {
+                    if (all[2 * r] != d->shard_off[r]) raise(BL_ERR_ARG, "shards must be contiguous in rank order (rank %d col_offset %lld)", r, (long long)all[2 * r]);
+                    d->shard_off[r + 1] = d->shard_off[r] + all[2 * r + 1];
+                }
+                d->sharded = d->world > 1 && d->p_global != p_local;
+                if (d->sharded && d->shard_off[d->world] != d->p_global) raise(BL_ERR_ARG, "shards cover %lld columns, p_global = %lld", (long long)d->shard_off[d->world], (long long)d->p_global);
+                if (!d->sharded) {
+                    for (int r = 0; r < d->world; r++)
+                        if (all[2 * r] != 0 || all[2 * r + 1] != p_local) raise(BL_ERR_ARG, "replicated design: every rank must hold all columns");
+                    d->shard_off.assign(2, 0);
+                    d->shard_off[1] = p_local;
+                }
+            } catch (...) {
+                delete d->comm;
+                if (d->owned) cudaFree(d->X);
+                delete d;
+                throw;
+            }
         }
         *out = d;
     });
@@ -1262,7 +1621,6 @@ bl_status bl_fit_path(bl_design *d, const double *y, const double *lambda, int n
         if (!d || d->magic != MAGIC_DESIGN) raise(BL_ERR_ARG, "bad design handle");
         if (!out) raise(BL_ERR_ARG, "out is NULL");
         *out = nullptr;
-        if (d->world > 1) raise(BL_ERR_ARG, "multi-GPU bl_fit_path is not available in this build");
         *out = fit_impl(d, y, nullptr, lambda, n_lambda, alpha, tol, max_iter, screen, opts, &s);
     });
     return g != BL_OK ? g : s;
@@ -1319,8 +1677,8 @@ bl_status bl_cv(bl_design *d, const double *y, const double *lambda, int n_lambd
         // each fit's CD kernel occupies one SM, so the folds share the GPU instead of queueing.
         // With world > 1 ranks, fold f runs on rank f mod world (replicated X) and E is summed.
         std::vector<int> mine;
-        for (int fo = 0; fo < n_folds; fo++)
-            if (fo % d->world == d->rank) mine.push_back(fo);
+        for (int fo = 0; fo < n_folds; fo++)             // sharded: every fit is collective -> all folds
+            if (d->sharded || fo % d->world == d->rank) mine.push_back(fo);
         std::vector<bl_status> fst(mine.size() + 1, BL_OK);
         std::vector<std::string> ferr(mine.size() + 1);
         std::vector<bl_path *> full(1, nullptr);
@@ -1354,7 +1712,9 @@ bl_status bl_cv(bl_design *d, const double *y, const double *lambda, int n_lambd
                 ferr[idx] = "host allocation failed";
             }
         };
-        {
+        if (d->sharded) {                               // collectives must be issued in the same order
+            for (size_t idx = 0; idx <= mine.size(); idx++) run_fold(idx);
+        } else {
             std::vector<std::thread> th;
             for (size_t idx = 0; idx <= mine.size(); idx++) th.emplace_back(run_fold, idx);
             for (auto &t : th) t.join();
@@ -1363,10 +1723,9 @@ bl_status bl_cv(bl_design *d, const double *y, const double *lambda, int n_lambd
         for (size_t idx = 0; idx < fst.size(); idx++)
             if (fst[idx] != BL_OK && s == BL_OK) { s = fst[idx]; g_err = ferr[idx]; }
         CK(cudaDeviceSynchronize());
-        if (d->world > 1) {
+        if (d->world > 1 && !d->sharded) {            // replicated: each rank ran its own folds
             std::lock_guard<std::mutex> lk(d->comm_mu);
-            CKN(ncclAllReduce(dE, dE, (size_t)n_lambda * n, ncclDouble, ncclSum, d->comm, 0));
-            CK(cudaStreamSynchronize(0));
+            d->comm->allreduce_sum(dE, (size_t)n_lambda * n, 0);
         }
         k_cv_reduce<<<n_lambda, 256>>>(dE, (int)n, dcv, dcv + n_lambda);
         CKL();
@@ -1446,7 +1805,7 @@ void bl_free(void *handle) {
         bl_design *d = (bl_design *)handle;
         for (bl_prep *pp : d->pool) free_prep(pp);
         d->pool.clear();
-        if (d->comm) ncclCommDestroy(d->comm);
+        delete d->comm;
         if (d->owned && d->X) cudaFree(d->X);
         d->magic = MAGIC_DEAD;
         delete d;

@@ -2069,6 +2069,29 @@ __global__ void __launch_bounds__(kG7Threads, 1) k_cd_gram7(CdGramArgs a, G7Work
     }
 }
 
+// ------------------------------------- sharded designs: working-set column store
+__global__ void k_iota(int *__restrict__ v, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) v[i] = i;
+}
+// Owner side of the column broadcast (C4): local columns cols[0..k) -> store
+// slots slot0.. (raw bytes, ld elements each) with their c, s.  grid = (k, any).
+__global__ void k_pack_cols(const char *__restrict__ X, int64_t col_bytes, const int *__restrict__ cols, int k,
+                            const double *__restrict__ c, const double *__restrict__ s, char *__restrict__ Xw,
+                            double *__restrict__ cw, double *__restrict__ sw, double *__restrict__ bw, int slot0) {
+    const int q = blockIdx.x;
+    if (q >= k) return;
+    const int j = cols[q];
+    const int4 *src = reinterpret_cast<const int4 *>(X + (int64_t)j * col_bytes);
+    int4 *dst = reinterpret_cast<int4 *>(Xw + (int64_t)(slot0 + q) * col_bytes);
+    for (int64_t i = threadIdx.x; i < col_bytes / 16; i += blockDim.x) dst[i] = src[i];
+    if (threadIdx.x == 0) {
+        cw[slot0 + q] = c[j];
+        sw[slot0 + q] = s[j];
+        bw[slot0 + q] = 0.0;
+    }
+}
+
 // ------------------------------------------------ a12: cross-validation errors
 // E[i] = r_i^2 for the held-out rows (mask == 0) of one fold at one lambda:
 // r on held-out rows is y_i - yhat_i from the fold's fit (the CD keeps the full-row

@@ -303,3 +303,47 @@ def test_cfg2_full_size_sampled():
         op = oracle.fit_path(inst, inst.y, [lams[k]], tol=1e-10)
         bo = op.beta[:, 0]
         assert np.abs(B[:, k] - bo).max() <= 1e-5 * np.abs(bo).max()
+
+
+def _sparse_col(gp, k, p):
+    b = np.zeros(p)
+    sl = slice(gp.col_ptr[k], gp.col_ptr[k + 1])
+    b[gp.feat[sl]] = gp.beta_std[sl]
+    return b
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg,ks", [("cfg3", (40, 99)), ("cfg4", (99,))])
+def test_full_size_sampled(cfg, ks):
+    """BASELINE cfg3 (fp32, p = 10^6, elastic net) and cfg4 (int8 GWAS-shaped,
+    p = 1,339,511) exactly as bench.py runs them (device-resident X, hybrid
+    screening, tol 1e-7): lambda_max against the oracle's full pass; at sampled
+    lambdas the KKT audit of the GPU solution over all p columns, and the GPU
+    solution against a cold-started oracle solve (the unique minimiser) to the
+    north-star tolerances."""
+    inst = synth.CONFIGS[cfg](device="cuda")
+    p, a = inst.p, inst.alpha
+    src = (inst.host_X(), inst.n)
+    d = bl.Design(inst.X, inst.n)
+    lm_g = d.lambda_max(inst.y, a)
+    lm_o = oracle.lambda_max(src, inst.y, a)[0]
+    assert lm_g == pytest.approx(lm_o, rel=1e-12)
+    lams = synth.lambda_grid(lm_g, 100, inst.ratio)
+    gp = d.fit_path(inst.y, lams, alpha=a, tol=inst.tol)
+    assert gp.n_converged == 100
+    for k in ks:
+        bg = _sparse_col(gp, k, p)
+        zv, nv = oracle.kkt(src, inst.y, bg, lams[k], a)
+        assert zv <= 1e-6 and nv <= 1e-6, (k, zv, nv)
+        op = oracle.fit_path(src, inst.y, [lams[k]], alpha=a, tol=1e-10)
+        bo = op.beta[:, 0]
+        scale = np.abs(bo).max()
+        assert np.abs(bg - bo).max() <= 1e-5 * scale, (k, np.abs(bg - bo).max() / scale)
+        qo = oracle.objective(src, inst.y, bo, lams[k], a)
+        qg = oracle.objective(src, inst.y, bg, lams[k], a)
+        assert abs(qg - qo) / qo <= 1e-7
+        ao, ag = np.abs(bo) >= 1e-8, np.abs(bg) >= 1e-8
+        if not np.array_equal(ao, ag):
+            _, _, z = oracle.kkt(src, inst.y, bo, lams[k], a, want_z=True)
+            bad = np.flatnonzero(ao != ag)
+            assert np.all(np.abs(np.abs(z[bad]) - a * lams[k]) <= 1e-9), bad
