@@ -10,8 +10,12 @@ through the C ABI (libbl.so).  Default workload = BASELINE cfg2 (configs[1]):
 n = 1000, p = 100,000, fp32 AR(1) design, alpha = 1, lambda to 0.1 lambda_max.
 X (400 MB) is larger than L2, so no flush is needed between steps.
 
-N > 1 (torchrun): each rank runs its own replica of the path (weak scaling, no
-data-path collective -- see DESIGN.md section 7); the time is the max over ranks.
+N > 1 (torchrun): the design is column-sharded over the ranks (whole
+1000-column blocks, BASELINE north star): scans, BEDPP and the strong rule run
+per shard, the small index lists are all-gathered and the working-set columns
+broadcast by their owners over NCCL, the CD runs replicated (DESIGN.md section
+7).  The same path is solved at every N (strong scaling); the time is the max
+over ranks.
 
 `--impl reference` times the fp64 CPU oracle (oracle/, naive CD, no screening)
 on this box's host cores on a bounded column sample of the same workload.
@@ -153,15 +157,31 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    inst = make_instance(args.config, device=f"cuda:{local_rank}")
+    if world > 1 and args.config == "cfg5":
+        j0, j1 = bl.shard_range(synth.cfg5.__defaults__[2], world, rank, block=synth.BLOCK)
+        inst = synth.cfg5(device=f"cuda:{local_rank}", col_range=(j0, j1))
+        p_global = synth.cfg5.__defaults__[2]
+    else:
+        inst = make_instance(args.config, device=f"cuda:{local_rank}")
+        p_global = inst.p
+        j0, j1 = bl.shard_range(p_global, world, rank, block=synth.BLOCK)
     X = inst.X if not isinstance(inst.X, np.ndarray) else torch.from_numpy(inst.X).cuda()
-    d = bl.Design(X, inst.n)
+    if world > 1 and X.shape[0] != j1 - j0:             # this rank's shard only
+        X = X[j0:j1].contiguous()
+        inst.X = X
+        torch.cuda.empty_cache()
+    dist_of = (lambda: bl.make_dist(rank, world, (j0, j1), p_global, device=local_rank)) if world > 1 else (lambda: None)
+    d = bl.Design(X, inst.n, dist=dist_of())
     lm = d.lambda_max(inst.y, inst.alpha)
     lams = synth.lambda_grid(lm, inst.nlam, inst.ratio)
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
 
+    is_cv = args.config == "cfg5"        # BASELINE cfg5: 10-fold CV -- a step is the whole CV
+
     def step(profile):
+        if is_cv:
+            return d.cv(inst.y, lams, K=10, alpha=inst.alpha, tol=inst.tol, seed=0, profile=profile, cd=args.cd)
         return d.fit_path(inst.y, lams, alpha=inst.alpha, tol=inst.tol, stream=sh, profile=profile, cd=args.cd)
 
     for _ in range(args.warmup):
@@ -185,7 +205,7 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
         dist.barrier()
-    last = perfs[-1]
+    last = perfs[-1].full if is_cv else perfs[-1]
     scan_ms = sum(p.perf["scan_ms"] for p in perfs)
     scan_bytes = sum(p.perf["scan_bytes"] for p in perfs)
     scan_launches = sum(p.perf["scan_launches"] for p in perfs)
@@ -197,21 +217,27 @@ def run_ours(args, rank, world, local_rank):
     cd_prof = [sum(p.perf["cd_prof"][u] for p in perfs) / args.steps / max(visits, 1) for u in range(4)]
 
     # end to end through the C ABI with HOST buffers (H2D of X inside the timed region)
-    Xh_t = torch.empty(X.shape, dtype=X.dtype, pin_memory=True)
-    Xh_t.copy_(X)
-    Xh = Xh_t.numpy()
-    e2e = []
-    for _ in range(max(1, min(args.steps, 3))):
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        dh = bl.Design(Xh, inst.n)
-        lm_h = dh.lambda_max(inst.y, inst.alpha)
-        ph = dh.fit_path(inst.y, synth.lambda_grid(lm_h, inst.nlam, inst.ratio), alpha=inst.alpha, tol=inst.tol)
-        dh.free()
-        torch.cuda.synchronize()
-        e2e.append(time.perf_counter() - t0)
-    h2d = Xh.nbytes + 8 * inst.n * 2 + 8 * inst.nlam
-    d2h = int(ph.beta_std.nbytes * 2 + ph.feat.nbytes + 8 * inst.nlam * 3)
+    x_bytes = X.numel() * X.element_size()
+    e2e, h2d, d2h = [], 0, 0
+    if x_bytes <= 40e9:
+        Xh_t = torch.empty(X.shape, dtype=X.dtype, pin_memory=True)
+        Xh_t.copy_(X)
+        Xh = Xh_t.numpy()
+        for _ in range(max(1, min(args.steps, 3))):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            dh = bl.Design(Xh, inst.n, dist=dist_of())
+            lm_h = dh.lambda_max(inst.y, inst.alpha)
+            lams_h = synth.lambda_grid(lm_h, inst.nlam, inst.ratio)
+            if is_cv:
+                ph = dh.cv(inst.y, lams_h, K=10, alpha=inst.alpha, tol=inst.tol, seed=0).full
+            else:
+                ph = dh.fit_path(inst.y, lams_h, alpha=inst.alpha, tol=inst.tol)
+            dh.free()
+            torch.cuda.synchronize()
+            e2e.append(time.perf_counter() - t0)
+        h2d = Xh.nbytes + 8 * inst.n * 2 + 8 * inst.nlam
+        d2h = int(ph.beta_std.nbytes * 2 + ph.feat.nbytes + 8 * inst.nlam * 3)
 
     if rank != 0:
         return
@@ -230,14 +256,17 @@ def run_ours(args, rank, world, local_rank):
         cpu = {"value": v, "unit": "s", "cores": 1, "kind": "oracle", "sample": sample, "raw_seconds": raw}
     line = {
         "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+        "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": {"cfg1": "f64", "cfg4": "i8"}.get(args.config, "f32") + "-in/f64-accum",
         "data": "synthetic",
-        "config": {"workload": args.config, "n": inst.n, "p": inst.p, "alpha": inst.alpha,
+        "config": {"workload": args.config, "n": inst.n, "p": p_global, "alpha": inst.alpha,
                    "n_lambda": inst.nlam, "lambda_min_ratio": inst.ratio, "tol": inst.tol,
-                   "screen": "hybrid (SSR-BEDPP)", "cd": args.cd, "X_bytes": int(X.numel() * X.element_size()),
+                   "screen": "hybrid (SSR-BEDPP)", "cd": args.cd, "X_bytes": int(x_bytes),
+                   "cv_folds": 10 if is_cv else None,
                    "l2_policy": "X larger than L2 (126 MB); no flush" if X.numel() * X.element_size() > 126e6
-                   else "X fits L2 (reported as such)", "parallelism": f"replicas x{world}"},
+                   else "X fits L2 (reported as such)", "parallelism": f"column-sharded x{world}" if world > 1 else "1 GPU",
+                   "p_global": p_global},
         "roofline": {"kernel": "k_scan_fp/k_scan_i8 (fused KKT + strong-rule scan)", "bound": "hbm",
                      "achieved": achieved, "peak": pk["hbm_gbs"], "peak_source": pk_src, "unit": "GB/s",
                      "frac": achieved / pk["hbm_gbs"] if achieved else None, "traffic": traffic,
@@ -250,8 +279,9 @@ def run_ours(args, rank, world, local_rank):
                      "cd_phase_cycles_per_visit": dict(zip(["lead", "bulk", "build_A", "catch_up"], cd_prof)),
                      "algorithmic_bytes_per_step": scan_bytes / args.steps},
         "cpu_baseline": cpu,
-        "e2e": {"value": statistics.median(e2e), "unit": "s", "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": d2h},
+        "e2e": ({"value": statistics.median(e2e), "unit": "s", "h2d_bytes_per_step": int(h2d),
+                 "d2h_bytes_per_step": d2h} if e2e else
+                {"value": None, "unit": "s", "note": "X > 40 GB: no pinned host copy on this box"}),
         "gpu_launches": int(launches / args.steps),
         "path": {"nnz_last": int(last.col_ptr[-1] - last.col_ptr[-2]), "kkt_rounds": int(last.kkt_rounds.sum()),
                  "cd_passes": int(last.passes.sum()), "cols_scanned": int(last.cols_scanned.sum()),

@@ -169,6 +169,9 @@ bl_status bl_path_perf(const bl_path *path, bl_perf *out);
 bl_status bl_cv_copy(const bl_cvres *cv, double *cve, double *cvse, int *lambda_min_index,
                      int32_t *fold_id_out, const bl_path **full_fit);
 bl_status bl_cv_errors(const bl_cvres *cv, double *E /* n_lambda x n, row-major */);
+/* Performance counters summed over every fit of the CV (K folds + the full-data
+ * fit; wall_ms = the slowest fit), filled when opts->profile == 1. */
+bl_status bl_cv_perf(const bl_cvres *cv, bl_perf *out);
 
 /* ---- single steps of the path, for parity tests and diagnostics ---------------
  * bl_prepare: one-time preprocessing for (y, optional training mask) (SURVEY 8(a)

@@ -60,7 +60,7 @@ class bl_perf(ctypes.Structure):
 
 _lib = None
 EXPORTS = ["bl_load_design", "bl_nccl_unique_id", "bl_lambda_max", "bl_fit_path", "bl_cv", "bl_path_info",
-           "bl_path_copy", "bl_path_perf", "bl_cv_copy", "bl_cv_errors", "bl_prepare", "bl_prep_copy",
+           "bl_path_copy", "bl_path_perf", "bl_cv_copy", "bl_cv_errors", "bl_cv_perf", "bl_prepare", "bl_prep_copy",
            "bl_bedpp", "bl_scan", "bl_free", "bl_last_error"]
 
 
@@ -84,6 +84,7 @@ def lib():
     L.bl_path_perf.argtypes = [P, P]
     L.bl_cv_copy.argtypes = [P, P, P, P, P, PP]
     L.bl_cv_errors.argtypes = [P, P]
+    L.bl_cv_perf.argtypes = [P, P]
     L.bl_prepare.argtypes = [P, P, P, D, PP]
     L.bl_prep_copy.argtypes = [P, P, P, P, P, P, P]
     L.bl_bedpp.argtypes = [P, D, P, P]
@@ -281,6 +282,9 @@ class CvResult:
         self.lambda_min_index = lmin.value
         self.E = np.empty((K_lam, n))
         _check(L.bl_cv_errors(handle, _p(self.E)))
+        pf = bl_perf()
+        _check(L.bl_cv_perf(handle, ctypes.byref(pf)))
+        self.perf = pf.as_dict()
         self.full = Path(full, BL_OK) if full.value else None
 
 

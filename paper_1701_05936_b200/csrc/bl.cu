@@ -206,6 +206,8 @@ struct bl_cvres {
     std::vector<double> cve, cvse, E;
     std::vector<int32_t> fold_id;
     bl_path *full;
+    bl_perf perf;            // summed over every fit of the CV (folds + full data)
+    std::mutex perf_mu;
 };
 
 // Per-(y, row mask) device workspace: one arena allocation carved into the
@@ -1367,6 +1369,16 @@ bl_path *fit_impl(bl_design *d, const double *y, const uint8_t *train, const dou
     return out;
 }
 
+void add_perf(bl_cvres *cv, const bl_perf &p) {
+    std::lock_guard<std::mutex> lk(cv->perf_mu);
+    bl_perf &q = cv->perf;
+    q.scan_ms += p.scan_ms; q.scan_bytes += p.scan_bytes; q.scan_launches += p.scan_launches;
+    q.cd_ms += p.cd_ms; q.cd_launches += p.cd_launches; q.prep_ms += p.prep_ms; q.prep_bytes += p.prep_bytes;
+    q.kernel_launches += p.kernel_launches; q.wall_ms = std::max(q.wall_ms, p.wall_ms);
+    q.cd_visits += p.cd_visits; q.cd_updates += p.cd_updates; q.cd_kernel_cycles += p.cd_kernel_cycles;
+    for (int u = 0; u < 4; u++) q.cd_prof[u] += p.cd_prof[u];
+}
+
 uint64_t splitmix64(uint64_t &state) {
     uint64_t z = (state += 0x9E3779B97F4A7C15ULL);
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
@@ -1665,6 +1677,7 @@ bl_status bl_cv(bl_design *d, const double *y, const double *lambda, int n_lambd
         cv->fold_id = f;
         cv->E.assign((size_t)n_lambda * n, 0.0);
         cv->full = nullptr;
+        std::memset(&cv->perf, 0, sizeof cv->perf);
         CK(cudaSetDevice(d->device));
         // device E (n_lambda x n): fold fits write disjoint held-out rows, so they run concurrently
         double *dE = nullptr, *dcv = nullptr;
@@ -1694,6 +1707,7 @@ bl_status bl_cv(bl_design *d, const double *y, const double *lambda, int n_lambd
                     bl_status fs = BL_OK;
                     bl_path *pth = fit_impl(d, y, train.data(), lambda, n_lambda, alpha, tol, max_iter,
                                             BL_SCREEN_HYBRID, &fo_opts, &fs, dE);
+                    add_perf(cv, pth->perf);
                     delete pth;
                     fst[idx] = fs;
                     if (fs != BL_OK) ferr[idx] = g_err;
@@ -1701,6 +1715,7 @@ bl_status bl_cv(bl_design *d, const double *y, const double *lambda, int n_lambd
                     bl_status fs = BL_OK;
                     full[0] = fit_impl(d, y, nullptr, lambda, n_lambda, alpha, tol, max_iter, BL_SCREEN_HYBRID,
                                        &fo_opts, &fs);
+                    add_perf(cv, full[0]->perf);
                     fst[idx] = fs;
                     if (fs != BL_OK) ferr[idx] = g_err;
                 }
@@ -1788,6 +1803,14 @@ bl_status bl_cv_copy(const bl_cvres *cv, double *cve, double *cvse, int *lambda_
         if (lambda_min_index) *lambda_min_index = cv->lmin;
         if (fold_id_out) std::copy(cv->fold_id.begin(), cv->fold_id.end(), fold_id_out);
         if (full_fit) *full_fit = cv->full;
+    });
+}
+
+bl_status bl_cv_perf(const bl_cvres *cv, bl_perf *out) {
+    return guard([&] {
+        if (!cv || cv->magic != MAGIC_CV) raise(BL_ERR_ARG, "bad cv handle");
+        if (!out) raise(BL_ERR_ARG, "out is NULL");
+        *out = cv->perf;
     });
 }
 

@@ -156,7 +156,7 @@ def _torch_dev(device):
 def _gen(device, seed, block):
     import torch
     g = torch.Generator(device=device)
-    g.manual_seed((seed * 1_000_003 + block * 7919 + 17) & 0x7FFF_FFFF_FFFF_FFFF)
+    g.manual_seed(int(seed * 1_000_003 + int(block) * 7919 + 17) & 0x7FFF_FFFF_FFFF_FFFF)
     return g
 
 
