@@ -1484,6 +1484,34 @@ struct G7Work {              // global workspace of one fit (see bl.cu gram_ws)
     uint8_t *inA;            // nW: slot is in the set G_AA was built for
 };
 
+// mbarrier / st.async helpers (CTA-local barriers; st.async writes 8 bytes into a
+// peer CTA's shared memory and completes them on the peer's mbarrier)
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arm(uint64_t *bar, unsigned bytes) {          // arrive + expect_tx
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_addr(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ uint32_t mapa(const void *p, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_async(uint32_t remote, double v, uint32_t remote_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
+                 ::"r"(remote), "l"(__double_as_longlong(v)), "r"(remote_bar) : "memory");
+}
+
 __device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory"); }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
 
@@ -1494,9 +1522,10 @@ __global__ void __launch_bounds__(kG7Threads, 1) k_cd_gram7(CdGramArgs a, G7Work
     extern __shared__ __align__(16) double sm[];
     __shared__ __align__(16) double dfull[32];         // leader: the block's updates (0 = none)
     __shared__ __align__(16) double rsh[32];
-    __shared__ __align__(16) double zsnap[2][32];      // owners: gradients of the next block (read by the leader)
-    __shared__ __align__(16) double dpub[2][32];       // leader: the block's updates (read by the owners)
-    __shared__ __align__(16) double dq[32];            // owners: local copy of the previous block's updates
+    constexpr int DZ = 4, DDMAX = kG7MaxR + 2;
+    __shared__ __align__(16) double zst[DZ][32];       // leader: ring of block gradients (st.async by the owners)
+    __shared__ __align__(16) double dq[DDMAX][32];     // owners: ring of the leader's block updates (st.async)
+    __shared__ __align__(8) uint64_t zfull[DZ], dfb[DDMAX], sfull[3], sempty[3];
     __shared__ int bslot[3][32];                       // leader: slots of the block
     __shared__ int ctl[2][8];                          // leader: command for the cluster (double-buffered)
     __shared__ int wcount[33];
@@ -1533,6 +1562,20 @@ __global__ void __launch_bounds__(kG7Threads, 1) k_cd_gram7(CdGramArgs a, G7Work
         }
     }
     for (int w = rank * T_ + t; w < nW; w += R * T_) wk.g[w] = a.z[a.Wst[w]];
+    // hand-off rings: slot / phase of block number gb (counted over all sweeps) are
+    // gb % D and (gb / D) & 1.  DD = NB + 2 slots bound every owner's lag: the
+    // leader only writes block gb's updates after the snapshots of blocks
+    // gb-NB+1..gb, which each owner sends after consuming the updates 2 blocks before.
+    const int DD = NB + 2;
+    if (t == 0) {
+        if (leader_cta) {
+            for (int u = 0; u < DZ; u++) { mbar_init(&zfull[u], 1); mbar_arm(&zfull[u], 256); }
+            for (int u = 0; u < 3; u++) { mbar_init(&sfull[u], kG7Helpers); mbar_init(&sempty[u], 1); }
+        } else {
+            for (int u = 0; u < DD; u++) { mbar_init(&dfb[u], 1); mbar_arm(&dfb[u], 256); }
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     __threadfence();
     cl.sync();
 
@@ -1606,12 +1649,12 @@ __global__ void __launch_bounds__(kG7Threads, 1) k_cd_gram7(CdGramArgs a, G7Work
         return (a0 + a1) + (a2 + a3);
     };
 
-    // leader warp: block at positions b0.. (stage buf; gradients in the owner's zsnap[zb]); acc = link term
-    auto lead = [&](bool active, int b0, int buf, int zb, double acc) {
+    // leader warp: block at positions b0.. (stage buf; zo = the owner's snapshot); acc = link term;
+    // gb = block number (ring slot of the published updates)
+    auto lead = [&](bool active, int b0, int buf, double zo, double acc, long long gb) {
         const long long t0 = clock64();
         const int s = bslot[buf][lane];
         const bool valid = s >= 0;
-        const double zo = cl.map_shared_rank(&zsnap[0][0], 1 + ((b0 >> 5) % NB))[zb * 32 + lane];
         double zc = 0.0, bo = 0.0;
         if (valid) {
             bo = bS[s];
@@ -1695,8 +1738,11 @@ __global__ void __launch_bounds__(kG7Threads, 1) k_cd_gram7(CdGramArgs a, G7Work
         }
         const long long t3 = clock64();
         dbg[2] += t3 - t2;
-        // publish the 32 updates (dense, local; the owners read them after the barrier)
-        dpub[(b0 >> 5) & 1][lane] = dfin;
+        // publish the 32 updates into every owner's ring slot (st.async, completes on its mbarrier)
+        {
+            const int ds = (int)(gb % DD);
+            for (int r = 1; r < R; r++) st_async(mapa(&dq[ds][lane], r), dfin, mapa(&dfb[ds], r));
+        }
         dfull[lane] = dfin;
         retries += round;
         dm = fmax(dm, fabs(dfin));
@@ -1728,97 +1774,116 @@ __global__ void __launch_bounds__(kG7Threads, 1) k_cd_gram7(CdGramArgs a, G7Work
         }
     };
 
-    // one sweep over `len` positions (active: act list; full: slots)
+    // one sweep over `len` positions (active: act list; full: slots).  No cluster
+    // barrier per block: the leader waits on its snapshot ring, the owners on
+    // their update ring, the leader's prefetch helpers on the stage ring.
+    long long gq = 0;                                       // blocks processed so far (all sweeps)
     auto sweep = [&](bool active, int len) {
         visits += len;
         const double *Mx = active ? a.GA : a.G;
         const int Q = (len + 31) >> 5;
-        // owner: its first position pair, with the G rows of the previous block in registers
-        const int k0 = 2 * t < owned ? own_pos(2 * t) : -1;
-        const int e0 = 2 * t;
-        double2 rv[32];
-        double acc = 0.0;
+        const long long g0 = gq;
+        gq += Q;
         if (leader_cta) {
-            if (wid == 0) { dm = 0.0; bm = 0.0; }
-            if (wid > 0) { prefetch(Mx, active, len, 0, 0); if (Q > 1) prefetch(Mx, active, len, 1, 1); }
-        } else if (wid == 0 && rank == 1) {                  // block 0's owner snapshots its gradients
-            zsnap[0][lane] = lane < len ? gl[lidx(lane)] : 0.0;
-        }
-        cluster_arrive();
-        // owners: the previous block's updates (read from the leader) -> every owned gradient
-        auto owner_apply = [&](int qp) {
-            if (wid == 0) dq[lane] = cl.map_shared_rank(&dpub[0][0], 0)[(qp & 1) * 32 + lane];
-            __syncthreads();
-            if (k0 >= 0) {
-                double gx = gl[e0], gy = gl[e0 + 1], hx = 0.0, hy = 0.0;
-#pragma unroll
-                for (int i = 0; i < 32; i += 2) {
-                    const double2 dd = *reinterpret_cast<const double2 *>(&dq[i]);
-                    gx = fma(-dd.x, rv[i].x, gx);
-                    gy = fma(-dd.x, rv[i].y, gy);
-                    hx = fma(-dd.y, rv[i + 1].x, hx);
-                    hy = fma(-dd.y, rv[i + 1].y, hy);
-                }
-                gl[e0] = gx + hx;
-                gl[e0 + 1] = gy + hy;
-            }
-            for (int e = e0 + 2 * T_; e < owned; e += 2 * T_) {   // further pairs: direct loads
-                const int k = own_pos(e);
-                if (k >= len) continue;
-                double gx = gl[e], gy = gl[e + 1];
-                for (int i = 0; i < 32; i++) {
-                    const double d = dq[i];
-                    if (d == 0.0) continue;
-                    const double2 g2 = __ldcg(reinterpret_cast<const double2 *>(Mx + (int64_t)(32 * qp + i) * ldG + k));
-                    gx = fma(-d, g2.x, gx);
-                    gy = fma(-d, g2.y, gy);
-                }
-                gl[e] = gx;
-                gl[e + 1] = gy;
-            }
-            __syncthreads();
-        };
-        for (int q = 0; q < Q; q++) {
-            const long long c0 = clock64();
-            if (leader_cta) {
-                cluster_wait();
-                if (wid == 0) {
-                    lead(active, 32 * q, q % 3, q & 1, acc);
-                    cluster_arrive();
-                    if (q + 1 < Q) { __syncwarp(); acc = link((q + 1) % 3); }
+            if (wid == 0) {
+                dm = 0.0;
+                bm = 0.0;
+                double acc = 0.0;
+                for (int q = 0; q < Q; q++) {
+                    const long long gb = g0 + q, c0 = clock64();
+                    const int ss = (int)(gb % 3), zs = (int)(gb % DZ);
+                    mbar_wait(&sfull[ss], (unsigned)((gb / 3) & 1));     // Gd, M, slots of block q
+                    mbar_wait(&zfull[zs], (unsigned)((gb / DZ) & 1));    // the owner's snapshot
+                    const long long c1 = clock64();
+                    dbg[4] += c1 - c0;
+                    const double zo = zst[zs][lane];
+                    __syncwarp();
+                    if (lane == 0) mbar_arm(&zfull[zs], 256);               // for block gb + DZ
+                    lead(active, 32 * q, ss, zo, acc, gb);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&sempty[ss]);                // stage free for block gb + 3
+                    if (q + 1 < Q) {
+                        const long long gn = gb + 1;
+                        mbar_wait(&sfull[gn % 3], (unsigned)((gn / 3) & 1));
+                        acc = link((int)(gn % 3));
+                    }
                     if (t == 0) pr_lead += clock64() - c0;
-                } else {
-                    if (q + 2 < Q) prefetch(Mx, active, len, q + 2, (q + 2) % 3);
-                    cluster_arrive();
                 }
             } else {
-                cluster_wait();
-                const long long c1 = clock64();
-                if (q > 0) owner_apply(q - 1);
-                const long long c2 = clock64();
-                dbg[5] += c2 - c1;
-                if (q + 1 < Q && wid == 0 && ((q + 1) % NB) == rank - 1) {   // snapshot of the next block
-                    const int k = 32 * (q + 1) + lane;
-                    zsnap[(q + 1) & 1][lane] = k < len ? gl[lidx(k)] : 0.0;
+                for (int q = 0; q < Q; q++) {                            // helpers: every block's stage
+                    const long long gb = g0 + q;
+                    const int ss = (int)(gb % 3);
+                    if (gb >= 3) mbar_wait(&sempty[ss], (unsigned)((gb / 3 - 1) & 1));
+                    prefetch(Mx, active, len, q, ss);
+                    mbar_arrive(&sfull[ss]);
                 }
-                cluster_arrive();
-                dbg[6] += clock64() - c2;
-                // G rows of block q for the next step (rows past the end: zero)
-                if (k0 >= 0) {
+            }
+        } else {
+            const int e0 = 2 * t;
+            const int k0 = e0 < owned ? own_pos(e0) : -1;
+            double2 rv[32];
+            auto load_rows = [&](int qq) {                 // G rows of block qq at this thread's first pair
+                if (k0 < 0) return;
 #pragma unroll
-                    for (int i = 0; i < 32; i++) {
-                        const int row = 32 * q + i;
-                        rv[i] = row < len ? __ldcg(reinterpret_cast<const double2 *>(Mx + (int64_t)row * ldG + k0))
-                                          : make_double2(0.0, 0.0);
-                    }
+                for (int i = 0; i < 32; i++) {
+                    const int row = 32 * qq + i;
+                    rv[i] = row < len ? __ldcg(reinterpret_cast<const double2 *>(Mx + (int64_t)row * ldG + k0))
+                                      : make_double2(0.0, 0.0);
                 }
+            };
+            auto send_snap = [&](int qq) {                 // warp 0: block qq's gradients -> the leader's ring
+                if (wid != 0 || qq >= Q || (qq % NB) != rank - 1) return;
+                const long long gb = g0 + qq;
+                const int zs = (int)(gb % DZ);
+                const int k = 32 * qq + lane;
+                st_async(mapa(&zst[zs][lane], 0), k < len ? gl[lidx(k)] : 0.0, mapa(&zfull[zs], 0));
+            };
+            send_snap(0);                                  // blocks 0 and 1 need no update first
+            send_snap(1);
+            load_rows(0);
+            for (int j = 0; j < Q; j++) {
+                const long long gb = g0 + j, c0 = clock64();
+                const int ds = (int)(gb % DD);
+                mbar_wait(&dfb[ds], (unsigned)((gb / DD) & 1));
+                const long long c1 = clock64();
+                dbg[4] += c1 - c0;
+                if (k0 >= 0) {
+                    double gx = gl[e0], gy = gl[e0 + 1], hx = 0.0, hy = 0.0;
+#pragma unroll
+                    for (int i = 0; i < 32; i += 2) {
+                        const double2 dd = *reinterpret_cast<const double2 *>(&dq[ds][i]);
+                        gx = fma(-dd.x, rv[i].x, gx);
+                        gy = fma(-dd.x, rv[i].y, gy);
+                        hx = fma(-dd.y, rv[i + 1].x, hx);
+                        hy = fma(-dd.y, rv[i + 1].y, hy);
+                    }
+                    gl[e0] = gx + hx;
+                    gl[e0 + 1] = gy + hy;
+                }
+                for (int e = e0 + 2 * T_; e < owned; e += 2 * T_) {   // further pairs: direct loads
+                    const int k = own_pos(e);
+                    if (k >= len) continue;
+                    double gx = gl[e], gy = gl[e + 1];
+                    for (int i = 0; i < min(32, len - 32 * j); i++) {
+                        const double d = dq[ds][i];
+                        if (d == 0.0) continue;
+                        const double2 g2 = __ldcg(reinterpret_cast<const double2 *>(Mx + (int64_t)(32 * j + i) * ldG + k));
+                        gx = fma(-d, g2.x, gx);
+                        gy = fma(-d, g2.y, gy);
+                    }
+                    gl[e] = gx;
+                    gl[e + 1] = gy;
+                }
+                __syncthreads();
+                if (t == 0) mbar_arm(&dfb[ds], 256);                // for block gb + DD
+                send_snap(j + 2);
+                if (j + 1 < Q) load_rows(j + 1);
+                dbg[5] += clock64() - c1;
                 if (t == 0) pr_bulk += clock64() - c0;
             }
         }
-        cluster_wait();
-        if (!leader_cta && Q > 0) owner_apply(Q - 1);        // flush: block Q-1's updates everywhere
         __syncthreads();
-        cl.sync();                                            // the leader's dpub is read before it changes
+        cl.sync();
     };
 
     // leader CTA: active list into act (smem) and the global copy
@@ -2027,7 +2092,7 @@ __global__ void __launch_bounds__(kG7Threads, 1) k_cd_gram7(CdGramArgs a, G7Work
     if (!leader_cta) {
         if (rank == 1 && t == 0) {
             a.st->cd_prof[1] = pr_bulk;
-            for (int u = 4; u < 8; u++) a.st->cd_dbg[u] = dbg[u];
+            for (int u = 4; u < 7; u++) a.st->cd_dbg[u] = dbg[u];
         }
         return;
     }
@@ -2066,6 +2131,7 @@ __global__ void __launch_bounds__(kG7Threads, 1) k_cd_gram7(CdGramArgs a, G7Work
         a.st->cd_cnt[2] = ncatch;
         a.st->cd_cnt[3] = nfull;
         for (int u = 0; u < 4; u++) a.st->cd_dbg[u] = dbg[u];
+        a.st->cd_dbg[7] = dbg[4];                           // leader: waits for snapshots / stages
     }
 }
 

@@ -60,7 +60,7 @@ std::vector<double> run(int ver, int nW, int passes_wanted, double lam, int R = 
         k_cd_gram6<false><<<1, kGram6Threads, gram6_smem(nW)>>>(a);
     } else {
         const void *kern = (const void *)k_cd_gram7<false>;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         if (R > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         void *args[] = {&a, &wk};
         cudaLaunchConfig_t cfg{};
@@ -86,10 +86,10 @@ std::vector<double> run(int ver, int nW, int passes_wanted, double lam, int R = 
            (double)h.cd_prof[3] / h.cd_visits, h.cd_cnt[0], h.cd_cnt[1], h.cd_cnt[2], h.cd_cnt[3],
            cudaGetErrorString(cudaGetLastError()));
     if (ver == 7) {
-        printf("      leader: zc %.1f  M %.1f  FS %.1f  tail %.1f | owner: pull %.1f apply %.1f push %.1f | sync(owner) %.1f  (cycles/visit)\n",
+        printf("      leader: zc %.1f  M %.1f  FS %.1f  tail %.1f | owner: wait %.1f apply+send %.1f | leader wait %.1f  (cycles/visit)\n",
                (double)h.cd_dbg[0] / h.cd_visits, (double)h.cd_dbg[1] / h.cd_visits, (double)h.cd_dbg[2] / h.cd_visits,
                (double)h.cd_dbg[3] / h.cd_visits, (double)h.cd_dbg[4] / h.cd_visits, (double)h.cd_dbg[5] / h.cd_visits,
-               (double)h.cd_dbg[6] / h.cd_visits, (double)h.cd_dbg[7] / h.cd_visits);
+               (double)h.cd_dbg[7] / h.cd_visits);
     }
     cudaFree(dG); cudaFree(dz); cudaFree(dbeta); cudaFree(ddb); cudaFree(dbw); cudaFree(dc); cudaFree(ds);
     cudaFree(dW); cudaFree(dord); cudaFree(dst); cudaFree(dGA);
