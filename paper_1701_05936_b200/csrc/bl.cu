@@ -978,14 +978,25 @@ G7Work gram_ws(bl_prep *pp) {
     return w;
 }
 
-// cluster size of the Gram CD kernel (CTA 0 leads, 1..R-1 own the gradients)
+// cluster size of the Gram CD kernel (CTA 0 leads, 1..R-1 own the gradients): 8
+// (portable), or 4 / 16 with BL_CD_CLUSTER
 int cd_cluster() {
     static int r = [] {
         const char *e = std::getenv("BL_CD_CLUSTER");
         int v = e ? std::atoi(e) : 8;
-        return std::min(std::max(v, 2), (int)kG7MaxR);
+        return v <= 4 ? 4 : v <= 8 ? 8 : 16;
     }();
     return r;
+}
+const void *gram7_kernel(bool enet, int R) {
+    static std::once_flag once;
+    std::call_once(once, [] {       // 16-CTA clusters are a non-portable size
+        cudaFuncSetAttribute((const void *)k_cd_gram7<false, 16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute((const void *)k_cd_gram7<true, 16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    });
+    if (R == 4) return enet ? (const void *)k_cd_gram7<true, 4> : (const void *)k_cd_gram7<false, 4>;
+    if (R == 16) return enet ? (const void *)k_cd_gram7<true, 16> : (const void *)k_cd_gram7<false, 16>;
+    return enet ? (const void *)k_cd_gram7<true, 8> : (const void *)k_cd_gram7<false, 8>;
 }
 void ensure_G(bl_prep *pp, int64_t need) {
     if (need <= pp->ldG) return;
@@ -1095,26 +1106,13 @@ void solve_cd(bl_prep *pp, int nW, double lam, double alpha, double tol, int max
     ga.st = pp->st;
     // cluster Gram CD: R CTAs of 256 threads (CTA 0 leads, 1..R-1 own the gradients)
     const int R = cd_cluster();
-    const void *kern = alpha < 1.0 ? (const void *)k_cd_gram7<true> : (const void *)k_cd_gram7<false>;
+    const void *kern = gram7_kernel(alpha < 1.0, R);
     const size_t smem = gram7_smem(nW, R);
     const size_t lim = allow_dyn_smem(kern);
     if (smem > lim) raise(BL_ERR_OOM, "Gram CD shared memory %zu > %zu (|W| = %d)", smem, lim, nW);
-    if (R > 8) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     G7Work wk = gram_ws(pp);
     void *args[] = {&ga, &wk};
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(R);
-    cfg.blockDim = dim3(kG7Threads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = pp->stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = R;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    CK(cudaLaunchKernelExC(&cfg, kern, args));
+    CK(cudaLaunchKernel(kern, dim3(R), dim3(kG7Threads), args, smem, pp->stream));
     pp->launches++;
     if (d->dt == DT_F64) M ? launch_resid_t<double, true>(pp, nW) : launch_resid_t<double, false>(pp, nW);
     else if (d->dt == DT_F32) M ? launch_resid_t<float, true>(pp, nW) : launch_resid_t<float, false>(pp, nW);

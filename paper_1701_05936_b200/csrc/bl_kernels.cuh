@@ -1465,11 +1465,12 @@ __global__ void __launch_bounds__(kGram6Threads, 1) k_cd_gram6(CdGramArgs a) {
 constexpr int kG7Threads = 256;
 constexpr int kG7Helpers = kG7Threads - 32;
 constexpr int kG7MaxR = 16;
+constexpr int kG7Stages = 4;                    // leader prefetch ring (Gd, Gp, M per stage)
 __host__ __device__ constexpr size_t gram7_smem(int nW, int R) {
-    // 9 x 8 KB leader buffers (3 stages of Gd, Gp, M) + the larger of the leader's
+    // 3 x kG7Stages x 8 KB leader buffers (stages of Gd, Gp, M) + the larger of the leader's
     // per-slot state (bS, bcat: 16 B; act, actp: 8 B; inA: 1 B) and an owner's
     // gradients + slots (12 B per owned position)
-    return (size_t)9 * 8192 +
+    return (size_t)3 * kG7Stages * 8192 +
            ((size_t)25 * (size_t)((nW + 33) & ~1) > (size_t)12 * (size_t)(nW / (R - 1) + 64)
                 ? (size_t)25 * (size_t)((nW + 33) & ~1)
                 : (size_t)12 * (size_t)(nW / (R - 1) + 64)) +
@@ -1515,8 +1516,10 @@ __device__ __forceinline__ void st_async(uint32_t remote, double v, uint32_t rem
 __device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory"); }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
 
-template <bool ENET>
-__global__ void __launch_bounds__(kG7Threads, 1) k_cd_gram7(CdGramArgs a, G7Work wk) {
+// The cluster shape is compiled in (__cluster_dims__) so the kernel launches with
+// <<<>>> (profilers do not see cudaLaunchKernelExC launches).
+template <bool ENET, int RC>
+__global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd_gram7(CdGramArgs a, G7Work wk) {
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     extern __shared__ __align__(16) double sm[];
@@ -1525,8 +1528,10 @@ __global__ void __launch_bounds__(kG7Threads, 1) k_cd_gram7(CdGramArgs a, G7Work
     constexpr int DZ = 4, DDMAX = kG7MaxR + 2;
     __shared__ __align__(16) double zst[DZ][32];       // leader: ring of block gradients (st.async by the owners)
     __shared__ __align__(16) double dq[DDMAX][32];     // owners: ring of the leader's block updates (st.async)
-    __shared__ __align__(8) uint64_t zfull[DZ], dfb[DDMAX], sfull[3], sempty[3];
-    __shared__ int bslot[3][32];                       // leader: slots of the block
+    constexpr int NS = kG7Stages;
+    __shared__ __align__(8) uint64_t zfull[DZ], dfb[DDMAX], sfull[NS], sempty[NS];
+    __shared__ int bslot[NS][32];                      // leader: slots of the block
+    __shared__ uint32_t rdq[kG7MaxR], rdfb[kG7MaxR];    // leader: owners' ring addresses (shared::cluster)
     __shared__ int ctl[2][8];                          // leader: command for the cluster (double-buffered)
     __shared__ int wcount[33];
     __shared__ double red[32];
@@ -1538,17 +1543,17 @@ __global__ void __launch_bounds__(kG7Threads, 1) k_cd_gram7(CdGramArgs a, G7Work
     const int nW = a.nW;
     const int nWp = (nW + 1) & ~1;
     const int64_t ldG = a.ldG;
-    double(*Gd)[32][32] = reinterpret_cast<double(*)[32][32]>(sm);            // [3]: strictly lower diag sub-block
-    double(*Gp)[32][32] = Gd + 3;                                              // [3]: previous block -> this block
-    double(*Mb)[32][32] = Gd + 6;                                              // [3]: M, column-major ([c][b])
+    double(*Gd)[32][32] = reinterpret_cast<double(*)[32][32]>(sm);            // [NS]: strictly lower diag sub-block
+    double(*Gp)[32][32] = Gd + NS;                                             // [NS]: previous block -> this block
+    double(*Mb)[32][32] = Gd + 2 * NS;                                         // [NS]: M, column-major ([c][b])
     // leader CTA per-slot state
-    double *bS = sm + 9 * 1024;                             // coefficients, by slot
+    double *bS = sm + 3 * NS * 1024;                        // coefficients, by slot
     double *bcat = bS + nWp;                                // coefficients at the last lazy catch-up
     int *act = reinterpret_cast<int *>(bcat + nWp);         // active slots (ascending)
     int *actp = act + nWp;                                  // the set G_AA / M were built for
     uint8_t *inA = reinterpret_cast<uint8_t *>(actp + nWp);
     // owner CTAs: gradients of the owned positions (local index = (j / NB) * 32 + k % 32) and their slots
-    double *gl = sm + 9 * 1024;
+    double *gl = sm + 3 * NS * 1024;
     const int gcap = (nW / 32 / NB + 2) * 32;
     int *sl = reinterpret_cast<int *>(gl + gcap);
     int owned = 0;                                          // owners: local positions currently held
@@ -1570,7 +1575,8 @@ __global__ void __launch_bounds__(kG7Threads, 1) k_cd_gram7(CdGramArgs a, G7Work
     if (t == 0) {
         if (leader_cta) {
             for (int u = 0; u < DZ; u++) { mbar_init(&zfull[u], 1); mbar_arm(&zfull[u], 256); }
-            for (int u = 0; u < 3; u++) { mbar_init(&sfull[u], kG7Helpers); mbar_init(&sempty[u], 1); }
+            for (int u = 0; u < NS; u++) { mbar_init(&sfull[u], kG7Helpers); mbar_init(&sempty[u], 1); }
+            for (int r = 1; r < R; r++) { rdq[r] = mapa(&dq[0][0], r); rdfb[r] = mapa(&dfb[0], r); }
         } else {
             for (int u = 0; u < DD; u++) { mbar_init(&dfb[u], 1); mbar_arm(&dfb[u], 256); }
         }
@@ -1604,32 +1610,41 @@ __global__ void __launch_bounds__(kG7Threads, 1) k_cd_gram7(CdGramArgs a, G7Work
     };
 
     // leader helpers: prefetch block qn's sub-blocks (and M in active sweeps) into stage buf
+    // leader helpers: prefetch block qn's sub-blocks into stage buf with 16-byte loads:
+    // the strictly lower diagonal block (full sweeps only -- active sweeps solve with
+    // M and fetch it only on a misprediction), the link from block qn-1, M (active).
+    // All loads of a thread are issued before its shared-memory stores.
     auto prefetch = [&](const double *Mx, bool active, int len, int qn, int buf) {
         const int u = t - 32;
         const int b0 = 32 * qn, nb1 = min(32, len - b0);
         const int nb0 = qn > 0 ? 32 : 0;
-        constexpr int NP = (3072 + kG7Helpers - 1) / kG7Helpers;
-        double v[NP];
+        constexpr int NP = (1536 + kG7Helpers - 1) / kG7Helpers;
+        double2 v[NP];
 #pragma unroll
         for (int k = 0; k < NP; k++) {
-            const int e = u + k * kG7Helpers;
-            const int r = (e >> 5) & 31, c = e & 31;
-            const double *src = nullptr;
-            if (e < 1024) {
-                if (c > r && c < nb1) src = Mx + (int64_t)(b0 + r) * ldG + b0 + c;
-            } else if (e < 2048) {
-                if (r < nb0 && c < nb1) src = Mx + (int64_t)(b0 - 32 + r) * ldG + b0 + c;
-            } else if (e < 3072 && active) {
-                src = a.MA + (int64_t)qn * 1024 + (e - 2048);
+            const int e = u + k * kG7Helpers;                 // pair index: [0,512) Gd, [512,1024) Gp, [1024,1536) M
+            const int r = (e >> 4) & 31, c = 2 * (e & 15);
+            const double2 *src = nullptr;
+            if (e < 512) {
+                if (!active && c + 1 > r && c < nb1) src = reinterpret_cast<const double2 *>(Mx + (int64_t)(b0 + r) * ldG + b0 + c);
+            } else if (e < 1024) {
+                if (r < nb0 && c < nb1) src = reinterpret_cast<const double2 *>(Mx + (int64_t)(b0 - 32 + r) * ldG + b0 + c);
+            } else if (e < 1536 && active) {
+                src = reinterpret_cast<const double2 *>(a.MA + (int64_t)qn * 1024 + 2 * (e - 1024));
             }
-            v[k] = src ? __ldcg(src) : 0.0;
+            v[k] = src ? __ldcg(src) : make_double2(0.0, 0.0);
+            if (e < 1024) {                                   // zero what lies outside the block / the lower part
+                const bool lo = e < 512;
+                if (lo ? !(c > r && c < nb1) : c >= nb1) v[k].x = 0.0;
+                if (lo ? !(c + 1 > r && c + 1 < nb1) : c + 1 >= nb1) v[k].y = 0.0;
+            }
         }
 #pragma unroll
         for (int k = 0; k < NP; k++) {
             const int e = u + k * kG7Helpers;
-            if (e < 1024) (&Gd[buf][0][0])[e] = v[k];
-            else if (e < 2048) (&Gp[buf][0][0])[e - 1024] = v[k];
-            else if (e < 3072 && active) (&Mb[buf][0][0])[e - 2048] = v[k];
+            if (e < 512) { if (!active) reinterpret_cast<double2 *>(&Gd[buf][0][0])[e] = v[k]; }
+            else if (e < 1024) reinterpret_cast<double2 *>(&Gp[buf][0][0])[e - 512] = v[k];
+            else if (e < 1536 && active) reinterpret_cast<double2 *>(&Mb[buf][0][0])[e - 1024] = v[k];
         }
         if (u < 32) bslot[buf][u] = u < nb1 ? (active ? act[b0 + u] : b0 + u) : -1;
     };
@@ -1689,6 +1704,12 @@ __global__ void __launch_bounds__(kG7Threads, 1) k_cd_gram7(CdGramArgs a, G7Work
             todo &= ~commit;
             if (mis) {
                 ++round;
+                {                                             // the strictly lower diagonal block (not prefetched)
+                    const int nb = __popc(__ballot_sync(FULL, valid));
+                    for (int r = 0; r < 32; r++)
+                        Gd[buf][r][lane] = (lane > r && lane < nb) ? __ldcg(a.GA + (int64_t)(b0 + r) * ldG + b0 + lane) : 0.0;
+                    __syncwarp();
+                }
                 unsigned cp = commit;
                 while (cp) {
                     const int p = __ffs(cp) - 1;
@@ -1741,7 +1762,8 @@ __global__ void __launch_bounds__(kG7Threads, 1) k_cd_gram7(CdGramArgs a, G7Work
         // publish the 32 updates into every owner's ring slot (st.async, completes on its mbarrier)
         {
             const int ds = (int)(gb % DD);
-            for (int r = 1; r < R; r++) st_async(mapa(&dq[ds][lane], r), dfin, mapa(&dfb[ds], r));
+            const uint32_t off = (uint32_t)((ds * 32 + lane) * 8), boff = (uint32_t)(ds * 8);
+            for (int r = 1; r < R; r++) st_async(rdq[r] + off, dfin, rdfb[r] + boff);
         }
         dfull[lane] = dfin;
         retries += round;
@@ -1791,8 +1813,8 @@ __global__ void __launch_bounds__(kG7Threads, 1) k_cd_gram7(CdGramArgs a, G7Work
                 double acc = 0.0;
                 for (int q = 0; q < Q; q++) {
                     const long long gb = g0 + q, c0 = clock64();
-                    const int ss = (int)(gb % 3), zs = (int)(gb % DZ);
-                    mbar_wait(&sfull[ss], (unsigned)((gb / 3) & 1));     // Gd, M, slots of block q
+                    const int ss = (int)(gb % NS), zs = (int)(gb % DZ);
+                    mbar_wait(&sfull[ss], (unsigned)((gb / NS) & 1));    // Gd, M, slots of block q
                     mbar_wait(&zfull[zs], (unsigned)((gb / DZ) & 1));    // the owner's snapshot
                     const long long c1 = clock64();
                     dbg[4] += c1 - c0;
@@ -1801,19 +1823,22 @@ __global__ void __launch_bounds__(kG7Threads, 1) k_cd_gram7(CdGramArgs a, G7Work
                     if (lane == 0) mbar_arm(&zfull[zs], 256);               // for block gb + DZ
                     lead(active, 32 * q, ss, zo, acc, gb);
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&sempty[ss]);                // stage free for block gb + 3
+                    if (lane == 0) mbar_arrive(&sempty[ss]);                // stage free for block gb + NS
                     if (q + 1 < Q) {
-                        const long long gn = gb + 1;
-                        mbar_wait(&sfull[gn % 3], (unsigned)((gn / 3) & 1));
-                        acc = link((int)(gn % 3));
+                        const long long gn = gb + 1, c2 = clock64();
+                        mbar_wait(&sfull[gn % NS], (unsigned)((gn / NS) & 1));
+                        const long long c3 = clock64();
+                        dbg[5] += c3 - c2;
+                        acc = link((int)(gn % NS));
+                        dbg[6] += clock64() - c3;
                     }
                     if (t == 0) pr_lead += clock64() - c0;
                 }
             } else {
                 for (int q = 0; q < Q; q++) {                            // helpers: every block's stage
                     const long long gb = g0 + q;
-                    const int ss = (int)(gb % 3);
-                    if (gb >= 3) mbar_wait(&sempty[ss], (unsigned)((gb / 3 - 1) & 1));
+                    const int ss = (int)(gb % NS);
+                    if (gb >= NS) mbar_wait(&sempty[ss], (unsigned)((gb / NS - 1) & 1));
                     prefetch(Mx, active, len, q, ss);
                     mbar_arrive(&sfull[ss]);
                 }
@@ -2090,10 +2115,7 @@ __global__ void __launch_bounds__(kG7Threads, 1) k_cd_gram7(CdGramArgs a, G7Work
     }
     cl.sync();                                              // no DSMEM access past this point
     if (!leader_cta) {
-        if (rank == 1 && t == 0) {
-            a.st->cd_prof[1] = pr_bulk;
-            for (int u = 4; u < 7; u++) a.st->cd_dbg[u] = dbg[u];
-        }
+        if (rank == 1 && t == 0) a.st->cd_prof[1] = pr_bulk;
         return;
     }
     double l1 = 0.0, l2 = 0.0, nnz = 0.0;
@@ -2130,8 +2152,7 @@ __global__ void __launch_bounds__(kG7Threads, 1) k_cd_gram7(CdGramArgs a, G7Work
         a.st->cd_cnt[1] = rebuilds;
         a.st->cd_cnt[2] = ncatch;
         a.st->cd_cnt[3] = nfull;
-        for (int u = 0; u < 4; u++) a.st->cd_dbg[u] = dbg[u];
-        a.st->cd_dbg[7] = dbg[4];                           // leader: waits for snapshots / stages
+        for (int u = 0; u < 8; u++) a.st->cd_dbg[u] = dbg[u];   // leader warp sub-phases
     }
 }
 

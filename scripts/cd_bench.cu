@@ -59,20 +59,12 @@ std::vector<double> run(int ver, int nW, int passes_wanted, double lam, int R = 
         cudaFuncSetAttribute(k_cd_gram6<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         k_cd_gram6<false><<<1, kGram6Threads, gram6_smem(nW)>>>(a);
     } else {
-        const void *kern = (const void *)k_cd_gram7<false>;
+        const void *kern = R == 4 ? (const void *)k_cd_gram7<false, 4> : R == 16 ? (const void *)k_cd_gram7<false, 16>
+                                                                               : (const void *)k_cd_gram7<false, 8>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         if (R > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         void *args[] = {&a, &wk};
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(R);
-        cfg.blockDim = dim3(kG7Threads);
-        cfg.dynamicSmemBytes = gram7_smem(nW, R);
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = R; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        cudaError_t e = cudaLaunchKernelExC(&cfg, kern, args);
+        cudaError_t e = cudaLaunchKernel(kern, dim3(R), dim3(kG7Threads), args, gram7_smem(nW, R), 0);
         if (e != cudaSuccess) printf("launch: %s\n", cudaGetErrorString(e));
     }
     cudaDeviceSynchronize();
@@ -86,10 +78,10 @@ std::vector<double> run(int ver, int nW, int passes_wanted, double lam, int R = 
            (double)h.cd_prof[3] / h.cd_visits, h.cd_cnt[0], h.cd_cnt[1], h.cd_cnt[2], h.cd_cnt[3],
            cudaGetErrorString(cudaGetLastError()));
     if (ver == 7) {
-        printf("      leader: zc %.1f  M %.1f  FS %.1f  tail %.1f | owner: wait %.1f apply+send %.1f | leader wait %.1f  (cycles/visit)\n",
+        printf("      leader (cycles/visit): zc %.1f  M %.1f  FS %.1f  tail %.1f | wait snap+stage %.1f | link wait %.1f  link %.1f\n",
                (double)h.cd_dbg[0] / h.cd_visits, (double)h.cd_dbg[1] / h.cd_visits, (double)h.cd_dbg[2] / h.cd_visits,
                (double)h.cd_dbg[3] / h.cd_visits, (double)h.cd_dbg[4] / h.cd_visits, (double)h.cd_dbg[5] / h.cd_visits,
-               (double)h.cd_dbg[7] / h.cd_visits);
+               (double)h.cd_dbg[6] / h.cd_visits);
     }
     cudaFree(dG); cudaFree(dz); cudaFree(dbeta); cudaFree(ddb); cudaFree(dbw); cudaFree(dc); cudaFree(ds);
     cudaFree(dW); cudaFree(dord); cudaFree(dst); cudaFree(dGA);
