@@ -418,19 +418,19 @@ void launch_scan(bl_prep *pp, ScanArgs a, const double *v_dev, bool timed, bool 
         a.v = v_dev;
         int V = 16 / itemsize(d->dt);
         size_t smem = (size_t)8 * round_up(d->n, 32 * V);
-        if (d->dt == DT_F32) {
-            allow_dyn_smem((const void *)k_scan_fp<float, 4>);
-            int grid = grid_for((const void *)k_scan_fp<float, 4>, kScanThreads, smem, d->nsm);
-            EvPairOpt ev(pp, events ? (timed ? &pp->ev_scan : &pp->ev_prep) : nullptr);
-            k_scan_fp<float, 4><<<grid, kScanThreads, smem, pp->stream>>>(a);
-            CKL();
-        } else {
-            allow_dyn_smem((const void *)k_scan_fp<double, 4>);
-            int grid = grid_for((const void *)k_scan_fp<double, 4>, kScanThreads, smem, d->nsm);
-            EvPairOpt ev(pp, events ? (timed ? &pp->ev_scan : &pp->ev_prep) : nullptr);
-            k_scan_fp<double, 4><<<grid, kScanThreads, smem, pp->stream>>>(a);
-            CKL();
-        }
+        // columns per warp iteration: 4 (more loads in flight) unless that leaves a
+        // badly quantised last wave on a small full-width scan (experiment knob BL_SCAN_C)
+        static const int cenv = [] { const char *e = std::getenv("BL_SCAN_C"); return e ? std::atoi(e) : 0; }();
+        const int C = cenv ? cenv : 4;
+        const void *kern = d->dt == DT_F32 ? (C == 8 ? (const void *)k_scan_fp<float, 8> : C == 2 ? (const void *)k_scan_fp<float, 2>
+                                                                                              : (const void *)k_scan_fp<float, 4>)
+                                           : (C == 8 ? (const void *)k_scan_fp<double, 8> : C == 2 ? (const void *)k_scan_fp<double, 2>
+                                                                                              : (const void *)k_scan_fp<double, 4>);
+        allow_dyn_smem(kern);
+        int grid = grid_for(kern, kScanThreads, smem, d->nsm);
+        EvPairOpt ev(pp, events ? (timed ? &pp->ev_scan : &pp->ev_prep) : nullptr);
+        void *args[] = {&a};
+        CK(cudaLaunchKernel(kern, dim3(grid), dim3(kScanThreads), args, smem, pp->stream));
     }
     pp->launches++;
 }

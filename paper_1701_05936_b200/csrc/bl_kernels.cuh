@@ -397,6 +397,21 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_i8(ScanArgs a) {
         int acc[4] = {0, 0, 0, 0};
         const int8_t *lg = ls + g * LL + 16 * t;
         int r = 0;
+        for (; r + 256 <= ld; r += 256) {     // four 64-row blocks per step: 8 loads in flight per lane
+            int4 xa[4], xb[4], l[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                xa[u] = __ldcs(reinterpret_cast<const int4 *>(pa + r + 64 * u + 16 * t));
+                xb[u] = __ldcs(reinterpret_cast<const int4 *>(pb + r + 64 * u + 16 * t));
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) l[u] = *reinterpret_cast<const int4 *>(lg + r + 64 * u);
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                mma_s8(acc, xa[u].x, xb[u].x, xa[u].y, xb[u].y, l[u].x, l[u].y);
+                mma_s8(acc, xa[u].z, xb[u].z, xa[u].w, xb[u].w, l[u].z, l[u].w);
+            }
+        }
         for (; r + 128 <= ld; r += 128) {     // two 64-row blocks per step
             int4 xa0 = __ldcs(reinterpret_cast<const int4 *>(pa + r + 16 * t));
             int4 xb0 = __ldcs(reinterpret_cast<const int4 *>(pb + r + 16 * t));
