@@ -1,0 +1,12 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+(nproc; free -g; nvidia-smi) > gpurun_out/host.txt 2>&1
+timeout 1200 python -m pytest tests -m gpu -q --timeout 900 -rf > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 600 python bench.py --steps 3 --warmup 3 > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
+timeout 600 python bench.py --impl reference --steps 1 --warmup 0 > gpurun_out/bench_ref.log 2>&1; echo "ref rc=$?" >> gpurun_out/bench_ref.log
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_scan_fp -s 40 -c 1 -o gpurun_out/prof_scan_cfg2 python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_scan2.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_scan_i8 -s 40 -c 1 -o gpurun_out/prof_scan_cfg4 python bench.py --config cfg4 --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_scan4.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_cd_gram7 -s 300 -c 1 -o gpurun_out/prof_cd_cfg2 python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_cd.log 2>&1
+echo done
