@@ -347,3 +347,84 @@ def test_full_size_sampled(cfg, ks):
             _, _, z = oracle.kkt(src, inst.y, bo, lams[k], a, want_z=True)
             bad = np.flatnonzero(ao != ag)
             assert np.all(np.abs(np.abs(z[bad]) - a * lams[k]) <= 1e-9), bad
+
+
+def test_cfg5_shaped_cv_reduced_p():
+    """BASELINE cfg5 (10-fold CV elastic net, n = 10,000, fp32 iid, alpha 0.5,
+    lambda to 0.05 lambda_max, seeded-permutation folds) with the identical
+    generator, n, K, alpha and seed at reduced p: fold ids,
+    the held-out error matrix, cve / cvse / lambda_min and the full-data path
+    against the oracle's CV."""
+    inst = synth.cfg5(device="cuda", p=2000)
+    K, a = 10, inst.alpha
+    src = (inst.host_X(), inst.n)
+    f = oracle.folds(inst.n, K, 0)
+    lm = oracle.lambda_max(src, inst.y, a)[0]
+    lams = synth.lambda_grid(lm, 30, inst.ratio)
+    E, cve, cvse, lmin = oracle.cv(src, inst.y, f, K, lams, alpha=a, tol=1e-11)
+    g = bl.Design(inst.X, inst.n).cv(inst.y, lams, K=K, alpha=a, tol=1e-9, seed=0)
+    assert np.array_equal(g.fold_id, f)
+    np.testing.assert_allclose(g.E, E, rtol=1e-6, atol=1e-9 * E.max())
+    np.testing.assert_allclose(g.cve, cve, rtol=1e-7)
+    np.testing.assert_allclose(g.cvse, cvse, rtol=1e-6)
+    assert g.lambda_min_index == lmin
+    op = oracle.fit_path(src, inst.y, lams, alpha=a, tol=1e-11)
+    compare_path(synth.Instance("cfg5r", inst.host_X(), inst.n, inst.y, alpha=a), g.full, op, a)
+
+
+@pytest.mark.slow
+def test_cfg5_full_size_cv_certificate():
+    """BASELINE cfg5 at full size (80 GB fp32 design in HBM, 10-fold CV) exactly as
+    bench.py runs it.  The oracle cannot hold it; instead an
+    independent fp64 checker -- torch fp64 matmuls on the device, no library
+    kernel -- certifies the full-data fit at sampled lambdas: KKT conditions to
+    1e-6 over all 2,000,000 columns and the elastic-net duality gap (P - D small
+    relative to P)."""
+    import torch
+    inst = synth.cfg5(device="cuda")
+    X, n, a = inst.X, inst.n, inst.alpha
+    d = bl.Design(X, n)
+    lm = d.lambda_max(inst.y, a)
+    lams = synth.lambda_grid(lm, 100, inst.ratio)
+    g = d.cv(inst.y, lams, K=10, alpha=a, tol=inst.tol, seed=0)
+    assert np.array_equal(g.fold_id, oracle.folds(n, 10, 0))
+    assert np.all(np.isfinite(g.cve)) and 0 <= g.lambda_min_index < 100
+    full = g.full
+    assert full.n_converged == 100
+    # column statistics in fp64 (chunks of 50k columns)
+    y = torch.as_tensor(inst.y, device="cuda", dtype=torch.float64)
+    yt = y - y.mean()
+    p = X.shape[0]
+    c = torch.empty(p, dtype=torch.float64, device="cuda")
+    s = torch.empty_like(c)
+    CH = 50_000
+    for j0 in range(0, p, CH):
+        B = X[j0:j0 + CH, :n].double()
+        c[j0:j0 + CH] = B.mean(1)
+        s[j0:j0 + CH] = (B - c[j0:j0 + CH, None]).pow(2).mean(1).sqrt()
+    for k in (40, 99):
+        lam = lams[k]
+        sl = slice(full.col_ptr[k], full.col_ptr[k + 1])
+        idx = torch.as_tensor(full.feat[sl], device="cuda")
+        bv = torch.as_tensor(full.beta_std[sl], device="cuda", dtype=torch.float64)
+        Xa = (X[idx, :n].double() - c[idx, None]) / s[idx, None]          # (k, n) standardised active columns
+        r = yt - Xa.T @ bv
+        z = torch.empty(p, dtype=torch.float64, device="cuda")
+        for j0 in range(0, p, CH):
+            B = X[j0:j0 + CH, :n].double()
+            z[j0:j0 + CH] = (B @ r - c[j0:j0 + CH] * r.sum()) / (n * s[j0:j0 + CH])
+        beta = torch.zeros(p, dtype=torch.float64, device="cuda")
+        beta[idx] = bv
+        inactive = beta == 0
+        kkt0 = float((z[inactive].abs() - a * lam).max())
+        kkt1 = float((z[idx] - a * lam * torch.sign(bv) - lam * (1 - a) * bv).abs().max()) if len(idx) else 0.0
+        assert kkt0 <= 1e-6 and kkt1 <= 1e-6, (k, kkt0, kkt1)
+        # duality gap of the (1/2n)-scaled elastic net, SURVEY 8(c.5)
+        nu, lp = n * lam * (1 - a), n * a * lam
+        gvec = n * z - nu * beta
+        sc = max(lp, float(gvec.abs().max()))
+        rr, bb = float(r @ r), float(bv @ bv)
+        P = 0.5 * rr + 0.5 * nu * bb + lp * float(bv.abs().sum())
+        Y2 = float(yt @ yt)
+        D = 0.5 * Y2 - 0.5 * lp ** 2 * ((rr + nu * bb) / sc ** 2 - 2 * float(r @ yt) / (lp * sc) + Y2 / lp ** 2)
+        assert -1e-9 * P <= P - D <= 1e-5 * P, (k, P, D)
