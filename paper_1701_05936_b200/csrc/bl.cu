@@ -253,6 +253,8 @@ struct bl_prep {
     int64_t ldG;
     int nG;                 // slots whose G row/column is computed
     double *rpart;          // per-block partials of the residual refresh
+    double *rbuf;           // residual refresh: per-chunk row partials (grows)
+    size_t rbuf_cap;
     // sharded designs: device scratch of the collectives, and the working-set column
     // store (every rank holds the W columns, broadcast by their owners, in slot order)
     void *cbuf;
@@ -473,6 +475,7 @@ void free_prep(bl_prep *pp) {
     if (pp->G) cudaFree(pp->G);
     if (pp->GA) cudaFree(pp->GA);
     if (pp->cbuf) cudaFree(pp->cbuf);
+    if (pp->rbuf) cudaFree(pp->rbuf);
     if (pp->Xw) cudaFree(pp->Xw);
     if (pp->cw) cudaFree(pp->cw);
     if (pp->own) cudaStreamDestroy(pp->own);
@@ -532,6 +535,18 @@ void ensure_W(bl_prep *pp, int64_t need) {
     pp->betaW = (double *)(pp->warena + 3 * ib);
     pp->dbeta = pp->betaW + 3 * nc;
     pp->Wcap = nc;
+}
+
+double *ensure_rbuf(bl_prep *pp, size_t count) {
+    if (count <= pp->rbuf_cap) return pp->rbuf;
+    CK(cudaStreamSynchronize(pp->stream));
+    if (pp->rbuf) CK(cudaFree(pp->rbuf));
+    pp->rbuf = nullptr;
+    const size_t nc = std::max<size_t>(count, 2 * pp->rbuf_cap);
+    cudaError_t e = cudaMalloc(&pp->rbuf, 8 * nc);
+    if (e != cudaSuccess) { cudaGetLastError(); pp->rbuf_cap = 0; raise(BL_ERR_OOM, "cudaMalloc(%zu) for the residual refresh: %s", 8 * nc, cudaGetErrorString(e)); }
+    pp->rbuf_cap = nc;
+    return pp->rbuf;
 }
 
 void *ensure_cbuf(bl_prep *pp, size_t bytes) {
@@ -1025,7 +1040,7 @@ void launch_gram_t(bl_prep *pp, int nW) {
     bl_design *d = pp->d;
     const void *kern = (const void *)k_gram<T, M>;
     allow_dyn_smem(kern);
-    dim3 grid(nW - pp->nG, (nW + 255) / 256);
+    dim3 grid(nW - pp->nG, (nW + 31) / 32);
     const CdView v = cd_view(pp);
     k_gram<T, M><<<grid, 256, 8 * d->n, pp->stream>>>((const T *)v.X, d->ld, (int)d->n, v.Wst, nW, pp->nG,
                                                        (int)pp->ldG, v.c, v.s, M ? pp->mask : nullptr,
@@ -1037,15 +1052,19 @@ void launch_gram_t(bl_prep *pp, int nW) {
 template <typename T, bool M>
 void launch_resid_t(bl_prep *pp, int nW) {
     bl_design *d = pp->d;
-    int nb = (int)((d->ld + 255) / 256);
+    const int nb = (int)((d->ld + 255) / 256);
+    const int nch = (nW + kResidChunk - 1) / kResidChunk;
     const CdView v = cd_view(pp);
-    k_resid_update<T, M><<<nb, 256, 0, pp->stream>>>((const T *)v.X, d->ld, (int)d->n, v.Wst, nW, pp->dbeta,
-                                                     v.c, v.s, M ? pp->mask : nullptr, pp->rfull, pp->rscan,
-                                                     pp->rpart);
+    double *part = ensure_rbuf(pp, (size_t)nch * d->ld);
+    k_resid_part<T, M><<<dim3(nb, nch), 256, 0, pp->stream>>>((const T *)v.X, d->ld, (int)d->n, v.Wst, nW, pp->dbeta,
+                                                              v.c, v.s, part);
+    CKL();
+    k_resid_apply<M><<<nb, 256, 0, pp->stream>>>(part, nch, d->ld, (int)d->n, M ? pp->mask : nullptr, pp->rfull,
+                                                pp->rscan, pp->rpart);
     CKL();
     k_resid_finish<<<1, 32, 0, pp->stream>>>(pp->rpart, nb, pp->st);
     CKL();
-    pp->launches += 2;
+    pp->launches += 3;
 }
 
 bool use_gram(bl_prep *pp, int nW) {

@@ -887,12 +887,14 @@ __global__ void __launch_bounds__(RM >= 16 ? 1024 : 512, 1) k_cd(CdArgs a) {
 // lambda(1-alpha));  g_k -= (b' - b_w) G_kw  for every k in W, with
 // G = X~_W' X~_W / n kept in HBM/L2 (identity (1), generalised to W x W).
 // g starts from the fused scan's z at the solve's residual; r is refreshed after
-// the solve from the coefficient changes (k_resid_update), so no drift crosses
+// the solve from the coefficient changes (k_resid_part / k_resid_apply), so no drift crosses
 // lambdas.  Storage slots are append-only; `ord` gives the cyclic (ascending
 // column) order.
 
 // G rows (and columns) for the new slots [first, nW): G[s][t] = sum_i m_i
-// x~_is x~_it / n, t in [0, nW).  grid = (nW - first, ceil(nW / 256)), 256 threads.
+// x~_is x~_it / n.  grid = (nW - first, ceil(nW / 32)), 256 threads: each warp
+// computes 4 entries with 8 independent loads in flight per lane (the earlier
+// one-entry-per-warp loop was L2-latency bound).
 template <typename T, bool MASK>
 __global__ void __launch_bounds__(256) k_gram(const T *__restrict__ X, int64_t ld, int n,
                                               const int *__restrict__ Wst, int nW, int first, int ldG,
@@ -907,21 +909,40 @@ __global__ void __launch_bounds__(256) k_gram(const T *__restrict__ X, int64_t l
         vs[i] = (!MASK || mask[i]) ? (to_d(xs[i]) - cs) * is : 0.0;
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int t0 = blockIdx.y * 256, t1 = min(nW, t0 + 256);
-    for (int tt = t0 + wid; tt < t1; tt += 8) {
-        const int jt = Wst[tt];
-        const T *xt = X + (int64_t)jt * ld;
-        const double ct = c[jt];
-        double acc0 = 0.0, acc1 = 0.0;
-        int i = lane;
-        for (; i + 32 < n; i += 64) {
-            acc0 = fma(vs[i], to_d(xt[i]) - ct, acc0);
-            acc1 = fma(vs[i + 32], to_d(xt[i + 32]) - ct, acc1);
+    const int t0 = blockIdx.y * 32 + wid * 4;
+    if (t0 >= nW) return;
+    const int nt = min(4, nW - t0);
+    const T *xt[4];
+    double ct[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        const int jt = Wst[t0 + min(q, nt - 1)];
+        xt[q] = X + (int64_t)jt * ld;
+        ct[q] = c[jt];
+    }
+    double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    int i = lane;
+    for (; i + 32 < n; i += 64) {
+        double xv[4][2];
+#pragma unroll
+        for (int q = 0; q < 4; q++) { xv[q][0] = to_d(xt[q][i]); xv[q][1] = to_d(xt[q][i + 32]); }
+        const double v0 = vs[i], v1 = vs[i + 32];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            acc[q][0] = fma(v0, xv[q][0] - ct[q], acc[q][0]);
+            acc[q][1] = fma(v1, xv[q][1] - ct[q], acc[q][1]);
         }
-        if (i < n) acc0 = fma(vs[i], to_d(xt[i]) - ct, acc0);
-        double d = warp_sum(acc0 + acc1);
-        if (lane == 0) {
-            double gv = d / s[jt] * inv_n;
+    }
+    if (i < n) {
+#pragma unroll
+        for (int q = 0; q < 4; q++) acc[q][0] = fma(vs[i], to_d(xt[q][i]) - ct[q], acc[q][0]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        const double dsum = warp_sum(acc[q][0] + acc[q][1]);
+        const int tt = t0 + q;
+        if (lane == 0 && q < nt) {
+            const double gv = dsum / s[Wst[tt]] * inv_n;
             G[(int64_t)sl * ldG + tt] = gv;
             if (tt < first) G[(int64_t)tt * ldG + sl] = gv;
         }
@@ -2222,45 +2243,81 @@ __global__ void k_cv_reduce(const double *__restrict__ E, int n, double *__restr
 }
 
 // r -= X~_W dbeta on every row (held-out rows included); r_scan = r on used
-// rows.  Rows are split over blocks (deterministic order over slots); per-block
-// partial sums of r_scan and r_scan^2 go to `part` (finished by k_resid_finish).
+// rows.  Two stages, deterministic: k_resid_part sums 64-column chunks of W per
+// row block into part[chunk][row]; k_resid_apply adds the chunks in order and
+// writes per-block partial sums of r_scan and r_scan^2 (finished by k_resid_finish).
+constexpr int kResidChunk = 64;
 template <typename T, bool MASK>
-__global__ void __launch_bounds__(256) k_resid_update(const T *__restrict__ X, int64_t ld, int n,
-                                                      const int *__restrict__ Wst, int nW,
-                                                      const double *__restrict__ dbeta,
-                                                      const double *__restrict__ c, const double *__restrict__ s,
-                                                      const uint8_t *__restrict__ mask, double *__restrict__ r,
-                                                      double *__restrict__ r_scan, double *__restrict__ part) {
-    __shared__ double red[32];
-    __shared__ int sj[256];
-    __shared__ double sf[256], sc[256];
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    double acc = 0.0;
-    for (int base = 0; base < nW; base += 256) {
-        int w = base + threadIdx.x;
-        __syncthreads();
-        if (w < nW) {
-            double d = dbeta[w];
-            int j = Wst[w];
-            sj[threadIdx.x] = j;
-            sf[threadIdx.x] = d / s[j];
-            sc[threadIdx.x] = c[j];
-        }
-        __syncthreads();
-        int cnt = min(256, nW - base);
-        if (i < n) {
-            for (int u = 0; u < cnt; u++) {
-                double f = sf[u];
-                if (f != 0.0) acc = fma(f, to_d(X[(int64_t)sj[u] * ld + i]) - sc[u], acc);
+__global__ void __launch_bounds__(256) k_resid_part(const T *__restrict__ X, int64_t ld, int n,
+                                                    const int *__restrict__ Wst, int nW,
+                                                    const double *__restrict__ dbeta,
+                                                    const double *__restrict__ c, const double *__restrict__ s,
+                                                    double *__restrict__ part) {
+    __shared__ int sj[kResidChunk];
+    __shared__ double sf[kResidChunk], sc[kResidChunk];
+    __shared__ int wcnt[2];
+    static_assert(kResidChunk == 64, "two warps compact the chunk");
+    const int tid = threadIdx.x, u0 = blockIdx.y * kResidChunk;
+    const int cnt = min(kResidChunk, nW - u0);
+    bool nz = false;
+    int j = 0, pos = 0;
+    double f = 0.0, cc = 0.0;
+    if (tid < kResidChunk) {                  // the chunk's nonzero updates, compacted in order
+        if (tid < cnt) {
+            const double d = dbeta[u0 + tid];
+            nz = d != 0.0;
+            if (nz) {
+                j = Wst[u0 + tid];
+                f = d / s[j];
+                cc = c[j];
             }
         }
+        const unsigned m = __ballot_sync(0xffffffffu, nz);
+        if ((tid & 31) == 0) wcnt[tid >> 5] = __popc(m);
+        pos = __popc(m & ((1u << (tid & 31)) - 1u));
     }
+    __syncthreads();
+    if (nz) {
+        const int q = pos + (tid >= 32 ? wcnt[0] : 0);
+        sj[q] = j;
+        sf[q] = f;
+        sc[q] = cc;
+    }
+    const int nnz = wcnt[0] + wcnt[1];
+    __syncthreads();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ld) return;
+    double acc = 0.0;
+    if (i < n) {
+        const int k = nnz;
+        int u = 0;
+        for (; u + 4 <= k; u += 4) {
+            const double x0 = to_d(X[(int64_t)sj[u] * ld + i]), x1 = to_d(X[(int64_t)sj[u + 1] * ld + i]);
+            const double x2 = to_d(X[(int64_t)sj[u + 2] * ld + i]), x3 = to_d(X[(int64_t)sj[u + 3] * ld + i]);
+            acc = fma(sf[u], x0 - sc[u], acc);
+            acc = fma(sf[u + 1], x1 - sc[u + 1], acc);
+            acc = fma(sf[u + 2], x2 - sc[u + 2], acc);
+            acc = fma(sf[u + 3], x3 - sc[u + 3], acc);
+        }
+        for (; u < k; u++) acc = fma(sf[u], to_d(X[(int64_t)sj[u] * ld + i]) - sc[u], acc);
+    }
+    part[(int64_t)blockIdx.y * ld + i] = acc;
+}
+
+template <bool MASK>
+__global__ void __launch_bounds__(256) k_resid_apply(const double *__restrict__ part, int nchunk, int64_t ld, int n,
+                                                     const uint8_t *__restrict__ mask, double *__restrict__ r,
+                                                     double *__restrict__ r_scan, double *__restrict__ bpart) {
+    __shared__ double red[32];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
     double rs = 0.0, rr = 0.0;
     if (i < n) {
-        double v = r[i] - acc;
+        double acc = 0.0;
+        for (int ch = 0; ch < nchunk; ch++) acc += part[(int64_t)ch * ld + i];
+        const double v = r[i] - acc;
         r[i] = v;
-        bool use = !MASK || mask[i];
-        double vs = use ? v : 0.0;
+        const bool use = !MASK || mask[i];
+        const double vs = use ? v : 0.0;
         r_scan[i] = vs;
         rs = vs;
         rr = vs * vs;
@@ -2269,7 +2326,7 @@ __global__ void __launch_bounds__(256) k_resid_update(const T *__restrict__ X, i
     }
     rs = block_sum(rs, red);
     rr = block_sum(rr, red);
-    if (threadIdx.x == 0) { part[2 * blockIdx.x] = rs; part[2 * blockIdx.x + 1] = rr; }
+    if (threadIdx.x == 0) { bpart[2 * blockIdx.x] = rs; bpart[2 * blockIdx.x + 1] = rr; }
 }
 
 __global__ void k_resid_finish(const double *__restrict__ part, int nb, RoundStatus *st) {
