@@ -4,12 +4,13 @@
 // warp-chain kernel (v5) and the pipelined single-thread-chain kernel (v6), and
 // the largest coefficient difference between the two (same cyclic order).
 // Build on the CPU box, run on the B200:
-//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_1701_05936_b200/csrc -o scripts/cd_bench scripts/cd_bench.cu
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_1701_05936_b200/csrc -I scripts -o scripts/cd_bench scripts/cd_bench.cu
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
 #include "bl_kernels.cuh"
+#include "gram6_ref.cuh"
 using namespace bl;
 
 std::vector<double> run(int ver, int nW, int passes_wanted, double lam, int R = 8) {
