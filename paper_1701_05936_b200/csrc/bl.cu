@@ -264,6 +264,7 @@ struct bl_prep {
     int *widx;              // identity 0..ws_cap-1 (slot -> column of the store)
     int64_t ws_cap;
     int star_root;          // rank owning x_* (sharded)
+    double batch_bytes;     // lockstep CV: X bytes read by the batched scans this fit timed
     int cd_mode;            // 0 auto (Gram when |W| <= 4096), 1 residual, 2 Gram
     cudaStream_t own;       // library stream (used when the caller passes none)
     // profiling
@@ -1138,74 +1139,94 @@ void solve_cd(bl_prep *pp, int nW, double lam, double alpha, double tol, int max
     else M ? launch_resid_t<int8_t, true>(pp, nW) : launch_resid_t<int8_t, false>(pp, nW);
 }
 
-// One full path.  Fills `out` (prefix on convergence failure).
-bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, double tol, int max_iter, int screen,
-                   int max_rounds, bl_path *out, double *heldout /* device, n_lambda x n, or nullptr */) {
-    bl_design *d = pp->d;
-    cudaStream_t st = pp->stream;
-    const double nt = pp->nt;
-    const double lmax = pp->hps.lmax;
-    const double snap = lmax * (1.0 - 1e-12);                 // Q25
-    out->n_lambda = K;
-    out->n_converged = 0;
-    out->lambda.assign(lambda, lambda + K);
-    out->a0.assign(K, 0.0);
-    out->obj.assign(K, 0.0);
-    out->passes.assign(K, 0);
-    out->kkt_rounds.assign(K, 0);
-    out->cols_scanned.assign(K, 0);
-    out->col_ptr.assign(K + 1, 0);
+// One full path as a per-fit state machine, so that one fit (run_path)
+// and the K+1 fits of a lockstep cross-validation (run_cv_lockstep) share every
+// step.  Per lambda: start() -> [solve() -> fused scan -> after_scan()]* -> record().
+struct PathRun {
+    bl_prep *pp;
+    const double *lambda;
+    int K;
+    double alpha, tol;
+    int max_iter, screen, max_rounds;
+    bl_path *out;
+    double *heldout;              // device, n_lambda x n, or nullptr
     WorkingSet W;
-    const int bthreads = 256;
-    const int bgrid = (int)std::min<int64_t>((d->p + bthreads - 1) / bthreads, (int64_t)d->nsm * 8);
-    const int use_bedpp = screen == BL_SCREEN_HYBRID;
     bool first = true;
-    double lam_prev = lmax;
+    double lam_prev = 0.0, lam = 0.0, lam_next = -1.0, snap = 0.0;
     std::vector<int> strong_next;
     bl_status status = BL_OK;
+    int bgrid = 1, use_bedpp = 0;
+    int k = -1, rounds = 0, passes = 0;
+    int64_t scanned = 0;
 
-
-    if (screen == BL_SCREEN_NONE) {
-        // W = every non-constant column; no screening, no scans (SPEC "policy none")
-        CK(cudaMemsetAsync(pp->st, 0, 4 * sizeof(int), st));
-        k_bedpp<<<bgrid, bthreads, 0, st>>>(d->p, pp->s, pp->a, pp->b, pp->ps, alpha, lmax, -1.0, 0, pp->flags,
-                                            pp->scope, pp->st);
+    void begin() {
+        bl_design *d = pp->d;
+        cudaStream_t st = pp->stream;
+        out->n_lambda = K;
+        out->n_converged = 0;
+        out->lambda.assign(lambda, lambda + K);
+        out->a0.assign(K, 0.0);
+        out->obj.assign(K, 0.0);
+        out->passes.assign(K, 0);
+        out->kkt_rounds.assign(K, 0);
+        out->cols_scanned.assign(K, 0);
+        out->col_ptr.assign(K + 1, 0);
+        const int bthreads = 256;
+        bgrid = (int)std::min<int64_t>((d->p + bthreads - 1) / bthreads, (int64_t)d->nsm * 8);
+        use_bedpp = screen == BL_SCREEN_HYBRID;
+        lam_prev = pp->hps.lmax;
+        snap = pp->hps.lmax * (1.0 - 1e-12);                   // Q25
+        if (screen == BL_SCREEN_NONE) {
+            // W = every non-constant column; no screening, no scans (SPEC "policy none")
+            CK(cudaMemsetAsync(pp->st, 0, 4 * sizeof(int), st));
+            k_bedpp<<<bgrid, 256, 0, st>>>(d->p, pp->s, pp->a, pp->b, pp->ps, alpha, pp->hps.lmax, -1.0, 0,
+                                           pp->flags, pp->scope, pp->st);
+            CKL();
+            pp->launches++;
+            CK(cudaMemcpyAsync(pp->hst, pp->st, sizeof(RoundStatus), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            std::vector<int> all = global_list(pp, pp->scope, pp->hst->nscope);
+            upload_W(pp, W, W.add(all));
+        }
+    }
+    void heldout_errors() {
+        if (!heldout) return;
+        bl_design *d = pp->d;
+        k_heldout<<<(unsigned)((d->n + 255) / 256), 256, 0, pp->stream>>>(pp->rfull, pp->mask, (int)d->n,
+                                                                          heldout + (size_t)k * d->n);
         CKL();
         pp->launches++;
-        CK(cudaMemcpyAsync(pp->hst, pp->st, sizeof(RoundStatus), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        std::vector<int> all = global_list(pp, pp->scope, pp->hst->nscope);
-        upload_W(pp, W, W.add(all));
     }
-
-    for (int k = 0; k < K; k++) {
-        const double lam = lambda[k];
+    // lambda_k: false if it is the null solution (recorded here)
+    bool start(int kk) {
+        bl_design *d = pp->d;
+        cudaStream_t st = pp->stream;
+        k = kk;
+        lam = lambda[k];
+        rounds = 0;
+        passes = 0;
+        scanned = 0;
         if (lam >= snap) {          // null solution, exactly (Q25)
             out->a0[k] = pp->hps.ybar;
-            out->obj[k] = pp->hps.Y2 / (2.0 * nt);
+            out->obj[k] = pp->hps.Y2 / (2.0 * pp->nt);
             out->col_ptr[k + 1] = out->col_ptr[k];
             out->n_converged = k + 1;
-            if (heldout) {          // null model: rfull = y_i - ybar_train
-                k_heldout<<<(unsigned)((d->n + 255) / 256), 256, 0, st>>>(pp->rfull, pp->mask, (int)d->n,
-                                                                          heldout + (size_t)k * d->n);
-                CKL();
-                pp->launches++;
-            }
-            continue;
+            heldout_errors();       // null model: rfull = y_i - ybar_train
+            return false;
         }
-        const double lam_next = k + 1 < K ? lambda[k + 1] : -1.0;
+        lam_next = k + 1 < K ? lambda[k + 1] : -1.0;
         if (screen != BL_SCREEN_NONE) {
             CK(cudaMemsetAsync(pp->st, 0, 4 * sizeof(int), st));   // counters only: sum r / rss persist
-            k_bedpp<<<bgrid, bthreads, 0, st>>>(d->p, pp->s, pp->a, pp->b, pp->ps, alpha, lam, lam_next, use_bedpp,
-                                                pp->flags, use_bedpp ? pp->scope : nullptr, pp->st);
+            k_bedpp<<<bgrid, 256, 0, st>>>(d->p, pp->s, pp->a, pp->b, pp->ps, alpha, lam, lam_next, use_bedpp,
+                                           pp->flags, use_bedpp ? pp->scope : nullptr, pp->st);
             CKL();
             pp->launches++;
             if (first) {
                 // strong set at the first solved lambda from the null solution z = a/n (a6)
-                double lp = std::min(lam_prev, lmax);
-                double thr = alpha * (2.0 * lam - lp);
-                k_ssr_init<<<bgrid, bthreads, 0, st>>>(d->p, pp->a, pp->s, pp->flags, pp->wflag, pp->ps,
-                                                       thr < 0.0 ? 0.0 : thr, pp->z, pp->strong, &pp->st->nstrong);
+                const double lp = std::min(lam_prev, pp->hps.lmax);
+                const double thr = alpha * (2.0 * lam - lp);
+                k_ssr_init<<<bgrid, 256, 0, st>>>(d->p, pp->a, pp->s, pp->flags, pp->wflag, pp->ps,
+                                                  thr < 0.0 ? 0.0 : thr, pp->z, pp->strong, &pp->st->nstrong);
                 CKL();
                 pp->launches++;
                 CK(cudaMemcpyAsync(pp->hst, pp->st, sizeof(RoundStatus), cudaMemcpyDeviceToHost, st));
@@ -1216,83 +1237,84 @@ bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, doubl
             upload_W(pp, W, W.add(strong_next));
             strong_next.clear();
         }
-        int rounds = 0;
-        int64_t scanned = 0;
-        int passes = 0;
-        for (;;) {
-            solve_cd(pp, W.size(), lam, alpha, tol, max_iter);
-            if (screen == BL_SCREEN_NONE) {
-                CK(cudaMemcpyAsync(pp->hst, pp->st, sizeof(RoundStatus), cudaMemcpyDeviceToHost, st));
-                CK(cudaStreamSynchronize(st));
-                passes += pp->hst->cd_passes;
-            out->cd_visits += pp->hst->cd_visits;
-            out->cd_updates += pp->hst->cd_updates;
-            out->cd_cycles += pp->hst->cd_cycles;
-            for (int u = 0; u < 4; u++) out->cd_prof[u] += pp->hst->cd_prof[u];
-                if (pp->hst->cd_status) { status = BL_ERR_CONVERGENCE; break; }
-                break;
-            }
-            // reset round counters (keep nscope / nsafe from BEDPP)
-            CK(cudaMemsetAsync(&pp->st->nviol, 0, 2 * sizeof(int), st));
-            ScanArgs sa{};
-            sa.list = use_bedpp ? pp->scope : nullptr;
-            sa.nlist = &pp->st->nscope;
-            sa.K1 = &pp->st->sumr;
-            sa.K2v = 1.0 / nt;
-            sa.out = pp->z;
-            sa.jfix = nullptr;
-            sa.scan = 1;
-            sa.flags = pp->flags;
-            sa.wflag = pp->wflag;
-            sa.thr_viol = alpha * lam;
-            sa.thr_strong = lam_next > 0.0 ? alpha * (2.0 * lam_next - lam) : -1.0;
-            if (sa.thr_strong < 0.0 && lam_next > 0.0) sa.thr_strong = 0.0;
-            sa.viol = pp->viol;
-            sa.nviol = &pp->st->nviol;
-            sa.strong = pp->strong;
-            sa.nstrong = &pp->st->nstrong;
-            launch_scan(pp, sa, pp->rscan, true);
-            CK(cudaMemcpyAsync(pp->hst, pp->st, sizeof(RoundStatus), cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
-            passes += pp->hst->cd_passes;
-            out->cd_visits += pp->hst->cd_visits;
-            out->cd_updates += pp->hst->cd_updates;
-            out->cd_cycles += pp->hst->cd_cycles;
-            for (int u = 0; u < 4; u++) out->cd_prof[u] += pp->hst->cd_prof[u];
-            // the round's counts over all shards (C3): violators, strong candidates, columns scanned
-            std::vector<int64_t> cnt = {pp->hst->nviol, pp->hst->nstrong, pp->hst->nscope};
-            if (d->sharded) cnt = gather_i64(pp, cnt.data(), 3);
-            int64_t nviol = 0, nscope = 0;
-            std::vector<int64_t> cv(d->sharded ? d->world : 1), cs(cv.size());
-            for (size_t r = 0; r < cv.size(); r++) {
-                cv[r] = cnt[3 * r];
-                cs[r] = cnt[3 * r + 1];
-                nviol += cnt[3 * r];
-                nscope += cnt[3 * r + 2];
-            }
-            scanned += use_bedpp ? nscope : pp->hps.n_live;
-            if (pp->hst->cd_status) { status = BL_ERR_CONVERGENCE; break; }
-            if (nviol > 0) {
-                if (++rounds > max_rounds) {
-                    g_err = "more than max KKT rounds at one lambda";
-                    status = BL_ERR_CONVERGENCE;
-                    break;
-                }
-                std::vector<int> v = d->sharded ? gather_list(pp, pp->viol, cv) : read_list(pp, pp->viol, pp->hst->nviol);
-                upload_W(pp, W, W.add(v));
-                continue;
-            }
-            strong_next = d->sharded ? gather_list(pp, pp->strong, cs) : read_list(pp, pp->strong, pp->hst->nstrong);
-            break;
+        return true;
+    }
+    void solve() {
+        solve_cd(pp, W.size(), lam, alpha, tol, max_iter);
+        if (screen != BL_SCREEN_NONE) CK(cudaMemsetAsync(&pp->st->nviol, 0, 2 * sizeof(int), pp->stream));
+    }
+    // the fused KKT + strong-rule scan of this round (a9)
+    ScanArgs scan_args() const {
+        ScanArgs sa{};
+        sa.list = use_bedpp ? pp->scope : nullptr;
+        sa.nlist = &pp->st->nscope;
+        sa.K1 = &pp->st->sumr;
+        sa.K2v = 1.0 / pp->nt;
+        sa.out = pp->z;
+        sa.jfix = nullptr;
+        sa.scan = 1;
+        sa.flags = pp->flags;
+        sa.wflag = pp->wflag;
+        sa.thr_viol = alpha * lam;
+        sa.thr_strong = lam_next > 0.0 ? alpha * (2.0 * lam_next - lam) : -1.0;
+        if (sa.thr_strong < 0.0 && lam_next > 0.0) sa.thr_strong = 0.0;
+        sa.viol = pp->viol;
+        sa.nviol = &pp->st->nviol;
+        sa.strong = pp->strong;
+        sa.nstrong = &pp->st->nstrong;
+        return sa;
+    }
+    void count_cd() {
+        passes += pp->hst->cd_passes;
+        out->cd_visits += pp->hst->cd_visits;
+        out->cd_updates += pp->hst->cd_updates;
+        out->cd_cycles += pp->hst->cd_cycles;
+        for (int u = 0; u < 4; u++) out->cd_prof[u] += pp->hst->cd_prof[u];
+    }
+    // after the round's status reached pp->hst: 0 = lambda done, 1 = re-solve, -1 = error (status set).
+    // `dense`: the scan covered every live column (batched CV scan).
+    int after_scan(bool dense = false) {
+        bl_design *d = pp->d;
+        count_cd();
+        if (screen == BL_SCREEN_NONE) {
+            if (pp->hst->cd_status) { status = BL_ERR_CONVERGENCE; return -1; }
+            return 0;
         }
-        if (status != BL_OK) {
-            if (g_err.empty() || pp->hst->cd_status)
-                g_err = "coordinate descent did not converge within max_iter passes at lambda index " + std::to_string(k);
-            break;
+        // the round's counts over all shards (C3): violators, strong candidates, columns scanned
+        std::vector<int64_t> cnt = {pp->hst->nviol, pp->hst->nstrong, pp->hst->nscope};
+        if (d->sharded) cnt = gather_i64(pp, cnt.data(), 3);
+        int64_t nviol = 0, nscope = 0;
+        std::vector<int64_t> cv(d->sharded ? d->world : 1), cs(cv.size());
+        for (size_t r = 0; r < cv.size(); r++) {
+            cv[r] = cnt[3 * r];
+            cs[r] = cnt[3 * r + 1];
+            nviol += cnt[3 * r];
+            nscope += cnt[3 * r + 2];
         }
-        // record lambda_k (a11)
+        scanned += (use_bedpp && !dense) ? nscope : pp->hps.n_live;
+        if (pp->hst->cd_status) { status = BL_ERR_CONVERGENCE; return -1; }
+        if (nviol > 0) {
+            if (++rounds > max_rounds) {
+                g_err = "more than max KKT rounds at one lambda";
+                status = BL_ERR_CONVERGENCE;
+                return -1;
+            }
+            std::vector<int> v = d->sharded ? gather_list(pp, pp->viol, cv) : read_list(pp, pp->viol, pp->hst->nviol);
+            upload_W(pp, W, W.add(v));
+            return 1;
+        }
+        strong_next = d->sharded ? gather_list(pp, pp->strong, cs) : read_list(pp, pp->strong, pp->hst->nstrong);
+        return 0;
+    }
+    void fail() {
+        if (g_err.empty() || pp->hst->cd_status)
+            g_err = "coordinate descent did not converge within max_iter passes at lambda index " + std::to_string(k);
+    }
+    // record lambda_k (a11)
+    void record() {
+        cudaStream_t st = pp->stream;
         RoundStatus rs = *pp->hst;
-        int nW = (int)W.size();
+        const int nW = (int)W.size();
         if (nW > 0) {
             ensure_host(pp->hbw, pp->hbw_cap, 3 * (size_t)nW);
             CK(cudaMemcpyAsync(pp->hbw, pp->betaW, 24 * (size_t)nW, cudaMemcpyDeviceToHost, st));
@@ -1301,9 +1323,9 @@ bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, doubl
         // unstandardise (Q4): beta_orig = beta/s_j, a0 = ybar - sum beta_orig c_j
         double shift = 0.0;
         for (int q = 0; q < nW; q++) {
-            double bq = pp->hbw[q];
+            const double bq = pp->hbw[q];
             if (bq == 0.0) continue;
-            double cq = pp->hbw[nW + q], sq = pp->hbw[2 * nW + q];
+            const double cq = pp->hbw[nW + q], sq = pp->hbw[2 * nW + q];
             out->feat.push_back(W.sorted[q]);
             out->beta_std.push_back(bq);
             out->beta_orig.push_back(bq / sq);
@@ -1311,21 +1333,36 @@ bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, doubl
         }
         out->col_ptr[k + 1] = (int64_t)out->feat.size();
         out->a0[k] = pp->hps.ybar - shift;
-        out->obj[k] = rs.rss / (2.0 * nt) + lam * (alpha * rs.l1 + 0.5 * (1.0 - alpha) * rs.l2);
+        out->obj[k] = rs.rss / (2.0 * pp->nt) + lam * (alpha * rs.l1 + 0.5 * (1.0 - alpha) * rs.l2);
         out->passes[k] = passes;
         out->kkt_rounds[k] = rounds + (screen == BL_SCREEN_NONE ? 0 : 1);
         out->cols_scanned[k] = scanned;
-        if (heldout) {
-            k_heldout<<<(unsigned)((d->n + 255) / 256), 256, 0, st>>>(pp->rfull, pp->mask, (int)d->n,
-                                                                      heldout + (size_t)k * d->n);
-            CKL();
-            pp->launches++;
-        }
+        heldout_errors();
         out->n_converged = k + 1;
         lam_prev = lam;
     }
+};
+
+bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, double tol, int max_iter, int screen,
+                   int max_rounds, bl_path *out, double *heldout /* device, n_lambda x n, or nullptr */) {
+    PathRun pr{pp, lambda, K, alpha, tol, max_iter, screen, max_rounds, out, heldout};
+    pr.begin();
+    cudaStream_t st = pp->stream;
+    for (int k = 0; k < K; k++) {
+        if (!pr.start(k)) continue;
+        int res;
+        do {
+            pr.solve();
+            if (screen != BL_SCREEN_NONE) launch_scan(pp, pr.scan_args(), pp->rscan, true);
+            CK(cudaMemcpyAsync(pp->hst, pp->st, sizeof(RoundStatus), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            res = pr.after_scan();
+        } while (res == 1);
+        if (res < 0) { pr.fail(); break; }
+        pr.record();
+    }
     CK(cudaStreamSynchronize(st));
-    return status;
+    return pr.status;
 }
 
 void validate_grid(const double *lambda, int K) {
@@ -1355,6 +1392,196 @@ void finish_perf(bl_prep *pp, bl_path *out, double wall_ms) {
     pf.cd_kernel_cycles = out->cd_cycles;
     for (int u = 0; u < 4; u++) pf.cd_prof[u] = out->cd_prof[u];
     pf.wall_ms = wall_ms;
+}
+
+// ---- NEXT-1: lockstep cross-validation with fold-batched scans
+// All fits of this rank (folds, and the full-data fit: fold index -1) advance
+// lambda by lambda.  Their CD solves run concurrently on their own streams; each
+// KKT round's fused scans of every fit still solving at that lambda are ONE pass
+// over X (k_scan_batch; int8 designs scan per fit).  Results are the same paths
+// as independent fits: every fit's arithmetic is unchanged, only the scan kernel
+// that evaluates the (identical) identity-(3) epilogue differs.
+struct LockFit {
+    bl_prep *pp = nullptr;
+    bl_path *out = nullptr;
+    std::unique_ptr<PathRun> run;
+    bool alive = true;
+    bl_status st = BL_OK;
+    std::string err;
+    cudaEvent_t solved = nullptr;
+};
+
+template <int NF>
+const void *batch_kernel_n(bool f64, int nb) {
+    if constexpr (NF > 1) {
+        if (nb < NF) return batch_kernel_n<NF - 1>(f64, nb);
+    }
+    return f64 ? (const void *)k_scan_batch<double, NF> : (const void *)k_scan_batch<float, NF>;
+}
+const void *batch_kernel(bool f64, int nb) { return batch_kernel_n<kBatchMax>(f64, nb); }
+
+void launch_scan_batch(bl_design *d, const std::vector<LockFit *> &fits, cudaStream_t sst, FitScan *dfs,
+                       FitScan *hfs, bl_prep *timer) {
+    const size_t nf = fits.size();
+    for (size_t u = 0; u < nf; u++) {
+        bl_prep *pp = fits[u]->pp;
+        const ScanArgs sa = fits[u]->run->scan_args();
+        FitScan &F = hfs[u];
+        F.r = pp->rscan;
+        F.K1 = sa.K1;
+        F.K2 = sa.K2v;
+        F.c = pp->c;
+        F.s = pp->s;
+        F.out = sa.out;
+        F.flags = sa.flags;
+        F.wflag = sa.wflag;
+        F.thr_viol = sa.thr_viol;
+        F.thr_strong = sa.thr_strong;
+        F.viol = sa.viol;
+        F.nviol = sa.nviol;
+        F.strong = sa.strong;
+        F.nstrong = sa.nstrong;
+    }
+    CK(cudaMemcpyAsync(dfs, hfs, sizeof(FitScan) * nf, cudaMemcpyHostToDevice, sst));
+    const bool f64 = d->dt == DT_F64;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (timer->profile) {
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaEventRecord(e0, sst));
+    }
+    for (size_t u0 = 0; u0 < nf; u0 += kBatchMax) {
+        int nb = (int)std::min<size_t>(kBatchMax, nf - u0);
+        const void *kern = batch_kernel(f64, nb);
+        const size_t smem = (size_t)8 * 2 * nb * kBatchRows;
+        allow_dyn_smem(kern);
+        const int grid = grid_for(kern, kBatchThreads, smem, d->nsm);
+        const void *X = d->X;
+        int64_t ld = d->ld, p = d->p;
+        int n = (int)d->n;
+        FitScan *fp = dfs + u0;
+        void *args[] = {&X, &ld, &n, &p, &fp, &nb};
+        CK(cudaLaunchKernel(kern, dim3(grid), dim3(kBatchThreads), args, smem, sst));
+        timer->launches++;
+        timer->batch_bytes += (double)d->n * itemsize(d->dt) * (double)d->p;
+    }
+    if (timer->profile) {
+        CK(cudaEventRecord(e1, sst));
+        timer->ev_scan.push_back({e0, e1});
+    }
+}
+
+// fit_ids: fold index per fit (-1 = full data).  Paths (prefix on failure) and
+// statuses per fit; held-out errors of the folds go to dE (n_lambda x n).
+void cv_lockstep(bl_design *d, const double *y, const std::vector<int32_t> &fold, const std::vector<int> &fit_ids,
+                 const double *lambda, int K, double alpha, double tol, int max_iter, const bl_opts *opts,
+                 double *dE, std::vector<bl_path *> &paths, std::vector<bl_status> &sts, std::vector<std::string> &errs) {
+    const int64_t n = d->n;
+    const size_t F = fit_ids.size();
+    bl_opts fo{};
+    if (opts) fo = *opts;
+    fo.stream = nullptr;                                   // every fit on its own library stream
+    const int rounds = opts && opts->max_kkt_rounds > 0 ? opts->max_kkt_rounds : 10;
+    std::vector<LockFit> fits(F);
+    cudaStream_t sst = nullptr;
+    FitScan *dfs = nullptr, *hfs = nullptr;
+    const bool batched = d->dt != DT_I8;
+    auto t0 = std::chrono::steady_clock::now();
+    auto cleanup = [&]() {
+        if (sst) cudaStreamSynchronize(sst);
+        for (auto &lf : fits) {
+            if (lf.solved) cudaEventDestroy(lf.solved);
+            if (lf.pp) release_prep(lf.pp);
+            lf.pp = nullptr;
+        }
+        if (dfs) cudaFree(dfs);
+        if (hfs) cudaFreeHost(hfs);
+        if (sst) cudaStreamDestroy(sst);
+    };
+    try {
+        CK(cudaStreamCreateWithFlags(&sst, cudaStreamNonBlocking));
+        CK(cudaMalloc(&dfs, sizeof(FitScan) * std::max<size_t>(F, 1)));
+        CK(cudaMallocHost(&hfs, sizeof(FitScan) * std::max<size_t>(F, 1)));
+        for (size_t u = 0; u < F; u++) {
+            LockFit &lf = fits[u];
+            std::vector<uint8_t> train;
+            if (fit_ids[u] >= 0) {
+                train.resize(n);
+                for (int64_t i = 0; i < n; i++) train[i] = fold[i] != fit_ids[u];
+            }
+            lf.pp = make_prep(d, y, train.empty() ? nullptr : train.data(), alpha, &fo);
+            lf.pp->batch_bytes = 0.0;
+            lf.out = new bl_path();
+            lf.out->magic = MAGIC_PATH;
+            lf.run.reset(new PathRun{lf.pp, lambda, K, alpha, tol, max_iter, BL_SCREEN_HYBRID, rounds, lf.out,
+                                     fit_ids[u] >= 0 ? dE : nullptr});
+            lf.run->begin();
+            CK(cudaEventCreateWithFlags(&lf.solved, cudaEventDisableTiming));
+        }
+        bl_prep *timer = fits.empty() ? nullptr : fits[0].pp;
+        for (int k = 0; k < K; k++) {
+            std::vector<LockFit *> pending;
+            for (auto &lf : fits)
+                if (lf.alive && lf.run->start(k)) pending.push_back(&lf);
+            std::vector<LockFit *> active = pending;
+            while (!pending.empty()) {
+                for (LockFit *lf : pending) {
+                    lf->run->solve();
+                    CK(cudaEventRecord(lf->solved, lf->pp->stream));
+                }
+                if (batched) {
+                    for (LockFit *lf : pending) CK(cudaStreamWaitEvent(sst, lf->solved, 0));
+                    launch_scan_batch(d, pending, sst, dfs, hfs, timer);
+                    for (LockFit *lf : pending)
+                        CK(cudaMemcpyAsync(lf->pp->hst, lf->pp->st, sizeof(RoundStatus), cudaMemcpyDeviceToHost, sst));
+                    CK(cudaStreamSynchronize(sst));
+                } else {
+                    for (LockFit *lf : pending) {
+                        launch_scan(lf->pp, lf->run->scan_args(), lf->pp->rscan, true);
+                        CK(cudaMemcpyAsync(lf->pp->hst, lf->pp->st, sizeof(RoundStatus), cudaMemcpyDeviceToHost,
+                                           lf->pp->stream));
+                    }
+                    for (LockFit *lf : pending) CK(cudaStreamSynchronize(lf->pp->stream));
+                }
+                std::vector<LockFit *> again;
+                for (LockFit *lf : pending) {
+                    const int res = lf->run->after_scan(batched);
+                    if (res == 1) again.push_back(lf);
+                    else if (res < 0) {
+                        lf->run->fail();
+                        lf->alive = false;
+                        lf->st = lf->run->status;
+                        lf->err = g_err;
+                        g_err.clear();
+                    }
+                }
+                pending.swap(again);
+            }
+            for (LockFit *lf : active)
+                if (lf->alive) lf->run->record();
+        }
+        const double wall = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        paths.assign(F, nullptr);
+        sts.assign(F, BL_OK);
+        errs.assign(F, std::string());
+        for (size_t u = 0; u < F; u++) {
+            LockFit &lf = fits[u];
+            finish_perf(lf.pp, lf.out, wall);
+            if (batched) {                                  // the batched passes: charged once, to fit 0
+                lf.out->perf.scan_bytes = u == 0 ? lf.pp->batch_bytes : 0.0;
+                if (u != 0) { lf.out->perf.scan_ms = 0.0; lf.out->perf.scan_launches = 0; }
+            }
+            paths[u] = lf.out;
+            lf.out = nullptr;
+            sts[u] = lf.st;
+            errs[u] = lf.err;
+        }
+    } catch (...) {
+        for (auto &lf : fits) delete lf.out;
+        cleanup();
+        throw;
+    }
+    cleanup();
 }
 
 bl_path *fit_impl(bl_design *d, const double *y, const uint8_t *train, const double *lambda, int K, double alpha,
@@ -1744,9 +1971,26 @@ bl_status bl_cv(bl_design *d, const double *y, const double *lambda, int n_lambd
                 ferr[idx] = "host allocation failed";
             }
         };
+        static const bool lockstep = [] { const char *e = std::getenv("BL_CV_LOCKSTEP"); return !e || std::atoi(e) != 0; }();
         if (d->sharded) {                               // collectives must be issued in the same order
             for (size_t idx = 0; idx <= mine.size(); idx++) run_fold(idx);
-        } else {
+        } else if (lockstep) {                          // NEXT-1: one pass over X per round for all fits
+            if (!(tol > 0.0)) raise(BL_ERR_ARG, "tol must be > 0");
+            if (max_iter < 1) raise(BL_ERR_ARG, "max_iter must be >= 1");
+            std::vector<int> ids(mine.begin(), mine.end());
+            ids.push_back(-1);
+            std::vector<bl_path *> paths;
+            std::vector<bl_status> sts;
+            std::vector<std::string> errs;
+            cv_lockstep(d, y, f, ids, lambda, n_lambda, alpha, tol, max_iter, opts, dE, paths, sts, errs);
+            for (size_t u = 0; u < ids.size(); u++) {
+                add_perf(cv, paths[u]->perf);
+                fst[u] = sts[u];
+                ferr[u] = errs[u];
+                if (ids[u] >= 0) delete paths[u];
+                else full[0] = paths[u];
+            }
+        } else {                                        // independent fits, one host thread + stream each
             std::vector<std::thread> th;
             for (size_t idx = 0; idx <= mine.size(); idx++) th.emplace_back(run_fold, idx);
             for (auto &t : th) t.join();

@@ -352,6 +352,159 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_fp(ScanArgs a) {
     }
 }
 
+// ------------------------- NEXT-1: fold-batched scan (lockstep cross-validation)
+// SURVEY 8(f) NEXT-1.  The K+1 fits of a CV scan the same X with different
+// residuals (each zero on its held-out rows) and fold-specific c, s (Q16); one
+// pass over X serves them all: per column, nf dot products against residual
+// chunks staged in shared memory, then each fit's identity-(3) epilogue with its
+// own KKT / strong-rule tests and compacted lists (as k_scan_fp's SCAN mode).
+// X traffic falls by the number of fits; the fp64 FMAs per byte rise by the
+// same factor (cfg5: 11 FMAs per 4-byte element, near the fp64 ridge).
+struct FitScan {
+    const double *r;                 // residual, zero on unused rows (>= n entries)
+    const double *K1;                // device: sum r
+    double K2;                       // 1 / n_used
+    const double *c, *s;
+    double *out;                     // z
+    const uint8_t *flags, *wflag;
+    double thr_viol, thr_strong;
+    int *viol, *nviol, *strong, *nstrong;
+};
+constexpr int kBatchMax = 12;        // fits per launch
+constexpr int kBatchRows = 256;      // rows per staged residual chunk
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// One CTA = 4 warps x 4 columns; lane l takes rows l, l+32, ... of every chunk
+// (conflict-free 8-byte shared loads of the residuals, coalesced loads of x).
+// Residual chunks are double-buffered with cp.async; x of the next chunk is
+// loaded into registers while the current chunk is multiplied.  NF = the exact
+// number of fits of the launch (compile-time: the fit loops unroll completely).
+constexpr int kBatchThreads = 128;  // 4 warps x 4 columns per CTA; two CTAs per SM overlap their chunk barriers
+static_assert(kBatchRows == 2 * kBatchThreads, "staging: one 16-byte copy per thread and fit");
+template <typename T, int NF>
+__global__ void __launch_bounds__(kBatchThreads, 2) k_scan_batch(const T *__restrict__ X, int64_t ld, int n, int64_t p,
+                                                                  const FitScan *__restrict__ fits, int nf_unused) {
+    extern __shared__ __align__(16) double rsb[];               // [2][NF][kBatchRows]
+    __shared__ FitScan fs[NF];
+    __shared__ double k1s[NF];
+    constexpr int RPL = kBatchRows / 32;                        // rows per lane per chunk
+    constexpr int TILE = 4 * kBatchThreads / 32;               // columns per CTA
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (threadIdx.x < NF) fs[threadIdx.x] = fits[threadIdx.x];
+    __syncthreads();
+    if (threadIdx.x < NF) k1s[threadIdx.x] = *fs[threadIdx.x].K1;
+    const double *rsrc[NF];                                     // this thread's staging sources
+#pragma unroll
+    for (int f = 0; f < NF; f++) rsrc[f] = fs[f].r + 2 * threadIdx.x;
+    const int nchunk = (n + kBatchRows - 1) / kBatchRows;
+    // residual chunk c -> buffer b: thread t copies rows i0 + 2t, i0 + 2t + 1 of every fit
+    auto stage = [&](int c, int b) {
+        const int i0 = c * kBatchRows, i = i0 + 2 * threadIdx.x;
+        double *dst = rsb + (size_t)b * NF * kBatchRows + 2 * threadIdx.x;
+        if (i + 1 < n) {
+#pragma unroll
+            for (int f = 0; f < NF; f++) cp_async16(dst + f * kBatchRows, rsrc[f] + i0);
+        } else {
+#pragma unroll
+            for (int f = 0; f < NF; f++) {
+                dst[f * kBatchRows] = i < n ? rsrc[f][i0] : 0.0;
+                dst[f * kBatchRows + 1] = 0.0;
+            }
+        }
+        cp_async_commit();
+    };
+    for (int64_t g0 = (int64_t)blockIdx.x * TILE; g0 < p; g0 += (int64_t)gridDim.x * TILE) {
+        const int64_t j0 = g0 + wid * 4;
+        const int nv = (int)max((int64_t)0, min((int64_t)4, p - j0));
+        const T *ptr[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) ptr[q] = X + (j0 + (q < nv ? q : 0)) * ld + lane;
+        double acc[4][NF];
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+#pragma unroll
+            for (int f = 0; f < NF; f++) acc[q][f] = 0.0;
+        // x of chunk c (rows i0 + 32 u + lane); unguarded when the chunk is full and all 4 columns exist
+        auto load_x = [&](int c, T (&xs)[RPL][4]) {
+            const int i0 = c * kBatchRows;
+            if (nv == 4 && i0 + kBatchRows <= n) {
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    const T *b = ptr[q] + i0;
+#pragma unroll
+                    for (int u = 0; u < RPL; u++) xs[u][q] = __ldcs(b + 32 * u);
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < RPL; u++) {
+                    const int i = i0 + 32 * u + lane;
+#pragma unroll
+                    for (int q = 0; q < 4; q++) xs[u][q] = (q < nv && i < n) ? __ldcs(ptr[q] + i0 + 32 * u) : T(0);
+                }
+            }
+        };
+        auto mult = [&](const T (&xs)[RPL][4], const double *rb) {
+#pragma unroll
+            for (int u = 0; u < RPL; u++) {
+                double rv[NF];
+#pragma unroll
+                for (int f = 0; f < NF; f++) rv[f] = rb[f * kBatchRows + 32 * u + lane];
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    const double xv = to_d(xs[u][q]);
+#pragma unroll
+                    for (int f = 0; f < NF; f++) acc[q][f] = fma(xv, rv[f], acc[q][f]);
+                }
+            }
+        };
+        T xa[RPL][4], xb[RPL][4];
+        __syncthreads();                                       // the previous tile's last chunk is consumed
+        stage(0, 0);
+        load_x(0, xa);
+        for (int c = 0; c < nchunk; c += 2) {                  // ping-pong x buffers, no register copies
+            cp_async_wait0();
+            __syncthreads();
+            if (c + 1 < nchunk) { stage(c + 1, 1); load_x(c + 1, xb); }
+            mult(xa, rsb);
+            if (c + 1 >= nchunk) break;
+            cp_async_wait0();
+            __syncthreads();
+            if (c + 2 < nchunk) { stage(c + 2, 0); load_x(c + 2, xa); }
+            mult(xb, rsb + (size_t)NF * kBatchRows);
+        }
+        if (nv == 0) continue;
+#pragma unroll
+        for (int f = 0; f < NF; f++) {
+            double d = 0.0;
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const double sq = warp_sum(acc[q][f]);
+                d = lane == q ? sq : d;
+            }
+            const FitScan &F = fs[f];
+            bool isv = false, iss = false;
+            const int64_t j = j0 + lane;
+            if (lane < nv) {
+                const double sj = F.s[j];
+                const double z = sj > 0.0 ? (d - F.c[j] * k1s[f]) * F.K2 / sj : 0.0;
+                F.out[j] = z;
+                const double az = fabs(z);
+                const bool inw = F.wflag[j] != 0;
+                const uint8_t fl = F.flags[j];
+                isv = !inw && (fl & 1) && az > F.thr_viol;
+                iss = !inw && (fl & 2) && F.thr_strong >= 0.0 && az >= F.thr_strong && sj > 0.0;
+            }
+            warp_append(isv, (int)j, F.viol, F.nviol);
+            warp_append(iss, (int)j, F.strong, F.nstrong);
+        }
+    }
+}
+
 // int8 design: exact integer dot products on the tensor cores.  The fp64 vector
 // v is quantised once per scan to a 64-bit fixed-point integer R_i = round(v_i
 // 2^S) (|R| < 2^62) split into 8 balanced base-256 digits (k_limbs); then
