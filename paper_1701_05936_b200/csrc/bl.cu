@@ -68,6 +68,7 @@ struct Err {
         if (r_ != ncclSuccess) raise(BL_ERR_NCCL, "%s: %s", #call, ncclGetErrorString(r_));       \
     } while (0)
 
+constexpr int kListPrefix = 2048;   // list entries copied back with each round's status
 int itemsize(int dt) { return dt == DT_F64 ? 8 : dt == DT_F32 ? 4 : 1; }
 int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
@@ -242,6 +243,7 @@ struct bl_prep {
     PrepScalars hps;
     RoundStatus *hst;       // pinned
     int *hlist;             // pinned read-back buffer (grows)
+    int *hpre;              // pinned: prefixes of the violator and strong lists, copied with each round's status
     int *hup;               // pinned upload staging (grows)
     double *hbw;            // pinned, 3*|W| entries (beta, c, s of W) (grows)
     size_t hlist_cap, hup_cap, hbw_cap;
@@ -470,6 +472,7 @@ void free_prep(bl_prep *pp) {
     if (pp->arena) cudaFree(pp->arena);
     if (pp->hst) cudaFreeHost(pp->hst);
     if (pp->hlist) cudaFreeHost(pp->hlist);
+    if (pp->hpre) cudaFreeHost(pp->hpre);
     if (pp->hbw) cudaFreeHost(pp->hbw);
     if (pp->hup) cudaFreeHost(pp->hup);
     if (pp->warena) cudaFree(pp->warena);
@@ -710,6 +713,7 @@ bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double a
         ensure_W(pp, std::min<int64_t>(p, 4096));
     }
     if (!pp->hst) CK(cudaMallocHost(&pp->hst, sizeof(RoundStatus)));
+    if (!pp->hpre) CK(cudaMallocHost(&pp->hpre, sizeof(int) * 2 * kListPrefix));
     cudaStream_t st = pp->stream;
     CK(cudaMemsetAsync(pp->beta, 0, 8 * p, st));
     CK(cudaMemsetAsync(pp->wflag, 0, p, st));
@@ -897,6 +901,24 @@ void upload_W(bl_prep *pp, const WorkingSet &ws, const std::vector<int> &added) 
             d->comm->bcast(pp->sw + slot0 + q0, 8 * (size_t)k, r, st);
         }
     }
+}
+
+// The round's status and the first kListPrefix entries of both index lists in
+// ONE device->host round trip (the lists are short except in rare rounds).
+int list_prefix(const bl_prep *pp) { return (int)std::min<int64_t>(kListPrefix, pp->p); }   // the lists hold p entries
+void copy_round(bl_prep *pp, cudaStream_t st) {
+    CK(cudaMemcpyAsync(pp->hst, pp->st, sizeof(RoundStatus), cudaMemcpyDeviceToHost, st));
+    const size_t m = sizeof(int) * (size_t)list_prefix(pp);
+    CK(cudaMemcpyAsync(pp->hpre, pp->viol, m, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(pp->hpre + kListPrefix, pp->strong, m, cudaMemcpyDeviceToHost, st));
+}
+std::vector<int> read_list(bl_prep *pp, const int *dev, int count);
+// list `which` (0 violators, 1 strong) of the round copied by copy_round
+std::vector<int> round_list(bl_prep *pp, int which, int count) {
+    if (count > list_prefix(pp)) return read_list(pp, which ? pp->strong : pp->viol, count);
+    std::vector<int> v(pp->hpre + which * kListPrefix, pp->hpre + which * kListPrefix + count);
+    std::sort(v.begin(), v.end());
+    return v;
 }
 
 std::vector<int> read_list(bl_prep *pp, const int *dev, int count) {
@@ -1207,6 +1229,7 @@ struct PathRun {
         passes = 0;
         scanned = 0;
         if (lam >= snap) {          // null solution, exactly (Q25)
+            flush();
             out->a0[k] = pp->hps.ybar;
             out->obj[k] = pp->hps.Y2 / (2.0 * pp->nt);
             out->col_ptr[k + 1] = out->col_ptr[k];
@@ -1299,46 +1322,68 @@ struct PathRun {
                 status = BL_ERR_CONVERGENCE;
                 return -1;
             }
-            std::vector<int> v = d->sharded ? gather_list(pp, pp->viol, cv) : read_list(pp, pp->viol, pp->hst->nviol);
+            std::vector<int> v = d->sharded ? gather_list(pp, pp->viol, cv) : round_list(pp, 0, pp->hst->nviol);
             upload_W(pp, W, W.add(v));
             return 1;
         }
-        strong_next = d->sharded ? gather_list(pp, pp->strong, cs) : read_list(pp, pp->strong, pp->hst->nstrong);
+        strong_next = d->sharded ? gather_list(pp, pp->strong, cs) : round_list(pp, 1, pp->hst->nstrong);
         return 0;
     }
     void fail() {
         if (g_err.empty() || pp->hst->cd_status)
             g_err = "coordinate descent did not converge within max_iter passes at lambda index " + std::to_string(k);
     }
-    // record lambda_k (a11)
-    void record() {
-        cudaStream_t st = pp->stream;
-        RoundStatus rs = *pp->hst;
-        const int nW = (int)W.size();
-        if (nW > 0) {
-            ensure_host(pp->hbw, pp->hbw_cap, 3 * (size_t)nW);
-            CK(cudaMemcpyAsync(pp->hbw, pp->betaW, 24 * (size_t)nW, cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
-        }
+    // record lambda_k (a11).  The coefficients are copied device -> pinned host without
+    // waiting; they are unstandardised in order when the buffer is full or the path ends.
+    struct Pending {
+        int k, nW, passes, rounds;
+        size_t off;
+        std::vector<int> sorted;
+        double lam;
+        RoundStatus rs;
+        int64_t scanned;
+    };
+    std::vector<Pending> pend;
+    size_t hoff = 0;
+    void emit(const Pending &r, const double *hb) {
         // unstandardise (Q4): beta_orig = beta/s_j, a0 = ybar - sum beta_orig c_j
         double shift = 0.0;
-        for (int q = 0; q < nW; q++) {
-            const double bq = pp->hbw[q];
+        for (int q = 0; q < r.nW; q++) {
+            const double bq = hb[q];
             if (bq == 0.0) continue;
-            const double cq = pp->hbw[nW + q], sq = pp->hbw[2 * nW + q];
-            out->feat.push_back(W.sorted[q]);
+            const double cq = hb[r.nW + q], sq = hb[2 * r.nW + q];
+            out->feat.push_back(r.sorted[q]);
             out->beta_std.push_back(bq);
             out->beta_orig.push_back(bq / sq);
             shift += bq * cq / sq;
         }
-        out->col_ptr[k + 1] = (int64_t)out->feat.size();
-        out->a0[k] = pp->hps.ybar - shift;
-        out->obj[k] = rs.rss / (2.0 * pp->nt) + lam * (alpha * rs.l1 + 0.5 * (1.0 - alpha) * rs.l2);
-        out->passes[k] = passes;
-        out->kkt_rounds[k] = rounds + (screen == BL_SCREEN_NONE ? 0 : 1);
-        out->cols_scanned[k] = scanned;
+        out->col_ptr[r.k + 1] = (int64_t)out->feat.size();
+        out->a0[r.k] = pp->hps.ybar - shift;
+        out->obj[r.k] = r.rs.rss / (2.0 * pp->nt) + r.lam * (alpha * r.rs.l1 + 0.5 * (1.0 - alpha) * r.rs.l2);
+        out->passes[r.k] = r.passes;
+        out->kkt_rounds[r.k] = r.rounds;
+        out->cols_scanned[r.k] = r.scanned;
+        out->n_converged = r.k + 1;
+    }
+    void flush() {
+        if (pend.empty()) return;
+        CK(cudaStreamSynchronize(pp->stream));
+        for (const Pending &r : pend) emit(r, pp->hbw + r.off);
+        pend.clear();
+        hoff = 0;
+    }
+    void record() {
+        const int nW = (int)W.size();
+        if (hoff + 3 * (size_t)nW > pp->hbw_cap) {
+            flush();
+            ensure_host(pp->hbw, pp->hbw_cap, std::max<size_t>(3 * (size_t)nW, (size_t)1 << 18));
+        }
+        if (nW > 0)
+            CK(cudaMemcpyAsync(pp->hbw + hoff, pp->betaW, 24 * (size_t)nW, cudaMemcpyDeviceToHost, pp->stream));
+        pend.push_back(Pending{k, nW, passes, rounds + (screen == BL_SCREEN_NONE ? 0 : 1), hoff, W.sorted, lam,
+                               *pp->hst, scanned});
+        hoff += 3 * (size_t)nW;
         heldout_errors();
-        out->n_converged = k + 1;
         lam_prev = lam;
     }
 };
@@ -1354,13 +1399,14 @@ bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, doubl
         do {
             pr.solve();
             if (screen != BL_SCREEN_NONE) launch_scan(pp, pr.scan_args(), pp->rscan, true);
-            CK(cudaMemcpyAsync(pp->hst, pp->st, sizeof(RoundStatus), cudaMemcpyDeviceToHost, st));
+            copy_round(pp, st);
             CK(cudaStreamSynchronize(st));
             res = pr.after_scan();
         } while (res == 1);
         if (res < 0) { pr.fail(); break; }
         pr.record();
     }
+    pr.flush();
     CK(cudaStreamSynchronize(st));
     return pr.status;
 }
@@ -1532,14 +1578,12 @@ void cv_lockstep(bl_design *d, const double *y, const std::vector<int32_t> &fold
                 if (batched) {
                     for (LockFit *lf : pending) CK(cudaStreamWaitEvent(sst, lf->solved, 0));
                     launch_scan_batch(d, pending, sst, dfs, hfs, timer);
-                    for (LockFit *lf : pending)
-                        CK(cudaMemcpyAsync(lf->pp->hst, lf->pp->st, sizeof(RoundStatus), cudaMemcpyDeviceToHost, sst));
+                    for (LockFit *lf : pending) copy_round(lf->pp, sst);
                     CK(cudaStreamSynchronize(sst));
                 } else {
                     for (LockFit *lf : pending) {
                         launch_scan(lf->pp, lf->run->scan_args(), lf->pp->rscan, true);
-                        CK(cudaMemcpyAsync(lf->pp->hst, lf->pp->st, sizeof(RoundStatus), cudaMemcpyDeviceToHost,
-                                           lf->pp->stream));
+                        copy_round(lf->pp, lf->pp->stream);
                     }
                     for (LockFit *lf : pending) CK(cudaStreamSynchronize(lf->pp->stream));
                 }
@@ -1560,6 +1604,7 @@ void cv_lockstep(bl_design *d, const double *y, const std::vector<int32_t> &fold
             for (LockFit *lf : active)
                 if (lf->alive) lf->run->record();
         }
+        for (auto &lf : fits) lf.run->flush();
         const double wall = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         paths.assign(F, nullptr);
         sts.assign(F, BL_OK);
