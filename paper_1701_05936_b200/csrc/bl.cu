@@ -1499,7 +1499,7 @@ void launch_scan_batch(bl_design *d, const std::vector<LockFit *> &fits, cudaStr
     for (size_t u0 = 0; u0 < nf; u0 += kBatchMax) {
         int nb = (int)std::min<size_t>(kBatchMax, nf - u0);
         const void *kern = batch_kernel(f64, nb);
-        const size_t smem = (size_t)8 * 2 * nb * kBatchRows;
+        const size_t smem = batch_smem(nb, itemsize(d->dt));
         allow_dyn_smem(kern);
         const int grid = grid_for(kern, kBatchThreads, smem, d->nsm);
         const void *X = d->X;

@@ -371,112 +371,101 @@ struct FitScan {
     int *viol, *nviol, *strong, *nstrong;
 };
 constexpr int kBatchMax = 12;        // fits per launch
-constexpr int kBatchRows = 256;      // rows per staged residual chunk
+constexpr int kBatchRows = 128;      // rows per pipeline stage
+constexpr int kBatchStages = 3;
+constexpr int kBatchThreads = 128;   // 4 warps x 4 columns per CTA
+constexpr int kBatchTile = 16;       // columns per CTA
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// One CTA = 4 warps x 4 columns; lane l takes rows l, l+32, ... of every chunk
-// (conflict-free 8-byte shared loads of the residuals, coalesced loads of x).
-// Residual chunks are double-buffered with cp.async; x of the next chunk is
-// loaded into registers while the current chunk is multiplied.  NF = the exact
-// number of fits of the launch (compile-time: the fit loops unroll completely).
-constexpr int kBatchThreads = 128;  // 4 warps x 4 columns per CTA; two CTAs per SM overlap their chunk barriers
-static_assert(kBatchRows == 2 * kBatchThreads, "staging: one 16-byte copy per thread and fit");
+// dynamic shared memory of one CTA: kBatchStages x (NF residual rows + 16 x-columns) x kBatchRows
+__host__ __device__ constexpr size_t batch_smem(int nf, int itemsize) {
+    return (size_t)kBatchStages * kBatchRows * ((size_t)8 * nf + (size_t)itemsize * kBatchTile);
+}
+
+// One CTA = 4 warps x 4 columns.  Per stage of kBatchRows rows, cp.async brings the
+// fits' residual rows and the tile's x rows into shared memory (3-stage ring);
+// lane l multiplies rows l, l+32, ... (conflict-free 4- / 8-byte shared loads).
+// NF = the exact number of fits of the launch (the fit loops unroll completely).
 template <typename T, int NF>
-__global__ void __launch_bounds__(kBatchThreads, 2) k_scan_batch(const T *__restrict__ X, int64_t ld, int n, int64_t p,
+__global__ void __launch_bounds__(kBatchThreads, 3) k_scan_batch(const T *__restrict__ X, int64_t ld, int n, int64_t p,
                                                                   const FitScan *__restrict__ fits, int nf_unused) {
-    extern __shared__ __align__(16) double rsb[];               // [2][NF][kBatchRows]
+    extern __shared__ __align__(16) double smb[];
     __shared__ FitScan fs[NF];
     __shared__ double k1s[NF];
-    constexpr int RPL = kBatchRows / 32;                        // rows per lane per chunk
-    constexpr int TILE = 4 * kBatchThreads / 32;               // columns per CTA
+    constexpr int RPL = kBatchRows / 32;
+    constexpr int XE = 16 / sizeof(T);                          // x elements per 16-byte copy
+    constexpr size_t STAGE_D = (size_t)NF * kBatchRows + (size_t)kBatchTile * kBatchRows * sizeof(T) / 8;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     if (threadIdx.x < NF) fs[threadIdx.x] = fits[threadIdx.x];
     __syncthreads();
     if (threadIdx.x < NF) k1s[threadIdx.x] = *fs[threadIdx.x].K1;
-    const double *rsrc[NF];                                     // this thread's staging sources
-#pragma unroll
-    for (int f = 0; f < NF; f++) rsrc[f] = fs[f].r + 2 * threadIdx.x;
     const int nchunk = (n + kBatchRows - 1) / kBatchRows;
-    // residual chunk c -> buffer b: thread t copies rows i0 + 2t, i0 + 2t + 1 of every fit
-    auto stage = [&](int c, int b) {
-        const int i0 = c * kBatchRows, i = i0 + 2 * threadIdx.x;
-        double *dst = rsb + (size_t)b * NF * kBatchRows + 2 * threadIdx.x;
-        if (i + 1 < n) {
-#pragma unroll
-            for (int f = 0; f < NF; f++) cp_async16(dst + f * kBatchRows, rsrc[f] + i0);
-        } else {
-#pragma unroll
-            for (int f = 0; f < NF; f++) {
-                dst[f * kBatchRows] = i < n ? rsrc[f][i0] : 0.0;
-                dst[f * kBatchRows + 1] = 0.0;
+    for (int64_t g0 = (int64_t)blockIdx.x * kBatchTile; g0 < p; g0 += (int64_t)gridDim.x * kBatchTile) {
+        const int ntile = (int)min((int64_t)kBatchTile, p - g0);
+        // stage chunk c into ring slot b: residual rows of every fit, x rows of every tile column
+        auto stage = [&](int c, int b) {
+            double *rs = smb + (size_t)b * STAGE_D;
+            T *xs = reinterpret_cast<T *>(rs + NF * kBatchRows);
+            const int i0 = c * kBatchRows;
+            const bool full = i0 + kBatchRows <= n;
+            for (int e = threadIdx.x; e < NF * kBatchRows / 2; e += kBatchThreads) {
+                const int f = e / (kBatchRows / 2), i = 2 * (e - f * (kBatchRows / 2));
+                double *dst = rs + f * kBatchRows + i;
+                if (full) cp_async16(dst, fs[f].r + i0 + i);
+                else { dst[0] = i0 + i < n ? fs[f].r[i0 + i] : 0.0; dst[1] = i0 + i + 1 < n ? fs[f].r[i0 + i + 1] : 0.0; }
             }
-        }
-        cp_async_commit();
-    };
-    for (int64_t g0 = (int64_t)blockIdx.x * TILE; g0 < p; g0 += (int64_t)gridDim.x * TILE) {
-        const int64_t j0 = g0 + wid * 4;
-        const int nv = (int)max((int64_t)0, min((int64_t)4, p - j0));
-        const T *ptr[4];
+            constexpr int XC = kBatchRows / XE;                 // 16-byte copies per column
+            for (int e = threadIdx.x; e < kBatchTile * XC; e += kBatchThreads) {
+                const int q = e / XC, i = (e - q * XC) * XE;
+                const T *src = X + (g0 + min(q, ntile - 1)) * ld + i0 + i;   // past-the-end columns: a valid column, ignored
+                T *dst = xs + q * kBatchRows + i;
+                if (i0 + i + XE <= ld) cp_async16(dst, src);
+                else {
 #pragma unroll
-        for (int q = 0; q < 4; q++) ptr[q] = X + (j0 + (q < nv ? q : 0)) * ld + lane;
+                    for (int u = 0; u < XE; u++) dst[u] = T(0);
+                }
+            }
+            cp_async_commit();
+        };
         double acc[4][NF];
 #pragma unroll
         for (int q = 0; q < 4; q++)
 #pragma unroll
             for (int f = 0; f < NF; f++) acc[q][f] = 0.0;
-        // x of chunk c (rows i0 + 32 u + lane); unguarded when the chunk is full and all 4 columns exist
-        auto load_x = [&](int c, T (&xs)[RPL][4]) {
-            const int i0 = c * kBatchRows;
-            if (nv == 4 && i0 + kBatchRows <= n) {
-#pragma unroll
-                for (int q = 0; q < 4; q++) {
-                    const T *b = ptr[q] + i0;
-#pragma unroll
-                    for (int u = 0; u < RPL; u++) xs[u][q] = __ldcs(b + 32 * u);
-                }
-            } else {
-#pragma unroll
-                for (int u = 0; u < RPL; u++) {
-                    const int i = i0 + 32 * u + lane;
-#pragma unroll
-                    for (int q = 0; q < 4; q++) xs[u][q] = (q < nv && i < n) ? __ldcs(ptr[q] + i0 + 32 * u) : T(0);
-                }
-            }
-        };
-        auto mult = [&](const T (&xs)[RPL][4], const double *rb) {
+        __syncthreads();                                       // the previous tile's stages are consumed
+        stage(0, 0);
+        if (nchunk > 1) stage(1, 1); else cp_async_commit();
+        for (int c = 0; c < nchunk; c++) {
+            cp_async_wait<1>();                                 // chunk c has landed (c + 1 may be in flight)
+            __syncthreads();
+            if (c + 2 < nchunk) stage(c + 2, (c + 2) % kBatchStages); else cp_async_commit();
+            const double *rs = smb + (size_t)(c % kBatchStages) * STAGE_D;
+            const T *xs = reinterpret_cast<const T *>(rs + NF * kBatchRows) + (wid * 4) * kBatchRows;
+            const bool tail = (c + 1) * kBatchRows > n;
 #pragma unroll
             for (int u = 0; u < RPL; u++) {
+                const int row = 32 * u + lane;
                 double rv[NF];
 #pragma unroll
-                for (int f = 0; f < NF; f++) rv[f] = rb[f * kBatchRows + 32 * u + lane];
+                for (int f = 0; f < NF; f++) rv[f] = rs[f * kBatchRows + row];
+                const bool ok = !tail || c * kBatchRows + row < n; // padding rows of X may hold anything
 #pragma unroll
                 for (int q = 0; q < 4; q++) {
-                    const double xv = to_d(xs[u][q]);
+                    const double xv = ok ? to_d(xs[q * kBatchRows + row]) : 0.0;
 #pragma unroll
                     for (int f = 0; f < NF; f++) acc[q][f] = fma(xv, rv[f], acc[q][f]);
                 }
             }
-        };
-        T xa[RPL][4], xb[RPL][4];
-        __syncthreads();                                       // the previous tile's last chunk is consumed
-        stage(0, 0);
-        load_x(0, xa);
-        for (int c = 0; c < nchunk; c += 2) {                  // ping-pong x buffers, no register copies
-            cp_async_wait0();
-            __syncthreads();
-            if (c + 1 < nchunk) { stage(c + 1, 1); load_x(c + 1, xb); }
-            mult(xa, rsb);
-            if (c + 1 >= nchunk) break;
-            cp_async_wait0();
-            __syncthreads();
-            if (c + 2 < nchunk) { stage(c + 2, 0); load_x(c + 2, xa); }
-            mult(xb, rsb + (size_t)NF * kBatchRows);
         }
+        cp_async_wait<0>();
+        const int64_t j0 = g0 + wid * 4;
+        const int nv = (int)max((int64_t)0, min((int64_t)4, p - j0));
         if (nv == 0) continue;
 #pragma unroll
         for (int f = 0; f < NF; f++) {
