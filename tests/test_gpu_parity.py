@@ -428,3 +428,29 @@ def test_cfg5_full_size_cv_certificate():
         Y2 = float(yt @ yt)
         D = 0.5 * Y2 - 0.5 * lp ** 2 * ((rr + nu * bb) / sc ** 2 - 2 * float(r @ yt) / (lp * sc) + Y2 / lp ** 2)
         assert -1e-9 * P <= P - D <= 1e-5 * P, (k, P, D)
+
+
+def test_max_n():
+    """n = 16,384, the largest n the CD keeps on chip (bl_load_design's limit)."""
+    inst = synth.random_instance(16384, 120, dtype=np.float32, seed=21, kind="corr", n_true=10)
+    lm = oracle.lambda_max(inst, inst.y)[0]
+    lams = synth.lambda_grid(lm, 12, 0.05)
+    for cd in ("gram", "residual"):
+        gp = design(inst).fit_path(inst.y, lams, tol=1e-9, cd=cd)
+        op = oracle.fit_path(inst, inst.y, lams, tol=1e-11)
+        compare_path(inst, gp, op, 1.0)
+    with pytest.raises(bl.BLError):
+        bl.Design(synth.to_colmajor(np.zeros((16385, 2), np.float32)), 16385)
+
+
+def test_large_working_set_switches_cd_flavour():
+    """A working set past the Gram CD's 4096 slots (nearly-ridge elastic net, p >> n):
+    auto mode must switch to residual-update CD mid-path and still match the oracle."""
+    a = 0.003                                                # nearly ridge: thousands of nonzeros
+    inst = synth.random_instance(300, 9000, dtype=np.float32, seed=23, kind="iid", n_true=5, alpha=a)
+    lm = oracle.lambda_max(inst, inst.y, a)[0]
+    lams = synth.lambda_grid(lm, 15, 0.05)
+    gp = design(inst).fit_path(inst.y, lams, alpha=a, tol=1e-9, cd="auto")
+    op = oracle.fit_path(inst, inst.y, lams, alpha=a, tol=1e-11, nnz_cap=9000 * 15)
+    assert np.count_nonzero(op.beta[:, -1]) > 4096          # the working set outgrew the Gram CD
+    compare_path(inst, gp, op, a)
