@@ -1194,7 +1194,7 @@ struct PathRun {
         out->cols_scanned.assign(K, 0);
         out->col_ptr.assign(K + 1, 0);
         const int bthreads = 256;
-        bgrid = (int)std::min<int64_t>((d->p + bthreads - 1) / bthreads, (int64_t)d->nsm * 8);
+        bgrid = (int)std::min<int64_t>((d->p + 4 * bthreads - 1) / (4 * bthreads), (int64_t)d->nsm * 8);   // k_bedpp: 1024 cols/block-step
         use_bedpp = screen == BL_SCREEN_HYBRID;
         lam_prev = pp->hps.lmax;
         snap = pp->hps.lmax * (1.0 - 1e-12);                   // Q25
@@ -1853,7 +1853,7 @@ bl_status bl_bedpp(bl_prep *pp, double lambda, uint8_t *keep, int64_t *n_keep) {
         CK(cudaSetDevice(d->device));
         cudaStream_t st = pp->stream;
         CK(cudaMemsetAsync(pp->st, 0, sizeof(RoundStatus), st));
-        int grid = (int)std::min<int64_t>((d->p + 255) / 256, (int64_t)d->nsm * 8);
+        int grid = (int)std::min<int64_t>((d->p + 1023) / 1024, (int64_t)d->nsm * 8);
         k_bedpp<<<grid, 256, 0, st>>>(d->p, pp->s, pp->a, pp->b, pp->ps, pp->alpha, lambda, -1.0, 1, pp->flags,
                                       pp->scope, pp->st);
         CKL();
@@ -1882,7 +1882,7 @@ bl_status bl_scan(bl_prep *pp, const double *r, double lam, double lam_next, con
         if (in_w) std::memcpy(w.data(), in_w, d->p);
         CK(cudaMemcpyAsync(pp->wflag, w.data(), d->p, cudaMemcpyHostToDevice, st));
         CK(cudaMemsetAsync(pp->st, 0, sizeof(RoundStatus), st));
-        int grid = (int)std::min<int64_t>((d->p + 255) / 256, (int64_t)d->nsm * 8);
+        int grid = (int)std::min<int64_t>((d->p + 1023) / 1024, (int64_t)d->nsm * 8);
         k_bedpp<<<grid, 256, 0, st>>>(d->p, pp->s, pp->a, pp->b, pp->ps, pp->alpha, lam, lam_next > 0 ? lam_next : -1.0,
                                       0, pp->flags, nullptr, pp->st);
         CKL();
