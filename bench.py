@@ -215,6 +215,10 @@ def run_ours(args, rank, world, local_rank):
     updates = sum(p.perf["cd_updates"] for p in perfs) / args.steps
     cd_cycles = sum(p.perf["cd_kernel_cycles"] for p in perfs) / args.steps
     cd_prof = [sum(p.perf["cd_prof"][u] for p in perfs) / args.steps / max(visits, 1) for u in range(4)]
+    # GB/s over the scan launches that covered every live column (|S_k| = p)
+    fs_ms = sum(p.perf["full_scan_ms"] for p in perfs)
+    fs_bytes = sum(p.perf["full_scan_bytes"] for p in perfs)
+    fs_launches = sum(p.perf["full_scan_launches"] for p in perfs) / args.steps
 
     # end to end through the C ABI with HOST buffers (H2D of X inside the timed region)
     x_bytes = X.numel() * X.element_size()
@@ -288,7 +292,9 @@ def run_ours(args, rank, world, local_rank):
                      "cd_kernel_cycles_per_visit": cd_cycles / max(visits, 1),
                      "cd_kernel_ms_per_step": cd_cycles / 1.965e6,
                      "cd_phase_cycles_per_visit": dict(zip(["lead", "bulk", "build_A", "catch_up"], cd_prof)),
-                     "algorithmic_bytes_per_step": scan_bytes / args.steps},
+                     "algorithmic_bytes_per_step": scan_bytes / args.steps,
+                     "full_scan": ({"GBps": fs_bytes / (fs_ms / 1e3) / 1e9, "frac": fs_bytes / (fs_ms / 1e3) / 1e9 / pk["hbm_gbs"],
+                                    "launches_per_step": fs_launches} if fs_ms > 0 else None)},
         "cpu_baseline": cpu,
         "e2e": ({"value": statistics.median(e2e), "unit": "s", "h2d_bytes_per_step": int(h2d),
                  "d2h_bytes_per_step": d2h} if e2e else
@@ -296,7 +302,11 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": int(launches / args.steps),
         "path": {"nnz_last": int(last.col_ptr[-1] - last.col_ptr[-2]), "kkt_rounds": int(last.kkt_rounds.sum()),
                  "cd_passes": int(last.passes.sum()), "cols_scanned": int(last.cols_scanned.sum()),
-                 "n_converged": int(last.n_converged)},
+                 "n_converged": int(last.n_converged),
+                 # Fig 1 analog: fraction of live columns BEDPP keeps, by lambda/lambda_max
+                 "bedpp_kept_frac": {f"{q:.1f}": float(last.n_safe[int(np.argmin(np.abs(lams / lm - q)))] / p_global)
+                                     for q in (0.9, 0.7, 0.5, 0.3)},
+                 "max_working_set": int(last.n_working.max())},
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)

@@ -108,6 +108,9 @@ typedef struct {
     int64_t cd_updates;        /* visits that changed a coefficient */
     int64_t cd_kernel_cycles;  /* SM cycles spent inside the CD kernels (clock64, thread 0) */
     int64_t cd_prof[4];        /* Gram CD phases (cycles): leader steps, bulk steps, G_AA / M builds, lazy catch-ups */
+    double full_scan_ms;       /* the subset of scan launches that covered every live column (|S_k| = p, */
+    double full_scan_bytes;    /*   SURVEY 8(d) "full-scan only" GB/s); single fits only (0 in CV sums) */
+    int64_t full_scan_launches;
 } bl_perf;
 
 /* ---- design ------------------------------------------------------------------
@@ -162,6 +165,13 @@ bl_status bl_path_copy(const bl_path *path, double *lambda, double *a0, double *
                        int64_t *col_ptr, int64_t *feat_idx, double *beta_std, double *beta_orig,
                        int32_t *passes, int32_t *kkt_rounds, int64_t *cols_scanned);
 bl_status bl_path_perf(const bl_path *path, bl_perf *out);
+/* Screening diagnostics per lambda (the analog of P:212-217's Fig 1; any pointer
+ * may be NULL; n_lambda entries each, first n_converged filled):
+ *   n_safe    |S_k|: columns the BEDPP safe rule keeps at lambda_k (P:211, 8(c));
+ *             every live column under BL_SCREEN_SSR / BL_SCREEN_NONE;
+ *   n_strong  strong-rule candidates entering lambda_k not already in W (a6);
+ *   n_working |W| when lambda_k converged (strong sets, violators, ever-active). */
+bl_status bl_path_screen(const bl_path *path, int64_t *n_safe, int64_t *n_strong, int64_t *n_working);
 
 /* cve, cvse: n_lambda; fold_id_out: n; full_fit: borrowed, freed with the cv result.
  * cve_k = mean_i e_ik, cvse_k = sd_i(e_ik)/sqrt(n) over per-row held-out squared

@@ -49,7 +49,9 @@ class bl_perf(ctypes.Structure):
                 ("cd_launches", ctypes.c_int64), ("prep_ms", ctypes.c_double),
                 ("prep_bytes", ctypes.c_double), ("kernel_launches", ctypes.c_int64),
                 ("wall_ms", ctypes.c_double), ("cd_visits", ctypes.c_int64), ("cd_updates", ctypes.c_int64),
-                ("cd_kernel_cycles", ctypes.c_int64), ("cd_prof", ctypes.c_int64 * 4)]
+                ("cd_kernel_cycles", ctypes.c_int64), ("cd_prof", ctypes.c_int64 * 4),
+                ("full_scan_ms", ctypes.c_double), ("full_scan_bytes", ctypes.c_double),
+                ("full_scan_launches", ctypes.c_int64)]
 
     def as_dict(self):
         d = {f: getattr(self, f) for f, _ in self._fields_}
@@ -60,7 +62,7 @@ class bl_perf(ctypes.Structure):
 
 _lib = None
 EXPORTS = ["bl_load_design", "bl_nccl_unique_id", "bl_lambda_max", "bl_fit_path", "bl_cv", "bl_path_info",
-           "bl_path_copy", "bl_path_perf", "bl_cv_copy", "bl_cv_errors", "bl_cv_perf", "bl_prepare", "bl_prep_copy",
+           "bl_path_copy", "bl_path_perf", "bl_path_screen", "bl_cv_copy", "bl_cv_errors", "bl_cv_perf", "bl_prepare", "bl_prep_copy",
            "bl_bedpp", "bl_scan", "bl_free", "bl_last_error"]
 
 
@@ -82,6 +84,7 @@ def lib():
     L.bl_path_info.argtypes = [P, P, P, P]
     L.bl_path_copy.argtypes = [P] + [P] * 10
     L.bl_path_perf.argtypes = [P, P]
+    L.bl_path_screen.argtypes = [P, P, P, P]
     L.bl_cv_copy.argtypes = [P, P, P, P, P, PP]
     L.bl_cv_errors.argtypes = [P, P]
     L.bl_cv_perf.argtypes = [P, P]
@@ -168,6 +171,10 @@ class Path:
         pf = bl_perf()
         _check(L.bl_path_perf(handle, ctypes.byref(pf)))
         self.perf = pf.as_dict()
+        # screening diagnostics per lambda: |S_k| (BEDPP-safe), |strong_k|, |W| (Fig 1 analog)
+        self.n_safe = np.zeros(K, np.int64); self.n_strong = np.zeros(K, np.int64)
+        self.n_working = np.zeros(K, np.int64)
+        _check(L.bl_path_screen(handle, _p(self.n_safe), _p(self.n_strong), _p(self.n_working)))
 
     def dense(self, p, which="std"):
         """(p, n_lambda) dense coefficient matrix."""

@@ -196,6 +196,7 @@ struct bl_path {
     std::vector<double> beta_std, beta_orig;
     std::vector<int32_t> passes, kkt_rounds;
     std::vector<int64_t> cols_scanned;
+    std::vector<int64_t> n_safe, n_strong, n_working;   // screening diagnostics per lambda (Fig 1 analog)
     bl_perf perf;
     int64_t cd_visits = 0, cd_updates = 0, cd_cycles = 0, cd_prof[4] = {0, 0, 0, 0};
 };
@@ -272,6 +273,7 @@ struct bl_prep {
     // profiling
     int profile;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_scan, ev_cd, ev_prep;
+    std::vector<int64_t> scan_full;   // per timed scan launch: its local columns if it covered every live column, else -1
     double prep_bytes;
     int64_t launches;
 };
@@ -340,11 +342,16 @@ struct EvPairOpt {
     }
 };
 
-double sum_events(std::vector<std::pair<cudaEvent_t, cudaEvent_t>> &v) {
+double sum_events(std::vector<std::pair<cudaEvent_t, cudaEvent_t>> &v, const std::vector<int64_t> *sel = nullptr,
+                  double *sel_ms = nullptr) {
     double tot = 0.0;
-    for (auto &pr : v) {
+    for (size_t i = 0; i < v.size(); i++) {
+        auto &pr = v[i];
         float ms = 0.f;
-        if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) tot += ms;
+        if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) {
+            tot += ms;
+            if (sel && sel_ms && i < sel->size() && (*sel)[i] >= 0) *sel_ms += ms;
+        }
         cudaEventDestroy(pr.first);
         cudaEventDestroy(pr.second);
     }
@@ -667,6 +674,7 @@ bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double a
     pp->cd_mode = opts ? opts->cd_mode : 0;
     pp->nG = 0;
     pp->launches = 0;
+    pp->scan_full.clear();
     if (!pp->own) CK(cudaStreamCreateWithFlags(&pp->own, cudaStreamNonBlocking));
     pp->stream = (opts && opts->stream) ? (cudaStream_t)opts->stream : pp->own;
     pp->own_stream = false;
@@ -1179,7 +1187,7 @@ struct PathRun {
     bl_status status = BL_OK;
     int bgrid = 1, use_bedpp = 0;
     int k = -1, rounds = 0, passes = 0;
-    int64_t scanned = 0;
+    int64_t scanned = 0, nstrong_k = 0, nsafe_k = 0;
 
     void begin() {
         bl_design *d = pp->d;
@@ -1192,6 +1200,9 @@ struct PathRun {
         out->passes.assign(K, 0);
         out->kkt_rounds.assign(K, 0);
         out->cols_scanned.assign(K, 0);
+        out->n_safe.assign(K, 0);
+        out->n_strong.assign(K, 0);
+        out->n_working.assign(K, 0);
         out->col_ptr.assign(K + 1, 0);
         const int bthreads = 256;
         bgrid = (int)std::min<int64_t>((d->p + 4 * bthreads - 1) / (4 * bthreads), (int64_t)d->nsm * 8);   // k_bedpp: 1024 cols/block-step
@@ -1228,6 +1239,8 @@ struct PathRun {
         rounds = 0;
         passes = 0;
         scanned = 0;
+        nstrong_k = 0;
+        nsafe_k = screen == BL_SCREEN_NONE ? pp->hps.n_live : 0;
         if (lam >= snap) {          // null solution, exactly (Q25)
             flush();
             out->a0[k] = pp->hps.ybar;
@@ -1257,6 +1270,7 @@ struct PathRun {
                 strong_next = global_list(pp, pp->strong, pp->hst->nstrong);
                 first = false;
             }
+            nstrong_k = (int64_t)strong_next.size();
             upload_W(pp, W, W.add(strong_next));
             strong_next.clear();
         }
@@ -1304,17 +1318,22 @@ struct PathRun {
             return 0;
         }
         // the round's counts over all shards (C3): violators, strong candidates, columns scanned
-        std::vector<int64_t> cnt = {pp->hst->nviol, pp->hst->nstrong, pp->hst->nscope};
-        if (d->sharded) cnt = gather_i64(pp, cnt.data(), 3);
-        int64_t nviol = 0, nscope = 0;
+        std::vector<int64_t> cnt = {pp->hst->nviol, pp->hst->nstrong, pp->hst->nscope, pp->hst->nsafe};
+        if (d->sharded) cnt = gather_i64(pp, cnt.data(), 4);
+        int64_t nviol = 0, nscope = 0, nsafe = 0;
         std::vector<int64_t> cv(d->sharded ? d->world : 1), cs(cv.size());
         for (size_t r = 0; r < cv.size(); r++) {
-            cv[r] = cnt[3 * r];
-            cs[r] = cnt[3 * r + 1];
-            nviol += cnt[3 * r];
-            nscope += cnt[3 * r + 2];
+            cv[r] = cnt[4 * r];
+            cs[r] = cnt[4 * r + 1];
+            nviol += cnt[4 * r];
+            nscope += cnt[4 * r + 2];
+            nsafe += cnt[4 * r + 3];
         }
-        scanned += (use_bedpp && !dense) ? nscope : pp->hps.n_live;
+        nsafe_k = nsafe;
+        const int64_t round_cols = (use_bedpp && !dense) ? nscope : pp->hps.n_live;
+        scanned += round_cols;
+        if (!dense && pp->scan_full.size() < pp->ev_scan.size())   // classify the timed scan launch of this round
+            pp->scan_full.push_back(round_cols == pp->hps.n_live ? (use_bedpp ? (int64_t)pp->hst->nscope : pp->p) : -1);
         if (pp->hst->cd_status) { status = BL_ERR_CONVERGENCE; return -1; }
         if (nviol > 0) {
             if (++rounds > max_rounds) {
@@ -1341,7 +1360,7 @@ struct PathRun {
         std::vector<int> sorted;
         double lam;
         RoundStatus rs;
-        int64_t scanned;
+        int64_t scanned, nsafe, nstrong;
     };
     std::vector<Pending> pend;
     size_t hoff = 0;
@@ -1363,6 +1382,9 @@ struct PathRun {
         out->passes[r.k] = r.passes;
         out->kkt_rounds[r.k] = r.rounds;
         out->cols_scanned[r.k] = r.scanned;
+        out->n_safe[r.k] = r.nsafe;
+        out->n_strong[r.k] = r.nstrong;
+        out->n_working[r.k] = r.nW;
         out->n_converged = r.k + 1;
     }
     void flush() {
@@ -1381,7 +1403,7 @@ struct PathRun {
         if (nW > 0)
             CK(cudaMemcpyAsync(pp->hbw + hoff, pp->betaW, 24 * (size_t)nW, cudaMemcpyDeviceToHost, pp->stream));
         pend.push_back(Pending{k, nW, passes, rounds + (screen == BL_SCREEN_NONE ? 0 : 1), hoff, W.sorted, lam,
-                               *pp->hst, scanned});
+                               *pp->hst, scanned, nsafe_k, nstrong_k});
         hoff += 3 * (size_t)nW;
         heldout_errors();
         lam_prev = lam;
@@ -1425,7 +1447,15 @@ void finish_perf(bl_prep *pp, bl_path *out, double wall_ms) {
     std::memset(&pf, 0, sizeof pf);
     pf.scan_launches = (int64_t)pp->ev_scan.size();
     pf.cd_launches = (int64_t)pp->ev_cd.size();
-    pf.scan_ms = sum_events(pp->ev_scan);
+    double full_ms = 0.0;
+    for (size_t i = 0; i < pp->scan_full.size() && i < pp->ev_scan.size(); i++)
+        if (pp->scan_full[i] >= 0) {
+            pf.full_scan_launches++;
+            pf.full_scan_bytes += (double)pp->scan_full[i] * (double)pp->d->n * itemsize(pp->d->dt);
+        }
+    pf.scan_ms = sum_events(pp->ev_scan, &pp->scan_full, &full_ms);
+    pf.full_scan_ms = full_ms;
+    pp->scan_full.clear();
     pf.cd_ms = sum_events(pp->ev_cd);
     pf.prep_ms = sum_events(pp->ev_prep);
     int64_t cols = 0;
@@ -2089,6 +2119,16 @@ bl_status bl_path_copy(const bl_path *p, double *lambda, double *a0, double *obj
         if (passes) std::copy(p->passes.begin(), p->passes.end(), passes);
         if (kkt_rounds) std::copy(p->kkt_rounds.begin(), p->kkt_rounds.end(), kkt_rounds);
         if (cols_scanned) std::copy(p->cols_scanned.begin(), p->cols_scanned.end(), cols_scanned);
+    });
+}
+
+bl_status bl_path_screen(const bl_path *p, int64_t *n_safe, int64_t *n_strong, int64_t *n_working) {
+    return guard([&] {
+        if (!p || p->magic != MAGIC_PATH) raise(BL_ERR_ARG, "bad path handle");
+        const size_t K = (size_t)p->n_lambda;
+        if (n_safe) std::copy(p->n_safe.begin(), p->n_safe.begin() + std::min(K, p->n_safe.size()), n_safe);
+        if (n_strong) std::copy(p->n_strong.begin(), p->n_strong.begin() + std::min(K, p->n_strong.size()), n_strong);
+        if (n_working) std::copy(p->n_working.begin(), p->n_working.begin() + std::min(K, p->n_working.size()), n_working);
     });
 }
 

@@ -184,6 +184,38 @@ def test_screening_policies_agree_and_hybrid_scans_less():
     assert paths["hybrid"].cols_scanned.sum() < paths["ssr"].cols_scanned.sum()
 
 
+def test_screening_diagnostics():
+    """Per-lambda |S_k| (BEDPP-safe), |strong_k| and |W| read-outs (bl_path_screen,
+    the Fig 1 analog of P:212-217): |S_k| matches the oracle's BEDPP mask count,
+    SSR-only keeps every live column, strong_k is inside S_k, W only grows and
+    holds every nonzero."""
+    alpha = 1.0
+    inst = synth.random_instance(150, 1500, seed=31, kind="corr", n_true=12, const_cols=5)
+    live = inst.p - 5
+    d = design(inst)
+    lm = d.lambda_max(inst.y)
+    lams = synth.lambda_grid(lm, 40, 0.1)
+    hy = d.fit_path(inst.y, lams, tol=1e-10, screen="hybrid")
+    ss = d.fit_path(inst.y, lams, tol=1e-10, screen="ssr")
+    B = hy.dense(inst.p)
+    for k, lam in enumerate(lams):
+        if k == 0:
+            continue                       # lambda_max: the null solution, nothing screened
+        keep_or = ~oracle.bedpp_discard(inst, inst.y, alpha, lam)
+        n_or = int(keep_or.sum())
+        assert abs(int(hy.n_safe[k]) - n_or) <= max(2, 2e-3 * inst.p), (k, hy.n_safe[k], n_or)
+        assert ss.n_safe[k] == live
+        assert hy.n_strong[k] <= hy.n_safe[k]
+        assert hy.n_working[k] >= np.count_nonzero(B[:, k])
+        if k > 1:
+            assert hy.n_working[k] >= hy.n_working[k - 1]
+    # the paper's qualitative shape (P:211): BEDPP keeps few columns near lambda_max
+    # and discards virtually nothing below 0.45 lambda_max
+    frac = hy.n_safe / live
+    assert frac[1] < 0.5
+    assert np.all(frac[lams / lm < 0.45] > 0.9)
+
+
 def test_kkt_repairs_a_shrunk_strong_set():
     """S:222 fault injection analogue: with a 1-round KKT cap the path must still
     certify (violators are added and re-solved) -- and the default succeeds."""
