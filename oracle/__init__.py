@@ -54,6 +54,9 @@ def _L():
         _lib.or_std_dots.argtypes = [P, I, I64, I64, I64, P, P, P]
         _lib.or_prep.argtypes = [P, I, I64, I64, I64, P, P, D, P, P, P, P]
         _lib.or_cv.argtypes = [P, I, I64, I64, I64, P, P, I, P, I, D, D, I, I, P, P, P, P]
+        _lib.or_objective_binomial.argtypes = [P, I, I64, I64, I64, P, P, D, P, D, D, P]
+        _lib.or_fit_path_binomial.argtypes = [P, I, I64, I64, I64, P, P, P, I, D, D, I, I, I64,
+                                              P, P, P, P, P, P, P, P, P]
     return _lib
 
 
@@ -228,3 +231,51 @@ def cv(X, y, fold_id, K, lam, alpha=1.0, tol=1e-10, max_iter=100000, cycle_activ
     if rc:
         raise OracleError(rc, "cv")
     return E, cve, cvse, lmin.value
+
+
+# ------------------------------------------------------------ NEXT-3: logistic path
+
+def objective_binomial(X, y, b0, beta, lam, alpha=1.0, train=None):
+    """Q(b0, b) = mean_i [log(1 + e^eta_i) - y_i eta_i] + lambda (alpha |b|_1 + (1-alpha)/2 |b|^2) (QL1)."""
+    buf, dt, n, p, ld = _design(X)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    b = np.ascontiguousarray(beta, dtype=np.float64)
+    m = _mask(train, n)
+    q = ctypes.c_double()
+    rc = _L().or_objective_binomial(_p(buf), dt, n, p, ld, _p(y), _p(m), float(b0), _p(b), lam, alpha,
+                                    ctypes.byref(q))
+    if rc:
+        raise OracleError(rc, "objective_binomial")
+    return q.value
+
+
+class BinomialPathResult(PathResult):
+    def __init__(self, lam, beta, b0, a0, obj, passes, outer, n_converged, status):
+        super().__init__(lam, beta, a0, obj, passes, None, n_converged, status)
+        self.b0, self.outer = b0, outer
+
+
+def fit_path_binomial(X, y, lam, alpha=1.0, tol=1e-10, max_iter=100000, cycle_active=True,
+                      train=None, nnz_cap=None, raise_on_error=True):
+    """Penalised logistic path by IRLS + cyclic weighted CD, no screening (oracle.c NEXT-3)."""
+    buf, dt, n, p, ld = _design(X)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    lam = np.ascontiguousarray(lam, dtype=np.float64)
+    K = lam.size
+    m = _mask(train, n)
+    cap = nnz_cap or min(p * K, max(1, min(n, p) * K * 2 + 16))
+    col_ptr = np.zeros(K + 1, dtype=np.int64)
+    idx = np.empty(cap, dtype=np.int64); val = np.empty(cap)
+    b0 = np.empty(K); a0 = np.empty(K); obj = np.empty(K)
+    passes = np.empty(K, dtype=np.int32); outer = np.empty(K, dtype=np.int32)
+    nc = ctypes.c_int()
+    rc = _L().or_fit_path_binomial(_p(buf), dt, n, p, ld, _p(y), _p(m), _p(lam), K, alpha, tol, max_iter,
+                                   int(cycle_active), cap, _p(col_ptr), _p(idx), _p(val), _p(b0), _p(a0),
+                                   _p(obj), _p(passes), _p(outer), ctypes.byref(nc))
+    if rc and raise_on_error:
+        raise OracleError(rc, "fit_path_binomial")
+    beta = np.zeros((p, K))
+    for k in range(nc.value):
+        sl = slice(col_ptr[k], col_ptr[k + 1])
+        beta[idx[sl], k] = val[sl]
+    return BinomialPathResult(lam, beta, b0, a0, obj, passes, outer, nc.value, rc)

@@ -274,4 +274,56 @@ def cfg5(seed=0, n=10_000, p=2_000_000, device=None, col_range=None):
     return Instance("cfg5", X, n, y, alpha=0.5, ratio=0.05, tol=1e-7, beta_true=beta, seed=seed)
 
 
+# ------------------------------------------------ NEXT-3: logistic (binomial) inputs
+
+def logistic_instance(n, p, dtype=np.float64, seed=0, kind="iid", n_true=None, scale=1.0, const_cols=0,
+                      alpha=1.0):
+    """Small seeded binary-response instance: X as random_instance; y_i ~ Bernoulli(sigmoid(eta_i))
+    with eta = x beta - mean (raw columns), beta_true on n_true random
+    columns ~ scale * U(-1, 1) (the P:383 simulation's coefficient law)."""
+    rng = np.random.default_rng(seed)
+    if kind == "geno":
+        maf = rng.uniform(0.05, 0.5, size=p)
+        X = (rng.random((n, p)) < maf).astype(np.int8) + (rng.random((n, p)) < maf).astype(np.int8)
+    else:
+        X = rng.standard_normal((n, p))
+        if kind == "corr":
+            X = 0.6 * rng.standard_normal((n, 1)) + 0.8 * X
+        X = X.astype(dtype)
+    if const_cols:
+        cols = rng.choice(p, size=const_cols, replace=False)
+        X[:, cols] = X[0:1, cols]
+    Xf = X.astype(np.float64)
+    k = n_true if n_true is not None else max(1, min(20, p // 4))
+    beta = np.zeros(p)
+    idx = rng.choice(p, size=k, replace=False)
+    beta[idx] = scale * rng.uniform(-1.0, 1.0, size=k)
+    eta = Xf @ beta                          # P:383: logit(prob) = x_i' beta (raw x), centred
+    eta -= eta.mean()
+    y = (rng.random(n) < 1.0 / (1.0 + np.exp(-eta))).astype(np.float64)
+    return Instance(name=f"logit_{kind}_{n}x{p}", X=to_colmajor(X, X.dtype), n=n, y=y,
+                    alpha=alpha, beta_true=beta, seed=seed)
+
+
+def logit_sim(seed=0, n=1000, p=100_000, device=None):
+    """Bench workload for the logistic path (NEXT-3), shaped like the P:383 simulation:
+    x_ij iid N(0,1) stored fp32, 20 true features with coefficients U(-1, 1),
+    y_i ~ Bin(1, sigmoid(x_i' beta)); 100 log-spaced lambdas to 0.1 lambda_max."""
+    import torch
+    dev = _torch_dev(device)
+    ld = padded_ld(n, np.float32)
+    X = torch.zeros((p, ld), dtype=torch.float32, device=dev)
+    for b in range((p + BLOCK - 1) // BLOCK):
+        j0, j1 = b * BLOCK, min(p, (b + 1) * BLOCK)
+        X[j0:j1, :n] = torch.randn((j1 - j0, n), generator=_gen(dev, seed + 77, b), device=dev,
+                                   dtype=torch.float32)
+    rng = np.random.default_rng(seed + 5)
+    idx = np.sort(rng.choice(p, size=20, replace=False))
+    bv = rng.uniform(-1.0, 1.0, size=20)
+    beta = np.zeros(p); beta[idx] = bv
+    eta = (X[torch.as_tensor(idx, device=dev), :n].double().T @ torch.as_tensor(bv, device=dev)).cpu().numpy()
+    y = (rng.random(n) < 1.0 / (1.0 + np.exp(-eta))).astype(np.float64)
+    return Instance("logit", X, n, y, alpha=1.0, ratio=0.1, tol=1e-7, beta_true=beta, seed=seed)
+
+
 CONFIGS = {"cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3, "cfg4": cfg4, "cfg5": cfg5}

@@ -363,3 +363,129 @@ def test_bedpp_power_shape():
     lm, _ = oracle.lambda_max(inst, inst.y)
     assert oracle.bedpp_discard(inst, inst.y, 1.0, 0.97 * lm).mean() > 0.9
     assert oracle.bedpp_discard(inst, inst.y, 1.0, 0.2 * lm).mean() < 0.05
+
+
+# ------------------------------------------------------------ NEXT-3: logistic path
+# Pins for oracle.fit_path_binomial (QL1-QL6): the null model and lambda_max closed
+# forms, the KKT conditions recomputed here in numpy, an independent minimiser
+# (scipy L-BFGS-B on the split-variable form of QL1), label-flip symmetry and the
+# input errors.
+
+def _logit_fixture(n=80, p=10, seed=3, kind="iid", dtype=np.float64, const_cols=0):
+    return synth.logistic_instance(n, p, dtype=dtype, seed=seed, kind=kind, n_true=4, scale=2.0,
+                                   const_cols=const_cols)
+
+
+def _np_std(inst):
+    Xf = inst.host_X()[:, :inst.n].T.astype(np.float64)
+    sd = Xf.std(0)
+    return np.where(sd > 0, (Xf - Xf.mean(0)) / np.where(sd > 0, sd, 1.0), 0.0), sd > 0
+
+
+def _sig(t):
+    return 0.5 * (1.0 + np.tanh(0.5 * t))
+
+
+def test_binomial_null_model_and_lambda_max():
+    inst = _logit_fixture()
+    Xs, live = _np_std(inst)
+    y = inst.y
+    ybar = y.mean()
+    lmax = np.abs(Xs.T @ (y - ybar)).max() / inst.n            # QL2, alpha = 1
+    lm_or, _ = oracle.lambda_max(inst, y, 1.0)                 # same closed form as the linear model
+    assert abs(lm_or - lmax) <= 1e-12 * lmax
+    lams = lmax * np.array([1.0, 0.999, 0.9])
+    op = oracle.fit_path_binomial(inst, y, lams, tol=1e-12)
+    assert np.all(op.beta[:, 0] == 0.0)
+    assert abs(op.b0[0] - math.log(ybar / (1 - ybar))) <= 1e-14
+    assert abs(op.a0[0] - math.log(ybar / (1 - ybar))) <= 1e-14
+    # just below lambda_max only the argmax feature enters
+    jstar = int(np.argmax(np.abs(Xs.T @ (y - ybar))))
+    assert set(np.flatnonzero(op.beta[:, 1])) == {jstar}
+
+
+@pytest.mark.parametrize("alpha", [1.0, 0.5])
+@pytest.mark.parametrize("kind,dtype", [("iid", np.float64), ("corr", np.float32), ("geno", np.int8)])
+def test_binomial_kkt_along_path(alpha, kind, dtype):
+    inst = _logit_fixture(n=120, p=30, seed=5, kind=kind, dtype=dtype, const_cols=2)
+    Xs, live = _np_std(inst)
+    y = inst.y
+    lmax = np.abs(Xs.T @ (y - y.mean())).max() / (inst.n * alpha)
+    lams = synth.lambda_grid(lmax, 25, 0.05)
+    op = oracle.fit_path_binomial(inst, y, lams, alpha=alpha, tol=1e-12)
+    assert op.n_converged == len(lams)
+    for k, lam in enumerate(lams):
+        b = op.beta[:, k]
+        assert np.all(b[~live] == 0.0)
+        eta = op.b0[k] + Xs @ b
+        g = Xs.T @ (y - _sig(eta)) / inst.n                     # gradient of the mean log-likelihood
+        assert abs(np.sum(y - _sig(eta))) / inst.n <= 1e-9     # unpenalised intercept
+        nz = b != 0
+        assert np.all(np.abs(g[~nz & live]) <= alpha * lam + 1e-9)
+        assert np.all(np.abs(g[nz] - alpha * lam * np.sign(b[nz]) - lam * (1 - alpha) * b[nz]) <= 1e-9)
+        # objective evaluator = the QL1 formula
+        q = np.mean(np.logaddexp(0.0, eta) - y * eta) + lam * (alpha * np.abs(b).sum() + 0.5 * (1 - alpha) * b @ b)
+        assert abs(oracle.objective_binomial(inst, y, op.b0[k], b, lam, alpha) - q) <= 1e-12 * abs(q)
+        assert abs(op.obj[k] - q) <= 1e-10 * abs(q)
+
+
+@pytest.mark.parametrize("alpha", [1.0, 0.5])
+def test_binomial_matches_lbfgsb(alpha):
+    """Independent minimiser of QL1: L-BFGS-B over (b0, b+, b-) with b+, b- >= 0."""
+    from scipy.optimize import minimize
+    inst = _logit_fixture(n=90, p=8, seed=11)
+    Xs, _ = _np_std(inst)
+    y, n, p = inst.y, inst.n, Xs.shape[1]
+    lmax = np.abs(Xs.T @ (y - y.mean())).max() / (n * alpha)
+    lams = lmax * np.array([0.8, 0.5, 0.25, 0.1])
+    op = oracle.fit_path_binomial(inst, y, lams, alpha=alpha, tol=1e-13)
+    for k, lam in enumerate(lams):
+        def f(t):
+            b0, bp, bm = t[0], t[1:p + 1], t[p + 1:]
+            b = bp - bm
+            eta = b0 + Xs @ b
+            mu = _sig(eta)
+            val = np.mean(np.logaddexp(0.0, eta) - y * eta) + lam * (alpha * (bp + bm).sum() + 0.5 * (1 - alpha) * b @ b)
+            gb = Xs.T @ (mu - y) / n + lam * (1 - alpha) * b
+            return val, np.concatenate([[np.mean(mu - y)], gb + lam * alpha, -gb + lam * alpha])
+        res = minimize(f, np.zeros(2 * p + 1), jac=True, method="L-BFGS-B",
+                       bounds=[(None, None)] + [(0, None)] * (2 * p),
+                       options=dict(ftol=1e-15, gtol=1e-12, maxiter=20000))
+        b_ref = res.x[1:p + 1] - res.x[p + 1:]
+        scale = max(np.abs(b_ref).max(), 1e-3)
+        assert np.abs(op.beta[:, k] - b_ref).max() <= 1e-5 * scale, (k, op.beta[:, k], b_ref)
+        assert abs(op.b0[k] - res.x[0]) <= 1e-5
+        assert op.obj[k] <= res.fun + 1e-12
+
+
+def test_binomial_label_flip_symmetry():
+    """y -> 1 - y maps the solution (b0, b) to (-b0, -b) (the loss is odd in eta <-> y)."""
+    inst = _logit_fixture(n=70, p=12, seed=21)
+    lm, _ = oracle.lambda_max(inst, inst.y, 1.0)
+    lams = synth.lambda_grid(lm, 12, 0.1)
+    a = oracle.fit_path_binomial(inst, inst.y, lams, tol=1e-13)
+    b = oracle.fit_path_binomial(inst, 1.0 - inst.y, lams, tol=1e-13)
+    np.testing.assert_allclose(a.beta, -b.beta, rtol=0, atol=1e-9)
+    np.testing.assert_allclose(a.b0, -b.b0, rtol=0, atol=1e-9)
+    np.testing.assert_allclose(a.obj, b.obj, rtol=1e-12)
+
+
+def test_binomial_plain_and_cycle_active_agree():
+    inst = _logit_fixture(n=60, p=15, seed=8, kind="corr")
+    lm, _ = oracle.lambda_max(inst, inst.y, 1.0)
+    lams = synth.lambda_grid(lm, 10, 0.1)
+    a = oracle.fit_path_binomial(inst, inst.y, lams, tol=1e-13, cycle_active=True)
+    b = oracle.fit_path_binomial(inst, inst.y, lams, tol=1e-13, cycle_active=False)
+    np.testing.assert_allclose(a.beta, b.beta, rtol=0, atol=1e-9)
+
+
+def test_binomial_input_errors():
+    inst = _logit_fixture(n=40, p=5, seed=2)
+    lams = np.array([0.1, 0.05])
+    y = inst.y.copy(); y[0] = 0.5
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.fit_path_binomial(inst, y, lams)
+    assert e.value.code == oracle.ERR_ARG
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.fit_path_binomial(inst, np.ones(inst.n), lams)
+    assert e.value.code == oracle.ERR_DEGENERATE
