@@ -151,6 +151,26 @@ bl_status bl_fit_path(bl_design *d, const double *y, const double *lambda, int n
  * recomputed on its training rows (Q16) without copying X: held-out rows are
  * masked.  The grid is shared.  Also fits the full data.
  * Errors: K < 2, K > n, an empty fold. */
+/* ---- NEXT-3: lasso / elastic-net penalised LOGISTIC regression path -------------
+ * SURVEY 8(f) NEXT-3; P:174 ("sparse linear and logistic regression models with
+ * lasso and elastic net penalties").  Minimises, per lambda_k,
+ *   Q(b0, b) = (1/n) sum_i [log(1 + e^eta_i) - y_i eta_i] + lambda [alpha |b|_1 + (1-alpha)/2 |b|^2],
+ *   eta_i = b0 + x~_i' b   (QL1; b0 unpenalised)
+ * by IRLS with weighted coordinate descent on W (QL4-QL6).  lambda_max is
+ * bl_lambda_max's value (QL2: the same closed form).  Screening: the sequential
+ * strong rule with z_j = x~_j'(y - p^)/n and the KKT check over all live columns;
+ * BL_SCREEN_HYBRID runs as BL_SCREEN_SSR (QL3: BEDPP is a linear-model rule and the
+ * paper's Slores formulas are not printed).
+ * y: n host doubles, each 0 or 1 (BL_ERR_ARG otherwise); a single class is
+ * BL_ERR_DEGENERATE.  The result is a bl_path: a0[k] is the intercept on the
+ * original scale (b0 - sum_j b_j c_j / s_j), objective[k] = Q at the solution.
+ * Other arguments, errors and ownership as bl_fit_path.  Not available under CV. */
+bl_status bl_fit_path_binomial(bl_design *d, const double *y, const double *lambda, int n_lambda, double alpha,
+                               double tol, int max_iter, int screen, const bl_opts *opts, bl_path **out);
+/* IRLS (outer) iterations of the last solve at each lambda (n_lambda entries; 0 for
+ * null-model lambdas).  BL_ERR_ARG for a linear-model path. */
+bl_status bl_path_irls(const bl_path *path, int32_t *outer);
+
 bl_status bl_cv(bl_design *d, const double *y, const double *lambda, int n_lambda, double alpha,
                 double tol, int max_iter, int n_folds, const int32_t *fold_id, uint64_t seed,
                 const bl_opts *opts, bl_cvres **out);

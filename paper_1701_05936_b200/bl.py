@@ -62,7 +62,7 @@ class bl_perf(ctypes.Structure):
 
 _lib = None
 EXPORTS = ["bl_load_design", "bl_nccl_unique_id", "bl_lambda_max", "bl_fit_path", "bl_cv", "bl_path_info",
-           "bl_path_copy", "bl_path_perf", "bl_path_screen", "bl_cv_copy", "bl_cv_errors", "bl_cv_perf", "bl_prepare", "bl_prep_copy",
+           "bl_path_copy", "bl_path_perf", "bl_path_screen", "bl_fit_path_binomial", "bl_path_irls", "bl_cv_copy", "bl_cv_errors", "bl_cv_perf", "bl_prepare", "bl_prep_copy",
            "bl_bedpp", "bl_scan", "bl_free", "bl_last_error"]
 
 
@@ -85,6 +85,8 @@ def lib():
     L.bl_path_copy.argtypes = [P] + [P] * 10
     L.bl_path_perf.argtypes = [P, P]
     L.bl_path_screen.argtypes = [P, P, P, P]
+    L.bl_fit_path_binomial.argtypes = [P, P, P, I, D, D, I, I, P, PP]
+    L.bl_path_irls.argtypes = [P, P]
     L.bl_cv_copy.argtypes = [P, P, P, P, P, PP]
     L.bl_cv_errors.argtypes = [P, P]
     L.bl_cv_perf.argtypes = [P, P]
@@ -249,6 +251,23 @@ class Design:
         _check(rc, allow=() if raise_on_error else (BL_ERR_CONVERGENCE,))
         try:
             return Path(h, rc)
+        finally:
+            lib().bl_free(h)
+
+    def fit_path_binomial(self, y, lam, alpha=1.0, tol=1e-7, max_iter=10000, screen="ssr", stream=None,
+                          profile=False, max_kkt_rounds=0, raise_on_error=True):
+        """Penalised logistic path (NEXT-3, bl_fit_path_binomial); y in {0, 1}."""
+        lam = _f64(lam)
+        o = bl_opts(stream, int(profile), max_kkt_rounds, 0)
+        h = ctypes.c_void_p()
+        rc = lib().bl_fit_path_binomial(self.h, _p(_f64(y)), _p(lam), lam.size, alpha, tol, max_iter,
+                                        SCREEN.get(screen, screen), ctypes.byref(o), ctypes.byref(h))
+        _check(rc, allow=() if raise_on_error else (BL_ERR_CONVERGENCE,))
+        try:
+            path = Path(h, rc)
+            path.outer = np.zeros(lam.size, np.int32)
+            _check(lib().bl_path_irls(h, _p(path.outer)))
+            return path
         finally:
             lib().bl_free(h)
 

@@ -197,6 +197,8 @@ struct bl_path {
     std::vector<int32_t> passes, kkt_rounds;
     std::vector<int64_t> cols_scanned;
     std::vector<int64_t> n_safe, n_strong, n_working;   // screening diagnostics per lambda (Fig 1 analog)
+    std::vector<int32_t> outer;                          // logistic path: IRLS iterations (last solve) per lambda
+    int family = 0;
     bl_perf perf;
     int64_t cd_visits = 0, cd_updates = 0, cd_cycles = 0, cd_prof[4] = {0, 0, 0, 0};
 };
@@ -232,6 +234,7 @@ struct bl_prep {
     int *scope, *viol, *strong, *W;
     int64_t Wcap;
     double *betaW, *yt, *rfull, *rscan, *vtmp;
+    double *yraw;             // y as given (the logistic path's 0/1 response)
     int8_t *limbs;
     double *limb_scale, *limb_sum;
     PrepScalars *ps;
@@ -702,7 +705,7 @@ bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double a
                o_rf = take(8 * pp->vlen), o_rs = take(8 * pp->vlen), o_vt = take(8 * pp->vlen),
                o_limbs = take((size_t)8 * pp->limb_ld), o_lsc = take(32), o_ps = take(sizeof(PrepScalars)),
                o_st = take(sizeof(RoundStatus)), o_av = take(8 * pp->amax_blocks), o_ai = take(8 * pp->amax_blocks),
-               o_nl = take(16), o_rp = take(16 * (pp->vlen / 256 + 1));
+               o_nl = take(16), o_rp = take(16 * (pp->vlen / 256 + 1)), o_yr = take(8 * pp->vlen);
         pp->arena_bytes = off;
         cudaError_t e = cudaMalloc(&pp->arena, off);
         if (e != cudaSuccess) { cudaGetLastError(); raise(BL_ERR_OOM, "cudaMalloc(%zu) failed: %s", off, cudaGetErrorString(e)); }
@@ -717,6 +720,7 @@ bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double a
         pp->ps = (PrepScalars *)(A + o_ps); pp->st = (RoundStatus *)(A + o_st);
         pp->amax_v = (double *)(A + o_av); pp->amax_i = (long long *)(A + o_ai); pp->nlive = (int *)(A + o_nl);
         pp->rpart = (double *)(A + o_rp);
+        pp->yraw = (double *)(A + o_yr);
         pp->Wcap = 0;
         ensure_W(pp, std::min<int64_t>(p, 4096));
     }
@@ -735,6 +739,7 @@ bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double a
     }
     // y -> device (staged through the rfull buffer, then centred in place into yt / rfull)
     CK(cudaMemcpyAsync(pp->vtmp, y, 8 * n, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(pp->yraw, pp->vtmp, 8 * n, cudaMemcpyDeviceToDevice, st));
     {
         EvPair ev(pp, &pp->ev_prep);
         k_center_y<<<1, 1024, 0, st>>>(pp->vtmp, (int)n, (int)pp->vlen, train ? pp->mask : nullptr, pp->nt,
@@ -1007,6 +1012,63 @@ void launch_cd(bl_prep *pp, int nW, double lam, double alpha, double tol, int ma
     pp->launches++;
 }
 
+// ---- NEXT-3 logistic path: IRLS + weighted CD, one CTA per fit (k_cd_logit)
+template <typename T, bool M>
+const void *logit_kernel_rm(int R) {
+    if (R <= 4) return (const void *)k_cd_logit<T, M, 4>;
+    if (R <= 8) return (const void *)k_cd_logit<T, M, 8>;
+    return (const void *)k_cd_logit<T, M, 16>;
+}
+const void *logit_kernel(int dt, bool mask, int R) {
+    if (dt == DT_F64) return mask ? logit_kernel_rm<double, true>(R) : logit_kernel_rm<double, false>(R);
+    if (dt == DT_F32) return mask ? logit_kernel_rm<float, true>(R) : logit_kernel_rm<float, false>(R);
+    return mask ? logit_kernel_rm<int8_t, true>(R) : logit_kernel_rm<int8_t, false>(R);
+}
+
+void launch_cd_logit(bl_prep *pp, int nW, double lam, double alpha, double tol, int max_iter) {
+    bl_design *d = pp->d;
+    const CdView v = cd_view(pp);
+    CdLogitArgs ca{};
+    ca.X = v.X;
+    ca.ld = d->ld;
+    ca.n = (int)d->n;
+    ca.W = v.Wsorted;
+    ca.nW = nW;
+    ca.c = v.c;
+    ca.s = v.s;
+    ca.beta = v.beta;
+    ca.eta = pp->rfull;                 // the logistic path keeps eta where the linear one keeps r
+    ca.y = pp->yraw;
+    ca.r_scan = pp->rscan;
+    ca.mask = pp->has_mask ? pp->mask : nullptr;
+    ca.lam_alpha = lam * alpha;
+    ca.lam_l2 = lam * (1.0 - alpha);
+    ca.inv_n = 1.0 / pp->nt;
+    ca.tol = tol;
+    ca.floor_ = 1e-13 * (alpha * lam + 1.0);   // Q6 noise floor (QL6)
+    ca.max_iter = max_iter;
+    ca.betaW_out = pp->betaW;
+    ca.st = pp->st;
+    const int T = cd_threads(d->n);
+    const int R = (int)((d->n + T - 1) / T);
+    const size_t smem = (size_t)kCdLogitSlotBytes * nW + (size_t)4 * round_up(d->n, 2) + 16;
+    const void *kern = logit_kernel(d->dt, pp->has_mask != 0, R);
+    const size_t lim = allow_dyn_smem(kern);
+    if (smem > lim)
+        raise(BL_ERR_OOM, "working set of %d columns does not fit the logistic CD kernel's shared memory (n=%lld)",
+              nW, (long long)d->n);
+    EvPair ev(pp, &pp->ev_cd);
+    void *args[] = {&ca};
+    CK(cudaLaunchKernel(kern, dim3(1), dim3(T), args, smem, pp->stream));
+    pp->launches++;
+}
+
+__global__ void k_logit_init(double *eta, int ld, const PrepScalars *ps, RoundStatus *st) {
+    const double yb = ps->ybar, b0 = log(yb / (1.0 - yb));     // the null model (QL2)
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ld; i += gridDim.x * blockDim.x) eta[i] = b0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->b0 = b0;
+}
+
 // ---- NEXT-2 Gram CD (covariance updates) -------------------------------------
 // Workspace after G: G_AA (ldG^2), block inverses (32 ldG), then the cluster
 // kernel's global state: gradients, catch-up deltas (fp64), active list, catch-up
@@ -1180,6 +1242,7 @@ struct PathRun {
     int max_iter, screen, max_rounds;
     bl_path *out;
     double *heldout;              // device, n_lambda x n, or nullptr
+    int family = 0;               // 0 gaussian, 1 binomial (NEXT-3)
     WorkingSet W;
     bool first = true;
     double lam_prev = 0.0, lam = 0.0, lam_next = -1.0, snap = 0.0;
@@ -1203,11 +1266,18 @@ struct PathRun {
         out->n_safe.assign(K, 0);
         out->n_strong.assign(K, 0);
         out->n_working.assign(K, 0);
+        out->outer.assign(K, 0);
+        out->family = family;
         out->col_ptr.assign(K + 1, 0);
         const int bthreads = 256;
         bgrid = (int)std::min<int64_t>((d->p + 4 * bthreads - 1) / (4 * bthreads), (int64_t)d->nsm * 8);   // k_bedpp: 1024 cols/block-step
-        use_bedpp = screen == BL_SCREEN_HYBRID;
+        use_bedpp = screen == BL_SCREEN_HYBRID && family == 0;   // QL3: BEDPP is a linear-model rule
         lam_prev = pp->hps.lmax;
+        if (family == 1) {
+            k_logit_init<<<(unsigned)((d->ld + 255) / 256), 256, 0, st>>>(pp->rfull, (int)d->ld, pp->ps, pp->st);
+            CKL();
+            pp->launches++;
+        }
         snap = pp->hps.lmax * (1.0 - 1e-12);                   // Q25
         if (screen == BL_SCREEN_NONE) {
             // W = every non-constant column; no screening, no scans (SPEC "policy none")
@@ -1243,8 +1313,14 @@ struct PathRun {
         nsafe_k = screen == BL_SCREEN_NONE ? pp->hps.n_live : 0;
         if (lam >= snap) {          // null solution, exactly (Q25)
             flush();
-            out->a0[k] = pp->hps.ybar;
-            out->obj[k] = pp->hps.Y2 / (2.0 * pp->nt);
+            if (family == 1) {          // null logistic model: b0 = logit(ybar), Q = binary entropy of ybar
+                const double yb = pp->hps.ybar;
+                out->a0[k] = std::log(yb / (1.0 - yb));
+                out->obj[k] = -(yb * std::log(yb) + (1.0 - yb) * std::log1p(-yb));
+            } else {
+                out->a0[k] = pp->hps.ybar;
+                out->obj[k] = pp->hps.Y2 / (2.0 * pp->nt);
+            }
             out->col_ptr[k + 1] = out->col_ptr[k];
             out->n_converged = k + 1;
             heldout_errors();       // null model: rfull = y_i - ybar_train
@@ -1277,7 +1353,8 @@ struct PathRun {
         return true;
     }
     void solve() {
-        solve_cd(pp, W.size(), lam, alpha, tol, max_iter);
+        if (family == 1) launch_cd_logit(pp, W.size(), lam, alpha, tol, max_iter);
+        else solve_cd(pp, W.size(), lam, alpha, tol, max_iter);
         if (screen != BL_SCREEN_NONE) CK(cudaMemsetAsync(&pp->st->nviol, 0, 2 * sizeof(int), pp->stream));
     }
     // the fused KKT + strong-rule scan of this round (a9)
@@ -1377,8 +1454,15 @@ struct PathRun {
             shift += bq * cq / sq;
         }
         out->col_ptr[r.k + 1] = (int64_t)out->feat.size();
-        out->a0[r.k] = pp->hps.ybar - shift;
-        out->obj[r.k] = r.rs.rss / (2.0 * pp->nt) + r.lam * (alpha * r.rs.l1 + 0.5 * (1.0 - alpha) * r.rs.l2);
+        const double pen = r.lam * (alpha * r.rs.l1 + 0.5 * (1.0 - alpha) * r.rs.l2);
+        if (family == 1) {              // QL1: intercept b0 on the standardised scale; loss sum in rs.rss
+            out->a0[r.k] = r.rs.b0 - shift;
+            out->obj[r.k] = r.rs.rss / pp->nt + pen;
+            out->outer[r.k] = r.rs.outer;
+        } else {
+            out->a0[r.k] = pp->hps.ybar - shift;
+            out->obj[r.k] = r.rs.rss / (2.0 * pp->nt) + pen;
+        }
         out->passes[r.k] = r.passes;
         out->kkt_rounds[r.k] = r.rounds;
         out->cols_scanned[r.k] = r.scanned;
@@ -1411,8 +1495,9 @@ struct PathRun {
 };
 
 bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, double tol, int max_iter, int screen,
-                   int max_rounds, bl_path *out, double *heldout /* device, n_lambda x n, or nullptr */) {
-    PathRun pr{pp, lambda, K, alpha, tol, max_iter, screen, max_rounds, out, heldout};
+                   int max_rounds, bl_path *out, double *heldout /* device, n_lambda x n, or nullptr */,
+                   int family = 0) {
+    PathRun pr{pp, lambda, K, alpha, tol, max_iter, screen, max_rounds, out, heldout, family};
     pr.begin();
     cudaStream_t st = pp->stream;
     for (int k = 0; k < K; k++) {
@@ -1661,7 +1746,7 @@ void cv_lockstep(bl_design *d, const double *y, const std::vector<int32_t> &fold
 
 bl_path *fit_impl(bl_design *d, const double *y, const uint8_t *train, const double *lambda, int K, double alpha,
                   double tol, int max_iter, int screen, const bl_opts *opts, bl_status *st_out,
-                  double *heldout = nullptr) {
+                  double *heldout = nullptr, int family = 0) {
     auto t0 = std::chrono::steady_clock::now();
     validate_grid(lambda, K);
     if (!(tol > 0.0)) raise(BL_ERR_ARG, "tol must be > 0");
@@ -1675,7 +1760,7 @@ bl_path *fit_impl(bl_design *d, const double *y, const uint8_t *train, const dou
     std::string saved;
     bl_status s;
     try {
-        s = run_path(pp, lambda, K, alpha, tol, max_iter, screen, rounds, out, heldout);
+        s = run_path(pp, lambda, K, alpha, tol, max_iter, screen, rounds, out, heldout, family);
     } catch (...) {
         delete out;
         throw;
@@ -1957,6 +2042,25 @@ bl_status bl_fit_path(bl_design *d, const double *y, const double *lambda, int n
     return g != BL_OK ? g : s;
 }
 
+bl_status bl_fit_path_binomial(bl_design *d, const double *y, const double *lambda, int n_lambda, double alpha,
+                               double tol, int max_iter, int screen, const bl_opts *opts, bl_path **out) {
+    bl_status s = BL_OK;
+    bl_status g = guard([&] {
+        if (!d || d->magic != MAGIC_DESIGN) raise(BL_ERR_ARG, "bad design handle");
+        if (!out) raise(BL_ERR_ARG, "out is NULL");
+        if (!y) raise(BL_ERR_ARG, "y is NULL");
+        *out = nullptr;
+        int64_t n1 = 0;
+        for (int64_t i = 0; i < d->n; i++) {
+            if (!(y[i] == 0.0 || y[i] == 1.0)) raise(BL_ERR_ARG, "binomial y[%lld] = %g is not 0 or 1", (long long)i, y[i]);
+            n1 += y[i] == 1.0;
+        }
+        if (n1 == 0 || n1 == d->n) raise(BL_ERR_DEGENERATE, "binomial y has a single class (S:311)");
+        *out = fit_impl(d, y, nullptr, lambda, n_lambda, alpha, tol, max_iter, screen, opts, &s, nullptr, 1);
+    });
+    return g != BL_OK ? g : s;
+}
+
 bl_status bl_cv(bl_design *d, const double *y, const double *lambda, int n_lambda, double alpha, double tol,
                 int max_iter, int n_folds, const int32_t *fold_id, uint64_t seed, const bl_opts *opts,
                 bl_cvres **out) {
@@ -2129,6 +2233,14 @@ bl_status bl_path_screen(const bl_path *p, int64_t *n_safe, int64_t *n_strong, i
         if (n_safe) std::copy(p->n_safe.begin(), p->n_safe.begin() + std::min(K, p->n_safe.size()), n_safe);
         if (n_strong) std::copy(p->n_strong.begin(), p->n_strong.begin() + std::min(K, p->n_strong.size()), n_strong);
         if (n_working) std::copy(p->n_working.begin(), p->n_working.begin() + std::min(K, p->n_working.size()), n_working);
+    });
+}
+
+bl_status bl_path_irls(const bl_path *p, int32_t *outer) {
+    return guard([&] {
+        if (!p || p->magic != MAGIC_PATH) raise(BL_ERR_ARG, "bad path handle");
+        if (p->family != 1) raise(BL_ERR_ARG, "not a logistic path");
+        if (outer) std::copy(p->outer.begin(), p->outer.end(), outer);
     });
 }
 

@@ -45,6 +45,8 @@ struct RoundStatus {
     long long cd_prof[4];              // Gram CD phase cycles: leader steps, bulk steps, G_AA/M builds, lazy catch-ups
     long long cd_cnt[4];               // Gram CD events: speculation retries, G_AA builds, catch-ups, full sweeps
     long long cd_dbg[8];               // Gram CD sub-phase cycles (micro-benchmarks only)
+    double b0;                         // logistic path: intercept on the standardised scale (in/out)
+    int outer, pad2;                   // logistic path: IRLS iterations of the last solve
 };
 
 // ---------------------------------------------------------------- small helpers
@@ -1056,6 +1058,308 @@ __global__ void __launch_bounds__(RM >= 16 ? 1024 : 512, 1) k_cd(CdArgs a) {
         a.st->cd_visits = visits;
         a.st->cd_updates = updates;
         a.st->cd_cycles = clock64() - clk0;
+    }
+}
+
+// ------------------------------ NEXT-3: logistic (binomial) path, IRLS + weighted CD
+// SURVEY 8(f) NEXT-3; objective QL1: mean_i [log(1+e^eta_i) - y_i eta_i]
+// + lambda (alpha |b|_1 + (1-alpha)/2 |b|^2), eta = b0 + X~ b.  ONE persistent CTA per
+// fit, the row layout of k_cd: thread t owns rows t + kT and keeps their working
+// residual rho_i = w_i (zr_i - eta_i) in registers.  Per IRLS (outer) iteration:
+//   pi = sigmoid(eta), w = max(pi (1-pi), 1e-5) (QL5), rho = y - pi on used rows;
+//   v_j = x~_j' W x~_j / n for every slot (one warp per column);
+//   weighted CD (active cycling, then full passes over W), intercept first per pass:
+//     b0 += sum rho / sum w;  rho -= d0 w
+//     u = x~_j' rho / n + v_j b_j;  b' = S(u, lambda alpha) / (v_j + lambda (1-alpha));
+//     rho -= (b' - b_j) w x~_j
+//   eta = b0 + X~_A b_A recomputed from the columns (all rows, held-out ones too);
+// until an outer iteration moves b by <= tol max|b| and b0 by <= tol max(1,|b0|) (QL6).
+// Output r_scan = y - pi on used rows (the KKT / strong-rule scan vector, SPEC S:312
+// "SSR screening uses z_j = x~_j'(y - p^)/n").  The weights are held in fp32: the
+// fixed point depends only on the exact gradient y - pi (QL5).
+struct CdLogitArgs {
+    const void *X;
+    int64_t ld;
+    int n;
+    const int *W;           // sorted slot columns (view)
+    int nW;
+    const double *c, *s;
+    double *beta;           // by view column
+    double *eta;            // ld entries: linear predictor on every row (in/out)
+    const double *y;        // n entries, 0/1
+    double *r_scan;         // ld entries out: y - pi on used rows, 0 elsewhere
+    const uint8_t *mask;
+    double lam_alpha, lam_l2, inv_n, tol, floor_;
+    int max_iter;
+    double *betaW_out;      // 3 nW: beta, c, s per slot
+    RoundStatus *st;        // st->b0 in/out
+};
+
+constexpr int kCdLogitSlotBytes = 48;    // beta, c, 1/s, v, beta_prev (fp64) + column, active (int32)
+
+__device__ __forceinline__ double sigmoid_d(double t) {
+    return t >= 0.0 ? 1.0 / (1.0 + exp(-t)) : exp(t) / (1.0 + exp(t));
+}
+
+template <typename T, bool MASK, int RM>
+__global__ void __launch_bounds__(RM >= 16 ? 1024 : 512, 1) k_cd_logit(CdLogitArgs a) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ double part[2][32];
+    __shared__ double red[32];
+    __shared__ int wcount[33];
+    const int T_ = blockDim.x, t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = T_ >> 5;
+    const int n = a.n, nW = a.nW;
+    const int R = (n + T_ - 1) / T_;
+    double *bw = sm, *cw = bw + nW, *iw = cw + nW, *vw = iw + nW, *bo = vw + nW;
+    int *Ws = reinterpret_cast<int *>(bo + nW);
+    int *act = Ws + nW;
+    float *wsm = reinterpret_cast<float *>(act + nW + (nW & 1));     // n weights (8-byte aligned start)
+    for (int w = t; w < nW; w += T_) {
+        const int j = a.W[w];
+        Ws[w] = j;
+        bw[w] = a.beta[j];
+        cw[w] = a.c[j];
+        iw[w] = 1.0 / a.s[j];
+    }
+    unsigned mbits = 0;
+#pragma unroll
+    for (int k = 0; k < RM; k++) {
+        const int i = t + k * T_;
+        const bool use = k < R && i < n && (!MASK || a.mask[i]);
+        mbits |= (use ? 1u : 0u) << k;
+    }
+    double b0 = a.st->b0;
+    __syncthreads();
+    const T *X = reinterpret_cast<const T *>(a.X);
+    const long long clk0 = clock64();
+    int passes = 0, outer = 0, status = 0, buf = 0;
+    long long visits = 0, updates = 0;
+    double rr[RM];
+    double sumw = 0.0;
+
+    // one sweep over slots list[0..len) (nullptr => all): returns max|db|, max|b|
+    auto sweep = [&](const int *list, int len, double &dmax, double &bmax) {
+        dmax = 0.0;
+        bmax = 0.0;
+        visits += len;
+        T xb[2][RM];
+        auto load_col = [&](T (&x)[RM], int qq) {
+            if (qq < len) {
+                const T *col = X + (int64_t)Ws[list ? list[qq] : qq] * a.ld;
+#pragma unroll
+                for (int k = 0; k < RM; k++) { const int i = t + k * T_; x[k] = (k < R && i < n) ? col[i] : T(0); }
+            }
+        };
+        load_col(xb[0], 0);
+        load_col(xb[1], 1);
+        for (int q0 = 0; q0 < len; q0 += 2) {
+#pragma unroll
+            for (int u = 0; u < 2; u++) {
+                const int q = q0 + u;
+                if (q < len) {
+                    const int w = list ? list[q] : q;
+                    const double b_old = bw[w], cj = cw[w], isj = iw[w], vj = vw[w];
+                    double p0 = 0.0, p1 = 0.0;
+#pragma unroll
+                    for (int k = 0; k < RM; k += 2) {
+                        if ((mbits >> k) & 1u) p0 = fma(to_d(xb[u][k]) - cj, rr[k], p0);
+                        if (k + 1 < RM && ((mbits >> (k + 1)) & 1u)) p1 = fma(to_d(xb[u][k + 1]) - cj, rr[k + 1], p1);
+                    }
+                    const double pt = warp_sum(p0 + p1);
+                    if (lane == 0) part[buf][wid] = pt;
+                    __syncthreads();
+                    double s0 = 0.0;
+                    for (int v = 0; v < nw; v++) s0 += part[buf][v];
+                    const double z = s0 * a.inv_n * isj + vj * b_old;
+                    const double bn = soft_threshold(z, a.lam_alpha) / (vj + a.lam_l2);
+                    const double d = bn - b_old;
+                    if (d != 0.0) {
+                        updates++;
+                        const double f = d * isj;
+#pragma unroll
+                        for (int k = 0; k < RM; k++)
+                            if ((mbits >> k) & 1u) rr[k] = fma(-f * (double)wsm[t + k * T_], to_d(xb[u][k]) - cj, rr[k]);
+                        if (t == 0) bw[w] = bn;
+                    }
+                    dmax = fmax(dmax, fabs(d));
+                    bmax = fmax(bmax, fabs(bn));
+                    buf ^= 1;
+                    load_col(xb[u], q + 2);
+                }
+            }
+        }
+        __syncthreads();
+    };
+    // intercept (unpenalised, first in every pass): b0 += sum rho / sum w
+    auto intercept = [&]() -> double {
+        double sr = 0.0;
+#pragma unroll
+        for (int k = 0; k < RM; k++)
+            if ((mbits >> k) & 1u) sr += rr[k];
+        const double d0 = block_sum(sr, red) / sumw;
+#pragma unroll
+        for (int k = 0; k < RM; k++)
+            if ((mbits >> k) & 1u) rr[k] = fma(-d0, (double)wsm[t + k * T_], rr[k]);
+        b0 += d0;
+        return fabs(d0);
+    };
+    auto build_active = [&]() -> int {
+        int total = 0;
+        for (int base = 0; base < nW; base += T_) {
+            const int w = base + t;
+            const bool nz = w < nW && bw[w] != 0.0;
+            const unsigned m = __ballot_sync(0xffffffffu, nz);
+            if (lane == 0) wcount[wid] = __popc(m);
+            __syncthreads();
+            if (t == 0) {
+                int run = 0;
+                for (int u = 0; u < nw; u++) { const int c0 = wcount[u]; wcount[u] = run; run += c0; }
+                wcount[32] = run;
+            }
+            __syncthreads();
+            if (nz) act[total + wcount[wid] + __popc(m & ((1u << lane) - 1u))] = w;
+            total += wcount[32];
+            __syncthreads();
+        }
+        return total;
+    };
+    auto converged = [&](double dmax, double bmax, double d0) {
+        return (dmax <= a.tol * bmax || dmax <= a.floor_) && (d0 <= a.tol * fmax(1.0, fabs(b0)) || d0 <= a.floor_);
+    };
+
+    for (;;) {                                            // ---- outer (IRLS) iterations
+        double wl = 0.0;
+#pragma unroll
+        for (int k = 0; k < RM; k++) {
+            const int i = t + k * T_;
+            rr[k] = 0.0;
+            if (k < R && i < n) {
+                float wv = 0.f;
+                if ((mbits >> k) & 1u) {
+                    const double pi = sigmoid_d(a.eta[i]);
+                    const double w = fmax(pi * (1.0 - pi), 1e-5);       // QL5
+                    wv = (float)w;
+                    rr[k] = a.y[i] - pi;
+                    wl += (double)wv;
+                }
+                wsm[i] = wv;
+            }
+        }
+        sumw = block_sum(wl, red);
+        __syncthreads();                                  // wsm complete
+        for (int w = wid; w < nW; w += nw) {              // v_j = x~_j' W x~_j / n, one warp per slot
+            const T *col = X + (int64_t)Ws[w] * a.ld;
+            const double cj = cw[w];
+            double acc = 0.0;
+            for (int i = lane; i < n; i += 32) {
+                const double x = to_d(col[i]) - cj;
+                acc = fma((double)wsm[i] * x, x, acc);
+            }
+            acc = warp_sum(acc);
+            if (lane == 0) { vw[w] = acc * iw[w] * iw[w] * a.inv_n; bo[w] = bw[w]; }
+        }
+        const double b0o = b0;
+        __syncthreads();
+        // ---- weighted CD on the quadratic model: active cycling, then full passes
+        for (int kind = 0; kind < 2 && !status; kind++) {
+            for (;;) {
+                const double d0 = intercept();
+                double dmax = 0.0, bmax = 0.0;
+                if (kind == 0) {
+                    const int na = build_active();
+                    if (na == 0) { if (++passes > a.max_iter) status = 3; break; }
+                    sweep(act, na, dmax, bmax);
+                } else {
+                    sweep(nullptr, nW, dmax, bmax);
+                }
+                if (++passes > a.max_iter) { status = 3; break; }
+                if (converged(dmax, bmax, d0)) break;
+            }
+        }
+        if (status) break;
+        // ---- eta = b0 + X~_A b_A on every row, from the columns
+        const int na = build_active();
+        double e[RM];
+#pragma unroll
+        for (int k = 0; k < RM; k++) e[k] = b0;
+        for (int q = 0; q < na; q++) {
+            const int w = act[q];
+            const T *col = X + (int64_t)Ws[w] * a.ld;
+            const double f = bw[w] * iw[w], cj = cw[w];
+#pragma unroll
+            for (int k = 0; k < RM; k++) {
+                const int i = t + k * T_;
+                if (k < R && i < n) e[k] = fma(f, to_d(col[i]) - cj, e[k]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < RM; k++) {
+            const int i = t + k * T_;
+            if (k < R && i < n) a.eta[i] = e[k];
+        }
+        // ---- outer convergence (QL6)
+        double dm = 0.0, bm = 0.0;
+        for (int w = t; w < nW; w += T_) { dm = fmax(dm, fabs(bw[w] - bo[w])); bm = fmax(bm, fabs(bw[w])); }
+        dm = block_max(dm, red);
+        __syncthreads();
+        bm = block_max(bm, red);
+        __syncthreads();
+        ++outer;
+        if (outer > a.max_iter) { status = 3; break; }
+        if (converged(dm, bm, fabs(b0 - b0o))) break;
+    }
+    __syncthreads();
+    // ---- write back: r_scan = y - pi, loss, penalty terms (a11)
+    double loss = 0.0, sr = 0.0;
+#pragma unroll
+    for (int k = 0; k < RM; k++) {
+        const int i = t + k * T_;
+        if (k < R && i < n) {
+            double v = 0.0;
+            if ((mbits >> k) & 1u) {
+                const double et = a.eta[i], yi = a.y[i];
+                v = yi - sigmoid_d(et);
+                loss += (et > 0.0 ? et + log1p(exp(-et)) : log1p(exp(et))) - yi * et;
+                sr += v;
+            }
+            a.r_scan[i] = v;
+        }
+    }
+    for (int i = n + t; i < (int)a.ld; i += T_) a.r_scan[i] = 0.0;
+    double l1 = 0.0, l2 = 0.0, nnz = 0.0;
+    for (int w = t; w < nW; w += T_) {
+        const double b = bw[w];
+        const int jw = Ws[w];
+        a.beta[jw] = b;
+        a.betaW_out[w] = b;
+        a.betaW_out[nW + w] = cw[w];
+        a.betaW_out[2 * nW + w] = a.s[jw];
+        l1 += fabs(b);
+        l2 = fma(b, b, l2);
+        nnz += b != 0.0 ? 1.0 : 0.0;
+    }
+    loss = block_sum(loss, red);
+    __syncthreads();
+    sr = block_sum(sr, red);
+    __syncthreads();
+    l1 = block_sum(l1, red);
+    __syncthreads();
+    l2 = block_sum(l2, red);
+    __syncthreads();
+    nnz = block_sum(nnz, red);
+    if (t == 0) {
+        a.st->cd_passes = passes;
+        a.st->cd_status = status;
+        a.st->rss = loss;          // logistic: sum of the per-row losses (objective = rss / n + penalty)
+        a.st->sumr = sr;
+        a.st->l1 = l1;
+        a.st->l2 = l2;
+        a.st->nnz = (int)nnz;
+        a.st->cd_visits = visits;
+        a.st->cd_updates = updates;
+        a.st->cd_cycles = clock64() - clk0;
+        a.st->b0 = b0;
+        a.st->outer = outer;
     }
 }
 
