@@ -96,12 +96,14 @@ class Clocks:
 
 def make_instance(name, device=None):
     import synth
+    if name == "logit":
+        return synth.logit_sim(device=device)
     return synth.CONFIGS[name](device=device) if name != "cfg1" else synth.cfg1()
 
 
 # ---------------------------------------------------------------- oracle legs
 
-def oracle_sample(inst, target_s=15.0, max_cols=None):
+def oracle_sample(inst, target_s=15.0, max_cols=None, binomial=False):
     """Time the oracle (as it stands) on the first p' columns of the workload
     with the full 100-lambda grid (grid anchored at the sample's own lambda_max),
     p' grown until one run takes >= target_s/4, then scaled linearly in p
@@ -116,14 +118,15 @@ def oracle_sample(inst, target_s=15.0, max_cols=None):
         import synth
         lams = synth.lambda_grid(lm, inst.nlam, inst.ratio)
         t0 = time.perf_counter()
-        oracle.fit_path(sub, inst.y, lams, alpha=inst.alpha, tol=inst.tol, cycle_active=True,
-                        raise_on_error=False)
+        fit = oracle.fit_path_binomial if binomial else oracle.fit_path
+        fit(sub, inst.y, lams, alpha=inst.alpha, tol=inst.tol, cycle_active=True, raise_on_error=False)
         dt = time.perf_counter() - t0
         if dt >= target_s / 4 or pp >= p_full or (max_cols and pp >= max_cols):
             break
         pp = min(p_full, max(pp * 2, int(pp * (target_s / 2) / max(dt, 1e-3))))
     scaled = dt * p_full / pp
-    return scaled, f"oracle (naive cyclic CD, fp64, tol {inst.tol:g}, no screening) on the first {pp} of {p_full} columns, full {inst.nlam}-lambda grid; scaled x{p_full / pp:.1f} (linear in p)", dt
+    what = "IRLS + naive cyclic weighted CD" if binomial else "naive cyclic CD"
+    return scaled, f"oracle ({what}, fp64, tol {inst.tol:g}, no screening) on the first {pp} of {p_full} columns, full {inst.nlam}-lambda grid; scaled x{p_full / pp:.1f} (linear in p)", dt
 
 
 def run_reference(args, rank, world):
@@ -134,7 +137,7 @@ def run_reference(args, rank, world):
         pass
     vals, samples = [], ""
     for _ in range(args.steps):
-        v, samples, raw = oracle_sample(inst, target_s=args.ref_seconds)
+        v, samples, raw = oracle_sample(inst, target_s=args.ref_seconds, binomial=args.config == "logit")
         vals.append(v)
     v = statistics.median(vals)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus,
@@ -178,8 +181,11 @@ def run_ours(args, rank, world, local_rank):
     sh = stream.cuda_stream
 
     is_cv = args.config == "cfg5"        # BASELINE cfg5: 10-fold CV -- a step is the whole CV
+    is_logit = args.config == "logit"    # NEXT-3: penalised logistic path (P:379-385 simulation shape)
 
     def step(profile):
+        if is_logit:
+            return d.fit_path_binomial(inst.y, lams, alpha=inst.alpha, tol=inst.tol, stream=sh, profile=profile)
         if is_cv:
             return d.cv(inst.y, lams, K=10, alpha=inst.alpha, tol=inst.tol, seed=0, profile=profile, cd=args.cd)
         return d.fit_path(inst.y, lams, alpha=inst.alpha, tol=inst.tol, stream=sh, profile=profile, cd=args.cd)
@@ -233,7 +239,9 @@ def run_ours(args, rank, world, local_rank):
             dh = bl.Design(Xh, inst.n, dist=dist_of())
             lm_h = dh.lambda_max(inst.y, inst.alpha)
             lams_h = synth.lambda_grid(lm_h, inst.nlam, inst.ratio)
-            if is_cv:
+            if is_logit:
+                ph = dh.fit_path_binomial(inst.y, lams_h, alpha=inst.alpha, tol=inst.tol)
+            elif is_cv:
                 ph = dh.cv(inst.y, lams_h, K=10, alpha=inst.alpha, tol=inst.tol, seed=0).full
             else:
                 ph = dh.fit_path(inst.y, lams_h, alpha=inst.alpha, tol=inst.tol)
@@ -267,7 +275,7 @@ def run_ours(args, rank, world, local_rank):
             traffic = None
     cpu = {"value": None, "unit": "s", "cores": 1, "kind": "oracle", "sample": "skipped (--no-cpu-baseline)"}
     if world == 1 and not args.no_cpu_baseline:
-        v, sample, raw = oracle_sample(inst, target_s=args.ref_seconds)
+        v, sample, raw = oracle_sample(inst, target_s=args.ref_seconds, binomial=is_logit)
         cpu = {"value": v, "unit": "s", "cores": 1, "kind": "oracle", "sample": sample, "raw_seconds": raw}
     line = {
         "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
@@ -277,7 +285,8 @@ def run_ours(args, rank, world, local_rank):
         "data": "synthetic",
         "config": {"workload": args.config, "n": inst.n, "p": p_global, "alpha": inst.alpha,
                    "n_lambda": inst.nlam, "lambda_min_ratio": inst.ratio, "tol": inst.tol,
-                   "screen": "hybrid (SSR-BEDPP)", "cd": args.cd, "X_bytes": int(x_bytes),
+                   "screen": "SSR (logistic, QL3)" if is_logit else "hybrid (SSR-BEDPP)",
+                   "model": "logistic" if is_logit else "gaussian", "cd": args.cd, "X_bytes": int(x_bytes),
                    "cv_folds": 10 if is_cv else None,
                    "l2_policy": "X larger than L2 (126 MB); no flush" if X.numel() * X.element_size() > 126e6
                    else "X fits L2 (reported as such)", "parallelism": f"column-sharded x{world}" if world > 1 else "1 GPU",
@@ -291,7 +300,7 @@ def run_ours(args, rank, world, local_rank):
                      "cd_ns_per_visit": cd_ms / args.steps * 1e6 / max(visits, 1),
                      "cd_kernel_cycles_per_visit": cd_cycles / max(visits, 1),
                      "cd_kernel_ms_per_step": cd_cycles / 1.965e6,
-                     "cd_phase_cycles_per_visit": dict(zip(["lead", "bulk", "build_A", "catch_up"], cd_prof)),
+                     "cd_phase_cycles_per_visit": dict(zip(["cd_passes", "weights_v", "eta", "intercept (within cd_passes)"] if is_logit else ["lead", "bulk", "build_A", "catch_up"], cd_prof)),
                      "algorithmic_bytes_per_step": scan_bytes / args.steps,
                      "full_scan": ({"GBps": fs_bytes / (fs_ms / 1e3) / 1e9, "frac": fs_bytes / (fs_ms / 1e3) / 1e9 / pk["hbm_gbs"],
                                     "launches_per_step": fs_launches} if fs_ms > 0 else None)},
@@ -306,7 +315,8 @@ def run_ours(args, rank, world, local_rank):
                  # Fig 1 analog: fraction of live columns BEDPP keeps, by lambda/lambda_max
                  "bedpp_kept_frac": {f"{q:.1f}": float(last.n_safe[int(np.argmin(np.abs(lams / lm - q)))] / p_global)
                                      for q in (0.9, 0.7, 0.5, 0.3)},
-                 "max_working_set": int(last.n_working.max())},
+                 "max_working_set": int(last.n_working.max()),
+                 **({"irls_iterations": int(last.outer.sum())} if hasattr(last, "outer") else {})},
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
@@ -317,7 +327,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "logit"],
+                    help="BASELINE cfg1-cfg5, or 'logit' (NEXT-3 logistic path, n=1000, p=100,000 fp32)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=15.0)

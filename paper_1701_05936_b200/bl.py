@@ -293,7 +293,10 @@ class Design:
             self.h = None
 
     def __del__(self):
-        self.free()
+        try:
+            self.free()
+        except Exception:      # interpreter shutdown: the module globals may already be gone
+            pass
 
 
 class CvResult:

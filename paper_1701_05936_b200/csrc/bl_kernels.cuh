@@ -1095,7 +1095,7 @@ struct CdLogitArgs {
     RoundStatus *st;        // st->b0 in/out
 };
 
-constexpr int kCdLogitSlotBytes = 48;    // beta, c, 1/s, v, beta_prev (fp64) + column, active (int32)
+constexpr int kCdLogitSlotBytes = 56;    // beta, c, 1/s, v, beta_prev, 1/(v + l2) (fp64) + column, active (int32)
 
 __device__ __forceinline__ double sigmoid_d(double t) {
     return t >= 0.0 ? 1.0 / (1.0 + exp(-t)) : exp(t) / (1.0 + exp(t));
@@ -1110,8 +1110,8 @@ __global__ void __launch_bounds__(RM >= 16 ? 1024 : 512, 1) k_cd_logit(CdLogitAr
     const int T_ = blockDim.x, t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = T_ >> 5;
     const int n = a.n, nW = a.nW;
     const int R = (n + T_ - 1) / T_;
-    double *bw = sm, *cw = bw + nW, *iw = cw + nW, *vw = iw + nW, *bo = vw + nW;
-    int *Ws = reinterpret_cast<int *>(bo + nW);
+    double *bw = sm, *cw = bw + nW, *iw = cw + nW, *vw = iw + nW, *bo = vw + nW, *dv = bo + nW;
+    int *Ws = reinterpret_cast<int *>(dv + nW);
     int *act = Ws + nW;
     float *wsm = reinterpret_cast<float *>(act + nW + (nW & 1));     // n weights (8-byte aligned start)
     for (int w = t; w < nW; w += T_) {
@@ -1134,6 +1134,7 @@ __global__ void __launch_bounds__(RM >= 16 ? 1024 : 512, 1) k_cd_logit(CdLogitAr
     const long long clk0 = clock64();
     int passes = 0, outer = 0, status = 0, buf = 0;
     long long visits = 0, updates = 0;
+    long long ph[4] = {0, 0, 0, 0};     // cycles: CD sweeps, weights + v_j, eta, intercepts (thread 0's clock)
     double rr[RM];
     double sumw = 0.0;
 
@@ -1158,7 +1159,7 @@ __global__ void __launch_bounds__(RM >= 16 ? 1024 : 512, 1) k_cd_logit(CdLogitAr
                 const int q = q0 + u;
                 if (q < len) {
                     const int w = list ? list[q] : q;
-                    const double b_old = bw[w], cj = cw[w], isj = iw[w], vj = vw[w];
+                    const double b_old = bw[w], cj = cw[w], isj = iw[w], vj = vw[w], idv = dv[w];
                     double p0 = 0.0, p1 = 0.0;
 #pragma unroll
                     for (int k = 0; k < RM; k += 2) {
@@ -1171,7 +1172,7 @@ __global__ void __launch_bounds__(RM >= 16 ? 1024 : 512, 1) k_cd_logit(CdLogitAr
                     double s0 = 0.0;
                     for (int v = 0; v < nw; v++) s0 += part[buf][v];
                     const double z = s0 * a.inv_n * isj + vj * b_old;
-                    const double bn = soft_threshold(z, a.lam_alpha) / (vj + a.lam_l2);
+                    const double bn = soft_threshold(z, a.lam_alpha) * idv;
                     const double d = bn - b_old;
                     if (d != 0.0) {
                         updates++;
@@ -1192,6 +1193,7 @@ __global__ void __launch_bounds__(RM >= 16 ? 1024 : 512, 1) k_cd_logit(CdLogitAr
     };
     // intercept (unpenalised, first in every pass): b0 += sum rho / sum w
     auto intercept = [&]() -> double {
+        const long long c0 = clock64();
         double sr = 0.0;
 #pragma unroll
         for (int k = 0; k < RM; k++)
@@ -1201,6 +1203,7 @@ __global__ void __launch_bounds__(RM >= 16 ? 1024 : 512, 1) k_cd_logit(CdLogitAr
         for (int k = 0; k < RM; k++)
             if ((mbits >> k) & 1u) rr[k] = fma(-d0, (double)wsm[t + k * T_], rr[k]);
         b0 += d0;
+        ph[3] += clock64() - c0;
         return fabs(d0);
     };
     auto build_active = [&]() -> int {
@@ -1228,6 +1231,7 @@ __global__ void __launch_bounds__(RM >= 16 ? 1024 : 512, 1) k_cd_logit(CdLogitAr
     };
 
     for (;;) {                                            // ---- outer (IRLS) iterations
+        long long c0 = clock64();
         double wl = 0.0;
 #pragma unroll
         for (int k = 0; k < RM; k++) {
@@ -1256,10 +1260,17 @@ __global__ void __launch_bounds__(RM >= 16 ? 1024 : 512, 1) k_cd_logit(CdLogitAr
                 acc = fma((double)wsm[i] * x, x, acc);
             }
             acc = warp_sum(acc);
-            if (lane == 0) { vw[w] = acc * iw[w] * iw[w] * a.inv_n; bo[w] = bw[w]; }
+            if (lane == 0) {
+                const double v = acc * iw[w] * iw[w] * a.inv_n;
+                vw[w] = v;
+                dv[w] = 1.0 / (v + a.lam_l2);
+                bo[w] = bw[w];
+            }
         }
         const double b0o = b0;
         __syncthreads();
+        ph[1] += clock64() - c0;
+        c0 = clock64();
         // ---- weighted CD on the quadratic model: active cycling, then full passes
         for (int kind = 0; kind < 2 && !status; kind++) {
             for (;;) {
@@ -1276,7 +1287,9 @@ __global__ void __launch_bounds__(RM >= 16 ? 1024 : 512, 1) k_cd_logit(CdLogitAr
                 if (converged(dmax, bmax, d0)) break;
             }
         }
+        ph[0] += clock64() - c0;
         if (status) break;
+        c0 = clock64();
         // ---- eta = b0 + X~_A b_A on every row, from the columns
         const int na = build_active();
         double e[RM];
@@ -1297,6 +1310,7 @@ __global__ void __launch_bounds__(RM >= 16 ? 1024 : 512, 1) k_cd_logit(CdLogitAr
             const int i = t + k * T_;
             if (k < R && i < n) a.eta[i] = e[k];
         }
+        ph[2] += clock64() - c0;
         // ---- outer convergence (QL6)
         double dm = 0.0, bm = 0.0;
         for (int w = t; w < nW; w += T_) { dm = fmax(dm, fabs(bw[w] - bo[w])); bm = fmax(bm, fabs(bw[w])); }
@@ -1360,6 +1374,7 @@ __global__ void __launch_bounds__(RM >= 16 ? 1024 : 512, 1) k_cd_logit(CdLogitAr
         a.st->cd_cycles = clock64() - clk0;
         a.st->b0 = b0;
         a.st->outer = outer;
+        for (int u = 0; u < 4; u++) a.st->cd_prof[u] = ph[u];
     }
 }
 
