@@ -255,10 +255,11 @@ class Design:
             lib().bl_free(h)
 
     def fit_path_binomial(self, y, lam, alpha=1.0, tol=1e-7, max_iter=10000, screen="ssr", stream=None,
-                          profile=False, max_kkt_rounds=0, raise_on_error=True):
-        """Penalised logistic path (NEXT-3, bl_fit_path_binomial); y in {0, 1}."""
+                          profile=False, max_kkt_rounds=0, raise_on_error=True, cd="auto"):
+        """Penalised logistic path (NEXT-3, bl_fit_path_binomial); y in {0, 1}.
+        cd: "auto" (covariance form while |W| < 2048) or "residual"."""
         lam = _f64(lam)
-        o = bl_opts(stream, int(profile), max_kkt_rounds, 0)
+        o = bl_opts(stream, int(profile), max_kkt_rounds, CD_MODE[cd])
         h = ctypes.c_void_p()
         rc = lib().bl_fit_path_binomial(self.h, _p(_f64(y)), _p(lam), lam.size, alpha, tol, max_iter,
                                         SCREEN.get(screen, screen), ctypes.byref(o), ctypes.byref(h))

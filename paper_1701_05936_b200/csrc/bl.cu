@@ -235,6 +235,10 @@ struct bl_prep {
     int64_t Wcap;
     double *betaW, *yt, *rfull, *rscan, *vtmp;
     double *yraw;             // y as given (the logistic path's 0/1 response)
+    double *LG = nullptr;     // logistic covariance CD: weighted Gram ((|W|+1)^2, ld ldLG)
+    int64_t ldLG = 0;
+    double *lgbuf = nullptr;  // logistic covariance CD: slot coefficients, weights, partial sums
+    size_t lgcap = 0;
     int8_t *limbs;
     double *limb_scale, *limb_sum;
     PrepScalars *ps;
@@ -492,6 +496,8 @@ void free_prep(bl_prep *pp) {
     if (pp->rbuf) cudaFree(pp->rbuf);
     if (pp->Xw) cudaFree(pp->Xw);
     if (pp->cw) cudaFree(pp->cw);
+    if (pp->LG) cudaFree(pp->LG);
+    if (pp->lgbuf) cudaFree(pp->lgbuf);
     if (pp->own) cudaStreamDestroy(pp->own);
     pp->magic = MAGIC_DEAD;
     delete pp;
@@ -1063,6 +1069,103 @@ void launch_cd_logit(bl_prep *pp, int nW, double lam, double alpha, double tol, 
     pp->launches++;
 }
 
+// covariance form (|W| + 1 <= kLogitGramMax): one IRLS iteration = k_logit_eta (eta, weights,
+// v = y - pi) -> k_gram_w (weighted Gram incl. the intercept) -> k_cd_logit_gram; the host reads
+// the status once per iteration.  The final k_logit_eta leaves r_scan = y - pi for the KKT scan.
+template <typename T, bool M>
+void solve_logit_gram_t(bl_prep *pp, int nW, double lam, double alpha, double tol, int max_iter) {
+    bl_design *d = pp->d;
+    cudaStream_t st = pp->stream;
+    const CdView v = cd_view(pp);
+    const int m = nW + 1;
+    const int64_t ld = d->ld;
+    const int nblk = (int)((ld + kLogitEtaThreads - 1) / kLogitEtaThreads);
+    if (m > pp->ldLG) {
+        int64_t nl = round_up(std::max<int64_t>(m, std::min<int64_t>(2 * pp->ldLG, kLogitGramMax)), 32);
+        if (pp->LG) CK(cudaFree(pp->LG));
+        pp->LG = nullptr;
+        cudaError_t e = cudaMalloc(&pp->LG, (size_t)8 * nl * nl);
+        if (e != cudaSuccess) { cudaGetLastError(); pp->ldLG = 0; raise(BL_ERR_OOM, "cudaMalloc for the weighted Gram: %s", cudaGetErrorString(e)); }
+        pp->ldLG = nl;
+    }
+    const size_t need = (size_t)8 * (kLogitGramMax + ld + 3 * (size_t)nblk);
+    if (need > pp->lgcap) {
+        if (pp->lgbuf) CK(cudaFree(pp->lgbuf));
+        pp->lgbuf = nullptr;
+        cudaError_t e = cudaMalloc(&pp->lgbuf, need);
+        if (e != cudaSuccess) { cudaGetLastError(); pp->lgcap = 0; raise(BL_ERR_OOM, "cudaMalloc for the logistic workspace: %s", cudaGetErrorString(e)); }
+        pp->lgcap = need;
+    }
+    double *bS = pp->lgbuf, *w = bS + kLogitGramMax, *part = w + ld;
+    const T *X = reinterpret_cast<const T *>(v.X);
+    const uint8_t *mask = M ? pp->mask : nullptr;
+    EvPair ev(pp, &pp->ev_cd);
+    k_logit_gather<<<(m + 255) / 256, 256, 0, st>>>(bS, v.beta, v.Wst, nW, pp->st);
+    CKL();
+    pp->launches++;
+    CdLogitGramArgs ga{};
+    ga.X = v.X; ga.ld = ld; ga.n = (int)d->n; ga.Wst = v.Wst; ga.nW = nW; ga.c = v.c; ga.s = v.s;
+    ga.G = pp->LG; ga.ldG = (int)pp->ldLG; ga.gz = v.z; ga.bS = bS;
+    ga.beta = v.beta; ga.lam_alpha = lam * alpha; ga.lam_l2 = lam * (1.0 - alpha); ga.inv_n = 1.0 / pp->nt;
+    ga.tol = tol; ga.floor_ = 1e-13 * (alpha * lam + 1.0); ga.max_iter = max_iter; ga.st = pp->st;
+    const size_t smem = (size_t)40 * m + (size_t)8 * (m + 1) + 16;   // gb, dv (16 B), bo (8 B), two sequences
+    const void *kcd = m <= kLGThreads ? (const void *)k_cd_logit_gram<T, 1>
+                    : m <= 2 * kLGThreads ? (const void *)k_cd_logit_gram<T, 2>
+                    : m <= 4 * kLGThreads ? (const void *)k_cd_logit_gram<T, 4>
+                                          : (const void *)k_cd_logit_gram<T, 8>;
+    const size_t lim = allow_dyn_smem(kcd);
+    if (smem > lim) raise(BL_ERR_OOM, "logistic covariance CD shared memory %zu > %zu", smem, lim);
+    const void *kgw = (const void *)k_gram_w<T, M>;
+    allow_dyn_smem(kgw);
+    for (int it = 0;; it++) {
+        k_logit_eta<T, M><<<nblk, kLogitEtaThreads, 0, st>>>(X, ld, (int)d->n, v.Wst, nW, v.c, v.s, bS, pp->yraw,
+                                                             mask, pp->rfull, w, pp->rscan, part, pp->st, it == 0);
+        CKL();
+        k_gram_w<T, M><<<dim3(m, (m + 31) / 32), 256, (size_t)8 * d->n, st>>>(X, ld, (int)d->n, v.Wst, nW,
+                                                                             (int)pp->ldLG, v.c, v.s, w,
+                                                                             1.0 / pp->nt, pp->LG, part, nblk,
+                                                                             pp->st);
+        CKL();
+        {                                      // g_W = x~_W' (y - pi) / n (identity (3) with K1 = sum(y - pi))
+            ScanArgs sa{};
+            sa.list = v.Wst;
+            sa.nlist = nullptr;
+            sa.nlist_host = nW;
+            sa.K1 = &pp->st->sumr;
+            sa.K2v = 1.0 / pp->nt;
+            sa.out = v.z;
+            launch_scan(pp, sa, pp->rscan, false, false, d->sharded ? pp->Xw : nullptr, v.c, v.s);
+        }
+        void *args[] = {&ga};
+        CK(cudaLaunchKernel(kcd, dim3(1), dim3(kLGThreads), args, smem, st));
+        pp->launches += 3;
+        CK(cudaMemcpyAsync(pp->hst, pp->st, sizeof(RoundStatus), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (pp->hst->cd_status || pp->hst->irls_done) break;
+    }
+    k_logit_eta<T, M><<<nblk, kLogitEtaThreads, 0, st>>>(X, ld, (int)d->n, v.Wst, nW, v.c, v.s, bS, pp->yraw, mask,
+                                                         pp->rfull, w, pp->rscan, part, pp->st, 0);
+    CKL();
+    k_logit_finish<<<1, 256, 0, st>>>(part, nblk, bS, nW, v.Wst, pp->ord_d, v.c, v.s, pp->betaW, pp->st);
+    CKL();
+    pp->launches += 2;
+}
+
+void solve_logit(bl_prep *pp, int nW, double lam, double alpha, double tol, int max_iter) {
+    bl_design *d = pp->d;
+    if (nW + 1 > kLogitGramMax || pp->cd_mode == 1) {       // residual form (or requested)
+        launch_cd_logit(pp, nW, lam, alpha, tol, max_iter);
+        return;
+    }
+    const bool M = pp->has_mask != 0;
+    if (d->dt == DT_F64) M ? solve_logit_gram_t<double, true>(pp, nW, lam, alpha, tol, max_iter)
+                           : solve_logit_gram_t<double, false>(pp, nW, lam, alpha, tol, max_iter);
+    else if (d->dt == DT_F32) M ? solve_logit_gram_t<float, true>(pp, nW, lam, alpha, tol, max_iter)
+                                : solve_logit_gram_t<float, false>(pp, nW, lam, alpha, tol, max_iter);
+    else M ? solve_logit_gram_t<int8_t, true>(pp, nW, lam, alpha, tol, max_iter)
+           : solve_logit_gram_t<int8_t, false>(pp, nW, lam, alpha, tol, max_iter);
+}
+
 __global__ void k_logit_init(double *eta, int ld, const PrepScalars *ps, RoundStatus *st) {
     const double yb = ps->ybar, b0 = log(yb / (1.0 - yb));     // the null model (QL2)
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ld; i += gridDim.x * blockDim.x) eta[i] = b0;
@@ -1353,7 +1456,7 @@ struct PathRun {
         return true;
     }
     void solve() {
-        if (family == 1) launch_cd_logit(pp, W.size(), lam, alpha, tol, max_iter);
+        if (family == 1) solve_logit(pp, W.size(), lam, alpha, tol, max_iter);
         else solve_cd(pp, W.size(), lam, alpha, tol, max_iter);
         if (screen != BL_SCREEN_NONE) CK(cudaMemsetAsync(&pp->st->nviol, 0, 2 * sizeof(int), pp->stream));
     }

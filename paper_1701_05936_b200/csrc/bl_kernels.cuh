@@ -46,7 +46,7 @@ struct RoundStatus {
     long long cd_cnt[4];               // Gram CD events: speculation retries, G_AA builds, catch-ups, full sweeps
     long long cd_dbg[8];               // Gram CD sub-phase cycles (micro-benchmarks only)
     double b0;                         // logistic path: intercept on the standardised scale (in/out)
-    int outer, pad2;                   // logistic path: IRLS iterations of the last solve
+    int outer, irls_done;              // logistic path: IRLS iterations of the last solve; converged flag
 };
 
 // ---------------------------------------------------------------- small helpers
@@ -1375,6 +1375,333 @@ __global__ void __launch_bounds__(RM >= 16 ? 1024 : 512, 1) k_cd_logit(CdLogitAr
         a.st->b0 = b0;
         a.st->outer = outer;
         for (int u = 0; u < 4; u++) a.st->cd_prof[u] = ph[u];
+    }
+}
+
+// ---------------- NEXT-3, covariance form: weighted Gram per IRLS iteration
+// For |W| + 1 <= kLogitGramMax the logistic solve runs one IRLS iteration as three
+// launches (host loop, one status read per iteration):
+//   k_logit_eta     eta = b0 + X~_W b (all rows), pi, w = max(pi(1-pi), 1e-5), v = y - pi
+//                   on used rows, per-block partial sums (fixed-order, deterministic);
+//   k_gram_w        Gw = X~_W' diag(w) X~_W / n over the slots plus the intercept slot
+//                   (a column of ones);
+//   k_cd_logit_gram the weighted CD of QL4 in covariance form: g = X~_W' rho / n, each
+//                   update g -= d Gw[:, j] (O(|W|)), one CTA, Gw rows prefetched D ahead.
+constexpr int kLogitGramMax = 2048;        // slots incl. the intercept
+constexpr int kLogitEtaThreads = 256;
+
+template <typename T, bool MASK>
+__global__ void __launch_bounds__(kLogitEtaThreads) k_logit_eta(const T *__restrict__ X, int64_t ld, int n,
+        const int *__restrict__ Wst, int nW, const double *__restrict__ c, const double *__restrict__ s,
+        const double *__restrict__ bS /* nW + 1: slots, then b0 */, const double *__restrict__ y,
+        const uint8_t *__restrict__ mask, double *__restrict__ eta, double *__restrict__ w,
+        double *__restrict__ v, double *__restrict__ part /* 3 per block: sum w, sum v, loss */,
+        RoundStatus *st, int reset) {
+    __shared__ double red[32];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    double wl = 0.0, vl = 0.0, ll = 0.0;
+    if (i < ld) {
+        double e = bS[nW];
+        if (i < n) {
+            for (int k = 0; k < nW; k++) {
+                const double b = bS[k];
+                if (b != 0.0) {
+                    const int j = Wst[k];
+                    e = fma(b / s[j], to_d(X[(int64_t)j * ld + i]) - c[j], e);
+                }
+            }
+        }
+        const bool use = i < n && (!MASK || mask[i]);
+        double wi = 0.0, vi = 0.0;
+        if (use) {
+            const double pi = sigmoid_d(e), yi = y[i];
+            wi = fmax(pi * (1.0 - pi), 1e-5);      // QL5
+            vi = yi - pi;
+            ll = (e > 0.0 ? e + log1p(exp(-e)) : log1p(exp(e))) - yi * e;
+        }
+        if (i < n) eta[i] = e;
+        w[i] = wi;
+        v[i] = vi;
+        wl = wi;
+        vl = vi;
+    }
+    wl = block_sum(wl, red);
+    vl = block_sum(vl, red);
+    ll = block_sum(ll, red);
+    if (threadIdx.x == 0) {
+        part[3 * blockIdx.x] = wl;
+        part[3 * blockIdx.x + 1] = vl;
+        part[3 * blockIdx.x + 2] = ll;
+        if (reset && blockIdx.x == 0) {
+            st->cd_passes = 0; st->cd_visits = 0; st->cd_updates = 0; st->cd_cycles = 0;
+            st->outer = 0; st->irls_done = 0; st->cd_status = 0;
+        }
+    }
+}
+
+// Gw[a][b] = sum_i w_i x~_ia x~_ib / n for slots a, b in [0, nW]; slot nW = the intercept
+// (x~ = 1 on every row).  Grid (nW + 1, ceil((nW + 1) / 32)); CTA (a, tile) stages
+// w x~_a in shared memory and its 8 warps form 4 dots each; tiles above the
+// diagonal are skipped and the mirror entry is written instead.
+template <typename T, bool MASK>
+__global__ void __launch_bounds__(256) k_gram_w(const T *__restrict__ X, int64_t ld, int n,
+                                                const int *__restrict__ Wst, int nW, int ldG,
+                                                const double *__restrict__ c, const double *__restrict__ s,
+                                                const double *__restrict__ w, double inv_n, double *__restrict__ G,
+                                                const double *__restrict__ part, int nblk, RoundStatus *st) {
+    extern __shared__ __align__(16) double vs[];
+    const int a = blockIdx.x;
+    if (a == 0 && blockIdx.y == 0 && threadIdx.x == 0) {   // sum (y - pi), fixed order (identity (3)'s K1)
+        double sv = 0.0;
+        for (int q = 0; q < nblk; q++) sv += part[3 * q + 1];
+        st->sumr = sv;
+    }
+    if ((int)blockIdx.y * 32 > a) return;
+    const bool ia = a == nW;
+    const int ja = ia ? 0 : Wst[a];
+    const double ca = ia ? 0.0 : c[ja], sa = ia ? 1.0 : 1.0 / s[ja];
+    const T *xa = X + (int64_t)ja * ld;
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        vs[i] = w[i] * (ia ? 1.0 : (to_d(xa[i]) - ca) * sa);      // w is 0 on unused rows
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int t0 = blockIdx.y * 32 + wid * 4;
+    if (t0 > a) return;
+    const int nt = min(4, a + 1 - t0);
+    const T *xt[4];
+    double ct[4], st_[4];
+    bool one[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        const int tb = t0 + min(q, nt - 1);
+        one[q] = tb == nW;
+        const int jt = one[q] ? 0 : Wst[tb];
+        xt[q] = X + (int64_t)jt * ld;
+        ct[q] = one[q] ? 0.0 : c[jt];
+        st_[q] = one[q] ? 1.0 : 1.0 / s[jt];
+    }
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int i = lane; i < n; i += 32) {
+        const double vi = vs[i];
+#pragma unroll
+        for (int q = 0; q < 4; q++) acc[q] = fma(vi, one[q] ? 1.0 : to_d(xt[q][i]) - ct[q], acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        const double dsum = warp_sum(acc[q]);
+        const int tt = t0 + q;
+        if (lane == 0 && q < nt) {
+            const double gv = dsum * st_[q] * inv_n;
+            G[(int64_t)a * ldG + tt] = gv;
+            G[(int64_t)tt * ldG + a] = gv;
+        }
+    }
+}
+
+struct CdLogitGramArgs {
+    const void *X;
+    int64_t ld;
+    int n;
+    const int *Wst;          // slot -> view column
+    int nW;                  // penalised slots; slot nW = intercept
+    const double *c, *s;
+    const double *G;         // (nW + 1)^2 weighted Gram, leading dimension ldG
+    int ldG;
+    const double *gz;        // x~_j' (y - pi) / n by view column (fused scan over W)
+    double *bS;              // nW + 1 in/out: slot coefficients, then b0
+    double *beta;            // by view column (out)
+    double lam_alpha, lam_l2, inv_n, tol, floor_;
+    int max_iter;
+    RoundStatus *st;
+};
+
+constexpr int kLGThreads = 256, kLGDepth = 4;
+
+// EP = g entries per thread (m <= EP * kLGThreads).  One __syncthreads per coefficient
+// update: every thread applies d G[k][j] to its own entries k != j, the barrier publishes
+// them, and only then are g[j] and b[j] (read by every thread at the visit) written; a
+// barrier closes each pass, so no index is read again before those writes are visible.
+template <typename T, int EP>
+__global__ void __launch_bounds__(kLGThreads, 1) k_cd_logit_gram(CdLogitGramArgs a) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ double red[32];
+    __shared__ int wcount[33];
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = kLGThreads / 32;
+    const int nW = a.nW, m = nW + 1;                  // coordinates incl. the intercept (index nW)
+    double2 *gb = reinterpret_cast<double2 *>(sm);    // (g_j, b_j): written only by j's owner thread
+    double2 *dv = gb + m;                             // (Gw_jj, 1 / (Gw_jj + lambda (1 - alpha)))
+    double *bo = reinterpret_cast<double *>(dv + m);  // b at the start of this IRLS iteration
+    int *seqA = reinterpret_cast<int *>(bo + m);      // active pass: intercept, then the nonzeros
+    int *seqF = seqA + m + 1;                         // full pass: intercept, then every slot
+    const long long clk0 = clock64();
+    const T *X = reinterpret_cast<const T *>(a.X);
+    (void)X;
+    // ---- g_k = x~_k' v / n from the fused scan over W (a.gz, by view column); the intercept's
+    // g = sum v / n from k_gram_w's fixed-order reduction (st->sumr)
+    for (int k = t; k < nW; k += kLGThreads) gb[k].x = a.gz[a.Wst[k]];
+    for (int k = t; k < m; k += kLGThreads) {
+        const double d = a.G[(int64_t)k * a.ldG + k];
+        dv[k] = make_double2(d, k == nW ? 1.0 / d : 1.0 / (d + a.lam_l2));
+        gb[k].y = a.bS[k];
+        bo[k] = a.bS[k];
+    }
+    for (int q = t; q <= nW; q += kLGThreads) seqF[q] = q == 0 ? nW : q - 1;
+    if (t == 0) seqA[0] = nW;
+    __syncthreads();
+    if (t == 0) gb[nW].x = a.st->sumr * a.inv_n;
+    __syncthreads();
+    // ---- weighted CD passes in covariance form
+    double gr[kLGDepth][EP];
+    int passes = 0, status = 0;
+    long long visits = 0, updates = 0;
+    auto row_load = [&](double (&r)[EP], int j) {
+        const double *Gj = a.G + (int64_t)j * a.ldG + t;
+#pragma unroll
+        for (int e = 0; e < EP; e++) r[e] = t + e * kLGThreads < m ? Gj[e * kLGThreads] : 0.0;
+    };
+    // one pass over seq[0..L) (seq[0] = the intercept)
+    auto pass = [&](const int *seq, int L, double &dmax, double &bmax, double &d0) {
+        dmax = 0.0;
+        bmax = 0.0;
+        d0 = 0.0;
+        visits += L - 1;
+#pragma unroll
+        for (int u = 0; u < kLGDepth; u++)
+            if (u < L) row_load(gr[u], seq[u]);
+        for (int q0 = 0; q0 < L; q0 += kLGDepth) {
+#pragma unroll
+            for (int u = 0; u < kLGDepth; u++) {
+                const int q = q0 + u;
+                if (q < L) {
+                    const int j = seq[q];
+                    const double2 gbj = gb[j], dvj = dv[j];
+                    const bool icpt = q == 0;
+                    const double u_ = fma(dvj.x, gbj.y, gbj.x);
+                    const double bn = (icpt ? u_ : soft_threshold(u_, a.lam_alpha)) * dvj.y;
+                    const double d = bn - gbj.y;
+                    if (d != 0.0) {                          // d is identical in every thread
+                        updates++;
+                        double gj = 0.0;
+#pragma unroll
+                        for (int e = 0; e < EP; e++) {
+                            const int k = t + e * kLGThreads;
+                            if (k < m) {
+                                const double nv = fma(-d, gr[u][e], gb[k].x);
+                                if (k != j) gb[k].x = nv;
+                                else gj = nv;
+                            }
+                        }
+                        __syncthreads();                     // every thread has read gb[j]; g[k != j] published
+                        if ((j & (kLGThreads - 1)) == t) gb[j] = make_double2(gj, bn);
+                    }
+                    if (icpt) d0 = fabs(d);
+                    else { dmax = fmax(dmax, fabs(d)); bmax = fmax(bmax, fabs(bn)); }
+                    if (q + kLGDepth < L) row_load(gr[u], seq[q + kLGDepth]);
+                }
+            }
+        }
+        __syncthreads();                                     // the pass's last (g_j, b_j) writes visible
+    };
+    auto build_active = [&]() -> int {
+        int total = 0;
+        for (int base = 0; base < nW; base += kLGThreads) {
+            const int k = base + t;
+            const bool nz = k < nW && gb[k].y != 0.0;
+            const unsigned msk = __ballot_sync(0xffffffffu, nz);
+            if (lane == 0) wcount[wid] = __popc(msk);
+            __syncthreads();
+            if (t == 0) {
+                int run = 0;
+                for (int u = 0; u < nw; u++) { const int c0 = wcount[u]; wcount[u] = run; run += c0; }
+                wcount[32] = run;
+            }
+            __syncthreads();
+            if (nz) seqA[1 + total + wcount[wid] + __popc(msk & ((1u << lane) - 1u))] = k;
+            total += wcount[32];
+            __syncthreads();
+        }
+        return total;
+    };
+    auto converged = [&](double dmax, double bmax, double d0, double b0) {
+        return (dmax <= a.tol * bmax || dmax <= a.floor_) && (d0 <= a.tol * fmax(1.0, fabs(b0)) || d0 <= a.floor_);
+    };
+    for (int kind = 0; kind < 2 && !status; kind++) {      // active cycling, then full passes
+        for (;;) {
+            double dmax, bmax, d0;
+            if (kind == 0) {
+                const int na = build_active();
+                if (na == 0) break;
+                pass(seqA, na + 1, dmax, bmax, d0);
+            } else {
+                pass(seqF, nW + 1, dmax, bmax, d0);
+            }
+            if (++passes > a.max_iter) { status = 3; break; }
+            if (converged(dmax, bmax, d0, gb[nW].y)) break;
+        }
+    }
+    __syncthreads();
+    // ---- outer (IRLS) convergence against the iteration's start point (QL6)
+    double dm = 0.0, bm = 0.0;
+    for (int k = t; k < nW; k += kLGThreads) { dm = fmax(dm, fabs(gb[k].y - bo[k])); bm = fmax(bm, fabs(gb[k].y)); }
+    dm = block_max(dm, red);
+    __syncthreads();
+    bm = block_max(bm, red);
+    const double b0 = gb[nW].y;
+    const bool done = converged(dm, bm, fabs(b0 - bo[nW]), b0);
+    for (int k = t; k < m; k += kLGThreads) {
+        a.bS[k] = gb[k].y;
+        if (k < nW) a.beta[a.Wst[k]] = gb[k].y;
+    }
+    if (t == 0) {
+        RoundStatus *st = a.st;
+        st->cd_passes += passes;
+        st->cd_visits += visits;
+        st->cd_updates += updates;
+        st->cd_cycles += clock64() - clk0;
+        st->outer += 1;
+        if (status) st->cd_status = status;
+        if (st->outer > a.max_iter) st->cd_status = 3;
+        st->irls_done = done ? 1 : 0;
+        st->b0 = b0;
+    }
+}
+
+__global__ void k_logit_gather(double *__restrict__ bS, const double *__restrict__ beta, const int *__restrict__ Wst,
+                               int nW, const RoundStatus *st) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k <= nW; k += gridDim.x * blockDim.x)
+        bS[k] = k < nW ? beta[Wst[k]] : st->b0;
+}
+
+// Final statistics of a logistic solve (a11): loss and sum(y - pi) from k_logit_eta's
+// partials (fixed order), l1 / l2 / nnz and the read-out (ord: sorted position -> slot).
+__global__ void k_logit_finish(const double *__restrict__ part, int nblk, const double *__restrict__ bS, int nW,
+                               const int *__restrict__ Wst, const int *__restrict__ ord, const double *__restrict__ c,
+                               const double *__restrict__ s, double *__restrict__ betaW_out, RoundStatus *st) {
+    __shared__ double red[32];
+    double l1 = 0.0, l2 = 0.0, nnz = 0.0;
+    for (int q = threadIdx.x; q < nW; q += blockDim.x) {     // read-out in ascending column order
+        const int k = ord[q];
+        const double bk = bS[k];
+        const int j = Wst[k];
+        betaW_out[q] = bk;
+        betaW_out[nW + q] = c[j];
+        betaW_out[2 * nW + q] = s[j];
+        l1 += fabs(bk);
+        l2 = fma(bk, bk, l2);
+        nnz += bk != 0.0 ? 1.0 : 0.0;
+    }
+    l1 = block_sum(l1, red);
+    l2 = block_sum(l2, red);
+    nnz = block_sum(nnz, red);
+    if (threadIdx.x == 0) {
+        double sv = 0.0, ll = 0.0;
+        for (int q = 0; q < nblk; q++) { sv += part[3 * q + 1]; ll += part[3 * q + 2]; }
+        st->rss = ll;
+        st->sumr = sv;
+        st->l1 = l1;
+        st->l2 = l2;
+        st->nnz = (int)nnz;
+        st->b0 = bS[nW];
     }
 }
 

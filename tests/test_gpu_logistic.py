@@ -52,30 +52,31 @@ def compare(inst, gp, op, alpha, lams):
         assert np.array_equal(ao, ag) or np.all(np.abs(bo[ao != ag]) < 1e-6), k
 
 
-@pytest.mark.parametrize("dtype,alpha,screen", [
-    (np.float64, 1.0, "ssr"), (np.float32, 1.0, "ssr"), (np.int8, 1.0, "ssr"),
-    (np.float32, 0.5, "ssr"), (np.float64, 0.5, "none"), (np.int8, 0.3, "hybrid")])
-def test_logistic_path_parity(dtype, alpha, screen):
+@pytest.mark.parametrize("dtype,alpha,screen,cd", [
+    (np.float64, 1.0, "ssr", "auto"), (np.float32, 1.0, "ssr", "auto"), (np.int8, 1.0, "ssr", "auto"),
+    (np.float32, 0.5, "ssr", "auto"), (np.float64, 0.5, "none", "auto"), (np.int8, 0.3, "hybrid", "auto"),
+    (np.float64, 1.0, "ssr", "residual"), (np.int8, 0.5, "ssr", "residual"), (np.float32, 1.0, "none", "residual")])
+def test_logistic_path_parity(dtype, alpha, screen, cd):
     kind = "geno" if dtype == np.int8 else "corr"
     inst = synth.logistic_instance(157, 613, dtype=dtype, seed=7, kind=kind, n_true=10, scale=1.5, const_cols=3)
     d = bl.Design(inst.host_X(), inst.n)
     lm = d.lambda_max(inst.y, alpha)
     lams = synth.lambda_grid(lm, 30, 0.15)
     op = oracle.fit_path_binomial(inst, inst.y, lams, alpha=alpha, tol=1e-12)
-    gp = d.fit_path_binomial(inst.y, lams, alpha=alpha, tol=1e-10, screen=screen)
+    gp = d.fit_path_binomial(inst.y, lams, alpha=alpha, tol=1e-10, screen=screen, cd=cd)
     compare(inst, gp, op, alpha, lams)
     assert np.all(gp.outer[1:] >= 1)
 
 
-@pytest.mark.parametrize("n", [1500, 5000, 9000])
-def test_logistic_row_layouts(n):
+@pytest.mark.parametrize("n,cd", [(1500, "residual"), (5000, "residual"), (9000, "residual"), (9000, "auto")])
+def test_logistic_row_layouts(n, cd):
     """n spans the 4 / 8 / 16 rows-per-thread variants of the CD kernel with ragged tails."""
     inst = synth.logistic_instance(n, 120, dtype=np.float32, seed=n, n_true=8, scale=1.0)
     d = bl.Design(inst.host_X(), inst.n)
     lm = d.lambda_max(inst.y)
     lams = synth.lambda_grid(lm, 12, 0.1)
     op = oracle.fit_path_binomial(inst, inst.y, lams, tol=1e-12)
-    gp = d.fit_path_binomial(inst.y, lams, tol=1e-10)
+    gp = d.fit_path_binomial(inst.y, lams, tol=1e-10, cd=cd)
     compare(inst, gp, op, 1.0, lams)
 
 
