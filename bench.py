@@ -174,7 +174,30 @@ def run_ours(args, rank, world, local_rank):
         inst.X = X
         torch.cuda.empty_cache()
     dist_of = (lambda: bl.make_dist(rank, world, (j0, j1), p_global, device=local_rank)) if world > 1 else (lambda: None)
-    d = bl.Design(X, inst.n, dist=dist_of())
+    host_res = args.resident == "host"    # NEXT-4: X stays in pinned host memory, streamed over PCIe
+    link_gbs = None
+    if host_res:
+        Xpin = torch.empty(X.shape, dtype=X.dtype, pin_memory=True)
+        Xpin.copy_(X)
+        # the host link's measured copy bandwidth (pinned -> device), the roof of a streamed scan
+        probe = torch.empty(min(X.numel(), (1 << 31) // X.element_size()), dtype=X.dtype, device=X.device)
+        src = Xpin.view(-1)[:probe.numel()]
+        probe.copy_(src, non_blocking=True)
+        torch.cuda.synchronize()
+        e0_, e1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0_.record()
+        for _ in range(3):
+            probe.copy_(src, non_blocking=True)
+        e1_.record()
+        torch.cuda.synchronize()
+        link_gbs = 3 * probe.numel() * probe.element_size() / (e0_.elapsed_time(e1_) / 1e3) / 1e9
+        del probe, X
+        inst.X = Xpin
+        torch.cuda.empty_cache()
+        X = Xpin
+        d = bl.Design(Xpin.numpy(), inst.n, dist=dist_of(), host_resident=True)
+    else:
+        d = bl.Design(X, inst.n, dist=dist_of())
     lm = d.lambda_max(inst.y, inst.alpha)
     lams = synth.lambda_grid(lm, inst.nlam, inst.ratio)
     stream = torch.cuda.current_stream()
@@ -230,13 +253,14 @@ def run_ours(args, rank, world, local_rank):
     x_bytes = X.numel() * X.element_size()
     e2e, h2d, d2h = [], 0, 0
     if x_bytes <= 40e9:
-        Xh_t = torch.empty(X.shape, dtype=X.dtype, pin_memory=True)
-        Xh_t.copy_(X)
+        Xh_t = X if host_res else torch.empty(X.shape, dtype=X.dtype, pin_memory=True)
+        if not host_res:
+            Xh_t.copy_(X)
         Xh = Xh_t.numpy()
         for _ in range(max(1, min(args.steps, 3))):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            dh = bl.Design(Xh, inst.n, dist=dist_of())
+            dh = bl.Design(Xh, inst.n, dist=dist_of(), host_resident=host_res)
             lm_h = dh.lambda_max(inst.y, inst.alpha)
             lams_h = synth.lambda_grid(lm_h, inst.nlam, inst.ratio)
             if is_logit:
@@ -256,6 +280,11 @@ def run_ours(args, rank, world, local_rank):
     pk, pk_src = peaks()
     achieved = scan_bytes / (scan_ms / 1e3) / 1e9 if scan_ms > 0 else None
     roof = None
+    if host_res:
+        roof = {"kernel": "k_scan_fp/k_scan_i8 over host-resident X (zero-copy over PCIe, NEXT-4)", "bound": "host link",
+                "achieved": achieved, "peak": link_gbs,
+                "peak_source": "measured pinned host -> device copy bandwidth in this run", "unit": "GB/s",
+                "frac": achieved / link_gbs if achieved and link_gbs else None, "traffic": None}
     if is_cv:
         # the fold-batched scan (one pass over X for all 11 fits) is fp64-FMA bound: 11 FMAs per element
         fits = 11
@@ -289,7 +318,7 @@ def run_ours(args, rank, world, local_rank):
                    "model": "logistic" if is_logit else "gaussian", "cd": args.cd, "X_bytes": int(x_bytes),
                    "cv_folds": 10 if is_cv else None,
                    "l2_policy": "X larger than L2 (126 MB); no flush" if X.numel() * X.element_size() > 126e6
-                   else "X fits L2 (reported as such)", "parallelism": f"column-sharded x{world}" if world > 1 else "1 GPU",
+                   else "X fits L2 (reported as such)", "resident": args.resident, "parallelism": f"column-sharded x{world}" if world > 1 else "1 GPU",
                    "p_global": p_global},
         "roofline": {**(roof or {"kernel": "k_scan_fp/k_scan_i8 (fused KKT + strong-rule scan)", "bound": "hbm",
                                  "achieved": achieved, "peak": pk["hbm_gbs"], "peak_source": pk_src, "unit": "GB/s",
@@ -330,6 +359,8 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "logit"],
                     help="BASELINE cfg1-cfg5, or 'logit' (NEXT-3 logistic path, n=1000, p=100,000 fp32)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--resident", default="device", choices=["device", "host"],
+                    help="where X lives: HBM (default) or pinned host memory read over PCIe (NEXT-4, out-of-core)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=15.0)
     ap.add_argument("--cd", default="auto", choices=["auto", "residual", "gram"],

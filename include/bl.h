@@ -120,6 +120,13 @@ typedef struct {
  * x_is_device_ptr = 1: X is a device pointer on the current device, BORROWED
  *   (caller keeps it alive until bl_free(design)); requires 16-byte aligned
  *   base and ld * itemsize % 16 == 0.
+ * x_is_device_ptr = 2: OUT-OF-CORE (the paper's memory-mapped
+ *   design): X is host memory, BORROWED and read in place -- the
+ *   library page-locks and maps it (cudaHostRegister, undone by bl_free; a range
+ *   the caller already pinned is only mapped), every full pass over X streams it
+ *   over the host link, and working-set columns are copied once into a device
+ *   store.  Same alignment rules as 1; padding rows are never read into results.
+ *   Results are bitwise identical to a device-resident design.
  * Errors: BL_ERR_ARG for n < 2, n > 16384 (r must fit one SM's shared
  * memory), p_local < 1, ld < n, bad dtype/alignment. */
 bl_status bl_load_design(const void *X, bl_dtype dt, int64_t n, int64_t p_local, int64_t ld,

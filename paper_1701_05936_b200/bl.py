@@ -119,15 +119,19 @@ def _f64(a):
 
 # ------------------------------------------------------------------ C-named calls
 
-def bl_load_design(X, n, dist=None):
-    """X: (p, ld) column-major buffer -- numpy (host, copied) or a CUDA torch
+def bl_load_design(X, n, dist=None, host_resident=False):
+    """X: (p, ld) column-major buffer -- numpy (host: copied to the device, or with
+    host_resident=True borrowed and streamed over PCIe, NEXT-4) or a CUDA torch
     tensor (device, borrowed: keep it alive).  Returns a raw handle."""
     h = ctypes.c_void_p()
     if isinstance(X, np.ndarray):
+        if host_resident and not X.flags.c_contiguous:
+            raise ValueError("host-resident X must be C-contiguous (p, ld)")
         X = np.ascontiguousarray(X)
         dt = _DT[X.dtype]
         p, ld = X.shape
-        rc = lib().bl_load_design(_p(X), dt, n, p, ld, 0, ctypes.byref(dist) if dist else None, ctypes.byref(h))
+        rc = lib().bl_load_design(_p(X), dt, n, p, ld, 2 if host_resident else 0,
+                                  ctypes.byref(dist) if dist else None, ctypes.byref(h))
     else:  # torch tensor on the device
         import torch
         dt = {torch.float64: BL_F64, torch.float32: BL_F32, torch.int8: BL_I8}[X.dtype]
@@ -230,11 +234,11 @@ class Prep:
 class Design:
     """Owner of a bl_design.  X is a (p, ld) column-major buffer (see synth)."""
 
-    def __init__(self, X, n, dist=None):
-        self._keep = X  # borrowed device buffers must outlive the design
+    def __init__(self, X, n, dist=None, host_resident=False):
+        self._keep = X  # borrowed device / host-resident buffers must outlive the design
         self.n = int(n)
         self.p = int(X.shape[0])
-        self.h = bl_load_design(X, self.n, dist)
+        self.h = bl_load_design(X, self.n, dist, host_resident)
 
     def lambda_max(self, y, alpha=1.0):
         out = ctypes.c_double()

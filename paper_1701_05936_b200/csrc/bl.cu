@@ -184,6 +184,9 @@ struct bl_design {
     int rank, world;
     Comm *comm;                      // world > 1 only
     bool sharded;                    // columns split over the ranks (p_global > p_local)
+    bool hostres = false;            // NEXT-4: X stays in (mapped, pinned) host memory, read over PCIe
+    bool wstore = false;             // CD reads its columns from the working-set store (sharded || hostres)
+    void *host_reg = nullptr;        // host range this design registered (unregistered by bl_free)
     std::vector<int64_t> shard_off;  // world + 1 global column offsets of the shards (rank order)
     std::mutex comm_mu;
 };
@@ -626,7 +629,7 @@ struct CdView {
     const int *Wsorted;      // W in ascending global order -> columns of the view
 };
 CdView cd_view(bl_prep *pp) {
-    if (!pp->d->sharded) return CdView{pp->d->X, pp->c, pp->s, pp->beta, pp->z, pp->Wst_d, pp->W};
+    if (!pp->d->wstore) return CdView{pp->d->X, pp->c, pp->s, pp->beta, pp->z, pp->Wst_d, pp->W};
     return CdView{pp->Xw, pp->cw, pp->sw, pp->bw, pp->zw, pp->widx, pp->ord_d};
 }
 
@@ -896,9 +899,10 @@ void upload_W(bl_prep *pp, const WorkingSet &ws, const std::vector<int> &added) 
         CKL();
         pp->launches++;
     }
-    if (d->sharded && !added.empty()) {
+    if (d->wstore && !added.empty()) {
         // C4: each new column is broadcast by its owner into every rank's store (slots
-        // nW - |added| ..; a shard's columns are contiguous in that order)
+        // nW - |added| ..; a shard's columns are contiguous in that order).  A host-resident
+        // design (NEXT-4) packs its new columns over PCIe into the device store the same way.
         const int64_t slot0 = (int64_t)nW - (int64_t)added.size();
         ensure_Ws(pp, (int64_t)nW, slot0);
         const size_t isz = itemsize(d->dt), colb = (size_t)d->ld * isz;
@@ -915,6 +919,7 @@ void upload_W(bl_prep *pp, const WorkingSet &ws, const std::vector<int> &added) 
                 CKL();
                 pp->launches++;
             }
+            if (!d->sharded) continue;
             d->comm->bcast((char *)pp->Xw + (size_t)(slot0 + q0) * colb, colb * k, r, st);
             d->comm->bcast(pp->cw + slot0 + q0, 8 * (size_t)k, r, st);
             d->comm->bcast(pp->sw + slot0 + q0, 8 * (size_t)k, r, st);
@@ -1134,7 +1139,7 @@ void solve_logit_gram_t(bl_prep *pp, int nW, double lam, double alpha, double to
             sa.K1 = &pp->st->sumr;
             sa.K2v = 1.0 / pp->nt;
             sa.out = v.z;
-            launch_scan(pp, sa, pp->rscan, false, false, d->sharded ? pp->Xw : nullptr, v.c, v.s);
+            launch_scan(pp, sa, pp->rscan, false, false, d->wstore ? pp->Xw : nullptr, v.c, v.s);
         }
         void *args[] = {&ga};
         CK(cudaLaunchKernel(kcd, dim3(1), dim3(kLGThreads), args, smem, st));
@@ -1297,7 +1302,7 @@ void solve_cd(bl_prep *pp, int nW, double lam, double alpha, double tol, int max
         sa.K1 = &pp->st->sumr;
         sa.K2v = 1.0 / pp->nt;
         sa.out = v.z;
-        launch_scan(pp, sa, pp->rscan, false, false, d->sharded ? pp->Xw : nullptr, v.c, v.s);
+        launch_scan(pp, sa, pp->rscan, false, false, d->wstore ? pp->Xw : nullptr, v.c, v.s);
     }
     CdGramArgs ga{};
     ga.Wst = v.Wst;
@@ -1947,7 +1952,42 @@ bl_status bl_load_design(const void *X, bl_dtype dt, int64_t n, int64_t p_local,
         }
         CK(cudaDeviceGetAttribute(&d->nsm, cudaDevAttrMultiProcessorCount, d->device));
         int isz = itemsize(dt);
-        if (x_is_device_ptr) {
+        if (x_is_device_ptr == 2) {
+            // NEXT-4: out-of-core.  X stays in host memory (borrowed), page-locked and mapped
+            // into the device address space; every full pass over X (stats, scans) streams it
+            // over PCIe, the working-set columns are copied once into a device store.
+            if (((uintptr_t)X % 16) != 0 || (ld * isz) % 16 != 0) {
+                delete d;
+                raise(BL_ERR_ARG, "host-resident X needs a 16-byte aligned base and ld*itemsize %% 16 == 0");
+            }
+            const size_t bytes = (size_t)ld * p_local * isz;
+            cudaPointerAttributes pa{};
+            const bool pinned = cudaPointerGetAttributes(&pa, X) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+            cudaGetLastError();
+            cudaError_t e = pinned ? cudaSuccess
+                                   : cudaHostRegister(const_cast<void *>(X), bytes, cudaHostRegisterMapped | cudaHostRegisterReadOnly);
+            if (pinned || e == cudaErrorHostMemoryAlreadyRegistered) {
+                cudaGetLastError();              // the caller pinned it: map without taking ownership
+            } else if (e != cudaSuccess) {
+                cudaGetLastError();
+                delete d;
+                raise(BL_ERR_OOM, "cudaHostRegister(%zu bytes): %s", bytes, cudaGetErrorString(e));
+            } else {
+                d->host_reg = const_cast<void *>(X);
+            }
+            void *dp = nullptr;
+            e = cudaHostGetDevicePointer(&dp, const_cast<void *>(X), 0);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                if (d->host_reg) cudaHostUnregister(d->host_reg);
+                delete d;
+                raise(BL_ERR_CUDA, "cudaHostGetDevicePointer: %s", cudaGetErrorString(e));
+            }
+            d->X = dp;
+            d->owned = false;
+            d->ld = ld;
+            d->hostres = true;
+        } else if (x_is_device_ptr == 1) {
             if (((uintptr_t)X % 16) != 0 || (ld * isz) % 16 != 0) {
                 delete d;
                 raise(BL_ERR_ARG, "device X needs a 16-byte aligned base and ld*itemsize %% 16 == 0");
@@ -1965,7 +2005,9 @@ bl_status bl_load_design(const void *X, bl_dtype dt, int64_t n, int64_t p_local,
             CK(cudaMemset(d->X, 0, bytes));
             CK(cudaMemcpy2D(d->X, ldp * isz, X, ld * isz, n * isz, p_local, cudaMemcpyHostToDevice));
         }
+        if (x_is_device_ptr < 0 || x_is_device_ptr > 2) { delete d; raise(BL_ERR_ARG, "x_is_device_ptr must be 0, 1 or 2"); }
         d->sharded = false;
+        d->wstore = d->hostres;
         d->shard_off.assign(2, 0);
         d->shard_off[1] = p_local;
         if (d->world > 1) {
@@ -2013,6 +2055,7 @@ bl_status bl_load_design(const void *X, bl_dtype dt, int64_t n, int64_t p_local,
                     d->shard_off[r + 1] = d->shard_off[r] + all[2 * r + 1];
                 }
                 d->sharded = d->world > 1 && d->p_global != p_local;
+                d->wstore = d->sharded || d->hostres;
                 if (d->sharded && d->shard_off[d->world] != d->p_global) raise(BL_ERR_ARG, "shards cover %lld columns, p_global = %lld", (long long)d->shard_off[d->world], (long long)d->p_global);
                 if (!d->sharded) {
                     for (int r = 0; r < d->world; r++)
@@ -2023,6 +2066,7 @@ bl_status bl_load_design(const void *X, bl_dtype dt, int64_t n, int64_t p_local,
             } catch (...) {
                 delete d->comm;
                 if (d->owned) cudaFree(d->X);
+                if (d->host_reg) cudaHostUnregister(d->host_reg);
                 delete d;
                 throw;
             }
@@ -2391,6 +2435,7 @@ void bl_free(void *handle) {
         d->pool.clear();
         delete d->comm;
         if (d->owned && d->X) cudaFree(d->X);
+        if (d->host_reg) cudaHostUnregister(d->host_reg);
         d->magic = MAGIC_DEAD;
         delete d;
     } else if (magic == MAGIC_PATH) {

@@ -1,0 +1,9 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_scan_fp -s 40 -c 1 -o gpurun_out/prof_scan_cfg2 python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_scan2.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_scan_i8 -s 40 -c 1 -o gpurun_out/prof_scan_cfg4 python bench.py --config cfg4 --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_scan4.log 2>&1
+
+timeout 900 python -m pytest tests/test_gpu_outofcore.py -q --timeout 600 -rf > gpurun_out/pytest_ooc.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_ooc.log
+timeout 900 python bench.py --config cfg3 --resident host --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/bench_cfg3_host.log 2>&1
+timeout 900 python bench.py --config cfg4 --resident host --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/bench_cfg4_host.log 2>&1
+echo done
