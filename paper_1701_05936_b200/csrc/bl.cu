@@ -242,6 +242,11 @@ struct bl_prep {
     int64_t ldLG = 0;
     double *lgbuf = nullptr;  // logistic covariance CD: slot coefficients, weights, partial sums
     size_t lgcap = 0;
+    // NEXT-4 host-resident designs: double-buffered column chunks for the streamed scans
+    char *sbuf[2] = {nullptr, nullptr};
+    int64_t scols = 0;        // columns per chunk
+    cudaStream_t cstream = nullptr;
+    cudaEvent_t copied[2] = {nullptr, nullptr}, used[2] = {nullptr, nullptr};
     int8_t *limbs;
     double *limb_scale, *limb_sum;
     PrepScalars *ps;
@@ -412,6 +417,48 @@ size_t allow_dyn_smem(const void *kern) {
 // (fp32/fp64 designs) -- for int8 designs v is quantised to limbs first.
 // `cols`: another column source with the design's layout (the sharded working-set
 // store) and its c, s; nullptr => the design.
+// NEXT-4: a dense scan of a host-resident design streams X through two device chunk
+// buffers: the copy engine fills chunk i+1 (cudaMemcpyAsync on its own stream) while
+// the scan kernel reads chunk i from HBM; events order buffer reuse.  The kernel sees
+// a "virtual base" X - j0 * ld, so column indices, outputs and lists stay global.
+constexpr size_t kStreamChunkBytes = (size_t)256 << 20;
+void ensure_stream_bufs(bl_prep *pp) {
+    if (pp->sbuf[0]) return;
+    bl_design *d = pp->d;
+    const size_t colb = (size_t)d->ld * itemsize(d->dt);
+    pp->scols = std::max<int64_t>(1, std::min<int64_t>(d->p, (int64_t)(kStreamChunkBytes / colb)));
+    for (int u = 0; u < 2; u++) {
+        cudaError_t e = cudaMalloc(&pp->sbuf[u], colb * pp->scols);
+        if (e != cudaSuccess) { cudaGetLastError(); raise(BL_ERR_OOM, "cudaMalloc for the streamed-scan buffers: %s", cudaGetErrorString(e)); }
+        CK(cudaEventCreateWithFlags(&pp->copied[u], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&pp->used[u], cudaEventDisableTiming));
+    }
+    CK(cudaStreamCreateWithFlags(&pp->cstream, cudaStreamNonBlocking));
+}
+
+template <typename F>
+void stream_chunks(bl_prep *pp, ScanArgs &a, F launch) {
+    bl_design *d = pp->d;
+    ensure_stream_bufs(pp);
+    const size_t colb = (size_t)d->ld * itemsize(d->dt);
+    const char *Xh = (const char *)d->X;
+    CK(cudaEventRecord(pp->used[0], pp->stream));       // the buffers are free once prior work on the fit stream is
+    CK(cudaEventRecord(pp->used[1], pp->stream));
+    int u = 0;
+    for (int64_t c0 = 0; c0 < d->p; c0 += pp->scols, u ^= 1) {
+        const int64_t k = std::min<int64_t>(pp->scols, d->p - c0);
+        CK(cudaStreamWaitEvent(pp->cstream, pp->used[u], 0));
+        CK(cudaMemcpyAsync(pp->sbuf[u], Xh + (size_t)c0 * colb, (size_t)k * colb, cudaMemcpyDefault, pp->cstream));
+        CK(cudaEventRecord(pp->copied[u], pp->cstream));
+        CK(cudaStreamWaitEvent(pp->stream, pp->copied[u], 0));
+        a.X = pp->sbuf[u] - (ptrdiff_t)((size_t)c0 * colb);     // virtual base: column j at X + j * ld
+        a.j0 = c0;
+        a.p = c0 + k;
+        launch();
+        CK(cudaEventRecord(pp->used[u], pp->stream));
+    }
+}
+
 void launch_scan(bl_prep *pp, ScanArgs a, const double *v_dev, bool timed, bool events = true,
                  const void *cols = nullptr, const double *cc = nullptr, const double *cs = nullptr) {
     bl_design *d = pp->d;
@@ -421,6 +468,23 @@ void launch_scan(bl_prep *pp, ScanArgs a, const double *v_dev, bool timed, bool 
     a.p = d->p;
     a.c = cols ? cc : pp->c;
     a.s = cols ? cs : pp->s;
+    // host-resident design, scan over the design: stream it densely when the scope covers
+    // at least half of the columns (columns outside the scope are gated off by their flags);
+    // a short scope list is read in place (zero-copy)
+    bool streamed = false;
+    if (d->hostres && !cols) {
+        int64_t m = a.list ? (a.nlist ? -1 : (int64_t)a.nlist_host) : d->p;
+        if (m < 0) {
+            int h = 0;
+            CK(cudaMemcpyAsync(&h, a.nlist, sizeof h, cudaMemcpyDeviceToHost, pp->stream));
+            CK(cudaStreamSynchronize(pp->stream));
+            m = h;
+        }
+        if (2 * m >= d->p && (!a.list || a.flags)) {
+            streamed = true;
+            a.list = nullptr;
+        }
+    }
     if (d->dt == DT_I8) {
         k_limbs<<<1, 1024, 0, pp->stream>>>(v_dev, (int)d->n, pp->limb_ld, pp->limbs, pp->limb_scale,
                                             pp->limb_sum);
@@ -434,8 +498,15 @@ void launch_scan(bl_prep *pp, ScanArgs a, const double *v_dev, bool timed, bool 
         allow_dyn_smem((const void *)k_scan_i8);
         int grid = grid_for((const void *)k_scan_i8, kScanThreads, smem, d->nsm);
         EvPairOpt ev(pp, events ? (timed ? &pp->ev_scan : &pp->ev_prep) : nullptr);
-        k_scan_i8<<<grid, kScanThreads, smem, pp->stream>>>(a);
-        CKL();
+        if (streamed) {
+            stream_chunks(pp, a, [&] {
+                k_scan_i8<<<grid, kScanThreads, smem, pp->stream>>>(a);
+                CKL();
+            });
+        } else {
+            k_scan_i8<<<grid, kScanThreads, smem, pp->stream>>>(a);
+            CKL();
+        }
     } else {
         a.v = v_dev;
         int V = 16 / itemsize(d->dt);
@@ -452,7 +523,11 @@ void launch_scan(bl_prep *pp, ScanArgs a, const double *v_dev, bool timed, bool 
         int grid = grid_for(kern, kScanThreads, smem, d->nsm);
         EvPairOpt ev(pp, events ? (timed ? &pp->ev_scan : &pp->ev_prep) : nullptr);
         void *args[] = {&a};
-        CK(cudaLaunchKernel(kern, dim3(grid), dim3(kScanThreads), args, smem, pp->stream));
+        if (streamed) {
+            stream_chunks(pp, a, [&] { CK(cudaLaunchKernel(kern, dim3(grid), dim3(kScanThreads), args, smem, pp->stream)); });
+        } else {
+            CK(cudaLaunchKernel(kern, dim3(grid), dim3(kScanThreads), args, smem, pp->stream));
+        }
     }
     pp->launches++;
 }
@@ -501,6 +576,12 @@ void free_prep(bl_prep *pp) {
     if (pp->cw) cudaFree(pp->cw);
     if (pp->LG) cudaFree(pp->LG);
     if (pp->lgbuf) cudaFree(pp->lgbuf);
+    for (int u = 0; u < 2; u++) {
+        if (pp->sbuf[u]) cudaFree(pp->sbuf[u]);
+        if (pp->copied[u]) cudaEventDestroy(pp->copied[u]);
+        if (pp->used[u]) cudaEventDestroy(pp->used[u]);
+    }
+    if (pp->cstream) cudaStreamDestroy(pp->cstream);
     if (pp->own) cudaStreamDestroy(pp->own);
     pp->magic = MAGIC_DEAD;
     delete pp;

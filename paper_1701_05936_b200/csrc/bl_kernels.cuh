@@ -227,7 +227,8 @@ struct ScanArgs {
     int64_t ld;
     int n;
     int64_t p;
-    const int *list;          // nullptr => dense 0..p-1
+    const int *list;          // nullptr => dense j0..p-1
+    int64_t j0;               // first column of a dense range (streamed chunks of a host-resident design)
     const int *nlist;         // device count of `list` (nullptr => nlist_host)
     int nlist_host;
     const double *v;          // fp64 vector, >= ld entries, zero beyond n (fp32/fp64 path)
@@ -270,10 +271,11 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_fp(ScanArgs a) {
     __syncthreads();
     const double K1 = *a.K1;
     const double K2 = a.K2 ? *a.K2 : a.K2v;
-    const int64_t m = a.list ? (a.nlist ? (int64_t)*a.nlist : (int64_t)a.nlist_host) : a.p;
+    const int64_t m = a.list ? (a.nlist ? (int64_t)*a.nlist : (int64_t)a.nlist_host) : a.p - a.j0;
     // a scope list holding every column (BEDPP kept all, lambda < ~0.5 lambda_max) is read
     // as the dense range: same columns, no index indirection, sequential DRAM pages
     const int *__restrict__ list = (a.list && m == a.p) ? nullptr : a.list;
+    const int64_t j0 = list ? 0 : a.j0;
     const int lane = threadIdx.x & 31;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -284,7 +286,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_fp(ScanArgs a) {
 #pragma unroll
         for (int q = 0; q < C; q++) {
             int64_t idx = g + q < m ? g + q : m - 1;
-            col[q] = list ? (int64_t)list[idx] : idx;
+            col[q] = list ? (int64_t)list[idx] : j0 + idx;
             ptr[q] = X + col[q] * a.ld;
         }
         double acc[C];
@@ -532,10 +534,11 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_i8(ScanArgs a) {
     const double K1 = *a.K1;
     const double K2 = a.K2 ? *a.K2 : a.K2v;
     const double scale = *a.limb_scale;
-    const int64_t m = a.list ? (a.nlist ? (int64_t)*a.nlist : (int64_t)a.nlist_host) : a.p;
+    const int64_t m = a.list ? (a.nlist ? (int64_t)*a.nlist : (int64_t)a.nlist_host) : a.p - a.j0;
     // a scope list holding every column (BEDPP kept all, lambda < ~0.5 lambda_max) is read
     // as the dense range: same columns, no index indirection, sequential DRAM pages
     const int *__restrict__ list = (a.list && m == a.p) ? nullptr : a.list;
+    const int64_t jd = list ? 0 : a.j0;
     const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -546,8 +549,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_i8(ScanArgs a) {
     for (int64_t g0 = gw * 16; g0 < m; g0 += nwarp * 16) {
         int64_t ia = g0 + g < m ? g0 + g : m - 1;
         int64_t ib = g0 + g + 8 < m ? g0 + g + 8 : m - 1;
-        int64_t ja = list ? (int64_t)list[ia] : ia;
-        int64_t jb = list ? (int64_t)list[ib] : ib;
+        int64_t ja = list ? (int64_t)list[ia] : jd + ia;
+        int64_t jb = list ? (int64_t)list[ib] : jd + ib;
         const int8_t *pa = X + ja * a.ld, *pb = X + jb * a.ld;
         int acc[4] = {0, 0, 0, 0};
         const int8_t *lg = ls + g * LL + 16 * t;
