@@ -291,7 +291,7 @@ def run_ours(args, rank, world, local_rank):
         flops = 2.0 * fits * scan_bytes / X.element_size()
         tfl = flops / (scan_ms / 1e3) / 1e12 if scan_ms > 0 else None
         fpk = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))["fp64_tflops"]
-        roof = {"kernel": "k_scan_batch (fold-batched fused scan, 11 residuals per pass over X)", "bound": "alu",
+        roof = {"kernel": "k_scan_batch_mma (fold-batched fused scan on the fp64 tensor cores, 11 residuals per pass over X)", "bound": "alu",
                 "achieved": tfl, "peak": fpk, "peak_source": "measured fp64 FMA throughput (scripts/fp64_peak.cu, profiles/fp64_peak.json)",
                 "unit": "TFLOP/s", "frac": tfl / fpk if tfl else None, "traffic": None,
                 "x_read_GBps": achieved, "x_read_frac_of_hbm": achieved / pk["hbm_gbs"] if achieved else None}

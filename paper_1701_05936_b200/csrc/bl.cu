@@ -1769,6 +1769,18 @@ const void *batch_kernel_n(bool f64, int nb) {
     return f64 ? (const void *)k_scan_batch<double, NF> : (const void *)k_scan_batch<float, NF>;
 }
 const void *batch_kernel(bool f64, int nb) { return batch_kernel_n<kBatchMax>(f64, nb); }
+template <int NF>
+const void *batch_mma_kernel_n(bool f64, int nb) {
+    if constexpr (NF > 1) {
+        if (nb < NF) return batch_mma_kernel_n<NF - 1>(f64, nb);
+    }
+    return f64 ? (const void *)k_scan_batch_mma<double, NF> : (const void *)k_scan_batch_mma<float, NF>;
+}
+// fold-batched scan flavour: DMMA (default) or the FMA kernel (BL_CV_MMA=0)
+bool batch_use_mma() {
+    static const bool v = [] { const char *e = std::getenv("BL_CV_MMA"); return !(e && e[0] == '0'); }();
+    return v;
+}
 
 void launch_scan_batch(bl_design *d, const std::vector<LockFit *> &fits, cudaStream_t sst, FitScan *dfs,
                        FitScan *hfs, bl_prep *timer) {
@@ -1802,16 +1814,18 @@ void launch_scan_batch(bl_design *d, const std::vector<LockFit *> &fits, cudaStr
     }
     for (size_t u0 = 0; u0 < nf; u0 += kBatchMax) {
         int nb = (int)std::min<size_t>(kBatchMax, nf - u0);
-        const void *kern = batch_kernel(f64, nb);
-        const size_t smem = batch_smem(nb, itemsize(d->dt));
+        const bool mma = batch_use_mma();
+        const void *kern = mma ? batch_mma_kernel_n<kBatchMax>(f64, nb) : batch_kernel(f64, nb);
+        const size_t smem = mma ? batch_mma_smem(nb) : batch_smem(nb, itemsize(d->dt));
+        const int threads = mma ? kBMThreads : kBatchThreads;
         allow_dyn_smem(kern);
-        const int grid = grid_for(kern, kBatchThreads, smem, d->nsm);
+        const int grid = grid_for(kern, threads, smem, d->nsm);
         const void *X = d->X;
         int64_t ld = d->ld, p = d->p;
         int n = (int)d->n;
         FitScan *fp = dfs + u0;
         void *args[] = {&X, &ld, &n, &p, &fp, &nb};
-        CK(cudaLaunchKernel(kern, dim3(grid), dim3(kBatchThreads), args, smem, sst));
+        CK(cudaLaunchKernel(kern, dim3(grid), dim3(threads), args, smem, sst));
         timer->launches++;
         timer->batch_bytes += (double)d->n * itemsize(d->dt) * (double)d->p;
     }

@@ -506,6 +506,175 @@ __global__ void __launch_bounds__(kBatchThreads, 3) k_scan_batch(const T *__rest
     }
 }
 
+// NEXT-1 on the fp64 tensor cores: the same contraction Z = X^T R (columns x fits, summed
+// over the rows) as k_scan_batch, issued as mma.m8n8k4.f64 (DMMA: 256 FMAs per
+// instruction; the measured DMMA rate equals the DFMA peak, scripts/dmma_peak.cu, but
+// one instruction replaces 8 FMAs per lane and the operands are fragments, not a
+// shared-memory load per FMA -- k_scan_batch was bound by shared-memory bandwidth).
+// M = 8 columns, N = 8 fits, K = 4 rows; a warp owns 32 columns (4 m-tiles) and all
+// fits (ceil(NF / 8) n-tiles).  The K index is permuted so that lane (g, t) covers rows
+// 4t..4t+3 of a 16-row group over the group's 4 MMAs: its x fragment is ONE 16-byte
+// global load (fp32) of column g, its residual fragments two 16-byte shared loads per
+// fit.  Residual rows stream through a 3-stage cp.async ring (fit stride 66 doubles:
+// conflict-free fragment loads); the accumulators land in a shared Z tile and the
+// identity-(3) epilogue, tests and list compaction run as in k_scan_batch.
+constexpr int kBMThreads = 256;              // 8 warps
+constexpr int kBMCols = 256;                 // columns per CTA tile (32 per warp)
+constexpr int kBMRows = 64;                  // residual rows per stage (4 groups of 16)
+constexpr int kBMStages = 3;
+constexpr int kBMStride = kBMRows + 2;       // doubles per fit in a stage
+constexpr int kBMZ = 17;                     // Z tile row stride (doubles)
+__host__ __device__ constexpr size_t batch_mma_smem(int nf) {
+    return (size_t)kBMStages * nf * kBMStride * 8 + (size_t)kBMCols * kBMZ * 8;
+}
+
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d[0]), "+d"(d[1]) : "d"(a), "d"(b));
+}
+
+// raw x fragment of one lane: 4 consecutive rows of one column, kept unconverted while in flight
+template <typename T> struct XFrag;
+template <> struct XFrag<float> {
+    float4 v;
+    __device__ __forceinline__ void load(const float *p, bool ok) {
+        v = ok ? __ldcs(reinterpret_cast<const float4 *>(p)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __device__ __forceinline__ double get(int u) const { return u == 0 ? v.x : u == 1 ? v.y : u == 2 ? v.z : v.w; }
+};
+template <> struct XFrag<double> {
+    double2 a, b;
+    __device__ __forceinline__ void load(const double *p, bool ok) {
+        a = ok ? __ldcs(reinterpret_cast<const double2 *>(p)) : make_double2(0.0, 0.0);
+        b = ok ? __ldcs(reinterpret_cast<const double2 *>(p + 2)) : make_double2(0.0, 0.0);
+    }
+    __device__ __forceinline__ double get(int u) const { return u == 0 ? a.x : u == 1 ? a.y : u == 2 ? b.x : b.y; }
+};
+
+template <typename T, int NF>
+__global__ void __launch_bounds__(kBMThreads, 2) k_scan_batch_mma(const T *__restrict__ X, int64_t ld, int n, int64_t p,
+                                                                   const FitScan *__restrict__ fits, int nf_unused) {
+    extern __shared__ __align__(16) double smb[];
+    __shared__ FitScan fs[NF];
+    __shared__ double k1s[NF];
+    constexpr int NT = (NF + 7) / 8, MT = 4;
+    constexpr int GPS = kBMRows / 16;                        // 16-row groups per stage
+    constexpr int D = sizeof(T) == 4 ? 2 : 1;                // x groups in flight per lane (GPS % D == 0)
+    double *ring = smb;
+    double *Zs = smb + (size_t)kBMStages * NF * kBMStride;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+    if (threadIdx.x < NF) fs[threadIdx.x] = fits[threadIdx.x];
+    __syncthreads();
+    if (threadIdx.x < NF) k1s[threadIdx.x] = *fs[threadIdx.x].K1;
+    const int nstage = (n + kBMRows - 1) / kBMRows;
+    double *zw = Zs + (size_t)(32 * wid) * kBMZ;                 // this warp's 32 Z rows
+    for (int64_t col0 = (int64_t)blockIdx.x * kBMCols; col0 < p; col0 += (int64_t)gridDim.x * kBMCols) {
+        auto stage = [&](int sidx, int b) {
+            double *rs = ring + (size_t)b * NF * kBMStride;
+            const int i0 = sidx * kBMRows;
+            const bool full = i0 + kBMRows <= n;
+            for (int e = threadIdx.x; e < NF * kBMRows / 2; e += kBMThreads) {
+                const int f = e / (kBMRows / 2), i = 2 * (e - f * (kBMRows / 2));
+                double *dst = rs + f * kBMStride + i;
+                if (full) cp_async16(dst, fs[f].r + i0 + i);
+                else { dst[0] = i0 + i < n ? fs[f].r[i0 + i] : 0.0; dst[1] = i0 + i + 1 < n ? fs[f].r[i0 + i + 1] : 0.0; }
+            }
+            cp_async_commit();
+        };
+        // this lane's columns (clamped: past-the-end columns read a valid column, ignored)
+        const T *xc[MT];
+#pragma unroll
+        for (int mt = 0; mt < MT; mt++) xc[mt] = X + min(col0 + 32 * wid + 8 * mt + g, p - 1) * ld;
+        double acc[MT][NT][2];
+#pragma unroll
+        for (int mt = 0; mt < MT; mt++)
+#pragma unroll
+            for (int nt = 0; nt < NT; nt++) { acc[mt][nt][0] = 0.0; acc[mt][nt][1] = 0.0; }
+        __syncthreads();                                       // the previous tile's stages are consumed
+        stage(0, 0);
+        if (nstage > 1) stage(1, 1); else cp_async_commit();
+        // x fragments D groups ahead (group q = rows 16q..16q+15; lane rows 16q + 4t .. + 3)
+        XFrag<T> xr[D][MT];
+        auto xload = [&](int slot, int q) {
+            const int r = 16 * q + 4 * t;
+            const bool ok = r < ld;                            // ld % 4 == 0: 4 rows are inside or outside together
+#pragma unroll
+            for (int mt = 0; mt < MT; mt++) xr[slot][mt].load(xc[mt] + r, ok);
+        };
+#pragma unroll
+        for (int q = 0; q < D; q++)
+            if (16 * q < n) xload(q, q);
+        for (int sidx = 0; sidx < nstage; sidx++) {
+            cp_async_wait<1>();
+            __syncthreads();
+            if (sidx + 2 < nstage) stage(sidx + 2, (sidx + 2) % kBMStages); else cp_async_commit();
+            const double *rs = ring + (size_t)(sidx % kBMStages) * NF * kBMStride;
+#pragma unroll
+            for (int kg = 0; kg < GPS; kg++) {
+                const int q = sidx * GPS + kg, r0 = 16 * q;
+                if (r0 >= n) break;                                 // warp-uniform
+                const int slot = kg % D;
+                double xa[MT][4];
+                const int rr = r0 + 4 * t;
+#pragma unroll
+                for (int mt = 0; mt < MT; mt++)
+#pragma unroll
+                    for (int u = 0; u < 4; u++) xa[mt][u] = rr + u < n ? xr[slot][mt].get(u) : 0.0;   // padding rows: anything
+                if (r0 + 16 * D < n) xload(slot, q + D);
+                double rb[NT][4];
+#pragma unroll
+                for (int nt = 0; nt < NT; nt++) {
+                    const int f = 8 * nt + g;
+                    if (f < NF) {
+                        const double2 q0 = *reinterpret_cast<const double2 *>(rs + f * kBMStride + kg * 16 + 4 * t);
+                        const double2 q1 = *reinterpret_cast<const double2 *>(rs + f * kBMStride + kg * 16 + 4 * t + 2);
+                        rb[nt][0] = q0.x; rb[nt][1] = q0.y; rb[nt][2] = q1.x; rb[nt][3] = q1.y;
+                    } else {
+                        rb[nt][0] = rb[nt][1] = rb[nt][2] = rb[nt][3] = 0.0;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+#pragma unroll
+                    for (int mt = 0; mt < MT; mt++)
+#pragma unroll
+                        for (int nt = 0; nt < NT; nt++) dmma884(acc[mt][nt], xa[mt][u], rb[nt][u]);
+            }
+        }
+        cp_async_wait<0>();
+        // accumulators -> this warp's Z rows: lane (g, t) holds Z[8 mt + g][8 nt + 2t, +1]
+#pragma unroll
+        for (int mt = 0; mt < MT; mt++)
+#pragma unroll
+            for (int nt = 0; nt < NT; nt++) {
+                zw[(8 * mt + g) * kBMZ + 8 * nt + 2 * t] = acc[mt][nt][0];
+                zw[(8 * mt + g) * kBMZ + 8 * nt + 2 * t + 1] = acc[mt][nt][1];
+            }
+        __syncwarp();
+        const int64_t j = col0 + 32 * wid + lane;
+        const bool inr = j < p;
+#pragma unroll
+        for (int f = 0; f < NF; f++) {
+            const FitScan &F = fs[f];
+            bool isv = false, iss = false;
+            if (inr) {
+                const double d = zw[lane * kBMZ + f];
+                const double sj = F.s[j];
+                const double z = sj > 0.0 ? (d - F.c[j] * k1s[f]) * F.K2 / sj : 0.0;
+                F.out[j] = z;
+                const double az = fabs(z);
+                const bool inw = F.wflag[j] != 0;
+                const uint8_t fl = F.flags[j];
+                isv = !inw && (fl & 1) && az > F.thr_viol;
+                iss = !inw && (fl & 2) && F.thr_strong >= 0.0 && az >= F.thr_strong && sj > 0.0;
+            }
+            warp_append(isv, (int)j, F.viol, F.nviol);
+            warp_append(iss, (int)j, F.strong, F.nstrong);
+        }
+        __syncwarp();
+    }
+}
+
 // int8 design: exact integer dot products on the tensor cores.  The fp64 vector
 // v is quantised once per scan to a 64-bit fixed-point integer R_i = round(v_i
 // 2^S) (|R| < 2^62) split into 8 balanced base-256 digits (k_limbs); then
