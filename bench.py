@@ -331,6 +331,10 @@ def run_ours(args, rank, world, local_rank):
                      "cd_kernel_ms_per_step": cd_cycles / 1.965e6,
                      "cd_phase_cycles_per_visit": dict(zip(["cd_passes", "weights_v", "eta", "intercept (within cd_passes)"] if is_logit else ["lead", "bulk", "build_A", "catch_up"], cd_prof)),
                      "algorithmic_bytes_per_step": scan_bytes / args.steps,
+                     "dominant_kernel_note": ("the fused scan is the method's bandwidth-bound kernel and BASELINE's metric; "
+                                              "by time the sequential CD (k_cd_gram7) dominates when cd_ms_per_step > "
+                                              "scan_ms_per_step -- it is latency-bound (no roofline), reported as "
+                                              "cd_ns_per_visit / cd_kernel_cycles_per_visit"),
                      "full_scan": ({"GBps": fs_bytes / (fs_ms / 1e3) / 1e9,
                                     "frac": fs_bytes / (fs_ms / 1e3) / 1e9 / (link_gbs if host_res else pk["hbm_gbs"]),
                                     "launches_per_step": fs_launches} if fs_ms > 0 else None)},
