@@ -31,6 +31,80 @@ namespace {
 
 thread_local std::string g_err;
 
+// ---- block cache for device and pinned-host allocations (process-wide)
+// bl_free and workspace growth return blocks here instead of cudaFree / cudaFreeHost
+// (which synchronise the device and unmap); a later allocation of a similar size
+// (need <= size <= 2 need) reuses one, so repeated design loads and fits skip the
+// driver's allocation path.  Callers return a block only after synchronising the
+// stream that used it (as they did before cudaFree).  At most kCacheCap bytes stay
+// cached per device (larger or surplus blocks go back to the driver), and a failed
+// allocation releases every cached block and retries.
+namespace cache {
+constexpr size_t kCacheCap = (size_t)2 << 30;
+struct Pool {
+    std::mutex mu;
+    std::multimap<size_t, void *> freeb;
+    std::map<void *, size_t> live;
+    size_t cached = 0;
+};
+Pool &pool(bool host) {
+    static std::mutex mu;
+    static std::map<int, std::unique_ptr<Pool>> pools;
+    int dev = -1;
+    if (!host) cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    auto &pp = pools[dev];
+    if (!pp) pp = std::make_unique<Pool>();
+    return *pp;
+}
+cudaError_t raw_alloc(void **p, size_t b, bool host) { return host ? cudaMallocHost(p, b) : cudaMalloc(p, b); }
+void raw_free(void *p, bool host) { if (host) cudaFreeHost(p); else cudaFree(p); }
+cudaError_t alloc(void **p, size_t bytes, bool host) {
+    Pool &P = pool(host);
+    {
+        std::lock_guard<std::mutex> lk(P.mu);
+        auto it = P.freeb.lower_bound(bytes);
+        if (it != P.freeb.end() && it->first <= 2 * bytes) {
+            *p = it->second;
+            P.live[*p] = it->first;
+            P.cached -= it->first;
+            P.freeb.erase(it);
+            return cudaSuccess;
+        }
+    }
+    cudaError_t e = raw_alloc(p, bytes, host);
+    if (e != cudaSuccess) {                          // release the cache and retry once
+        cudaGetLastError();
+        std::lock_guard<std::mutex> lk(P.mu);
+        for (auto &kv : P.freeb) raw_free(kv.second, host);
+        P.freeb.clear();
+        P.cached = 0;
+        e = raw_alloc(p, bytes, host);
+    }
+    if (e == cudaSuccess) {
+        std::lock_guard<std::mutex> lk(P.mu);
+        P.live[*p] = bytes;
+    }
+    return e;
+}
+void release(void *p, bool host) {
+    if (!p) return;
+    Pool &P = pool(host);
+    std::lock_guard<std::mutex> lk(P.mu);
+    auto it = P.live.find(p);
+    if (it == P.live.end()) { raw_free(p, host); return; }
+    const size_t b = it->second;
+    P.live.erase(it);
+    if (P.cached + b > kCacheCap) { raw_free(p, host); return; }
+    P.freeb.emplace(b, p);
+    P.cached += b;
+}
+cudaError_t dmalloc(void **p, size_t bytes) { return alloc(p, bytes, false); }
+cudaError_t hmalloc(void **p, size_t bytes) { return alloc(p, bytes, true); }
+void dfree(void *p) { release(p, false); }
+void hfree(void *p) { release(p, true); }
+}  // namespace cache
+
 enum Magic : uint32_t { MAGIC_DESIGN = 0xB1DE5160u, MAGIC_PATH = 0xB1BA7400u, MAGIC_CV = 0xB1C0FF00u,
                         MAGIC_PREP = 0xB1B4E900u, MAGIC_DEAD = 0xDEADDEADu };
 
@@ -428,7 +502,7 @@ void ensure_stream_bufs(bl_prep *pp) {
     const size_t colb = (size_t)d->ld * itemsize(d->dt);
     pp->scols = std::max<int64_t>(1, std::min<int64_t>(d->p, (int64_t)(kStreamChunkBytes / colb)));
     for (int u = 0; u < 2; u++) {
-        cudaError_t e = cudaMalloc(&pp->sbuf[u], colb * pp->scols);
+        cudaError_t e = cache::dmalloc((void **)&pp->sbuf[u], colb * pp->scols);
         if (e != cudaSuccess) { cudaGetLastError(); raise(BL_ERR_OOM, "cudaMalloc for the streamed-scan buffers: %s", cudaGetErrorString(e)); }
         CK(cudaEventCreateWithFlags(&pp->copied[u], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&pp->used[u], cudaEventDisableTiming));
@@ -561,23 +635,23 @@ void free_prep(bl_prep *pp) {
     sum_events(pp->ev_scan);
     sum_events(pp->ev_cd);
     sum_events(pp->ev_prep);
-    if (pp->arena) cudaFree(pp->arena);
-    if (pp->hst) cudaFreeHost(pp->hst);
-    if (pp->hlist) cudaFreeHost(pp->hlist);
-    if (pp->hpre) cudaFreeHost(pp->hpre);
-    if (pp->hbw) cudaFreeHost(pp->hbw);
-    if (pp->hup) cudaFreeHost(pp->hup);
-    if (pp->warena) cudaFree(pp->warena);
-    if (pp->G) cudaFree(pp->G);
-    if (pp->GA) cudaFree(pp->GA);
-    if (pp->cbuf) cudaFree(pp->cbuf);
-    if (pp->rbuf) cudaFree(pp->rbuf);
-    if (pp->Xw) cudaFree(pp->Xw);
-    if (pp->cw) cudaFree(pp->cw);
-    if (pp->LG) cudaFree(pp->LG);
-    if (pp->lgbuf) cudaFree(pp->lgbuf);
+    if (pp->arena) cache::dfree(pp->arena);
+    if (pp->hst) cache::hfree(pp->hst);
+    if (pp->hlist) cache::hfree(pp->hlist);
+    if (pp->hpre) cache::hfree(pp->hpre);
+    if (pp->hbw) cache::hfree(pp->hbw);
+    if (pp->hup) cache::hfree(pp->hup);
+    if (pp->warena) cache::dfree(pp->warena);
+    if (pp->G) cache::dfree(pp->G);
+    if (pp->GA) cache::dfree(pp->GA);
+    if (pp->cbuf) cache::dfree(pp->cbuf);
+    if (pp->rbuf) cache::dfree(pp->rbuf);
+    if (pp->Xw) cache::dfree(pp->Xw);
+    if (pp->cw) cache::dfree(pp->cw);
+    if (pp->LG) cache::dfree(pp->LG);
+    if (pp->lgbuf) cache::dfree(pp->lgbuf);
     for (int u = 0; u < 2; u++) {
-        if (pp->sbuf[u]) cudaFree(pp->sbuf[u]);
+        if (pp->sbuf[u]) cache::dfree(pp->sbuf[u]);
         if (pp->copied[u]) cudaEventDestroy(pp->copied[u]);
         if (pp->used[u]) cudaEventDestroy(pp->used[u]);
     }
@@ -615,9 +689,9 @@ void ensure_host(Tp *&ptr, size_t &cap, size_t need) {
     if (need <= cap) return;
     size_t nc = std::max<size_t>(need, 2 * cap);
     nc = std::max<size_t>(nc, 1024);
-    if (ptr) CK(cudaFreeHost(ptr));
+    if (ptr) cache::hfree(ptr);
     ptr = nullptr;
-    CK(cudaMallocHost((void **)&ptr, nc * sizeof(Tp)));
+    CK(cache::hmalloc((void **)&ptr, nc * sizeof(Tp)));
     cap = nc;
 }
 
@@ -627,11 +701,11 @@ void ensure_W(bl_prep *pp, int64_t need) {
     int64_t nc = std::max<int64_t>(std::max<int64_t>(need, 2 * pp->Wcap), 1024);
     nc = std::min<int64_t>(std::max<int64_t>(nc, need), std::max<int64_t>(pp->d->sharded ? pp->d->p_global : pp->p, 1));
     CK(cudaStreamSynchronize(pp->stream));
-    if (pp->warena) CK(cudaFree(pp->warena));
+    if (pp->warena) cache::dfree(pp->warena);
     pp->warena = nullptr;
     size_t ib = (size_t)round_up(4 * nc, 256);
     size_t bytes = 3 * ib + (size_t)32 * nc;
-    cudaError_t e = cudaMalloc(&pp->warena, bytes);
+    cudaError_t e = cache::dmalloc((void **)&pp->warena, bytes);
     if (e != cudaSuccess) { cudaGetLastError(); raise(BL_ERR_OOM, "cudaMalloc(%zu) for W: %s", bytes, cudaGetErrorString(e)); }
     pp->W = (int *)pp->warena;
     pp->Wst_d = (int *)(pp->warena + ib);
@@ -644,10 +718,10 @@ void ensure_W(bl_prep *pp, int64_t need) {
 double *ensure_rbuf(bl_prep *pp, size_t count) {
     if (count <= pp->rbuf_cap) return pp->rbuf;
     CK(cudaStreamSynchronize(pp->stream));
-    if (pp->rbuf) CK(cudaFree(pp->rbuf));
+    if (pp->rbuf) cache::dfree(pp->rbuf);
     pp->rbuf = nullptr;
     const size_t nc = std::max<size_t>(count, 2 * pp->rbuf_cap);
-    cudaError_t e = cudaMalloc(&pp->rbuf, 8 * nc);
+    cudaError_t e = cache::dmalloc((void **)&pp->rbuf, 8 * nc);
     if (e != cudaSuccess) { cudaGetLastError(); pp->rbuf_cap = 0; raise(BL_ERR_OOM, "cudaMalloc(%zu) for the residual refresh: %s", 8 * nc, cudaGetErrorString(e)); }
     pp->rbuf_cap = nc;
     return pp->rbuf;
@@ -656,10 +730,10 @@ double *ensure_rbuf(bl_prep *pp, size_t count) {
 void *ensure_cbuf(bl_prep *pp, size_t bytes) {
     if (bytes <= pp->cbuf_cap) return pp->cbuf;
     CK(cudaStreamSynchronize(pp->stream));
-    if (pp->cbuf) CK(cudaFree(pp->cbuf));
+    if (pp->cbuf) cache::dfree(pp->cbuf);
     pp->cbuf = nullptr;
     size_t nb = std::max<size_t>(std::max<size_t>(bytes, 2 * pp->cbuf_cap), 4096);
-    cudaError_t e = cudaMalloc(&pp->cbuf, nb);
+    cudaError_t e = cache::dmalloc((void **)&pp->cbuf, nb);
     if (e != cudaSuccess) { cudaGetLastError(); pp->cbuf_cap = 0; raise(BL_ERR_OOM, "cudaMalloc(%zu) for collectives: %s", nb, cudaGetErrorString(e)); }
     pp->cbuf_cap = nb;
     return pp->cbuf;
@@ -673,11 +747,11 @@ void ensure_Ws(bl_prep *pp, int64_t need, int64_t have) {
     const int64_t nc = std::max<int64_t>(std::max<int64_t>(need, 2 * pp->ws_cap), 256);
     void *X2 = nullptr;
     double *v2 = nullptr;
-    cudaError_t e = cudaMalloc(&X2, (size_t)d->ld * nc * isz);
-    if (e == cudaSuccess) e = cudaMalloc(&v2, (size_t)8 * 4 * nc + (size_t)4 * nc);
+    cudaError_t e = cache::dmalloc((void **)&X2, (size_t)d->ld * nc * isz);
+    if (e == cudaSuccess) e = cache::dmalloc((void **)&v2, (size_t)8 * 4 * nc + (size_t)4 * nc);
     if (e != cudaSuccess) {
         cudaGetLastError();
-        if (X2) cudaFree(X2);
+        if (X2) cache::dfree(X2);
         raise(BL_ERR_OOM, "cudaMalloc for the working-set column store (%lld columns): %s", (long long)nc, cudaGetErrorString(e));
     }
     cudaStream_t st = pp->stream;
@@ -692,8 +766,8 @@ void ensure_Ws(bl_prep *pp, int64_t need, int64_t have) {
     k_iota<<<(unsigned)((nc + 255) / 256), 256, 0, st>>>(w2, (int)nc);
     CKL();
     CK(cudaStreamSynchronize(st));
-    if (pp->Xw) cudaFree(pp->Xw);
-    if (pp->cw) cudaFree(pp->cw);
+    if (pp->Xw) cache::dfree(pp->Xw);
+    if (pp->cw) cache::dfree(pp->cw);
     pp->Xw = X2;
     pp->cw = c2; pp->sw = s2; pp->bw = b2; pp->zw = z2;
     pp->widx = w2;
@@ -797,7 +871,7 @@ bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double a
                o_st = take(sizeof(RoundStatus)), o_av = take(8 * pp->amax_blocks), o_ai = take(8 * pp->amax_blocks),
                o_nl = take(16), o_rp = take(16 * (pp->vlen / 256 + 1)), o_yr = take(8 * pp->vlen);
         pp->arena_bytes = off;
-        cudaError_t e = cudaMalloc(&pp->arena, off);
+        cudaError_t e = cache::dmalloc((void **)&pp->arena, off);
         if (e != cudaSuccess) { cudaGetLastError(); raise(BL_ERR_OOM, "cudaMalloc(%zu) failed: %s", off, cudaGetErrorString(e)); }
         char *A = pp->arena;
         pp->c = (double *)(A + o_c); pp->s = (double *)(A + o_s); pp->a = (double *)(A + o_a);
@@ -814,8 +888,8 @@ bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double a
         pp->Wcap = 0;
         ensure_W(pp, std::min<int64_t>(p, 4096));
     }
-    if (!pp->hst) CK(cudaMallocHost(&pp->hst, sizeof(RoundStatus)));
-    if (!pp->hpre) CK(cudaMallocHost(&pp->hpre, sizeof(int) * 2 * kListPrefix));
+    if (!pp->hst) CK(cache::hmalloc((void **)&pp->hst, sizeof(RoundStatus)));
+    if (!pp->hpre) CK(cache::hmalloc((void **)&pp->hpre, sizeof(int) * 2 * kListPrefix));
     cudaStream_t st = pp->stream;
     CK(cudaMemsetAsync(pp->beta, 0, 8 * p, st));
     CK(cudaMemsetAsync(pp->wflag, 0, p, st));
@@ -1168,17 +1242,17 @@ void solve_logit_gram_t(bl_prep *pp, int nW, double lam, double alpha, double to
     const int nblk = (int)((ld + kLogitEtaThreads - 1) / kLogitEtaThreads);
     if (m > pp->ldLG) {
         int64_t nl = round_up(std::max<int64_t>(m, std::min<int64_t>(2 * pp->ldLG, kLogitGramMax)), 32);
-        if (pp->LG) CK(cudaFree(pp->LG));
+        if (pp->LG) cache::dfree(pp->LG);
         pp->LG = nullptr;
-        cudaError_t e = cudaMalloc(&pp->LG, (size_t)8 * nl * nl);
+        cudaError_t e = cache::dmalloc((void **)&pp->LG, (size_t)8 * nl * nl);
         if (e != cudaSuccess) { cudaGetLastError(); pp->ldLG = 0; raise(BL_ERR_OOM, "cudaMalloc for the weighted Gram: %s", cudaGetErrorString(e)); }
         pp->ldLG = nl;
     }
     const size_t need = (size_t)8 * (kLogitGramMax + ld + 3 * (size_t)nblk);
     if (need > pp->lgcap) {
-        if (pp->lgbuf) CK(cudaFree(pp->lgbuf));
+        if (pp->lgbuf) cache::dfree(pp->lgbuf);
         pp->lgbuf = nullptr;
-        cudaError_t e = cudaMalloc(&pp->lgbuf, need);
+        cudaError_t e = cache::dmalloc((void **)&pp->lgbuf, need);
         if (e != cudaSuccess) { cudaGetLastError(); pp->lgcap = 0; raise(BL_ERR_OOM, "cudaMalloc for the logistic workspace: %s", cudaGetErrorString(e)); }
         pp->lgcap = need;
     }
@@ -1198,7 +1272,8 @@ void solve_logit_gram_t(bl_prep *pp, int nW, double lam, double alpha, double to
     const void *kcd = m <= kLGThreads ? (const void *)k_cd_logit_gram<T, 1>
                     : m <= 2 * kLGThreads ? (const void *)k_cd_logit_gram<T, 2>
                     : m <= 4 * kLGThreads ? (const void *)k_cd_logit_gram<T, 4>
-                                          : (const void *)k_cd_logit_gram<T, 8>;
+                    : m <= 8 * kLGThreads ? (const void *)k_cd_logit_gram<T, 8>
+                                          : (const void *)k_cd_logit_gram<T, 16>;
     const size_t lim = allow_dyn_smem(kcd);
     if (smem > lim) raise(BL_ERR_OOM, "logistic covariance CD shared memory %zu > %zu", smem, lim);
     const void *kgw = (const void *)k_gram_w<T, M>;
@@ -1300,19 +1375,19 @@ void ensure_G(bl_prep *pp, int64_t need) {
     int64_t nl = std::max<int64_t>(std::max<int64_t>(need, 2 * pp->ldG), 256);
     nl = round_up(nl, 32);
     double *G2 = nullptr;
-    cudaError_t e = cudaMalloc(&G2, (size_t)8 * nl * nl);
+    cudaError_t e = cache::dmalloc((void **)&G2, (size_t)8 * nl * nl);
     if (e != cudaSuccess) { cudaGetLastError(); raise(BL_ERR_OOM, "cudaMalloc for the %lld^2 Gram matrix: %s", (long long)nl, cudaGetErrorString(e)); }
     CK(cudaMemsetAsync(G2, 0, (size_t)8 * nl * nl, pp->stream));   // rows/columns past |W| are read (x 0) by bulk copies
     if (pp->G && pp->nG > 0)
         CK(cudaMemcpy2DAsync(G2, 8 * nl, pp->G, 8 * pp->ldG, 8 * (size_t)pp->nG, pp->nG, cudaMemcpyDeviceToDevice,
                              pp->stream));
-    if (pp->G) { CK(cudaStreamSynchronize(pp->stream)); CK(cudaFree(pp->G)); }
+    if (pp->G) { CK(cudaStreamSynchronize(pp->stream)); cache::dfree(pp->G); }
     pp->G = G2;
     pp->ldG = nl;
     // CD workspaces (contents need not survive): compact G_AA (ldG x ldG) + per-block inverses
-    if (pp->GA) CK(cudaFree(pp->GA));
+    if (pp->GA) cache::dfree(pp->GA);
     pp->GA = nullptr;
-    e = cudaMalloc(&pp->GA, gram_ws_bytes(nl));
+    e = cache::dmalloc((void **)&pp->GA, gram_ws_bytes(nl));
     if (e != cudaSuccess) { cudaGetLastError(); pp->GA = nullptr; raise(BL_ERR_OOM, "cudaMalloc for the %lld^2 G_AA workspace: %s", (long long)nl, cudaGetErrorString(e)); }
     CK(cudaMemsetAsync(pp->GA, 0, gram_ws_bytes(nl), pp->stream));
 }
@@ -1858,14 +1933,14 @@ void cv_lockstep(bl_design *d, const double *y, const std::vector<int32_t> &fold
             if (lf.pp) release_prep(lf.pp);
             lf.pp = nullptr;
         }
-        if (dfs) cudaFree(dfs);
-        if (hfs) cudaFreeHost(hfs);
+        if (dfs) cache::dfree(dfs);
+        if (hfs) cache::hfree(hfs);
         if (sst) cudaStreamDestroy(sst);
     };
     try {
         CK(cudaStreamCreateWithFlags(&sst, cudaStreamNonBlocking));
-        CK(cudaMalloc(&dfs, sizeof(FitScan) * std::max<size_t>(F, 1)));
-        CK(cudaMallocHost(&hfs, sizeof(FitScan) * std::max<size_t>(F, 1)));
+        CK(cache::dmalloc((void **)&dfs, sizeof(FitScan) * std::max<size_t>(F, 1)));
+        CK(cache::hmalloc((void **)&hfs, sizeof(FitScan) * std::max<size_t>(F, 1)));
         for (size_t u = 0; u < F; u++) {
             LockFit &lf = fits[u];
             std::vector<uint8_t> train;
@@ -2093,7 +2168,7 @@ bl_status bl_load_design(const void *X, bl_dtype dt, int64_t n, int64_t p_local,
         } else {
             int64_t ldp = round_up(n, 16 / isz);
             size_t bytes = (size_t)ldp * p_local * isz;
-            cudaError_t e = cudaMalloc(&d->X, bytes);
+            cudaError_t e = cache::dmalloc((void **)&d->X, bytes);
             if (e != cudaSuccess) { delete d; raise(BL_ERR_OOM, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e)); }
             d->owned = true;
             d->ld = ldp;
@@ -2137,13 +2212,13 @@ bl_status bl_load_design(const void *X, bl_dtype dt, int64_t n, int64_t p_local,
                 }
                 // shard table (C0): every rank's (col_offset, p_local), in rank order
                 int64_t *dbuf = nullptr;
-                CK(cudaMalloc(&dbuf, 16 * (size_t)(d->world + 1)));
+                CK(cache::dmalloc((void **)&dbuf, 16 * (size_t)(d->world + 1)));
                 const int64_t mine[2] = {d->col_offset, p_local};
                 CK(cudaMemcpy(dbuf, mine, 16, cudaMemcpyHostToDevice));
                 std::vector<int64_t> all(2 * (size_t)d->world);
                 d->comm->allgather(dbuf, dbuf + 2, 16, 0);
                 CK(cudaMemcpy(all.data(), dbuf + 2, 16 * (size_t)d->world, cudaMemcpyDeviceToHost));
-                cudaFree(dbuf);
+                cache::dfree(dbuf);
                 d->shard_off.assign(d->world + 1, 0);
                 for (int r = 0; r < d->world; r++) {
                     if (all[2 * r] != d->shard_off[r]) raise(BL_ERR_ARG, "shards must be contiguous in rank order (rank %d col_offset %lld)", r, (long long)all[2 * r]);
@@ -2160,7 +2235,7 @@ bl_status bl_load_design(const void *X, bl_dtype dt, int64_t n, int64_t p_local,
                 }
             } catch (...) {
                 delete d->comm;
-                if (d->owned) cudaFree(d->X);
+                if (d->owned) cache::dfree(d->X);
                 if (d->host_reg) cudaHostUnregister(d->host_reg);
                 delete d;
                 throw;
@@ -2346,10 +2421,10 @@ bl_status bl_cv(bl_design *d, const double *y, const double *lambda, int n_lambd
         CK(cudaSetDevice(d->device));
         // device E (n_lambda x n): fold fits write disjoint held-out rows, so they run concurrently
         double *dE = nullptr, *dcv = nullptr;
-        cudaError_t e = cudaMalloc(&dE, 8 * (size_t)n_lambda * n + 16 * (size_t)n_lambda);
+        cudaError_t e = cache::dmalloc((void **)&dE, 8 * (size_t)n_lambda * n + 16 * (size_t)n_lambda);
         if (e != cudaSuccess) { cudaGetLastError(); delete cv; raise(BL_ERR_OOM, "cudaMalloc for CV errors: %s", cudaGetErrorString(e)); }
         dcv = dE + (size_t)n_lambda * n;
-        struct Free { double *p; ~Free() { if (p) cudaFree(p); } } fr{dE};
+        struct Free { double *p; ~Free() { if (p) cache::dfree(p); } } fr{dE};
         CK(cudaMemset(dE, 0, 8 * (size_t)n_lambda * n));
         // fold-parallel: fold fits run concurrently on their own streams --
         // each fit's CD kernel occupies one SM, so the folds share the GPU instead of queueing.
@@ -2529,7 +2604,7 @@ void bl_free(void *handle) {
         for (bl_prep *pp : d->pool) free_prep(pp);
         d->pool.clear();
         delete d->comm;
-        if (d->owned && d->X) cudaFree(d->X);
+        if (d->owned && d->X) cache::dfree(d->X);
         if (d->host_reg) cudaHostUnregister(d->host_reg);
         d->magic = MAGIC_DEAD;
         delete d;
