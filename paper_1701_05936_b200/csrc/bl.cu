@@ -2172,8 +2172,10 @@ bl_status bl_load_design(const void *X, bl_dtype dt, int64_t n, int64_t p_local,
             if (e != cudaSuccess) { delete d; raise(BL_ERR_OOM, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e)); }
             d->owned = true;
             d->ld = ldp;
-            CK(cudaMemset(d->X, 0, bytes));
-            CK(cudaMemcpy2D(d->X, ldp * isz, X, ld * isz, n * isz, p_local, cudaMemcpyHostToDevice));
+            if (ld == ldp) CK(cudaMemcpy(d->X, X, (size_t)ld * p_local * isz, cudaMemcpyHostToDevice));
+            else CK(cudaMemcpy2D(d->X, ldp * isz, X, ld * isz, n * isz, p_local, cudaMemcpyHostToDevice));
+            if (ldp > n)                               // padding rows are zero (whatever the caller's held)
+                CK(cudaMemset2D((char *)d->X + n * isz, ldp * isz, 0, (ldp - n) * isz, p_local));
         }
         if (x_is_device_ptr < 0 || x_is_device_ptr > 2) { delete d; raise(BL_ERR_ARG, "x_is_device_ptr must be 0, 1 or 2"); }
         d->sharded = false;
