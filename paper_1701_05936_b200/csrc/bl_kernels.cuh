@@ -557,7 +557,10 @@ __global__ void __launch_bounds__(kBMThreads, 2) k_scan_batch_mma(const T *__res
     extern __shared__ __align__(16) double smb[];
     __shared__ FitScan fs[NF];
     __shared__ double k1s[NF];
-    constexpr int NT = (NF + 7) / 8, MT = 4;
+    // fits 0..7 on the tensor cores; 1-4 further fits (cfg5: 11 = 8 + 3) as DFMAs on the same x
+    // fragments instead of a second, mostly empty 8-fit MMA tile
+    constexpr int NR = (NF > 8 && NF - 8 <= 4) ? NF - 8 : 0;
+    constexpr int NT = NR ? 1 : (NF + 7) / 8, MT = 4;
     constexpr int GPS = kBMRows / 16;                        // 16-row groups per stage
     constexpr int D = sizeof(T) == 4 ? 2 : 1;                // x groups in flight per lane (GPS % D == 0)
     double *ring = smb;
@@ -586,10 +589,14 @@ __global__ void __launch_bounds__(kBMThreads, 2) k_scan_batch_mma(const T *__res
 #pragma unroll
         for (int mt = 0; mt < MT; mt++) xc[mt] = X + min(col0 + 32 * wid + 8 * mt + g, p - 1) * ld;
         double acc[MT][NT][2];
+        double accr[MT][NR > 0 ? NR : 1];
 #pragma unroll
-        for (int mt = 0; mt < MT; mt++)
+        for (int mt = 0; mt < MT; mt++) {
 #pragma unroll
             for (int nt = 0; nt < NT; nt++) { acc[mt][nt][0] = 0.0; acc[mt][nt][1] = 0.0; }
+#pragma unroll
+            for (int f = 0; f < (NR > 0 ? NR : 1); f++) accr[mt][f] = 0.0;
+        }
         __syncthreads();                                       // the previous tile's stages are consumed
         stage(0, 0);
         if (nstage > 1) stage(1, 1); else cp_async_commit();
@@ -639,6 +646,22 @@ __global__ void __launch_bounds__(kBMThreads, 2) k_scan_batch_mma(const T *__res
                     for (int mt = 0; mt < MT; mt++)
 #pragma unroll
                         for (int nt = 0; nt < NT; nt++) dmma884(acc[mt][nt], xa[mt][u], rb[nt][u]);
+                if constexpr (NR > 0) {                            // fits 8.. : this lane's 4 rows, its 4 columns
+#pragma unroll
+                    for (int f = 0; f < NR; f++) {
+                        const double2 q0 = *reinterpret_cast<const double2 *>(rs + (8 + f) * kBMStride + kg * 16 + 4 * t);
+                        const double2 q1 = *reinterpret_cast<const double2 *>(rs + (8 + f) * kBMStride + kg * 16 + 4 * t + 2);
+#pragma unroll
+                        for (int mt = 0; mt < MT; mt++) {
+                            double v = accr[mt][f];
+                            v = fma(xa[mt][0], q0.x, v);
+                            v = fma(xa[mt][1], q0.y, v);
+                            v = fma(xa[mt][2], q1.x, v);
+                            v = fma(xa[mt][3], q1.y, v);
+                            accr[mt][f] = v;
+                        }
+                    }
+                }
             }
         }
         cp_async_wait<0>();
@@ -650,6 +673,17 @@ __global__ void __launch_bounds__(kBMThreads, 2) k_scan_batch_mma(const T *__res
                 zw[(8 * mt + g) * kBMZ + 8 * nt + 2 * t] = acc[mt][nt][0];
                 zw[(8 * mt + g) * kBMZ + 8 * nt + 2 * t + 1] = acc[mt][nt][1];
             }
+        if constexpr (NR > 0) {                                    // sum the DFMA partials over the 4 row lanes
+#pragma unroll
+            for (int mt = 0; mt < MT; mt++)
+#pragma unroll
+                for (int f = 0; f < NR; f++) {
+                    double v = accr[mt][f];
+                    v += __shfl_xor_sync(0xffffffffu, v, 1);
+                    v += __shfl_xor_sync(0xffffffffu, v, 2);
+                    if (t == 0) zw[(8 * mt + g) * kBMZ + 8 + f] = v;
+                }
+        }
         __syncwarp();
         const int64_t j = col0 + 32 * wid + lane;
         const bool inr = j < p;
