@@ -1312,20 +1312,6 @@ void solve_logit_gram_t(bl_prep *pp, int nW, double lam, double alpha, double to
     pp->launches += 2;
 }
 
-void solve_logit(bl_prep *pp, int nW, double lam, double alpha, double tol, int max_iter) {
-    bl_design *d = pp->d;
-    if (nW + 1 > kLogitGramMax || pp->cd_mode == 1) {       // residual form (or requested)
-        launch_cd_logit(pp, nW, lam, alpha, tol, max_iter);
-        return;
-    }
-    const bool M = pp->has_mask != 0;
-    if (d->dt == DT_F64) M ? solve_logit_gram_t<double, true>(pp, nW, lam, alpha, tol, max_iter)
-                           : solve_logit_gram_t<double, false>(pp, nW, lam, alpha, tol, max_iter);
-    else if (d->dt == DT_F32) M ? solve_logit_gram_t<float, true>(pp, nW, lam, alpha, tol, max_iter)
-                                : solve_logit_gram_t<float, false>(pp, nW, lam, alpha, tol, max_iter);
-    else M ? solve_logit_gram_t<int8_t, true>(pp, nW, lam, alpha, tol, max_iter)
-           : solve_logit_gram_t<int8_t, false>(pp, nW, lam, alpha, tol, max_iter);
-}
 
 __global__ void k_logit_init(double *eta, int ld, const PrepScalars *ps, RoundStatus *st) {
     const double yb = ps->ybar, b0 = log(yb / (1.0 - yb));     // the null model (QL2)
@@ -1434,6 +1420,146 @@ bool use_gram(bl_prep *pp, int nW) {
 }
 
 // One CD solve at lambda on the current W (a8), either flavour.
+// NEXT-3, lasso: the IRLS iteration's quadratic model solved by the cluster Gram CD (k_cd_gram7)
+// in intercept-eliminated, unit-curvature coordinates (k_logit_g7_* kernels).
+template <typename T, bool M>
+void solve_logit_g7_t(bl_prep *pp, int nW, double lam, double alpha, double tol, int max_iter) {
+    bl_design *d = pp->d;
+    cudaStream_t st = pp->stream;
+    const CdView v = cd_view(pp);
+    const int m = nW + 1;
+    const int64_t ld = d->ld;
+    const int nblk = (int)((ld + kLogitEtaThreads - 1) / kLogitEtaThreads);
+    if (m > pp->ldLG) {
+        int64_t nl = round_up(std::max<int64_t>(m, std::min<int64_t>(2 * pp->ldLG, kLogitGramMax)), 32);
+        if (pp->LG) cache::dfree(pp->LG);
+        pp->LG = nullptr;
+        cudaError_t e = cache::dmalloc((void **)&pp->LG, (size_t)8 * nl * nl);
+        if (e != cudaSuccess) { cudaGetLastError(); pp->ldLG = 0; raise(BL_ERR_OOM, "cudaMalloc for the weighted Gram: %s", cudaGetErrorString(e)); }
+        pp->ldLG = nl;
+    }
+    const size_t need = (size_t)8 * (kLogitGramMax + ld + 3 * (size_t)nblk + 4 * (size_t)kLogitGramMax + 8);
+    if (need > pp->lgcap) {
+        if (pp->lgbuf) cache::dfree(pp->lgbuf);
+        pp->lgbuf = nullptr;
+        cudaError_t e = cache::dmalloc((void **)&pp->lgbuf, need);
+        if (e != cudaSuccess) { cudaGetLastError(); pp->lgcap = 0; raise(BL_ERR_OOM, "cudaMalloc for the logistic workspace: %s", cudaGetErrorString(e)); }
+        pp->lgcap = need;
+    }
+    ensure_G(pp, nW);
+    double *bS = pp->lgbuf, *w = bS + kLogitGramMax, *part = w + ld, *ws = part + 3 * (size_t)nblk;
+    long long *acc = reinterpret_cast<long long *>(ws + 4 * (size_t)kLogitGramMax);
+    const T *X = reinterpret_cast<const T *>(v.X);
+    const uint8_t *mask = M ? pp->mask : nullptr;
+    const double inv_n = 1.0 / pp->nt, floor_ = 1e-13 * (alpha * lam + 1.0);
+    EvPair ev(pp, &pp->ev_cd);
+    k_logit_gather<<<(m + 255) / 256, 256, 0, st>>>(bS, v.beta, v.Wst, nW, pp->st);
+    CKL();
+    CK(cudaMemsetAsync(acc, 0, 8 * sizeof(long long), st));
+    CdGramArgs ga{};
+    ga.Wst = v.Wst;
+    ga.ord = pp->ord_d;
+    ga.nW = nW;
+    ga.ldG = (int)pp->ldG;
+    ga.G = pp->G;
+    ga.GA = pp->GA;
+    ga.MA = pp->GA + pp->ldG * pp->ldG;
+    ga.z = v.z;
+    ga.beta = v.beta;
+    ga.dbeta = pp->dbeta;
+    ga.lam_alpha = lam * alpha;
+    ga.inv_den = 1.0;
+    ga.tol = tol;
+    ga.floor_ = floor_;
+    ga.max_iter = max_iter;
+    ga.betaW_out = pp->betaW;
+    ga.c = v.c;
+    ga.s = v.s;
+    ga.st = pp->st;
+    ga.tau = ws + nW;
+    const int R = cd_cluster();
+    const void *kern = gram7_kernel(false, R);
+    const size_t smem = gram7_smem(nW, R);
+    const size_t lim = allow_dyn_smem(kern);
+    if (smem > lim) raise(BL_ERR_OOM, "Gram CD shared memory %zu > %zu (|W| = %d)", smem, lim, nW);
+    const void *kgw = (const void *)k_gram_w<T, M>;
+    allow_dyn_smem(kgw);
+    for (int it = 0;; it++) {
+        k_logit_eta<T, M><<<nblk, kLogitEtaThreads, 0, st>>>(X, ld, (int)d->n, v.Wst, nW, v.c, v.s, bS, pp->yraw,
+                                                             mask, pp->rfull, w, pp->rscan, part, pp->st, it == 0);
+        CKL();
+        k_gram_w<T, M><<<dim3(m, (m + 31) / 32), 256, (size_t)8 * d->n, st>>>(X, ld, (int)d->n, v.Wst, nW,
+                                                                             (int)pp->ldLG, v.c, v.s, w, inv_n,
+                                                                             pp->LG, part, nblk, pp->st);
+        CKL();
+        {                                      // g_W = x~_W' (y - pi) / n
+            ScanArgs sa{};
+            sa.list = v.Wst;
+            sa.nlist = nullptr;
+            sa.nlist_host = nW;
+            sa.K1 = &pp->st->sumr;
+            sa.K2v = inv_n;
+            sa.out = v.z;
+            launch_scan(pp, sa, pp->rscan, false, false, d->wstore ? pp->Xw : nullptr, v.c, v.s);
+        }
+        k_logit_g7_slots<<<(nW + 255) / 256, 256, 0, st>>>(nW, pp->LG, (int)pp->ldLG, v.Wst, bS, v.z, v.beta, ws,
+                                                            lam * alpha, inv_n, pp->st);
+        CKL();
+        k_logit_g7_schur<<<dim3(nW, (nW + 255) / 256), 256, 0, st>>>(nW, pp->LG, (int)pp->ldLG, ws, pp->G,
+                                                                     (int)pp->ldG);
+        CKL();
+        G7Work wk = gram_ws(pp);
+        void *args[] = {&ga, &wk};
+        CK(cudaLaunchKernel(kern, dim3(R), dim3(kG7Threads), args, smem, st));
+        k_logit_g7_post<<<1, 256, 0, st>>>(nW, pp->LG, (int)pp->ldLG, v.Wst, v.beta, bS, ws, inv_n, tol, floor_,
+                                           max_iter, pp->st, acc);
+        CKL();
+        pp->launches += 6;
+        CK(cudaMemcpyAsync(pp->hst, pp->st, sizeof(RoundStatus), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (pp->hst->cd_status || pp->hst->irls_done) break;
+    }
+    pp->nG = 0;                                // G now holds this model, not the linear Gram
+    k_logit_eta<T, M><<<nblk, kLogitEtaThreads, 0, st>>>(X, ld, (int)d->n, v.Wst, nW, v.c, v.s, bS, pp->yraw, mask,
+                                                         pp->rfull, w, pp->rscan, part, pp->st, 0);
+    CKL();
+    k_logit_finish<<<1, 256, 0, st>>>(part, nblk, bS, nW, v.Wst, pp->ord_d, v.c, v.s, pp->betaW, pp->st);
+    CKL();
+    k_logit_g7_counters<<<1, 1, 0, st>>>(pp->st, acc);
+    CKL();
+    pp->launches += 3;
+}
+
+bool logit_use_g7() {
+    static const bool v = [] { const char *e = std::getenv("BL_LOGIT_G7"); return !(e && e[0] == '0'); }();
+    return v;
+}
+
+void solve_logit(bl_prep *pp, int nW, double lam, double alpha, double tol, int max_iter) {
+    bl_design *d = pp->d;
+    if (nW + 1 > kLogitGramMax || pp->cd_mode == 1) {       // residual form (or requested)
+        launch_cd_logit(pp, nW, lam, alpha, tol, max_iter);
+        return;
+    }
+    const bool M = pp->has_mask != 0;
+    if (alpha == 1.0 && nW >= 1 && logit_use_g7()) {        // lasso: the cluster Gram CD
+        if (d->dt == DT_F64) M ? solve_logit_g7_t<double, true>(pp, nW, lam, alpha, tol, max_iter)
+                               : solve_logit_g7_t<double, false>(pp, nW, lam, alpha, tol, max_iter);
+        else if (d->dt == DT_F32) M ? solve_logit_g7_t<float, true>(pp, nW, lam, alpha, tol, max_iter)
+                                    : solve_logit_g7_t<float, false>(pp, nW, lam, alpha, tol, max_iter);
+        else M ? solve_logit_g7_t<int8_t, true>(pp, nW, lam, alpha, tol, max_iter)
+               : solve_logit_g7_t<int8_t, false>(pp, nW, lam, alpha, tol, max_iter);
+        return;
+    }
+    if (d->dt == DT_F64) M ? solve_logit_gram_t<double, true>(pp, nW, lam, alpha, tol, max_iter)
+                           : solve_logit_gram_t<double, false>(pp, nW, lam, alpha, tol, max_iter);
+    else if (d->dt == DT_F32) M ? solve_logit_gram_t<float, true>(pp, nW, lam, alpha, tol, max_iter)
+                                : solve_logit_gram_t<float, false>(pp, nW, lam, alpha, tol, max_iter);
+    else M ? solve_logit_gram_t<int8_t, true>(pp, nW, lam, alpha, tol, max_iter)
+           : solve_logit_gram_t<int8_t, false>(pp, nW, lam, alpha, tol, max_iter);
+}
+
+
 void solve_cd(bl_prep *pp, int nW, double lam, double alpha, double tol, int max_iter) {
     if (!use_gram(pp, nW)) {
         launch_cd(pp, nW, lam, alpha, tol, max_iter);

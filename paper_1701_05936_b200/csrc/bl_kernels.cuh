@@ -1911,6 +1911,92 @@ __global__ void k_logit_finish(const double *__restrict__ part, int nblk, const 
     }
 }
 
+// ---- NEXT-3 on the cluster Gram CD (lasso, alpha = 1): one IRLS iteration's quadratic model
+// with the intercept eliminated (Schur complement of the intercept row of Gw) and each
+// coordinate scaled to unit curvature, so k_cd_gram7 solves it unchanged except for a per-slot
+// threshold: gamma_j = sqrt(D_j) beta_j, D_j = Gw_jj - Gw_j0^2 / Gw_00,
+//   G''_jk = (Gw_jk - Gw_j0 Gw_k0 / Gw_00) / sqrt(D_j D_k),  z_j = (g_j - Gw_j0 g_0 / Gw_00) / sqrt(D_j),
+//   tau_j = lambda alpha / sqrt(D_j).
+// The intercept follows from the solved coefficients: d0 = (g_0 - sum_j Gw_j0 d_j) / Gw_00.
+// ws (per slot, 4 nW doubles): sc = 1/sqrt(D), tau, beta at the iteration's start; acc (8).
+__global__ void k_logit_g7_slots(int nW, const double *__restrict__ LG, int ldL, const int *__restrict__ Wst,
+                                 const double *__restrict__ bS, double *__restrict__ z, double *__restrict__ beta,
+                                 double *__restrict__ ws, double lam_alpha, double inv_n, const RoundStatus *st) {
+    const double h00 = LG[(int64_t)nW * ldL + nW], g0 = st->sumr * inv_n;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nW; k += gridDim.x * blockDim.x) {
+        const double h = LG[(int64_t)k * ldL + nW];
+        const double D = LG[(int64_t)k * ldL + k] - h * h / h00;
+        const double sc = D > 0.0 ? 1.0 / sqrt(D) : 0.0;
+        const int j = Wst[k];
+        ws[k] = sc;
+        ws[nW + k] = lam_alpha * sc;
+        ws[2 * nW + k] = bS[k];
+        z[j] = (z[j] - h * g0 / h00) * sc;
+        beta[j] = sc > 0.0 ? bS[k] / sc : 0.0;
+    }
+}
+
+__global__ void k_logit_g7_schur(int nW, const double *__restrict__ LG, int ldL, const double *__restrict__ ws,
+                                 double *__restrict__ G, int ldG) {
+    const int a = blockIdx.x;
+    const double h00 = LG[(int64_t)nW * ldL + nW], ha = LG[(int64_t)a * ldL + nW], sa = ws[a];
+    for (int b = blockIdx.y * blockDim.x + threadIdx.x; b < nW; b += gridDim.y * blockDim.x)
+        G[(int64_t)a * ldG + b] = (LG[(int64_t)a * ldL + b] - ha * LG[(int64_t)b * ldL + nW] / h00) * sa * ws[b];
+}
+
+// after k_cd_gram7: back to beta, the intercept step, the IRLS convergence test (QL6) and the
+// solve counters accumulated over the iterations (acc: passes, visits, updates, cycles)
+__global__ void k_logit_g7_post(int nW, const double *__restrict__ LG, int ldL, const int *__restrict__ Wst,
+                                double *__restrict__ beta, double *__restrict__ bS, const double *__restrict__ ws,
+                                double inv_n, double tol, double floor_, int max_iter, RoundStatus *st,
+                                long long *acc) {
+    __shared__ double red[32];
+    const double h00 = LG[(int64_t)nW * ldL + nW], g0 = st->sumr * inv_n;
+    double hd = 0.0, dm = 0.0, bm = 0.0;
+    for (int k = threadIdx.x; k < nW; k += blockDim.x) {
+        const int j = Wst[k];
+        const double bn = beta[j] * ws[k];
+        const double d = bn - ws[2 * nW + k];
+        beta[j] = bn;
+        bS[k] = bn;
+        hd = fma(LG[(int64_t)k * ldL + nW], d, hd);
+        dm = fmax(dm, fabs(d));
+        bm = fmax(bm, fabs(bn));
+    }
+    hd = block_sum(hd, red);
+    __syncthreads();
+    dm = block_max(dm, red);
+    __syncthreads();
+    bm = block_max(bm, red);
+    if (threadIdx.x == 0) {
+        const double d0 = (g0 - hd) / h00;
+        const double b0 = bS[nW] + d0;
+        bS[nW] = b0;
+        st->b0 = b0;
+        const bool ok_b = dm <= tol * bm || dm <= floor_;
+        const bool ok_0 = fabs(d0) <= tol * fmax(1.0, fabs(b0)) || fabs(d0) <= floor_;
+        acc[0] += st->cd_passes;
+        acc[1] += st->cd_visits;
+        acc[2] += st->cd_updates;
+        acc[3] += st->cd_cycles;
+        acc[4] += 1;
+        if (st->cd_status) acc[5] = st->cd_status;
+        if (acc[4] > max_iter) acc[5] = 3;
+        st->irls_done = ok_b && ok_0;
+        st->outer = (int)acc[4];
+        st->cd_status = (int)acc[5];
+    }
+}
+
+__global__ void k_logit_g7_counters(RoundStatus *st, const long long *acc) {
+    st->cd_passes = (int)acc[0];
+    st->cd_visits = acc[1];
+    st->cd_updates = acc[2];
+    st->cd_cycles = acc[3];
+    st->outer = (int)acc[4];
+    st->cd_status = (int)acc[5];
+}
+
 // ------------------------------- NEXT-2: covariance-update ("Gram") CD on W
 // SURVEY 8(f) NEXT-2 (glmnet's covariance updates; the paper's CD "only iterates
 // over features in the active set").  Same iterates as the residual CD
@@ -1997,6 +2083,8 @@ struct CdGramArgs {
     double *betaW_out;       // 3*nW: beta, c, s per slot (cyclic order)
     const double *c, *s;
     RoundStatus *st;
+    const double *tau;       // per-slot soft threshold (nullptr: lam_alpha for every slot); the
+                             // logistic path's scaled coordinates (NEXT-3, lasso only)
 };
 
 // Cluster Gram CD (v7): the v6 algorithm above with its bulk spread over a
@@ -2152,7 +2240,7 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
     long long visits = 0, updates = 0, pr_lead = 0, pr_bulk = 0, retries = 0, rebuilds = 0;
     long long pr_build = 0, pr_catch = 0, ncatch = 0, nfull = 0;
     long long dbg[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    const double la = a.lam_alpha, inv_den = a.inv_den;
+    const double la0 = a.lam_alpha, inv_den = a.inv_den;
     double dm = 0.0, bm = 0.0;                              // leader warp: per-lane running maxima
 
     auto block_rank = [&](bool nz, int &pos) -> int {     // order-preserving CTA compaction
@@ -2237,6 +2325,7 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
             bo = bS[s];
             zc = (zo - acc) + bo;
         }
+        const double la = (a.tau && valid) ? a.tau[s] : la0;      // this lane's threshold
         const double(*GL)[32] = Gd[buf];
         int pred = bo > 0.0 ? 1 : (bo < 0.0 ? -1 : 0);
         double dfin = 0.0, bnfin = bo;
