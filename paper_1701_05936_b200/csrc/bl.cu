@@ -1420,8 +1420,9 @@ bool use_gram(bl_prep *pp, int nW) {
 }
 
 // One CD solve at lambda on the current W (a8), either flavour.
-// NEXT-3, lasso: the IRLS iteration's quadratic model solved by the cluster Gram CD (k_cd_gram7)
-// in intercept-eliminated, unit-curvature coordinates (k_logit_g7_* kernels).
+// NEXT-3: the IRLS iteration's quadratic model solved by the cluster Gram CD (k_cd_gram7) in
+// intercept-eliminated, unit-curvature coordinates (k_logit_g7_* kernels; per-slot thresholds and,
+// for alpha < 1, per-slot ridge denominators).
 template <typename T, bool M>
 void solve_logit_g7_t(bl_prep *pp, int nW, double lam, double alpha, double tol, int max_iter) {
     bl_design *d = pp->d;
@@ -1477,8 +1478,9 @@ void solve_logit_g7_t(bl_prep *pp, int nW, double lam, double alpha, double tol,
     ga.s = v.s;
     ga.st = pp->st;
     ga.tau = ws + nW;
+    ga.idv = alpha < 1.0 ? ws + 3 * (size_t)nW : nullptr;
     const int R = cd_cluster();
-    const void *kern = gram7_kernel(false, R);
+    const void *kern = gram7_kernel(alpha < 1.0, R);
     const size_t smem = gram7_smem(nW, R);
     const size_t lim = allow_dyn_smem(kern);
     if (smem > lim) raise(BL_ERR_OOM, "Gram CD shared memory %zu > %zu (|W| = %d)", smem, lim, nW);
@@ -1503,7 +1505,7 @@ void solve_logit_g7_t(bl_prep *pp, int nW, double lam, double alpha, double tol,
             launch_scan(pp, sa, pp->rscan, false, false, d->wstore ? pp->Xw : nullptr, v.c, v.s);
         }
         k_logit_g7_slots<<<(nW + 255) / 256, 256, 0, st>>>(nW, pp->LG, (int)pp->ldLG, v.Wst, bS, v.z, v.beta, ws,
-                                                            lam * alpha, inv_n, pp->st);
+                                                            lam * alpha, lam * (1.0 - alpha), inv_n, pp->st);
         CKL();
         k_logit_g7_schur<<<dim3(nW, (nW + 255) / 256), 256, 0, st>>>(nW, pp->LG, (int)pp->ldLG, ws, pp->G,
                                                                      (int)pp->ldG);
@@ -1542,7 +1544,7 @@ void solve_logit(bl_prep *pp, int nW, double lam, double alpha, double tol, int 
         return;
     }
     const bool M = pp->has_mask != 0;
-    if (alpha == 1.0 && nW >= 1 && logit_use_g7()) {        // lasso: the cluster Gram CD
+    if (nW >= 1 && logit_use_g7()) {                         // the cluster Gram CD
         if (d->dt == DT_F64) M ? solve_logit_g7_t<double, true>(pp, nW, lam, alpha, tol, max_iter)
                                : solve_logit_g7_t<double, false>(pp, nW, lam, alpha, tol, max_iter);
         else if (d->dt == DT_F32) M ? solve_logit_g7_t<float, true>(pp, nW, lam, alpha, tol, max_iter)

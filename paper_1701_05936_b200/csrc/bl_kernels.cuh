@@ -1911,17 +1911,18 @@ __global__ void k_logit_finish(const double *__restrict__ part, int nblk, const 
     }
 }
 
-// ---- NEXT-3 on the cluster Gram CD (lasso, alpha = 1): one IRLS iteration's quadratic model
+// ---- NEXT-3 on the cluster Gram CD: one IRLS iteration's quadratic model
 // with the intercept eliminated (Schur complement of the intercept row of Gw) and each
 // coordinate scaled to unit curvature, so k_cd_gram7 solves it unchanged except for a per-slot
 // threshold: gamma_j = sqrt(D_j) beta_j, D_j = Gw_jj - Gw_j0^2 / Gw_00,
 //   G''_jk = (Gw_jk - Gw_j0 Gw_k0 / Gw_00) / sqrt(D_j D_k),  z_j = (g_j - Gw_j0 g_0 / Gw_00) / sqrt(D_j),
-//   tau_j = lambda alpha / sqrt(D_j).
+//   tau_j = lambda alpha / sqrt(D_j),  1 / curvature_j = 1 / (1 + lambda (1 - alpha) / D_j).
 // The intercept follows from the solved coefficients: d0 = (g_0 - sum_j Gw_j0 d_j) / Gw_00.
 // ws (per slot, 4 nW doubles): sc = 1/sqrt(D), tau, beta at the iteration's start; acc (8).
 __global__ void k_logit_g7_slots(int nW, const double *__restrict__ LG, int ldL, const int *__restrict__ Wst,
                                  const double *__restrict__ bS, double *__restrict__ z, double *__restrict__ beta,
-                                 double *__restrict__ ws, double lam_alpha, double inv_n, const RoundStatus *st) {
+                                 double *__restrict__ ws, double lam_alpha, double lam_l2, double inv_n,
+                                 const RoundStatus *st) {
     const double h00 = LG[(int64_t)nW * ldL + nW], g0 = st->sumr * inv_n;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nW; k += gridDim.x * blockDim.x) {
         const double h = LG[(int64_t)k * ldL + nW];
@@ -1931,6 +1932,7 @@ __global__ void k_logit_g7_slots(int nW, const double *__restrict__ LG, int ldL,
         ws[k] = sc;
         ws[nW + k] = lam_alpha * sc;
         ws[2 * nW + k] = bS[k];
+        ws[3 * nW + k] = 1.0 / (1.0 + lam_l2 * sc * sc);        // ridge term in scaled coordinates
         z[j] = (z[j] - h * g0 / h00) * sc;
         beta[j] = sc > 0.0 ? bS[k] / sc : 0.0;
     }
@@ -2083,8 +2085,9 @@ struct CdGramArgs {
     double *betaW_out;       // 3*nW: beta, c, s per slot (cyclic order)
     const double *c, *s;
     RoundStatus *st;
-    const double *tau;       // per-slot soft threshold (nullptr: lam_alpha for every slot); the
-                             // logistic path's scaled coordinates (NEXT-3, lasso only)
+    const double *tau;       // per-slot soft threshold (nullptr: lam_alpha for every slot) and
+    const double *idv;       // per-slot 1 / curvature (nullptr: inv_den): the logistic path's
+                             // scaled coordinates (NEXT-3)
 };
 
 // Cluster Gram CD (v7): the v6 algorithm above with its bulk spread over a
@@ -2240,7 +2243,7 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
     long long visits = 0, updates = 0, pr_lead = 0, pr_bulk = 0, retries = 0, rebuilds = 0;
     long long pr_build = 0, pr_catch = 0, ncatch = 0, nfull = 0;
     long long dbg[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    const double la0 = a.lam_alpha, inv_den = a.inv_den;
+    const double la0 = a.lam_alpha, inv_den0 = a.inv_den;
     double dm = 0.0, bm = 0.0;                              // leader warp: per-lane running maxima
 
     auto block_rank = [&](bool nz, int &pos) -> int {     // order-preserving CTA compaction
@@ -2326,6 +2329,7 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
             zc = (zo - acc) + bo;
         }
         const double la = (a.tau && valid) ? a.tau[s] : la0;      // this lane's threshold
+        const double inv_den = (a.idv && valid) ? a.idv[s] : inv_den0;
         const double(*GL)[32] = Gd[buf];
         int pred = bo > 0.0 ? 1 : (bo < 0.0 ? -1 : 0);
         double dfin = 0.0, bnfin = bo;
@@ -2604,7 +2608,8 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
                 const int b0 = 32 * q, nb = min(32, na - b0);
                 for (int e = lane; e < 1024; e += 32) {
                     const int p = e >> 5, b = e & 31;
-                    N[p][b] = (b > p && b < nb) ? inv_den * __ldcg(a.GA + (int64_t)(b0 + p) * ldG + b0 + b) : 0.0;
+                    N[p][b] = (b > p && b < nb) ? (a.idv ? a.idv[__ldcg(wk.act + b0 + b)] : inv_den0) *
+                                                      __ldcg(a.GA + (int64_t)(b0 + p) * ldG + b0 + b) : 0.0;
                 }
                 __syncwarp();
                 double x[32];
