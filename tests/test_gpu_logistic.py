@@ -145,3 +145,27 @@ def test_logistic_sharded_is_G_invariant():
     for r in range(G):
         np.testing.assert_array_equal(out[r].dense(inst.p), ref.dense(inst.p))
         np.testing.assert_array_equal(out[r].a0, ref.a0)
+
+
+def test_logistic_single_cta_covariance_form():
+    """The single-CTA covariance-form kernel (k_cd_logit_gram, selected with BL_LOGIT_G7=0,
+    read once per process) against the oracle, in a child process."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, oracle, synth\n"
+        "from paper_1701_05936_b200 import bl\n"
+        "inst = synth.logistic_instance(157, 613, dtype=np.float32, seed=7, kind='corr', n_true=10, scale=1.5)\n"
+        "d = bl.Design(inst.host_X(), inst.n)\n"
+        "for alpha in (1.0, 0.5):\n"
+        "    lams = synth.lambda_grid(d.lambda_max(inst.y, alpha), 20, 0.15)\n"
+        "    op = oracle.fit_path_binomial(inst, inst.y, lams, alpha=alpha, tol=1e-12)\n"
+        "    B = d.fit_path_binomial(inst.y, lams, alpha=alpha, tol=1e-10).dense(inst.p)\n"
+        "    for k in range(len(lams)):\n"
+        "        sc = np.abs(op.beta[:, k]).max()\n"
+        "        assert np.abs(B[:, k] - op.beta[:, k]).max() <= 1e-5 * sc or sc == 0.0, (alpha, k)\n"
+        "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, BL_LOGIT_G7="0", PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
