@@ -363,6 +363,7 @@ struct bl_prep {
     int profile;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_scan, ev_cd, ev_prep;
     std::vector<int64_t> scan_full;   // per timed scan launch: its local columns if it covered every live column, else -1
+    int scan_rev = 0;                 // direction of the next KKT scan (alternates, see ScanArgs::rev)
     double prep_bytes;
     int64_t launches;
 };
@@ -557,6 +558,7 @@ void launch_scan(bl_prep *pp, ScanArgs a, const double *v_dev, bool timed, bool 
         if (2 * m >= d->p && (!a.list || a.flags)) {
             streamed = true;
             a.list = nullptr;
+            a.rev = 0;
         }
     }
     if (d->dt == DT_I8) {
@@ -1768,6 +1770,8 @@ struct PathRun {
         sa.nviol = &pp->st->nviol;
         sa.strong = pp->strong;
         sa.nstrong = &pp->st->nstrong;
+        sa.rev = pp->scan_rev;
+        pp->scan_rev ^= 1;
         return sa;
     }
     void count_cd() {

@@ -229,6 +229,8 @@ struct ScanArgs {
     int64_t p;
     const int *list;          // nullptr => dense j0..p-1
     int64_t j0;               // first column of a dense range (streamed chunks of a host-resident design)
+    int rev;                  // visit the columns in reverse order: consecutive KKT scans alternate
+                              // direction, so each starts on the columns the previous one left in L2
     const int *nlist;         // device count of `list` (nullptr => nlist_host)
     int nlist_host;
     const double *v;          // fp64 vector, >= ld entries, zero beyond n (fp32/fp64 path)
@@ -286,6 +288,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_fp(ScanArgs a) {
 #pragma unroll
         for (int q = 0; q < C; q++) {
             int64_t idx = g + q < m ? g + q : m - 1;
+            if (a.rev) idx = m - 1 - idx;
             col[q] = list ? (int64_t)list[idx] : j0 + idx;
             ptr[q] = X + col[q] * a.ld;
         }
@@ -752,6 +755,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_i8(ScanArgs a) {
     for (int64_t g0 = gw * 16; g0 < m; g0 += nwarp * 16) {
         int64_t ia = g0 + g < m ? g0 + g : m - 1;
         int64_t ib = g0 + g + 8 < m ? g0 + g + 8 : m - 1;
+        if (a.rev) { ia = m - 1 - ia; ib = m - 1 - ib; }
         int64_t ja = list ? (int64_t)list[ia] : jd + ia;
         int64_t jb = list ? (int64_t)list[ib] : jd + ib;
         const int8_t *pa = X + ja * a.ld, *pb = X + jb * a.ld;
