@@ -1043,16 +1043,10 @@ void upload_W(bl_prep *pp, const WorkingSet &ws, const std::vector<int> &added) 
     for (size_t q = 0; q < nW; q++) { h[q] = ws.sorted[q] - off; h[nW + q] = ws.slots[q] - off; }
     std::memcpy(h + 2 * nW, ord.data(), 4 * nW);
     std::memcpy(h + 3 * nW, mine.data(), 4 * mine.size());
-    if (nW) {
-        if (!d->sharded) {
-            CK(cudaMemcpyAsync(pp->W, h, 4 * nW, cudaMemcpyHostToDevice, st));
-            CK(cudaMemcpyAsync(pp->Wst_d, h + nW, 4 * nW, cudaMemcpyHostToDevice, st));
-        }
-        CK(cudaMemcpyAsync(pp->ord_d, h + 2 * nW, 4 * nW, cudaMemcpyHostToDevice, st));
-    }
-    if (!mine.empty()) {
-        CK(cudaMemcpyAsync(pp->viol, h + 3 * nW, 4 * mine.size(), cudaMemcpyHostToDevice, st));
-        k_set_flags<<<(unsigned)((mine.size() + 255) / 256), 256, 0, st>>>(pp->viol, (int)mine.size(), pp->wflag, 1);
+    if (nW || !mine.empty()) {                 // one launch reads the staging in place (zero-copy)
+        const int total = (int)std::max(nW, mine.size());
+        k_upload_W<<<(unsigned)std::min(64, (total + 255) / 256), 256, 0, st>>>(
+            h, (int)nW, (int)mine.size(), d->sharded ? 0 : 1, pp->W, pp->Wst_d, pp->ord_d, pp->viol, pp->wflag);
         CKL();
         pp->launches++;
     }

@@ -1049,6 +1049,26 @@ __global__ void k_ssr_init(int64_t p, const double *__restrict__ a, const double
     }
 }
 
+// working-set upload in one launch: the host's pinned staging (sorted columns, slots, cyclic
+// order, this shard's new columns) is read in place over the host link (zero-copy) and
+// scattered into the device arrays; new columns get their "in W" flag
+__global__ void k_upload_W(const int *__restrict__ h, int nW, int nnew, int write_w, int *__restrict__ W,
+                           int *__restrict__ Wst, int *__restrict__ ord, int *__restrict__ fresh,
+                           uint8_t *__restrict__ wflag) {
+    const int total = max(nW, nnew);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        if (i < nW) {
+            if (write_w) { W[i] = h[i]; Wst[i] = h[nW + i]; }
+            ord[i] = h[2 * nW + i];
+        }
+        if (i < nnew) {
+            const int j = h[3 * nW + i];
+            fresh[i] = j;
+            wflag[j] = 1;
+        }
+    }
+}
+
 __global__ void k_set_flags(const int *__restrict__ idx, int cnt, uint8_t *__restrict__ f, uint8_t val) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < cnt) f[idx[i]] = val;
