@@ -72,3 +72,33 @@ def test_host_resident_pinned_by_caller_and_alignment():
     with pytest.raises(bl.BLError) as e:
         bl.Design(X, 120, host_resident=True)
     assert e.value.code == bl.BL_ERR_ARG
+
+
+def test_host_resident_sharded_is_G_invariant():
+    """Column shards that each stay in host memory (loopback transport, 2 ranks) give the
+    single-GPU path bitwise."""
+    import os
+    import threading
+    inst = synth.random_instance(130, 700, dtype=np.float32, seed=47, kind="corr", n_true=10)
+    Xh = np.ascontiguousarray(inst.host_X())
+    ref_d = bl.Design(Xh, inst.n)
+    lams = synth.lambda_grid(ref_d.lambda_max(inst.y), 25, 0.1)
+    ref = ref_d.fit_path(inst.y, lams, tol=1e-9)
+    G, key = 2, os.urandom(128)
+    out, errs = [None] * G, []
+
+    def work(r):
+        try:
+            j0, j1 = bl.shard_range(inst.p, G, r)
+            shard = np.ascontiguousarray(Xh[j0:j1])
+            d = bl.Design(shard, inst.n, dist=bl.loopback_dist(r, G, (j0, j1), inst.p, key), host_resident=True)
+            out[r] = d.fit_path(inst.y, lams, tol=1e-9)
+            d.free()
+        except Exception as e:  # noqa: BLE001
+            errs.append((r, e))
+    th = [threading.Thread(target=work, args=(r,)) for r in range(G)]
+    [t.start() for t in th]
+    [t.join(timeout=600) for t in th]
+    assert not errs, errs
+    for r in range(G):
+        same_path(out[r], ref)
