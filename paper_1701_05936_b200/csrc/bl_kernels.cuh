@@ -128,8 +128,16 @@ __global__ void __launch_bounds__(256) k_colstats(const T *__restrict__ X, int64
         const T *col = X + j * ld;
         if constexpr (sizeof(T) == 1) {
             long long s1 = 0, s2 = 0;
+            int a1 = 0, a2 = 0;          // full 16-row chunks: 4-way byte dot products (dp4a), exact in int32
             for (int i = lane * V; i < n; i += 32 * V) {
                 int4 raw = __ldg(reinterpret_cast<const int4 *>(col + i));
+                if (!MASK && i + V <= n) {
+                    a1 = __dp4a(raw.x, 0x01010101, a1); a2 = __dp4a(raw.x, raw.x, a2);
+                    a1 = __dp4a(raw.y, 0x01010101, a1); a2 = __dp4a(raw.y, raw.y, a2);
+                    a1 = __dp4a(raw.z, 0x01010101, a1); a2 = __dp4a(raw.z, raw.z, a2);
+                    a1 = __dp4a(raw.w, 0x01010101, a1); a2 = __dp4a(raw.w, raw.w, a2);
+                    continue;
+                }
                 const int8_t *xb = reinterpret_cast<const int8_t *>(&raw);
 #pragma unroll
                 for (int e = 0; e < V; e++) {
@@ -139,6 +147,8 @@ __global__ void __launch_bounds__(256) k_colstats(const T *__restrict__ X, int64
                     s2 += x * x;
                 }
             }
+            s1 += a1;                    // per lane <= 512 rows x 127^2 < 2^31 (n <= 16384)
+            s2 += a2;
             s1 = warp_sum_ll(s1);
             s2 = warp_sum_ll(s2);
             if (lane == 0) {
