@@ -2619,18 +2619,32 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
     // positions M = (I + inv N^T)^-1 (blocks split over the CTAs' warps; scratch =
     // each CTA's first 8 KB buffers)
     auto build_A = [&](int na) {
-        for (int i = rank; i < na; i += R) {
-            const int64_t rs = (int64_t)__ldcg(wk.act + i) * ldG;
-            for (int j0 = t; j0 < na; j0 += 4 * T_) {
-                double v[4];
+        // G_AA gather: each thread's column slots are read once per 4 T_ columns, then 8 rows
+        // per step are gathered with 32 independent loads in flight (the row-at-a-time loop
+        // paid two dependent L2 round trips per row)
+        constexpr int RB = 4;
+        for (int jb = 0; jb < na; jb += 4 * T_) {
+            int aj[4];
 #pragma unroll
-                for (int k = 0; k < 4; k++) {
-                    const int j = min(j0 + k * T_, na - 1);
-                    v[k] = __ldg(a.G + rs + __ldcg(wk.act + j));
+            for (int k = 0; k < 4; k++) aj[k] = __ldcg(wk.act + min(jb + t + k * T_, na - 1));
+            for (int i0 = rank; i0 < na; i0 += RB * R) {
+                int64_t rs[RB];
+#pragma unroll
+                for (int r = 0; r < RB; r++) rs[r] = (int64_t)__ldcg(wk.act + min(i0 + r * R, na - 1)) * ldG;
+                double v[RB][4];
+#pragma unroll
+                for (int r = 0; r < RB; r++)
+#pragma unroll
+                    for (int k = 0; k < 4; k++) v[r][k] = __ldg(a.G + rs[r] + aj[k]);
+#pragma unroll
+                for (int r = 0; r < RB; r++) {
+                    const int i = i0 + r * R;
+                    if (i < na) {
+#pragma unroll
+                        for (int k = 0; k < 4; k++)
+                            if (jb + t + k * T_ < na) a.GA[(int64_t)i * ldG + jb + t + k * T_] = v[r][k];
+                    }
                 }
-#pragma unroll
-                for (int k = 0; k < 4; k++)
-                    if (j0 + k * T_ < na) a.GA[(int64_t)i * ldG + j0 + k * T_] = v[k];
             }
         }
         __threadfence();
@@ -2640,10 +2654,15 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
             double(*N)[32] = Gd[wid];
             for (int q = rank * nw + wid; q < nblk; q += nw * R) {
                 const int b0 = 32 * q, nb = min(32, na - b0);
-                for (int e = lane; e < 1024; e += 32) {
-                    const int p = e >> 5, b = e & 31;
-                    N[p][b] = (b > p && b < nb) ? (a.idv ? a.idv[__ldcg(wk.act + b0 + b)] : inv_den0) *
-                                                      __ldcg(a.GA + (int64_t)(b0 + p) * ldG + b0 + b) : 0.0;
+                {                                   // lane b loads column b of the block: 32 loads in flight
+                    const int b = lane;
+                    const double sc = b < nb ? (a.idv ? a.idv[__ldcg(wk.act + b0 + b)] : inv_den0) : 0.0;
+                    double col[32];
+#pragma unroll
+                    for (int p = 0; p < 32; p++)
+                        col[p] = (b > p && b < nb) ? __ldcg(a.GA + (int64_t)(b0 + p) * ldG + b0 + b) : 0.0;
+#pragma unroll
+                    for (int p = 0; p < 32; p++) N[p][b] = sc * col[p];
                 }
                 __syncwarp();
                 double x[32];
