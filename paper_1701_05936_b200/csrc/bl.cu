@@ -1637,6 +1637,11 @@ struct PathRun {
     std::vector<int> strong_next;
     bl_status status = BL_OK;
     int bgrid = 1, use_bedpp = 0;
+    // once every live column is safe (BEDPP keeps all below ~0.5 lambda_max; it only keeps more
+    // as lambda falls), the flags are constant: one k_bedpp pass without the rule sets them and
+    // later lambdas skip the kernel (keeping extra columns is always safe: the KKT check covers them)
+    int flags_const = 0;          // 1: flags hold "safe now and next" for every live column
+    bool bedpp_skipped = false;
     int k = -1, rounds = 0, passes = 0;
     int64_t scanned = 0, nstrong_k = 0, nsafe_k = 0;
 
@@ -1717,10 +1722,14 @@ struct PathRun {
         lam_next = k + 1 < K ? lambda[k + 1] : -1.0;
         if (screen != BL_SCREEN_NONE) {
             CK(cudaMemsetAsync(pp->st, 0, 4 * sizeof(int), st));   // counters only: sum r / rss persist
-            k_bedpp<<<bgrid, 256, 0, st>>>(d->p, pp->s, pp->a, pp->b, pp->ps, alpha, lam, lam_next, use_bedpp,
-                                           pp->flags, use_bedpp ? pp->scope : nullptr, pp->st);
-            CKL();
-            pp->launches++;
+            bedpp_skipped = !use_bedpp && flags_const && !first;
+            if (!bedpp_skipped) {
+                k_bedpp<<<bgrid, 256, 0, st>>>(d->p, pp->s, pp->a, pp->b, pp->ps, alpha, lam, lam_next, use_bedpp,
+                                               pp->flags, use_bedpp ? pp->scope : nullptr, pp->st);
+                CKL();
+                pp->launches++;
+                if (!use_bedpp && lam_next > 0.0) flags_const = 1;
+            }
             if (first) {
                 // strong set at the first solved lambda from the null solution z = a/n (a6)
                 const double lp = std::min(lam_prev, pp->hps.lmax);
@@ -1796,11 +1805,12 @@ struct PathRun {
             nscope += cnt[4 * r + 2];
             nsafe += cnt[4 * r + 3];
         }
-        nsafe_k = nsafe;
+        nsafe_k = bedpp_skipped ? (int64_t)pp->hps.n_live : nsafe;
         const int64_t round_cols = (use_bedpp && !dense) ? nscope : pp->hps.n_live;
         scanned += round_cols;
         if (!dense && pp->scan_full.size() < pp->ev_scan.size())   // classify the timed scan launch of this round
             pp->scan_full.push_back(round_cols == pp->hps.n_live ? (use_bedpp ? (int64_t)pp->hst->nscope : pp->p) : -1);
+        if (use_bedpp && nsafe == pp->hps.n_live) use_bedpp = 0;   // BEDPP keeps everything from here on
         if (pp->hst->cd_status) { status = BL_ERR_CONVERGENCE; return -1; }
         if (nviol > 0) {
             if (++rounds > max_rounds) {
