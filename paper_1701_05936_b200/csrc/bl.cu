@@ -1399,11 +1399,9 @@ void launch_resid_t(bl_prep *pp, int nW) {
                                                               v.c, v.s, part);
     CKL();
     k_resid_apply<M><<<nb, 256, 0, pp->stream>>>(part, nch, d->ld, (int)d->n, M ? pp->mask : nullptr, pp->rfull,
-                                                pp->rscan, pp->rpart);
+                                                pp->rscan, pp->rpart, pp->st);
     CKL();
-    k_resid_finish<<<1, 32, 0, pp->stream>>>(pp->rpart, nb, pp->st);
-    CKL();
-    pp->launches += 3;
+    pp->launches += 2;
 }
 
 bool use_gram(bl_prep *pp, int nW) {

@@ -47,6 +47,7 @@ struct RoundStatus {
     long long cd_dbg[8];               // Gram CD sub-phase cycles (micro-benchmarks only)
     double b0;                         // logistic path: intercept on the standardised scale (in/out)
     int outer, irls_done;              // logistic path: IRLS iterations of the last solve; converged flag
+    unsigned int blk_done, pad3;       // k_resid_apply's block counter (the last block reduces; self-resetting)
 };
 
 // ---------------------------------------------------------------- small helpers
@@ -2980,7 +2981,8 @@ __global__ void __launch_bounds__(256) k_resid_part(const T *__restrict__ X, int
 template <bool MASK>
 __global__ void __launch_bounds__(256) k_resid_apply(const double *__restrict__ part, int nchunk, int64_t ld, int n,
                                                      const uint8_t *__restrict__ mask, double *__restrict__ r,
-                                                     double *__restrict__ r_scan, double *__restrict__ bpart) {
+                                                     double *__restrict__ r_scan, double *__restrict__ bpart,
+                                                     RoundStatus *st) {
     __shared__ double red[32];
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     double rs = 0.0, rr = 0.0;
@@ -2999,7 +3001,22 @@ __global__ void __launch_bounds__(256) k_resid_apply(const double *__restrict__ 
     }
     rs = block_sum(rs, red);
     rr = block_sum(rr, red);
-    if (threadIdx.x == 0) { bpart[2 * blockIdx.x] = rs; bpart[2 * blockIdx.x + 1] = rr; }
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        bpart[2 * blockIdx.x] = rs;
+        bpart[2 * blockIdx.x + 1] = rr;
+        __threadfence();
+        last = atomicAdd(&st->blk_done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {       // the last block: sum r and ||r||^2 in a fixed block order
+        __threadfence();
+        double s1 = 0.0, s2 = 0.0;
+        for (int b = 0; b < (int)gridDim.x; b++) { s1 += __ldcg(bpart + 2 * b); s2 += __ldcg(bpart + 2 * b + 1); }
+        st->sumr = s1;
+        st->rss = s2;
+        st->blk_done = 0;
+    }
 }
 
 __global__ void k_resid_finish(const double *__restrict__ part, int nb, RoundStatus *st) {
