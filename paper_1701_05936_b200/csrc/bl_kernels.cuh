@@ -2785,14 +2785,14 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
                 ctl[ph][0] = cmd_catch; ctl[ph][1] = ncat; ctl[ph][2] = cmd_build;
                 ctl[ph][3] = mode; ctl[ph][4] = len; ctl[ph][5] = reload;
             }
-            __threadfence();
+            // cl.sync()'s arrive.release / wait.acquire orders these writes for the cluster
         }
         cl.sync();
         const int *rc = cl.map_shared_rank(&ctl[ph][0], 0);
         const int cmd_catch = rc[0], ncat = rc[1], cmd_build = rc[2], mode = rc[3], len = rc[4], reload = rc[5];
         if (!leader_cta && (reload || mode < 0)) owner_store();
         if (mode < 0) break;
-        if (reload) { __threadfence(); cl.sync(); }
+        if (reload) cl.sync();                              // owners' stores ordered by the release barrier
         if (cmd_catch) {
             const long long c0 = clock64();
             catch_up(ncat);
