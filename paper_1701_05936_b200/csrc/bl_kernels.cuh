@@ -2648,7 +2648,7 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
                 }
             }
         }
-        __threadfence();
+        // (cl.sync: release / acquire at cluster scope)
         cl.sync();
         const int nblk = (na + 31) / 32;
         {
@@ -2685,7 +2685,7 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
                 __syncwarp();
             }
         }
-        __threadfence();
+        // (cl.sync: release / acquire at cluster scope)
         cl.sync();
     };
 
@@ -2713,7 +2713,7 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
                 if (k + 1 < nW && !__ldcg(wk.inA + k + 1)) wk.g[k + 1] -= gy;
             }
         }
-        __threadfence();
+        // (cl.sync: release / acquire at cluster scope)
         cl.sync();
     };
 
