@@ -486,3 +486,30 @@ def test_large_working_set_switches_cd_flavour():
     op = oracle.fit_path(inst, inst.y, lams, alpha=a, tol=1e-11, nnz_cap=9000 * 15)
     assert np.count_nonzero(op.beta[:, -1]) > 4096          # the working set outgrew the Gram CD
     compare_path(inst, gp, op, a)
+
+
+def test_concurrent_fits_on_one_design():
+    """S:90 / S:341: concurrent fits on one design (the workspace pool and the library's block
+    cache under contention) give exactly the sequential results."""
+    import threading
+    inst = synth.random_instance(140, 900, dtype=np.float32, seed=61, kind="corr", n_true=10)
+    d = design(inst)
+    lams = synth.lambda_grid(d.lambda_max(inst.y), 30, 0.1)
+    ys = [inst.y, inst.y[::-1].copy(), inst.y * 0.5 + 1.0, np.roll(inst.y, 7)]
+    ref = [d.fit_path(y, lams, tol=1e-9) for y in ys]
+    out, errs = [None] * len(ys), []
+
+    def work(i):
+        try:
+            for _ in range(3):
+                out[i] = d.fit_path(ys[i], lams, tol=1e-9)
+        except Exception as e:  # noqa: BLE001
+            errs.append((i, e))
+    th = [threading.Thread(target=work, args=(i,)) for i in range(len(ys))]
+    [t.start() for t in th]
+    [t.join(timeout=600) for t in th]
+    assert not errs, errs
+    for a, b in zip(out, ref):
+        np.testing.assert_array_equal(a.col_ptr, b.col_ptr)
+        np.testing.assert_array_equal(a.feat, b.feat)
+        np.testing.assert_array_equal(a.beta_std, b.beta_std)
