@@ -2270,8 +2270,7 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    __threadfence();
-    cl.sync();
+    cl.sync();                                              // release / acquire at cluster scope
 
     const long long clk0 = clock64();
     int passes = 0, status = 0;
