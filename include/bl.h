@@ -111,6 +111,10 @@ typedef struct {
     double full_scan_ms;       /* the subset of scan launches that covered every live column (|S_k| = p, */
     double full_scan_bytes;    /*   SURVEY 8(d) "full-scan only" GB/s); single fits only (0 in CV sums) */
     int64_t full_scan_launches;
+    int64_t cd_events[4];      /* Gram CD events: speculation retries, G_AA builds, catch-ups, full sweeps */
+    int64_t cd_sub[8];         /* Gram CD leader-warp sub-phase cycles: block prologue, active mat-vec,
+                                  forward substitution, publish, waits (stage + snapshot), next-stage wait,
+                                  link product, (unused) */
 } bl_perf;
 
 /* ---- design ------------------------------------------------------------------

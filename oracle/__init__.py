@@ -28,9 +28,10 @@ class OracleError(RuntimeError):
 
 
 def build(force: bool = False) -> str:
-    """Compile oracle.c -> liboracle.so (plain -O2, no fast-math, portable ISA)."""
+    """Compile oracle.c -> liboracle.so (plain -O2, no fast-math, portable ISA; OpenMP for
+    the optional host threads, set_threads)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-std=c99", "-fPIC", "-shared", "-o", _LIB, _SRC, "-lm"])
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-fopenmp", "-fPIC", "-shared", "-o", _LIB, _SRC, "-lm"])
     return _LIB
 
 
@@ -57,7 +58,24 @@ def _L():
         _lib.or_objective_binomial.argtypes = [P, I, I64, I64, I64, P, P, D, P, D, D, P]
         _lib.or_fit_path_binomial.argtypes = [P, I, I64, I64, I64, P, P, P, I, D, D, I, I, I64,
                                               P, P, P, P, P, P, P, P, P]
+        _lib.or_set_threads.argtypes = [I]
+        _lib.or_set_threads.restype = None
+        _lib.or_get_threads.restype = I
+        _lib.or_path_begin.argtypes = [P, I, I64, I64, I64, P, P, D, ctypes.POINTER(P)]
+        _lib.or_path_run.argtypes = [P, P, I, D, I, I, I64, P, P, P, P, P, P, P, P]
+        _lib.or_path_end.argtypes = [P]
+        _lib.or_path_end.restype = None
     return _lib
+
+
+def set_threads(t: int) -> None:
+    """Host threads of the oracle (1 = the pure serial oracle).  Results are bitwise
+    identical for every t (oracle.c: g_threads)."""
+    _L().or_set_threads(int(t))
+
+
+def get_threads() -> int:
+    return _L().or_get_threads()
 
 
 def _p(a):
@@ -208,6 +226,53 @@ def fit_path(X, y, lam, alpha=1.0, tol=1e-10, max_iter=100000, cycle_active=True
         sl = slice(col_ptr[k], col_ptr[k + 1])
         beta[idx[sl], k] = val[sl]
     return PathResult(lam, beta, a0, obj, passes, resid, nc.value, rc)
+
+
+class PathSession:
+    """A pathwise solve run in consecutive chunks of the lambda grid with warm starts
+    (or_path_begin / or_path_run / or_path_end): the chunks together are exactly
+    fit_path over the concatenated grid."""
+
+    def __init__(self, X, y, alpha=1.0, train=None):
+        buf, dt, n, p, ld = _design(X)
+        self._buf = buf                       # the C side reads X in place
+        self.n, self.p = n, p
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        m = _mask(train, n)
+        h = ctypes.c_void_p()
+        rc = _L().or_path_begin(_p(buf), dt, n, p, ld, _p(y), _p(m), alpha, ctypes.byref(h))
+        if rc:
+            raise OracleError(rc, "path_begin")
+        self.h = h
+
+    def run(self, lam, tol=1e-10, max_iter=100000, cycle_active=True, nnz_cap=None):
+        lam = np.ascontiguousarray(lam, dtype=np.float64)
+        K = lam.size
+        cap = nnz_cap or min(self.p * K, max(1, min(self.n, self.p) * K * 2 + 16))
+        col_ptr = np.zeros(K + 1, dtype=np.int64)
+        idx = np.empty(cap, dtype=np.int64); val = np.empty(cap)
+        a0 = np.empty(K); obj = np.empty(K); passes = np.empty(K, dtype=np.int32)
+        nc = ctypes.c_int()
+        rc = _L().or_path_run(self.h, _p(lam), K, tol, max_iter, int(cycle_active), cap, _p(col_ptr), _p(idx),
+                              _p(val), _p(a0), _p(obj), _p(passes), None, ctypes.byref(nc))
+        if rc:
+            raise OracleError(rc, "path_run")
+        beta = np.zeros((self.p, K))
+        for k in range(nc.value):
+            sl = slice(col_ptr[k], col_ptr[k + 1])
+            beta[idx[sl], k] = val[sl]
+        return PathResult(lam, beta, a0, obj, passes, None, nc.value, rc)
+
+    def close(self):
+        if getattr(self, "h", None):
+            _L().or_path_end(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def folds(n, K, seed):

@@ -33,6 +33,20 @@
 #include <stdlib.h>
 #include <string.h>
 
+/* Host threads.  1 = the pure serial oracle.  With T > 1
+ * only loops whose iterations are independent per column run in parallel (each
+ * column's dot product is still one thread's plain ascending-i loop), and the
+ * coordinate-descent full pass is block-speculative: the dot products of a block
+ * of columns are computed in parallel against the current residual and committed
+ * in index order; the first committed change ends the block (the rest are
+ * recomputed against the updated residual).  Every value is therefore computed
+ * by exactly the same arithmetic as the serial pass: the iterates are bitwise
+ * identical for every T (pinned by tests/test_oracle_pins.py). */
+static int g_threads = 1;
+void or_set_threads(int t) { g_threads = t < 1 ? 1 : t; }
+int or_get_threads(void) { return g_threads; }
+#define OR_PAR _Pragma("omp parallel for schedule(static) if(g_threads > 1) num_threads(g_threads)")
+
 enum { OR_OK = 0, OR_ERR_ARG = 1, OR_ERR_DEGENERATE = 2, OR_ERR_CONVERGENCE = 3 };
 enum { OR_F64 = 0, OR_F32 = 1, OR_I8 = 2 };
 
@@ -66,6 +80,7 @@ int or_column_stats(const void *X, int dt, int64_t n, int64_t p, int64_t ld,
     if (!X || n < 2 || p < 1 || ld < n || dt < 0 || dt > 2) return OR_ERR_ARG;
     int64_t nt = count_rows(train, n);
     if (nt < 2) return OR_ERR_ARG;
+    OR_PAR
     for (int64_t j = 0; j < p; j++) {
         double sum = 0.0;
         for (int64_t i = 0; i < n; i++)
@@ -138,11 +153,13 @@ int or_lambda_max(const void *X, int dt, int64_t n, int64_t p, int64_t ld,
     center_y(y, n, train, nt, yt);
     double best = -1.0;
     int64_t jb = -1;
-    for (int64_t j = 0; j < p; j++) {
-        if (s[j] == 0.0) continue;
-        double a = fabs(std_dot(X, dt, n, ld, j, c, s, train, yt));
-        if (a > best) { best = a; jb = j; }
-    }
+    double *av = malloc(sizeof(double) * p);
+    OR_PAR
+    for (int64_t j = 0; j < p; j++)
+        av[j] = s[j] == 0.0 ? -1.0 : fabs(std_dot(X, dt, n, ld, j, c, s, train, yt));
+    for (int64_t j = 0; j < p; j++)
+        if (s[j] != 0.0 && av[j] > best) { best = av[j]; jb = j; }
+    free(av);
     if (jb < 0 || best == 0.0) { rc = OR_ERR_DEGENERATE; goto done; }
     *lambda_max = best / ((double)nt * alpha);
     *jstar = jb;
@@ -161,6 +178,7 @@ int or_std_dots(const void *X, int dt, int64_t n, int64_t p, int64_t ld,
     int rc = or_column_stats(X, dt, n, p, ld, train, c, s);
     if (rc == OR_OK) {
         double nd = (double)count_rows(train, n);
+        OR_PAR
         for (int64_t j = 0; j < p; j++)
             z[j] = s[j] == 0.0 ? 0.0 : std_dot(X, dt, n, ld, j, c, s, train, v) / nd;
     }
@@ -183,12 +201,14 @@ int or_prep(const void *X, int dt, int64_t n, int64_t p, int64_t ld, const doubl
     center_y(y, n, train, nt, yt);
     int64_t js = -1;
     double best = -1.0;
-    for (int64_t j = 0; j < p; j++) {
+    OR_PAR
+    for (int64_t j = 0; j < p; j++)
         a[j] = s[j] == 0.0 ? 0.0 : std_dot(X, dt, n, ld, j, c, s, train, yt);
+    for (int64_t j = 0; j < p; j++)
         if (s[j] != 0.0 && fabs(a[j]) > best) { best = fabs(a[j]); js = j; }
-    }
     if (js < 0 || best == 0.0) { rc = OR_ERR_DEGENERATE; goto done; }
     for (int64_t i = 0; i < n; i++) xs[i] = in_rows(train, i) ? xstd(X, dt, ld, i, js, c, s) : 0.0;
+    OR_PAR
     for (int64_t j = 0; j < p; j++)
         b[j] = s[j] == 0.0 ? 0.0 : std_dot(X, dt, n, ld, j, c, s, train, xs);
     *jstar = js;
@@ -258,9 +278,13 @@ int or_kkt(const void *X, int dt, int64_t n, int64_t p, int64_t ld,
             if (in_rows(train, i)) r[i] -= xstd(X, dt, ld, i, j, c, s) * beta[j];
     }
     double zv = -INFINITY, nv = 0.0;
+    double *zz = malloc(sizeof(double) * p);
+    OR_PAR
+    for (int64_t j = 0; j < p; j++)
+        zz[j] = s[j] == 0.0 ? 0.0 : std_dot(X, dt, n, ld, j, c, s, train, r) / (double)nt;
     for (int64_t j = 0; j < p; j++) {
         if (s[j] == 0.0) { if (z) z[j] = 0.0; continue; }
-        double zj = std_dot(X, dt, n, ld, j, c, s, train, r) / (double)nt;
+        double zj = zz[j];
         if (z) z[j] = zj;
         if (beta[j] == 0.0) {
             double v = fabs(zj) - alpha * lambda;
@@ -271,6 +295,7 @@ int or_kkt(const void *X, int dt, int64_t n, int64_t p, int64_t ld,
             if (v > nv) nv = v;
         }
     }
+    free(zz);
     *zero_viol = zv;
     *nonzero_viol = nv;
 done:
@@ -308,10 +333,11 @@ int or_bedpp(const void *X, int dt, int64_t n, int64_t p, int64_t ld,
     for (int64_t i = 0; i < n; i++) Y2 += yt[i] * yt[i];
     int64_t js = -1;
     double best = -1.0;
-    for (int64_t j = 0; j < p; j++) {
+    OR_PAR
+    for (int64_t j = 0; j < p; j++)
         a[j] = s[j] == 0.0 ? 0.0 : std_dot(X, dt, n, ld, j, c, s, train, yt);
+    for (int64_t j = 0; j < p; j++)
         if (s[j] != 0.0 && fabs(a[j]) > best) { best = fabs(a[j]); js = j; }
-    }
     if (js < 0 || best == 0.0) { rc = OR_ERR_DEGENERATE; goto done; }
     for (int64_t i = 0; i < n; i++) xs[i] = in_rows(train, i) ? xstd(X, dt, ld, i, js, c, s) : 0.0;
     double nd = (double)nt;
@@ -326,6 +352,7 @@ int or_bedpp(const void *X, int dt, int64_t n, int64_t p, int64_t ld,
     double rad = m * Y2 - nd * nd * A * A;
     if (rad < 0.0) rad = 0.0;
     double rhs = 2.0 * nd * L * A - (A - L) * sqrt(rad);
+    OR_PAR
     for (int64_t j = 0; j < p; j++) {
         if (s[j] == 0.0) { discard[j] = 1; continue; }
         if (j == js) { discard[j] = 0; continue; }
@@ -344,12 +371,14 @@ done:
 /* One coordinate update of naive cyclic CD:
  *   z = x~_j^T r / n + b_j ;  b' = S(z, lambda alpha) / (1 + lambda (1 - alpha))
  *   r <- r - (b' - b_j) x~_j
+ * split into the dot product x~_j^T r (std_dot) and the commit below, so that the
+ * serial and the block-speculative passes run the same arithmetic.
  * Returns |b' - b_j|. */
-static double cd_update(const void *X, int dt, int64_t n, int64_t ld, int64_t j,
+static double cd_commit(const void *X, int dt, int64_t n, int64_t ld, int64_t j,
                         const double *c, const double *s, const uint8_t *train, double nd,
-                        double lambda, double alpha, double *beta, double *r)
+                        double lambda, double alpha, double dot, double *beta, double *r)
 {
-    double z = std_dot(X, dt, n, ld, j, c, s, train, r) / nd + beta[j];
+    double z = dot / nd + beta[j];
     double bn = soft(z, lambda * alpha) / (1.0 + lambda * (1.0 - alpha));
     double d = bn - beta[j];
     if (d != 0.0) {
@@ -360,7 +389,123 @@ static double cd_update(const void *X, int dt, int64_t n, int64_t ld, int64_t j,
     return fabs(d);
 }
 
-/* Pathwise coordinate descent, warm starts, no screening.
+static double cd_update(const void *X, int dt, int64_t n, int64_t ld, int64_t j,
+                        const double *c, const double *s, const uint8_t *train, double nd,
+                        double lambda, double alpha, double *beta, double *r)
+{
+    return cd_commit(X, dt, n, ld, j, c, s, train, nd, lambda, alpha,
+                     std_dot(X, dt, n, ld, j, c, s, train, r), beta, r);
+}
+
+enum { OR_SPEC_MAX = 65536 };   /* largest speculative block (columns) */
+
+/* One full pass over every non-constant column, ascending j.  g_threads > 1:
+ * block-speculative -- the dot products of columns j..j+B-1 are computed in
+ * parallel against the current r, then committed in index order; after the first
+ * committed change the block ends and the next one starts at the following
+ * column (so every dot product a commit uses was taken against exactly the
+ * residual the serial pass would use).  B doubles after a change-free block and
+ * falls back to 8 T after a change. */
+static void full_pass(const void *X, int dt, int64_t n, int64_t p, int64_t ld,
+                      const double *c, const double *s, const uint8_t *train, double nd,
+                      double lam, double alpha, double *beta, double *r, double *dot,
+                      double *dmax_out, double *bmax_out)
+{
+    double dmax = 0.0, bmax = 0.0;
+    if (g_threads <= 1) {
+        for (int64_t j = 0; j < p; j++) {
+            if (s[j] == 0.0) continue;
+            double d = cd_update(X, dt, n, ld, j, c, s, train, nd, lam, alpha, beta, r);
+            if (d > dmax) dmax = d;
+            if (fabs(beta[j]) > bmax) bmax = fabs(beta[j]);
+        }
+    } else {
+        const int64_t B0 = 8 * (int64_t)g_threads;
+        int64_t B = B0, j = 0;
+        while (j < p) {
+            const int64_t j0 = j, je = j + B < p ? j + B : p;
+            OR_PAR
+            for (int64_t q = j0; q < je; q++)
+                dot[q - j0] = s[q] == 0.0 ? 0.0 : std_dot(X, dt, n, ld, q, c, s, train, r);
+            int changed = 0;
+            while (j < je) {
+                const int64_t jj = j++;
+                if (s[jj] == 0.0) continue;
+                double d = cd_commit(X, dt, n, ld, jj, c, s, train, nd, lam, alpha, dot[jj - j0], beta, r);
+                if (d > dmax) dmax = d;
+                if (fabs(beta[jj]) > bmax) bmax = fabs(beta[jj]);
+                if (d != 0.0) { changed = 1; break; }
+            }
+            B = changed ? B0 : (2 * B <= OR_SPEC_MAX ? 2 * B : OR_SPEC_MAX);
+        }
+    }
+    *dmax_out = dmax;
+    *bmax_out = bmax;
+}
+
+/* State of one pathwise solve (warm starts carry beta and r from one lambda to
+ * the next).  or_fit_path = or_path_begin + or_path_run over the whole grid +
+ * or_path_end; bench.py's reference arm runs the grid in consecutive chunks. */
+typedef struct {
+    const void *X;
+    int dt;
+    int64_t n, p, ld, nt;
+    uint8_t *train;          /* copy, or NULL */
+    double *y;               /* copy */
+    double alpha, nd, ybar, lmax, sigma_y;
+    double *c, *s, *beta, *r, *dot;
+} or_path_t;
+
+void or_path_end(or_path_t *st)
+{
+    if (!st) return;
+    free(st->train); free(st->y); free(st->c); free(st->s); free(st->beta); free(st->r); free(st->dot);
+    free(st);
+}
+
+/* Column stats, y~ (r = y~, beta = 0) and lambda_max of the fit (SURVEY 8(c.2)
+ * steps 1-5). */
+int or_path_begin(const void *X, int dt, int64_t n, int64_t p, int64_t ld,
+                  const double *y, const uint8_t *train, double alpha, or_path_t **out)
+{
+    *out = NULL;
+    if (!X || !y || !(alpha > 0.0 && alpha <= 1.0)) return OR_ERR_ARG;
+    or_path_t *st = calloc(1, sizeof(or_path_t));
+    st->X = X; st->dt = dt; st->n = n; st->p = p; st->ld = ld; st->alpha = alpha;
+    st->c = malloc(sizeof(double) * p); st->s = malloc(sizeof(double) * p);
+    st->beta = calloc(p, sizeof(double)); st->r = malloc(sizeof(double) * n);
+    st->dot = malloc(sizeof(double) * OR_SPEC_MAX);
+    st->y = malloc(sizeof(double) * n);
+    memcpy(st->y, y, sizeof(double) * n);
+    if (train) { st->train = malloc(n); memcpy(st->train, train, n); }
+    int rc = or_column_stats(X, dt, n, p, ld, st->train, st->c, st->s);
+    if (rc) { or_path_end(st); return rc; }
+    st->nt = count_rows(st->train, n);
+    st->nd = (double)st->nt;
+    st->ybar = center_y(st->y, n, st->train, st->nt, st->r);
+    double yy = 0.0, lmax = 0.0;
+    int any = 0;
+    for (int64_t i = 0; i < n; i++) yy += st->r[i] * st->r[i];
+    double *av = malloc(sizeof(double) * p);
+    OR_PAR
+    for (int64_t j = 0; j < p; j++)
+        av[j] = st->s[j] == 0.0 ? 0.0
+                                : fabs(std_dot(X, dt, n, ld, j, st->c, st->s, st->train, st->r)) / (st->nd * alpha);
+    for (int64_t j = 0; j < p; j++) {
+        if (st->s[j] == 0.0) continue;
+        any = 1;
+        if (av[j] > lmax) lmax = av[j];
+    }
+    free(av);
+    if (yy == 0.0 || !any || lmax == 0.0) { or_path_end(st); return OR_ERR_DEGENERATE; }
+    st->lmax = lmax;
+    st->sigma_y = sqrt(yy / st->nd);
+    *out = st;
+    return OR_OK;
+}
+
+/* Pathwise coordinate descent, warm starts, no screening,
+ * over lambda[0..nlam) continuing from the state's beta and r.
  *
  * Convergence (Q6): a pass converges when max_j |delta beta_j| <= tol * max_j |beta_j|
  * (or falls below the fp64 noise floor 1e-13 (alpha lambda + sd(y~))).
@@ -370,7 +515,7 @@ static double cd_update(const void *X, int dt, int64_t n, int64_t ld, int64_t j,
  * pass converges (so this accelerates, it never screens).
  * max_iter (Q7) counts passes (full and active) per lambda.
  *
- * Outputs (caller-owned):
+ * Outputs (caller-owned), k indexing this call's lambdas:
  *   col_ptr[nlam+1], idx[nnz_cap], beta[nnz_cap]  sparse standardised beta per lambda
  *   a0[nlam]      intercept on the original scale: ybar - sum_j beta_j c_j / s_j (Q4)
  *   obj[nlam]     objective Q at the returned beta (running residual)
@@ -379,43 +524,27 @@ static double cd_update(const void *X, int dt, int64_t n, int64_t ld, int64_t j,
  *                 the training subset get their held-out residual), column k = lambda_k.
  *   n_converged   number of lambdas solved before an error.
  */
-int or_fit_path(const void *X, int dt, int64_t n, int64_t p, int64_t ld,
-                const double *y, const uint8_t *train,
-                const double *lambda, int nlam, double alpha, double tol, int max_iter,
+int or_path_run(or_path_t *st, const double *lambda, int nlam, double tol, int max_iter,
                 int cycle_active, int64_t nnz_cap,
                 int64_t *col_ptr, int64_t *idx, double *beta_out,
                 double *a0, double *obj, int32_t *passes, double *resid, int *n_converged)
 {
-    if (!X || !y || !lambda || nlam < 1 || !(alpha > 0.0 && alpha <= 1.0) || !(tol > 0.0) ||
-        max_iter < 1)
-        return OR_ERR_ARG;
+    if (n_converged) *n_converged = 0;
+    if (!st || !lambda || nlam < 1 || !(tol > 0.0) || max_iter < 1) return OR_ERR_ARG;
     for (int k = 0; k < nlam; k++) {
         if (!(lambda[k] > 0.0)) return OR_ERR_ARG;
         if (k > 0 && !(lambda[k] < lambda[k - 1])) return OR_ERR_ARG;
     }
-    double *c = malloc(sizeof(double) * p), *s = malloc(sizeof(double) * p);
-    double *beta = calloc(p, sizeof(double)), *r = malloc(sizeof(double) * n);
-    int rc = or_column_stats(X, dt, n, p, ld, train, c, s);
+    const void *X = st->X;
+    const int dt = st->dt;
+    const int64_t n = st->n, p = st->p, ld = st->ld;
+    const uint8_t *train = st->train;
+    const double *c = st->c, *s = st->s, *y = st->y;
+    double *beta = st->beta, *r = st->r;
+    const double alpha = st->alpha, nd = st->nd, ybar = st->ybar, lmax = st->lmax;
+    int rc = OR_OK;
     int64_t nnz = 0;
-    if (n_converged) *n_converged = 0;
     col_ptr[0] = 0;
-    if (rc) goto done;
-    int64_t nt = count_rows(train, n);
-    double nd = (double)nt;
-    double ybar = center_y(y, n, train, nt, r);
-    double yy = 0.0, lmax = 0.0;
-    {
-        int any = 0;
-        for (int64_t i = 0; i < n; i++) yy += r[i] * r[i];
-        for (int64_t j = 0; j < p; j++) {
-            if (s[j] == 0.0) continue;
-            any = 1;
-            double a = fabs(std_dot(X, dt, n, ld, j, c, s, train, r)) / (nd * alpha);
-            if (a > lmax) lmax = a;
-        }
-        if (yy == 0.0 || !any || lmax == 0.0) { rc = OR_ERR_DEGENERATE; goto done; }
-    }
-    double sigma_y = sqrt(yy / nd);
     for (int k = 0; k < nlam; k++) {
         double lam = lambda[k];
         int np_ = 0;
@@ -426,7 +555,7 @@ int or_fit_path(const void *X, int dt, int64_t n, int64_t p, int64_t ld,
         int snap = lam >= lmax * (1.0 - 1e-12);
         /* Q6 noise floor: coefficient changes below 1e-13 (alpha lambda + sd(y~))
          * are fp64 rounding of z, not progress. */
-        double floor_ = 1e-13 * (alpha * lam + sigma_y);
+        double floor_ = 1e-13 * (alpha * lam + st->sigma_y);
         for (; !snap;) {
             /* optional active cycling (acceleration only) */
             if (cycle_active) {
@@ -446,13 +575,8 @@ int or_fit_path(const void *X, int dt, int64_t n, int64_t p, int64_t ld,
                 }
             }
             /* full pass over every non-constant column, ascending j */
-            double dmax = 0.0, bmax = 0.0;
-            for (int64_t j = 0; j < p; j++) {
-                if (s[j] == 0.0) continue;
-                double d = cd_update(X, dt, n, ld, j, c, s, train, nd, lam, alpha, beta, r);
-                if (d > dmax) dmax = d;
-                if (fabs(beta[j]) > bmax) bmax = fabs(beta[j]);
-            }
+            double dmax, bmax;
+            full_pass(X, dt, n, p, ld, c, s, train, nd, lam, alpha, beta, r, st->dot, &dmax, &bmax);
             if (++np_ > max_iter) { rc = OR_ERR_CONVERGENCE; goto done; }
             if (dmax <= tol * bmax || dmax <= floor_) break;
         }
@@ -487,7 +611,32 @@ int or_fit_path(const void *X, int dt, int64_t n, int64_t p, int64_t ld,
         if (n_converged) *n_converged = k + 1;
     }
 done:
-    free(c); free(s); free(beta); free(r);
+    return rc;
+}
+
+/* The whole grid in one call (the path of SURVEY 8(c.2)). */
+int or_fit_path(const void *X, int dt, int64_t n, int64_t p, int64_t ld,
+                const double *y, const uint8_t *train,
+                const double *lambda, int nlam, double alpha, double tol, int max_iter,
+                int cycle_active, int64_t nnz_cap,
+                int64_t *col_ptr, int64_t *idx, double *beta_out,
+                double *a0, double *obj, int32_t *passes, double *resid, int *n_converged)
+{
+    if (n_converged) *n_converged = 0;
+    if (!X || !y || !lambda || nlam < 1 || !(alpha > 0.0 && alpha <= 1.0) || !(tol > 0.0) ||
+        max_iter < 1)
+        return OR_ERR_ARG;
+    for (int k = 0; k < nlam; k++) {
+        if (!(lambda[k] > 0.0)) return OR_ERR_ARG;
+        if (k > 0 && !(lambda[k] < lambda[k - 1])) return OR_ERR_ARG;
+    }
+    col_ptr[0] = 0;
+    or_path_t *st = NULL;
+    int rc = or_path_begin(X, dt, n, p, ld, y, train, alpha, &st);
+    if (rc) return rc;
+    rc = or_path_run(st, lambda, nlam, tol, max_iter, cycle_active, nnz_cap, col_ptr, idx, beta_out,
+                     a0, obj, passes, resid, n_converged);
+    or_path_end(st);
     return rc;
 }
 
@@ -721,6 +870,7 @@ int or_fit_path_binomial(const void *X, int dt, int64_t n, int64_t p, int64_t ld
                 e[i] = (y[i] - pi) / wi;           /* zr_i - eta_i */
                 sw += wi;
             }
+            OR_PAR
             for (int64_t j = 0; j < p; j++) {
                 v[j] = 0.0;
                 if (s[j] == 0.0) continue;

@@ -51,11 +51,14 @@ class bl_perf(ctypes.Structure):
                 ("wall_ms", ctypes.c_double), ("cd_visits", ctypes.c_int64), ("cd_updates", ctypes.c_int64),
                 ("cd_kernel_cycles", ctypes.c_int64), ("cd_prof", ctypes.c_int64 * 4),
                 ("full_scan_ms", ctypes.c_double), ("full_scan_bytes", ctypes.c_double),
-                ("full_scan_launches", ctypes.c_int64)]
+                ("full_scan_launches", ctypes.c_int64), ("cd_events", ctypes.c_int64 * 4),
+                ("cd_sub", ctypes.c_int64 * 8)]
 
     def as_dict(self):
         d = {f: getattr(self, f) for f, _ in self._fields_}
         d["cd_prof"] = list(self.cd_prof)
+        d["cd_events"] = list(self.cd_events)
+        d["cd_sub"] = list(self.cd_sub)
         return d
 
 

@@ -277,7 +277,8 @@ struct bl_path {
     std::vector<int32_t> outer;                          // logistic path: IRLS iterations (last solve) per lambda
     int family = 0;
     bl_perf perf;
-    int64_t cd_visits = 0, cd_updates = 0, cd_cycles = 0, cd_prof[4] = {0, 0, 0, 0};
+    int64_t cd_visits = 0, cd_updates = 0, cd_cycles = 0, cd_prof[4] = {0, 0, 0, 0}, cd_cnt[4] = {0, 0, 0, 0},
+            cd_dbg[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 };
 
 struct bl_cvres {
@@ -1781,6 +1782,8 @@ struct PathRun {
         out->cd_updates += pp->hst->cd_updates;
         out->cd_cycles += pp->hst->cd_cycles;
         for (int u = 0; u < 4; u++) out->cd_prof[u] += pp->hst->cd_prof[u];
+        for (int u = 0; u < 4; u++) out->cd_cnt[u] += pp->hst->cd_cnt[u];
+        for (int u = 0; u < 8; u++) out->cd_dbg[u] += pp->hst->cd_dbg[u];
     }
     // after the round's status reached pp->hst: 0 = lambda done, 1 = re-solve, -1 = error (status set).
     // `dense`: the scan covered every live column (batched CV scan).
@@ -1950,6 +1953,8 @@ void finish_perf(bl_prep *pp, bl_path *out, double wall_ms) {
     pf.cd_updates = out->cd_updates;
     pf.cd_kernel_cycles = out->cd_cycles;
     for (int u = 0; u < 4; u++) pf.cd_prof[u] = out->cd_prof[u];
+    for (int u = 0; u < 4; u++) pf.cd_events[u] = out->cd_cnt[u];
+    for (int u = 0; u < 8; u++) pf.cd_sub[u] = out->cd_dbg[u];
     pf.wall_ms = wall_ms;
 }
 
@@ -2193,6 +2198,8 @@ void add_perf(bl_cvres *cv, const bl_perf &p) {
     q.kernel_launches += p.kernel_launches; q.wall_ms = std::max(q.wall_ms, p.wall_ms);
     q.cd_visits += p.cd_visits; q.cd_updates += p.cd_updates; q.cd_kernel_cycles += p.cd_kernel_cycles;
     for (int u = 0; u < 4; u++) q.cd_prof[u] += p.cd_prof[u];
+    for (int u = 0; u < 4; u++) q.cd_events[u] += p.cd_events[u];
+    for (int u = 0; u < 8; u++) q.cd_sub[u] += p.cd_sub[u];
 }
 
 uint64_t splitmix64(uint64_t &state) {

@@ -1,0 +1,21 @@
+"""Gram CD leader-warp sub-phase breakdown (bl_perf.cd_sub / cd_events) per config."""
+import sys
+import numpy as np
+sys.path.insert(0, ".")
+import synth
+from paper_1701_05936_b200 import bl
+
+for cfg in sys.argv[1:]:
+    inst = synth.CONFIGS[cfg](device="cuda")
+    d = bl.Design(inst.X, inst.n)
+    lams = synth.lambda_grid(d.lambda_max(inst.y, inst.alpha), inst.nlam, inst.ratio)
+    d.fit_path(inst.y, lams, alpha=inst.alpha, tol=inst.tol)
+    gp = d.fit_path(inst.y, lams, alpha=inst.alpha, tol=inst.tol, profile=True)
+    pf = gp.perf
+    v = pf["cd_visits"]
+    blocks = v / 32
+    names = ["prologue", "active_matvec", "fwd_subst", "publish", "wait_stage+snap", "wait_next_stage", "link", "-"]
+    print(cfg, "cd_ms", round(pf["cd_ms"], 2), "visits", v, "cycles/visit", round(pf["cd_kernel_cycles"] / v, 1))
+    print("  events (retries, builds, catchups, full sweeps):", pf["cd_events"])
+    print("  phases per visit (lead, bulk, build, catch):", [round(x / v, 1) for x in pf["cd_prof"]])
+    print("  leader sub-phases per BLOCK:", {n: round(x / blocks, 1) for n, x in zip(names, pf["cd_sub"])})

@@ -489,3 +489,182 @@ def test_binomial_input_errors():
     with pytest.raises(oracle.OracleError) as e:
         oracle.fit_path_binomial(inst, np.ones(inst.n), lams)
     assert e.value.code == oracle.ERR_DEGENERATE
+
+
+# ------------------------------------------------------------------ identities (1)-(3)
+# or_std_dots / or_prep form every standardised value explicitly, element by element;
+# these pins check them against the paper's identity arithmetic (a different formula,
+# evaluated here in numpy) and against SPEC's printed identity examples.
+
+def _identity_stats(X, m):
+    """Column mean and population SD over the rows m (numpy; pins only)."""
+    Xm = X[m]
+    return Xm.mean(0), Xm.std(0)
+
+
+def test_identity_worked_examples():
+    """S:132-142 (identity (1) P:261, identity (2) P:262): x = (1,2,3), x' = (3,2,1):
+    x~'x~' = -3, x~'x~ = n; x~'y for y = x: 2 sqrt(3/2); y == 1: 0; r = 0: 0."""
+    xx = GOLD["identity_xx"][0]
+    xy, x1 = GOLD["identity_xy"]
+    X = np.column_stack([xx["xj"], xx["xk"]]).astype(np.float64)
+    y = np.array(xy["y"], dtype=np.float64)
+    o = oracle.prep(X, y)                          # a_0 = +2.449, a_1 = -2.449: tie -> j* = 0 (lowest)
+    assert o["jstar"] == 0
+    assert o["a"][0] == pytest.approx(xy["value"], rel=1e-15)
+    assert o["a"][1] == pytest.approx(-xy["value"], rel=1e-15)
+    assert o["b"][1] == pytest.approx(xx["value"], rel=1e-15)     # x~_1' x~_*  = -3
+    assert o["b"][0] == pytest.approx(3.0, rel=1e-15)             # x~_*' x~_*  = n
+    # or_std_dots returns x~'v / n_t
+    z = oracle.std_dots(X[:, :1], np.array(xy["y"], dtype=np.float64))
+    assert 3 * z[0] == pytest.approx(xy["value"], rel=1e-15)
+    z1 = oracle.std_dots(X[:, :1], np.array(x1["y"], dtype=np.float64))
+    assert abs(z1[0]) <= 1e-15 and x1["value"] == 0.0
+    assert np.all(oracle.std_dots(X, np.zeros(3)) == 0.0)
+
+
+def test_std_dots_and_prep_match_identities():
+    """over >= 1000 random small instances (fp64 / fp32 / int8, with and without a
+    row mask, with constant columns), the explicit standardisation of or_std_dots and
+    or_prep agrees to 1e-12 with the identities of P:261-263:
+      (3)  x~_j'v = (x_j'v - c_j sum v) / s_j            (v zero outside the rows)
+      (2)  a_j = x~_j'y~ = x_j'y~ / s_j                   (sum y~ = 0)
+      (1)  b_j = x~_j'x~_* = (x_j'x_* - n_t c_j c_*) / (s_j s_*),  b_j* = n_t
+    A dropped centring term, a missing 1/n_t under a mask or a sign slip fails here."""
+    rng = np.random.default_rng(2024)
+    count = 0
+    for it in range(1000):
+        n = int(rng.integers(3, 40))
+        p = int(rng.integers(1, 9))
+        dt = [np.float64, np.float32, np.int8][it % 3]
+        if dt == np.int8:
+            X = rng.integers(0, 3, (n, p)).astype(np.int8)
+        else:
+            X = (rng.standard_normal((n, p)) * rng.uniform(0.2, 5, p) + rng.uniform(-3, 3, p)).astype(dt)
+        if it % 7 == 0:
+            X[:, 0] = X[0, 0]                      # a constant column
+        m = np.ones(n, bool)
+        if it % 2:
+            m[rng.choice(n, int(rng.integers(0, n - 2)), replace=False)] = False
+        train = None if m.all() else m
+        Xd = X.astype(np.float64)
+        c, s = _identity_stats(Xd, m)
+        live = np.ptp(Xd[m], axis=0) > 0          # Q13: constant on the rows <=> s_j = 0 exactly
+        s = np.where(live, s, 0.0)
+        # identity (3) for a random v (zero outside the rows)
+        v = rng.standard_normal(n) * m
+        nt = m.sum()
+        z = oracle.std_dots(X, v, train)
+        zi = np.zeros(p)
+        zi[live] = (Xd[:, live].T @ v - c[live] * v.sum()) / (s[live] * nt)
+        scale = (np.abs(Xd - c) / np.where(live, s, 1.0)).T @ np.abs(v) / nt
+        assert np.all(np.abs(z - zi) <= 1e-12 * np.maximum(scale, 1e-300)), (it, z, zi)
+        assert np.all(z[~live] == 0.0)
+        # identities (2) and (1) through or_prep
+        y = rng.standard_normal(n) + 0.5 * Xd[:, -1]
+        yt = (y - y[m].mean()) * m
+        if not live.any() or not np.any(np.abs(Xd[:, live].T @ yt) > 0):
+            continue
+        o = oracle.prep(X, y, 1.0, train)
+        a = np.zeros(p)
+        a[live] = Xd[:, live].T @ yt / s[live]
+        sa = (np.abs(Xd - c) / np.where(live, s, 1.0)).T @ np.abs(yt)
+        assert np.all(np.abs(o["a"] - a) <= 1e-12 * np.maximum(sa, 1e-300)), (it, o["a"], a)
+        js = o["jstar"]
+        assert live[js] and np.abs(a[js]) >= np.abs(a[live]).max() * (1 - 1e-12)
+        b = np.zeros(p)
+        xs = Xd[m][:, js]
+        b[live] = (Xd[m][:, live].T @ xs - nt * c[live] * c[js]) / (s[live] * s[js])
+        assert np.all(np.abs(o["b"] - b) <= 1e-12 * nt * (1 + np.abs(c) / np.where(live, s, 1.0)) *
+                      (1 + abs(c[js]) / s[js])), (it, o["b"], b)
+        assert o["b"][js] == pytest.approx(nt, rel=1e-12)
+        assert o["lambda_max"] == pytest.approx(abs(a[js]) / nt, rel=1e-12)
+        count += 1
+    assert count >= 900
+
+
+# ------------------------------------------------------------------ KKT audit (S:221-222, S:329)
+
+@pytest.mark.parametrize("alpha,masked", [(1.0, False), (0.5, True)])
+def test_kkt_audit_pins(alpha, masked):
+    """or_kkt against closed forms and a numpy recomputation:
+      * the null solution at lambda_max has no violation (zv = 0 up to rounding, nv = 0),
+        and at 1.25 lambda_max zv = -0.25 alpha lambda_max exactly (S:221);
+      * at a converged solution zv, nv ~ 0; zeroing one active coordinate j0 (a
+        constructed violation) gives, in closed form,
+        |z_j0| - alpha lam = |b_j0| (1 + lam (1 - alpha))   (x~_j0'x~_j0 = n_t),
+        and zv / nv equal a numpy recomputation from r = y~ - X~ b (explicit) to 1e-12.
+    A stale residual, a missing 1/n_t or a sign slip in the nonzero test fails."""
+    inst = synth.random_instance(60, 25, seed=71, kind="corr", n_true=6)
+    n, p = inst.n, inst.p
+    m = np.ones(n, bool)
+    if masked:
+        m[::5] = False
+    train = None if not masked else m
+    lm, _ = oracle.lambda_max(inst, inst.y, alpha, train)
+    zv, nv = oracle.kkt(inst, inst.y, np.zeros(p), lm, alpha, train)
+    assert abs(zv) <= 1e-12 * alpha * lm and nv == 0.0
+    zv, nv = oracle.kkt(inst, inst.y, np.zeros(p), 1.25 * lm, alpha, train)
+    assert zv == pytest.approx(-0.25 * alpha * lm, rel=1e-11)
+    lam = 0.3 * lm
+    fit = oracle.fit_path(inst, inst.y, synth.lambda_grid(lm, 12, 0.3), alpha=alpha, tol=1e-13, train=train)
+    b = fit.beta[:, -1].copy()
+    zv, nv = oracle.kkt(inst, inst.y, b, lam, alpha, train)
+    assert zv <= 1e-10 and nv <= 1e-10
+    act = np.flatnonzero(b)
+    assert act.size >= 2
+    j0 = act[np.argmax(np.abs(b[act]))]
+    bp = b.copy()
+    bp[j0] = 0.0
+    zv2, nv2, z2 = oracle.kkt(inst, inst.y, bp, lam, alpha, train, want_z=True)
+    assert abs(z2[j0]) - alpha * lam == pytest.approx(abs(b[j0]) * (1 + lam * (1 - alpha)), rel=1e-8)
+    # numpy recomputation (explicit standardisation over the rows, population SD)
+    Xd = inst.dense()
+    Xs = (Xd - Xd[m].mean(0)) / Xd[m].std(0)
+    yt = (inst.y - inst.y[m].mean()) * m
+    r = (yt - Xs @ bp) * m
+    z = Xs.T @ r / m.sum()
+    zero = bp == 0
+    zv_np = np.max(np.abs(z[zero]) - alpha * lam)
+    nz = ~zero
+    nv_np = np.max(np.abs(z[nz] - alpha * lam * np.sign(bp[nz]) - lam * (1 - alpha) * bp[nz]))
+    assert zv2 == pytest.approx(zv_np, rel=1e-12, abs=1e-14)
+    assert nv2 == pytest.approx(nv_np, rel=1e-12, abs=1e-14)
+    np.testing.assert_allclose(z2, z, rtol=0, atol=1e-13)
+
+
+# ------------------------------------------------------------------ host threads (SURVEY 8(c.2) item 8)
+
+@pytest.mark.parametrize("kind,dtype,alpha", [("corr", np.float32, 1.0), ("iid", np.float64, 0.5),
+                                              ("geno", np.int8, 1.0)])
+def test_threaded_oracle_is_bitwise_serial(kind, dtype, alpha):
+    """The block-speculative threaded pass reproduces the serial iterates bitwise (beta,
+    passes, objective), and the chunked session (warm starts across calls) equals one
+    call over the whole grid."""
+    inst = synth.random_instance(90, 2500, dtype=dtype, seed=81, kind=kind, n_true=10, const_cols=3)
+    lm, _ = oracle.lambda_max(inst, inst.y, alpha)
+    lams = synth.lambda_grid(lm, 25, 0.05)
+    r = np.random.default_rng(3).standard_normal(inst.n)
+
+    def per_column():
+        return (oracle.column_stats(inst), oracle.std_dots(inst, r), oracle.prep(inst, inst.y, alpha),
+                oracle.lambda_max(inst, inst.y, alpha), oracle.bedpp_discard(inst, inst.y, alpha, 0.7 * lm),
+                oracle.kkt(inst, inst.y, np.zeros(inst.p), 0.5 * lm, alpha, want_z=True))
+    try:
+        oracle.set_threads(1)
+        a = oracle.fit_path(inst, inst.y, lams, alpha=alpha, tol=1e-10)
+        one = per_column()
+        oracle.set_threads(4)
+        b = oracle.fit_path(inst, inst.y, lams, alpha=alpha, tol=1e-10)
+        four = per_column()
+        s = oracle.PathSession(inst, inst.y, alpha)
+        parts = [s.run(lams[i:i + 6], tol=1e-10) for i in range(0, len(lams), 6)]
+        s.close()
+    finally:
+        oracle.set_threads(1)
+    assert np.array_equal(a.beta, b.beta) and np.array_equal(a.passes, b.passes) and np.array_equal(a.obj, b.obj)
+    assert np.array_equal(np.concatenate([q.beta for q in parts], axis=1), a.beta)
+    assert np.array_equal(np.concatenate([q.passes for q in parts]), a.passes)
+    flat = lambda t: [np.asarray(u) for v in t for u in (v.values() if isinstance(v, dict) else v if isinstance(v, tuple) else (v,))]
+    for u, v in zip(flat(one), flat(four)):
+        assert np.array_equal(u, v)
