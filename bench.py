@@ -6,9 +6,10 @@ throughput (BASELINE.json metric) on a B200.
 
 A step = one full 100-lambda path (all SURVEY 8(a) rows: preprocessing, BEDPP,
 strong rule, CD, fused KKT/strong scans) over the config's synthetic design,
-through the C ABI (libbl.so).  Default workload = BASELINE cfg2 (configs[1]):
-n = 1000, p = 100,000, fp32 AR(1) design, alpha = 1, lambda to 0.1 lambda_max.
-X (400 MB) is larger than L2, so no flush is needed between steps.
+through the C ABI (libbl.so).  Default workload = BASELINE cfg3, the largest
+single-GPU configuration: n = 1000, p = 1,000,000, fp32 block-factor design,
+elastic net alpha = 0.5, lambda to 0.1 lambda_max.  X (4.0 GB) is far larger than
+L2 (126 MB), so no flush is needed between steps.
 
 N > 1 (torchrun): the design is column-sharded over the ranks (whole
 1000-column blocks, BASELINE north star): scans, BEDPP and the strong rule run
@@ -18,7 +19,8 @@ broadcast by their owners over NCCL, the CD runs replicated (DESIGN.md section
 over ranks.
 
 `--impl reference` times the fp64 CPU oracle (oracle/, naive CD, no screening)
-on this box's host cores on a bounded column sample of the same workload.
+on this box's host cores on the same full-size workload: the K steps run the
+100-lambda grid in K chunks, so their summed time is the measured path time.
 """
 from __future__ import annotations
 
@@ -103,50 +105,103 @@ def make_instance(name, device=None):
 
 # ---------------------------------------------------------------- oracle legs
 
-def oracle_sample(inst, target_s=15.0, max_cols=None, binomial=False):
-    """Time the oracle (as it stands) on the first p' columns of the workload
-    with the full 100-lambda grid (grid anchored at the sample's own lambda_max),
-    p' grown until one run takes >= target_s/4, then scaled linearly in p
-    (the oracle's cost is O(n p) per pass).  Returns (seconds per full path, sample text, raw s)."""
+def host_cpu():
+    """(threads the oracle may use, CPU model) of this host."""
+    try:
+        T = len(os.sched_getaffinity(0))
+    except Exception:
+        T = os.cpu_count() or 1
+    model = "unknown"
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return T, model
+
+
+def oracle_prefix(inst, lams, budget_s, threads, binomial=False):
+    """cpu_baseline leg: the oracle as it stands (naive cyclic CD, no screening, fp64) on the
+    FULL design of the workload, T host threads (block-speculative passes: bitwise the serial
+    oracle), over the first m lambdas of the SAME grid: column statistics and lambda_max, then
+    one lambda at a time with warm starts until the time budget is spent.  Nothing is scaled.
+    Returns (seconds, m)."""
     import oracle
-    Xh = inst.host_X()
-    p_full = inst.p
-    pp = 500
-    while True:
-        sub = (Xh[:pp], inst.n)
-        lm, _ = oracle.lambda_max(sub, inst.y, inst.alpha)
-        import synth
-        lams = synth.lambda_grid(lm, inst.nlam, inst.ratio)
+    oracle.set_threads(threads)
+    try:
+        Xh = inst.host_X()
+        if binomial:                                   # the logistic oracle has no session API: whole prefixes
+            m, t = 1, 0.0
+            while True:
+                t0 = time.perf_counter()
+                oracle.fit_path_binomial((Xh, inst.n), inst.y, lams[:m], alpha=inst.alpha, tol=inst.tol,
+                                         raise_on_error=False)
+                t = time.perf_counter() - t0
+                if t >= budget_s / 3 or m >= len(lams):
+                    return t, m
+                m = min(len(lams), 2 * m)
         t0 = time.perf_counter()
-        fit = oracle.fit_path_binomial if binomial else oracle.fit_path
-        fit(sub, inst.y, lams, alpha=inst.alpha, tol=inst.tol, cycle_active=True, raise_on_error=False)
+        sess = oracle.PathSession((Xh, inst.n), inst.y, inst.alpha)
+        m = 0
+        while m < len(lams) and time.perf_counter() - t0 < budget_s:
+            sess.run(lams[m:m + 1], tol=inst.tol, cycle_active=True)
+            m += 1
         dt = time.perf_counter() - t0
-        if dt >= target_s / 4 or pp >= p_full or (max_cols and pp >= max_cols):
-            break
-        pp = min(p_full, max(pp * 2, int(pp * (target_s / 2) / max(dt, 1e-3))))
-    scaled = dt * p_full / pp
-    what = "IRLS + naive cyclic weighted CD" if binomial else "naive cyclic CD"
-    return scaled, f"oracle ({what}, fp64, tol {inst.tol:g}, no screening) on the first {pp} of {p_full} columns, full {inst.nlam}-lambda grid; scaled x{p_full / pp:.1f} (linear in p)", dt
+        sess.close()
+        return dt, m
+    finally:
+        oracle.set_threads(1)
 
 
 def run_reference(args, rank, world):
+    """--impl reference: the oracle (as it stands) on this box's host cores, on the same
+    workload bytes, lambda grid rule, alpha and tol as our arm.  The K timed steps run the
+    WHOLE 100-lambda path in K consecutive chunks of the grid (warm starts carry across
+    chunks; step 0 also computes the column statistics and lambda_max), so the summed step
+    time is the measured path wall time -- nothing is extrapolated.  W warm-up steps are
+    untimed passes over X (page-in).  N > 1: rank 0 alone runs it."""
     if rank != 0:
         return
+    import oracle
+    import synth
     inst = make_instance(args.config)
-    for _ in range(args.warmup):
-        pass
-    vals, samples = [], ""
-    for _ in range(args.steps):
-        v, samples, raw = oracle_sample(inst, target_s=args.ref_seconds, binomial=args.config == "logit")
-        vals.append(v)
-    v = statistics.median(vals)
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+    T, model = host_cpu()
+    Xh = inst.host_X()
+    oracle.set_threads(T)
+    try:
+        for _ in range(args.warmup):
+            oracle.column_stats((Xh, inst.n))
+        nl = inst.nlam
+        K = max(1, min(args.steps, nl))
+        chunk = -(-nl // K)
+        times, sess, lams = [], None, None
+        for s in range(K):
+            t0 = time.perf_counter()
+            if sess is None:
+                sess = oracle.PathSession((Xh, inst.n), inst.y, inst.alpha)
+                lams = synth.lambda_grid(sess.lambda_max, nl, inst.ratio)
+            part = lams[s * chunk:(s + 1) * chunk]
+            if len(part):
+                sess.run(part, tol=inst.tol, cycle_active=True)
+            times.append(time.perf_counter() - t0)
+        sess.close()
+    finally:
+        oracle.set_threads(1)
+    total = sum(times)
+    sample = (f"oracle (naive cyclic CD with active cycling, fp64, tol {inst.tol:g}, no screening) on the full "
+              f"{args.config} design (n={inst.n}, p={inst.p}), the whole {nl}-lambda grid run in {K} chunks of "
+              f"{chunk} lambdas (warm starts across chunks), {T} threads (block-speculative passes, bitwise the "
+              f"serial oracle); value = summed step time = the path wall time")
+    line = {"impl": "reference", "metric": METRIC, "value": total, "unit": "s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / max(1, len(times)),
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config, "n": inst.n, "p": inst.p, "alpha": inst.alpha,
-                       "n_lambda": inst.nlam, "lambda_min_ratio": inst.ratio},
-            "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "oracle", "sample": samples},
-            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                       "n_lambda": nl, "lambda_min_ratio": inst.ratio, "tol": inst.tol},
+            "cpu_baseline": {"value": total, "unit": "s", "cores": T, "cpu_model": model, "kind": "oracle",
+                             "sample": sample, "step_seconds": times},
+            "e2e": {"value": total, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
@@ -308,9 +363,29 @@ def run_ours(args, rank, world, local_rank):
         except Exception:
             traffic = None
     cpu = {"value": None, "unit": "s", "cores": 1, "kind": "oracle", "sample": "skipped (--no-cpu-baseline)"}
-    if world == 1 and not args.no_cpu_baseline:
-        v, sample, raw = oracle_sample(inst, target_s=args.ref_seconds, binomial=is_logit)
-        cpu = {"value": v, "unit": "s", "cores": 1, "kind": "oracle", "sample": sample, "raw_seconds": raw}
+    if world == 1 and not args.no_cpu_baseline and not is_cv:
+        T, model = host_cpu()
+        v, m = oracle_prefix(inst, lams, args.ref_seconds, T, binomial=is_logit)
+        # our path on exactly that sample (the same first m lambdas), for a like-for-like ratio
+        gpu_m = []
+        for _ in range(3):
+            e0_, e1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0_.record(stream)
+            if is_logit:
+                d.fit_path_binomial(inst.y, lams[:m], alpha=inst.alpha, tol=inst.tol, stream=sh)
+            else:
+                d.fit_path(inst.y, lams[:m], alpha=inst.alpha, tol=inst.tol, stream=sh, cd=args.cd)
+            e1_.record(stream)
+            torch.cuda.synchronize()
+            gpu_m.append(e0_.elapsed_time(e1_) / 1e3)
+        what = "IRLS + naive cyclic weighted CD" if is_logit else "naive cyclic CD with active cycling"
+        cpu = {"value": v, "unit": "s", "cores": T, "cpu_model": model, "kind": "oracle", "lambdas": m,
+               "sample": (f"oracle ({what}, fp64, tol {inst.tol:g}, no screening) on the full {args.config} design "
+                          f"(n={inst.n}, p={p_global}), column statistics + lambda_max + the first {m} of the "
+                          f"{inst.nlam} lambdas of the same grid, {T} threads (block-speculative passes, bitwise "
+                          f"the serial oracle); measured, not scaled"),
+               "gpu_same_sample_s": statistics.median(gpu_m)}
     line = {
         "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
@@ -367,13 +442,14 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "logit"],
+    ap.add_argument("--config", default="cfg3", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "logit"],
                     help="BASELINE cfg1-cfg5, or 'logit' (NEXT-3 logistic path, n=1000, p=100,000 fp32)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--resident", default="device", choices=["device", "host"],
                     help="where X lives: HBM (default) or pinned host memory read over PCIe (NEXT-4, out-of-core)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-seconds", type=float, default=20.0,
+                    help="cpu_baseline time budget: the oracle runs lambdas of the grid until it is spent")
     ap.add_argument("--cd", default="auto", choices=["auto", "residual", "gram"],
                     help="CD flavour: residual updates (r on chip) or covariance updates (NEXT-2)")
     args = ap.parse_args()

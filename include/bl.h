@@ -25,7 +25,10 @@
  *    is locked to 0 and they are excluded from lambda_max, BEDPP and scans (Q13).
  *  - Host pointers are only read during the call (copied); results are owned by
  *    the library until bl_free.  A design is immutable after load; concurrent
- *    fits on one design from different host threads are allowed.
+ *    fits on one single-GPU design from different host threads are allowed (S:90,
+ *    S:341).  A multi-rank design (world > 1) accepts one call at a time: its
+ *    collectives must be issued in the same order on every rank, so a second
+ *    concurrent call on the same design returns BL_ERR_ARG.
  */
 #ifndef BL_H
 #define BL_H
@@ -84,13 +87,27 @@ typedef struct {
     int backend;
 } bl_dist;
 
-/* Optional execution options (NULL => defaults). */
+/* Optional execution options (NULL or all-zero => defaults).  None of them changes a
+ * result beyond floating-point association order, except the TEST-ONLY fault switch. */
 typedef struct {
     void *stream;        /* cudaStream_t to run on; NULL => library-owned stream */
     int profile;         /* 1 => time every scan / CD launch with CUDA events (bl_path_perf) */
-    int max_kkt_rounds;  /* <= 0 => 10 */
+    int max_kkt_rounds;  /* cap on the KKT rounds R_k (solve + scan) at one lambda; <= 0 => 10.
+                            A lambda that still has violators after R_k = cap rounds ends the path with
+                            BL_ERR_CONVERGENCE (the converged prefix is returned) */
     int cd_mode;         /* 0 auto (Gram/covariance updates while |W| <= 4096),
                             1 residual-update CD (r held on chip), 2 Gram only */
+    int cv_mode;         /* bl_cv on a single-GPU or sharded design: 0 (default) the K+1 fits advance
+                            lambda in lockstep and each KKT round's scans of all fits are one pass over X
+                             on the fp64 tensor cores (int8: integer tensor cores);
+                            1 the same with the fp64-FMA batched kernel; 2 independent concurrent fits
+                            (one pass over X per fit and round) */
+    int cd_cluster;      /* CTAs per Gram-CD cluster: 0 => 8 (portable); 4, 8 or 16 */
+    int64_t stream_chunk_bytes; /* out-of-core designs (x_is_device_ptr = 2): bytes of X per streamed
+                            chunk (two chunks are resident); 0 => 256 MB */
+    int fault_strong_drop; /* TEST ONLY (S:222 fault injection): 1 => the strong rule admits no
+                            candidate to the working set in advance, so every feature that enters the
+                            model must be found by the KKT check (re-solve, re-check); 0 => off */
 } bl_opts;
 
 /* Per-fit performance counters (filled when opts->profile == 1). */

@@ -65,6 +65,8 @@ def _L():
         _lib.or_path_run.argtypes = [P, P, I, D, I, I, I64, P, P, P, P, P, P, P, P]
         _lib.or_path_end.argtypes = [P]
         _lib.or_path_end.restype = None
+        _lib.or_path_lambda_max.argtypes = [P]
+        _lib.or_path_lambda_max.restype = D
     return _lib
 
 
@@ -244,6 +246,7 @@ class PathSession:
         if rc:
             raise OracleError(rc, "path_begin")
         self.h = h
+        self.lambda_max = _L().or_path_lambda_max(h)   # max_j |x~_j'y~| / (n alpha) (Q3)
 
     def run(self, lam, tol=1e-10, max_iter=100000, cycle_active=True, nnz_cap=None):
         lam = np.ascontiguousarray(lam, dtype=np.float64)

@@ -463,6 +463,8 @@ void or_path_end(or_path_t *st)
     free(st);
 }
 
+double or_path_lambda_max(const or_path_t *st) { return st ? st->lmax : 0.0; }
+
 /* Column stats, y~ (r = y~, beta = 0) and lambda_max of the fit (SURVEY 8(c.2)
  * steps 1-5). */
 int or_path_begin(const void *X, int dt, int64_t n, int64_t p, int64_t ld,
@@ -600,7 +602,8 @@ int or_path_run(or_path_t *st, const double *lambda, int nlam, double tol, int m
         if (obj) obj[k] = rss / (2.0 * nd) + lam * (alpha * l1 + 0.5 * (1.0 - alpha) * l2);
         if (passes) passes[k] = np_;
         if (resid) {
-            /* every row: y_i - (ybar + sum_j x~_ij beta_j), formed explicitly */
+            /* every row: y_i - (ybar + sum_j x~_ij beta_j), formed explicitly (rows independent) */
+            OR_PAR
             for (int64_t i = 0; i < n; i++) {
                 double f = ybar;
                 for (int64_t j = 0; j < p; j++)

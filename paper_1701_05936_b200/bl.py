@@ -40,7 +40,17 @@ class bl_dist(ctypes.Structure):
 
 class bl_opts(ctypes.Structure):
     _fields_ = [("stream", ctypes.c_void_p), ("profile", ctypes.c_int), ("max_kkt_rounds", ctypes.c_int),
-                ("cd_mode", ctypes.c_int)]
+                ("cd_mode", ctypes.c_int), ("cv_mode", ctypes.c_int), ("cd_cluster", ctypes.c_int),
+                ("stream_chunk_bytes", ctypes.c_int64), ("fault_strong_drop", ctypes.c_int)]
+
+
+CV_MODE = {"batched": 0, "batched_fma": 1, "independent": 2}
+
+
+def _opts(stream=None, profile=False, max_kkt_rounds=0, cd="auto", cv_mode="batched", cd_cluster=0,
+          stream_chunk_bytes=0, fault_strong_drop=0):
+    return bl_opts(stream, int(profile), int(max_kkt_rounds), CD_MODE[cd], CV_MODE[cv_mode], int(cd_cluster),
+                   int(stream_chunk_bytes), int(fault_strong_drop))
 
 
 class bl_perf(ctypes.Structure):
@@ -249,9 +259,10 @@ class Design:
         return out.value
 
     def fit_path(self, y, lam, alpha=1.0, tol=1e-7, max_iter=10000, screen="hybrid", stream=None,
-                 profile=False, max_kkt_rounds=0, raise_on_error=True, cd="auto"):
+                 profile=False, max_kkt_rounds=0, raise_on_error=True, cd="auto", **opts):
+        """opts: cd_cluster, stream_chunk_bytes, fault_strong_drop (bl_opts, include/bl.h)."""
         lam = _f64(lam)
-        o = bl_opts(stream, int(profile), max_kkt_rounds, CD_MODE[cd])
+        o = _opts(stream, profile, max_kkt_rounds, cd, **opts)
         h = ctypes.c_void_p()
         rc = lib().bl_fit_path(self.h, _p(_f64(y)), _p(lam), lam.size, alpha, tol, max_iter,
                                SCREEN.get(screen, screen), ctypes.byref(o), ctypes.byref(h))
@@ -262,11 +273,11 @@ class Design:
             lib().bl_free(h)
 
     def fit_path_binomial(self, y, lam, alpha=1.0, tol=1e-7, max_iter=10000, screen="ssr", stream=None,
-                          profile=False, max_kkt_rounds=0, raise_on_error=True, cd="auto"):
+                          profile=False, max_kkt_rounds=0, raise_on_error=True, cd="auto", **opts):
         """Penalised logistic path (NEXT-3, bl_fit_path_binomial); y in {0, 1}.
         cd: "auto" (covariance form while |W| < 2048) or "residual"."""
         lam = _f64(lam)
-        o = bl_opts(stream, int(profile), max_kkt_rounds, CD_MODE[cd])
+        o = _opts(stream, profile, max_kkt_rounds, cd, **opts)
         h = ctypes.c_void_p()
         rc = lib().bl_fit_path_binomial(self.h, _p(_f64(y)), _p(lam), lam.size, alpha, tol, max_iter,
                                         SCREEN.get(screen, screen), ctypes.byref(o), ctypes.byref(h))
@@ -280,10 +291,12 @@ class Design:
             lib().bl_free(h)
 
     def cv(self, y, lam, K=10, alpha=1.0, tol=1e-7, max_iter=10000, fold_id=None, seed=0, stream=None,
-           profile=False, cd="auto"):
+           profile=False, cd="auto", cv_mode="batched", max_kkt_rounds=0, **opts):
+        """cv_mode: "batched" (lockstep fits, one fold-batched pass over X per round on the tensor
+        cores; default), "batched_fma", "independent" (bl_opts.cv_mode)."""
         lam = _f64(lam)
         f = None if fold_id is None else np.ascontiguousarray(fold_id, dtype=np.int32)
-        o = bl_opts(stream, int(profile), 0, CD_MODE[cd])
+        o = _opts(stream, profile, max_kkt_rounds, cd, cv_mode, **opts)
         h = ctypes.c_void_p()
         _check(lib().bl_cv(self.h, _p(_f64(y)), _p(lam), lam.size, alpha, tol, max_iter, K, _p(f), seed,
                            ctypes.byref(o), ctypes.byref(h)))

@@ -57,5 +57,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(name: str, defines: list[str]) -> str:
+    """An instrumented copy of the library (e.g. -DBL_G7_SUBPHASES=1) for micro-benchmarks:
+    lib<name>.so next to libbl.so; scripts load it by setting bl.LIB_PATH before the first call."""
+    out = os.path.join(PKG, f"lib{name}.so")
+    ninc, nlib = nccl_dirs()
+    cmd = [nvcc(), *NVCC_FLAGS, *defines, "-I", os.path.join(ROOT, "include"), "-I", ninc, "-o", out, *SRC,
+           "-L", nlib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + nlib]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError(f"nvcc failed building {out}")
+    return out
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))

@@ -16,6 +16,7 @@
 #include <cstdarg>
 #include <cstdlib>
 #include <cstdio>
+#include <atomic>
 #include <condition_variable>
 #include <cstring>
 #include <map>
@@ -263,6 +264,7 @@ struct bl_design {
     void *host_reg = nullptr;        // host range this design registered (unregistered by bl_free)
     std::vector<int64_t> shard_off;  // world + 1 global column offsets of the shards (rank order)
     std::mutex comm_mu;
+    std::atomic<int> busy{0};        // world > 1: one call at a time (collective order, bl.h)
 };
 
 struct bl_path {
@@ -359,6 +361,9 @@ struct bl_prep {
     int star_root;          // rank owning x_* (sharded)
     double batch_bytes;     // lockstep CV: X bytes read by the batched scans this fit timed
     int cd_mode;            // 0 auto (Gram when |W| <= 4096), 1 residual, 2 Gram
+    int cd_cluster;         // CTAs per Gram-CD cluster (4, 8, 16)
+    int fault_strong_drop;  // TEST ONLY (bl_opts): admit no strong-rule candidate in advance
+    size_t chunk_bytes;     // out-of-core: bytes per streamed chunk (the buffers are sized for it)
     cudaStream_t own;       // library stream (used when the caller passes none)
     // profiling
     int profile;
@@ -384,6 +389,21 @@ void check_device() {
     if (prop.major != 10)
         raise(BL_ERR_CUDA, "device %d is sm_%d%d; libbl is built for sm_100a only", dev, prop.major, prop.minor);
 }
+
+// A multi-rank design accepts one call at a time (include/bl.h): two concurrent calls
+// could issue their collectives in different orders on different ranks.
+struct BusyGuard {
+    bl_design *d;
+    bool held = false;
+    explicit BusyGuard(bl_design *d_) : d(d_) {
+        if (d->world <= 1) return;
+        int expect = 0;
+        if (!d->busy.compare_exchange_strong(expect, 1))
+            raise(BL_ERR_ARG, "a multi-rank design accepts one call at a time (collectives must run in the same order on every rank)");
+        held = true;
+    }
+    ~BusyGuard() { if (held) d->busy.store(0); }
+};
 
 template <typename F>
 bl_status guard(F &&f) {
@@ -502,14 +522,14 @@ void ensure_stream_bufs(bl_prep *pp) {
     if (pp->sbuf[0]) return;
     bl_design *d = pp->d;
     const size_t colb = (size_t)d->ld * itemsize(d->dt);
-    pp->scols = std::max<int64_t>(1, std::min<int64_t>(d->p, (int64_t)(kStreamChunkBytes / colb)));
+    pp->scols = std::max<int64_t>(1, std::min<int64_t>(d->p, (int64_t)(pp->chunk_bytes / colb)));
     for (int u = 0; u < 2; u++) {
         cudaError_t e = cache::dmalloc((void **)&pp->sbuf[u], colb * pp->scols);
         if (e != cudaSuccess) { cudaGetLastError(); raise(BL_ERR_OOM, "cudaMalloc for the streamed-scan buffers: %s", cudaGetErrorString(e)); }
-        CK(cudaEventCreateWithFlags(&pp->copied[u], cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&pp->used[u], cudaEventDisableTiming));
+        if (!pp->copied[u]) CK(cudaEventCreateWithFlags(&pp->copied[u], cudaEventDisableTiming));
+        if (!pp->used[u]) CK(cudaEventCreateWithFlags(&pp->used[u], cudaEventDisableTiming));
     }
-    CK(cudaStreamCreateWithFlags(&pp->cstream, cudaStreamNonBlocking));
+    if (!pp->cstream) CK(cudaStreamCreateWithFlags(&pp->cstream, cudaStreamNonBlocking));
 }
 
 template <typename F>
@@ -588,14 +608,8 @@ void launch_scan(bl_prep *pp, ScanArgs a, const double *v_dev, bool timed, bool 
         a.v = v_dev;
         int V = 16 / itemsize(d->dt);
         size_t smem = (size_t)8 * round_up(d->n, 32 * V);
-        // columns per warp iteration: 4 (more loads in flight) unless that leaves a
-        // badly quantised last wave on a small full-width scan (experiment knob BL_SCAN_C)
-        static const int cenv = [] { const char *e = std::getenv("BL_SCAN_C"); return e ? std::atoi(e) : 0; }();
-        const int C = cenv ? cenv : 4;
-        const void *kern = d->dt == DT_F32 ? (C == 8 ? (const void *)k_scan_fp<float, 8> : C == 2 ? (const void *)k_scan_fp<float, 2>
-                                                                                              : (const void *)k_scan_fp<float, 4>)
-                                           : (C == 8 ? (const void *)k_scan_fp<double, 8> : C == 2 ? (const void *)k_scan_fp<double, 2>
-                                                                                              : (const void *)k_scan_fp<double, 4>);
+        // 4 columns per warp iteration (16-byte loads, four columns' loads in flight per lane)
+        const void *kern = d->dt == DT_F32 ? (const void *)k_scan_fp<float, 4> : (const void *)k_scan_fp<double, 4>;
         allow_dyn_smem(kern);
         int grid = grid_for(kern, kScanThreads, smem, d->nsm);
         EvPairOpt ev(pp, events ? (timed ? &pp->ev_scan : &pp->ev_prep) : nullptr);
@@ -842,6 +856,18 @@ bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double a
     pp->ld = d->ld;
     pp->profile = opts ? opts->profile : 0;
     pp->cd_mode = opts ? opts->cd_mode : 0;
+    {
+        const int cc = opts ? opts->cd_cluster : 0;
+        if (cc != 0 && cc != 4 && cc != 8 && cc != 16) raise(BL_ERR_ARG, "cd_cluster must be 0, 4, 8 or 16 (got %d)", cc);
+        pp->cd_cluster = cc == 0 ? 8 : cc;
+        if (opts && opts->stream_chunk_bytes < 0) raise(BL_ERR_ARG, "stream_chunk_bytes must be >= 0");
+        const size_t cb = opts && opts->stream_chunk_bytes > 0 ? (size_t)opts->stream_chunk_bytes : kStreamChunkBytes;
+        if (cb != pp->chunk_bytes && pp->sbuf[0]) {          // a reused workspace with other chunk buffers
+            for (int u = 0; u < 2; u++) { cache::dfree(pp->sbuf[u]); pp->sbuf[u] = nullptr; }
+        }
+        pp->chunk_bytes = cb;
+        pp->fault_strong_drop = opts ? opts->fault_strong_drop : 0;
+    }
     pp->nG = 0;
     pp->launches = 0;
     pp->scan_full.clear();
@@ -930,7 +956,7 @@ bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double a
     // lambda_max, j*
     k_argmax1<<<pp->amax_blocks, 256, 0, st>>>(pp->a, pp->s, p, pp->amax_v, pp->amax_i, pp->nlive);
     CKL();
-    k_argmax2<<<1, 32, 0, st>>>(pp->amax_v, pp->amax_i, pp->amax_blocks, pp->a, pp->c, pp->s, alpha, pp->nlive,
+    k_argmax2<<<1, 256, 0, st>>>(pp->amax_v, pp->amax_i, pp->amax_blocks, pp->a, pp->c, pp->s, alpha, pp->nlive,
                                 pp->ps);
     CKL();
     pp->launches += 2;
@@ -1333,16 +1359,6 @@ G7Work gram_ws(bl_prep *pp) {
     return w;
 }
 
-// cluster size of the Gram CD kernel (CTA 0 leads, 1..R-1 own the gradients): 8
-// (portable), or 4 / 16 with BL_CD_CLUSTER
-int cd_cluster() {
-    static int r = [] {
-        const char *e = std::getenv("BL_CD_CLUSTER");
-        int v = e ? std::atoi(e) : 8;
-        return v <= 4 ? 4 : v <= 8 ? 8 : 16;
-    }();
-    return r;
-}
 const void *gram7_kernel(bool enet, int R) {
     static std::once_flag once;
     std::call_once(once, [] {       // 16-CTA clusters are a non-portable size
@@ -1474,7 +1490,7 @@ void solve_logit_g7_t(bl_prep *pp, int nW, double lam, double alpha, double tol,
     ga.st = pp->st;
     ga.tau = ws + nW;
     ga.idv = alpha < 1.0 ? ws + 3 * (size_t)nW : nullptr;
-    const int R = cd_cluster();
+    const int R = pp->cd_cluster;   // CTA 0 leads, 1..R-1 own the gradients
     const void *kern = gram7_kernel(alpha < 1.0, R);
     const size_t smem = gram7_smem(nW, R);
     const size_t lim = allow_dyn_smem(kern);
@@ -1527,11 +1543,6 @@ void solve_logit_g7_t(bl_prep *pp, int nW, double lam, double alpha, double tol,
     pp->launches += 3;
 }
 
-bool logit_use_g7() {
-    static const bool v = [] { const char *e = std::getenv("BL_LOGIT_G7"); return !(e && e[0] == '0'); }();
-    return v;
-}
-
 void solve_logit(bl_prep *pp, int nW, double lam, double alpha, double tol, int max_iter) {
     bl_design *d = pp->d;
     if (nW + 1 > kLogitGramMax || pp->cd_mode == 1) {       // residual form (or requested)
@@ -1539,7 +1550,7 @@ void solve_logit(bl_prep *pp, int nW, double lam, double alpha, double tol, int 
         return;
     }
     const bool M = pp->has_mask != 0;
-    if (nW >= 1 && logit_use_g7()) {                         // the cluster Gram CD
+    if (nW >= 1) {                                           // the cluster Gram CD
         if (d->dt == DT_F64) M ? solve_logit_g7_t<double, true>(pp, nW, lam, alpha, tol, max_iter)
                                : solve_logit_g7_t<double, false>(pp, nW, lam, alpha, tol, max_iter);
         else if (d->dt == DT_F32) M ? solve_logit_g7_t<float, true>(pp, nW, lam, alpha, tol, max_iter)
@@ -1604,7 +1615,7 @@ void solve_cd(bl_prep *pp, int nW, double lam, double alpha, double tol, int max
     ga.s = v.s;
     ga.st = pp->st;
     // cluster Gram CD: R CTAs of 256 threads (CTA 0 leads, 1..R-1 own the gradients)
-    const int R = cd_cluster();
+    const int R = pp->cd_cluster;   // CTA 0 leads, 1..R-1 own the gradients
     const void *kern = gram7_kernel(alpha < 1.0, R);
     const size_t smem = gram7_smem(nW, R);
     const size_t lim = allow_dyn_smem(kern);
@@ -1742,6 +1753,7 @@ struct PathRun {
                 strong_next = global_list(pp, pp->strong, pp->hst->nstrong);
                 first = false;
             }
+            if (pp->fault_strong_drop) strong_next.clear();   // TEST ONLY: the KKT check must find them
             nstrong_k = (int64_t)strong_next.size();
             upload_W(pp, W, W.add(strong_next));
             strong_next.clear();
@@ -1814,7 +1826,7 @@ struct PathRun {
         if (use_bedpp && nsafe == pp->hps.n_live) use_bedpp = 0;   // BEDPP keeps everything from here on
         if (pp->hst->cd_status) { status = BL_ERR_CONVERGENCE; return -1; }
         if (nviol > 0) {
-            if (++rounds > max_rounds) {
+            if (++rounds >= max_rounds) {             // R_k = rounds + 1 would exceed the cap
                 g_err = "more than max KKT rounds at one lambda";
                 status = BL_ERR_CONVERGENCE;
                 return -1;
@@ -1990,14 +2002,8 @@ const void *batch_mma_kernel_n(bool f64, int nb) {
     }
     return f64 ? (const void *)k_scan_batch_mma<double, NF> : (const void *)k_scan_batch_mma<float, NF>;
 }
-// fold-batched scan flavour: DMMA (default) or the FMA kernel (BL_CV_MMA=0)
-bool batch_use_mma() {
-    static const bool v = [] { const char *e = std::getenv("BL_CV_MMA"); return !(e && e[0] == '0'); }();
-    return v;
-}
-
 void launch_scan_batch(bl_design *d, const std::vector<LockFit *> &fits, cudaStream_t sst, FitScan *dfs,
-                       FitScan *hfs, bl_prep *timer) {
+                       FitScan *hfs, bl_prep *timer, bool mma) {
     const size_t nf = fits.size();
     for (size_t u = 0; u < nf; u++) {
         bl_prep *pp = fits[u]->pp;
@@ -2028,7 +2034,6 @@ void launch_scan_batch(bl_design *d, const std::vector<LockFit *> &fits, cudaStr
     }
     for (size_t u0 = 0; u0 < nf; u0 += kBatchMax) {
         int nb = (int)std::min<size_t>(kBatchMax, nf - u0);
-        const bool mma = batch_use_mma();
         const void *kern = mma ? batch_mma_kernel_n<kBatchMax>(f64, nb) : batch_kernel(f64, nb);
         const size_t smem = mma ? batch_mma_smem(nb) : batch_smem(nb, itemsize(d->dt));
         const int threads = mma ? kBMThreads : kBatchThreads;
@@ -2064,6 +2069,7 @@ void cv_lockstep(bl_design *d, const double *y, const std::vector<int32_t> &fold
     cudaStream_t sst = nullptr;
     FitScan *dfs = nullptr, *hfs = nullptr;
     const bool batched = d->dt != DT_I8;
+    const bool mma = !opts || opts->cv_mode == 0;         // fold-batched scan on the fp64 tensor cores
     auto t0 = std::chrono::steady_clock::now();
     auto cleanup = [&]() {
         if (sst) cudaStreamSynchronize(sst);
@@ -2087,16 +2093,27 @@ void cv_lockstep(bl_design *d, const double *y, const std::vector<int32_t> &fold
                 train.resize(n);
                 for (int64_t i = 0; i < n; i++) train[i] = fold[i] != fit_ids[u];
             }
-            lf.pp = make_prep(d, y, train.empty() ? nullptr : train.data(), alpha, &fo);
-            lf.pp->batch_bytes = 0.0;
             lf.out = new bl_path();
             lf.out->magic = MAGIC_PATH;
+            try {                                          // one degenerate fold (e.g. y constant on its
+                lf.pp = make_prep(d, y, train.empty() ? nullptr : train.data(), alpha, &fo);   // training rows)
+            } catch (const Err &er) {                      // fails that fit only, as in the threaded mode
+                if (d->sharded) throw;                     // (a sharded fit is collective: every rank fails it)
+                lf.alive = false;
+                lf.st = er.code;
+                lf.err = g_err;
+                g_err.clear();
+                continue;
+            }
+            lf.pp->batch_bytes = 0.0;
             lf.run.reset(new PathRun{lf.pp, lambda, K, alpha, tol, max_iter, BL_SCREEN_HYBRID, rounds, lf.out,
                                      fit_ids[u] >= 0 ? dE : nullptr});
             lf.run->begin();
             CK(cudaEventCreateWithFlags(&lf.solved, cudaEventDisableTiming));
         }
-        bl_prep *timer = fits.empty() ? nullptr : fits[0].pp;
+        bl_prep *timer = nullptr;
+        for (auto &lf : fits)
+            if (lf.pp) { timer = lf.pp; break; }
         for (int k = 0; k < K; k++) {
             std::vector<LockFit *> pending;
             for (auto &lf : fits)
@@ -2109,7 +2126,7 @@ void cv_lockstep(bl_design *d, const double *y, const std::vector<int32_t> &fold
                 }
                 if (batched) {
                     for (LockFit *lf : pending) CK(cudaStreamWaitEvent(sst, lf->solved, 0));
-                    launch_scan_batch(d, pending, sst, dfs, hfs, timer);
+                    launch_scan_batch(d, pending, sst, dfs, hfs, timer, mma);
                     for (LockFit *lf : pending) copy_round(lf->pp, sst);
                     CK(cudaStreamSynchronize(sst));
                 } else {
@@ -2136,17 +2153,18 @@ void cv_lockstep(bl_design *d, const double *y, const std::vector<int32_t> &fold
             for (LockFit *lf : active)
                 if (lf->alive) lf->run->record();
         }
-        for (auto &lf : fits) lf.run->flush();
+        for (auto &lf : fits)
+            if (lf.run) lf.run->flush();
         const double wall = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         paths.assign(F, nullptr);
         sts.assign(F, BL_OK);
         errs.assign(F, std::string());
         for (size_t u = 0; u < F; u++) {
             LockFit &lf = fits[u];
-            finish_perf(lf.pp, lf.out, wall);
-            if (batched) {                                  // the batched passes: charged once, to fit 0
-                lf.out->perf.scan_bytes = u == 0 ? lf.pp->batch_bytes : 0.0;
-                if (u != 0) { lf.out->perf.scan_ms = 0.0; lf.out->perf.scan_launches = 0; }
+            if (lf.pp) finish_perf(lf.pp, lf.out, wall);
+            if (batched && lf.pp) {                         // the batched passes: charged once, to the timer fit
+                lf.out->perf.scan_bytes = lf.pp == timer ? lf.pp->batch_bytes : 0.0;
+                if (lf.pp != timer) { lf.out->perf.scan_ms = 0.0; lf.out->perf.scan_launches = 0; }
             }
             paths[u] = lf.out;
             lf.out = nullptr;
@@ -2239,6 +2257,7 @@ bl_status bl_load_design(const void *X, bl_dtype dt, int64_t n, int64_t p_local,
         if (p_local < 1) raise(BL_ERR_ARG, "p must be >= 1");
         if (ld < n) raise(BL_ERR_ARG, "ld < n");
         if (p_local > INT32_MAX) raise(BL_ERR_ARG, "p_local too large");
+        if (x_is_device_ptr < 0 || x_is_device_ptr > 2) raise(BL_ERR_ARG, "x_is_device_ptr must be 0, 1 or 2");
         check_device();
         bl_design *d = new bl_design();
         d->magic = MAGIC_DESIGN;
@@ -2318,7 +2337,6 @@ bl_status bl_load_design(const void *X, bl_dtype dt, int64_t n, int64_t p_local,
             if (ldp > n)                               // padding rows are zero (whatever the caller's held)
                 CK(cudaMemset2D((char *)d->X + n * isz, ldp * isz, 0, (ldp - n) * isz, p_local));
         }
-        if (x_is_device_ptr < 0 || x_is_device_ptr > 2) { delete d; raise(BL_ERR_ARG, "x_is_device_ptr must be 0, 1 or 2"); }
         d->sharded = false;
         d->wstore = d->hostres;
         d->shard_off.assign(2, 0);
@@ -2392,6 +2410,7 @@ bl_status bl_prepare(bl_design *d, const double *y, const uint8_t *train, double
     return guard([&] {
         if (!d || d->magic != MAGIC_DESIGN) raise(BL_ERR_ARG, "bad design handle");
         if (!out) raise(BL_ERR_ARG, "out is NULL");
+        BusyGuard bg(d);
         *out = make_prep(d, y, train, alpha, nullptr);
     });
 }
@@ -2400,6 +2419,7 @@ bl_status bl_lambda_max(bl_design *d, const double *y, double alpha, double *out
     return guard([&] {
         if (!d || d->magic != MAGIC_DESIGN) raise(BL_ERR_ARG, "bad design handle");
         if (!out) raise(BL_ERR_ARG, "out is NULL");
+        BusyGuard bg(d);
         bl_prep *pp = make_prep(d, y, nullptr, alpha, nullptr);
         *out = pp->hps.lmax;
         free_prep(pp);
@@ -2497,6 +2517,7 @@ bl_status bl_fit_path(bl_design *d, const double *y, const double *lambda, int n
         if (!d || d->magic != MAGIC_DESIGN) raise(BL_ERR_ARG, "bad design handle");
         if (!out) raise(BL_ERR_ARG, "out is NULL");
         *out = nullptr;
+        BusyGuard bg(d);
         *out = fit_impl(d, y, nullptr, lambda, n_lambda, alpha, tol, max_iter, screen, opts, &s);
     });
     return g != BL_OK ? g : s;
@@ -2516,6 +2537,7 @@ bl_status bl_fit_path_binomial(bl_design *d, const double *y, const double *lamb
             n1 += y[i] == 1.0;
         }
         if (n1 == 0 || n1 == d->n) raise(BL_ERR_DEGENERATE, "binomial y has a single class (S:311)");
+        BusyGuard bg(d);
         *out = fit_impl(d, y, nullptr, lambda, n_lambda, alpha, tol, max_iter, screen, opts, &s, nullptr, 1);
     });
     return g != BL_OK ? g : s;
@@ -2532,6 +2554,11 @@ bl_status bl_cv(bl_design *d, const double *y, const double *lambda, int n_lambd
         const int64_t n = d->n;
         if (n_folds < 2 || n_folds > n) raise(BL_ERR_ARG, "need 2 <= K <= n (K = %d, n = %lld)", n_folds, (long long)n);
         validate_grid(lambda, n_lambda);
+        if (!(tol > 0.0)) raise(BL_ERR_ARG, "tol must be > 0");
+        if (max_iter < 1) raise(BL_ERR_ARG, "max_iter must be >= 1");
+        const int cv_mode = opts ? opts->cv_mode : 0;
+        if (cv_mode < 0 || cv_mode > 2) raise(BL_ERR_ARG, "cv_mode must be 0, 1 or 2 (got %d)", cv_mode);
+        BusyGuard bg(d);
         std::vector<int32_t> f(n);
         if (fold_id) {
             for (int64_t i = 0; i < n; i++) {
@@ -2552,7 +2579,15 @@ bl_status bl_cv(bl_design *d, const double *y, const double *lambda, int n_lambd
         for (int64_t i = 0; i < n; i++) cnt[f[i]]++;
         for (int k = 0; k < n_folds; k++)
             if (cnt[k] == 0) raise(BL_ERR_ARG, "fold %d is empty", k);
-        bl_cvres *cv = new bl_cvres();
+        struct CvOwner {                                // the result is the caller's only on success
+            bl_cvres *p;
+            ~CvOwner() {
+                if (!p) return;
+                if (p->full) { p->full->magic = MAGIC_DEAD; delete p->full; }
+                delete p;
+            }
+        } cvo{new bl_cvres()};
+        bl_cvres *cv = cvo.p;
         cv->magic = MAGIC_CV;
         cv->n_lambda = n_lambda;
         cv->K = n_folds;
@@ -2565,15 +2600,15 @@ bl_status bl_cv(bl_design *d, const double *y, const double *lambda, int n_lambd
         // device E (n_lambda x n): fold fits write disjoint held-out rows, so they run concurrently
         double *dE = nullptr, *dcv = nullptr;
         cudaError_t e = cache::dmalloc((void **)&dE, 8 * (size_t)n_lambda * n + 16 * (size_t)n_lambda);
-        if (e != cudaSuccess) { cudaGetLastError(); delete cv; raise(BL_ERR_OOM, "cudaMalloc for CV errors: %s", cudaGetErrorString(e)); }
+        if (e != cudaSuccess) { cudaGetLastError(); raise(BL_ERR_OOM, "cudaMalloc for CV errors: %s", cudaGetErrorString(e)); }
         dcv = dE + (size_t)n_lambda * n;
         struct Free { double *p; ~Free() { if (p) cache::dfree(p); } } fr{dE};
         CK(cudaMemset(dE, 0, 8 * (size_t)n_lambda * n));
-        // fold-parallel: fold fits run concurrently on their own streams --
-        // each fit's CD kernel occupies one SM, so the folds share the GPU instead of queueing.
-        // With world > 1 ranks, fold f runs on rank f mod world (replicated X) and E is summed.
+        // fold-parallel.  With world > 1 ranks and a replicated design, fold f
+        // runs on rank f mod world and E is summed; a sharded design runs every fit on every
+        // rank (each fit's collectives span the shards).
         std::vector<int> mine;
-        for (int fo = 0; fo < n_folds; fo++)             // sharded: every fit is collective -> all folds
+        for (int fo = 0; fo < n_folds; fo++)
             if (d->sharded || fo % d->world == d->rank) mine.push_back(fo);
         std::vector<bl_status> fst(mine.size() + 1, BL_OK);
         std::vector<std::string> ferr(mine.size() + 1);
@@ -2610,12 +2645,7 @@ bl_status bl_cv(bl_design *d, const double *y, const double *lambda, int n_lambd
                 ferr[idx] = "host allocation failed";
             }
         };
-        static const bool lockstep = [] { const char *e = std::getenv("BL_CV_LOCKSTEP"); return !e || std::atoi(e) != 0; }();
-        if (d->sharded) {                               // collectives must be issued in the same order
-            for (size_t idx = 0; idx <= mine.size(); idx++) run_fold(idx);
-        } else if (lockstep) {                          // NEXT-1: one pass over X per round for all fits
-            if (!(tol > 0.0)) raise(BL_ERR_ARG, "tol must be > 0");
-            if (max_iter < 1) raise(BL_ERR_ARG, "max_iter must be >= 1");
+        if (cv_mode <= 1) {                             // NEXT-1: one pass over X per round for all fits
             std::vector<int> ids(mine.begin(), mine.end());
             ids.push_back(-1);
             std::vector<bl_path *> paths;
@@ -2629,6 +2659,8 @@ bl_status bl_cv(bl_design *d, const double *y, const double *lambda, int n_lambd
                 if (ids[u] >= 0) delete paths[u];
                 else full[0] = paths[u];
             }
+        } else if (d->sharded) {                        // collectives must be issued in the same order
+            for (size_t idx = 0; idx <= mine.size(); idx++) run_fold(idx);
         } else {                                        // independent fits, one host thread + stream each
             std::vector<std::thread> th;
             for (size_t idx = 0; idx <= mine.size(); idx++) th.emplace_back(run_fold, idx);
@@ -2654,6 +2686,7 @@ bl_status bl_cv(bl_design *d, const double *y, const double *lambda, int n_lambd
             if (cv->cve[k] < cv->cve[best]) best = k;
         cv->lmin = best;
         *out = cv;
+        cvo.p = nullptr;
     });
     return g != BL_OK ? g : s;
 }

@@ -927,14 +927,32 @@ __global__ void k_argmax1(const double *__restrict__ a, const double *__restrict
     }
 }
 
-__global__ void k_argmax2(const double *__restrict__ bv, const long long *__restrict__ bi, int nb,
-                          const double *__restrict__ a, const double *__restrict__ c, const double *__restrict__ s,
-                          double alpha, const int *__restrict__ nlive, PrepScalars *ps) {
-    if (threadIdx.x != 0) return;
+// Stage 2: one block of 256 threads reduces the per-block bests (strided loads,
+// then warp shuffles and one shared-memory round); the (value, lowest index) order
+// is associative, so the result does not depend on the reduction shape.
+__device__ __forceinline__ void argmax_merge(double &best, long long &bj, double v2, long long j2) {
+    if (v2 > best || (v2 == best && j2 >= 0 && (bj < 0 || j2 < bj))) { best = v2; bj = j2; }
+}
+__global__ void __launch_bounds__(256) k_argmax2(const double *__restrict__ bv, const long long *__restrict__ bi, int nb,
+                                                 const double *__restrict__ a, const double *__restrict__ c,
+                                                 const double *__restrict__ s, double alpha,
+                                                 const int *__restrict__ nlive, PrepScalars *ps) {
+    __shared__ double sv[8];
+    __shared__ long long si[8];
     double best = -1.0;
     long long bj = -1;
-    for (int b = 0; b < nb; b++)
-        if (bv[b] > best || (bv[b] == best && bi[b] >= 0 && (bj < 0 || bi[b] < bj))) { best = bv[b]; bj = bi[b]; }
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) argmax_merge(best, bj, bv[b], bi[b]);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double v2 = __shfl_xor_sync(0xffffffffu, best, o);
+        const long long j2 = __shfl_xor_sync(0xffffffffu, bj, o);
+        argmax_merge(best, bj, v2, j2);
+    }
+    if (lane == 0) { sv[wid] = best; si[wid] = bj; }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    for (int w = 1; w < (int)(blockDim.x >> 5); w++) argmax_merge(best, bj, sv[w], si[w]);
     ps->jstar = bj;
     ps->n_live = *nlive;
     if (bj >= 0) {
@@ -2152,6 +2170,12 @@ struct CdGramArgs {
 // them.  Catch-ups, G_AA and M builds are split over the cluster.
 constexpr int kG7Threads = 256;
 constexpr int kG7Helpers = kG7Threads - 32;
+// Leader-warp sub-phase timers (bl_perf.cd_sub): six extra clock64 reads per block, so
+// they are compiled in only for the CD micro-benchmarks (-DBL_G7_SUBPHASES=1).
+#ifndef BL_G7_SUBPHASES
+#define BL_G7_SUBPHASES 0
+#endif
+#define G7CLK() (BL_G7_SUBPHASES ? clock64() : 0LL)
 constexpr int kG7MaxR = 16;
 constexpr int kG7Stages = 4;                    // leader prefetch ring (Gd, Gp, M per stage)
 __host__ __device__ constexpr size_t gram7_smem(int nW, int R) {
@@ -2215,7 +2239,8 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
     __shared__ __align__(16) double rsh[32];
     constexpr int DZ = 4, DDMAX = kG7MaxR + 2;
     __shared__ __align__(16) double zst[DZ][32];       // leader: ring of block gradients (st.async by the owners)
-    __shared__ __align__(16) double dq[DDMAX][32];     // owners: ring of the leader's block updates (st.async)
+    __shared__ __align__(16) double dq[DDMAX][32];     // owners: ring of the leader's block updates (bulk copies)
+    __shared__ __align__(16) double dsrc[DDMAX][32];   // leader: staging ring the bulk copies read
     constexpr int NS = kG7Stages;
     __shared__ __align__(8) uint64_t zfull[DZ], dfb[DDMAX], sfull[NS], sempty[NS];
     __shared__ int bslot[NS][32];                      // leader: slots of the block
@@ -2354,7 +2379,7 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
     // leader warp: block at positions b0.. (stage buf; zo = the owner's snapshot); acc = link term;
     // gb = block number (ring slot of the published updates)
     auto lead = [&](bool active, int b0, int buf, double zo, double acc, long long gb) {
-        const long long t0 = clock64();
+        const long long t0 = G7CLK();
         const int s = bslot[buf][lane];
         const bool valid = s >= 0;
         double zc = 0.0, bo = 0.0;
@@ -2369,7 +2394,7 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
         double dfin = 0.0, bnfin = bo;
         unsigned todo = __ballot_sync(FULL, valid);
         int round = 0;
-        const long long t1 = clock64();
+        const long long t1 = G7CLK();
         dbg[0] += t1 - t0;
         if (active) {
             const double las = pred > 0 ? la : -la;
@@ -2409,7 +2434,7 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
                 if ((todo >> lane) & 1u) pred = zc > la ? 1 : (zc < -la ? -1 : 0);
             }
         }
-        const long long t2 = clock64();
+        const long long t2 = G7CLK();
         dbg[1] += t2 - t1;
         while (todo) {
             const unsigned Pm = __ballot_sync(FULL, pred != 0) & todo;
@@ -2446,13 +2471,28 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
             }
             if ((todo >> lane) & 1u) pred = tb;   // the first mismatch is exact now; the rest re-predicted
         }
-        const long long t3 = clock64();
+        const long long t3 = G7CLK();
         dbg[2] += t3 - t2;
-        // publish the 32 updates into every owner's ring slot (st.async, completes on its mbarrier)
+        // publish the 32 updates into every owner's ring slot: the block is staged in this CTA's
+        // shared memory, then lanes 1..R-1 each issue ONE 256-byte bulk copy into owner `lane`'s
+        // ring, completing on that owner's mbarrier (32 x (R-1) 8-byte remote stores were the
+        // leader's largest per-block cost).  Slot ds is rewritten DD blocks later: before that,
+        // the issuing lane waits until its copy of block gb - DD + 1 has been read.
         {
             const int ds = (int)(gb % DD);
-            const uint32_t off = (uint32_t)((ds * 32 + lane) * 8), boff = (uint32_t)(ds * 8);
-            for (int r = 1; r < R; r++) st_async(rdq[r] + off, dfin, rdfb[r] + boff);
+            const bool issuer = lane >= 1 && lane < R;
+            if (issuer) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(RC) : "memory");   // DD - 1 = RC
+            __syncwarp();
+            dsrc[ds][lane] = dfin;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> async proxy
+            __syncwarp();
+            if (issuer) {
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], 256, [%2];"
+                    ::"r"(rdq[lane] + (uint32_t)(ds * 256)), "r"(smem_addr(&dsrc[ds][0])), "r"(rdfb[lane] + (uint32_t)(ds * 8))
+                    : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
         }
         dfull[lane] = dfin;
         retries += round;
@@ -2460,7 +2500,7 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
         bm = fmax(bm, fabs(bnfin));
         if (valid) bS[s] = bnfin;
         updates += __popc(__ballot_sync(FULL, valid && dfin != 0.0));
-        dbg[3] += clock64() - t3;
+        dbg[3] += G7CLK() - t3;
     };
 
     // owners: positions / slots of local index e for a sweep of `len` positions
@@ -2505,8 +2545,8 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
                     const int ss = (int)(gb % NS), zs = (int)(gb % DZ);
                     mbar_wait(&sfull[ss], (unsigned)((gb / NS) & 1));    // Gd, M, slots of block q
                     mbar_wait(&zfull[zs], (unsigned)((gb / DZ) & 1));    // the owner's snapshot
-                    const long long c1 = clock64();
-                    dbg[4] += c1 - c0;
+                    const long long c1 = G7CLK();
+                    dbg[4] += BL_G7_SUBPHASES ? c1 - c0 : 0;
                     const double zo = zst[zs][lane];
                     __syncwarp();
                     if (lane == 0) mbar_arm(&zfull[zs], 256);               // for block gb + DZ
@@ -2514,12 +2554,12 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&sempty[ss]);                // stage free for block gb + NS
                     if (q + 1 < Q) {
-                        const long long gn = gb + 1, c2 = clock64();
+                        const long long gn = gb + 1, c2 = G7CLK();
                         mbar_wait(&sfull[gn % NS], (unsigned)((gn / NS) & 1));
-                        const long long c3 = clock64();
+                        const long long c3 = G7CLK();
                         dbg[5] += c3 - c2;
                         acc = link((int)(gn % NS));
-                        dbg[6] += clock64() - c3;
+                        dbg[6] += G7CLK() - c3;
                     }
                     if (t == 0) pr_lead += clock64() - c0;
                 }
@@ -2559,8 +2599,8 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
                 const long long gb = g0 + j, c0 = clock64();
                 const int ds = (int)(gb % DD);
                 mbar_wait(&dfb[ds], (unsigned)((gb / DD) & 1));
-                const long long c1 = clock64();
-                dbg[4] += c1 - c0;
+                const long long c1 = G7CLK();
+                dbg[4] += BL_G7_SUBPHASES ? c1 - c0 : 0;
                 if (k0 >= 0) {
                     double gx = gl[e0], gy = gl[e0 + 1], hx = 0.0, hy = 0.0;
 #pragma unroll
@@ -2592,7 +2632,7 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
                 if (t == 0) mbar_arm(&dfb[ds], 256);                // for block gb + DD
                 send_snap(j + 2);
                 if (j + 1 < Q) load_rows(j + 1);
-                dbg[5] += clock64() - c1;
+                dbg[5] += G7CLK() - c1;
                 if (t == 0) pr_bulk += clock64() - c0;
             }
         }
@@ -2822,6 +2862,7 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
             if (red[2] == 0.0) full = conv;
         }
     }
+    if (leader_cta && wid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     cl.sync();                                              // no DSMEM access past this point
     if (!leader_cta) {
         if (rank == 1 && t == 0) a.st->cd_prof[1] = pr_bulk;

@@ -4,6 +4,9 @@ import numpy as np
 sys.path.insert(0, ".")
 import synth
 from paper_1701_05936_b200 import bl
+import os
+if os.environ.get("CD_PHASES_LIB"):        # the -DBL_G7_SUBPHASES=1 build (build.build_variant)
+    bl.LIB_PATH = os.environ["CD_PHASES_LIB"]
 
 for cfg in sys.argv[1:]:
     inst = synth.CONFIGS[cfg](device="cuda")

@@ -42,6 +42,28 @@ def test_host_resident_path_is_bitwise_equal(dtype, alpha, cd):
         assert np.abs(B[:, k] - op.beta[:, k]).max() <= 1e-5 * sc or sc == 0.0
 
 
+@pytest.mark.parametrize("dtype", [np.float32, np.float64, np.int8])
+def test_streamed_chunks_cross_boundaries(dtype):
+    """The streamed dense scans with a small bl_opts.stream_chunk_bytes: >= 3 chunks per pass
+    with a short last chunk (buffer flips, shifted virtual bases, the copied / used event
+    waits) give the device-resident path bitwise."""
+    kind = "geno" if dtype == np.int8 else "corr"
+    inst = synth.random_instance(203, 2101, dtype=dtype, seed=42, kind=kind, n_true=12, const_cols=2)
+    Xh = np.ascontiguousarray(inst.host_X())
+    colb = Xh.shape[1] * Xh.itemsize
+    chunk = 500 * colb                                    # 2101 columns -> 500, 500, 500, 500, 101
+    assert -(-inst.p // 500) >= 3 and inst.p % 500 != 0
+    dd = bl.Design(Xh, inst.n)
+    dh = bl.Design(Xh, inst.n, host_resident=True)
+    lm = dd.lambda_max(inst.y, 1.0)
+    lams = synth.lambda_grid(lm, 30, 0.05)
+    a = dd.fit_path(inst.y, lams, tol=1e-9)
+    b = dh.fit_path(inst.y, lams, tol=1e-9, stream_chunk_bytes=chunk)
+    same_path(a, b)
+    c = dh.fit_path(inst.y, lams, tol=1e-9, stream_chunk_bytes=chunk + 7 * colb)   # re-sized buffers on reuse
+    same_path(a, c)
+
+
 def test_host_resident_cv_and_logistic():
     inst = synth.random_instance(150, 800, dtype=np.float32, seed=43, kind="corr", n_true=8)
     Xh = np.ascontiguousarray(inst.host_X())
