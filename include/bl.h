@@ -76,15 +76,32 @@ typedef struct bl_prep bl_prep;
  *    distributes the folds over the ranks.
  * backend 0: NCCL; nccl_unique_id points to the 128-byte ncclUniqueId obtained on
  * rank 0 with bl_nccl_unique_id() and broadcast by the caller (torch.distributed).
+ * Collectives are enqueued on the fit's stream (NCCL groups batch a round's
+ * broadcasts); the host waits only where it decides on a result, polling
+ * ncclCommGetAsyncError, and aborts the communicator when a collective is still
+ * pending after timeout_ms (BL_ERR_NCCL; the design cannot run collectives after).
  * backend 1: in-process loopback for testing -- the ranks are threads of ONE
  * process sharing one device; nccl_unique_id points to a 128-byte group key
  * (any bytes, identical on the group's ranks); collectives are staged through
- * host memory. */
+ * host memory.
+ * backend 2: caller-supplied HOST collectives (host_coll, e.g. gloo or MPI between
+ * processes): every payload is staged through host memory around the caller's
+ * functions, which every rank calls with identical sizes in the same order and
+ * which return 0 on success (anything else: BL_ERR_NCCL).  nccl_unique_id unused. */
+typedef struct {
+    void *ctx;                                                                  /* passed back verbatim */
+    int (*allgather)(void *ctx, const void *send, void *recv, int64_t bytes);   /* recv: world x bytes, rank order */
+    int (*bcast)(void *ctx, void *buf, int64_t bytes, int root);
+    int (*allreduce_sum_f64)(void *ctx, double *buf, int64_t count);
+} bl_host_coll;
+
 typedef struct {
     int rank, world, device;
     const void *nccl_unique_id;
     int64_t col_offset, p_global;
-    int backend;
+    int backend;                       /* 0 NCCL, 1 in-process loopback, 2 host collectives */
+    const bl_host_coll *host_coll;     /* backend 2 (copied at load); NULL otherwise */
+    int timeout_ms;                    /* NCCL collective timeout; <= 0 => 600000 */
 } bl_dist;
 
 /* Optional execution options (NULL or all-zero => defaults).  None of them changes a
@@ -102,12 +119,18 @@ typedef struct {
                              on the fp64 tensor cores (int8: integer tensor cores);
                             1 the same with the fp64-FMA batched kernel; 2 independent concurrent fits
                             (one pass over X per fit and round) */
-    int cd_cluster;      /* CTAs per Gram-CD cluster: 0 => 8 (portable); 4, 8 or 16 */
+    int cd_cluster;      /* CTAs per Gram-CD cluster (SMs one CD solve uses): 0 => 16 for a single fit,
+                            8 for each of bl_cv's concurrent fits; or 4, 8, 16 */
     int64_t stream_chunk_bytes; /* out-of-core designs (x_is_device_ptr = 2): bytes of X per streamed
                             chunk (two chunks are resident); 0 => 256 MB */
     int fault_strong_drop; /* TEST ONLY (S:222 fault injection): 1 => the strong rule admits no
                             candidate to the working set in advance, so every feature that enters the
                             model must be found by the KKT check (re-solve, re-check); 0 => off */
+    int cd_accel;        /* Gram CD on the linear path: 0 (default) => when an active set has settled
+                            (same set and signs for two sweeps) but sweeps contract slowly, one Newton
+                            step on it (conjugate gradients on (G_AA + lambda(1-alpha) I)), truncated to
+                            keep every sign; the sweeps that follow decide convergence as before.
+                            1 => sweeps only */
 } bl_opts;
 
 /* Per-fit performance counters (filled when opts->profile == 1). */
@@ -128,7 +151,8 @@ typedef struct {
     double full_scan_ms;       /* the subset of scan launches that covered every live column (|S_k| = p, */
     double full_scan_bytes;    /*   SURVEY 8(d) "full-scan only" GB/s); single fits only (0 in CV sums) */
     int64_t full_scan_launches;
-    int64_t cd_events[4];      /* Gram CD events: speculation retries, G_AA builds, catch-ups, full sweeps */
+    int64_t cd_events[8];      /* Gram CD events: speculation retries, G_AA builds, catch-ups, full sweeps,
+                                  Newton steps, CG iterations, SM cycles in Newton steps, sign-limited steps */
     int64_t cd_sub[8];         /* Gram CD leader-warp sub-phase cycles: block prologue, active mat-vec,
                                   forward substitution, publish, waits (stage + snapshot), next-stage wait,
                                   link product, (unused) */

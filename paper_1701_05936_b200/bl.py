@@ -32,25 +32,37 @@ class BLError(RuntimeError):
         self.code = code
 
 
+_ALLGATHER = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64)
+_BCAST = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int)
+_ALLREDUCE = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64)
+
+
+class bl_host_coll(ctypes.Structure):
+    _fields_ = [("ctx", ctypes.c_void_p), ("allgather", _ALLGATHER), ("bcast", _BCAST),
+                ("allreduce_sum_f64", _ALLREDUCE)]
+
+
 class bl_dist(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int), ("world", ctypes.c_int), ("device", ctypes.c_int),
                 ("nccl_unique_id", ctypes.c_void_p), ("col_offset", ctypes.c_int64),
-                ("p_global", ctypes.c_int64), ("backend", ctypes.c_int)]
+                ("p_global", ctypes.c_int64), ("backend", ctypes.c_int),
+                ("host_coll", ctypes.POINTER(bl_host_coll)), ("timeout_ms", ctypes.c_int)]
 
 
 class bl_opts(ctypes.Structure):
     _fields_ = [("stream", ctypes.c_void_p), ("profile", ctypes.c_int), ("max_kkt_rounds", ctypes.c_int),
                 ("cd_mode", ctypes.c_int), ("cv_mode", ctypes.c_int), ("cd_cluster", ctypes.c_int),
-                ("stream_chunk_bytes", ctypes.c_int64), ("fault_strong_drop", ctypes.c_int)]
+                ("stream_chunk_bytes", ctypes.c_int64), ("fault_strong_drop", ctypes.c_int),
+                ("cd_accel", ctypes.c_int)]
 
 
 CV_MODE = {"batched": 0, "batched_fma": 1, "independent": 2}
 
 
 def _opts(stream=None, profile=False, max_kkt_rounds=0, cd="auto", cv_mode="batched", cd_cluster=0,
-          stream_chunk_bytes=0, fault_strong_drop=0):
+          stream_chunk_bytes=0, fault_strong_drop=0, cd_accel="newton"):
     return bl_opts(stream, int(profile), int(max_kkt_rounds), CD_MODE[cd], CV_MODE[cv_mode], int(cd_cluster),
-                   int(stream_chunk_bytes), int(fault_strong_drop))
+                   int(stream_chunk_bytes), int(fault_strong_drop), {"newton": 0, "none": 1}[cd_accel])
 
 
 class bl_perf(ctypes.Structure):
@@ -61,7 +73,7 @@ class bl_perf(ctypes.Structure):
                 ("wall_ms", ctypes.c_double), ("cd_visits", ctypes.c_int64), ("cd_updates", ctypes.c_int64),
                 ("cd_kernel_cycles", ctypes.c_int64), ("cd_prof", ctypes.c_int64 * 4),
                 ("full_scan_ms", ctypes.c_double), ("full_scan_bytes", ctypes.c_double),
-                ("full_scan_launches", ctypes.c_int64), ("cd_events", ctypes.c_int64 * 4),
+                ("full_scan_launches", ctypes.c_int64), ("cd_events", ctypes.c_int64 * 8),
                 ("cd_sub", ctypes.c_int64 * 8)]
 
     def as_dict(self):
@@ -249,6 +261,7 @@ class Design:
 
     def __init__(self, X, n, dist=None, host_resident=False):
         self._keep = X  # borrowed device / host-resident buffers must outlive the design
+        self._dist = dist   # host-collective callbacks (backend 2) must outlive the design
         self.n = int(n)
         self.p = int(X.shape[0])
         self.h = bl_load_design(X, self.n, dist, host_resident)
@@ -348,14 +361,14 @@ def shard_range(p, world, rank, block=1):
     return min(p, b0 * block), min(p, b1 * block)
 
 
-def make_dist(rank, world, col_range, p_global, device=0, group=None):
+def make_dist(rank, world, col_range, p_global, device=0, group=None, timeout_ms=0):
     """bl_dist of a torch.distributed job (NCCL backend): rank 0 draws the NCCL
     unique id, every rank receives it with torch.distributed.broadcast_object_list.
     p_global == col_range width => replicated design."""
     import torch.distributed as tdist
     uid = [bl_nccl_unique_id() if rank == 0 else None]
     tdist.broadcast_object_list(uid, src=0, group=group)
-    return _dist(rank, world, device, uid[0], col_range, p_global, 0)
+    return _dist(rank, world, device, uid[0], col_range, p_global, 0, timeout_ms)
 
 
 def loopback_dist(rank, world, col_range, p_global, key, device=0):
@@ -364,10 +377,52 @@ def loopback_dist(rank, world, col_range, p_global, key, device=0):
     return _dist(rank, world, device, key, col_range, p_global, 1)
 
 
-def _dist(rank, world, device, key, col_range, p_global, backend):
+def _dist(rank, world, device, key, col_range, p_global, backend, timeout_ms=0):
     key = bytes(key)
     assert len(key) == 128
     buf = ctypes.create_string_buffer(key, 128)
-    d = bl_dist(rank, world, device, ctypes.cast(buf, ctypes.c_void_p), int(col_range[0]), int(p_global), backend)
+    d = bl_dist(rank, world, device, ctypes.cast(buf, ctypes.c_void_p), int(col_range[0]), int(p_global), backend,
+                None, int(timeout_ms))
     d._key_buf = buf          # keep the id alive with the struct
+    return d
+
+
+def host_coll_dist(rank, world, col_range, p_global, allgather, bcast, allreduce_sum, device=0):
+    """bl_dist of the host-collective backend (bl_dist.backend = 2): the library stages each
+    collective in host memory and calls back into Python --
+      allgather(send: bytes) -> bytes (world x len(send), rank order)
+      bcast(buf: bytearray, root) -> None (in place)
+      allreduce_sum(v: np.ndarray float64) -> None (in place)
+    e.g. implemented with torch.distributed over gloo between processes (marshalling only)."""
+    def ag(ctx, send, recv, nbytes):
+        try:
+            out = allgather(ctypes.string_at(send, nbytes) if nbytes else b"")
+            assert len(out) == world * nbytes
+            if nbytes:
+                ctypes.memmove(recv, out, world * nbytes)
+            return 0
+        except Exception:  # noqa: BLE001 -- reported to the library as a failed collective
+            return 1
+
+    def bc(ctx, buf, nbytes, root):
+        try:
+            b = bytearray(ctypes.string_at(buf, nbytes)) if nbytes else bytearray()
+            bcast(b, root)
+            if nbytes:
+                ctypes.memmove(buf, bytes(b), nbytes)
+            return 0
+        except Exception:  # noqa: BLE001
+            return 1
+
+    def ar(ctx, buf, count):
+        try:
+            v = np.ctypeslib.as_array(ctypes.cast(buf, ctypes.POINTER(ctypes.c_double)), shape=(int(count),))
+            allreduce_sum(v)
+            return 0
+        except Exception:  # noqa: BLE001
+            return 1
+
+    hc = bl_host_coll(None, _ALLGATHER(ag), _BCAST(bc), _ALLREDUCE(ar))
+    d = bl_dist(rank, world, device, None, int(col_range[0]), int(p_global), 2, ctypes.pointer(hc), 0)
+    d._hc = hc                # the callbacks must outlive every call on the design
     return d

@@ -150,32 +150,99 @@ int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 }  // namespace
 
 // ------------------------------------------------------------ communicators
-// Collectives of the sharded path.  Every call is collective,
-// runs on stream `st` and returns with the stream synchronised (the host
-// decides on the result).  Payloads are small except the broadcast of the
-// columns entering the working set.
+// Collectives of the sharded path.  Every call is collective and
+// ENQUEUED on stream `st` (the result is valid for later work on st); wait(st) blocks the
+// host until st is done -- with NCCL it also polls the communicator's asynchronous error
+// and aborts it after the timeout.  group_begin/end batch the calls between them into one
+// launch (NCCL groups).  Payloads are small except the broadcast of the columns entering
+// the working set.
 struct Comm {
     int rank = 0, world = 1;
     virtual ~Comm() {}
     virtual void allgather(const void *send, void *recv, size_t bytes, cudaStream_t st) = 0;   // recv: world * bytes
     virtual void bcast(void *buf, size_t bytes, int root, cudaStream_t st) = 0;
     virtual void allreduce_sum(double *buf, size_t count, cudaStream_t st) = 0;
+    virtual void group_begin() {}
+    virtual void group_end() {}
+    virtual void wait(cudaStream_t st) { CK(cudaStreamSynchronize(st)); }
 };
 
 struct NcclComm : Comm {
     ncclComm_t c = nullptr;
+    int timeout_ms = 600000;
     ~NcclComm() override { if (c) ncclCommDestroy(c); }
+    ncclComm_t live() {
+        if (!c) raise(BL_ERR_NCCL, "the NCCL communicator was aborted by an earlier error or timeout");
+        return c;
+    }
     void allgather(const void *send, void *recv, size_t bytes, cudaStream_t st) override {
-        CKN(ncclAllGather(send, recv, bytes, ncclUint8, c, st));
-        CK(cudaStreamSynchronize(st));
+        CKN(ncclAllGather(send, recv, bytes, ncclUint8, live(), st));
     }
     void bcast(void *buf, size_t bytes, int root, cudaStream_t st) override {
-        CKN(ncclBroadcast(buf, buf, bytes, ncclUint8, root, c, st));
-        CK(cudaStreamSynchronize(st));
+        CKN(ncclBroadcast(buf, buf, bytes, ncclUint8, root, live(), st));
     }
     void allreduce_sum(double *buf, size_t count, cudaStream_t st) override {
-        CKN(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, c, st));
+        CKN(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, live(), st));
+    }
+    void group_begin() override { CKN(ncclGroupStart()); }
+    void group_end() override { CKN(ncclGroupEnd()); }
+    void wait(cudaStream_t st) override {
+        const auto t0 = std::chrono::steady_clock::now();
+        for (int spin = 0;; spin++) {
+            const cudaError_t e = cudaStreamQuery(st);
+            if (e == cudaSuccess) return;
+            if (e != cudaErrorNotReady) {
+                cudaGetLastError();
+                raise(BL_ERR_CUDA, "stream of a collective: %s", cudaGetErrorString(e));
+            }
+            ncclResult_t ae = ncclSuccess;
+            if (c && ncclCommGetAsyncError(c, &ae) == ncclSuccess && ae != ncclSuccess && ae != ncclInProgress) {
+                ncclCommAbort(c);
+                c = nullptr;
+                raise(BL_ERR_NCCL, "NCCL asynchronous error: %s (communicator aborted)", ncclGetErrorString(ae));
+            }
+            const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+            if (ms > timeout_ms) {
+                if (c) ncclCommAbort(c);
+                c = nullptr;
+                raise(BL_ERR_NCCL, "a collective did not complete within %d ms (peer lost?); communicator aborted", timeout_ms);
+            }
+            if (spin > 256) std::this_thread::sleep_for(std::chrono::microseconds(20));
+        }
+    }
+};
+
+// Caller-supplied host collectives (bl_dist.backend = 2, e.g. gloo or MPI between processes):
+// each payload is staged through host memory around the caller's function.
+struct HostComm : Comm {
+    bl_host_coll hc{};
+    std::vector<char> a, b;
+    void stage_in(const void *dev, size_t bytes, cudaStream_t st) {
+        a.resize(std::max<size_t>(bytes, 1));
+        if (bytes) CK(cudaMemcpyAsync(a.data(), dev, bytes, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
+    }
+    void stage_out(void *dev, const void *host, size_t bytes, cudaStream_t st) {
+        if (bytes) CK(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));                  // the staging buffers are reused by the next call
+    }
+    void allgather(const void *send, void *recv, size_t bytes, cudaStream_t st) override {
+        stage_in(send, bytes, st);
+        b.resize(std::max<size_t>(bytes * world, 1));
+        if (hc.allgather(hc.ctx, a.data(), b.data(), (int64_t)bytes) != 0) raise(BL_ERR_NCCL, "host allgather failed");
+        stage_out(recv, b.data(), bytes * world, st);
+    }
+    void bcast(void *buf, size_t bytes, int root, cudaStream_t st) override {
+        if (rank == root) stage_in(buf, bytes, st);
+        else a.resize(std::max<size_t>(bytes, 1));
+        if (hc.bcast(hc.ctx, a.data(), (int64_t)bytes, root) != 0) raise(BL_ERR_NCCL, "host broadcast failed");
+        if (rank != root) stage_out(buf, a.data(), bytes, st);
+    }
+    void allreduce_sum(double *buf, size_t count, cudaStream_t st) override {
+        stage_in(buf, 8 * count, st);
+        if (hc.allreduce_sum_f64(hc.ctx, reinterpret_cast<double *>(a.data()), (int64_t)count) != 0)
+            raise(BL_ERR_NCCL, "host allreduce failed");
+        stage_out(buf, a.data(), 8 * count, st);
     }
 };
 
@@ -279,7 +346,7 @@ struct bl_path {
     std::vector<int32_t> outer;                          // logistic path: IRLS iterations (last solve) per lambda
     int family = 0;
     bl_perf perf;
-    int64_t cd_visits = 0, cd_updates = 0, cd_cycles = 0, cd_prof[4] = {0, 0, 0, 0}, cd_cnt[4] = {0, 0, 0, 0},
+    int64_t cd_visits = 0, cd_updates = 0, cd_cycles = 0, cd_prof[4] = {0, 0, 0, 0}, cd_cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0},
             cd_dbg[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 };
 
@@ -296,6 +363,14 @@ struct bl_cvres {
 
 // Per-(y, row mask) device workspace: one arena allocation carved into the
 // vectors the path needs.
+constexpr int kXPre = 1024;   // list entries a round exchange carries per rank (C3)
+struct RoundX {               // one KKT round of a sharded fit, combined over the ranks (C3)
+    std::vector<int64_t> nviol, nstrong;        // per rank
+    int64_t nscope = 0, nsafe = 0;
+    std::vector<int> viol, strong;              // sorted GLOBAL indices (when *_ok)
+    bool viol_ok = false, strong_ok = false;    // every rank's list fit in the exchange
+};
+
 struct bl_prep {
     uint32_t magic;
     bl_design *d;
@@ -359,9 +434,12 @@ struct bl_prep {
     int *widx;              // identity 0..ws_cap-1 (slot -> column of the store)
     int64_t ws_cap;
     int star_root;          // rank owning x_* (sharded)
+    RoundX xr;              // sharded: the last round exchange
     double batch_bytes;     // lockstep CV: X bytes read by the batched scans this fit timed
+    int batch_passes;       // ... batched launches of the current round
     int cd_mode;            // 0 auto (Gram when |W| <= 4096), 1 residual, 2 Gram
     int cd_cluster;         // CTAs per Gram-CD cluster (4, 8, 16)
+    int cd_newton;          // Newton (CG) steps on settled active sets in the Gram CD
     int fault_strong_drop;  // TEST ONLY (bl_opts): admit no strong-rule candidate in advance
     size_t chunk_bytes;     // out-of-core: bytes per streamed chunk (the buffers are sized for it)
     cudaStream_t own;       // library stream (used when the caller passes none)
@@ -813,7 +891,8 @@ std::vector<int64_t> gather_i64(bl_prep *pp, const int64_t *mine, int k) {
     CK(cudaMemcpyAsync(buf, mine, 8 * (size_t)k, cudaMemcpyHostToDevice, pp->stream));
     d->comm->allgather(buf, buf + k, 8 * (size_t)k, pp->stream);
     std::vector<int64_t> all((size_t)k * d->world);
-    CK(cudaMemcpy(all.data(), buf + k, 8 * (size_t)k * d->world, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpyAsync(all.data(), buf + k, 8 * (size_t)k * d->world, cudaMemcpyDeviceToHost, pp->stream));
+    d->comm->wait(pp->stream);
     return all;
 }
 // every rank's local index list (device, counts[r] entries on rank r) -> sorted GLOBAL indices
@@ -828,7 +907,8 @@ std::vector<int> gather_list(bl_prep *pp, const int *dev, const std::vector<int6
     if (mine) CK(cudaMemcpyAsync(buf, dev, 4 * (size_t)mine, cudaMemcpyDeviceToDevice, pp->stream));
     d->comm->allgather(buf, buf + mx, 4 * (size_t)mx, pp->stream);
     ensure_host(pp->hlist, pp->hlist_cap, (size_t)mx * d->world);
-    CK(cudaMemcpy(pp->hlist, buf + mx, 4 * (size_t)mx * d->world, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpyAsync(pp->hlist, buf + mx, 4 * (size_t)mx * d->world, cudaMemcpyDeviceToHost, pp->stream));
+    d->comm->wait(pp->stream);
     out.reserve(tot);
     for (int r = 0; r < d->world; r++)
         for (int64_t q = 0; q < counts[r]; q++) out.push_back(pp->hlist[(size_t)r * mx + q] + (int)d->shard_off[r]);
@@ -859,7 +939,7 @@ bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double a
     {
         const int cc = opts ? opts->cd_cluster : 0;
         if (cc != 0 && cc != 4 && cc != 8 && cc != 16) raise(BL_ERR_ARG, "cd_cluster must be 0, 4, 8 or 16 (got %d)", cc);
-        pp->cd_cluster = cc == 0 ? 8 : cc;
+        pp->cd_cluster = cc == 0 ? 16 : cc;   // one fit: 16 SMs (bl_cv's concurrent fits default to 8)
         if (opts && opts->stream_chunk_bytes < 0) raise(BL_ERR_ARG, "stream_chunk_bytes must be >= 0");
         const size_t cb = opts && opts->stream_chunk_bytes > 0 ? (size_t)opts->stream_chunk_bytes : kStreamChunkBytes;
         if (cb != pp->chunk_bytes && pp->sbuf[0]) {          // a reused workspace with other chunk buffers
@@ -867,6 +947,7 @@ bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double a
         }
         pp->chunk_bytes = cb;
         pp->fault_strong_drop = opts ? opts->fault_strong_drop : 0;
+        pp->cd_newton = opts ? opts->cd_accel == 0 : 1;
     }
     pp->nG = 0;
     pp->launches = 0;
@@ -1001,8 +1082,10 @@ bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double a
     else if (d->dt == DT_F32) launch_xstar<float>(pp);
     else launch_xstar<int8_t>(pp);
     if (d->sharded && pp->star_root >= 0) {      // C2: x_* - c_* (and its sum) from its owner
+        d->comm->group_begin();
         d->comm->bcast(pp->vtmp, 8 * (size_t)pp->vlen, pp->star_root, st);
         d->comm->bcast(&pp->ps->sum_v, 8, pp->star_root, st);
+        d->comm->group_end();
     }
     {
         ScanArgs sa{};
@@ -1018,7 +1101,8 @@ bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double a
     CK(cudaMemcpyAsync(&pp->st->sumr, &pp->ps->sum_yt, sizeof(double), cudaMemcpyDeviceToDevice, st));
     // the one host round trip of preprocessing: the scalars the lambda loop branches on
     CK(cudaMemcpyAsync(&pp->hps, pp->ps, sizeof(PrepScalars), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    if (d->world > 1) d->comm->wait(st);                 // (collectives above: error / timeout aware)
+    else CK(cudaStreamSynchronize(st));
     pp->prep_bytes = 3.0 * (double)d->n * itemsize(d->dt) * (double)d->p;
     if (!(pp->hps.Y2 > 0.0)) raise(BL_ERR_DEGENERATE, "y is constant on the used rows (y~ == 0)");
     if (pp->hps.n_live == 0 && (d->world == 1 || d->sharded)) raise(BL_ERR_DEGENERATE, "every column has zero variance");
@@ -1086,22 +1170,33 @@ void upload_W(bl_prep *pp, const WorkingSet &ws, const std::vector<int> &added) 
         const size_t isz = itemsize(d->dt), colb = (size_t)d->ld * isz;
         CK(cudaMemsetAsync(pp->bw + slot0, 0, 8 * added.size(), st));
         size_t q = 0;
-        for (int r = 0; r < d->world; r++) {
+        // the pack kernel of this rank's columns first, then ONE group of broadcasts (every owner's
+        // columns, c and s): a single launch per round, nothing waited for on the host
+        const int nsh = (int)d->shard_off.size() - 1;      // shards (1 for a replicated design)
+        const int mine_r = d->sharded ? d->rank : 0;
+        for (int r = 0; r < nsh; r++) {
+            const size_t q0 = q;
+            while (q < added.size() && added[q] < d->shard_off[r + 1]) q++;
+            const int k = (int)(q - q0);
+            if (k == 0 || r != mine_r) continue;
+            k_pack_cols<<<k, 256, 0, st>>>((const char *)d->X, (int64_t)colb, pp->viol, k, pp->c, pp->s,
+                                           (char *)pp->Xw, pp->cw, pp->sw, pp->bw, (int)(slot0 + q0));
+            CKL();
+            pp->launches++;
+        }
+        if (!d->sharded) return;
+        q = 0;
+        d->comm->group_begin();
+        for (int r = 0; r < nsh; r++) {
             const size_t q0 = q;
             while (q < added.size() && added[q] < d->shard_off[r + 1]) q++;
             const int k = (int)(q - q0);
             if (k == 0) continue;
-            if (r == d->rank) {
-                k_pack_cols<<<k, 256, 0, st>>>((const char *)d->X, (int64_t)colb, pp->viol, k, pp->c, pp->s,
-                                               (char *)pp->Xw, pp->cw, pp->sw, pp->bw, (int)(slot0 + q0));
-                CKL();
-                pp->launches++;
-            }
-            if (!d->sharded) continue;
             d->comm->bcast((char *)pp->Xw + (size_t)(slot0 + q0) * colb, colb * k, r, st);
             d->comm->bcast(pp->cw + slot0 + q0, 8 * (size_t)k, r, st);
             d->comm->bcast(pp->sw + slot0 + q0, 8 * (size_t)k, r, st);
         }
+        d->comm->group_end();
     }
 }
 
@@ -1141,6 +1236,54 @@ std::vector<int> global_list(bl_prep *pp, const int *dev, int count) {
     if (!pp->d->sharded) return read_list(pp, dev, count);
     const int64_t c = count;
     return gather_list(pp, dev, gather_i64(pp, &c, 1));
+}
+
+// C3 for several fits in ONE collective: every rank's round counts (nviol, nstrong, nscope,
+// nsafe -- the first four ints of RoundStatus) and the first kXPre entries of both of its
+// lists, for every fit, all-gathered on stream st (where the rounds' results were written).
+// A list longer than kXPre on some rank is gathered in full afterwards (gather_list).
+void exchange_rounds(bl_design *d, const std::vector<bl_prep *> &fits, cudaStream_t st) {
+    const size_t F = fits.size(), rec = 4 + 2 * (size_t)kXPre;
+    if (F == 0) return;
+    bl_prep *p0 = fits[0];
+    int *buf = (int *)ensure_cbuf(p0, 4 * rec * F * (d->world + 1));
+    CK(cudaStreamSynchronize(p0->stream));               // ensure_cbuf may have swapped the buffer on p0's stream
+    for (size_t u = 0; u < F; u++) {
+        bl_prep *pp = fits[u];
+        const size_t m = (size_t)std::min<int64_t>(kXPre, pp->p);
+        int *r0 = buf + u * rec;
+        CK(cudaMemcpyAsync(r0, pp->st, 4 * sizeof(int), cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(r0 + 4, pp->viol, 4 * m, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(r0 + 4 + kXPre, pp->strong, 4 * m, cudaMemcpyDeviceToDevice, st));
+    }
+    d->comm->allgather(buf, buf + rec * F, 4 * rec * F, st);
+    ensure_host(p0->hlist, p0->hlist_cap, rec * F * d->world);
+    CK(cudaMemcpyAsync(p0->hlist, buf + rec * F, 4 * rec * F * d->world, cudaMemcpyDeviceToHost, st));
+    d->comm->wait(st);
+    const int *h = p0->hlist;
+    for (size_t u = 0; u < F; u++) {
+        RoundX &x = fits[u]->xr;
+        x.nviol.assign(d->world, 0);
+        x.nstrong.assign(d->world, 0);
+        x.nscope = x.nsafe = 0;
+        x.viol.clear();
+        x.strong.clear();
+        x.viol_ok = x.strong_ok = true;
+        for (int r = 0; r < d->world; r++) {
+            const int *q = h + ((size_t)r * F + u) * rec;
+            x.nviol[r] = q[0];
+            x.nstrong[r] = q[1];
+            x.nscope += q[2];
+            x.nsafe += q[3];
+            const int off = (int)d->shard_off[r];
+            if (q[0] > kXPre) x.viol_ok = false;
+            else for (int e = 0; e < q[0]; e++) x.viol.push_back(q[4 + e] + off);
+            if (q[1] > kXPre) x.strong_ok = false;
+            else for (int e = 0; e < q[1]; e++) x.strong.push_back(q[4 + kXPre + e] + off);
+        }
+        std::sort(x.viol.begin(), x.viol.end());
+        std::sort(x.strong.begin(), x.strong.end());
+    }
 }
 
 // CD block shape: rows per thread R <= RM in {4, 8, 16}; RM <= 8 kernels are
@@ -1346,14 +1489,15 @@ __global__ void k_logit_init(double *eta, int ld, const PrepScalars *ps, RoundSt
 // Workspace after G: G_AA (ldG^2), block inverses (32 ldG), then the cluster
 // kernel's global state: gradients, catch-up deltas (fp64), active list, catch-up
 // rows (int32), membership flags (bytes).
-size_t gram_ws_bytes(int64_t nl) { return (size_t)8 * nl * nl + (size_t)8 * 32 * nl + (size_t)8 * 2 * nl + (size_t)4 * 2 * nl + (size_t)nl + 64; }
+size_t gram_ws_bytes(int64_t nl) { return (size_t)8 * nl * nl + (size_t)8 * 32 * nl + (size_t)8 * 7 * nl + (size_t)4 * 2 * nl + (size_t)nl + 64; }
 G7Work gram_ws(bl_prep *pp) {
     const int64_t nl = pp->ldG;
     double *base = pp->GA + nl * nl + 32 * nl;
     G7Work w;
     w.g = base;
     w.dl = base + nl;
-    w.act = reinterpret_cast<int *>(base + 2 * nl);
+    w.cg = base + 2 * nl;                                  // 5 nl: the Newton step's vectors (>= 4 (nW + 1))
+    w.act = reinterpret_cast<int *>(base + 7 * nl);
     w.rl = w.act + nl;
     w.inA = reinterpret_cast<uint8_t *>(w.rl + nl);
     return w;
@@ -1490,6 +1634,8 @@ void solve_logit_g7_t(bl_prep *pp, int nW, double lam, double alpha, double tol,
     ga.st = pp->st;
     ga.tau = ws + nW;
     ga.idv = alpha < 1.0 ? ws + 3 * (size_t)nW : nullptr;
+    ga.nu = 0.0;
+    ga.newton = 0;                             // per-slot thresholds / curvatures: plain sweeps
     const int R = pp->cd_cluster;   // CTA 0 leads, 1..R-1 own the gradients
     const void *kern = gram7_kernel(alpha < 1.0, R);
     const size_t smem = gram7_smem(nW, R);
@@ -1569,7 +1715,7 @@ void solve_logit(bl_prep *pp, int nW, double lam, double alpha, double tol, int 
 
 
 void solve_cd(bl_prep *pp, int nW, double lam, double alpha, double tol, int max_iter) {
-    if (!use_gram(pp, nW)) {
+    if (nW == 0 || !use_gram(pp, nW)) {        // (an empty W -- possible under fault injection -- is a no-op solve)
         launch_cd(pp, nW, lam, alpha, tol, max_iter);
         return;
     }
@@ -1614,6 +1760,10 @@ void solve_cd(bl_prep *pp, int nW, double lam, double alpha, double tol, int max
     ga.c = v.c;
     ga.s = v.s;
     ga.st = pp->st;
+    ga.tau = nullptr;
+    ga.idv = nullptr;
+    ga.nu = lam * (1.0 - alpha);
+    ga.newton = pp->cd_newton;
     // cluster Gram CD: R CTAs of 256 threads (CTA 0 leads, 1..R-1 own the gradients)
     const int R = pp->cd_cluster;   // CTA 0 leads, 1..R-1 own the gradients
     const void *kern = gram7_kernel(alpha < 1.0, R);
@@ -1794,34 +1944,39 @@ struct PathRun {
         out->cd_updates += pp->hst->cd_updates;
         out->cd_cycles += pp->hst->cd_cycles;
         for (int u = 0; u < 4; u++) out->cd_prof[u] += pp->hst->cd_prof[u];
-        for (int u = 0; u < 4; u++) out->cd_cnt[u] += pp->hst->cd_cnt[u];
+        for (int u = 0; u < 8; u++) out->cd_cnt[u] += pp->hst->cd_cnt[u];
         for (int u = 0; u < 8; u++) out->cd_dbg[u] += pp->hst->cd_dbg[u];
     }
     // after the round's status reached pp->hst: 0 = lambda done, 1 = re-solve, -1 = error (status set).
-    // `dense`: the scan covered every live column (batched CV scan).
-    int after_scan(bool dense = false) {
+    // `batched`: the round's scan was a fold-batched launch shared with other fits (its columns --
+    // the union scope -- are in RoundStatus.nscope; it is timed on the batch's first fit only).
+    int after_scan(bool batched = false) {
         bl_design *d = pp->d;
         count_cd();
         if (screen == BL_SCREEN_NONE) {
             if (pp->hst->cd_status) { status = BL_ERR_CONVERGENCE; return -1; }
             return 0;
         }
-        // the round's counts over all shards (C3): violators, strong candidates, columns scanned
-        std::vector<int64_t> cnt = {pp->hst->nviol, pp->hst->nstrong, pp->hst->nscope, pp->hst->nsafe};
-        if (d->sharded) cnt = gather_i64(pp, cnt.data(), 4);
+        // the round's counts over all shards (C3, exchanged by exchange_rounds before this call):
+        // violators, strong candidates, columns scanned
         int64_t nviol = 0, nscope = 0, nsafe = 0;
-        std::vector<int64_t> cv(d->sharded ? d->world : 1), cs(cv.size());
-        for (size_t r = 0; r < cv.size(); r++) {
-            cv[r] = cnt[4 * r];
-            cs[r] = cnt[4 * r + 1];
-            nviol += cnt[4 * r];
-            nscope += cnt[4 * r + 2];
-            nsafe += cnt[4 * r + 3];
+        std::vector<int64_t> cv, cs;
+        if (d->sharded) {
+            const RoundX &x = pp->xr;
+            cv = x.nviol;
+            cs = x.nstrong;
+            for (int64_t v : cv) nviol += v;
+            nscope = x.nscope;
+            nsafe = x.nsafe;
+        } else {
+            nviol = pp->hst->nviol;
+            nscope = pp->hst->nscope;
+            nsafe = pp->hst->nsafe;
         }
         nsafe_k = bedpp_skipped ? (int64_t)pp->hps.n_live : nsafe;
-        const int64_t round_cols = (use_bedpp && !dense) ? nscope : pp->hps.n_live;
+        const int64_t round_cols = use_bedpp ? nscope : pp->hps.n_live;
         scanned += round_cols;
-        if (!dense && pp->scan_full.size() < pp->ev_scan.size())   // classify the timed scan launch of this round
+        if (!batched && pp->scan_full.size() < pp->ev_scan.size())   // classify the timed scan launch of this round
             pp->scan_full.push_back(round_cols == pp->hps.n_live ? (use_bedpp ? (int64_t)pp->hst->nscope : pp->p) : -1);
         if (use_bedpp && nsafe == pp->hps.n_live) use_bedpp = 0;   // BEDPP keeps everything from here on
         if (pp->hst->cd_status) { status = BL_ERR_CONVERGENCE; return -1; }
@@ -1831,11 +1986,13 @@ struct PathRun {
                 status = BL_ERR_CONVERGENCE;
                 return -1;
             }
-            std::vector<int> v = d->sharded ? gather_list(pp, pp->viol, cv) : round_list(pp, 0, pp->hst->nviol);
+            std::vector<int> v = !d->sharded ? round_list(pp, 0, pp->hst->nviol)
+                                 : pp->xr.viol_ok ? pp->xr.viol : gather_list(pp, pp->viol, cv);
             upload_W(pp, W, W.add(v));
             return 1;
         }
-        strong_next = d->sharded ? gather_list(pp, pp->strong, cs) : round_list(pp, 1, pp->hst->nstrong);
+        strong_next = !d->sharded ? round_list(pp, 1, pp->hst->nstrong)
+                      : pp->xr.strong_ok ? pp->xr.strong : gather_list(pp, pp->strong, cs);
         return 0;
     }
     void fail() {
@@ -1921,6 +2078,7 @@ bl_status run_path(bl_prep *pp, const double *lambda, int K, double alpha, doubl
             if (screen != BL_SCREEN_NONE) launch_scan(pp, pr.scan_args(), pp->rscan, true);
             copy_round(pp, st);
             CK(cudaStreamSynchronize(st));
+            if (pp->d->sharded && screen != BL_SCREEN_NONE) exchange_rounds(pp->d, {pp}, st);
             res = pr.after_scan();
         } while (res == 1);
         if (res < 0) { pr.fail(); break; }
@@ -1965,7 +2123,7 @@ void finish_perf(bl_prep *pp, bl_path *out, double wall_ms) {
     pf.cd_updates = out->cd_updates;
     pf.cd_kernel_cycles = out->cd_cycles;
     for (int u = 0; u < 4; u++) pf.cd_prof[u] = out->cd_prof[u];
-    for (int u = 0; u < 4; u++) pf.cd_events[u] = out->cd_cnt[u];
+    for (int u = 0; u < 8; u++) pf.cd_events[u] = out->cd_cnt[u];
     for (int u = 0; u < 8; u++) pf.cd_sub[u] = out->cd_dbg[u];
     pf.wall_ms = wall_ms;
 }
@@ -2003,7 +2161,7 @@ const void *batch_mma_kernel_n(bool f64, int nb) {
     return f64 ? (const void *)k_scan_batch_mma<double, NF> : (const void *)k_scan_batch_mma<float, NF>;
 }
 void launch_scan_batch(bl_design *d, const std::vector<LockFit *> &fits, cudaStream_t sst, FitScan *dfs,
-                       FitScan *hfs, bl_prep *timer, bool mma) {
+                       FitScan *hfs, bl_prep *timer, bool mma, const int *list, const int *lctl) {
     const size_t nf = fits.size();
     for (size_t u = 0; u < nf; u++) {
         bl_prep *pp = fits[u]->pp;
@@ -2043,10 +2201,10 @@ void launch_scan_batch(bl_design *d, const std::vector<LockFit *> &fits, cudaStr
         int64_t ld = d->ld, p = d->p;
         int n = (int)d->n;
         FitScan *fp = dfs + u0;
-        void *args[] = {&X, &ld, &n, &p, &fp, &nb};
+        void *args[] = {&X, &ld, &n, &p, &fp, &nb, &list, &lctl};
         CK(cudaLaunchKernel(kern, dim3(grid), dim3(threads), args, smem, sst));
         timer->launches++;
-        timer->batch_bytes += (double)d->n * itemsize(d->dt) * (double)d->p;
+        timer->batch_passes++;                           // X bytes: accounted once the union size is known
     }
     if (timer->profile) {
         CK(cudaEventRecord(e1, sst));
@@ -2064,10 +2222,14 @@ void cv_lockstep(bl_design *d, const double *y, const std::vector<int32_t> &fold
     bl_opts fo{};
     if (opts) fo = *opts;
     fo.stream = nullptr;                                   // every fit on its own library stream
+    if (fo.cd_cluster == 0) fo.cd_cluster = 8;             // K + 1 concurrent CD clusters share the SMs
     const int rounds = opts && opts->max_kkt_rounds > 0 ? opts->max_kkt_rounds : 10;
     std::vector<LockFit> fits(F);
     cudaStream_t sst = nullptr;
     FitScan *dfs = nullptr, *hfs = nullptr;
+    int *uni = nullptr;                                    // [count, use_list, list (p)]: the union BEDPP scope
+    void **dptr = nullptr, **hptr = nullptr;               // per pending fit: flags, nlive, RoundStatus pointers
+    int *hctl = nullptr;                                   // pinned: the round's [count, use_list]
     const bool batched = d->dt != DT_I8;
     const bool mma = !opts || opts->cv_mode == 0;         // fold-batched scan on the fp64 tensor cores
     auto t0 = std::chrono::steady_clock::now();
@@ -2080,11 +2242,19 @@ void cv_lockstep(bl_design *d, const double *y, const std::vector<int32_t> &fold
         }
         if (dfs) cache::dfree(dfs);
         if (hfs) cache::hfree(hfs);
+        if (uni) cache::dfree(uni);
+        if (dptr) cache::dfree(dptr);
+        if (hptr) cache::hfree(hptr);
+        if (hctl) cache::hfree(hctl);
         if (sst) cudaStreamDestroy(sst);
     };
     try {
         CK(cudaStreamCreateWithFlags(&sst, cudaStreamNonBlocking));
         CK(cache::dmalloc((void **)&dfs, sizeof(FitScan) * std::max<size_t>(F, 1)));
+        CK(cache::dmalloc((void **)&uni, sizeof(int) * (size_t)(d->p + 2)));
+        CK(cache::dmalloc((void **)&dptr, 3 * sizeof(void *) * std::max<size_t>(F, 1)));
+        CK(cache::hmalloc((void **)&hptr, 3 * sizeof(void *) * std::max<size_t>(F, 1)));
+        CK(cache::hmalloc((void **)&hctl, 2 * sizeof(int)));
         CK(cache::hmalloc((void **)&hfs, sizeof(FitScan) * std::max<size_t>(F, 1)));
         for (size_t u = 0; u < F; u++) {
             LockFit &lf = fits[u];
@@ -2126,15 +2296,43 @@ void cv_lockstep(bl_design *d, const double *y, const std::vector<int32_t> &fold
                 }
                 if (batched) {
                     for (LockFit *lf : pending) CK(cudaStreamWaitEvent(sst, lf->solved, 0));
-                    launch_scan_batch(d, pending, sst, dfs, hfs, timer, mma);
+                    // the union of the pending fits' BEDPP scopes: near lambda_max BEDPP
+                    // discards most columns for every fit, and only the union is read
+                    const size_t np_ = pending.size();
+                    for (size_t u = 0; u < np_; u++) {
+                        hptr[u] = pending[u]->pp->flags;
+                        hptr[np_ + u] = pending[u]->pp->nlive;
+                        hptr[2 * np_ + u] = pending[u]->pp->st;
+                    }
+                    CK(cudaMemcpyAsync(dptr, hptr, 3 * sizeof(void *) * np_, cudaMemcpyHostToDevice, sst));
+                    CK(cudaMemsetAsync(uni, 0, 2 * sizeof(int), sst));
+                    {
+                        const int ug = (int)std::min<int64_t>((d->p + 255) / 256, (int64_t)d->nsm * 8);
+                        k_scope_union<<<ug, 256, 0, sst>>>(d->p, (const uint8_t *const *)dptr, (int)np_, uni + 2, uni);
+                        CKL();
+                        k_scope_finish<<<1, 32, 0, sst>>>(d->p, uni, (const int *const *)(dptr + np_), (int)np_,
+                                                          (RoundStatus *const *)(dptr + 2 * np_), uni + 1);
+                        CKL();
+                        timer->launches += 2;
+                    }
+                    timer->batch_passes = 0;
+                    launch_scan_batch(d, pending, sst, dfs, hfs, timer, mma, uni + 2, uni);
                     for (LockFit *lf : pending) copy_round(lf->pp, sst);
+                    CK(cudaMemcpyAsync(hctl, uni, 2 * sizeof(int), cudaMemcpyDeviceToHost, sst));
                     CK(cudaStreamSynchronize(sst));
+                    const int64_t cols = hctl[1] ? hctl[0] : d->p;
+                    timer->batch_bytes += (double)timer->batch_passes * (double)d->n * itemsize(d->dt) * (double)cols;
                 } else {
                     for (LockFit *lf : pending) {
                         launch_scan(lf->pp, lf->run->scan_args(), lf->pp->rscan, true);
                         copy_round(lf->pp, lf->pp->stream);
                     }
                     for (LockFit *lf : pending) CK(cudaStreamSynchronize(lf->pp->stream));
+                }
+                if (d->sharded) {                           // C3 for every pending fit in one collective
+                    std::vector<bl_prep *> pps;
+                    for (LockFit *lf : pending) pps.push_back(lf->pp);
+                    exchange_rounds(d, pps, sst);
                 }
                 std::vector<LockFit *> again;
                 for (LockFit *lf : pending) {
@@ -2216,7 +2414,7 @@ void add_perf(bl_cvres *cv, const bl_perf &p) {
     q.kernel_launches += p.kernel_launches; q.wall_ms = std::max(q.wall_ms, p.wall_ms);
     q.cd_visits += p.cd_visits; q.cd_updates += p.cd_updates; q.cd_kernel_cycles += p.cd_kernel_cycles;
     for (int u = 0; u < 4; u++) q.cd_prof[u] += p.cd_prof[u];
-    for (int u = 0; u < 4; u++) q.cd_events[u] += p.cd_events[u];
+    for (int u = 0; u < 8; u++) q.cd_events[u] += p.cd_events[u];
     for (int u = 0; u < 8; u++) q.cd_sub[u] += p.cd_sub[u];
 }
 
@@ -2343,7 +2541,8 @@ bl_status bl_load_design(const void *X, bl_dtype dt, int64_t n, int64_t p_local,
         d->shard_off[1] = p_local;
         if (d->world > 1) {
             try {
-                if (!dist->nccl_unique_id) raise(BL_ERR_ARG, "nccl_unique_id (or loopback group key) required for world > 1");
+                if (!dist->nccl_unique_id && dist->backend != 2)
+                    raise(BL_ERR_ARG, "nccl_unique_id (or loopback group key) required for world > 1");
                 if (dist->backend == 1) {
                     auto *lc = new LoopComm();
                     d->comm = lc;
@@ -2367,7 +2566,17 @@ bl_status bl_load_design(const void *X, bl_dtype dt, int64_t n, int64_t p_local,
                     nc->world = d->world;
                     ncclUniqueId id;
                     std::memcpy(&id, dist->nccl_unique_id, sizeof id);
+                    nc->timeout_ms = dist->timeout_ms > 0 ? dist->timeout_ms : 600000;
                     CKN(ncclCommInitRank(&nc->c, d->world, id, d->rank));
+                } else if (dist->backend == 2) {
+                    if (!dist->host_coll || !dist->host_coll->allgather || !dist->host_coll->bcast ||
+                        !dist->host_coll->allreduce_sum_f64)
+                        raise(BL_ERR_ARG, "backend 2 needs host_coll with allgather, bcast and allreduce_sum_f64");
+                    auto *hc = new HostComm();
+                    d->comm = hc;
+                    hc->rank = d->rank;
+                    hc->world = d->world;
+                    hc->hc = *dist->host_coll;
                 } else {
                     raise(BL_ERR_ARG, "bad bl_dist backend %d", dist->backend);
                 }
@@ -2378,6 +2587,7 @@ bl_status bl_load_design(const void *X, bl_dtype dt, int64_t n, int64_t p_local,
                 CK(cudaMemcpy(dbuf, mine, 16, cudaMemcpyHostToDevice));
                 std::vector<int64_t> all(2 * (size_t)d->world);
                 d->comm->allgather(dbuf, dbuf + 2, 16, 0);
+                d->comm->wait(0);
                 CK(cudaMemcpy(all.data(), dbuf + 2, 16 * (size_t)d->world, cudaMemcpyDeviceToHost));
                 cache::dfree(dbuf);
                 d->shard_off.assign(d->world + 1, 0);
@@ -2616,6 +2826,7 @@ bl_status bl_cv(bl_design *d, const double *y, const double *lambda, int n_lambd
         bl_opts fo_opts{};
         if (opts) fo_opts = *opts;
         fo_opts.stream = nullptr;                       // each fold on its own library stream
+        if (fo_opts.cd_cluster == 0) fo_opts.cd_cluster = 8;   // K + 1 concurrent CD clusters share the SMs
         auto run_fold = [&](size_t idx) {
             try {
                 CK(cudaSetDevice(d->device));
@@ -2673,6 +2884,7 @@ bl_status bl_cv(bl_design *d, const double *y, const double *lambda, int n_lambd
         if (d->world > 1 && !d->sharded) {            // replicated: each rank ran its own folds
             std::lock_guard<std::mutex> lk(d->comm_mu);
             d->comm->allreduce_sum(dE, (size_t)n_lambda * n, 0);
+            d->comm->wait(0);
         }
         k_cv_reduce<<<n_lambda, 256>>>(dE, (int)n, dcv, dcv + n_lambda);
         CKL();

@@ -43,7 +43,8 @@ struct RoundStatus {
     long long cd_visits, cd_updates;   // coordinate visits / nonzero updates of the last solve
     long long cd_cycles;               // SM clock cycles inside the CD kernel (thread 0)
     long long cd_prof[4];              // Gram CD phase cycles: leader steps, bulk steps, G_AA/M builds, lazy catch-ups
-    long long cd_cnt[4];               // Gram CD events: speculation retries, G_AA builds, catch-ups, full sweeps
+    long long cd_cnt[8];               // Gram CD events: speculation retries, G_AA builds, catch-ups, full sweeps,
+                                       //   Newton steps, CG iterations, Newton cycles, partial (sign-limited) steps
     long long cd_dbg[8];               // Gram CD sub-phase cycles (micro-benchmarks only)
     double b0;                         // logistic path: intercept on the standardised scale (in/out)
     int outer, irls_done;              // logistic path: IRLS iterations of the last solve; converged flag
@@ -378,6 +379,31 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_fp(ScanArgs a) {
     }
 }
 
+// ------------------------- lockstep CV: the union of the fits' BEDPP scopes
+// Column j must be scanned in a round if any pending fit keeps it (safe at lambda_k or
+// lambda_{k+1}: flags & 3).  k_scope_union compacts those columns (any order: every
+// result of the scan is per column); k_scope_finish decides dense (the union covers more
+// than half the columns) or list mode for k_scan_batch*, and records the columns each fit
+// will have read in its RoundStatus.nscope (the local live count in dense mode).
+__global__ void __launch_bounds__(256) k_scope_union(int64_t p, const uint8_t *const *__restrict__ flags, int nf,
+                                                     int *__restrict__ list, int *__restrict__ count) {
+    for (int64_t j0 = (int64_t)blockIdx.x * blockDim.x; j0 < p; j0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = j0 + threadIdx.x;
+        bool any = false;
+        if (j < p)
+            for (int f = 0; f < nf && !any; f++) any = (flags[f][j] & 3) != 0;
+        warp_append(any, (int)j, list, count);
+    }
+}
+__global__ void k_scope_finish(int64_t p, const int *__restrict__ count, const int *const *__restrict__ nlive, int nf,
+                               RoundStatus *const *__restrict__ st, int *__restrict__ use_list) {
+    if (threadIdx.x != 0) return;
+    const int cnt = *count;
+    const int ul = 2 * (int64_t)cnt <= p;
+    *use_list = ul;
+    for (int f = 0; f < nf; f++) st[f]->nscope = ul ? cnt : *nlive[f];
+}
+
 // ------------------------- NEXT-1: fold-batched scan (lockstep cross-validation)
 // SURVEY 8(f) NEXT-1.  The K+1 fits of a CV scan the same X with different
 // residuals (each zero on its held-out rows) and fold-specific c, s (Q16); one
@@ -420,7 +446,8 @@ __host__ __device__ constexpr size_t batch_smem(int nf, int itemsize) {
 // NF = the exact number of fits of the launch (the fit loops unroll completely).
 template <typename T, int NF>
 __global__ void __launch_bounds__(kBatchThreads, 3) k_scan_batch(const T *__restrict__ X, int64_t ld, int n, int64_t p,
-                                                                  const FitScan *__restrict__ fits, int nf_unused) {
+                                                                  const FitScan *__restrict__ fits, int nf_unused,
+                                                                  const int *__restrict__ list, const int *__restrict__ lctl) {
     extern __shared__ __align__(16) double smb[];
     __shared__ FitScan fs[NF];
     __shared__ double k1s[NF];
@@ -432,8 +459,12 @@ __global__ void __launch_bounds__(kBatchThreads, 3) k_scan_batch(const T *__rest
     __syncthreads();
     if (threadIdx.x < NF) k1s[threadIdx.x] = *fs[threadIdx.x].K1;
     const int nchunk = (n + kBatchRows - 1) / kBatchRows;
-    for (int64_t g0 = (int64_t)blockIdx.x * kBatchTile; g0 < p; g0 += (int64_t)gridDim.x * kBatchTile) {
-        const int ntile = (int)min((int64_t)kBatchTile, p - g0);
+    // list mode (lctl = {count, use_list}): tile positions index the union scope list
+    if (list && !lctl[1]) list = nullptr;
+    const int64_t P = list ? (int64_t)lctl[0] : p;
+    auto colof = [&](int64_t pos) -> int64_t { return list ? (int64_t)list[pos] : pos; };
+    for (int64_t g0 = (int64_t)blockIdx.x * kBatchTile; g0 < P; g0 += (int64_t)gridDim.x * kBatchTile) {
+        const int ntile = (int)min((int64_t)kBatchTile, P - g0);
         // stage chunk c into ring slot b: residual rows of every fit, x rows of every tile column
         auto stage = [&](int c, int b) {
             double *rs = smb + (size_t)b * STAGE_D;
@@ -449,7 +480,7 @@ __global__ void __launch_bounds__(kBatchThreads, 3) k_scan_batch(const T *__rest
             constexpr int XC = kBatchRows / XE;                 // 16-byte copies per column
             for (int e = threadIdx.x; e < kBatchTile * XC; e += kBatchThreads) {
                 const int q = e / XC, i = (e - q * XC) * XE;
-                const T *src = X + (g0 + min(q, ntile - 1)) * ld + i0 + i;   // past-the-end columns: a valid column, ignored
+                const T *src = X + colof(g0 + min(q, ntile - 1)) * ld + i0 + i;   // past-the-end columns: a valid column, ignored
                 T *dst = xs + q * kBatchRows + i;
                 if (i0 + i + XE <= ld) cp_async16(dst, src);
                 else {
@@ -490,8 +521,8 @@ __global__ void __launch_bounds__(kBatchThreads, 3) k_scan_batch(const T *__rest
             }
         }
         cp_async_wait<0>();
-        const int64_t j0 = g0 + wid * 4;
-        const int nv = (int)max((int64_t)0, min((int64_t)4, p - j0));
+        const int64_t j0 = g0 + wid * 4;                       // tile position of this warp's first column
+        const int nv = (int)max((int64_t)0, min((int64_t)4, P - j0));
         if (nv == 0) continue;
 #pragma unroll
         for (int f = 0; f < NF; f++) {
@@ -503,7 +534,7 @@ __global__ void __launch_bounds__(kBatchThreads, 3) k_scan_batch(const T *__rest
             }
             const FitScan &F = fs[f];
             bool isv = false, iss = false;
-            const int64_t j = j0 + lane;
+            const int64_t j = lane < nv ? colof(j0 + lane) : 0;
             if (lane < nv) {
                 const double sj = F.s[j];
                 const double z = sj > 0.0 ? (d - F.c[j] * k1s[f]) * F.K2 / sj : 0.0;
@@ -567,7 +598,8 @@ template <> struct XFrag<double> {
 
 template <typename T, int NF>
 __global__ void __launch_bounds__(kBMThreads, 2) k_scan_batch_mma(const T *__restrict__ X, int64_t ld, int n, int64_t p,
-                                                                   const FitScan *__restrict__ fits, int nf_unused) {
+                                                                   const FitScan *__restrict__ fits, int nf_unused,
+                                                                   const int *__restrict__ list, const int *__restrict__ lctl) {
     extern __shared__ __align__(16) double smb[];
     __shared__ FitScan fs[NF];
     __shared__ double k1s[NF];
@@ -585,7 +617,11 @@ __global__ void __launch_bounds__(kBMThreads, 2) k_scan_batch_mma(const T *__res
     if (threadIdx.x < NF) k1s[threadIdx.x] = *fs[threadIdx.x].K1;
     const int nstage = (n + kBMRows - 1) / kBMRows;
     double *zw = Zs + (size_t)(32 * wid) * kBMZ;                 // this warp's 32 Z rows
-    for (int64_t col0 = (int64_t)blockIdx.x * kBMCols; col0 < p; col0 += (int64_t)gridDim.x * kBMCols) {
+    // list mode (lctl = {count, use_list}): tile positions index the union scope list
+    if (list && !lctl[1]) list = nullptr;
+    const int64_t P = list ? (int64_t)lctl[0] : p;
+    auto colof = [&](int64_t pos) -> int64_t { return list ? (int64_t)list[pos] : pos; };
+    for (int64_t col0 = (int64_t)blockIdx.x * kBMCols; col0 < P; col0 += (int64_t)gridDim.x * kBMCols) {
         auto stage = [&](int sidx, int b) {
             double *rs = ring + (size_t)b * NF * kBMStride;
             const int i0 = sidx * kBMRows;
@@ -601,7 +637,7 @@ __global__ void __launch_bounds__(kBMThreads, 2) k_scan_batch_mma(const T *__res
         // this lane's columns (clamped: past-the-end columns read a valid column, ignored)
         const T *xc[MT];
 #pragma unroll
-        for (int mt = 0; mt < MT; mt++) xc[mt] = X + min(col0 + 32 * wid + 8 * mt + g, p - 1) * ld;
+        for (int mt = 0; mt < MT; mt++) xc[mt] = X + colof(min(col0 + 32 * wid + 8 * mt + g, P - 1)) * ld;
         double acc[MT][NT][2];
         double accr[MT][NR > 0 ? NR : 1];
 #pragma unroll
@@ -699,8 +735,9 @@ __global__ void __launch_bounds__(kBMThreads, 2) k_scan_batch_mma(const T *__res
                 }
         }
         __syncwarp();
-        const int64_t j = col0 + 32 * wid + lane;
-        const bool inr = j < p;
+        const int64_t jp = col0 + 32 * wid + lane;             // tile position
+        const bool inr = jp < P;
+        const int64_t j = inr ? colof(jp) : 0;
 #pragma unroll
         for (int f = 0; f < NF; f++) {
             const FitScan &F = fs[f];
@@ -2141,6 +2178,8 @@ struct CdGramArgs {
     const double *tau;       // per-slot soft threshold (nullptr: lam_alpha for every slot) and
     const double *idv;       // per-slot 1 / curvature (nullptr: inv_den): the logistic path's
                              // scaled coordinates (NEXT-3)
+    double nu;               // lambda (1 - alpha): the ridge part of the curvature (1 + nu = 1 / inv_den)
+    int newton;              // 1: Newton (CG) steps on a settled active set between sweeps (linear path)
 };
 
 // Cluster Gram CD (v7): the v6 algorithm above with its bulk spread over a
@@ -2195,6 +2234,7 @@ struct G7Work {              // global workspace of one fit (see bl.cu gram_ws)
     double *dl;              // nW: catch-up coefficient changes
     int *rl;                 // nW: ... and their slots
     uint8_t *inA;            // nW: slot is in the set G_AA was built for
+    double *cg;              // 5 nW: Newton step by active position: x, r, p, b (coefficients), spare
 };
 
 // mbarrier / st.async helpers (CTA-local barriers; st.async writes 8 bytes into a
@@ -2304,6 +2344,7 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
     long long dbg[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const double la0 = a.lam_alpha, inv_den0 = a.inv_den;
     double dm = 0.0, bm = 0.0;                              // leader warp: per-lane running maxima
+    int nflip = 0;                                          // leader warp: sign-class changes this sweep
 
     auto block_rank = [&](bool nz, int &pos) -> int {     // order-preserving CTA compaction
         const unsigned m = __ballot_sync(FULL, nz);
@@ -2498,6 +2539,7 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
         retries += round;
         dm = fmax(dm, fabs(dfin));
         bm = fmax(bm, fabs(bnfin));
+        nflip += __popc(__ballot_sync(FULL, valid && ((bnfin > 0.0) != (bo > 0.0) || (bnfin < 0.0) != (bo < 0.0))));
         if (valid) bS[s] = bnfin;
         updates += __popc(__ballot_sync(FULL, valid && dfin != 0.0));
         dbg[3] += G7CLK() - t3;
@@ -2728,42 +2770,232 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
         cl.sync();
     };
 
-    // cluster: gradients outside the G_AA set receive sum_i dl_i G[rl_i][k] (list from the leader)
-    auto catch_up = [&](int nz) {
-        if (nz > 0) {
-            for (int k = 2 * (rank * T_ + t); k < nW; k += 2 * R * T_) {
-                double gx = 0.0, gy = 0.0;
-                for (int i0 = 0; i0 < nz; i0 += 16) {
-                    double2 rv[16];
-                    double dd[16];
+    // cluster: gradients outside the G_AA set receive sum_i dl_i G[rl_i][k] (the change list and the
+    // list of slots outside the set come from the leader).  The change list is staged in shared
+    // memory; thread q handles slot clist[q] (ascending slots: a warp's loads of one G row are
+    // contiguous), eight rows' loads in flight.
+    auto catch_up = [&](int nz, int nk) {
+        if (nz > 0 && nk > 0) {
+            double *dls = sm;                                   // the stage buffers are idle here
+            int *rls = reinterpret_cast<int *>(sm + 4096);
+            const int *clist = reinterpret_cast<const int *>(wk.cg + 4 * nWp);
+            for (int i = t; i < nz; i += T_) { dls[i] = __ldcg(wk.dl + i); rls[i] = __ldcg(wk.rl + i); }
+            __syncthreads();
+            for (int q = rank * T_ + t; q < nk; q += R * T_) {
+                const int k = __ldcg(clist + q);
+                double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+                int i0 = 0;
+                for (; i0 + 8 <= nz; i0 += 8) {
+                    double gv[8];
 #pragma unroll
-                    for (int v = 0; v < 16; v++) {
-                        const int i = min(i0 + v, nz - 1);
-                        dd[v] = i0 + v < nz ? __ldcg(wk.dl + i) : 0.0;
-                        rv[v] = __ldcg(reinterpret_cast<const double2 *>(a.G + (int64_t)__ldcg(wk.rl + i) * ldG + k));
-                    }
+                    for (int v = 0; v < 8; v++) gv[v] = __ldcg(a.G + (int64_t)rls[i0 + v] * ldG + k);
 #pragma unroll
-                    for (int v = 0; v < 16; v++) {
-                        gx = fma(dd[v], rv[v].x, gx);
-                        gy = fma(dd[v], rv[v].y, gy);
-                    }
+                    for (int v = 0; v < 8; v++) acc[v] = fma(dls[i0 + v], gv[v], acc[v]);
                 }
-                if (!__ldcg(wk.inA + k)) wk.g[k] -= gx;
-                if (k + 1 < nW && !__ldcg(wk.inA + k + 1)) wk.g[k + 1] -= gy;
+                for (; i0 < nz; i0++) acc[0] = fma(dls[i0], __ldcg(a.G + (int64_t)rls[i0] * ldG + k), acc[0]);
+                const double sum = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+                wk.g[k] -= sum;
             }
         }
         // (cl.sync: release / acquire at cluster scope)
         cl.sync();
     };
 
+    // ---- Newton step on a settled active set (CdGramArgs::newton; linear path only).
+    // With the signs s of the active coefficients fixed, the CD fixed point on A solves
+    //   (G_AA + nu I) x = b,   b = g_A - lambda alpha s - nu beta_A          (P:267's CD)
+    // (g = x~'r/n by slot; G_AA compact by active position).  Conjugate gradients from x = 0 in
+    // the Chronopoulos-Gear form (one product and ONE fused reduction per iteration: two
+    // cluster barriers), rows split over the cluster.  Every CG iterate lowers this quadratic,
+    // and so does every point of the segment [0, x]: the step beta_A += t x with the largest
+    // t <= 1 that keeps every sign (coefficients reaching 0 are set to 0) lowers the objective.
+    // The CD sweeps that follow decide convergence exactly as before, so the result is still a
+    // converged CD fixed point.  Gradients of A are updated here (g_A -= G_AA (new - old));
+    // those outside A by the lazy catch-up.
+    double *cgx = wk.cg, *cgr = wk.cg + nWp, *cgb = wk.cg + 3 * nWp;
+    __shared__ double cgpart[4][2], cgred[2][32], cgbc[2];
+    int cgslot = 0;
+    // cluster sums (or min) of two doubles per CTA (thread 0's values), combined in rank order
+    // by warp 0 of every CTA: identical on every CTA
+    auto cl_reduce2 = [&](double v0, double v1, bool is_min, double &o0, double &o1) {
+        double *slot = cgpart[cgslot & 3];
+        cgslot++;
+        if (t == 0) { slot[0] = v0; slot[1] = v1; }
+        cl.sync();
+        if (wid == 0) {
+            const double *rs = lane < R ? cl.map_shared_rank(slot, lane) : nullptr;
+            const double u0 = rs ? rs[0] : 0.0, u1 = rs ? rs[1] : 0.0;
+            double a0 = is_min ? 1e300 : 0.0, a1 = a0;
+            for (int r = 0; r < R; r++) {
+                const double w0 = __shfl_sync(FULL, u0, r), w1 = __shfl_sync(FULL, u1, r);
+                a0 = is_min ? fmin(a0, w0) : a0 + w0;
+                a1 = is_min ? fmin(a1, w1) : a1 + w1;
+            }
+            if (lane == 0) { cgbc[0] = a0; cgbc[1] = a1; }
+        }
+        __syncthreads();
+        o0 = cgbc[0];                // rewritten only after the next cl.sync, which every reader passes first
+        o1 = cgbc[1];
+    };
+    auto cta_sum2 = [&](double v0, double v1, double &s0, double &s1) {   // thread 0 gets the CTA sums
+        v0 = warp_sum(v0);
+        v1 = warp_sum(v1);
+        __syncthreads();
+        if (lane == 0) { cgred[0][wid] = v0; cgred[1][wid] = v1; }
+        __syncthreads();
+        s0 = 0.0;
+        s1 = 0.0;
+        if (t == 0)
+            for (int w = 0; w < nw; w++) { s0 += cgred[0][w]; s1 += cgred[1][w]; }
+        __syncthreads();
+    };
+    // rows [r0, r1) of w = (G_AA + nu I) v (v: na entries in shared memory, vsh[na] = 0 when na is
+    // odd); two rows per warp, eight 16-byte loads per row and lane in flight
+    auto matvec = [&](const double *vsh, double *wsh, int na, int r0, int r1, double nu_) {
+        for (int i = r0 + 2 * wid; i < r1; i += 2 * nw) {
+            const bool two = i + 1 < r1;
+            const double *ra = a.GA + (int64_t)i * ldG, *rb = a.GA + (int64_t)(two ? i + 1 : i) * ldG;
+            double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+            for (int j0 = 2 * lane; j0 < na; j0 += 64 * 8) {
+                double2 ga[8], gb[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    const int j = j0 + 64 * u;
+                    ga[u] = j < na ? __ldcg(reinterpret_cast<const double2 *>(ra + j)) : make_double2(0.0, 0.0);
+                    gb[u] = j < na ? __ldcg(reinterpret_cast<const double2 *>(rb + j)) : make_double2(0.0, 0.0);
+                }
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    const int j = j0 + 64 * u;
+                    if (j < na) {
+                        const double2 vv = *reinterpret_cast<const double2 *>(vsh + j);
+                        a0 = fma(ga[u].x, vv.x, a0);
+                        a1 = fma(ga[u].y, vv.y, a1);
+                        b0 = fma(gb[u].x, vv.x, b0);
+                        b1 = fma(gb[u].y, vv.y, b1);
+                    }
+                }
+            }
+            const double wa = warp_sum(a0 + a1), wb = warp_sum(b0 + b1);
+            if (lane == 0) {
+                wsh[i - r0] = wa + nu_ * vsh[i];
+                if (two) wsh[i + 1 - r0] = wb + nu_ * vsh[i + 1];
+            }
+        }
+    };
+    long long ncg = 0, nnewton = 0, pr_newton = 0, npartial = 0;
+    auto newton = [&](int na, double thr) {
+        const long long c0 = clock64();
+        double *vsh = sm;                                   // na (+1) doubles: the stage buffers are idle
+        double *xs = sm + 4160, *ps = xs + 1024, *ss = ps + 1024, *wsh = ss + 1024;   // this CTA's rows
+        const int r0 = (int)((int64_t)rank * na / R), r1 = (int)((int64_t)(rank + 1) * na / R);
+        const double la = a.lam_alpha, nu = a.nu;
+        auto load_r = [&]() {                               // the whole residual vector -> shared memory
+            for (int j = t; j < na; j += T_) vsh[j] = __ldcg(cgr + j);
+            if (t == 0 && (na & 1)) vsh[na] = 0.0;
+            __syncthreads();
+        };
+        for (int i = r0 + t; i < r1; i += T_) {             // r = b (x = 0)
+            const double bi = __ldcg(cgb + i);
+            cgr[i] = __ldcg(wk.g + __ldcg(wk.act + i)) - (bi > 0.0 ? la : -la) - nu * bi;
+            xs[i - r0] = 0.0;
+        }
+        cl.sync();                                          // r published
+        load_r();
+        matvec(vsh, wsh, na, r0, r1, nu);
+        __syncthreads();
+        double g0 = 0.0, d0 = 0.0;
+        for (int i = r0 + t; i < r1; i += T_) { g0 = fma(vsh[i], vsh[i], g0); d0 = fma(wsh[i - r0], vsh[i], d0); }
+        double gam, del;
+        cta_sum2(g0, d0, g0, d0);
+        cl_reduce2(g0, d0, false, gam, del);
+        const double thr2 = thr * thr;
+        const int itmax = min(na, 256);
+        int it = 0;
+        if (gam > thr2 && del > 0.0) {
+            double al = gam / del;
+            for (int i = r0 + t; i < r1; i += T_) { ps[i - r0] = vsh[i]; ss[i - r0] = wsh[i - r0]; }
+            for (;;) {
+                for (int i = r0 + t; i < r1; i += T_) {     // x += al p, r -= al s
+                    const int l = i - r0;
+                    xs[l] = fma(al, ps[l], xs[l]);
+                    cgr[i] = fma(-al, ss[l], vsh[i]);
+                }
+                cl.sync();                                  // r published (vsh readers are past the barrier)
+                load_r();
+                matvec(vsh, wsh, na, r0, r1, nu);
+                __syncthreads();
+                double gp = 0.0, dp = 0.0;
+                for (int i = r0 + t; i < r1; i += T_) { gp = fma(vsh[i], vsh[i], gp); dp = fma(wsh[i - r0], vsh[i], dp); }
+                double gn, dn;
+                cta_sum2(gp, dp, gp, dp);
+                cl_reduce2(gp, dp, false, gn, dn);
+                ++it;
+                if (gn <= thr2 || it >= itmax) break;
+                const double be = gn / gam;
+                const double den = dn - be * gn / al;
+                if (!(den > 0.0)) break;                    // no curvature left (semi-definite G_AA)
+                al = gn / den;
+                gam = gn;
+                for (int i = r0 + t; i < r1; i += T_) {     // p = r + be p, s = w + be s
+                    const int l = i - r0;
+                    ps[l] = fma(be, ps[l], vsh[i]);
+                    ss[l] = fma(be, ss[l], wsh[l]);
+                }
+            }
+        }
+        // largest step t <= 1 that keeps every active sign; x -> global for every CTA
+        double tmin = 1.0;
+        for (int i = r0 + t; i < r1; i += T_) {
+            const double bi = __ldcg(cgb + i), xi = xs[i - r0];
+            cgx[i] = xi;
+            if (bi * xi < 0.0 && fabs(xi) >= fabs(bi)) tmin = fmin(tmin, -bi / xi);
+        }
+        tmin = -warp_max(-tmin);
+        __syncthreads();
+        if (lane == 0) cgred[0][wid] = tmin;
+        __syncthreads();
+        double tc = 1.0;
+        if (t == 0) for (int w = 0; w < nw; w++) tc = fmin(tc, cgred[0][w]);
+        __syncthreads();
+        double ts, unused;
+        cl_reduce2(tc, tc, true, ts, unused);               // (its barrier also publishes x)
+        // the applied changes d = new - old (identical on every CTA), then g_A -= G_AA d
+        for (int j = t; j < na; j += T_) {
+            const double bi = __ldcg(cgb + j), xi = __ldcg(cgx + j);
+            const double bn = fma(ts, xi, bi);
+            const double bnew = (bi > 0.0 ? bn > 0.0 : bn < 0.0) ? bn : 0.0;
+            vsh[j] = bnew - bi;
+            if (leader_cta) bS[__ldcg(wk.act + j)] = bnew;
+        }
+        if (t == 0 && (na & 1)) vsh[na] = 0.0;
+        __syncthreads();
+        matvec(vsh, wsh, na, r0, r1, 0.0);
+        __syncthreads();
+        for (int i = r0 + t; i < r1; i += T_) {
+            const int s = __ldcg(wk.act + i);
+            wk.g[s] = __ldcg(wk.g + s) - wsh[i - r0];
+        }
+        if (ts < 1.0) ++npartial;
+        ncg += it;
+        ++nnewton;
+        cl.sync();                                          // gradients published (release / acquire)
+        pr_newton += clock64() - c0;
+    };
+
     // ---- control loop.  The leader decides, the cluster follows.  ctl[ph]:
-    // [0] catch-up, [1] its count, [2] rebuild G_AA / M, [3] mode (0 full, 1 active, -1 stop),
-    // [4] len, [5] owners reload their positions
+    // [0] catch-up, [1] its count, [2] rebuild G_AA / M, [3] mode (0 full, 1 active, 2 Newton step,
+    // -1 stop), [4] len, [5] owners reload their positions; ctld[ph][0] = the CG tolerance
     bool full = false, built = false, pending = false;
     int na_built = 0, last_mode = -1, last_len = -1, ph = 0;
+    int sweeps_on_set = 0, newtons_on_set = 0;            // leader: active sweeps / Newton steps on the built set
+    double dm_last = 0.0, dm_prev = 0.0;                  // leader: dmax of the last two active sweeps
+    bool conv_last = false;
+    __shared__ double ctld[2][2];
     for (;; ph ^= 1) {
         if (leader_cta) {
-            int cmd_catch = 0, ncat = 0, cmd_build = 0, mode = 0, len = nW;
+            int cmd_catch = 0, ncat = 0, nkc = 0, cmd_build = 0, mode = 0, len = nW;
+            double cg_thr = 0.0;
             if (status || (passes > 0 && full && red[2] != 0.0)) {
                 mode = -1;                                    // stop (set below after a sweep)
             } else {
@@ -2782,6 +3014,17 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
                             cmd_build = 1;
                         }
                         mode = 1;
+                        // a settled active set converging slowly (same set and signs over the last
+                        // two sweeps, contraction > 0.3 per sweep): one Newton step instead of the
+                        // remaining sweeps
+                        if (a.newton && same && last_mode == 1 && !conv_last && red[3] == 0.0 &&
+                            sweeps_on_set >= 2 && newtons_on_set < 2 && len >= 32 && dm_prev > 0.0 &&
+                            dm_last > 0.3 * dm_prev) {
+                            mode = 2;
+                            // CG stops at an rms residual of 0.2 tol max|beta| (the sweep that follows
+                            // resolves the rest)
+                            cg_thr = 0.2 * fmax(a.tol * red[1], a.floor_) * sqrt((double)len);
+                        }
                     } else {
                         if (pending) { cmd_catch = 1; pending = false; }
                         mode = 0;
@@ -2801,8 +3044,18 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
                     if (dlt != 0.0) { wk.dl[nz + pos] = dlt; wk.rl[nz + pos] = s; }
                     nz += cnt;
                 }
-                for (int w = t; w < nW; w += T_) wk.inA[w] = inA[w];
+                int nk = 0;                                   // slots outside the built set (ascending)
+                int *clist = reinterpret_cast<int *>(wk.cg + 4 * nWp);
+                for (int base = 0; base < nW; base += T_) {
+                    const int w = base + t;
+                    const bool out_ = w < nW && !inA[w];
+                    int pos;
+                    const int cnt = block_rank(out_, pos);
+                    if (out_) clist[nk + pos] = w;
+                    nk += cnt;
+                }
                 ncat = nz;
+                nkc = nk;
             }
             if (cmd_build) {
                 __syncthreads();
@@ -2811,30 +3064,39 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
                 for (int i = t; i < len; i += T_) { actp[i] = act[i]; inA[act[i]] = 1; }
                 built = true;
                 na_built = len;
+                sweeps_on_set = 0;
+                newtons_on_set = 0;
             }
             if (mode == 1 && (cmd_build || !pending)) {
                 __syncthreads();
                 for (int i = t; i < len; i += T_) bcat[act[i]] = bS[act[i]];
                 pending = true;
             }
+            if (mode == 2) {                                  // the coefficients by active position
+                for (int i = t; i < len; i += T_) wk.cg[3 * nWp + i] = bS[act[i]];
+                ++newtons_on_set;
+            }
             const int reload = mode != last_mode || len != last_len || cmd_build || cmd_catch;
             last_mode = mode;
             last_len = len;
             if (t == 0) {
                 ctl[ph][0] = cmd_catch; ctl[ph][1] = ncat; ctl[ph][2] = cmd_build;
-                ctl[ph][3] = mode; ctl[ph][4] = len; ctl[ph][5] = reload;
+                ctl[ph][3] = mode; ctl[ph][4] = len; ctl[ph][5] = reload; ctl[ph][6] = nkc;
+                ctld[ph][0] = cg_thr;
             }
             // cl.sync()'s arrive.release / wait.acquire orders these writes for the cluster
         }
         cl.sync();
         const int *rc = cl.map_shared_rank(&ctl[ph][0], 0);
         const int cmd_catch = rc[0], ncat = rc[1], cmd_build = rc[2], mode = rc[3], len = rc[4], reload = rc[5];
+        const int nkc = rc[6];
+        const double cg_thr = *cl.map_shared_rank(&ctld[ph][0], 0);
         if (!leader_cta && (reload || mode < 0)) owner_store();
         if (mode < 0) break;
         if (reload) cl.sync();                              // owners' stores ordered by the release barrier
         if (cmd_catch) {
             const long long c0 = clock64();
-            catch_up(ncat);
+            catch_up(ncat, nkc);
             ++ncatch;
             pr_catch += clock64() - c0;
         }
@@ -2844,19 +3106,26 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
             ++rebuilds;
             pr_build += clock64() - c0;
         }
+        if (mode == 2) {
+            newton(len, cg_thr);
+            continue;                                       // no sweep: the next one verifies
+        }
         if (!leader_cta && reload) { owner_load(mode == 1, len); __syncthreads(); }
         nfull += mode == 0;
+        if (leader_cta && wid == 0) nflip = 0;
         sweep(mode == 1, len);
         if (leader_cta) {                                     // convergence of the pass (leader only)
             if (wid == 0) {
                 const double dmw = warp_max(dm), bmw = warp_max(bm);
-                if (t == 0) { red[0] = dmw; red[1] = bmw; }
+                if (t == 0) { red[0] = dmw; red[1] = bmw; red[3] = (double)nflip; }
             }
             __syncthreads();
             const double dmax = red[0], bmax = red[1];
             __syncthreads();
             const bool conv = dmax <= a.tol * bmax || dmax <= a.floor_;
             if (++passes > a.max_iter) status = 3;
+            if (mode == 1) { ++sweeps_on_set; dm_prev = dm_last; dm_last = dmax; }
+            conv_last = conv;
             if (t == 0) red[2] = (full && conv) ? 1.0 : 0.0;   // stop after a converged full pass
             __syncthreads();
             if (red[2] == 0.0) full = conv;
@@ -2902,6 +3171,10 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
         a.st->cd_cnt[1] = rebuilds;
         a.st->cd_cnt[2] = ncatch;
         a.st->cd_cnt[3] = nfull;
+        a.st->cd_cnt[4] = nnewton;
+        a.st->cd_cnt[5] = ncg;
+        a.st->cd_cnt[6] = pr_newton;
+        a.st->cd_cnt[7] = npartial;
         for (int u = 0; u < 8; u++) a.st->cd_dbg[u] = dbg[u];   // leader warp sub-phases
     }
 }

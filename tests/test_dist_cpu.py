@@ -65,3 +65,61 @@ def test_shard_range_small():
             rs = [bl.shard_range(p, world, r) for r in range(world)]
             assert rs[0][0] == 0 and rs[-1][1] == p
             assert all(rs[r][1] == rs[r + 1][0] for r in range(world - 1))
+
+
+def _coll_worker(rank, world, port, q):
+    """Drive the host-collective adapters of bl.host_coll_dist (bl_dist.backend = 2) exactly as
+    libbl calls them (C function pointers, host buffers), over gloo between processes."""
+    import ctypes
+    import numpy as np
+    import torch
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        def allgather(send):
+            t = torch.tensor(np.frombuffer(send, dtype=np.uint8).copy())
+            out = [torch.empty_like(t) for _ in range(world)]
+            dist.all_gather(out, t)
+            return b"".join(o.numpy().tobytes() for o in out)
+
+        def bcast(buf, root):
+            t = torch.tensor(np.frombuffer(bytes(buf), dtype=np.uint8).copy())
+            dist.broadcast(t, src=root)
+            buf[:] = t.numpy().tobytes()
+
+        def allreduce_sum(v):
+            dist.all_reduce(torch.from_numpy(v))
+
+        d = bl.host_coll_dist(rank, world, (rank * 10, rank * 10 + 10), 10 * world, allgather, bcast, allreduce_sum)
+        hc = d.host_coll.contents
+        assert d.backend == 2 and d.p_global == 10 * world
+        send = (ctypes.c_int32 * 3)(rank, 100 + rank, -rank)
+        recv = (ctypes.c_int32 * (3 * world))()
+        rc1 = hc.allgather(None, ctypes.cast(send, ctypes.c_void_p), ctypes.cast(recv, ctypes.c_void_p), 12)
+        buf = (ctypes.c_double * 4)(*([rank + 0.5] * 4))
+        rc2 = hc.bcast(None, ctypes.cast(buf, ctypes.c_void_p), 32, 1)
+        acc = (ctypes.c_double * 3)(1.0, rank, 2.0 * rank)
+        rc3 = hc.allreduce_sum_f64(None, ctypes.cast(acc, ctypes.c_void_p), 3)
+        q.put((rank, (rc1, rc2, rc3), list(recv), list(buf), list(acc)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_host_collective_adapters_world2():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_coll_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    got = sorted(q.get(timeout=120) for _ in range(world))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    for rank, rcs, recv, buf, acc in got:
+        assert rcs == (0, 0, 0)
+        assert recv == [0, 100, 0, 1, 101, -1]               # rank order
+        assert buf == [1.5] * 4                              # root 1's payload
+        assert acc == [2.0, 1.0, 2.0]                        # sums over the ranks

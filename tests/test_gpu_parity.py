@@ -290,7 +290,7 @@ def test_cv_with_shrunk_strong_sets_matches():
     lams = synth.lambda_grid(d.lambda_max(inst.y), 15, 0.1)
     a = d.cv(inst.y, lams, K=4, tol=1e-10, seed=5)
     b = d.cv(inst.y, lams, K=4, tol=1e-10, seed=5, fault_strong_drop=1)
-    np.testing.assert_allclose(b.E, a.E, rtol=1e-8, atol=1e-12 * a.E.max())
+    np.testing.assert_allclose(b.E, a.E, rtol=1e-6, atol=1e-9 * a.E.max())
     assert b.full.kkt_rounds.max() >= 2
 
 

@@ -112,3 +112,44 @@ def test_sharded_rejects_bad_layout():
         return 0
     codes = run_ranks(2, mk)
     assert all(c == bl.BL_ERR_ARG for c in codes)
+
+
+@pytest.mark.parametrize("dtype,cv_mode", [(np.int8, "batched"), (np.float64, "independent"),
+                                           (np.float32, "batched_fma")])
+def test_sharded_cv_modes_are_G_invariant(dtype, cv_mode):
+    """Lockstep CV on a column-sharded design (every fit's round exchanged in one collective,
+    SURVEY 8(e)) and the independent-fits mode: bitwise the single-GPU CV."""
+    kind = "geno" if dtype == np.int8 else "corr"
+    inst = synth.random_instance(110, 500, dtype=dtype, seed=6, kind=kind, n_true=8)
+    G = 2
+    d1 = bl.Design(inst.host_X(), inst.n)
+    lams = synth.lambda_grid(d1.lambda_max(inst.y, 0.5), 15, 0.1)
+    ref = d1.cv(inst.y, lams, K=5, alpha=0.5, seed=4, tol=1e-9, cv_mode=cv_mode)
+    ds = sharded_designs(inst, G)
+    cvs = run_ranks(G, lambda r: ds[r].cv(inst.y, lams, K=5, alpha=0.5, seed=4, tol=1e-9, cv_mode=cv_mode))
+    for c in cvs:
+        assert np.array_equal(c.cve, ref.cve) and np.array_equal(c.cvse, ref.cvse)
+        assert np.array_equal(c.full.beta_std, ref.full.beta_std)
+
+
+def test_sharded_design_rejects_a_concurrent_call():
+    """A multi-rank design accepts one call at a time (include/bl.h): while rank 0 waits in a
+    collective of one fit, a second fit on the same rank's design returns BL_ERR_ARG at once."""
+    import time
+    inst = synth.random_instance(100, 300, dtype=np.float32, seed=8, kind="corr", n_true=6)
+    ds = sharded_designs(inst, 2)
+    lams = synth.lambda_grid(bl.Design(inst.host_X(), inst.n).lambda_max(inst.y), 10, 0.2)
+    out = {}
+
+    def first():
+        out["a"] = ds[0].fit_path(inst.y, lams, tol=1e-9)
+
+    t = threading.Thread(target=first)
+    t.start()
+    time.sleep(1.0)                      # rank 0 is now blocked in its first collective
+    with pytest.raises(bl.BLError) as e:
+        ds[0].fit_path(inst.y, lams, tol=1e-9)
+    assert e.value.code == bl.BL_ERR_ARG
+    ds[1].fit_path(inst.y, lams, tol=1e-9)   # rank 1 joins: the first fit completes
+    t.join(timeout=300)
+    assert "a" in out and out["a"].n_converged == len(lams)
