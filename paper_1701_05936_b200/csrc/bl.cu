@@ -2154,6 +2154,13 @@ const void *batch_kernel_n(bool f64, int nb) {
 }
 const void *batch_kernel(bool f64, int nb) { return batch_kernel_n<kBatchMax>(f64, nb); }
 template <int NF>
+const void *batch_i8_kernel_n(int nb) {
+    if constexpr (NF > 1) {
+        if (nb < NF) return batch_i8_kernel_n<NF - 1>(nb);
+    }
+    return (const void *)k_scan_batch_i8<NF>;
+}
+template <int NF>
 const void *batch_mma_kernel_n(bool f64, int nb) {
     if constexpr (NF > 1) {
         if (nb < NF) return batch_mma_kernel_n<NF - 1>(f64, nb);
@@ -2181,6 +2188,13 @@ void launch_scan_batch(bl_design *d, const std::vector<LockFit *> &fits, cudaStr
         F.nviol = sa.nviol;
         F.strong = sa.strong;
         F.nstrong = sa.nstrong;
+        F.limbs = nullptr;
+        F.limb_scale = nullptr;
+        if (d->dt == DT_I8) {                       // the quantised residual (k_limbs, launched by the caller)
+            F.limbs = pp->limbs;
+            F.limb_scale = pp->limb_scale;
+            F.K1 = pp->limb_sum;                    // identity (3) holds exactly for the quantised vector
+        }
     }
     CK(cudaMemcpyAsync(dfs, hfs, sizeof(FitScan) * nf, cudaMemcpyHostToDevice, sst));
     const bool f64 = d->dt == DT_F64;
@@ -2192,16 +2206,26 @@ void launch_scan_batch(bl_design *d, const std::vector<LockFit *> &fits, cudaStr
     }
     for (size_t u0 = 0; u0 < nf; u0 += kBatchMax) {
         int nb = (int)std::min<size_t>(kBatchMax, nf - u0);
-        const void *kern = mma ? batch_mma_kernel_n<kBatchMax>(f64, nb) : batch_kernel(f64, nb);
-        const size_t smem = mma ? batch_mma_smem(nb) : batch_smem(nb, itemsize(d->dt));
-        const int threads = mma ? kBMThreads : kBatchThreads;
+        const bool i8 = d->dt == DT_I8;
+        const void *kern = i8 ? batch_i8_kernel_n<kBatchMax>(nb)
+                         : mma ? batch_mma_kernel_n<kBatchMax>(f64, nb) : batch_kernel(f64, nb);
+        const size_t smem = i8 ? batch_i8_smem(nb) : mma ? batch_mma_smem(nb) : batch_smem(nb, itemsize(d->dt));
+        const int threads = i8 ? kScanThreads : mma ? kBMThreads : kBatchThreads;
         allow_dyn_smem(kern);
         const int grid = grid_for(kern, threads, smem, d->nsm);
         const void *X = d->X;
         int64_t ld = d->ld, p = d->p;
         int n = (int)d->n;
         FitScan *fp = dfs + u0;
+        int limb_ld = fits[u0]->pp->limb_ld;
         void *args[] = {&X, &ld, &n, &p, &fp, &nb, &list, &lctl};
+        void *args_i8[] = {&X, &ld, &n, &p, &fp, &limb_ld, &list, &lctl};
+        if (i8) {
+            CK(cudaLaunchKernel(kern, dim3(grid), dim3(threads), args_i8, smem, sst));
+            timer->launches++;
+            timer->batch_passes++;
+            continue;
+        }
         CK(cudaLaunchKernel(kern, dim3(grid), dim3(threads), args, smem, sst));
         timer->launches++;
         timer->batch_passes++;                           // X bytes: accounted once the union size is known
@@ -2230,7 +2254,7 @@ void cv_lockstep(bl_design *d, const double *y, const std::vector<int32_t> &fold
     int *uni = nullptr;                                    // [count, use_list, list (p)]: the union BEDPP scope
     void **dptr = nullptr, **hptr = nullptr;               // per pending fit: flags, nlive, RoundStatus pointers
     int *hctl = nullptr;                                   // pinned: the round's [count, use_list]
-    const bool batched = d->dt != DT_I8;
+    const bool batched = true;                           // every round is one fold-batched pass (int8: IMMA)
     const bool mma = !opts || opts->cv_mode == 0;         // fold-batched scan on the fp64 tensor cores
     auto t0 = std::chrono::steady_clock::now();
     auto cleanup = [&]() {
@@ -2294,7 +2318,7 @@ void cv_lockstep(bl_design *d, const double *y, const std::vector<int32_t> &fold
                     lf->run->solve();
                     CK(cudaEventRecord(lf->solved, lf->pp->stream));
                 }
-                if (batched) {
+                {
                     for (LockFit *lf : pending) CK(cudaStreamWaitEvent(sst, lf->solved, 0));
                     // the union of the pending fits' BEDPP scopes: near lambda_max BEDPP
                     // discards most columns for every fit, and only the union is read
@@ -2306,6 +2330,14 @@ void cv_lockstep(bl_design *d, const double *y, const std::vector<int32_t> &fold
                     }
                     CK(cudaMemcpyAsync(dptr, hptr, 3 * sizeof(void *) * np_, cudaMemcpyHostToDevice, sst));
                     CK(cudaMemsetAsync(uni, 0, 2 * sizeof(int), sst));
+                    if (d->dt == DT_I8)                     // every fit's residual -> 8 digit planes (Q27)
+                        for (LockFit *lf : pending) {
+                            bl_prep *q = lf->pp;
+                            k_limbs<<<1, 1024, 0, sst>>>(q->rscan, (int)d->n, q->limb_ld, q->limbs, q->limb_scale,
+                                                         q->limb_sum);
+                            CKL();
+                            timer->launches++;
+                        }
                     {
                         const int ug = (int)std::min<int64_t>((d->p + 255) / 256, (int64_t)d->nsm * 8);
                         k_scope_union<<<ug, 256, 0, sst>>>(d->p, (const uint8_t *const *)dptr, (int)np_, uni + 2, uni);
@@ -2322,12 +2354,6 @@ void cv_lockstep(bl_design *d, const double *y, const std::vector<int32_t> &fold
                     CK(cudaStreamSynchronize(sst));
                     const int64_t cols = hctl[1] ? hctl[0] : d->p;
                     timer->batch_bytes += (double)timer->batch_passes * (double)d->n * itemsize(d->dt) * (double)cols;
-                } else {
-                    for (LockFit *lf : pending) {
-                        launch_scan(lf->pp, lf->run->scan_args(), lf->pp->rscan, true);
-                        copy_round(lf->pp, lf->pp->stream);
-                    }
-                    for (LockFit *lf : pending) CK(cudaStreamSynchronize(lf->pp->stream));
                 }
                 if (d->sharded) {                           // C3 for every pending fit in one collective
                     std::vector<bl_prep *> pps;

@@ -421,6 +421,8 @@ struct FitScan {
     const uint8_t *flags, *wflag;
     double thr_viol, thr_strong;
     int *viol, *nviol, *strong, *nstrong;
+    const int8_t *limbs;             // int8 designs: the fit's quantised residual (8 digit planes x limb_ld)
+    const double *limb_scale;        //   2^-S of the quantisation (K1 then points to the quantised sum)
 };
 constexpr int kBatchMax = 12;        // fits per launch
 constexpr int kBatchRows = 128;      // rows per pipeline stage
@@ -870,6 +872,109 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_i8(ScanArgs a) {
         if (a.scan) {
             warp_append(isv, (int)j, a.viol, a.nviol);
             warp_append(iss, (int)j, a.strong, a.nstrong);
+        }
+    }
+}
+
+// NEXT-1 for int8 designs: the fold-batched scan on the integer tensor cores.  Every fit's
+// residual is quantised to 8 digit planes (k_limbs, Q27); one pass over X serves all fits:
+// per 32-row k-step a lane's A fragment (two columns x 16 rows, k_scan_i8's mapping) is loaded
+// ONCE and multiplied by each fit's B fragment (its 8 digit planes x the same rows) --
+// mma.m16n8k32.s8, exact int32 accumulation per fit.  The fits' digit planes stream through
+// shared memory in 256-row chunks (double-buffered cp.async; the whole set would not fit at
+// n = 2898 x 11 fits).  Epilogue per fit as k_scan_batch (identity (3) with the fit's c, s,
+// quantised sum and 1/n_used; KKT / strong-rule tests; list compaction).
+constexpr int kBIRows = 256;                   // rows per chunk
+__host__ __device__ constexpr size_t batch_i8_smem(int nf) { return (size_t)2 * nf * 8 * kBIRows; }
+
+template <int NF>
+__global__ void __launch_bounds__(kScanThreads) k_scan_batch_i8(const int8_t *__restrict__ X, int64_t ld, int n, int64_t p,
+                                                              const FitScan *__restrict__ fits, int limb_ld,
+                                                              const int *__restrict__ list, const int *__restrict__ lctl) {
+    extern __shared__ __align__(16) int8_t lsb[];      // [2][NF][8][kBIRows]
+    __shared__ FitScan fs[NF];
+    __shared__ double k1s[NF], scs[NF];
+    if (threadIdx.x < NF) fs[threadIdx.x] = fits[threadIdx.x];
+    __syncthreads();
+    if (threadIdx.x < NF) { k1s[threadIdx.x] = *fs[threadIdx.x].K1; scs[threadIdx.x] = *fs[threadIdx.x].limb_scale; }
+    if (list && !lctl[1]) list = nullptr;
+    const int64_t P = list ? (int64_t)lctl[0] : p;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+    const int nchunk = (int)((ld + kBIRows - 1) / kBIRows);
+    constexpr int STAGE = NF * 8 * kBIRows;
+    // CTA tile = 8 warps x 16 columns
+    for (int64_t c0 = (int64_t)blockIdx.x * 128; c0 < P; c0 += (int64_t)gridDim.x * 128) {
+        const int64_t g0 = c0 + 16 * wid;
+        const int64_t ia = min(g0 + g, P - 1), ib = min(g0 + g + 8, P - 1);
+        const int64_t ja = list ? (int64_t)list[ia] : ia, jb = list ? (int64_t)list[ib] : ib;
+        const int8_t *pa = X + ja * ld, *pb = X + jb * ld;
+        int acc[NF][4];
+#pragma unroll
+        for (int f = 0; f < NF; f++) acc[f][0] = acc[f][1] = acc[f][2] = acc[f][3] = 0;
+        auto stage = [&](int ch, int b) {
+            int8_t *dst0 = lsb + (size_t)b * STAGE;
+            const int r0 = ch * kBIRows;
+            for (int e = threadIdx.x; e < NF * 8 * (kBIRows / 16); e += kScanThreads) {
+                const int fl = e / (kBIRows / 16), q = e - fl * (kBIRows / 16);
+                const int f = fl >> 3, l = fl & 7;
+                int8_t *dst = dst0 + (size_t)fl * kBIRows + 16 * q;
+                const int r = r0 + 16 * q;
+                if (r + 16 <= limb_ld) cp_async16(dst, fs[f].limbs + (size_t)l * limb_ld + r);
+                else *reinterpret_cast<int4 *>(dst) = make_int4(0, 0, 0, 0);
+            }
+            cp_async_commit();
+        };
+        __syncthreads();                                   // the previous tile's stages are consumed
+        stage(0, 0);
+        for (int ch = 0; ch < nchunk; ch++) {
+            if (ch + 1 < nchunk) stage(ch + 1, (ch + 1) & 1); else cp_async_commit();
+            cp_async_wait<1>();
+            __syncthreads();
+            const int8_t *st = lsb + (size_t)(ch & 1) * STAGE;
+            const int r0 = ch * kBIRows;
+#pragma unroll
+            for (int u = 0; u < kBIRows / 64; u++) {
+                const int r = r0 + 64 * u + 16 * t;
+                const bool in = r < ld;                     // ld % 16 == 0: 16 rows in or out together
+                const int4 xa = in ? __ldcs(reinterpret_cast<const int4 *>(pa + r)) : make_int4(0, 0, 0, 0);
+                const int4 xb = in ? __ldcs(reinterpret_cast<const int4 *>(pb + r)) : make_int4(0, 0, 0, 0);
+#pragma unroll
+                for (int f = 0; f < NF; f++) {
+                    const int4 l = *reinterpret_cast<const int4 *>(st + (size_t)(f * 8 + g) * kBIRows + 64 * u + 16 * t);
+                    mma_s8(acc[f], xa.x, xb.x, xa.y, xb.y, l.x, l.y);
+                    mma_s8(acc[f], xa.z, xb.z, xa.w, xb.w, l.z, l.w);
+                }
+            }
+            __syncthreads();                               // stage (ch & 1) is rewritten at ch + 2
+        }
+        cp_async_wait<0>();
+        // acc[f][0], acc[f][1]: column ja, limbs 2t, 2t+1; acc[f][2], acc[f][3]: column jb
+        const bool valid = (t == 0 && g0 + g < P) || (t == 1 && g0 + g + 8 < P);
+        const int64_t j = t == 0 ? ja : jb;
+#pragma unroll
+        for (int f = 0; f < NF; f++) {
+            const double w0 = ldexp(scs[f], 16 * t), w1 = ldexp(scs[f], 16 * t + 8);
+            double da = fma((double)acc[f][0], w0, (double)acc[f][1] * w1);
+            double db = fma((double)acc[f][2], w0, (double)acc[f][3] * w1);
+            da += __shfl_xor_sync(0xffffffffu, da, 1);
+            db += __shfl_xor_sync(0xffffffffu, db, 1);
+            da += __shfl_xor_sync(0xffffffffu, da, 2);
+            db += __shfl_xor_sync(0xffffffffu, db, 2);
+            const double d = t == 0 ? da : db;
+            const FitScan &F = fs[f];
+            bool isv = false, iss = false;
+            if (valid) {
+                const double sj = F.s[j];
+                const double z = sj > 0.0 ? (d - F.c[j] * k1s[f]) * F.K2 / sj : 0.0;
+                F.out[j] = z;
+                const double az = fabs(z);
+                const bool inw = F.wflag[j] != 0;
+                const uint8_t fl = F.flags[j];
+                isv = !inw && (fl & 1) && az > F.thr_viol;
+                iss = !inw && (fl & 2) && F.thr_strong >= 0.0 && az >= F.thr_strong && sj > 0.0;
+            }
+            warp_append(isv, (int)j, F.viol, F.nviol);
+            warp_append(iss, (int)j, F.strong, F.nstrong);
         }
     }
 }
@@ -2883,7 +2988,7 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
             }
         }
     };
-    long long ncg = 0, nnewton = 0, pr_newton = 0, npartial = 0;
+    long long ncg = 0, nnewton = 0, pr_newton = 0, npartial = 0, nchecks = 0;
     auto newton = [&](int na, double thr) {
         const long long c0 = clock64();
         double *vsh = sm;                                   // na (+1) doubles: the stage buffers are idle
@@ -2991,12 +3096,13 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
     int sweeps_on_set = 0, newtons_on_set = 0;            // leader: active sweeps / Newton steps on the built set
     double dm_last = 0.0, dm_prev = 0.0;                  // leader: dmax of the last two active sweeps
     bool conv_last = false;
+    bool check_ok = false, force_full = false;            // leader: the W check (mode 3) passed / failed
     __shared__ double ctld[2][2];
     for (;; ph ^= 1) {
         if (leader_cta) {
-            int cmd_catch = 0, ncat = 0, nkc = 0, cmd_build = 0, mode = 0, len = nW;
+            int cmd_catch = 0, ncat = 0, nkc = 0, cmd_build = 0, mode = 0, len = nW, nz3 = 0;
             double cg_thr = 0.0;
-            if (status || (passes > 0 && full && red[2] != 0.0)) {
+            if (status || check_ok || (passes > 0 && full && red[2] != 0.0)) {
                 mode = -1;                                    // stop (set below after a sweep)
             } else {
                 for (;;) {
@@ -3027,7 +3133,13 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
                         }
                     } else {
                         if (pending) { cmd_catch = 1; pending = false; }
-                        mode = 0;
+                        // with Newton steps on (CdGramArgs::newton), the full pass that must confirm a
+                        // converged active set is first replaced by its exact outcome for the zero
+                        // coordinates: a zero coefficient stays zero in a CD update iff |g_w| <= its
+                        // threshold, and the active ones just passed a converged sweep.  Only if some
+                        // zero coordinate would move does the full sweep run.
+                        mode = (a.newton && !force_full) ? 3 : 0;
+                        force_full = false;
                         len = nW;
                     }
                     break;
@@ -3076,12 +3188,24 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
                 for (int i = t; i < len; i += T_) wk.cg[3 * nWp + i] = bS[act[i]];
                 ++newtons_on_set;
             }
+            if (mode == 3) {                                  // the zero coordinates of W (slots)
+                int *zl = reinterpret_cast<int *>(wk.cg);
+                __syncthreads();
+                for (int base = 0; base < nW; base += T_) {
+                    const int w = base + t;
+                    const bool z0 = w < nW && bS[w] == 0.0;
+                    int pos;
+                    const int cnt = block_rank(z0, pos);
+                    if (z0) zl[nz3 + pos] = w;
+                    nz3 += cnt;
+                }
+            }
             const int reload = mode != last_mode || len != last_len || cmd_build || cmd_catch;
             last_mode = mode;
             last_len = len;
             if (t == 0) {
                 ctl[ph][0] = cmd_catch; ctl[ph][1] = ncat; ctl[ph][2] = cmd_build;
-                ctl[ph][3] = mode; ctl[ph][4] = len; ctl[ph][5] = reload; ctl[ph][6] = nkc;
+                ctl[ph][3] = mode; ctl[ph][4] = len; ctl[ph][5] = reload; ctl[ph][6] = nkc; ctl[ph][7] = nz3;
                 ctld[ph][0] = cg_thr;
             }
             // cl.sync()'s arrive.release / wait.acquire orders these writes for the cluster
@@ -3089,7 +3213,7 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
         cl.sync();
         const int *rc = cl.map_shared_rank(&ctl[ph][0], 0);
         const int cmd_catch = rc[0], ncat = rc[1], cmd_build = rc[2], mode = rc[3], len = rc[4], reload = rc[5];
-        const int nkc = rc[6];
+        const int nkc = rc[6], nz3 = rc[7];
         const double cg_thr = *cl.map_shared_rank(&ctld[ph][0], 0);
         if (!leader_cta && (reload || mode < 0)) owner_store();
         if (mode < 0) break;
@@ -3109,6 +3233,25 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
         if (mode == 2) {
             newton(len, cg_thr);
             continue;                                       // no sweep: the next one verifies
+        }
+        if (mode == 3) {                                    // the W check: would a zero coordinate move?
+            const int *zl = reinterpret_cast<const int *>(wk.cg);
+            double nv = 0.0;
+            for (int q = rank * T_ + t; q < nz3; q += R * T_) {
+                const int w = __ldcg(zl + q);
+                const double thr = a.tau ? a.tau[w] : a.lam_alpha;
+                nv += fabs(__ldcg(wk.g + w)) > thr ? 1.0 : 0.0;
+            }
+            double tot = 0.0, unused;
+            double cs;
+            cta_sum2(nv, 0.0, cs, unused);
+            cl_reduce2(cs, 0.0, false, tot, unused);
+            ++nchecks;
+            if (leader_cta) {
+                if (tot == 0.0) check_ok = true;
+                else force_full = true;
+            }
+            continue;
         }
         if (!leader_cta && reload) { owner_load(mode == 1, len); __syncthreads(); }
         nfull += mode == 0;
@@ -3175,6 +3318,7 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
         a.st->cd_cnt[5] = ncg;
         a.st->cd_cnt[6] = pr_newton;
         a.st->cd_cnt[7] = npartial;
+        dbg[7] = nchecks;                                   // (slot 7: W checks, not a sub-phase)
         for (int u = 0; u < 8; u++) a.st->cd_dbg[u] = dbg[u];   // leader warp sub-phases
     }
 }

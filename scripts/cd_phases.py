@@ -26,8 +26,9 @@ for cfg in sys.argv[1:]:
     pf = gp.perf
     v = pf["cd_visits"]
     blocks = v / 32
-    names = ["prologue", "active_matvec", "fwd_subst", "publish", "wait_stage+snap", "wait_next_stage", "link", "-"]
+    names = ["prologue", "active_matvec", "fwd_subst", "publish", "wait_stage+snap", "wait_next_stage", "link", "w_checks(count)"]
     print(cfg, "cluster", R or 8, "cd_ms", round(pf["cd_ms"], 2), "path_ms", round(pf["wall_ms"], 2), "visits", v, "cycles/visit", round(pf["cd_kernel_cycles"] / v, 1))
     print("  events (retries, builds, catchups, full sweeps, newton, cg iters, newton cycles, partial):", pf["cd_events"])
     print("  phases per visit (lead, bulk, build, catch):", [round(x / v, 1) for x in pf["cd_prof"]])
-    print("  leader sub-phases per BLOCK:", {n: round(x / blocks, 1) for n, x in zip(names, pf["cd_sub"])})
+    print("  leader sub-phases per BLOCK:", {n: round(x / blocks, 1) for n, x in zip(names[:7], pf["cd_sub"][:7])},
+          "W checks:", pf["cd_sub"][7])
