@@ -1767,9 +1767,13 @@ void solve_cd(bl_prep *pp, int nW, double lam, double alpha, double tol, int max
     // cluster Gram CD: R CTAs of 256 threads (CTA 0 leads, 1..R-1 own the gradients)
     const int R = pp->cd_cluster;   // CTA 0 leads, 1..R-1 own the gradients
     const void *kern = gram7_kernel(alpha < 1.0, R);
-    const size_t smem = gram7_smem(nW, R);
+    const size_t need = gram7_smem(nW, R);
     const size_t lim = allow_dyn_smem(kern);
-    if (smem > lim) raise(BL_ERR_OOM, "Gram CD shared memory %zu > %zu (|W| = %d)", smem, lim, nW);
+    if (need > lim) raise(BL_ERR_OOM, "Gram CD shared memory %zu > %zu (|W| = %d)", need, lim, nW);
+    // one CTA per SM either way (255 registers x 256 threads): take all of the SM's shared memory,
+    // the Newton steps keep G_AA rows in it
+    const size_t smem = lim;
+    ga.smem_bytes = (int)smem;
     G7Work wk = gram_ws(pp);
     void *args[] = {&ga, &wk};
     CK(cudaLaunchKernel(kern, dim3(R), dim3(kG7Threads), args, smem, pp->stream));

@@ -131,7 +131,21 @@ __global__ void __launch_bounds__(256) k_colstats(const T *__restrict__ X, int64
         if constexpr (sizeof(T) == 1) {
             long long s1 = 0, s2 = 0;
             int a1 = 0, a2 = 0;          // full 16-row chunks: 4-way byte dot products (dp4a), exact in int32
-            for (int i = lane * V; i < n; i += 32 * V) {
+            int i = lane * V;
+            if (!MASK)                   // four full 16-row chunks per lane and step: four loads in flight
+                for (; i + 3 * 32 * V + V <= n; i += 4 * 32 * V) {
+                    int4 raw[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) raw[u] = __ldg(reinterpret_cast<const int4 *>(col + i + u * 32 * V));
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        a1 = __dp4a(raw[u].x, 0x01010101, a1); a2 = __dp4a(raw[u].x, raw[u].x, a2);
+                        a1 = __dp4a(raw[u].y, 0x01010101, a1); a2 = __dp4a(raw[u].y, raw[u].y, a2);
+                        a1 = __dp4a(raw[u].z, 0x01010101, a1); a2 = __dp4a(raw[u].z, raw[u].z, a2);
+                        a1 = __dp4a(raw[u].w, 0x01010101, a1); a2 = __dp4a(raw[u].w, raw[u].w, a2);
+                    }
+                }
+            for (; i < n; i += 32 * V) {
                 int4 raw = __ldg(reinterpret_cast<const int4 *>(col + i));
                 if (!MASK && i + V <= n) {
                     a1 = __dp4a(raw.x, 0x01010101, a1); a2 = __dp4a(raw.x, raw.x, a2);
@@ -160,25 +174,37 @@ __global__ void __launch_bounds__(256) k_colstats(const T *__restrict__ X, int64
                 s[j] = num <= 0 ? 0.0 : sqrt((double)num) / nt;
             }
         } else {
-            double K = to_d(col[i0]);
-            double s1 = 0.0, s2 = 0.0;
-            for (int i = lane * V; i < n; i += 32 * V) {
-                T xv[V];
-                *reinterpret_cast<int4 *>(xv) = __ldg(reinterpret_cast<const int4 *>(col + i));
+            // four 16-byte loads in flight per lane (independent partial sums, combined in a fixed
+            // order): one load per lane and iteration left the HBM stream latency-bound (0.6 of peak)
+            const double K = to_d(col[i0]);
+            double s1[4] = {0.0, 0.0, 0.0, 0.0}, s2[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int i = lane * V; i < n; i += 4 * 32 * V) {
+                T xv[4][V];
 #pragma unroll
-                for (int e = 0; e < V; e++) {
-                    bool use = (i + e < n) && (!MASK || mask[i + e]);
-                    double d = use ? to_d(xv[e]) - K : 0.0;
-                    s1 += d;
-                    s2 = fma(d, d, s2);
+                for (int u = 0; u < 4; u++) {
+                    const int iu = i + u * 32 * V;
+                    if (iu < n) *reinterpret_cast<int4 *>(xv[u]) = __ldg(reinterpret_cast<const int4 *>(col + iu));
+                    else *reinterpret_cast<int4 *>(xv[u]) = make_int4(0, 0, 0, 0);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int iu = i + u * 32 * V;
+#pragma unroll
+                    for (int e = 0; e < V; e++) {
+                        const bool use = (iu + e < n) && (!MASK || mask[iu + e]);
+                        const double d = use ? to_d(xv[u][e]) - K : 0.0;
+                        s1[u] += d;
+                        s2[u] = fma(d, d, s2[u]);
+                    }
                 }
             }
-            s1 = warp_sum(s1);
-            s2 = warp_sum(s2);
+            double t1 = (s1[0] + s1[1]) + (s1[2] + s1[3]), t2 = (s2[0] + s2[1]) + (s2[2] + s2[3]);
+            t1 = warp_sum(t1);
+            t2 = warp_sum(t2);
             if (lane == 0) {
-                double var = (s2 - s1 * s1 / nt) / nt;
-                c[j] = K + s1 / nt;
-                s[j] = (var > 0.0 && s2 != 0.0) ? sqrt(var) : 0.0;
+                double var = (t2 - t1 * t1 / nt) / nt;
+                c[j] = K + t1 / nt;
+                s[j] = (var > 0.0 && t2 != 0.0) ? sqrt(var) : 0.0;
             }
         }
     }
@@ -2285,6 +2311,7 @@ struct CdGramArgs {
                              // scaled coordinates (NEXT-3)
     double nu;               // lambda (1 - alpha): the ridge part of the curvature (1 + nu = 1 / inv_den)
     int newton;              // 1: Newton (CG) steps on a settled active set between sweeps (linear path)
+    int smem_bytes;          // dynamic shared memory of the launch (the Newton step caches G_AA rows in it)
 };
 
 // Cluster Gram CD (v7): the v6 algorithm above with its bulk spread over a
@@ -2320,6 +2347,26 @@ constexpr int kG7Helpers = kG7Threads - 32;
 #define BL_G7_SUBPHASES 0
 #endif
 #define G7CLK() (BL_G7_SUBPHASES ? clock64() : 0LL)
+// CG iteration sub-phase timers (owner rank 1 -> cd_sub[0..4]; micro-benchmarks only)
+#ifndef BL_CG_PHASES
+#define BL_CG_PHASES 0
+#endif
+#define CGCLK() (BL_CG_PHASES ? clock64() : 0LL)
+// Newton step (Q30) trigger: after BL_NEWTON_SWEEPS active sweeps on the same set and signs, the last
+// one contracting by more than BL_NEWTON_RHO; at most BL_NEWTON_MAX steps per set
+#ifndef BL_NEWTON_SWEEPS
+#define BL_NEWTON_SWEEPS 1
+#endif
+#ifndef BL_NEWTON_RHO
+#define BL_NEWTON_RHO 0.3
+#endif
+#ifndef BL_NEWTON_MAX
+#define BL_NEWTON_MAX 2
+#endif
+// Newton step (Q30): CG stops at an rms residual of BL_CG_RTOL x tol x max|beta|
+#ifndef BL_CG_RTOL
+#define BL_CG_RTOL 0.2
+#endif
 constexpr int kG7MaxR = 16;
 constexpr int kG7Stages = 4;                    // leader prefetch ring (Gd, Gp, M per stage)
 __host__ __device__ constexpr size_t gram7_smem(int nW, int R) {
@@ -2955,29 +3002,46 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
         __syncthreads();
     };
     // rows [r0, r1) of w = (G_AA + nu I) v (v: na entries in shared memory, vsh[na] = 0 when na is
-    // odd); two rows per warp, eight 16-byte loads per row and lane in flight
-    auto matvec = [&](const double *vsh, double *wsh, int na, int r0, int r1, double nu_) {
+    // odd); two rows per warp.  The first ncache rows of this CTA are read from a shared-memory copy
+    // (gc, row stride nap), the rest from L2 with eight 16-byte loads per row and lane in flight.
+    // Both paths accumulate in the same order, so the result does not depend on the caching.
+    auto matvec = [&](const double *vsh, double *wsh, int na, int r0, int r1, double nu_, const double *gc, int ncache,
+                      int nap) {
         for (int i = r0 + 2 * wid; i < r1; i += 2 * nw) {
             const bool two = i + 1 < r1;
-            const double *ra = a.GA + (int64_t)i * ldG, *rb = a.GA + (int64_t)(two ? i + 1 : i) * ldG;
+            const int l = i - r0;
             double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
-            for (int j0 = 2 * lane; j0 < na; j0 += 64 * 8) {
-                double2 ga[8], gb[8];
-#pragma unroll
-                for (int u = 0; u < 8; u++) {
-                    const int j = j0 + 64 * u;
-                    ga[u] = j < na ? __ldcg(reinterpret_cast<const double2 *>(ra + j)) : make_double2(0.0, 0.0);
-                    gb[u] = j < na ? __ldcg(reinterpret_cast<const double2 *>(rb + j)) : make_double2(0.0, 0.0);
+            if (l + (two ? 1 : 0) < ncache) {
+                const double *ra = gc + (size_t)l * nap, *rb = gc + (size_t)(two ? l + 1 : l) * nap;
+                for (int j = 2 * lane; j < na; j += 64) {
+                    const double2 ga = *reinterpret_cast<const double2 *>(ra + j);
+                    const double2 gb = *reinterpret_cast<const double2 *>(rb + j);
+                    const double2 vv = *reinterpret_cast<const double2 *>(vsh + j);
+                    a0 = fma(ga.x, vv.x, a0);
+                    a1 = fma(ga.y, vv.y, a1);
+                    b0 = fma(gb.x, vv.x, b0);
+                    b1 = fma(gb.y, vv.y, b1);
                 }
+            } else {
+                const double *ra = a.GA + (int64_t)i * ldG, *rb = a.GA + (int64_t)(two ? i + 1 : i) * ldG;
+                for (int j0 = 2 * lane; j0 < na; j0 += 64 * 8) {
+                    double2 ga[8], gb[8];
 #pragma unroll
-                for (int u = 0; u < 8; u++) {
-                    const int j = j0 + 64 * u;
-                    if (j < na) {
-                        const double2 vv = *reinterpret_cast<const double2 *>(vsh + j);
-                        a0 = fma(ga[u].x, vv.x, a0);
-                        a1 = fma(ga[u].y, vv.y, a1);
-                        b0 = fma(gb[u].x, vv.x, b0);
-                        b1 = fma(gb[u].y, vv.y, b1);
+                    for (int u = 0; u < 8; u++) {
+                        const int j = j0 + 64 * u;
+                        ga[u] = j < na ? __ldcg(reinterpret_cast<const double2 *>(ra + j)) : make_double2(0.0, 0.0);
+                        gb[u] = j < na ? __ldcg(reinterpret_cast<const double2 *>(rb + j)) : make_double2(0.0, 0.0);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; u++) {
+                        const int j = j0 + 64 * u;
+                        if (j < na) {
+                            const double2 vv = *reinterpret_cast<const double2 *>(vsh + j);
+                            a0 = fma(ga[u].x, vv.x, a0);
+                            a1 = fma(ga[u].y, vv.y, a1);
+                            b0 = fma(gb[u].x, vv.x, b0);
+                            b1 = fma(gb[u].y, vv.y, b1);
+                        }
                     }
                 }
             }
@@ -2992,8 +3056,19 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
     auto newton = [&](int na, double thr) {
         const long long c0 = clock64();
         double *vsh = sm;                                   // na (+1) doubles: the stage buffers are idle
-        double *xs = sm + 4160, *ps = xs + 1024, *ss = ps + 1024, *wsh = ss + 1024;   // this CTA's rows
-        const int r0 = (int)((int64_t)rank * na / R), r1 = (int)((int64_t)(rank + 1) * na / R);
+        double *xs = sm + 4160, *ps = xs + 1536, *ss = ps + 1536, *wsh = ss + 1536;   // this CTA's rows
+        // rows of G_AA are split over the owner CTAs (the leader keeps its per-slot state in shared
+        // memory); each owner copies as many of its rows as fit into its (otherwise idle) shared memory
+        const int r0 = rank == 0 ? 0 : (int)((int64_t)(rank - 1) * na / NB);
+        const int r1 = rank == 0 ? 0 : (int)((int64_t)rank * na / NB);
+        const int nap = (na + 1) & ~1;
+        double *gc = sm + 10304;
+        const int cap = rank == 0 ? 0 : (int)(((int64_t)a.smem_bytes / 8 - 10304) / nap);
+        const int ncache = max(0, min(r1 - r0, cap));
+        for (int e = t; e < ncache * nap; e += T_) {
+            const int l = e / nap, j = e - l * nap;
+            gc[e] = j < na ? __ldcg(a.GA + (int64_t)(r0 + l) * ldG + j) : 0.0;
+        }
         const double la = a.lam_alpha, nu = a.nu;
         auto load_r = [&]() {                               // the whole residual vector -> shared memory
             for (int j = t; j < na; j += T_) vsh[j] = __ldcg(cgr + j);
@@ -3007,7 +3082,7 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
         }
         cl.sync();                                          // r published
         load_r();
-        matvec(vsh, wsh, na, r0, r1, nu);
+        matvec(vsh, wsh, na, r0, r1, nu, gc, ncache, nap);
         __syncthreads();
         double g0 = 0.0, d0 = 0.0;
         for (int i = r0 + t; i < r1; i += T_) { g0 = fma(vsh[i], vsh[i], g0); d0 = fma(wsh[i - r0], vsh[i], d0); }
@@ -3026,15 +3101,24 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
                     xs[l] = fma(al, ps[l], xs[l]);
                     cgr[i] = fma(-al, ss[l], vsh[i]);
                 }
+                const long long q0 = CGCLK();
                 cl.sync();                                  // r published (vsh readers are past the barrier)
+                const long long q1 = CGCLK();
                 load_r();
-                matvec(vsh, wsh, na, r0, r1, nu);
+                const long long q2 = CGCLK();
+                matvec(vsh, wsh, na, r0, r1, nu, gc, ncache, nap);
                 __syncthreads();
+                const long long q3 = CGCLK();
                 double gp = 0.0, dp = 0.0;
                 for (int i = r0 + t; i < r1; i += T_) { gp = fma(vsh[i], vsh[i], gp); dp = fma(wsh[i - r0], vsh[i], dp); }
                 double gn, dn;
                 cta_sum2(gp, dp, gp, dp);
+                const long long q4 = CGCLK();
                 cl_reduce2(gp, dp, false, gn, dn);
+                const long long q5 = CGCLK();
+                if (BL_CG_PHASES && rank == 1 && t == 0) {    // (an owner's view; sub-phase cycles)
+                    dbg[0] += q1 - q0; dbg[1] += q2 - q1; dbg[2] += q3 - q2; dbg[3] += q4 - q3; dbg[4] += q5 - q4;
+                }
                 ++it;
                 if (gn <= thr2 || it >= itmax) break;
                 const double be = gn / gam;
@@ -3075,7 +3159,7 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
         }
         if (t == 0 && (na & 1)) vsh[na] = 0.0;
         __syncthreads();
-        matvec(vsh, wsh, na, r0, r1, 0.0);
+        matvec(vsh, wsh, na, r0, r1, 0.0, gc, ncache, nap);
         __syncthreads();
         for (int i = r0 + t; i < r1; i += T_) {
             const int s = __ldcg(wk.act + i);
@@ -3120,16 +3204,15 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
                             cmd_build = 1;
                         }
                         mode = 1;
-                        // a settled active set converging slowly (same set and signs over the last
-                        // two sweeps, contraction > 0.3 per sweep): one Newton step instead of the
-                        // remaining sweeps
+                        // a settled active set (the last sweep kept the set and every sign, and did
+                        // not converge): one Newton step instead of the remaining sweeps
                         if (a.newton && same && last_mode == 1 && !conv_last && red[3] == 0.0 &&
-                            sweeps_on_set >= 2 && newtons_on_set < 2 && len >= 32 && dm_prev > 0.0 &&
-                            dm_last > 0.3 * dm_prev) {
+                            sweeps_on_set >= BL_NEWTON_SWEEPS && newtons_on_set < BL_NEWTON_MAX && len >= 32 &&
+                            (BL_NEWTON_SWEEPS < 2 || (dm_prev > 0.0 && dm_last > BL_NEWTON_RHO * dm_prev))) {
                             mode = 2;
                             // CG stops at an rms residual of 0.2 tol max|beta| (the sweep that follows
                             // resolves the rest)
-                            cg_thr = 0.2 * fmax(a.tol * red[1], a.floor_) * sqrt((double)len);
+                            cg_thr = BL_CG_RTOL * fmax(a.tol * red[1], a.floor_) * sqrt((double)len);
                         }
                     } else {
                         if (pending) { cmd_catch = 1; pending = false; }
@@ -3278,6 +3361,8 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
     cl.sync();                                              // no DSMEM access past this point
     if (!leader_cta) {
         if (rank == 1 && t == 0) a.st->cd_prof[1] = pr_bulk;
+        if (BL_CG_PHASES && rank == 1 && t == 0)
+            for (int u = 0; u < 5; u++) a.st->cd_dbg[u] = dbg[u];
         return;
     }
     double l1 = 0.0, l2 = 0.0, nnz = 0.0;
@@ -3319,7 +3404,7 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
         a.st->cd_cnt[6] = pr_newton;
         a.st->cd_cnt[7] = npartial;
         dbg[7] = nchecks;                                   // (slot 7: W checks, not a sub-phase)
-        for (int u = 0; u < 8; u++) a.st->cd_dbg[u] = dbg[u];   // leader warp sub-phases
+        for (int u = BL_CG_PHASES ? 5 : 0; u < 8; u++) a.st->cd_dbg[u] = dbg[u];   // leader warp sub-phases
     }
 }
 
