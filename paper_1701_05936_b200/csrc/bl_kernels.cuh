@@ -592,9 +592,19 @@ __global__ void __launch_bounds__(kBatchThreads, 3) k_scan_batch(const T *__rest
 // conflict-free fragment loads); the accumulators land in a shared Z tile and the
 // identity-(3) epilogue, tests and list compaction run as in k_scan_batch.
 constexpr int kBMThreads = 256;              // 8 warps
-constexpr int kBMCols = 256;                 // columns per CTA tile (32 per warp)
-constexpr int kBMRows = 64;                  // residual rows per stage (4 groups of 16)
-constexpr int kBMStages = 3;
+#ifndef BL_BM_MT
+#define BL_BM_MT 4
+#endif
+constexpr int kBMMT = BL_BM_MT;              // m-tiles (8 columns each) per warp
+constexpr int kBMCols = 64 * kBMMT;          // columns per CTA tile (8 kBMMT per warp)
+#ifndef BL_BM_ROWS
+#define BL_BM_ROWS 64
+#endif
+#ifndef BL_BM_STAGES
+#define BL_BM_STAGES 3
+#endif
+constexpr int kBMRows = BL_BM_ROWS;          // residual rows per stage (groups of 16)
+constexpr int kBMStages = BL_BM_STAGES;
 constexpr int kBMStride = kBMRows + 2;       // doubles per fit in a stage
 constexpr int kBMZ = 17;                     // Z tile row stride (doubles)
 __host__ __device__ constexpr size_t batch_mma_smem(int nf) {
@@ -624,8 +634,14 @@ template <> struct XFrag<double> {
     __device__ __forceinline__ double get(int u) const { return u == 0 ? a.x : u == 1 ? a.y : u == 2 ? b.x : b.y; }
 };
 
+#ifndef BL_BM_MINB
+#define BL_BM_MINB 2
+#endif
+#ifndef BL_BM_NOREM
+#define BL_BM_NOREM 0
+#endif
 template <typename T, int NF>
-__global__ void __launch_bounds__(kBMThreads, 2) k_scan_batch_mma(const T *__restrict__ X, int64_t ld, int n, int64_t p,
+__global__ void __launch_bounds__(kBMThreads, BL_BM_MINB) k_scan_batch_mma(const T *__restrict__ X, int64_t ld, int n, int64_t p,
                                                                    const FitScan *__restrict__ fits, int nf_unused,
                                                                    const int *__restrict__ list, const int *__restrict__ lctl) {
     extern __shared__ __align__(16) double smb[];
@@ -633,8 +649,8 @@ __global__ void __launch_bounds__(kBMThreads, 2) k_scan_batch_mma(const T *__res
     __shared__ double k1s[NF];
     // fits 0..7 on the tensor cores; 1-4 further fits (cfg5: 11 = 8 + 3) as DFMAs on the same x
     // fragments instead of a second, mostly empty 8-fit MMA tile
-    constexpr int NR = (NF > 8 && NF - 8 <= 4) ? NF - 8 : 0;
-    constexpr int NT = NR ? 1 : (NF + 7) / 8, MT = 4;
+    constexpr int NR = (!BL_BM_NOREM && NF > 8 && NF - 8 <= 4) ? NF - 8 : 0;
+    constexpr int NT = NR ? 1 : (NF + 7) / 8, MT = kBMMT;
     constexpr int GPS = kBMRows / 16;                        // 16-row groups per stage
     constexpr int D = sizeof(T) == 4 ? 2 : 1;                // x groups in flight per lane (GPS % D == 0)
     double *ring = smb;
@@ -644,7 +660,7 @@ __global__ void __launch_bounds__(kBMThreads, 2) k_scan_batch_mma(const T *__res
     __syncthreads();
     if (threadIdx.x < NF) k1s[threadIdx.x] = *fs[threadIdx.x].K1;
     const int nstage = (n + kBMRows - 1) / kBMRows;
-    double *zw = Zs + (size_t)(32 * wid) * kBMZ;                 // this warp's 32 Z rows
+    double *zw = Zs + (size_t)(8 * MT * wid) * kBMZ;             // this warp's 8 MT Z rows
     // list mode (lctl = {count, use_list}): tile positions index the union scope list
     if (list && !lctl[1]) list = nullptr;
     const int64_t P = list ? (int64_t)lctl[0] : p;
@@ -665,7 +681,7 @@ __global__ void __launch_bounds__(kBMThreads, 2) k_scan_batch_mma(const T *__res
         // this lane's columns (clamped: past-the-end columns read a valid column, ignored)
         const T *xc[MT];
 #pragma unroll
-        for (int mt = 0; mt < MT; mt++) xc[mt] = X + colof(min(col0 + 32 * wid + 8 * mt + g, P - 1)) * ld;
+        for (int mt = 0; mt < MT; mt++) xc[mt] = X + colof(min(col0 + 8 * MT * wid + 8 * mt + g, P - 1)) * ld;
         double acc[MT][NT][2];
         double accr[MT][NR > 0 ? NR : 1];
 #pragma unroll
@@ -763,8 +779,8 @@ __global__ void __launch_bounds__(kBMThreads, 2) k_scan_batch_mma(const T *__res
                 }
         }
         __syncwarp();
-        const int64_t jp = col0 + 32 * wid + lane;             // tile position
-        const bool inr = jp < P;
+        const int64_t jp = col0 + 8 * MT * wid + lane;         // tile position
+        const bool inr = lane < 8 * MT && jp < P;
         const int64_t j = inr ? colof(jp) : 0;
 #pragma unroll
         for (int f = 0; f < NF; f++) {
