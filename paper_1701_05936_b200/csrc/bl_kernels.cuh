@@ -2869,18 +2869,21 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
     // positions M = (I + inv N^T)^-1 (blocks split over the CTAs' warps; scratch =
     // each CTA's first 8 KB buffers)
     auto build_A = [&](int na) {
-        // G_AA gather: each thread's column slots are read once per 4 T_ columns, then 8 rows
-        // per step are gathered with 32 independent loads in flight (the row-at-a-time loop
-        // paid two dependent L2 round trips per row)
-        constexpr int RB = 4;
+        // G_AA gather: the active list is staged in shared memory, each thread's column slots are read
+        // once per 4 T_ columns, then 8 rows per step are gathered with 32 independent loads in flight
+        // (the row-at-a-time loop paid two dependent L2 round trips per row)
+        constexpr int RB = 8;
+        int *acts = reinterpret_cast<int *>(sm + 8192);     // (the idle M stage buffers)
+        for (int i = t; i < na; i += T_) acts[i] = __ldcg(wk.act + i);
+        __syncthreads();
         for (int jb = 0; jb < na; jb += 4 * T_) {
             int aj[4];
 #pragma unroll
-            for (int k = 0; k < 4; k++) aj[k] = __ldcg(wk.act + min(jb + t + k * T_, na - 1));
+            for (int k = 0; k < 4; k++) aj[k] = acts[min(jb + t + k * T_, na - 1)];
             for (int i0 = rank; i0 < na; i0 += RB * R) {
                 int64_t rs[RB];
 #pragma unroll
-                for (int r = 0; r < RB; r++) rs[r] = (int64_t)__ldcg(wk.act + min(i0 + r * R, na - 1)) * ldG;
+                for (int r = 0; r < RB; r++) rs[r] = (int64_t)acts[min(i0 + r * R, na - 1)] * ldG;
                 double v[RB][4];
 #pragma unroll
                 for (int r = 0; r < RB; r++)
@@ -2897,6 +2900,7 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
                 }
             }
         }
+        __syncthreads();                                    // acts is overwritten by the M scratch below
         // (cl.sync: release / acquire at cluster scope)
         cl.sync();
         const int nblk = (na + 31) / 32;
@@ -2943,26 +2947,40 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
     // memory; thread q handles slot clist[q] (ascending slots: a warp's loads of one G row are
     // contiguous), eight rows' loads in flight.
     auto catch_up = [&](int nz, int nk) {
+        // slots in groups of 32 (lane = slot: each warp-load of a G row touches consecutive slots),
+        // groups block-cyclic over the CTAs; within a CTA the 8 warps split the change list and
+        // their partial sums are combined in warp order (deterministic).  One thread per slot with
+        // the whole list left most of the cluster idle: ~55k cycles per catch-up on cfg3.
         if (nz > 0 && nk > 0) {
             double *dls = sm;                                   // the stage buffers are idle here
             int *rls = reinterpret_cast<int *>(sm + 4096);
+            double *part = sm + 6144;                           // [8 warps][32 slots]
             const int *clist = reinterpret_cast<const int *>(wk.cg + 4 * nWp);
             for (int i = t; i < nz; i += T_) { dls[i] = __ldcg(wk.dl + i); rls[i] = __ldcg(wk.rl + i); }
             __syncthreads();
-            for (int q = rank * T_ + t; q < nk; q += R * T_) {
-                const int k = __ldcg(clist + q);
+            const int i0w = (int)((int64_t)wid * nz / nw), i1w = (int)((int64_t)(wid + 1) * nz / nw);
+            const int ngrp = (nk + 31) >> 5;
+            for (int g = rank; g < ngrp; g += R) {
+                const int q = 32 * g + lane;
+                const int k = __ldcg(clist + min(q, nk - 1));
                 double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-                int i0 = 0;
-                for (; i0 + 8 <= nz; i0 += 8) {
+                int i = i0w;
+                for (; i + 8 <= i1w; i += 8) {
                     double gv[8];
 #pragma unroll
-                    for (int v = 0; v < 8; v++) gv[v] = __ldcg(a.G + (int64_t)rls[i0 + v] * ldG + k);
+                    for (int v = 0; v < 8; v++) gv[v] = __ldcg(a.G + (int64_t)rls[i + v] * ldG + k);
 #pragma unroll
-                    for (int v = 0; v < 8; v++) acc[v] = fma(dls[i0 + v], gv[v], acc[v]);
+                    for (int v = 0; v < 8; v++) acc[v] = fma(dls[i + v], gv[v], acc[v]);
                 }
-                for (; i0 < nz; i0++) acc[0] = fma(dls[i0], __ldcg(a.G + (int64_t)rls[i0] * ldG + k), acc[0]);
-                const double sum = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-                wk.g[k] -= sum;
+                for (; i < i1w; i++) acc[0] = fma(dls[i], __ldcg(a.G + (int64_t)rls[i] * ldG + k), acc[0]);
+                part[wid * 32 + lane] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+                __syncthreads();
+                if (wid == 0 && q < nk) {
+                    double sum = 0.0;
+                    for (int w = 0; w < nw; w++) sum += part[w * 32 + lane];
+                    wk.g[k] -= sum;
+                }
+                __syncthreads();
             }
         }
         // (cl.sync: release / acquire at cluster scope)
