@@ -2451,6 +2451,8 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
     __shared__ __align__(16) double dsrc[DDMAX][32];   // leader: staging ring the bulk copies read
     constexpr int NS = kG7Stages;
     __shared__ __align__(8) uint64_t zfull[DZ], dfb[DDMAX], sfull[NS], sempty[NS];
+    __shared__ __align__(8) uint64_t cgbar[2];         // Newton CG: [0] residual pieces, [1] partial sums
+    __shared__ __align__(16) double cgpsum[kG7MaxR][2]; // Newton CG: every CTA's two partial sums
     __shared__ int bslot[NS][32];                      // leader: slots of the block
     __shared__ uint32_t rdq[kG7MaxR], rdfb[kG7MaxR];    // leader: owners' ring addresses (shared::cluster)
     __shared__ int ctl[2][8];                          // leader: command for the cluster (double-buffered)
@@ -2501,6 +2503,8 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
         } else {
             for (int u = 0; u < DD; u++) { mbar_init(&dfb[u], 1); mbar_arm(&dfb[u], 256); }
         }
+        mbar_init(&cgbar[0], 1);
+        mbar_init(&cgbar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     cl.sync();                                              // release / acquire at cluster scope
@@ -3087,6 +3091,7 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
         }
     };
     long long ncg = 0, nnewton = 0, pr_newton = 0, npartial = 0, nchecks = 0;
+    unsigned rph = 0u, pph = 0u;                            // Newton CG: phase parities of cgbar[0], cgbar[1]
     auto newton = [&](int na, double thr) {
         const long long c0 = clock64();
         double *vsh = sm;                                   // na (+1) doubles: the stage buffers are idle
@@ -3104,25 +3109,67 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
             gc[e] = j < na ? __ldcg(a.GA + (int64_t)(r0 + l) * ldG + j) : 0.0;
         }
         const double la = a.lam_alpha, nu = a.nu;
-        auto load_r = [&]() {                               // the whole residual vector -> shared memory
-            for (int j = t; j < na; j += T_) vsh[j] = __ldcg(cgr + j);
-            if (t == 0 && (na & 1)) vsh[na] = 0.0;
-            __syncthreads();
+        // The residual's rows travel straight into every other owner's vsh (st.async, completing on
+        // that owner's cgbar[0]), and the partial sums into every CTA's cgpsum (cgbar[1]): no
+        // cluster barrier and no L2 round trip per iteration.  Reuse is safe without more
+        // synchronisation: a CTA sends phase k+1 only after the reduction of phase k, which
+        // needs every peer's partial k, which a peer sends only after it finished reading its
+        // vsh / slots of phase k.
+        const int own = r1 - r0;
+        auto share_r = [&]() {                              // this CTA's rows (already in vsh) -> the peers
+            __syncthreads();                                // (the rows were written by other threads)
+            if (rank != 0) {
+                const int npeer = NB - 1;
+                for (int e = t; e < own * npeer; e += T_) {
+                    const int i = r0 + e % own;
+                    int pr = 1 + e / own;
+                    if (pr >= rank) ++pr;
+                    st_async(mapa(vsh + i, pr), vsh[i], mapa(&cgbar[0], pr));
+                }
+                if (t == 0) {
+                    if (na & 1) vsh[na] = 0.0;
+                    mbar_arm(&cgbar[0], (unsigned)(8 * (na - own)));
+                }
+                __syncthreads();
+                mbar_wait(&cgbar[0], rph);
+            }
+            rph ^= 1u;
+        };
+        auto p2p_reduce2 = [&](double v0, double v1, double &o0, double &o1) {   // (thread 0's values)
+            if (wid == 0) {
+                const double u0 = __shfl_sync(FULL, v0, 0), u1 = __shfl_sync(FULL, v1, 0);
+                if (lane < R && lane != rank) {             // the peers' slots [rank]
+                    const uint32_t dst = mapa(&cgpsum[rank][0], lane), bar = mapa(&cgbar[1], lane);
+                    st_async(dst, u0, bar);
+                    st_async(dst + 8, u1, bar);
+                }
+                if (lane == 0) {
+                    cgpsum[rank][0] = u0;                   // this CTA's own slot
+                    cgpsum[rank][1] = u1;
+                    mbar_arm(&cgbar[1], (unsigned)(16 * (R - 1)));
+                }
+            }
+            mbar_wait(&cgbar[1], pph);
+            pph ^= 1u;
+            __syncthreads();                                // (the own slot, written by thread 0)
+            double s0 = 0.0, s1 = 0.0;
+            for (int r = 0; r < R; r++) { s0 += cgpsum[r][0]; s1 += cgpsum[r][1]; }   // rank order
+            o0 = s0;
+            o1 = s1;
         };
         for (int i = r0 + t; i < r1; i += T_) {             // r = b (x = 0)
             const double bi = __ldcg(cgb + i);
-            cgr[i] = __ldcg(wk.g + __ldcg(wk.act + i)) - (bi > 0.0 ? la : -la) - nu * bi;
+            vsh[i] = __ldcg(wk.g + __ldcg(wk.act + i)) - (bi > 0.0 ? la : -la) - nu * bi;
             xs[i - r0] = 0.0;
         }
-        cl.sync();                                          // r published
-        load_r();
+        share_r();
         matvec(vsh, wsh, na, r0, r1, nu, gc, ncache, nap);
         __syncthreads();
         double g0 = 0.0, d0 = 0.0;
         for (int i = r0 + t; i < r1; i += T_) { g0 = fma(vsh[i], vsh[i], g0); d0 = fma(wsh[i - r0], vsh[i], d0); }
         double gam, del;
         cta_sum2(g0, d0, g0, d0);
-        cl_reduce2(g0, d0, false, gam, del);
+        p2p_reduce2(g0, d0, gam, del);
         const double thr2 = thr * thr;
         const int itmax = min(na, 256);
         int it = 0;
@@ -3133,13 +3180,11 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
                 for (int i = r0 + t; i < r1; i += T_) {     // x += al p, r -= al s
                     const int l = i - r0;
                     xs[l] = fma(al, ps[l], xs[l]);
-                    cgr[i] = fma(-al, ss[l], vsh[i]);
+                    vsh[i] = fma(-al, ss[l], vsh[i]);
                 }
                 const long long q0 = CGCLK();
-                cl.sync();                                  // r published (vsh readers are past the barrier)
-                const long long q1 = CGCLK();
-                load_r();
-                const long long q2 = CGCLK();
+                share_r();                                  // (every peer finished reading vsh: reduction k)
+                const long long q1 = CGCLK(), q2 = q1;
                 matvec(vsh, wsh, na, r0, r1, nu, gc, ncache, nap);
                 __syncthreads();
                 const long long q3 = CGCLK();
@@ -3148,7 +3193,7 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
                 double gn, dn;
                 cta_sum2(gp, dp, gp, dp);
                 const long long q4 = CGCLK();
-                cl_reduce2(gp, dp, false, gn, dn);
+                p2p_reduce2(gp, dp, gn, dn);
                 const long long q5 = CGCLK();
                 if (BL_CG_PHASES && rank == 1 && t == 0) {    // (an owner's view; sub-phase cycles)
                     dbg[0] += q1 - q0; dbg[1] += q2 - q1; dbg[2] += q3 - q2; dbg[3] += q4 - q3; dbg[4] += q5 - q4;
