@@ -3109,36 +3109,38 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
             gc[e] = j < na ? __ldcg(a.GA + (int64_t)(r0 + l) * ldG + j) : 0.0;
         }
         const double la = a.lam_alpha, nu = a.nu;
-        // The residual's rows travel straight into every other owner's vsh (st.async, completing on
-        // that owner's cgbar[0]), and the partial sums into every CTA's cgpsum (cgbar[1]): no
-        // cluster barrier and no L2 round trip per iteration.  Reuse is safe without more
-        // synchronisation: a CTA sends phase k+1 only after the reduction of phase k, which
-        // needs every peer's partial k, which a peer sends only after it finished reading its
-        // vsh / slots of phase k.
+        // The CG iterations run on the owner CTAs only (the leader holds no rows; it rejoins at the
+        // step below).  The residual's rows travel straight into every other owner's vsh
+        // (st.async, completing on that owner's cgbar[0]), and the partial sums into every owner's
+        // cgpsum (cgbar[1]): no cluster barrier and no L2 round trip per iteration.  Reuse is safe
+        // without more synchronisation because every owner both sends and needs both messages: an
+        // owner sends phase k+1 of either only after the reduction of phase k, which needs every
+        // peer's partial k, which a peer sends only after it finished reading its vsh / slots of
+        // phase k.  (With the leader taking part, it -- needing nothing from the others between two
+        // reductions -- sent its partial k+1 as soon as its own reduction k completed, which could
+        // reach an owner still waiting on a slow partial k: a phase mix-up that deadlocked a run.)
         const int own = r1 - r0;
         auto share_r = [&]() {                              // this CTA's rows (already in vsh) -> the peers
             __syncthreads();                                // (the rows were written by other threads)
-            if (rank != 0) {
-                const int npeer = NB - 1;
-                for (int e = t; e < own * npeer; e += T_) {
-                    const int i = r0 + e % own;
-                    int pr = 1 + e / own;
-                    if (pr >= rank) ++pr;
-                    st_async(mapa(vsh + i, pr), vsh[i], mapa(&cgbar[0], pr));
-                }
-                if (t == 0) {
-                    if (na & 1) vsh[na] = 0.0;
-                    mbar_arm(&cgbar[0], (unsigned)(8 * (na - own)));
-                }
-                __syncthreads();
-                mbar_wait(&cgbar[0], rph);
+            const int npeer = NB - 1;
+            for (int e = t; e < own * npeer; e += T_) {
+                const int i = r0 + e % own;
+                int pr = 1 + e / own;
+                if (pr >= rank) ++pr;
+                st_async(mapa(vsh + i, pr), vsh[i], mapa(&cgbar[0], pr));
             }
+            if (t == 0) {
+                if (na & 1) vsh[na] = 0.0;
+                mbar_arm(&cgbar[0], (unsigned)(8 * (na - own)));
+            }
+            __syncthreads();
+            mbar_wait(&cgbar[0], rph);
             rph ^= 1u;
         };
-        auto p2p_reduce2 = [&](double v0, double v1, double &o0, double &o1) {   // (thread 0's values)
+        auto p2p_reduce2 = [&](double v0, double v1, double &o0, double &o1) {   // owners; thread 0's values
             if (wid == 0) {
                 const double u0 = __shfl_sync(FULL, v0, 0), u1 = __shfl_sync(FULL, v1, 0);
-                if (lane < R && lane != rank) {             // the peers' slots [rank]
+                if (lane >= 1 && lane < R && lane != rank) {   // the other owners' slots [rank]
                     const uint32_t dst = mapa(&cgpsum[rank][0], lane), bar = mapa(&cgbar[1], lane);
                     st_async(dst, u0, bar);
                     st_async(dst + 8, u1, bar);
@@ -3146,17 +3148,19 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
                 if (lane == 0) {
                     cgpsum[rank][0] = u0;                   // this CTA's own slot
                     cgpsum[rank][1] = u1;
-                    mbar_arm(&cgbar[1], (unsigned)(16 * (R - 1)));
+                    mbar_arm(&cgbar[1], (unsigned)(16 * (R - 2)));
                 }
             }
             mbar_wait(&cgbar[1], pph);
             pph ^= 1u;
             __syncthreads();                                // (the own slot, written by thread 0)
             double s0 = 0.0, s1 = 0.0;
-            for (int r = 0; r < R; r++) { s0 += cgpsum[r][0]; s1 += cgpsum[r][1]; }   // rank order
+            for (int r = 1; r < R; r++) { s0 += cgpsum[r][0]; s1 += cgpsum[r][1]; }   // owner rank order
             o0 = s0;
             o1 = s1;
         };
+        int it = 0;
+        if (rank != 0) {                                    // ---- CG on the owners
         for (int i = r0 + t; i < r1; i += T_) {             // r = b (x = 0)
             const double bi = __ldcg(cgb + i);
             vsh[i] = __ldcg(wk.g + __ldcg(wk.act + i)) - (bi > 0.0 ? la : -la) - nu * bi;
@@ -3172,7 +3176,6 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
         p2p_reduce2(g0, d0, gam, del);
         const double thr2 = thr * thr;
         const int itmax = min(na, 256);
-        int it = 0;
         if (gam > thr2 && del > 0.0) {
             double al = gam / del;
             for (int i = r0 + t; i < r1; i += T_) { ps[i - r0] = vsh[i]; ss[i - r0] = wsh[i - r0]; }
@@ -3212,6 +3215,7 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
                 }
             }
         }
+        }                                                   // ---- (owners)
         // largest step t <= 1 that keeps every active sign; x -> global for every CTA
         double tmin = 1.0;
         for (int i = r0 + t; i < r1; i += T_) {
@@ -3439,7 +3443,10 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
     if (leader_cta && wid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     cl.sync();                                              // no DSMEM access past this point
     if (!leader_cta) {
-        if (rank == 1 && t == 0) a.st->cd_prof[1] = pr_bulk;
+        if (rank == 1 && t == 0) {
+            a.st->cd_prof[1] = pr_bulk;
+            a.st->cd_cnt[5] = ncg;                          // (CG iterations run on the owners)
+        }
         if (BL_CG_PHASES && rank == 1 && t == 0)
             for (int u = 0; u < 5; u++) a.st->cd_dbg[u] = dbg[u];
         return;
@@ -3479,7 +3486,6 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
         a.st->cd_cnt[2] = ncatch;
         a.st->cd_cnt[3] = nfull;
         a.st->cd_cnt[4] = nnewton;
-        a.st->cd_cnt[5] = ncg;
         a.st->cd_cnt[6] = pr_newton;
         a.st->cd_cnt[7] = npartial;
         dbg[7] = nchecks;                                   // (slot 7: W checks, not a sub-phase)
