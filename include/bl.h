@@ -116,9 +116,11 @@ typedef struct {
                             1 residual-update CD (r held on chip), 2 Gram only */
     int cv_mode;         /* bl_cv on a single-GPU or sharded design: 0 (default) the K+1 fits advance
                             lambda in lockstep and each KKT round's scans of all fits are one pass over X
-                             on the fp64 tensor cores (int8: integer tensor cores);
-                            1 the same with the fp64-FMA batched kernel; 2 independent concurrent fits
-                            (one pass over X per fit and round) */
+                            (SURVEY NEXT-1): fp32 designs on the tcgen05 integer tensor cores (exact digit
+                            products), fp64 designs on the fp64 tensor cores, int8
+                            designs on the integer mma.sync path; 1 the same with the fp64-FMA batched
+                            kernel; 2 independent concurrent fits (one pass over X per fit and round);
+                            3 as 0 but fp32 designs on the fp64 tensor cores (DMMA) */
     int cd_cluster;      /* CTAs per Gram-CD cluster (SMs one CD solve uses): 0 => 16 for a single fit,
                             8 for each of bl_cv's concurrent fits; or 4, 8, 16 */
     int64_t stream_chunk_bytes; /* out-of-core designs (x_is_device_ptr = 2): bytes of X per streamed

@@ -56,7 +56,7 @@ class bl_opts(ctypes.Structure):
                 ("cd_accel", ctypes.c_int)]
 
 
-CV_MODE = {"batched": 0, "batched_fma": 1, "independent": 2}
+CV_MODE = {"batched": 0, "batched_fma": 1, "independent": 2, "batched_dmma": 3}
 
 
 def _opts(stream=None, profile=False, max_kkt_rounds=0, cd="auto", cv_mode="batched", cd_cluster=0,

@@ -8,7 +8,7 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 SRC = [os.path.join(PKG, "csrc", "bl.cu")]
-DEPS = SRC + [os.path.join(PKG, "csrc", "bl_kernels.cuh"), os.path.join(ROOT, "include", "bl.h")]
+DEPS = SRC + [os.path.join(PKG, "csrc", "bl_kernels.cuh"), os.path.join(PKG, "csrc", "bl_tc.cuh"), os.path.join(ROOT, "include", "bl.h")]
 LIB = os.path.join(PKG, "libbl.so")
 
 NVCC_FLAGS = [

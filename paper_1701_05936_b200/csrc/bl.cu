@@ -7,6 +7,7 @@
 // per KKT round decides whether to re-solve ("post-convergence check").
 #include "bl.h"
 #include "bl_kernels.cuh"
+#include "bl_tc.cuh"
 
 #include <nccl.h>
 
@@ -332,6 +333,7 @@ struct bl_design {
     std::vector<int64_t> shard_off;  // world + 1 global column offsets of the shards (rank order)
     std::mutex comm_mu;
     std::atomic<int> busy{0};        // world > 1: one call at a time (collective order, bl.h)
+    float *xsc = nullptr;            // fp32: 2^-E_j per column (k_xscale), the tensor-core scan's digit scale
 };
 
 struct bl_path {
@@ -2171,8 +2173,42 @@ const void *batch_mma_kernel_n(bool f64, int nb) {
     }
     return f64 ? (const void *)k_scan_batch_mma<double, NF> : (const void *)k_scan_batch_mma<float, NF>;
 }
+// fold-batched scan kernels (bl_opts.cv_mode): BK_TC the integer tensor cores (tcgen05, fp32 designs),
+// BK_DMMA the fp64 tensor cores (fp64 designs, or on request), BK_FMA fp64 FMAs; int8 designs: IMMA
+enum BatchKind { BK_TC = 0, BK_FMA = 1, BK_DMMA = 3 };
+template <int NF>
+const void *batch_tc_kernel_n(int nb) {
+    if constexpr (NF > 1) {
+        if (nb < NF) return batch_tc_kernel_n<NF - 1>(nb);
+    }
+    return (const void *)k_scan_batch_tc<NF>;
+}
+// the per-column digit scale of an fp32 design (one pass over X, once per design)
+const float *design_xscale(bl_design *d, cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(d->pool_mu);
+    if (!d->xsc) {
+        float *x = nullptr;
+        CK(cache::dmalloc((void **)&x, sizeof(float) * (size_t)std::max<int64_t>(d->p, 1)));
+        const int grid = (int)std::min<int64_t>((d->p + 7) / 8, (int64_t)d->nsm * 8);
+        k_xscale<<<grid, 256, 0, st>>>((const float *)d->X, d->ld, (int)d->n, d->p, x);
+        CKL();
+        CK(cudaStreamSynchronize(st));
+        d->xsc = x;
+    }
+    return d->xsc;
+}
+struct TcScratch {
+    int8_t *img = nullptr;           // residual digit tiles of one pass (stages x tc_bbytes(kTcMaxFits))
+    double *rsc = nullptr;           // 2^-S_f per fit
+    int *dsum = nullptr;             // digit sums per (fit, digit)
+    ~TcScratch() {
+        if (img) cache::dfree(img);
+        if (rsc) cache::dfree(rsc);
+        if (dsum) cache::dfree(dsum);
+    }
+};
 void launch_scan_batch(bl_design *d, const std::vector<LockFit *> &fits, cudaStream_t sst, FitScan *dfs,
-                       FitScan *hfs, bl_prep *timer, bool mma, const int *list, const int *lctl) {
+                       FitScan *hfs, bl_prep *timer, int bk, const int *list, const int *lctl, TcScratch *tcs) {
     const size_t nf = fits.size();
     for (size_t u = 0; u < nf; u++) {
         bl_prep *pp = fits[u]->pp;
@@ -2208,9 +2244,41 @@ void launch_scan_batch(bl_design *d, const std::vector<LockFit *> &fits, cudaStr
         CK(cudaEventCreate(&e1));
         CK(cudaEventRecord(e0, sst));
     }
-    for (size_t u0 = 0; u0 < nf; u0 += kBatchMax) {
-        int nb = (int)std::min<size_t>(kBatchMax, nf - u0);
+    const bool tc = bk == BK_TC && d->dt == DT_F32;
+    const bool mma = bk == BK_DMMA || (bk == BK_TC && d->dt == DT_F64);
+    const int nst = (int)((d->n + kTcRows - 1) / kTcRows);
+    const float *xsc = tc ? design_xscale(d, sst) : nullptr;
+    if (tc && !tcs->img) {
+        CK(cache::dmalloc((void **)&tcs->img, (size_t)nst * tc_bbytes(kTcMaxFits)));
+        CK(cache::dmalloc((void **)&tcs->rsc, sizeof(double) * kTcMaxFits));
+        CK(cache::dmalloc((void **)&tcs->dsum, sizeof(int) * kTcRL * kTcMaxFits));
+    }
+    for (size_t u0 = 0; u0 < nf; u0 += (tc ? kTcMaxFits : kBatchMax)) {
+        int nb = (int)std::min<size_t>(tc ? kTcMaxFits : kBatchMax, nf - u0);
         const bool i8 = d->dt == DT_I8;
+        if (tc) {                                    // residual digits, then the tensor-core pass
+            FitScan *fp = dfs + u0;
+            CK(cudaMemsetAsync(tcs->img, 0, (size_t)nst * tc_bbytes(nb), sst));
+            k_rimg<<<nb, 1024, 0, sst>>>(fp, (int)d->n, tc_n(nb) / 2, tcs->img, tcs->rsc, tcs->dsum);
+            CKL();
+            const void *kern = batch_tc_kernel_n<kTcMaxFits>(nb);
+            const size_t smem = tc_smem(nb);
+            allow_dyn_smem(kern);
+            // CTA pairs (cluster dims 2), one CTA per SM, persistent over 256-column tiles
+            const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>((d->p + 2 * kTcCols - 1) / (2 * kTcCols),
+                                                                          (int64_t)d->nsm / 2));
+            const float *X = (const float *)d->X;
+            int64_t ld = d->ld, p = d->p;
+            int n = (int)d->n;
+            const int8_t *img = tcs->img;
+            const double *rsc = tcs->rsc;
+            const int *dsum = tcs->dsum;
+            void *args[] = {&X, &ld, &n, &p, &fp, &xsc, &img, &rsc, &dsum, &list, &lctl};
+            CK(cudaLaunchKernel(kern, dim3(2 * pairs), dim3(kTcThreads), args, smem, sst));
+            timer->launches += 2;
+            timer->batch_passes++;
+            continue;
+        }
         const void *kern = i8 ? batch_i8_kernel_n<kBatchMax>(nb)
                          : mma ? batch_mma_kernel_n<kBatchMax>(f64, nb) : batch_kernel(f64, nb);
         const size_t smem = i8 ? batch_i8_smem(nb) : mma ? batch_mma_smem(nb) : batch_smem(nb, itemsize(d->dt));
@@ -2259,7 +2327,8 @@ void cv_lockstep(bl_design *d, const double *y, const std::vector<int32_t> &fold
     void **dptr = nullptr, **hptr = nullptr;               // per pending fit: flags, nlive, RoundStatus pointers
     int *hctl = nullptr;                                   // pinned: the round's [count, use_list]
     const bool batched = true;                           // every round is one fold-batched pass (int8: IMMA)
-    const bool mma = !opts || opts->cv_mode == 0;         // fold-batched scan on the fp64 tensor cores
+    const int bk = opts ? opts->cv_mode : BK_TC;           // fold-batched scan kernel (BatchKind)
+    TcScratch tcs;
     auto t0 = std::chrono::steady_clock::now();
     auto cleanup = [&]() {
         if (sst) cudaStreamSynchronize(sst);
@@ -2352,7 +2421,7 @@ void cv_lockstep(bl_design *d, const double *y, const std::vector<int32_t> &fold
                         timer->launches += 2;
                     }
                     timer->batch_passes = 0;
-                    launch_scan_batch(d, pending, sst, dfs, hfs, timer, mma, uni + 2, uni);
+                    launch_scan_batch(d, pending, sst, dfs, hfs, timer, bk, uni + 2, uni, &tcs);
                     for (LockFit *lf : pending) copy_round(lf->pp, sst);
                     CK(cudaMemcpyAsync(hctl, uni, 2 * sizeof(int), cudaMemcpyDeviceToHost, sst));
                     CK(cudaStreamSynchronize(sst));
@@ -2797,7 +2866,7 @@ bl_status bl_cv(bl_design *d, const double *y, const double *lambda, int n_lambd
         if (!(tol > 0.0)) raise(BL_ERR_ARG, "tol must be > 0");
         if (max_iter < 1) raise(BL_ERR_ARG, "max_iter must be >= 1");
         const int cv_mode = opts ? opts->cv_mode : 0;
-        if (cv_mode < 0 || cv_mode > 2) raise(BL_ERR_ARG, "cv_mode must be 0, 1 or 2 (got %d)", cv_mode);
+        if (cv_mode < 0 || cv_mode > 3) raise(BL_ERR_ARG, "cv_mode must be 0, 1, 2 or 3 (got %d)", cv_mode);
         BusyGuard bg(d);
         std::vector<int32_t> f(n);
         if (fold_id) {
@@ -2886,7 +2955,7 @@ bl_status bl_cv(bl_design *d, const double *y, const double *lambda, int n_lambd
                 ferr[idx] = "host allocation failed";
             }
         };
-        if (cv_mode <= 1) {                             // NEXT-1: one pass over X per round for all fits
+        if (cv_mode != 2) {                             // NEXT-1: one pass over X per round for all fits
             std::vector<int> ids(mine.begin(), mine.end());
             ids.push_back(-1);
             std::vector<bl_path *> paths;
@@ -3023,6 +3092,7 @@ void bl_free(void *handle) {
         d->pool.clear();
         delete d->comm;
         if (d->owned && d->X) cache::dfree(d->X);
+        if (d->xsc) cache::dfree(d->xsc);
         if (d->host_reg) cudaHostUnregister(d->host_reg);
         d->magic = MAGIC_DEAD;
         delete d;
