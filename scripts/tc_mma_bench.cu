@@ -133,7 +133,7 @@ __device__ __forceinline__ void mma_i8_2sm(uint32_t dtmem, uint64_t ad, uint64_t
         "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}\n"
         ::"r"(dtmem), "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
 }
-template <int N>
+template <int N, int TS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1) k_bench2(int iters, int per_commit, long long *out) {
     __shared__ volatile int stop;
     extern __shared__ uint8_t sm_raw[];
@@ -164,10 +164,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1) k_bench2(int
         uint32_t v = threadIdx.x;
         int k = 0;
         const long long tend = clock64() + (long long)iters * per_commit * 180;
-        while (clock64() < tend) {
+        if (out[1] == 1) {
+            while (clock64() < tend) {
 #pragma unroll 8
-            for (int u = 0; u < 64; u++) { w[((k + u) * 512 + threadIdx.x - 128) % 12288] = v; v += 3; }
-            k += 64;
+                for (int u = 0; u < 64; u++) { w[((k + u) * 512 + threadIdx.x - 128) % 12288] = v; v += 3; }
+                k += 64;
+            }
+        } else {                                  // tcgen05.st traffic: x4 stores into columns 352 .. 447
+            const uint32_t tl = tmem + ((uint32_t)(32 * (wid & 3)) << 16) + 352;
+            while (clock64() < tend) {
+#pragma unroll 4
+                for (int u = 0; u < 24; u++) tc_st4(tl + 4 * u, v, v + 1, v + 2, v + 3);
+                tc_wait_st();
+                v += 7;
+            }
         }
     }
     if (rank == 0 && threadIdx.x == 0) {
@@ -177,10 +187,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1) k_bench2(int
         long long t0 = clock64();
         uint32_t ph = 0;
         for (int it = 0; it < iters; it++) {
+#pragma unroll 12
             for (int q = 0; q < per_commit; q++) {
                 const int ks = q & 1, a = (q >> 1) % 6;
                 const uint32_t aoff = a * 8192 + 256 * ks, boff = 49152 + 256 * ks;
-                mma_i8_2sm(tmem + (uint32_t)((a % (480 / N)) * N), mk_desc(base + aoff, 0), mk_desc(base + boff, 0), ids, q != 0);
+                if (TS == 0)
+                    mma_i8_2sm(tmem + (uint32_t)((a % (480 / N)) * N), mk_desc(base + aoff, 0), mk_desc(base + boff, 0), ids, q != 0);
+                else   // A from TMEM columns 256 + 16 a + 8 ks, D in [0, 2N)
+                    tc_mma2_ts(tmem + (uint32_t)((a / 3) * N), tmem + 256 + 16 * (a % 6) + 8 * ks, mk_desc(base + boff, 0), ids,
+                               q != 0);
             }
             asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
                          ::"r"(smem_addr(&bar)), "h"((uint16_t)3) : "memory");
@@ -199,30 +214,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1) k_bench2(int
         asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
     }
 }
-template <int N>
+template <int N, int ts = 0>
 void run2(int per_commit, int sts) {
     long long *d, h;
-    cudaMalloc(&d, 16);
-    long long init[2] = {0, sts};
-    cudaMemcpy(d, init, 16, cudaMemcpyHostToDevice);
+    cudaMalloc(&d, 24);
+    long long init[3] = {0, sts, ts};
+    cudaMemcpy(d, init, 24, cudaMemcpyHostToDevice);
     const int iters = 2000;
     const size_t smem = 65536 + 65536 + 1024;
-    cudaFuncSetAttribute(k_bench2<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_bench2<N><<<148, 640, smem>>>(10, per_commit, d);
-    k_bench2<N><<<148, 640, smem>>>(iters, per_commit, d);
+    cudaFuncSetAttribute(k_bench2<N, ts>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_bench2<N, ts><<<148, 640, smem>>>(10, per_commit, d);
+    k_bench2<N, ts><<<148, 640, smem>>>(iters, per_commit, d);
     cudaError_t e = cudaDeviceSynchronize();
     cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
     const double per = (double)h / iters / per_commit;
-    printf("sts=%d per_commit=%d i8 cta_group::2 M=256 N=%3d: %.1f cycles per MMA = %.0f MAC/clk per SM  %s\n", sts, per_commit, N, per, 128.0 * N * 32 / per,
+    printf("A=%s sts=%d per_commit=%d i8 cta_group::2 M=256 N=%3d: %.1f cycles per MMA = %.0f MAC/clk per SM  %s\n",
+           ts ? "tmem" : "smem", sts, per_commit, N, per, 128.0 * N * 32 / per,
            cudaGetErrorString(e));
     cudaFree(d);
 }
 int main2() {
     run2<80>(48, 0);
-    run2<80>(48, 1);
-    run2<80>(12, 0);
-    run2<80>(12, 1);
-    run2<256>(48, 0);
-    run2<256>(48, 1);
+    run2<96>(48, 0);
+    run2<96>(12, 0);
+    run2<96, 1>(48, 0);
+    run2<96, 1>(12, 0);
+    run2<96, 1>(48, 1);
+    run2<96, 1>(48, 2);
+    run2<96, 1>(12, 2);
+    run2<160, 1>(48, 0);
+    run2<256, 1>(48, 0);
     return 0;
 }

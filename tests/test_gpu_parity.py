@@ -357,17 +357,24 @@ def test_deterministic_repeat():
 
 # ------------------------------------------------------------------ a12 cross-validation
 
-@pytest.mark.parametrize("dtype,alpha,cd", [(np.float64, 1.0, "gram"), (np.int8, 0.5, "gram"),
-                                           (np.float32, 0.5, "residual")])
-def test_cv_parity(dtype, alpha, cd):
+@pytest.mark.parametrize("dtype,alpha,cd,cv_mode,n,p", [
+    (np.float64, 1.0, "gram", "batched", 90, 150),         # fp64 tensor cores (DMMA)
+    (np.int8, 0.5, "gram", "batched", 90, 150),            # integer mma.sync
+    (np.float32, 0.5, "residual", "batched", 90, 150),     # tcgen05 (ld % 8 == 4: 16-byte loads)
+    (np.float32, 1.0, "gram", "batched", 96, 1300),        # tcgen05, ld % 8 == 0 (32-byte loads), 6 pair tiles
+    (np.float32, 0.5, "gram", "batched", 203, 700),        # tcgen05, ragged last stage (203 = 3 x 64 + 11)
+    (np.float32, 0.5, "gram", "batched_dmma", 90, 150),    # the fp64-tensor-core kernel on an fp32 design
+    (np.float32, 1.0, "gram", "batched_fma", 90, 150)])
+def test_cv_parity(dtype, alpha, cd, cv_mode, n, p):
+    """bl_cv against the oracle's CV (a12) for every fold-batched scan kernel."""
     kind = "geno" if dtype == np.int8 else "iid"
-    inst = synth.random_instance(90, 150, dtype=dtype, seed=53, kind=kind, n_true=6, const_cols=1)
+    inst = synth.random_instance(n, p, dtype=dtype, seed=53, kind=kind, n_true=6, const_cols=1)
     K = 5
     f = oracle.folds(inst.n, K, 1234)
     lm = oracle.lambda_max(inst, inst.y, alpha)[0]
     lams = synth.lambda_grid(lm, 20, 0.05)
     E, cve, cvse, lmin = oracle.cv(inst, inst.y, f, K, lams, alpha=alpha, tol=1e-12)
-    g = design(inst).cv(inst.y, lams, K=K, alpha=alpha, tol=1e-10, seed=1234, cd=cd)
+    g = design(inst).cv(inst.y, lams, K=K, alpha=alpha, tol=1e-10, seed=1234, cd=cd, cv_mode=cv_mode)
     assert np.array_equal(g.fold_id, f)            # same counter-based permutation (Q18)
     np.testing.assert_allclose(g.E, E, rtol=1e-6, atol=1e-9 * E.max())
     np.testing.assert_allclose(g.cve, cve, rtol=1e-7)
