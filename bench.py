@@ -265,7 +265,8 @@ def run_ours(args, rank, world, local_rank):
         if is_logit:
             return d.fit_path_binomial(inst.y, lams, alpha=inst.alpha, tol=inst.tol, stream=sh, profile=profile)
         if is_cv:
-            return d.cv(inst.y, lams, K=10, alpha=inst.alpha, tol=inst.tol, seed=0, profile=profile, cd=args.cd)
+            return d.cv(inst.y, lams, K=10, alpha=inst.alpha, tol=inst.tol, seed=0, profile=profile, cd=args.cd,
+                        cv_mode=args.cv_mode)
         return d.fit_path(inst.y, lams, alpha=inst.alpha, tol=inst.tol, stream=sh, profile=profile, cd=args.cd)
 
     for _ in range(args.warmup):
@@ -346,15 +347,23 @@ def run_ours(args, rank, world, local_rank):
                 "peak_source": "measured pinned host -> device copy bandwidth in this run", "unit": "GB/s",
                 "frac": achieved / link_gbs if achieved and link_gbs else None, "traffic": None}
     if is_cv:
-        # the fold-batched scan (one pass over X for all 11 fits) is fp64-FMA bound: 11 FMAs per element
         fits = 11
         flops = 2.0 * fits * scan_bytes / X.element_size()
         tfl = flops / (scan_ms / 1e3) / 1e12 if scan_ms > 0 else None
-        fpk = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))["fp64_tflops"]
-        roof = {"kernel": "k_scan_batch_mma (fold-batched fused scan on the fp64 tensor cores, 11 residuals per pass over X)", "bound": "alu",
-                "achieved": tfl, "peak": fpk, "peak_source": "measured fp64 FMA throughput (scripts/fp64_peak.cu, profiles/fp64_peak.json)",
-                "unit": "TFLOP/s", "frac": tfl / fpk if tfl else None, "traffic": None,
-                "x_read_GBps": achieved, "x_read_frac_of_hbm": achieved / pk["hbm_gbs"] if achieved else None}
+        if args.cv_mode == "batched" and X.dtype == torch.float32:
+            # the fold-batched scan on the tcgen05 integer tensor cores (exact digit products): one pass
+            # over X serves all 11 fits and the int8 MMAs have >100x the needed rate -- bound by reading X
+            roof = {"kernel": "k_scan_batch_tc (fold-batched fused scan, tcgen05 kind::i8 on SM pairs, 11 residuals per pass over X)",
+                    "bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "peak_source": pk_src, "unit": "GB/s",
+                    "frac": achieved / pk["hbm_gbs"] if achieved else None, "traffic": None,
+                    "useful_fp64_equiv_TFLOPs": tfl}
+        else:
+            # the fp64 tensor-core / FMA kernels: 11 FMAs per element, at the fp64 ridge
+            fpk = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))["fp64_tflops"]
+            roof = {"kernel": "k_scan_batch_mma (fold-batched fused scan on the fp64 tensor cores, 11 residuals per pass over X)", "bound": "alu",
+                    "achieved": tfl, "peak": fpk, "peak_source": "measured fp64 FMA throughput (scripts/fp64_peak.cu, profiles/fp64_peak.json)",
+                    "unit": "TFLOP/s", "frac": tfl / fpk if tfl else None, "traffic": None,
+                    "x_read_GBps": achieved, "x_read_frac_of_hbm": achieved / pk["hbm_gbs"] if achieved else None}
     traffic = None
     tf = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
     if os.path.exists(tf):
@@ -396,7 +405,7 @@ def run_ours(args, rank, world, local_rank):
                    "n_lambda": inst.nlam, "lambda_min_ratio": inst.ratio, "tol": inst.tol,
                    "screen": "SSR (logistic, QL3)" if is_logit else "hybrid (SSR-BEDPP)",
                    "model": "logistic" if is_logit else "gaussian", "cd": args.cd, "X_bytes": int(x_bytes),
-                   "cv_folds": 10 if is_cv else None,
+                   "cv_folds": 10 if is_cv else None, "cv_mode": args.cv_mode if is_cv else None,
                    "l2_policy": "X larger than L2 (126 MB); no flush" if X.numel() * X.element_size() > 126e6
                    else "X fits L2 (reported as such)", "resident": args.resident, "parallelism": f"column-sharded x{world}" if world > 1 else "1 GPU",
                    "p_global": p_global},
@@ -450,6 +459,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=20.0,
                     help="cpu_baseline time budget: the oracle runs lambdas of the grid until it is spent")
+    ap.add_argument("--cv-mode", default="batched", choices=["batched", "batched_dmma", "batched_fma", "independent"],
+                    help="cfg5: the fold-batched scan kernel (bl_opts.cv_mode)")
     ap.add_argument("--cd", default="auto", choices=["auto", "residual", "gram"],
                     help="CD flavour: residual updates (r on chip) or covariance updates (NEXT-2)")
     args = ap.parse_args()
