@@ -278,7 +278,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
         const int qq = wid & 3, h = (wid - 5) >> 2, m = 32 * qq + lane;
         const uint32_t tl = tmem + ((uint32_t)(32 * qq) << 16) + ABASE + 4 * h;
         const bool copier = wid == 5 && lane == 0;
-        const bool v8ok = (ld & 7) == 0;                           // 32-byte aligned column segments
+        const bool v8ok = (ld & 7) == 0 && (reinterpret_cast<uintptr_t>(X) & 31) == 0;   // 32-byte aligned segments
         uint32_t g = 0;                                            // stage counter (all tiles)
         for (int64_t tile = pair0; tile < ntiles; tile += npair) {
             const int64_t jc = colof(min(tile * 2 * kTcCols + q * kTcCols + m, P - 1));   // past the end: ignored

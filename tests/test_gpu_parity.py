@@ -347,6 +347,24 @@ def test_device_pointer_design_matches_host():
     assert np.array_equal(a.beta_std, b.beta_std) and np.array_equal(a.feat, b.feat)
 
 
+def test_tc_batched_scan_alignment_paths_agree():
+    """The tcgen05 fold-batched scan reads 32-byte segments when the design's base and ld allow it
+    and 16-byte ones otherwise; its arithmetic is exact integer digit products, so a CV on a
+    design whose base is only 16-byte aligned is bitwise the CV on an aligned copy."""
+    import torch
+    inst = synth.random_instance(96, 900, dtype=np.float32, seed=61, n_true=6)
+    hx = inst.host_X()                                   # (p, ld), ld = 96
+    buf = torch.zeros(hx.size + 4, dtype=torch.float32, device="cuda")
+    mis = buf[4:].view(hx.shape)                         # base 16 bytes past a 256-byte boundary
+    mis.copy_(torch.from_numpy(hx))
+    ali = torch.from_numpy(hx).cuda()
+    assert mis.data_ptr() % 32 == 16 and ali.data_ptr() % 32 == 0
+    lams = synth.lambda_grid(oracle.lambda_max(inst, inst.y)[0], 15, 0.05)
+    a = bl.Design(ali, inst.n).cv(inst.y, lams, K=5, tol=1e-10, seed=3)
+    b = bl.Design(mis, inst.n).cv(inst.y, lams, K=5, tol=1e-10, seed=3)
+    assert np.array_equal(a.E, b.E) and np.array_equal(a.full.beta_std, b.full.beta_std)
+
+
 def test_deterministic_repeat():
     inst = synth.random_instance(128, 3000, dtype=np.float32, seed=47, kind="corr")
     d = design(inst)
