@@ -8,6 +8,7 @@ import sys
 LIB = sys.argv[1] if len(sys.argv) > 1 else "paper_1701_05936_b200/libbl.so"
 CLASSES = [
     ("DMMA", r"\bDMMA\b"), ("IMMA", r"\bIMMA\b"), ("HMMA", r"\bHMMA\b"), ("UTCMMA (tcgen05)", r"\bUTC\w*MMA\b"),
+    ("STTM (tcgen05.st)", r"\bSTTM"), ("LDTM (tcgen05.ld)", r"\bLDTM"), ("UTCBAR (tcgen05.commit)", r"\bUTCBAR"),
     ("UBLKCP (bulk copy)", r"\bUBLKCP\b"), ("UTMALDG (TMA)", r"\bUTMALDG\b"), ("SYNCS (mbarrier)", r"\bSYNCS\b"),
     ("STAS (st.async)", r"\bSTAS\b"), ("LDGSTS (cp.async)", r"\bLDGSTS\b"), ("DFMA", r"\bDFMA\b"),
     ("UCGABAR (cluster barrier)", r"\bUCGABAR"), ("LDG", r"\bLDG\b"), ("STG", r"\bSTG\b"),
