@@ -37,18 +37,18 @@
 //
 // Roles (a cluster of 2 CTAs = one SM pair, persistent over 256-column tiles; CTA rank q owns
 // tile columns 128 q .. 128 q + 127 = its 128 TMEM lanes):
-//   warps 0-3   epilogue: tcgen05.ld of the 6 x N accumulator columns of their 32 TMEM
+//   warps 0-3   epilogue: tcgen05.ld of the 2 x N accumulator columns of their 32 TMEM
 //               lanes, bias removal, recombination, identity (3), KKT / strong tests,
 //               ballot-compacted lists (as k_scan_batch)
-//   warp  4     TMEM allocation (cta_group::2); in rank 0, lane 0 issues the pair's MMAs and
-//               commits; in rank 1, lane 0 relays "stage full" to rank 0's barrier
-//   warps 5-20  converters: warp (lane quarter wid % 4, row group (wid - 5) / 4): column
-//               32 (wid % 4) + lane, 16 rows of each stage -> registers (float4 loads, two
+//   warps 4-19  converters: warp (lane quarter wid % 4, row group (wid - 4) / 4): column
+//               32 (wid % 4) + lane, 16 rows of each stage -> registers (32-byte loads, two
 //               stages ahead) -> five digit-plane words x 4 -> tcgen05.st into the stage's A
 //               slot in TMEM (lane = column, 16 columns of 4 K-bytes per plane); converter 0
 //               also bulk-copies (cp.async.bulk, mbarrier tx count) this CTA's half of the
 //               stage's residual digit tiles (3 byte-plane variants x N / 2 rows: the
 //               cta_group::2 B split), prepared once per pass by k_rimg
+//   warp 20     TMEM allocation (cta_group::2); in rank 0, lane 0 issues the pair's MMAs and
+//               commits; in rank 1, lane 0 relays "stage full" to rank 0's barrier
 // Ring of kTcStages stages: A slots in TMEM (80 columns each), B slots in shared memory;
 // barriers full (converter warps + bulk tx), pfull (rank 1's relay, in rank 0), empty
 // (multicast commit), tfull (multicast commit), tempty (8 epilogue warps of the pair, in
@@ -66,6 +66,7 @@ constexpr int kTcRL = 6;                         // residual digits
 constexpr int kTcDiag = 8;                       // diagonals s = byte + digit, 0 .. 7
 constexpr int kTcConvWarps = 16;
 constexpr int kTcThreads = 32 * (4 + 1 + kTcConvWarps);
+constexpr int kTcMmaWarp = 4 + kTcConvWarps;     // warps 0-3 epilogue, 4-19 converters (whole warpgroups), 20 MMA
 constexpr int kTcAcols = kTcXL * kTcRows / 4;    // TMEM columns of one A slot (80)
 constexpr int kTcMaxFits = 12;                   // 8 * 12 = 96 = N; 2 N + 4 * 80 = 512 TMEM columns
 __host__ __device__ constexpr int tc_n(int nf) { return ((kTcDiag * nf + 15) / 16) * 16; }
@@ -249,7 +250,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
         mbar_init(&tempty, 8);                                  // the pair's 8 epilogue warps
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (wid == 4) {
+    if (wid == kTcMmaWarp) {
         asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_sh)),
                      "r"(512));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
@@ -271,13 +272,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     const int nst = (n + kTcRows - 1) / kTcRows;
     auto colof = [&](int64_t pos) -> int64_t { return list ? (int64_t)list[pos] : pos; };
 
-    if (wid >= 5) {
+    if (wid >= 4 && wid < kTcMmaWarp) {
         // ---------------- converters: column m = 32 (wid % 4) + lane (= its TMEM lane), rows
-        // 16 h .. 16 h + 15 of every stage, h = (wid - 5) / 4: two 32-byte loads per stage (four
+        // 16 h .. 16 h + 15 of every stage, h = (wid - 4) / 4: two 32-byte loads per stage (four
         // 16-byte loads if ld % 8 != 0), held in registers two stages ahead (three sets in rotation)
-        const int qq = wid & 3, h = (wid - 5) >> 2, m = 32 * qq + lane;
+        const int qq = wid & 3, h = (wid - 4) >> 2, m = 32 * qq + lane;
         const uint32_t tl = tmem + ((uint32_t)(32 * qq) << 16) + ABASE + 4 * h;
-        const bool copier = wid == 5 && lane == 0;
+        const bool copier = wid == 4 && lane == 0;
         const bool v8ok = (ld & 7) == 0 && (reinterpret_cast<uintptr_t>(X) & 31) == 0;   // 32-byte aligned segments
         uint32_t g = 0;                                            // stage counter (all tiles)
         for (int64_t tile = pair0; tile < ntiles; tile += npair) {
@@ -369,7 +370,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
                 if (s + 2 < nst) step(xd, xb, s + 2);
             }
         }
-    } else if (wid == 4) {
+    } else if (wid == kTcMmaWarp) {
         if (lane == 0 && q == 0) {
             // ---------------- MMA issuer of the pair (rank 0)
             uint32_t g = 0, it = 0;
@@ -469,7 +470,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     tc_fence_before();
     cluster_arrive();                                              // both CTAs done: every MMA has retired
     cluster_wait();
-    if (wid == 4) {
+    if (wid == kTcMmaWarp) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
     }
