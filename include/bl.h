@@ -280,6 +280,18 @@ bl_status bl_bedpp(bl_prep *pp, double lambda, uint8_t *keep, int64_t *n_keep);
 bl_status bl_scan(bl_prep *pp, const double *r, double lam, double lam_next, const uint8_t *in_w,
                   double *z, int32_t *viol, int64_t *n_viol, int32_t *strong, int64_t *n_strong);
 
+/* Fold-batched scan (SURVEY 8(a) a9 + a12, NEXT-1; one pass over X for several
+ * fits): the fused scan of bl_scan for nf fits of ONE design at once, by the kernel bl_cv's
+ * lockstep rounds use for that design (cv_mode as in bl_opts: 0 the default -- fp32 designs on
+ * the tcgen05 integer tensor cores, fp64 on the fp64 tensor cores, int8 on the integer mma.sync
+ * path; 1 the fp64-FMA kernel; 3 fp32 designs on the fp64 tensor cores).  pps: nf distinct
+ * preps (bl_prepare, any row masks); r[u]: fit u's residual (n host doubles, 0 on rows outside
+ * its mask).  z: nf x p_local doubles, fit-major (NULL: not copied); n_viol / n_strong: nf
+ * counts of the two tests at (lam, lam_next) with no working set (NULL: not copied).  Errors:
+ * BL_ERR_ARG for bad handles, repeated preps, preps of different designs or another cv_mode. */
+bl_status bl_scan_batch(bl_prep *const *pps, int nf, const double *const *r, double lam, double lam_next,
+                        int cv_mode, double *z, int64_t *n_viol, int64_t *n_strong);
+
 /* NULL-safe, idempotent per live handle: frees a design, path, cv result or prep. */
 void bl_free(void *handle);
 const char *bl_last_error(void);

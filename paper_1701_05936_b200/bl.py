@@ -88,7 +88,7 @@ class bl_perf(ctypes.Structure):
 _lib = None
 EXPORTS = ["bl_load_design", "bl_nccl_unique_id", "bl_lambda_max", "bl_fit_path", "bl_cv", "bl_path_info",
            "bl_path_copy", "bl_path_perf", "bl_path_screen", "bl_fit_path_binomial", "bl_path_irls", "bl_cv_copy", "bl_cv_errors", "bl_cv_perf", "bl_prepare", "bl_prep_copy",
-           "bl_bedpp", "bl_scan", "bl_free", "bl_last_error"]
+           "bl_bedpp", "bl_scan", "bl_scan_batch", "bl_free", "bl_last_error"]
 
 
 def lib():
@@ -119,6 +119,7 @@ def lib():
     L.bl_prep_copy.argtypes = [P, P, P, P, P, P, P]
     L.bl_bedpp.argtypes = [P, D, P, P]
     L.bl_scan.argtypes = [P, P, D, D, P, P, P, P, P, P]
+    L.bl_scan_batch.argtypes = [P, ctypes.c_int, P, D, D, ctypes.c_int, P, P, P]
     L.bl_free.argtypes = [P]
     L.bl_free.restype = None
     L.bl_last_error.restype = ctypes.c_char_p
@@ -254,6 +255,21 @@ class Prep:
         if getattr(self, "h", None):
             lib().bl_free(self.h)
             self.h = None
+
+
+def scan_batch(preps, rs, lam, lam_next=-1.0, cv_mode="batched"):
+    """bl_scan_batch: the fused scans of several fits of one design in one fold-batched pass.
+    Returns z (nf, p) and the violator / strong counts per fit."""
+    nf = len(preps)
+    rs = [_f64(r) for r in rs]
+    hs = (ctypes.c_void_p * nf)(*[pr.h.value for pr in preps])
+    rp = (ctypes.c_void_p * nf)(*[r.ctypes.data for r in rs])
+    p = preps[0].p
+    z = np.empty((nf, p))
+    nv = np.empty(nf, np.int64); ns = np.empty(nf, np.int64)
+    _check(lib().bl_scan_batch(ctypes.cast(hs, ctypes.c_void_p), nf, ctypes.cast(rp, ctypes.c_void_p), lam, lam_next,
+                               CV_MODE[cv_mode], _p(z), _p(nv), _p(ns)))
+    return z, nv, ns
 
 
 class Design:

@@ -2207,35 +2207,36 @@ struct TcScratch {
         if (dsum) cache::dfree(dsum);
     }
 };
-void launch_scan_batch(bl_design *d, const std::vector<LockFit *> &fits, cudaStream_t sst, FitScan *dfs,
-                       FitScan *hfs, bl_prep *timer, int bk, const int *list, const int *lctl, TcScratch *tcs) {
-    const size_t nf = fits.size();
-    for (size_t u = 0; u < nf; u++) {
-        bl_prep *pp = fits[u]->pp;
-        const ScanArgs sa = fits[u]->run->scan_args();
-        FitScan &F = hfs[u];
-        F.r = pp->rscan;
-        F.K1 = sa.K1;
-        F.K2 = sa.K2v;
-        F.c = pp->c;
-        F.s = pp->s;
-        F.out = sa.out;
-        F.flags = sa.flags;
-        F.wflag = sa.wflag;
-        F.thr_viol = sa.thr_viol;
-        F.thr_strong = sa.thr_strong;
-        F.viol = sa.viol;
-        F.nviol = sa.nviol;
-        F.strong = sa.strong;
-        F.nstrong = sa.nstrong;
-        F.limbs = nullptr;
-        F.limb_scale = nullptr;
-        if (d->dt == DT_I8) {                       // the quantised residual (k_limbs, launched by the caller)
-            F.limbs = pp->limbs;
-            F.limb_scale = pp->limb_scale;
-            F.K1 = pp->limb_sum;                    // identity (3) holds exactly for the quantised vector
-        }
+// the batched kernels' view of one fit (its ScanArgs plus the residual and column statistics)
+FitScan fitscan_of(const bl_design *d, bl_prep *pp, const ScanArgs &sa) {
+    FitScan F{};
+    F.r = pp->rscan;
+    F.K1 = sa.K1;
+    F.K2 = sa.K2v;
+    F.c = pp->c;
+    F.s = pp->s;
+    F.out = sa.out;
+    F.flags = sa.flags;
+    F.wflag = sa.wflag;
+    F.thr_viol = sa.thr_viol;
+    F.thr_strong = sa.thr_strong;
+    F.viol = sa.viol;
+    F.nviol = sa.nviol;
+    F.strong = sa.strong;
+    F.nstrong = sa.nstrong;
+    F.limbs = nullptr;
+    F.limb_scale = nullptr;
+    if (d->dt == DT_I8) {                           // the quantised residual (k_limbs, launched by the caller)
+        F.limbs = pp->limbs;
+        F.limb_scale = pp->limb_scale;
+        F.K1 = pp->limb_sum;                        // identity (3) holds exactly for the quantised vector
     }
+    return F;
+}
+// One fold-batched pass for the nf fits whose FitScan entries are in hfs (host); int8 designs
+// need the fits' digit planes (k_limbs) already launched on sst.  limb_ld: the fits' plane stride.
+void launch_scan_batch_fs(bl_design *d, size_t nf, int limb_ld, cudaStream_t sst, FitScan *dfs, FitScan *hfs,
+                          bl_prep *timer, int bk, const int *list, const int *lctl, TcScratch *tcs) {
     CK(cudaMemcpyAsync(dfs, hfs, sizeof(FitScan) * nf, cudaMemcpyHostToDevice, sst));
     const bool f64 = d->dt == DT_F64;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -2289,7 +2290,6 @@ void launch_scan_batch(bl_design *d, const std::vector<LockFit *> &fits, cudaStr
         int64_t ld = d->ld, p = d->p;
         int n = (int)d->n;
         FitScan *fp = dfs + u0;
-        int limb_ld = fits[u0]->pp->limb_ld;
         void *args[] = {&X, &ld, &n, &p, &fp, &nb, &list, &lctl};
         void *args_i8[] = {&X, &ld, &n, &p, &fp, &limb_ld, &list, &lctl};
         if (i8) {
@@ -2306,6 +2306,13 @@ void launch_scan_batch(bl_design *d, const std::vector<LockFit *> &fits, cudaStr
         CK(cudaEventRecord(e1, sst));
         timer->ev_scan.push_back({e0, e1});
     }
+}
+
+void launch_scan_batch(bl_design *d, const std::vector<LockFit *> &fits, cudaStream_t sst, FitScan *dfs,
+                       FitScan *hfs, bl_prep *timer, int bk, const int *list, const int *lctl, TcScratch *tcs) {
+    for (size_t u = 0; u < fits.size(); u++) hfs[u] = fitscan_of(d, fits[u]->pp, fits[u]->run->scan_args());
+    launch_scan_batch_fs(d, fits.size(), fits.empty() ? 0 : fits[0]->pp->limb_ld, sst, dfs, hfs, timer, bk, list, lctl,
+                         tcs);
 }
 
 // fit_ids: fold index per fit (-1 = full data).  Paths (prefix on failure) and
@@ -2816,6 +2823,85 @@ bl_status bl_scan(bl_prep *pp, const double *r, double lam, double lam_next, con
         if (strong) std::copy(sv.begin(), sv.end(), strong);
         if (n_viol) *n_viol = (int64_t)v.size();
         if (n_strong) *n_strong = (int64_t)sv.size();
+    });
+}
+
+bl_status bl_scan_batch(bl_prep *const *pps, int nf, const double *const *r, double lam, double lam_next, int cv_mode,
+                        double *z, int64_t *n_viol, int64_t *n_strong) {
+    return guard([&] {
+        if (!pps || nf < 1) raise(BL_ERR_ARG, "need nf >= 1 preps");
+        if (!r) raise(BL_ERR_ARG, "r is NULL");
+        if (cv_mode != 0 && cv_mode != 1 && cv_mode != 3) raise(BL_ERR_ARG, "cv_mode must be 0, 1 or 3 (got %d)", cv_mode);
+        bl_design *d = nullptr;
+        for (int u = 0; u < nf; u++) {
+            if (!pps[u] || pps[u]->magic != MAGIC_PREP) raise(BL_ERR_ARG, "bad prep handle %d", u);
+            if (!r[u]) raise(BL_ERR_ARG, "r[%d] is NULL", u);
+            if (u == 0) d = pps[0]->d;
+            else if (pps[u]->d != d) raise(BL_ERR_ARG, "preps of different designs");
+            for (int v = 0; v < u; v++)
+                if (pps[v] == pps[u]) raise(BL_ERR_ARG, "prep %d repeated", u);
+        }
+        CK(cudaSetDevice(d->device));
+        cudaStream_t st = pps[0]->stream;
+        std::vector<FitScan> hfs(nf);
+        for (int u = 0; u < nf; u++) {                 // each fit's round inputs, as bl_scan sets them up
+            bl_prep *pp = pps[u];
+            if (pp->stream != st) {                    // (preps made by bl_prepare have their own streams)
+                cudaEvent_t ev;
+                CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                CK(cudaEventRecord(ev, pp->stream));
+                CK(cudaStreamWaitEvent(st, ev, 0));
+                CK(cudaEventDestroy(ev));
+            }
+            std::vector<double> rv(pp->vlen, 0.0);
+            std::memcpy(rv.data(), r[u], 8 * d->n);
+            CK(cudaMemcpyAsync(pp->rscan, rv.data(), 8 * pp->vlen, cudaMemcpyHostToDevice, st));
+            CK(cudaMemsetAsync(pp->wflag, 0, d->p, st));
+            CK(cudaMemsetAsync(pp->st, 0, sizeof(RoundStatus), st));
+            const int grid = (int)std::min<int64_t>((d->p + 1023) / 1024, (int64_t)d->nsm * 8);
+            k_bedpp<<<grid, 256, 0, st>>>(d->p, pp->s, pp->a, pp->b, pp->ps, pp->alpha, lam,
+                                          lam_next > 0 ? lam_next : -1.0, 0, pp->flags, nullptr, pp->st);
+            CKL();
+            k_vsum<<<1, 1024, 0, st>>>(pp->rscan, (int)d->n, pp->limb_scale + 2);
+            CKL();
+            if (d->dt == DT_I8) {
+                k_limbs<<<1, 1024, 0, st>>>(pp->rscan, (int)d->n, pp->limb_ld, pp->limbs, pp->limb_scale, pp->limb_sum);
+                CKL();
+            }
+            ScanArgs sa{};
+            sa.K1 = pp->limb_scale + 2;
+            sa.K2v = 1.0 / pp->nt;
+            sa.out = pp->z;
+            sa.flags = pp->flags;
+            sa.wflag = pp->wflag;
+            sa.thr_viol = pp->alpha * lam;
+            sa.thr_strong = lam_next > 0.0 ? std::max(0.0, pp->alpha * (2.0 * lam_next - lam)) : -1.0;
+            sa.viol = pp->viol;
+            sa.nviol = &pp->st->nviol;
+            sa.strong = pp->strong;
+            sa.nstrong = &pp->st->nstrong;
+            hfs[u] = fitscan_of(d, pp, sa);
+        }
+        FitScan *dfs = nullptr;
+        CK(cache::dmalloc((void **)&dfs, sizeof(FitScan) * nf));
+        TcScratch tcs;
+        try {
+            launch_scan_batch_fs(d, (size_t)nf, pps[0]->limb_ld, st, dfs, hfs.data(), pps[0], cv_mode, nullptr, nullptr,
+                                 &tcs);
+            for (int u = 0; u < nf; u++) {
+                if (z) CK(cudaMemcpyAsync(z + (size_t)u * d->p, pps[u]->z, 8 * d->p, cudaMemcpyDeviceToHost, st));
+                CK(cudaMemcpyAsync(pps[u]->hst, pps[u]->st, sizeof(RoundStatus), cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+                if (n_viol) n_viol[u] = pps[u]->hst->nviol;
+                if (n_strong) n_strong[u] = pps[u]->hst->nstrong;
+            }
+        } catch (...) {
+            cudaStreamSynchronize(st);
+            cache::dfree(dfs);
+            throw;
+        }
+        CK(cudaStreamSynchronize(st));
+        cache::dfree(dfs);
     });
 }
 

@@ -13,14 +13,14 @@
 //       u8 planes, 2^{8 j - 37}); the top byte of each carries the bias 64, removed exactly in
 //       the epilogue with the residual digit sums
 //   r_i ~ 2^{-S_f} R_i,  R = rint(r 2^{S_f}), |R| <= 2^46, six balanced base-256 digits (s8)
-//       (|r - r~| <= 2^{-S_f - 1} <= 2^-47 max_i |r_i|)
+//       (|r - r~| <= 2^{-S_f - 1} <= 2^-46 max_i |r_i|)
 //
 // Products of X byte j and residual digit b have the weight of the "diagonal" s = j + b, so the
 // byte planes of a chunk accumulate into ONE int32 accumulator per (fit, s) -- the B operand of
 // byte plane j holds digit b = s - j in column (f, s) -- with no rounding at all (|.| <= n
 // (255 + 255 + 96) 128 < 2^31 for n <= 27,000).  The epilogue removes the bias in int32, then
 // recombines the 2 x 8 diagonals per (column, fit) in fp64 in a fixed order.  The result differs from the exact dot product of the fp32 x and fp64 r by at most
-// 2^-36 max|x_j| ||r||_1 + 2^-47 max|r| ||x_j||_1 + the fp64 rounding of the recombination
+// 2^-36 max|x_j| ||r||_1 + 2^-46 max|r| ||x_j||_1 + the fp64 rounding of the recombination
 // (k_scan_batch_tc).
 //
 // Why integers: the fp64 pipe (DMMA = DFMA rate, 36 TFLOP/s) puts an 11-fit pass at the ridge

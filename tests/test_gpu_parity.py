@@ -107,6 +107,47 @@ def test_scan_parity(dtype):
     assert np.all(np.diff(viol) > 0) and np.all(np.diff(strong) > 0)   # sorted, unique
 
 
+@pytest.mark.parametrize("dtype,cv_mode", [(np.float32, "batched"), (np.float32, "batched_dmma"),
+                                           (np.float32, "batched_fma"), (np.float64, "batched"),
+                                           (np.float64, "batched_fma"), (np.int8, "batched")])
+def test_scan_batch_parity(dtype, cv_mode):
+    """bl_scan_batch (the fold-batched scan bl_cv's rounds use) element by element against the
+    oracle's explicit standardised dots, for 11 fits with their own row masks (10 folds + full).
+    fp64 kernels: within 1e-12 ||r||.  The tcgen05 kernel (fp32, cv_mode 0) works on 37-bit / 47-bit
+    fixed-point digits (DESIGN Q32): within its stated bound 2^-36 max|x_j| ||r||_1 + 2^-46 max|r|
+    ||x_j||_1 (per column, / n s_j) plus 1e-13 ||r|| for the fp64 recombination."""
+    kind = "geno" if dtype == np.int8 else "iid"
+    inst = synth.random_instance(301, 1031, dtype=dtype, seed=19, kind=kind, const_cols=2)
+    d = design(inst)
+    f = oracle.folds(inst.n, 10, 7)
+    rng = np.random.default_rng(9)
+    masks = [f != k for k in range(10)] + [np.ones(inst.n, bool)]
+    preps = [d.prepare(inst.y, m, 0.5) for m in masks]
+    rs = [rng.standard_normal(inst.n) * (1.0 + 100.0 * (u == 3)) * m for u, m in enumerate(masks)]
+    lam, lam_next = 0.04, 0.036
+    z, nv, ns = bl.scan_batch(preps, rs, lam, lam_next, cv_mode)
+    Xh = inst.host_X()[:, :inst.n].astype(np.float64)            # (p, n)
+    for u, (m, r) in enumerate(zip(masks, rs)):
+        z_or = oracle.std_dots(inst, r, m)
+        nr = np.linalg.norm(r)
+        if dtype == np.float32 and cv_mode == "batched":
+            c, s = oracle.column_stats(inst, m)
+            nt = int(m.sum())
+            bound = (2.0 ** -36 * np.abs(Xh).max(1) * np.abs(r).sum()
+                     + 2.0 ** -46 * np.abs(r).max() * np.abs(Xh).sum(1)) / (nt * np.where(s > 0, s, 1.0)) + 1e-13 * nr
+            assert np.all(np.abs(z[u] - z_or) <= bound), u
+            assert np.abs(z[u] - z_or).max() <= 1e-11 * nr
+        else:
+            assert np.abs(z[u] - z_or).max() <= 1e-12 * nr, u
+        # the two tests (alpha = 0.5): counts equal outside a tie band of the screening thresholds
+        live = oracle.column_stats(inst, m)[1] > 0
+        thr_v, thr_s = 0.5 * lam, 0.5 * (2 * lam_next - lam)
+        tight = (np.abs(np.abs(z_or) - thr_v) < 1e-10 * nr) | (np.abs(np.abs(z_or) - thr_s) < 1e-10 * nr)
+        ev = np.sum(live & (np.abs(z_or) > thr_v) & ~tight)
+        es = np.sum(live & (np.abs(z_or) >= thr_s) & ~tight)
+        assert ev <= nv[u] <= ev + tight.sum() and es <= ns[u] <= es + tight.sum(), u
+
+
 # ------------------------------------------------------------------ a5 BEDPP
 
 def bedpp_band(inst, alpha, lam, train=None):

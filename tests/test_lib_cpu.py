@@ -45,6 +45,17 @@ def test_sass_is_sm100a_with_tensor_core_scan():
     assert "IMMA.16832.S8.S8" in sec
 
 
+def test_sass_batched_scan_is_tcgen05():
+    """The fp32 fold-batched scan issues tcgen05 MMAs on SM pairs (UTCIMMA.2CTA) with the A operand
+    written to tensor memory (STTM) and the accumulators read back from it (LDTM)."""
+    import subprocess
+    from paper_1701_05936_b200 import build
+    sass = subprocess.run(["cuobjdump", "-sass", build.build()], capture_output=True, text=True).stdout
+    sec = sass.split("Function : _ZN2bl15k_scan_batch_tcILi11EEE")[1].split("Function :")[0]
+    for ins in ("UTCIMMA.2CTA", "STTM", "LDTM", "UTCBAR.2CTA.MULTICAST"):
+        assert ins in sec, ins
+
+
 def test_no_gpu_means_loud_failure():
     import torch
     if torch.cuda.is_available():
