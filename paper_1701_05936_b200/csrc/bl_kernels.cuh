@@ -3041,24 +3041,27 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
     };
     // rows [r0, r1) of w = (G_AA + nu I) v (v: na entries in shared memory, vsh[na] = 0 when na is
     // odd); two rows per warp.  The first ncache rows of this CTA are read from a shared-memory copy
-    // (gc, row stride nap), the rest from L2 with eight 16-byte loads per row and lane in flight.
-    // Both paths accumulate in the same order, so the result does not depend on the caching.
-    auto matvec = [&](const double *vsh, double *wsh, int na, int r0, int r1, double nu_, const double *gc, int ncache,
+    // (gc, row stride nap) held in fp32 -- twice the rows fit, half the bytes per product -- the rest
+    // from L2 (fp64) with eight 16-byte loads per row and lane in flight.  The CG solves with this
+    // operator (its recurrence residual is the residual for it); the step it yields is only an
+    // accelerator: the fp64 sweeps that follow decide convergence (Q30), and the gradient update
+    // after the step uses the fp64 G_AA (matvec with gc = nullptr).
+    auto matvec = [&](const double *vsh, double *wsh, int na, int r0, int r1, double nu_, const float *gc, int ncache,
                       int nap) {
         for (int i = r0 + 2 * wid; i < r1; i += 2 * nw) {
             const bool two = i + 1 < r1;
             const int l = i - r0;
             double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
-            if (l + (two ? 1 : 0) < ncache) {
-                const double *ra = gc + (size_t)l * nap, *rb = gc + (size_t)(two ? l + 1 : l) * nap;
+            if (gc && l + (two ? 1 : 0) < ncache) {
+                const float *ra = gc + (size_t)l * nap, *rb = gc + (size_t)(two ? l + 1 : l) * nap;
                 for (int j = 2 * lane; j < na; j += 64) {
-                    const double2 ga = *reinterpret_cast<const double2 *>(ra + j);
-                    const double2 gb = *reinterpret_cast<const double2 *>(rb + j);
+                    const float2 ga = *reinterpret_cast<const float2 *>(ra + j);
+                    const float2 gb = *reinterpret_cast<const float2 *>(rb + j);
                     const double2 vv = *reinterpret_cast<const double2 *>(vsh + j);
-                    a0 = fma(ga.x, vv.x, a0);
-                    a1 = fma(ga.y, vv.y, a1);
-                    b0 = fma(gb.x, vv.x, b0);
-                    b1 = fma(gb.y, vv.y, b1);
+                    a0 = fma((double)ga.x, vv.x, a0);
+                    a1 = fma((double)ga.y, vv.y, a1);
+                    b0 = fma((double)gb.x, vv.x, b0);
+                    b1 = fma((double)gb.y, vv.y, b1);
                 }
             } else {
                 const double *ra = a.GA + (int64_t)i * ldG, *rb = a.GA + (int64_t)(two ? i + 1 : i) * ldG;
@@ -3094,19 +3097,22 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
     unsigned rph = 0u, pph = 0u;                            // Newton CG: phase parities of cgbar[0], cgbar[1]
     auto newton = [&](int na, double thr) {
         const long long c0 = clock64();
-        double *vsh = sm;                                   // na (+1) doubles: the stage buffers are idle
-        double *xs = sm + 4160, *ps = xs + 1536, *ss = ps + 1536, *wsh = ss + 1536;   // this CTA's rows
+        // shared memory (the stage buffers are idle): vsh = the full vector (na, +1 pad when odd),
+        // then this CTA's rows of x, p, s, w, then as many of its G_AA rows as fit
+        const int vlen = (na + 2) & ~1, owp = ((na + NB - 1) / NB + 2) & ~1;
+        double *vsh = sm;
+        double *xs = sm + vlen, *ps = xs + owp, *ss = ps + owp, *wsh = ss + owp;
         // rows of G_AA are split over the owner CTAs (the leader keeps its per-slot state in shared
         // memory); each owner copies as many of its rows as fit into its (otherwise idle) shared memory
         const int r0 = rank == 0 ? 0 : (int)((int64_t)(rank - 1) * na / NB);
         const int r1 = rank == 0 ? 0 : (int)((int64_t)rank * na / NB);
         const int nap = (na + 1) & ~1;
-        double *gc = sm + 10304;
-        const int cap = rank == 0 ? 0 : (int)(((int64_t)a.smem_bytes / 8 - 10304) / nap);
+        float *gc = reinterpret_cast<float *>(wsh + owp);   // fp32 rows (8-byte aligned: nap even)
+        const int cap = rank == 0 ? 0 : (int)(((int64_t)a.smem_bytes / 8 - (vlen + 4 * owp)) * 2 / nap);
         const int ncache = max(0, min(r1 - r0, cap));
         for (int e = t; e < ncache * nap; e += T_) {
             const int l = e / nap, j = e - l * nap;
-            gc[e] = j < na ? __ldcg(a.GA + (int64_t)(r0 + l) * ldG + j) : 0.0;
+            gc[e] = j < na ? (float)__ldcg(a.GA + (int64_t)(r0 + l) * ldG + j) : 0.f;
         }
         const double la = a.lam_alpha, nu = a.nu;
         // The CG iterations run on the owner CTAs only (the leader holds no rows; it rejoins at the
@@ -3242,7 +3248,7 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
         }
         if (t == 0 && (na & 1)) vsh[na] = 0.0;
         __syncthreads();
-        matvec(vsh, wsh, na, r0, r1, 0.0, gc, ncache, nap);
+        matvec(vsh, wsh, na, r0, r1, 0.0, nullptr, 0, nap);      // fp64 G_AA: the exact gradient update
         __syncthreads();
         for (int i = r0 + t; i < r1; i += T_) {
             const int s = __ldcg(wk.act + i);

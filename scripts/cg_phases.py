@@ -2,7 +2,7 @@ import sys, os
 sys.path.insert(0, ".")
 import synth
 from paper_1701_05936_b200 import bl
-bl.LIB_PATH = "paper_1701_05936_b200/libbl_cgphases.so"
+bl.LIB_PATH = "paper_1701_05936_b200/libcgphases.so"   # build.build_variant("cgphases", ["-DBL_CG_PHASES=1"])
 for cfg in ("cfg3",):
     inst = synth.CONFIGS[cfg](device="cuda")
     d = bl.Design(inst.X, inst.n)
