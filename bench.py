@@ -399,7 +399,8 @@ def run_ours(args, rank, world, local_rank):
         "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
         "scaling": "strong" if world > 1 else "weak",
-        "vs_baseline": None, "dtype": {"cfg1": "f64", "cfg4": "i8"}.get(args.config, "f32") + "-in/f64-accum",
+        "vs_baseline": None, "dtype": ("f32-in/i8-digit-exact-scan/f64-accum" if is_cv and args.cv_mode == "batched"
+                  else {"cfg1": "f64", "cfg4": "i8"}.get(args.config, "f32") + "-in/f64-accum"),
         "data": "synthetic",
         "config": {"workload": args.config, "n": inst.n, "p": p_global, "alpha": inst.alpha,
                    "n_lambda": inst.nlam, "lambda_min_ratio": inst.ratio, "tol": inst.tol,
