@@ -2245,7 +2245,8 @@ void launch_scan_batch_fs(bl_design *d, size_t nf, int limb_ld, cudaStream_t sst
         CK(cudaEventCreate(&e1));
         CK(cudaEventRecord(e0, sst));
     }
-    const bool tc = bk == BK_TC && d->dt == DT_F32;
+    // (the integer accumulators are exact for n <= 27,000 -- bl_tc.cuh; designs hold n <= 16,384)
+    const bool tc = bk == BK_TC && d->dt == DT_F32 && d->n <= 27000;
     const bool mma = bk == BK_DMMA || (bk == BK_TC && d->dt == DT_F64);
     const int nst = (int)((d->n + kTcRows - 1) / kTcRows);
     const float *xsc = tc ? design_xscale(d, sst) : nullptr;
