@@ -2247,7 +2247,7 @@ void launch_scan_batch_fs(bl_design *d, size_t nf, int limb_ld, cudaStream_t sst
     }
     // (the integer accumulators are exact for n <= 27,000 -- bl_tc.cuh; designs hold n <= 16,384)
     const bool tc = bk == BK_TC && d->dt == DT_F32 && d->n <= 27000;
-    const bool mma = bk == BK_DMMA || (bk == BK_TC && d->dt == DT_F64);
+    const bool mma = bk == BK_DMMA || (bk == BK_TC && !tc);     // fp64 designs (and any the tc path declines)
     const int nst = (int)((d->n + kTcRows - 1) / kTcRows);
     const float *xsc = tc ? design_xscale(d, sst) : nullptr;
     if (tc && !tcs->img) {
