@@ -38,11 +38,14 @@ thread_local std::string g_err;
 // (which synchronise the device and unmap); a later allocation of a similar size
 // (need <= size <= 2 need) reuses one, so repeated design loads and fits skip the
 // driver's allocation path.  Callers return a block only after synchronising the
-// stream that used it (as they did before cudaFree).  At most kCacheCap bytes stay
+// stream that used it (as they did before cudaFree).  At most kCacheCapDev / kCacheCapHost bytes stay
 // cached per device (larger or surplus blocks go back to the driver), and a failed
 // allocation releases every cached block and retries.
 namespace cache {
-constexpr size_t kCacheCap = (size_t)2 << 30;
+// freed blocks kept for reuse (a failed allocation flushes the cache and retries): up to 8 GB of
+// device memory -- a cfg3 / cfg4-sized design reloaded in a loop reuses its buffer instead of a
+// cudaMalloc + cudaFree of 4 GB per load -- and 2 GB of pinned host memory
+constexpr size_t kCacheCapDev = (size_t)8 << 30, kCacheCapHost = (size_t)2 << 30;
 struct Pool {
     std::mutex mu;
     std::multimap<size_t, void *> freeb;
@@ -97,7 +100,7 @@ void release(void *p, bool host) {
     if (it == P.live.end()) { raw_free(p, host); return; }
     const size_t b = it->second;
     P.live.erase(it);
-    if (P.cached + b > kCacheCap) { raw_free(p, host); return; }
+    if (P.cached + b > (host ? kCacheCapHost : kCacheCapDev)) { raw_free(p, host); return; }
     P.freeb.emplace(b, p);
     P.cached += b;
 }
