@@ -922,7 +922,11 @@ std::vector<int> gather_list(bl_prep *pp, const int *dev, const std::vector<int6
 }
 
 // One-time preprocessing for (y, optional training mask).
-bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double alpha, const bl_opts *opts) {
+// Preprocessing of one fit (a2-a4), in stages so that bl_cv's lockstep fits can
+// share the two store-mode scans (a_j and b_j) as fold-batched passes (make_prep runs them per fit):
+// prep_begin (workspace, y~, column statistics), the a_j scan, prep_mid (lambda_max, j*, x~_*),
+// the b_j scan, prep_end (the solve's start, the one host round trip, degenerate-input checks).
+bl_prep *prep_begin(bl_design *d, const double *y, const uint8_t *train, double alpha, const bl_opts *opts) {
     if (!y) raise(BL_ERR_ARG, "y is NULL");
     if (!(alpha > 0.0 && alpha <= 1.0)) raise(BL_ERR_ARG, "alpha must be in (0, 1], got %g", alpha);
     CK(cudaSetDevice(d->device));
@@ -1029,6 +1033,11 @@ bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double a
         else if (d->dt == DT_F32) launch_colstats<float>(pp, (int)i0);
         else launch_colstats<int8_t>(pp, (int)i0);
     }
+    guard.pp = nullptr;
+    return pp;
+}
+
+void prep_a_scan(bl_prep *pp) {
     // a_j = x~_j' y~  (identity (2))
     {
         ScanArgs sa{};
@@ -1039,6 +1048,12 @@ bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double a
         sa.jfix = nullptr;
         launch_scan(pp, sa, pp->yt, false);
     }
+}
+
+void prep_mid(bl_prep *pp, double alpha) {
+    bl_design *d = pp->d;
+    const int64_t p = d->p;
+    cudaStream_t st = pp->stream;
     // lambda_max, j*
     k_argmax1<<<pp->amax_blocks, 256, 0, st>>>(pp->a, pp->s, p, pp->amax_v, pp->amax_i, pp->nlive);
     CKL();
@@ -1092,6 +1107,9 @@ bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double a
         d->comm->bcast(&pp->ps->sum_v, 8, pp->star_root, st);
         d->comm->group_end();
     }
+}
+
+void prep_b_scan(bl_prep *pp) {
     {
         ScanArgs sa{};
         sa.K1 = &pp->ps->sum_v;
@@ -1101,6 +1119,11 @@ bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double a
         sa.fixval = &pp->ps->nt;
         launch_scan(pp, sa, pp->vtmp, false);
     }
+}
+
+void prep_end(bl_prep *pp) {
+    bl_design *d = pp->d;
+    cudaStream_t st = pp->stream;
     // the solve starts from r = y~: r_scan <- y~ (used rows), sum r <- sum y~
     CK(cudaMemcpyAsync(pp->rscan, pp->yt, 8 * pp->vlen, cudaMemcpyDeviceToDevice, st));
     CK(cudaMemcpyAsync(&pp->st->sumr, &pp->ps->sum_yt, sizeof(double), cudaMemcpyDeviceToDevice, st));
@@ -1112,6 +1135,15 @@ bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double a
     if (!(pp->hps.Y2 > 0.0)) raise(BL_ERR_DEGENERATE, "y is constant on the used rows (y~ == 0)");
     if (pp->hps.n_live == 0 && (d->world == 1 || d->sharded)) raise(BL_ERR_DEGENERATE, "every column has zero variance");
     if (!(pp->hps.A > 0.0) && (d->world == 1 || d->sharded)) raise(BL_ERR_DEGENERATE, "lambda_max == 0: y~ orthogonal to every column");
+}
+
+bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double alpha, const bl_opts *opts) {
+    bl_prep *pp = prep_begin(d, y, train, alpha, opts);
+    PrepGuard guard{pp};
+    prep_a_scan(pp);
+    prep_mid(pp, alpha);
+    prep_b_scan(pp);
+    prep_end(pp);
     guard.pp = nullptr;
     return pp;
 }
@@ -2239,7 +2271,7 @@ FitScan fitscan_of(const bl_design *d, bl_prep *pp, const ScanArgs &sa) {
 // One fold-batched pass for the nf fits whose FitScan entries are in hfs (host); int8 designs
 // need the fits' digit planes (k_limbs) already launched on sst.  limb_ld: the fits' plane stride.
 void launch_scan_batch_fs(bl_design *d, size_t nf, int limb_ld, cudaStream_t sst, FitScan *dfs, FitScan *hfs,
-                          bl_prep *timer, int bk, const int *list, const int *lctl, TcScratch *tcs) {
+                          bl_prep *timer, int bk, const int *list, const int *lctl, TcScratch *tcs, bool prep = false) {
     CK(cudaMemcpyAsync(dfs, hfs, sizeof(FitScan) * nf, cudaMemcpyHostToDevice, sst));
     const bool f64 = d->dt == DT_F64;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -2281,7 +2313,7 @@ void launch_scan_batch_fs(bl_design *d, size_t nf, int limb_ld, cudaStream_t sst
             void *args[] = {&X, &ld, &n, &p, &fp, &xsc, &img, &rsc, &dsum, &list, &lctl};
             CK(cudaLaunchKernel(kern, dim3(2 * pairs), dim3(kTcThreads), args, smem, sst));
             timer->launches += 2;
-            timer->batch_passes++;
+            if (!prep) timer->batch_passes++;
             continue;
         }
         const void *kern = i8 ? batch_i8_kernel_n<kBatchMax>(nb)
@@ -2299,16 +2331,16 @@ void launch_scan_batch_fs(bl_design *d, size_t nf, int limb_ld, cudaStream_t sst
         if (i8) {
             CK(cudaLaunchKernel(kern, dim3(grid), dim3(threads), args_i8, smem, sst));
             timer->launches++;
-            timer->batch_passes++;
+            if (!prep) timer->batch_passes++;
             continue;
         }
         CK(cudaLaunchKernel(kern, dim3(grid), dim3(threads), args, smem, sst));
         timer->launches++;
-        timer->batch_passes++;                           // X bytes: accounted once the union size is known
+        if (!prep) timer->batch_passes++;                           // X bytes: accounted once the union size is known
     }
     if (timer->profile) {
         CK(cudaEventRecord(e1, sst));
-        timer->ev_scan.push_back({e0, e1});
+        (prep ? timer->ev_prep : timer->ev_scan).push_back({e0, e1});
     }
 }
 
@@ -2364,25 +2396,101 @@ void cv_lockstep(bl_design *d, const double *y, const std::vector<int32_t> &fold
         CK(cache::hmalloc((void **)&hptr, 3 * sizeof(void *) * std::max<size_t>(F, 1)));
         CK(cache::hmalloc((void **)&hctl, 2 * sizeof(int)));
         CK(cache::hmalloc((void **)&hfs, sizeof(FitScan) * std::max<size_t>(F, 1)));
+        // Preprocessing in stages (a2-a4): every fit's a_j and b_j store-mode scans run as two
+        // fold-batched passes over X instead of 2 (K + 1) -- NEXT-1 applied to the preprocessing
+        // (one X serves every fold); column statistics stay per fit.  A fit whose
+        // preprocessing fails (e.g. y constant on its training rows) drops out, as in the threaded mode.
+        auto drop = [&](LockFit &lf, const Err &er) {
+            lf.alive = false;
+            lf.st = er.code;
+            lf.err = g_err;
+            g_err.clear();
+            if (lf.pp) { release_prep(lf.pp); lf.pp = nullptr; }
+        };
+        auto prep_batch = [&](int which) {             // 0: a_j = x~'y~, 1: b_j = x~'x~_* (b_j* = n)
+            std::vector<LockFit *> live;
+            for (auto &lf : fits)
+                if (lf.alive && lf.pp) live.push_back(&lf);
+            if (live.empty()) return;
+            std::vector<PrepScalars> hs(live.size());
+            for (size_t u = 0; u < live.size(); u++) {
+                bl_prep *pp = live[u]->pp;
+                if (which == 1) {                          // 1 / s_* and j* of every fit on the host
+                    CK(cudaMemcpyAsync(&hs[u], pp->ps, sizeof(PrepScalars), cudaMemcpyDeviceToHost, pp->stream));
+                    CK(cudaStreamSynchronize(pp->stream));
+                }
+                cudaEvent_t ev;
+                CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                CK(cudaEventRecord(ev, pp->stream));
+                CK(cudaStreamWaitEvent(sst, ev, 0));
+                CK(cudaEventDestroy(ev));
+            }
+            for (size_t u = 0; u < live.size(); u++) {
+                bl_prep *pp = live[u]->pp;
+                const double *v = which ? pp->vtmp : pp->yt;
+                if (d->dt == DT_I8) {                      // the vector's digit planes (Q27)
+                    k_limbs<<<1, 1024, 0, sst>>>(v, (int)d->n, pp->limb_ld, pp->limbs, pp->limb_scale, pp->limb_sum);
+                    CKL();
+                }
+                ScanArgs sa{};
+                sa.K1 = which ? &pp->ps->sum_v : &pp->ps->sum_yt;
+                sa.K2v = which ? hs[u].inv_s_star : 1.0;
+                sa.out = which ? pp->b : pp->a;
+                sa.flags = pp->flags;
+                sa.wflag = pp->wflag;
+                sa.thr_viol = HUGE_VAL;                    // store mode: no tests, no lists
+                sa.thr_strong = -1.0;
+                sa.viol = pp->viol;
+                sa.nviol = &pp->st->nviol;
+                sa.strong = pp->strong;
+                sa.nstrong = &pp->st->nstrong;
+                hfs[u] = fitscan_of(d, pp, sa);
+                hfs[u].r = v;
+            }
+            // the fp64 tensor-core (or FMA) kernel: a_j and b_j feed lambda_max and BEDPP, kept fp64
+            launch_scan_batch_fs(d, live.size(), live[0]->pp->limb_ld, sst, dfs, hfs, live[0]->pp,
+                                 bk == BK_FMA ? BK_FMA : BK_DMMA, nullptr, nullptr, &tcs, true);
+            if (which == 1)
+                for (size_t u = 0; u < live.size(); u++)
+                    if (hs[u].jstar >= 0)                  // b_j* = n exactly (identity (1))
+                        CK(cudaMemcpyAsync(live[u]->pp->b + hs[u].jstar, &live[u]->pp->ps->nt, sizeof(double),
+                                           cudaMemcpyDeviceToDevice, sst));
+            cudaEvent_t ev;
+            CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            CK(cudaEventRecord(ev, sst));
+            for (LockFit *lf : live) CK(cudaStreamWaitEvent(lf->pp->stream, ev, 0));
+            CK(cudaEventDestroy(ev));
+            CK(cudaStreamSynchronize(sst));                // (hfs is rewritten by the next pass)
+        };
+        std::vector<std::vector<uint8_t>> trains(F);
         for (size_t u = 0; u < F; u++) {
             LockFit &lf = fits[u];
-            std::vector<uint8_t> train;
             if (fit_ids[u] >= 0) {
-                train.resize(n);
-                for (int64_t i = 0; i < n; i++) train[i] = fold[i] != fit_ids[u];
+                trains[u].resize(n);
+                for (int64_t i = 0; i < n; i++) trains[u][i] = fold[i] != fit_ids[u];
             }
             lf.out = new bl_path();
             lf.out->magic = MAGIC_PATH;
-            try {                                          // one degenerate fold (e.g. y constant on its
-                lf.pp = make_prep(d, y, train.empty() ? nullptr : train.data(), alpha, &fo);   // training rows)
-            } catch (const Err &er) {                      // fails that fit only, as in the threaded mode
+            try {
+                lf.pp = prep_begin(d, y, trains[u].empty() ? nullptr : trains[u].data(), alpha, &fo);
+            } catch (const Err &er) {
                 if (d->sharded) throw;                     // (a sharded fit is collective: every rank fails it)
-                lf.alive = false;
-                lf.st = er.code;
-                lf.err = g_err;
-                g_err.clear();
-                continue;
+                drop(lf, er);
             }
+        }
+        prep_batch(0);
+        for (auto &lf : fits) {
+            if (!lf.alive || !lf.pp) continue;
+            try { prep_mid(lf.pp, alpha); } catch (const Err &er) { if (d->sharded) throw; drop(lf, er); }
+        }
+        prep_batch(1);
+        for (auto &lf : fits) {
+            if (!lf.alive || !lf.pp) continue;
+            try { prep_end(lf.pp); } catch (const Err &er) { if (d->sharded) throw; drop(lf, er); }
+        }
+        for (size_t u = 0; u < F; u++) {
+            LockFit &lf = fits[u];
+            if (!lf.alive || !lf.pp) continue;
             lf.pp->batch_bytes = 0.0;
             lf.run.reset(new PathRun{lf.pp, lambda, K, alpha, tol, max_iter, BL_SCREEN_HYBRID, rounds, lf.out,
                                      fit_ids[u] >= 0 ? dE : nullptr});
