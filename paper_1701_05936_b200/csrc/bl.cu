@@ -926,7 +926,8 @@ std::vector<int> gather_list(bl_prep *pp, const int *dev, const std::vector<int6
 // share the two store-mode scans (a_j and b_j) as fold-batched passes (make_prep runs them per fit):
 // prep_begin (workspace, y~, column statistics), the a_j scan, prep_mid (lambda_max, j*, x~_*),
 // the b_j scan, prep_end (the solve's start, the one host round trip, degenerate-input checks).
-bl_prep *prep_begin(bl_design *d, const double *y, const uint8_t *train, double alpha, const bl_opts *opts) {
+bl_prep *prep_begin(bl_design *d, const double *y, const uint8_t *train, double alpha, const bl_opts *opts,
+                    bool skip_colstats = false) {
     if (!y) raise(BL_ERR_ARG, "y is NULL");
     if (!(alpha > 0.0 && alpha <= 1.0)) raise(BL_ERR_ARG, "alpha must be in (0, 1], got %g", alpha);
     CK(cudaSetDevice(d->device));
@@ -1029,7 +1030,8 @@ bl_prep *prep_begin(bl_design *d, const double *y, const uint8_t *train, double 
                                        pp->yt, pp->rfull, pp->ps);
         CKL();
         pp->launches++;
-        if (d->dt == DT_F64) launch_colstats<double>(pp, (int)i0);
+        if (skip_colstats) {                            // (bl_cv: all fits' statistics in one pass)
+        } else if (d->dt == DT_F64) launch_colstats<double>(pp, (int)i0);
         else if (d->dt == DT_F32) launch_colstats<float>(pp, (int)i0);
         else launch_colstats<int8_t>(pp, (int)i0);
     }
@@ -2462,6 +2464,10 @@ void cv_lockstep(bl_design *d, const double *y, const std::vector<int32_t> &fold
             CK(cudaEventDestroy(ev));
             CK(cudaStreamSynchronize(sst));                // (hfs is rewritten by the next pass)
         };
+        // column statistics of every fit in one pass (k_colstats_folds): folds partition the rows
+        int kfold = 0;
+        for (int64_t i = 0; i < n; i++) kfold = std::max(kfold, (int)fold[i] + 1);
+        const bool fold_stats = F <= 32 && kfold <= 32;
         std::vector<std::vector<uint8_t>> trains(F);
         for (size_t u = 0; u < F; u++) {
             LockFit &lf = fits[u];
@@ -2472,10 +2478,55 @@ void cv_lockstep(bl_design *d, const double *y, const std::vector<int32_t> &fold
             lf.out = new bl_path();
             lf.out->magic = MAGIC_PATH;
             try {
-                lf.pp = prep_begin(d, y, trains[u].empty() ? nullptr : trains[u].data(), alpha, &fo);
+                lf.pp = prep_begin(d, y, trains[u].empty() ? nullptr : trains[u].data(), alpha, &fo, fold_stats);
             } catch (const Err &er) {
                 if (d->sharded) throw;                     // (a sharded fit is collective: every rank fails it)
                 drop(lf, er);
+            }
+        }
+        if (fold_stats) {
+            std::vector<LockFit *> live;
+            std::vector<int> ff;
+            std::vector<double> nts;
+            std::vector<double *> ptrs;
+            for (size_t u = 0; u < F; u++)
+                if (fits[u].alive && fits[u].pp) {
+                    live.push_back(&fits[u]);
+                    ff.push_back(fit_ids[u]);
+                    nts.push_back(fits[u].pp->nt);
+                    ptrs.push_back(fits[u].pp->c);
+                    ptrs.push_back(fits[u].pp->s);
+                }
+            if (!live.empty()) {
+                const size_t nl = live.size();
+                std::vector<int8_t> fh(n);
+                for (int64_t i = 0; i < n; i++) fh[i] = (int8_t)fold[i];
+                char *buf = nullptr;                       // [fold ids (n, padded)][fit folds][nt][c, s pointers]
+                const size_t o_ff = round_up((size_t)n, 16), o_nt = o_ff + round_up(4 * nl, 16),
+                             o_p = o_nt + 8 * nl, tot = o_p + 16 * nl;
+                CK(cache::dmalloc((void **)&buf, tot));
+                CK(cudaMemcpyAsync(buf, fh.data(), n, cudaMemcpyHostToDevice, sst));
+                CK(cudaMemcpyAsync(buf + o_ff, ff.data(), 4 * nl, cudaMemcpyHostToDevice, sst));
+                CK(cudaMemcpyAsync(buf + o_nt, nts.data(), 8 * nl, cudaMemcpyHostToDevice, sst));
+                CK(cudaMemcpyAsync(buf + o_p, ptrs.data(), 16 * nl, cudaMemcpyHostToDevice, sst));
+                const void *kern = d->dt == DT_F64 ? (const void *)k_colstats_folds<double>
+                                 : d->dt == DT_F32 ? (const void *)k_colstats_folds<float>
+                                                   : (const void *)k_colstats_folds<int8_t>;
+                const size_t smem = (size_t)8 * kfold * 64 * 8 + round_up((size_t)n, 16);
+                allow_dyn_smem(kern);
+                const int grid = grid_for(kern, 256, smem, d->nsm);
+                const void *Xp = d->X;
+                int64_t ld = d->ld, p = d->p;
+                int nn = (int)n, K_ = kfold, nfl = (int)nl;
+                const int8_t *fd = (const int8_t *)buf;
+                const int *ffd = (const int *)(buf + o_ff);
+                const double *ntd = (const double *)(buf + o_nt);
+                double *const *csd = (double *const *)(buf + o_p);
+                void *args[] = {&Xp, &ld, &nn, &p, &fd, &K_, &ffd, &nfl, &ntd, &csd};
+                CK(cudaLaunchKernel(kern, dim3(grid), dim3(256), args, smem, sst));
+                live[0]->pp->launches++;
+                CK(cudaStreamSynchronize(sst));            // (host vectors above; a one-time pass)
+                cache::dfree(buf);
             }
         }
         prep_batch(0);

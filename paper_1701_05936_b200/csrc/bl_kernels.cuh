@@ -210,6 +210,63 @@ __global__ void __launch_bounds__(256) k_colstats(const T *__restrict__ X, int64
     }
 }
 
+// ------------------------------------------- a2 for the K + 1 fits of a cross-validation, one pass
+// Each row belongs to exactly one fold, and fit u's training rows are all rows but fold
+// fit_fold[u] (-1: all rows).  Per column (one warp) the shifted sums of every fold's rows
+// (shift K = x_0j) accumulate in this warp's shared-memory slots [fold][lane] (fold ids of the
+// rows staged once per CTA); then fit u's sums = all folds' minus its held-out fold's, and
+// c_j, s_j follow as in k_colstats (population SD).  One pass over X instead of K + 1.
+template <typename T>
+__global__ void __launch_bounds__(256) k_colstats_folds(const T *__restrict__ X, int64_t ld, int n, int64_t p,
+                                                        const int8_t *__restrict__ fold, int K,
+                                                        const int *__restrict__ fit_fold, int nf,
+                                                        const double *__restrict__ nt, double *const *__restrict__ cs) {
+    extern __shared__ __align__(16) double accs[];          // [8 warps][K][2][32]
+    int8_t *fsm = reinterpret_cast<int8_t *>(accs + (size_t)8 * K * 64);
+    constexpr int V = 16 / sizeof(T);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) fsm[i] = fold[i];
+    __syncthreads();
+    double *acc = accs + (size_t)wid * K * 64;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t j = gw; j < p; j += nwarp) {
+        const T *col = X + j * ld;
+        for (int f = 0; f < K; f++) { acc[f * 64 + lane] = 0.0; acc[f * 64 + 32 + lane] = 0.0; }
+        __syncwarp();
+        const double Ks = to_d(col[0]);
+        for (int i = lane * V; i < n; i += 32 * V) {
+            T xv[V];
+            *reinterpret_cast<int4 *>(xv) = __ldg(reinterpret_cast<const int4 *>(col + i));
+#pragma unroll
+            for (int e = 0; e < V; e++) {
+                if (i + e < n) {
+                    const double d = to_d(xv[e]) - Ks;
+                    double *a = acc + fsm[i + e] * 64 + lane;
+                    a[0] += d;
+                    a[32] = fma(d, d, a[32]);
+                }
+            }
+        }
+        __syncwarp();
+        double t1 = 0.0, t2 = 0.0, h1 = 0.0, h2 = 0.0;      // lane u < nf: fit u's held-out fold sums
+        const int fu = lane < nf ? fit_fold[lane] : -1;
+        for (int f = 0; f < K; f++) {
+            const double f1 = warp_sum(acc[f * 64 + lane]), f2 = warp_sum(acc[f * 64 + 32 + lane]);
+            t1 += f1;
+            t2 += f2;
+            if (f == fu) { h1 = f1; h2 = f2; }
+        }
+        if (lane < nf) {
+            const double s1 = t1 - h1, s2 = t2 - h2, m = nt[lane];
+            const double var = (s2 - s1 * s1 / m) / m;
+            cs[2 * lane][j] = Ks + s1 / m;
+            cs[2 * lane + 1][j] = (var > 0.0 && s2 != 0.0) ? sqrt(var) : 0.0;
+        }
+        __syncwarp();
+    }
+}
+
 // ------------------------------------------- a2 helper: y~ = (y - ybar) on the rows
 // One block.  Writes yt (ld entries, 0 outside the mask / beyond n), the
 // full-row starting residual rfull = y - ybar (beta = 0) and the scalars.
