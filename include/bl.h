@@ -295,6 +295,11 @@ bl_status bl_scan_batch(bl_prep *const *pps, int nf, const double *const *r, dou
 /* NULL-safe, idempotent per live handle: frees a design, path, cv result or prep. */
 void bl_free(void *handle);
 const char *bl_last_error(void);
+/* Return the library's cached allocations to the CUDA driver.  Freed design / workspace buffers
+ * are kept for reuse (at most 8 GB of device and 2 GB of pinned host memory per process; an
+ * allocation that fails flushes them and retries), so another allocator in the process -- e.g.
+ * PyTorch's -- may want them back first.  Safe at any time no library call is running. */
+void bl_trim(void);
 
 #ifdef __cplusplus
 }

@@ -88,7 +88,7 @@ class bl_perf(ctypes.Structure):
 _lib = None
 EXPORTS = ["bl_load_design", "bl_nccl_unique_id", "bl_lambda_max", "bl_fit_path", "bl_cv", "bl_path_info",
            "bl_path_copy", "bl_path_perf", "bl_path_screen", "bl_fit_path_binomial", "bl_path_irls", "bl_cv_copy", "bl_cv_errors", "bl_cv_perf", "bl_prepare", "bl_prep_copy",
-           "bl_bedpp", "bl_scan", "bl_scan_batch", "bl_free", "bl_last_error"]
+           "bl_bedpp", "bl_scan", "bl_scan_batch", "bl_free", "bl_last_error", "bl_trim"]
 
 
 def lib():
@@ -123,8 +123,10 @@ def lib():
     L.bl_free.argtypes = [P]
     L.bl_free.restype = None
     L.bl_last_error.restype = ctypes.c_char_p
-    for f in EXPORTS[:-2]:
-        getattr(L, f).restype = ctypes.c_int
+    L.bl_trim.restype = None
+    for f in EXPORTS:
+        if f not in ("bl_free", "bl_last_error", "bl_trim"):
+            getattr(L, f).restype = ctypes.c_int
     _lib = L
     return L
 
@@ -255,6 +257,11 @@ class Prep:
         if getattr(self, "h", None):
             lib().bl_free(self.h)
             self.h = None
+
+
+def trim():
+    """bl_trim: hand the library's cached device / pinned-host blocks back to the driver."""
+    lib().bl_trim()
 
 
 def scan_batch(preps, rs, lam, lam_next=-1.0, cv_mode="batched"):

@@ -104,6 +104,16 @@ void release(void *p, bool host) {
     P.freeb.emplace(b, p);
     P.cached += b;
 }
+// every cached block of this process back to the driver (bl_trim)
+void trim() {
+    for (bool host : {false, true}) {
+        Pool &P = pool(host);
+        std::lock_guard<std::mutex> lk(P.mu);
+        for (auto &kv : P.freeb) raw_free(kv.second, host);
+        P.freeb.clear();
+        P.cached = 0;
+    }
+}
 cudaError_t dmalloc(void **p, size_t bytes) { return alloc(p, bytes, false); }
 cudaError_t hmalloc(void **p, size_t bytes) { return alloc(p, bytes, true); }
 void dfree(void *p) { release(p, false); }
@@ -2701,6 +2711,12 @@ uint64_t splitmix64(uint64_t &state) {
 extern "C" {
 
 const char *bl_last_error(void) { return g_err.c_str(); }
+
+void bl_trim(void) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cache::trim();
+    cudaGetLastError();
+}
 
 bl_status bl_nccl_unique_id(void *out128) {
     return guard([&] {

@@ -406,6 +406,19 @@ def test_tc_batched_scan_alignment_paths_agree():
     assert np.array_equal(a.E, b.E) and np.array_equal(a.full.beta_std, b.full.beta_std)
 
 
+def test_trim_returns_cached_blocks():
+    """bl_trim hands the allocation cache back to the driver; later loads and fits still work."""
+    import torch
+    inst = synth.random_instance(64, 200, dtype=np.float32, seed=67)
+    lams = synth.lambda_grid(oracle.lambda_max(inst, inst.y)[0], 5, 0.3)
+    a = bl.Design(inst.host_X(), inst.n).fit_path(inst.y, lams, tol=1e-10)
+    free0 = torch.cuda.mem_get_info()[0]
+    bl.trim()
+    assert torch.cuda.mem_get_info()[0] >= free0
+    b = bl.Design(inst.host_X(), inst.n).fit_path(inst.y, lams, tol=1e-10)
+    assert np.array_equal(a.beta_std, b.beta_std)
+
+
 def test_deterministic_repeat():
     inst = synth.random_instance(128, 3000, dtype=np.float32, seed=47, kind="corr")
     d = design(inst)
