@@ -461,6 +461,7 @@ struct bl_prep {
     // profiling
     int profile;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_scan, ev_cd, ev_prep;
+    std::vector<cudaEvent_t> evpool;   // timing events of finished profiled fits, reused (no create per launch)
     std::vector<int64_t> scan_full;   // per timed scan launch: its local columns if it covered every live column, else -1
     int scan_rev = 0;                 // direction of the next KKT scan (alternates, see ScanArgs::rev)
     double prep_bytes;
@@ -512,15 +513,25 @@ bl_status guard(F &&f) {
     }
 }
 
+cudaEvent_t ev_get(bl_prep *pp) {
+    cudaEvent_t e;
+    if (!pp->evpool.empty()) {
+        e = pp->evpool.back();
+        pp->evpool.pop_back();
+    } else {
+        CK(cudaEventCreate(&e));
+    }
+    return e;
+}
+
 struct EvPair {
     bl_prep *pp;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> *vec;
     cudaEvent_t e1 = nullptr;
     EvPair(bl_prep *pp_, std::vector<std::pair<cudaEvent_t, cudaEvent_t>> *v) : pp(pp_), vec(v) {
         if (!pp->profile) return;
-        cudaEvent_t e0;
-        CK(cudaEventCreate(&e0));
-        CK(cudaEventCreate(&e1));
+        cudaEvent_t e0 = ev_get(pp);
+        e1 = ev_get(pp);
         CK(cudaEventRecord(e0, pp->stream));
         vec->push_back({e0, e1});
     }
@@ -535,9 +546,8 @@ struct EvPairOpt {
     cudaEvent_t e1 = nullptr;
     EvPairOpt(bl_prep *pp_, std::vector<std::pair<cudaEvent_t, cudaEvent_t>> *v) : pp(pp_), vec(v) {
         if (!pp->profile || !vec) return;
-        cudaEvent_t e0;
-        CK(cudaEventCreate(&e0));
-        CK(cudaEventCreate(&e1));
+        cudaEvent_t e0 = ev_get(pp);
+        e1 = ev_get(pp);
         CK(cudaEventRecord(e0, pp->stream));
         vec->push_back({e0, e1});
     }
@@ -547,7 +557,7 @@ struct EvPairOpt {
 };
 
 double sum_events(std::vector<std::pair<cudaEvent_t, cudaEvent_t>> &v, const std::vector<int64_t> *sel = nullptr,
-                  double *sel_ms = nullptr) {
+                  double *sel_ms = nullptr, std::vector<cudaEvent_t> *pool = nullptr) {
     double tot = 0.0;
     for (size_t i = 0; i < v.size(); i++) {
         auto &pr = v[i];
@@ -556,8 +566,13 @@ double sum_events(std::vector<std::pair<cudaEvent_t, cudaEvent_t>> &v, const std
             tot += ms;
             if (sel && sel_ms && i < sel->size() && (*sel)[i] >= 0) *sel_ms += ms;
         }
-        cudaEventDestroy(pr.first);
-        cudaEventDestroy(pr.second);
+        if (pool) {
+            pool->push_back(pr.first);
+            pool->push_back(pr.second);
+        } else {
+            cudaEventDestroy(pr.first);
+            cudaEventDestroy(pr.second);
+        }
     }
     v.clear();
     return tot;
@@ -745,6 +760,8 @@ void free_prep(bl_prep *pp) {
     sum_events(pp->ev_scan);
     sum_events(pp->ev_cd);
     sum_events(pp->ev_prep);
+    for (cudaEvent_t e : pp->evpool) cudaEventDestroy(e);
+    pp->evpool.clear();
     if (pp->arena) cache::dfree(pp->arena);
     if (pp->hst) cache::hfree(pp->hst);
     if (pp->hlist) cache::hfree(pp->hlist);
@@ -780,9 +797,9 @@ struct PrepGuard {
 void release_prep(bl_prep *pp) {
     if (!pp) return;
     if (pp->stream) cudaStreamSynchronize(pp->stream);
-    sum_events(pp->ev_scan);
-    sum_events(pp->ev_cd);
-    sum_events(pp->ev_prep);
+    sum_events(pp->ev_scan, nullptr, nullptr, &pp->evpool);
+    sum_events(pp->ev_cd, nullptr, nullptr, &pp->evpool);
+    sum_events(pp->ev_prep, nullptr, nullptr, &pp->evpool);
     pp->stream = pp->own;          // never keep a caller's stream beyond the call
     std::lock_guard<std::mutex> lk(pp->d->pool_mu);
     if (pp->d->pool.size() < 4) pp->d->pool.push_back(pp);
@@ -1166,16 +1183,31 @@ bl_prep *make_prep(bl_design *d, const double *y, const uint8_t *train, double a
 // order); `slots` = append order (stable storage slots of the Gram matrix).
 struct WorkingSet {
     std::vector<int> sorted, slots;
+    std::vector<int> ord;          // ord[q] = the storage slot of sorted[q] (the cyclic order over slots)
     // add candidates; returns the columns that were not yet in W (sorted, unique)
     std::vector<int> add(std::vector<int> cand) {
         std::sort(cand.begin(), cand.end());
         cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
         std::vector<int> fresh;
         std::set_difference(cand.begin(), cand.end(), sorted.begin(), sorted.end(), std::back_inserter(fresh));
-        std::vector<int> out;
+        if (fresh.empty()) return fresh;
+        // merge the sorted columns and their slots in one pass: fresh[i] takes slot |W| + i
+        const int base = (int)sorted.size();
+        std::vector<int> out, ord2;
         out.reserve(sorted.size() + fresh.size());
-        std::merge(sorted.begin(), sorted.end(), fresh.begin(), fresh.end(), std::back_inserter(out));
+        ord2.reserve(sorted.size() + fresh.size());
+        size_t a = 0, b = 0;
+        while (a < sorted.size() || b < fresh.size()) {
+            if (b == fresh.size() || (a < sorted.size() && sorted[a] < fresh[b])) {
+                out.push_back(sorted[a]);
+                ord2.push_back(ord[a++]);
+            } else {
+                out.push_back(fresh[b]);
+                ord2.push_back(base + (int)b++);
+            }
+        }
         sorted.swap(out);
+        ord.swap(ord2);
         slots.insert(slots.end(), fresh.begin(), fresh.end());
         return fresh;
     }
@@ -1190,10 +1222,9 @@ void upload_W(bl_prep *pp, const WorkingSet &ws, const std::vector<int> &added) 
     ensure_W(pp, (int64_t)nW);
     ensure_host(pp->hup, pp->hup_cap, 3 * nW + added.size() + 1);
     cudaStream_t st = pp->stream;
-    // cyclic order over storage slots: slots sorted by column
-    std::vector<int> ord(nW);
-    for (size_t q = 0; q < nW; q++) ord[q] = (int)q;
-    std::sort(ord.begin(), ord.end(), [&](int u, int v) { return ws.slots[u] < ws.slots[v]; });
+    // nothing new: W, its slots and order are on the device already (W only grows within a path)
+    if (added.empty()) return;
+    const std::vector<int> &ord = ws.ord;   // cyclic order over storage slots: slots sorted by column
     // this shard's new columns (local indices) -> the "in W" flags of the scans
     std::vector<int> mine;
     for (int g : added)
@@ -1253,10 +1284,9 @@ void upload_W(bl_prep *pp, const WorkingSet &ws, const std::vector<int> &added) 
 // ONE device->host round trip (the lists are short except in rare rounds).
 int list_prefix(const bl_prep *pp) { return (int)std::min<int64_t>(kListPrefix, pp->p); }   // the lists hold p entries
 void copy_round(bl_prep *pp, cudaStream_t st) {
-    CK(cudaMemcpyAsync(pp->hst, pp->st, sizeof(RoundStatus), cudaMemcpyDeviceToHost, st));
-    const size_t m = sizeof(int) * (size_t)list_prefix(pp);
-    CK(cudaMemcpyAsync(pp->hpre, pp->viol, m, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(pp->hpre + kListPrefix, pp->strong, m, cudaMemcpyDeviceToHost, st));
+    k_round_out<<<1, 256, 0, st>>>(pp->st, pp->viol, pp->strong, list_prefix(pp), pp->hst, pp->hpre, kListPrefix);
+    CKL();
+    pp->launches++;
 }
 std::vector<int> read_list(bl_prep *pp, const int *dev, int count);
 // list `which` (0 violators, 1 strong) of the round copied by copy_round
@@ -2162,11 +2192,11 @@ void finish_perf(bl_prep *pp, bl_path *out, double wall_ms) {
             pf.full_scan_launches++;
             pf.full_scan_bytes += (double)pp->scan_full[i] * (double)pp->d->n * itemsize(pp->d->dt);
         }
-    pf.scan_ms = sum_events(pp->ev_scan, &pp->scan_full, &full_ms);
+    pf.scan_ms = sum_events(pp->ev_scan, &pp->scan_full, &full_ms, &pp->evpool);
     pf.full_scan_ms = full_ms;
     pp->scan_full.clear();
-    pf.cd_ms = sum_events(pp->ev_cd);
-    pf.prep_ms = sum_events(pp->ev_prep);
+    pf.cd_ms = sum_events(pp->ev_cd, nullptr, nullptr, &pp->evpool);
+    pf.prep_ms = sum_events(pp->ev_prep, nullptr, nullptr, &pp->evpool);
     int64_t cols = 0;
     for (int k = 0; k < out->n_converged; k++) cols += out->cols_scanned[k];
     pf.scan_bytes = (double)cols * (double)pp->d->n * itemsize(pp->d->dt);

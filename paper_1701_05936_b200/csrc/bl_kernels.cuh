@@ -1339,6 +1339,21 @@ __global__ void k_upload_W(const int *__restrict__ h, int nW, int nnew, int writ
     }
 }
 
+// The round's status and the first `pre` entries of both index lists, written by ONE
+// block straight into pinned host memory (mapped, UVA): one launch instead of three
+// device->host copies per KKT round, and only the entries the counts say exist.
+// Visible to the host once the stream is synchronised (the kernel has completed).
+__global__ void k_round_out(const RoundStatus *__restrict__ st, const int *__restrict__ viol,
+                            const int *__restrict__ strong, int pre, RoundStatus *hst, int *hpre, int stride) {
+    static_assert(sizeof(RoundStatus) % 8 == 0, "RoundStatus is copied in 8-byte words");
+    const long long *s = reinterpret_cast<const long long *>(st);
+    long long *h = reinterpret_cast<long long *>(hst);
+    for (int i = threadIdx.x; i < (int)(sizeof(RoundStatus) / 8); i += blockDim.x) h[i] = s[i];
+    const int nv = min(max(st->nviol, 0), pre), ns = min(max(st->nstrong, 0), pre);
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) hpre[i] = viol[i];
+    for (int i = threadIdx.x; i < ns; i += blockDim.x) hpre[stride + i] = strong[i];
+}
+
 __global__ void k_set_flags(const int *__restrict__ idx, int cnt, uint8_t *__restrict__ f, uint8_t val) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < cnt) f[idx[i]] = val;
