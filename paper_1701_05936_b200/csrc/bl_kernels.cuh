@@ -3119,23 +3119,53 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
     // accelerator: the fp64 sweeps that follow decide convergence (Q30), and the gradient update
     // after the step uses the fp64 G_AA (matvec with gc = nullptr).
     auto matvec = [&](const double *vsh, double *wsh, int na, int r0, int r1, double nu_, const float *gc, int ncache,
-                      int nap) {
-        for (int i = r0 + 2 * wid; i < r1; i += 2 * nw) {
-            const bool two = i + 1 < r1;
-            const int l = i - r0;
-            double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
-            if (gc && l + (two ? 1 : 0) < ncache) {
-                const float *ra = gc + (size_t)l * nap, *rb = gc + (size_t)(two ? l + 1 : l) * nap;
+                      int nap, float *vf) {
+        int rs = r0;                                        // first row of the L2 (fp64) part
+        if (gc && ncache > 0) {
+            // the cached rows: fp32 products with an fp32 copy of v, four rows per warp sharing each
+            // v load, the lane's partial sums (<= na/64 terms) in fp32, the warp sum in fp64 -- the
+            // per-element fp32 -> fp64 conversions (16 per SM clock) bound the fp64 form
+            for (int j = t; j < nap; j += T_) vf[j] = j < na ? (float)vsh[j] : 0.f;
+            __syncthreads();
+            for (int l0 = 4 * wid; l0 < ncache; l0 += 4 * nw) {
+                const int nr = min(4, ncache - l0);
+                const float *g0 = gc + (size_t)l0 * nap;
+                float2 acc[4];
+#pragma unroll
+                for (int q = 0; q < 4; q++) acc[q] = make_float2(0.f, 0.f);
+#pragma unroll 2
                 for (int j = 2 * lane; j < na; j += 64) {
-                    const float2 ga = *reinterpret_cast<const float2 *>(ra + j);
-                    const float2 gb = *reinterpret_cast<const float2 *>(rb + j);
-                    const double2 vv = *reinterpret_cast<const double2 *>(vsh + j);
-                    a0 = fma((double)ga.x, vv.x, a0);
-                    a1 = fma((double)ga.y, vv.y, a1);
-                    b0 = fma((double)gb.x, vv.x, b0);
-                    b1 = fma((double)gb.y, vv.y, b1);
+                    const float2 vv = *reinterpret_cast<const float2 *>(vf + j);
+#pragma unroll
+                    for (int q = 0; q < 4; q++)
+                        if (q < nr) {
+                            const float2 g = *reinterpret_cast<const float2 *>(g0 + (size_t)q * nap + j);
+                            acc[q].x = fmaf(g.x, vv.x, acc[q].x);
+                            acc[q].y = fmaf(g.y, vv.y, acc[q].y);
+                        }
                 }
-            } else {
+                // the four row sums in one butterfly (fixed order): after the xor-16 and xor-8
+                // exchanges each lane holds one row's partial (row 2 (lane >> 4 & 1) + (lane >> 3 & 1))
+                const double v0 = (double)acc[0].x + (double)acc[0].y, v1 = (double)acc[1].x + (double)acc[1].y;
+                const double v2 = (double)acc[2].x + (double)acc[2].y, v3 = (double)acc[3].x + (double)acc[3].y;
+                const bool hi16 = lane & 16, hi8 = lane & 8;
+                double ka = hi16 ? v2 : v0, kb = hi16 ? v3 : v1;
+                ka += __shfl_xor_sync(FULL, hi16 ? v0 : v2, 16);
+                kb += __shfl_xor_sync(FULL, hi16 ? v1 : v3, 16);
+                double kr = hi8 ? kb : ka;
+                kr += __shfl_xor_sync(FULL, hi8 ? ka : kb, 8);
+                kr += __shfl_xor_sync(FULL, kr, 4);
+                kr += __shfl_xor_sync(FULL, kr, 2);
+                kr += __shfl_xor_sync(FULL, kr, 1);
+                const int q = (hi16 ? 2 : 0) + (hi8 ? 1 : 0);
+                if ((lane & 7) == 0 && q < nr) wsh[l0 + q] = kr + nu_ * vsh[r0 + l0 + q];
+            }
+            rs = r0 + ncache;
+        }
+        for (int i = rs + 2 * wid; i < r1; i += 2 * nw) {
+            const bool two = i + 1 < r1;
+            double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+            {
                 const double *ra = a.GA + (int64_t)i * ldG, *rb = a.GA + (int64_t)(two ? i + 1 : i) * ldG;
                 for (int j0 = 2 * lane; j0 < na; j0 += 64 * 8) {
                     double2 ga[8], gb[8];
@@ -3179,8 +3209,9 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
         const int r0 = rank == 0 ? 0 : (int)((int64_t)(rank - 1) * na / NB);
         const int r1 = rank == 0 ? 0 : (int)((int64_t)rank * na / NB);
         const int nap = (na + 1) & ~1;
-        float *gc = reinterpret_cast<float *>(wsh + owp);   // fp32 rows (8-byte aligned: nap even)
-        const int cap = rank == 0 ? 0 : (int)(((int64_t)a.smem_bytes / 8 - (vlen + 4 * owp)) * 2 / nap);
+        float *vf = reinterpret_cast<float *>(wsh + owp);   // fp32 copy of v (vlen entries)
+        float *gc = vf + vlen;                              // fp32 rows (8-byte aligned: vlen, nap even)
+        const int cap = rank == 0 ? 0 : (int)((((int64_t)a.smem_bytes / 8 - (vlen + 4 * owp)) * 2 - vlen) / nap);
         const int ncache = max(0, min(r1 - r0, cap));
         for (int e = t; e < ncache * nap; e += T_) {
             const int l = e / nap, j = e - l * nap;
@@ -3245,7 +3276,7 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
             xs[i - r0] = 0.0;
         }
         share_r();
-        matvec(vsh, wsh, na, r0, r1, nu, gc, ncache, nap);
+        matvec(vsh, wsh, na, r0, r1, nu, gc, ncache, nap, vf);
         __syncthreads();
         double g0 = 0.0, d0 = 0.0;
         for (int i = r0 + t; i < r1; i += T_) { g0 = fma(vsh[i], vsh[i], g0); d0 = fma(wsh[i - r0], vsh[i], d0); }
@@ -3266,7 +3297,7 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
                 const long long q0 = CGCLK();
                 share_r();                                  // (every peer finished reading vsh: reduction k)
                 const long long q1 = CGCLK(), q2 = q1;
-                matvec(vsh, wsh, na, r0, r1, nu, gc, ncache, nap);
+                matvec(vsh, wsh, na, r0, r1, nu, gc, ncache, nap, vf);
                 __syncthreads();
                 const long long q3 = CGCLK();
                 double gp = 0.0, dp = 0.0;
@@ -3320,7 +3351,7 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
         }
         if (t == 0 && (na & 1)) vsh[na] = 0.0;
         __syncthreads();
-        matvec(vsh, wsh, na, r0, r1, 0.0, nullptr, 0, nap);      // fp64 G_AA: the exact gradient update
+        matvec(vsh, wsh, na, r0, r1, 0.0, nullptr, 0, nap, nullptr);   // fp64 G_AA: the exact gradient update
         __syncthreads();
         for (int i = r0 + t; i < r1; i += T_) {
             const int s = __ldcg(wk.act + i);
