@@ -3213,9 +3213,22 @@ __global__ void __cluster_dims__(RC, 1, 1) __launch_bounds__(kG7Threads, 1) k_cd
         float *gc = vf + vlen;                              // fp32 rows (8-byte aligned: vlen, nap even)
         const int cap = rank == 0 ? 0 : (int)((((int64_t)a.smem_bytes / 8 - (vlen + 4 * owp)) * 2 - vlen) / nap);
         const int ncache = max(0, min(r1 - r0, cap));
-        for (int e = t; e < ncache * nap; e += T_) {
-            const int l = e / nap, j = e - l * nap;
-            gc[e] = j < na ? (float)__ldcg(a.GA + (int64_t)(r0 + l) * ldG + j) : 0.f;
+        for (int l = wid; l < ncache; l += nw) {            // a row per warp, 16 loads per lane in flight
+            const double *src = a.GA + (int64_t)(r0 + l) * ldG;
+            float *dst = gc + (size_t)l * nap;
+            for (int j0 = 2 * lane; j0 < na; j0 += 64 * 8) {
+                double2 v[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    const int j = j0 + 64 * u;
+                    v[u] = j < na ? __ldcg(reinterpret_cast<const double2 *>(src + j)) : make_double2(0.0, 0.0);
+                }
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    const int j = j0 + 64 * u;
+                    if (j < na) *reinterpret_cast<float2 *>(dst + j) = make_float2((float)v[u].x, j + 1 < na ? (float)v[u].y : 0.f);
+                }
+            }
         }
         const double la = a.lam_alpha, nu = a.nu;
         // The CG iterations run on the owner CTAs only (the leader holds no rows; it rejoins at the
