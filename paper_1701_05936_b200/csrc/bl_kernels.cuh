@@ -1913,19 +1913,50 @@ __global__ void __launch_bounds__(kLogitEtaThreads) k_logit_eta(const T *__restr
         double *__restrict__ v, double *__restrict__ part /* 3 per block: sum w, sum v, loss */,
         RoundStatus *st, int reset) {
     __shared__ double red[32];
+    __shared__ double cb[kLogitEtaThreads], cc[kLogitEtaThreads];   // a chunk's nonzero slots: b / s_j, c_j
+    __shared__ int cj[kLogitEtaThreads], wcnt[kLogitEtaThreads / 32 + 1];
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     double wl = 0.0, vl = 0.0, ll = 0.0;
-    if (i < ld) {
-        double e = bS[nW];
+    double e = bS[nW];
+    // the slots in chunks of one per thread: the nonzero ones compacted (slot order kept) into shared
+    // memory, then every row's dot over them with 8 column loads in flight -- the same terms in the
+    // same order as a sequential loop over the slots (one dependent L2 load per slot was the cost)
+    for (int k0 = 0; k0 < nW; k0 += kLogitEtaThreads) {
+        const int k = k0 + threadIdx.x;
+        const double b = k < nW ? bS[k] : 0.0;
+        const bool nz = b != 0.0;
+        const unsigned m = __ballot_sync(0xffffffffu, nz);
+        if (lane == 0) wcnt[wid] = __popc(m);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int run = 0;
+            for (int u = 0; u < kLogitEtaThreads / 32; u++) { const int c0 = wcnt[u]; wcnt[u] = run; run += c0; }
+            wcnt[kLogitEtaThreads / 32] = run;
+        }
+        __syncthreads();
+        if (nz) {
+            const int pos = wcnt[wid] + __popc(m & ((1u << lane) - 1u));
+            const int j = Wst[k];
+            cb[pos] = b / s[j];
+            cc[pos] = c[j];
+            cj[pos] = j;
+        }
+        __syncthreads();
+        const int cnt = wcnt[kLogitEtaThreads / 32];
         if (i < n) {
-            for (int k = 0; k < nW; k++) {
-                const double b = bS[k];
-                if (b != 0.0) {
-                    const int j = Wst[k];
-                    e = fma(b / s[j], to_d(X[(int64_t)j * ld + i]) - c[j], e);
-                }
+            for (int q = 0; q < cnt; q += 8) {
+                T xv[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) xv[u] = q + u < cnt ? X[(int64_t)cj[q + u] * ld + i] : T(0);
+#pragma unroll
+                for (int u = 0; u < 8; u++)
+                    if (q + u < cnt) e = fma(cb[q + u], to_d(xv[u]) - cc[q + u], e);
             }
         }
+        __syncthreads();                                    // (the chunk's staging is rewritten next)
+    }
+    if (i < ld) {
         const bool use = i < n && (!MASK || mask[i]);
         double wi = 0.0, vi = 0.0;
         if (use) {
