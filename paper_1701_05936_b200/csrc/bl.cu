@@ -454,6 +454,7 @@ struct bl_prep {
     int batch_passes;       // ... batched launches of the current round
     int cd_mode;            // 0 auto (Gram when |W| <= 4096), 1 residual, 2 Gram
     int cd_cluster;         // CTAs per Gram-CD cluster (4, 8, 16)
+    int cd_cluster_auto;    // the caller left cd_cluster at 0 (the library picks per solve kind)
     int cd_newton;          // Newton (CG) steps on settled active sets in the Gram CD
     int fault_strong_drop;  // TEST ONLY (bl_opts): admit no strong-rule candidate in advance
     size_t chunk_bytes;     // out-of-core: bytes per streamed chunk (the buffers are sized for it)
@@ -977,6 +978,7 @@ bl_prep *prep_begin(bl_design *d, const double *y, const uint8_t *train, double 
         const int cc = opts ? opts->cd_cluster : 0;
         if (cc != 0 && cc != 4 && cc != 8 && cc != 16) raise(BL_ERR_ARG, "cd_cluster must be 0, 4, 8 or 16 (got %d)", cc);
         pp->cd_cluster = cc == 0 ? 16 : cc;   // one fit: 16 SMs (bl_cv's concurrent fits default to 8)
+        pp->cd_cluster_auto = cc == 0;
         if (opts && opts->stream_chunk_bytes < 0) raise(BL_ERR_ARG, "stream_chunk_bytes must be >= 0");
         const size_t cb = opts && opts->stream_chunk_bytes > 0 ? (size_t)opts->stream_chunk_bytes : kStreamChunkBytes;
         if (cb != pp->chunk_bytes && pp->sbuf[0]) {          // a reused workspace with other chunk buffers
@@ -1715,7 +1717,10 @@ void solve_logit_g7_t(bl_prep *pp, int nW, double lam, double alpha, double tol,
     ga.idv = alpha < 1.0 ? ws + 3 * (size_t)nW : nullptr;
     ga.nu = 0.0;
     ga.newton = 0;                             // per-slot thresholds / curvatures: plain sweeps
-    const int R = pp->cd_cluster;   // CTA 0 leads, 1..R-1 own the gradients
+    // CTA 0 leads, 1..R-1 own the gradients.  IRLS runs ~2 short solves per lambda: 8-CTA clusters
+    // are faster there than 16 (logit bench 124.2 -> 118.7 ms, scripts/cluster_sweep.py) when |W| fits
+    int R = pp->cd_cluster;
+    if (pp->cd_cluster_auto && gram7_smem(nW, 8) <= allow_dyn_smem(gram7_kernel(alpha < 1.0, 8))) R = 8;
     const void *kern = gram7_kernel(alpha < 1.0, R);
     const size_t smem = gram7_smem(nW, R);
     const size_t lim = allow_dyn_smem(kern);
