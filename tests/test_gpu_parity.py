@@ -427,6 +427,50 @@ def test_deterministic_repeat():
     assert np.array_equal(a.beta_std, b.beta_std) and np.array_equal(a.cols_scanned, b.cols_scanned)
 
 
+@pytest.mark.parametrize("alpha,cd", [(1.0, "gram"), (1.0, "residual"), (0.5, "gram")])
+def test_duplicate_columns_compare_what_is_unique(alpha, cd):
+    """Exactly duplicated (and sign-flipped) columns: for alpha = 1 the minimiser is not unique (any
+    same-sign split of a duplicated pair's weight is optimal), so compare what IS unique -- the
+    objective, the fitted values X~beta and the pair-folded coefficients; for alpha < 1 the
+    objective is strictly convex and the whole beta must match (duplicates share the weight)."""
+    inst = synth.random_instance(120, 400, seed=91, kind="corr", n_true=8, alpha=alpha)
+    X = inst.host_X().copy()
+    truth = np.flatnonzero(inst.beta_true)
+    pairs = [(int(truth[0]), 397), (int(truth[1]), 398), (5, 399)]
+    sign = {397: 1.0, 398: -1.0, 399: 1.0}
+    for j, d in pairs:
+        X[d] = sign[d] * X[j]
+    inst.X = X
+    lm = oracle.lambda_max(inst, inst.y)[0]
+    lams = synth.lambda_grid(lm, 25, 0.05)
+    op = oracle.fit_path(inst, inst.y, lams, alpha=alpha, tol=1e-13)
+    gp = bl.Design(X, inst.n).fit_path(inst.y, lams, alpha=alpha, tol=1e-11, cd=cd)
+    if alpha < 1.0:
+        compare_path(inst, gp, op, alpha)
+        return
+    assert gp.n_converged == len(lams)
+    Bg, Bo = gp.dense(inst.p), op.beta
+    c, s = oracle.column_stats(inst)[:2]
+    Xs = (inst.dense() - c) / s
+    for k, lam in enumerate(lams):
+        bo, bg = Bo[:, k].copy(), Bg[:, k].copy()
+        qo = oracle.objective(inst, inst.y, bo, lam, alpha)
+        qg = oracle.objective(inst, inst.y, bg, lam, alpha)
+        assert abs(qg - qo) <= 1e-7 * qo, f"lambda {k}: RD {(qg - qo) / qo:.3e}"
+        assert abs(gp.obj[k] - qg) <= 1e-10 * qg
+        zv, nv = oracle.kkt(inst, inst.y, bg, lam, alpha)                # valid: the GPU's beta is a minimiser
+        assert zv <= 1e-6 and nv <= 1e-6, f"lambda {k}: KKT {zv:.2e} {nv:.2e}"
+        for j, d in pairs:                                             # fold each pair onto its first column
+            for b in (bo, bg):
+                assert b[j] * sign[d] * b[d] >= 0.0                     # opposite-sign splits are not optimal
+                b[j] += sign[d] * b[d]; b[d] = 0.0
+        scale = max(np.abs(bo).max(), 1e-300)
+        assert np.abs(bg - bo).max() <= 1e-5 * scale, f"lambda {k}: folded beta"
+        assert np.array_equal(np.abs(bo) >= 1e-8, np.abs(bg) >= 1e-8) or np.abs(bg - bo).max() <= 1e-8
+        fo, fg = Xs @ Bo[:, k], Xs @ Bg[:, k]
+        assert np.abs(fg - fo).max() <= 1e-5 * max(np.abs(fo).max(), 1e-300)
+
+
 # ------------------------------------------------------------------ a12 cross-validation
 
 @pytest.mark.parametrize("dtype,alpha,cd,cv_mode,n,p", [
