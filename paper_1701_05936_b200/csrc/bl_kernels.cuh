@@ -174,20 +174,24 @@ __global__ void __launch_bounds__(256) k_colstats(const T *__restrict__ X, int64
                 s[j] = num <= 0 ? 0.0 : sqrt((double)num) / nt;
             }
         } else {
-            // four 16-byte loads in flight per lane (independent partial sums, combined in a fixed
-            // order): one load per lane and iteration left the HBM stream latency-bound (0.6 of peak)
+            // U 16-byte loads in flight per lane (independent partial sums, combined in a fixed
+            // order): one load per lane and iteration left the HBM stream latency-bound (0.6 of
+            // peak), four 0.75; eight cover a 1000-row fp32 column in one step
+            constexpr int U = 8;
             const double K = to_d(col[i0]);
-            double s1[4] = {0.0, 0.0, 0.0, 0.0}, s2[4] = {0.0, 0.0, 0.0, 0.0};
-            for (int i = lane * V; i < n; i += 4 * 32 * V) {
-                T xv[4][V];
+            double s1[U], s2[U];
 #pragma unroll
-                for (int u = 0; u < 4; u++) {
+            for (int u = 0; u < U; u++) s1[u] = s2[u] = 0.0;
+            for (int i = lane * V; i < n; i += U * 32 * V) {
+                T xv[U][V];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
                     const int iu = i + u * 32 * V;
-                    if (iu < n) *reinterpret_cast<int4 *>(xv[u]) = __ldg(reinterpret_cast<const int4 *>(col + iu));
+                    if (iu < n) *reinterpret_cast<int4 *>(xv[u]) = __ldcs(reinterpret_cast<const int4 *>(col + iu));
                     else *reinterpret_cast<int4 *>(xv[u]) = make_int4(0, 0, 0, 0);
                 }
 #pragma unroll
-                for (int u = 0; u < 4; u++) {
+                for (int u = 0; u < U; u++) {
                     const int iu = i + u * 32 * V;
 #pragma unroll
                     for (int e = 0; e < V; e++) {
@@ -198,7 +202,8 @@ __global__ void __launch_bounds__(256) k_colstats(const T *__restrict__ X, int64
                     }
                 }
             }
-            double t1 = (s1[0] + s1[1]) + (s1[2] + s1[3]), t2 = (s2[0] + s2[1]) + (s2[2] + s2[3]);
+            double t1 = ((s1[0] + s1[1]) + (s1[2] + s1[3])) + ((s1[4] + s1[5]) + (s1[6] + s1[7]));
+            double t2 = ((s2[0] + s2[1]) + (s2[2] + s2[3])) + ((s2[4] + s2[5]) + (s2[6] + s2[7]));
             t1 = warp_sum(t1);
             t2 = warp_sum(t2);
             if (lane == 0) {
